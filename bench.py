@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the ScaleSim planner hot path (BASELINE.json metric):
+  agent-plans/sec (1M agents per GPU, 1/2/4/8 B200) and % HBM roofline; transfer GB/s vs
+  the host link measured in the same run.
+
+One step = score + plan (+ transfer call, a no-op for logical sizes) of every agent of the
+C4 workload (1M independent AgentSociety-shaped agents per GPU, budget 25% of agent memory,
+theta = 4, logical block sizes).  Inputs are resident in HBM; every timed step reads its own
+16 MB record buffer (K distinct buffers, > 126 MB L2), so no step is served from L2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+For N > 1 launch with torchrun (one rank per GPU); agents shard by contiguous id, the global
+budget cut runs over NCCL inside the library (weak scaling: 1M agents per GPU).
+`--impl reference` times the CPU oracle (the reference arm of this tier) on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import tracegen as tg  # noqa: E402
+
+WARM_IN = 16  # untimed trace steps that bring residency to steady state before warmup
+BYTES_PER_AGENT_SCORE = 16.125  # k_score algorithmic bytes: 16 B record + 1/8 B residency bit
+BYTES_PER_AGENT_STEP = 16.25  # whole step: record + old and new residency bits
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML in a thread during the timed region."""
+
+    def __init__(self, dev=0):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        names = {getattr(N, k): k for k in dir(N) if k.startswith("nvmlClocksEventReason") or
+                 k.startswith("nvmlClocksThrottleReason")}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
+                    N, "nvmlDeviceGetCurrentClocksEventReasons") else N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in names.items():
+                    if isinstance(bit, int) and bit and (r & bit) == bit and bit & (bit - 1) == 0:
+                        self.reasons.add(name.replace("nvmlClocksEventReason", "").replace(
+                            "nvmlClocksThrottleReason", ""))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.N:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.N:
+            self.t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"None", "GpuIdle", "ApplicationsClocksSetting"}),
+                "samples": len(self.samples)}
+
+
+def c4_shard(n_local: int, steps: int, seed: int, rank: int):
+    """The C4 trace of this rank's shard (independent agents, C3 footprints, logical sizes)."""
+    w = tg.config_c4(seed=seed + 1000 * rank, steps=steps, n=n_local)
+    return w
+
+
+def oracle_steps(w, steps, res=None, budget=None):
+    import oracle
+    res = np.zeros(w.n, np.uint8) if res is None else res
+    budget = w.budget if budget is None else budget
+    for s in steps:
+        d, _ = oracle.score(w.rec[s], None, int(w.now[s]))
+        p = oracle.plan(w.rec[s], d, res, w.theta, budget)
+        res = p["resident"]
+    return res
+
+
+def cpu_baseline(w, target_s=10.0, max_s=30.0):
+    """The oracle as it stands, single-threaded, on a bounded sample of the same workload."""
+    import oracle
+    res = oracle_steps(w, range(min(WARM_IN, w.steps)))
+    t0 = time.perf_counter()
+    n_steps = 0
+    s = WARM_IN
+    while True:
+        d, _ = oracle.score(w.rec[s], None, int(w.now[s]))
+        p = oracle.plan(w.rec[s], d, res, w.theta, w.budget)
+        res = p["resident"]
+        n_steps += 1
+        s = s + 1 if s + 1 < w.steps else WARM_IN
+        el = time.perf_counter() - t0
+        if el >= target_s or el >= max_s:
+            break
+    return {"value": w.n * n_steps / el, "unit": "agent-plans/s", "cores": 1, "kind": "oracle",
+            "sample": f"C4 shard of {w.n} agents, {n_steps} consecutive steps after a {WARM_IN}-step warm-in, "
+                      f"score+plan, single thread, {el:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """Reference arm of this tier: the CPU oracle on the same workload (rank 0 only)."""
+    if rank != 0:
+        return
+    n = args.n
+    w = c4_shard(n, WARM_IN + args.warmup + args.steps, args.seed, 0)
+    res = oracle_steps(w, range(WARM_IN + args.warmup))
+    import oracle
+    t0 = time.perf_counter()
+    for s in range(WARM_IN + args.warmup, WARM_IN + args.warmup + args.steps):
+        d, _ = oracle.score(w.rec[s], None, int(w.now[s]))
+        p = oracle.plan(w.rec[s], d, res, w.theta, w.budget)
+        res = p["resident"]
+    el = time.perf_counter() - t0
+    v = n * args.steps / el
+    line = {"metric": "agent-plans/sec (1M agents, 1/2/4/8 B200) % HBM roofline; transfer GB/s vs host link",
+            "impl": "reference", "value": v, "unit": "agent-plans/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"c4: {n} independent agents (AgentSociety-shaped), budget 25%, theta 4, "
+                                   "logical sizes", "n_agents": n},
+            "cpu_baseline": {"value": v, "unit": "agent-plans/s", "cores": 1, "kind": "oracle",
+                             "sample": f"full workload, {args.steps} steps after {WARM_IN + args.warmup} warm steps"},
+            "e2e": {"value": v, "unit": "agent-plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def link_peak(torch, dev):
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d2 = torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def best(fn, reps=6):
+        b = 1e9
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            t = time.perf_counter()
+            fn()
+            torch.cuda.synchronize(dev)
+            b = min(b, time.perf_counter() - t)
+        return b
+
+    def bidir():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    r = {"h2d_GBs": n / best(lambda: d.copy_(h, non_blocking=True)) / 1e9,
+         "d2h_GBs": n / best(lambda: h.copy_(d, non_blocking=True)) / 1e9,
+         "bidir_GBs": 2 * n / best(bidir) / 1e9}
+    del h, d, h2, d2
+    return r
+
+
+def transfer_leg(torch, dev, seed):
+    """C2 (10k agents, 7B LoRA + KV pages, budget 25%): physical block transfers, timed
+    with CUDA events on the copy stream; against the link peak measured here."""
+    from paper_2601_21473_b200.planner import Planner
+    w = tg.config_c2(seed=seed, steps=24, host_bytes=8 << 30)
+    b = w.blocks
+    host = torch.empty(int(b.host_bytes), dtype=torch.uint8).pin_memory()
+    pl = Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
+                 page_bytes=w.page_bytes, transfer=True, host_arena=host, device=dev.index)
+    tot_b, tot_t, steps = 0, 0.0, 0
+    h2d_b = d2h_b = 0
+    for s in range(w.steps):
+        pl.set_records(w.rec[s])
+        pl.score(int(w.now[s]))
+        pl.plan()
+        pl.stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(pl.copy_stream)
+        pl.transfer()
+        e1.record(pl.copy_stream)
+        hdr = pl.sync()
+        if s >= 8:  # steady state
+            moved = hdr["n_h2d"] * w.page_bytes + hdr["n_d2h"] * w.page_bytes
+            tot_b += moved
+            h2d_b += hdr["n_h2d"] * w.page_bytes
+            d2h_b += hdr["n_d2h"] * w.page_bytes
+            tot_t += e0.elapsed_time(e1) / 1e3
+            steps += 1
+    pl.close()
+    del host
+    return {"bytes_per_step": tot_b / max(steps, 1), "h2d_bytes_per_step": h2d_b / max(steps, 1),
+            "d2h_bytes_per_step": d2h_b / max(steps, 1), "GBs": tot_b / max(tot_t, 1e-12) / 1e9,
+            "steps": steps, "workload": "c2: 10k agents, 7B rank-16 LoRA + 917,504 B KV pages, budget 25%, "
+                                        "host arena 8 GiB (offsets aliased), SM-driven page copies"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000, help="agents per GPU")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph")
+    ap.add_argument("--no-transfer-leg", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=32)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    from paper_2601_21473_b200 import _lib
+    from paper_2601_21473_b200.planner import Planner
+
+    n = args.n
+    W, K = args.warmup, args.steps
+    T = WARM_IN + W + K
+    w = c4_shard(n, T, args.seed, rank)
+    budget = w.budget
+    nccl_id = None
+    if world > 1:
+        tot = torch.tensor([int(w.footprint.sum())], dtype=torch.int64, device=dev)
+        dist.all_reduce(tot)
+        budget = int(tot.item()) // 4
+        obj = [None]
+        if rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            _lib.check(_lib.lib().scalesim_nccl_unique_id(buf), "scalesim_nccl_unique_id")
+            obj = [bytes(buf.raw)]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    b = w.blocks
+    pl = Planner(n * world, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, w.theta,
+                 transfer=False, device=local, shard=(rank * n, (rank + 1) * n), rank=rank, world=world,
+                 nccl_id=nccl_id)
+    # all step records resident in HBM (T distinct 16 MB buffers, > L2)
+    recs = torch.from_numpy(np.ascontiguousarray(w.rec).view(np.uint8).reshape(T, -1)).to(dev)
+    ptr = [recs[s].data_ptr() for s in range(T)]
+
+    def eager_step(s):
+        pl.set_inputs_ptr(ptr[s])
+        pl.step(int(w.now[s]))
+
+    for s in range(WARM_IN + W):
+        eager_step(s)
+    pl.sync()
+
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    t_base = WARM_IN + W
+
+    def timed_steps():
+        for k in range(K):
+            s = t_base + k
+            pl.set_inputs_ptr(ptr[s])
+            ev_s[k].record(pl.stream)
+            pl.score(int(w.now[s]))
+            ev_e[k].record(pl.stream)
+            pl.plan()
+            pl.transfer()
+        pl.join()
+
+    graph = None
+    mode = "eager"
+    if not args.eager:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            lc0 = pl.launch_count()
+            with torch.cuda.graph(graph, stream=pl.stream):
+                timed_steps()
+            launches = pl.launch_count() - lc0
+            graph.upload() if hasattr(graph, "upload") else None
+            mode = "cuda-graph"
+        except Exception as e:  # capture failed: fall back to eager launches
+            sys.stderr.write(f"graph capture failed ({e}); timing eager launches\n")
+            graph = None
+            torch.cuda.synchronize(dev)
+    # note: capturing does not run the kernels, so the residency is still at step t_base-1
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        if graph is not None:
+            t0.record(pl.stream)
+            graph.replay()
+            t1.record(pl.stream)
+        else:
+            lc0 = pl.launch_count()
+            t0.record(pl.stream)
+            timed_steps()
+            t1.record(pl.stream)
+            launches = pl.launch_count() - lc0
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    ms_score = [ev_s[k].elapsed_time(ev_e[k]) for k in range(K)]
+    hdr = pl.sync()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / K
+    value = n * world * K / (ms / 1e3)
+
+    # ---- e2e: the same metric through the host entry point (host buffers, copies inside)
+    e2e_k = min(args.e2e_steps, K)
+    rec_pinned = torch.from_numpy(np.ascontiguousarray(w.rec[t_base:t_base + e2e_k])).pin_memory()
+    rec_host = [rec_pinned[k].numpy() for k in range(e2e_k)]
+    pf = np.zeros(n, np.uint32)
+    ev = np.zeros(n, np.uint32)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_e = time.perf_counter()
+    h2d_b = d2h_b = 0
+    for k in range(e2e_k):
+        h = pl.step_host(int(w.now[t_base + k]), rec_host[k], None, pf, ev)
+        h2d_b += rec_host[k].nbytes
+        d2h_b += 128 + 4 * (h["n_prefetch"] + h["n_evict"])
+    el_e = time.perf_counter() - t_e
+    if world > 1:
+        t = torch.tensor([el_e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el_e = float(t.item())
+    e2e = {"value": n * world * e2e_k / el_e, "unit": "agent-plans/s", "h2d_bytes_per_step": h2d_b // e2e_k,
+           "d2h_bytes_per_step": d2h_b // e2e_k, "steps": e2e_k,
+           "api": "scalesim_step_host (pinned host records in, header + lists out, synchronous)"}
+
+    if rank != 0:
+        pl.close()
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    pk = peaks()
+    score_ms = float(np.mean(ms_score))
+    achieved = n * BYTES_PER_AGENT_SCORE / (score_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "k_score (+int/plan-init prologue) = scalesim_score",
+            "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+            "traffic": None, "score_ms": score_ms, "score_share_of_step": score_ms / ms_per_step,
+            "step_frac": n * BYTES_PER_AGENT_STEP / (ms_per_step / 1e3) / 1e9 / pk["hbm_gbs"],
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback 6650"}
+    line = {"metric": "agent-plans/sec (1M agents, 1/2/4/8 B200) % HBM roofline; transfer GB/s vs host link",
+            "value": value, "unit": "agent-plans/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "c4: 1M independent AgentSociety-shaped agents per GPU (C3 footprints, logical "
+                                   "sizes), budget 25% of agent memory, theta 4, ~5% active/step",
+                       "n_agents_per_gpu": n, "n_agents": n * world, "parallelism": f"id-shard x{world}",
+                       "l2": f"{K} distinct 16 MB record buffers (> 126 MB L2)", "timing": mode,
+                       "last_plan": {k: hdr[k] for k in ("n_prefetch", "n_evict", "cut_bits", "status")}},
+            "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": sampler.result()}
+    pl.close()
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    if not args.no_transfer_leg:
+        lp = link_peak(torch, dev)
+        tl = transfer_leg(torch, dev, args.seed)
+        tl["link"] = lp
+        tl["frac_of_link"] = tl["GBs"] / max(lp["bidir_GBs"] if tl["d2h_bytes_per_step"] else lp["h2d_GBs"], 1e-9)
+        line["transfer"] = tl
+    line["cpu"] = {"cores": os.cpu_count()}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

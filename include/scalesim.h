@@ -1,0 +1,221 @@
+/*
+ * scalesim.h — C ABI (v1) of the B200-native ScaleSim invocation-distance memory planner.
+ *
+ * The operation (arXiv 2601.21473, /root/reference/PAPER.md = P:<line>, SPEC.md = S:<line>):
+ * every simulation step, (1) score every agent's invocation distance (§3.2, P:197-229,
+ * Eq. 1, Eq. 2), (2) rank agents by (distance, agent id), (3) keep the
+ * longest prefix of that order that fits the GPU memory budget, which yields the evict
+ * list (Table 1 Evict; §3.3) and the prefetch list (Table 1
+ * DispatchLoadTasks; §3.3), and (4) move the agents' memory blocks
+ * between pinned host memory and HBM (Table 1 Load).  The readings the paper
+ * leaves open are DESIGN.md §3 (R1..R17).
+ *
+ * Mapping of the paper's interface (Table 1) onto this ABI:
+ *   agent distances from the frontend -> scalesim_score (computed here from agent state)
+ *   Evict + DispatchLoadTasks         -> scalesim_plan  (one stateless plan per step)
+ *   Load                              -> scalesim_transfer
+ *   HandleReq                         -> stays with the caller: it marks requesting agents
+ *                                        WAITING (distance 0) in their record.
+ *
+ * Conventions (all calls):
+ *   - Every entry point returns scalesim_status and never throws or aborts.
+ *   - Ownership: the caller owns every buffer (typically torch tensors) and keeps them alive
+ *     until scalesim_destroy.  The library never allocates device memory after init; all
+ *     scratch lives in the caller's workspace (size from scalesim_workspace_bytes).
+ *   - Asynchrony: score/plan/transfer/step enqueue work on the caller's CUDA streams and
+ *     return without a host synchronisation (graph-capturable).  Device-detected conditions
+ *     (budget too small for the active agents, malformed records) are reported in the
+ *     device status word and surface at scalesim_sync.  Sticky CUDA/NCCL errors surface at
+ *     the next call as SCALESIM_E_CUDA / SCALESIM_E_NCCL.
+ *   - Threading: one context per host thread.  Not re-entrant on one context.
+ *   - Determinism: outputs are a pure function of (records, kinematics, residency, config),
+ *     independent of launch configuration and of the number of ranks.
+ */
+#ifndef SCALESIM_H
+#define SCALESIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCALESIM_ABI_VERSION 1u
+
+typedef struct scalesim_ctx scalesim_ctx;
+
+typedef enum {
+  SCALESIM_OK = 0,
+  SCALESIM_E_INVALID = 1,        /* bad argument: null/misaligned pointer, size mismatch, block size
+                                    not a page multiple, arena smaller than the budget, ... (S:487 exit 2) */
+  SCALESIM_E_INSUFFICIENT = 2,   /* the active (distance 0) agents do not fit the budget; the plan is
+                                    still produced and keeps the longest fitting prefix (R11) */
+  SCALESIM_E_NOT_RESTORABLE = 3, /* reserved: a planned block without host backing */
+  SCALESIM_E_ORDER = 4,          /* calls out of order: plan before score, transfer of a stale plan */
+  SCALESIM_E_CUDA = 5,
+  SCALESIM_E_NCCL = 6,
+  SCALESIM_E_INVARIANT = 7,      /* device self-check failed (S:487 exit 3) */
+  SCALESIM_E_BAD_INPUT = 8       /* malformed agent record or non-finite kinematics (status word) */
+} scalesim_status;
+
+/* Bits of the device status word (plan header field SCALESIM_H_STATUS). */
+#define SCALESIM_ST_INSUFFICIENT 1u /* a distance-0 agent is outside the kept set */
+#define SCALESIM_ST_BAD_RECORD 2u   /* class 3, or an INT agent whose kin index >= n_kin */
+#define SCALESIM_ST_BAD_KIN 4u      /* ACTING INT agent with non-finite kinematics (excluded) */
+#define SCALESIM_ST_NO_PAGES 8u     /* free page pool exhausted (cannot happen for a valid config) */
+
+/* Config flags. */
+#define SCALESIM_F_NO_TRANSFER 1u   /* plan + byte accounting only: no arena, no pages, no copies
+                                       (logical sizes, BASELINE configs 4 and 5) */
+#define SCALESIM_F_KEEP_DIST 2u     /* keep per-agent distances readable after plan (dist view) */
+
+/* Agent record: 4 x uint32 per agent, 16-byte aligned, one 128-bit load.
+ *   [0] t_next : action-end tick (ACTING independent / interaction agents), or remaining hop
+ *                count to the diffusion wave (ACTING diffusion agents; 0xFFFFFFFF = unreachable)
+ *   [1] footprint bytes of the agent (must equal the sum of its block sizes)
+ *   [2] flags  : bits 0-1 phase {0 ACTING, 1 WAITING, 2 GENERATING, 3 IDLE}
+ *                bits 2-3 class {0 independent, 1 interaction, 2 diffusion}
+ *                bit 4    dirty (KV / history written since last write-back, R13)
+ *   [3] index into the kinematics array (interaction agents)
+ * Kinematics: 4 x float per entry = {x, y, vx, vy} (Eq. 2).
+ * Block kinds: 0 LORA (never written back), 1 KV page, 2 HIST (written back when dirty). */
+
+typedef struct {
+  uint32_t abi_version;   /* SCALESIM_ABI_VERSION */
+  uint32_t flags;         /* SCALESIM_F_* */
+  uint64_t n_agents;      /* global number of agents N (ids 0..N-1) */
+  uint64_t shard_begin;   /* this rank's contiguous id range [shard_begin, shard_end) */
+  uint64_t shard_end;
+  uint64_t n_kin;         /* entries in the kinematics array (0 if no interaction agents) */
+  uint64_t budget_bytes;  /* global GPU memory budget B for agent memory */
+  float theta[3];         /* prefetch thresholds per class (R4); +inf allowed, >= 0 */
+  float hop_scale;        /* ticks per hop for diffusion distances (R5), > 0, finite */
+  uint64_t page_bytes;    /* device arena page size; every block size is a multiple; 4096-aligned */
+  int32_t device;         /* CUDA device ordinal */
+  int32_t rank, world;    /* world > 1: NCCL exchange for the global cut */
+  const void *nccl_unique_id; /* 128 bytes from scalesim_nccl_unique_id on rank 0, broadcast by the
+                                 caller (e.g. torch.distributed); ignored when world == 1 */
+  void *stream;           /* cudaStream_t for score/plan (0 = legacy default stream) */
+  void *copy_stream;      /* cudaStream_t for the block transfers (must differ from stream to overlap) */
+} scalesim_config;
+
+typedef struct {
+  /* device, read each step: the caller writes them before scalesim_score / scalesim_step */
+  const uint32_t *agent_rec;    /* 4 * n_local uint32, n_local = shard_end - shard_begin, 16-B aligned */
+  const float *agent_kin;       /* 4 * n_kin float, 16-B aligned; may be NULL when n_kin == 0 */
+  /* device, read-only after init: CSR agent -> memory blocks (local agents) */
+  const uint64_t *blk_ptr;      /* n_local + 1 */
+  const uint32_t *blk_size;     /* n_blocks, multiples of page_bytes */
+  const uint64_t *blk_host_off; /* n_blocks, byte offset of the block in host_arena (page aligned) */
+  const uint8_t *blk_kind;      /* n_blocks, 0 LORA / 1 KV / 2 HIST */
+  uint64_t n_blocks;
+  uint64_t n_block_pages;       /* sum over blocks of blk_size / page_bytes */
+  /* arenas (ignored with SCALESIM_F_NO_TRANSFER) */
+  void *host_arena;             /* pinned, device-mapped (cudaHostAlloc / torch pin_memory) */
+  uint64_t host_bytes;
+  void *dev_arena;              /* HBM; dev_bytes / page_bytes pages, >= ceil(budget / page_bytes) */
+  uint64_t dev_bytes;
+  /* scratch: device, >= scalesim_workspace_bytes(), 256-B aligned, owned by the library until destroy */
+  void *workspace;
+  uint64_t workspace_bytes;
+  /* optional device bitmap (n_local bits, 32-agent words) of agents resident at init; their
+     blocks receive pages in id order and (unless NO_TRANSFER) are loaded at init */
+  const uint32_t *resident_init;
+} scalesim_tables;
+
+/* Header fields of a plan (uint64 each), device: scalesim_plan_view.header, host: scalesim_plan_host. */
+enum {
+  SCALESIM_H_N_PREFETCH = 0, /* entries of prefetch_ids */
+  SCALESIM_H_N_EVICT = 1,    /* entries of evict_ids */
+  SCALESIM_H_BYTES_H2D = 2,  /* sum of footprints of prefetched agents */
+  SCALESIM_H_BYTES_D2H = 3,  /* sum of KV+HIST block bytes of evicted dirty agents (R13) */
+  SCALESIM_H_CUT_BITS = 4,   /* f32 bits of the boundary distance D*; 0xFFFFFFFF if all fit */
+  SCALESIM_H_CUT_REM = 5,    /* B - bytes(eligible agents with distance < D*) */
+  SCALESIM_H_STATUS = 6,     /* SCALESIM_ST_* bits */
+  SCALESIM_H_N_D2H = 7,      /* page descriptors in d2h_desc */
+  SCALESIM_H_N_H2D = 8,      /* page descriptors in h2d_desc */
+  SCALESIM_H_KEPT_BYTES = 9, /* bytes of the kept (resident) set, global */
+  SCALESIM_H_N_ELIGIBLE = 10,/* eligible agents on this rank */
+  SCALESIM_H_POOL_HEAD = 11, /* free-page FIFO counters after this plan */
+  SCALESIM_H_POOL_TAIL = 12,
+  SCALESIM_H_FIELDS = 16
+};
+
+typedef struct {
+  /* device views into the workspace; valid until the next scalesim_plan / scalesim_step */
+  const uint32_t *prefetch_ids;    /* global agent ids, ascending (distance, id): most urgent first */
+  const uint32_t *evict_ids;       /* global agent ids, descending (distance, id): largest first */
+  const uint32_t *resident_bitmap; /* kept set after this plan, n_local bits */
+  const float *dist;               /* per local agent distance (valid with SCALESIM_F_KEEP_DIST) */
+  const uint32_t *page_table;      /* per block page: device page index, 0xFFFFFFFF = not resident */
+  const uint64_t *d2h_desc;        /* pairs {host byte offset, device page}, n_d2h entries */
+  const uint64_t *h2d_desc;        /* pairs {host byte offset, device page}, n_h2d entries */
+  const uint64_t *header;          /* SCALESIM_H_FIELDS uint64 */
+  void *done_event;                /* cudaEvent_t recorded on copy_stream after this plan's transfer */
+} scalesim_plan_view;
+
+typedef struct {
+  uint64_t f[SCALESIM_H_FIELDS];   /* host copy of the header, indexed by SCALESIM_H_* */
+} scalesim_plan_host;
+
+/* Bytes of workspace the context needs (0 on invalid config).  Pure host function. */
+uint64_t scalesim_workspace_bytes(const scalesim_config *cfg, const scalesim_tables *tables);
+
+/* Validate cfg/tables, take the workspace, build the page pool from resident_init, create the
+ * NCCL communicator when world > 1.  Synchronous.  *out is NULL on error. */
+scalesim_status scalesim_init(const scalesim_config *cfg, const scalesim_tables *tables, scalesim_ctx **out);
+
+/* (1) Score: invocation distance of every local agent at tick now_tick (Eq. 1-2),
+ * eligibility (R4) and the byte-weighted distance histogram.  If dist_out (device, n_local
+ * floats) is non-NULL the distances are also written there.  Async on cfg.stream. */
+scalesim_status scalesim_score(scalesim_ctx *ctx, int64_t now_tick, float *dist_out);
+
+/* (2)+(3) Plan: rank by (distance, id), cut the longest prefix within the budget, emit the
+ * evict/prefetch lists, the new residency, byte totals and (unless NO_TRANSFER) the page
+ * assignment and copy descriptors.  Requires a preceding scalesim_score.  With world > 1
+ * the NCCL exchange for the global cut runs inside, on cfg.stream.  out may be NULL. */
+scalesim_status scalesim_plan(scalesim_ctx *ctx, scalesim_plan_view *out);
+
+/* (4) Transfer: write back the dirty evicted blocks, then load the prefetched blocks
+ * (device page <-> pinned host), on copy_stream, after the plan's event; records the plan's
+ * done_event.  Requires the most recent plan. */
+scalesim_status scalesim_transfer(scalesim_ctx *ctx, const scalesim_plan_view *plan);
+
+/* score + plan + transfer of one step. */
+scalesim_status scalesim_step(scalesim_ctx *ctx, int64_t now_tick, scalesim_plan_view *out);
+
+/* End-to-end step from HOST buffers: copies host_rec (4*n_local uint32) and host_kin
+ * (4*n_kin float, may be NULL) to the device, runs scalesim_step, waits, and copies the
+ * plan header and lists back (prefetch_out/evict_out: host, n_local capacity each, may be
+ * NULL).  Synchronous.  Returns SCALESIM_E_INSUFFICIENT / _BAD_INPUT per the status word. */
+scalesim_status scalesim_step_host(scalesim_ctx *ctx, int64_t now_tick, const uint32_t *host_rec,
+                                   const float *host_kin, scalesim_plan_host *out,
+                                   uint32_t *prefetch_out, uint32_t *evict_out);
+
+/* Point the context at another record / kinematics buffer (same sizes; device). */
+scalesim_status scalesim_set_inputs(scalesim_ctx *ctx, const uint32_t *agent_rec, const float *agent_kin);
+
+/* Wait for the last plan (and its transfer) and copy its header to the host.  Returns
+ * SCALESIM_E_INSUFFICIENT / SCALESIM_E_BAD_INPUT according to the status word. */
+scalesim_status scalesim_sync(scalesim_ctx *ctx, scalesim_plan_host *out);
+
+/* NCCL unique id (128 bytes) for rank 0 to broadcast. */
+scalesim_status scalesim_nccl_unique_id(void *out128);
+
+/* Make cfg.stream wait for the last plan's transfer (joins copy_stream back into the
+ * caller's stream: required before reading arena pages on cfg.stream, and before ending a
+ * CUDA-graph capture that contains scalesim_transfer). */
+scalesim_status scalesim_join(scalesim_ctx *ctx);
+
+/* Launches of library kernels enqueued so far (for the bench's gpu_launches). */
+uint64_t scalesim_launch_count(const scalesim_ctx *ctx);
+
+/* Destroy the context (synchronises its streams).  NULL is a no-op. */
+void scalesim_destroy(scalesim_ctx *ctx);
+
+const char *scalesim_strerror(scalesim_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCALESIM_H */

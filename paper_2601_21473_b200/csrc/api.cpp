@@ -1,0 +1,593 @@
+// api.cpp — the C ABI of include/scalesim.h: validation, workspace carve-up, the step
+// sequence of launches (kernels.cu), and the NCCL exchange of the global cut (world > 1).
+#include "../../include/scalesim.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "internal.h"
+
+namespace ss {
+
+static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t n_block_pages,
+                   uint64_t n_dev_pages, uint64_t world, bool transfer) {
+  Layout L = {};
+  L.n_local = n_local;
+  L.n_words = (n_local + 31) / 32;
+  L.n_kin = n_kin;
+  L.n_tiles = (n_local + TILE - 1) / TILE;
+  L.n_blocks = n_blocks;
+  L.n_block_pages = transfer ? n_block_pages : 0;
+  L.n_dev_pages = transfer ? n_dev_pages : 0;
+  L.desc_cap = transfer ? (n_block_pages < n_dev_pages ? n_block_pages : n_dev_pages) : 0;
+  L.world = world;
+  L.max_sort_chunks = (n_local + SORT_CH - 1) / SORT_CH + 1;
+  L.max_exp_chunks = (n_local + EXP_CH - 1) / EXP_CH + 1;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) {
+    uint64_t o = off;
+    off = align_up(off + (bytes ? bytes : 1), 256);
+    return o;
+  };
+  const uint64_t n1 = n_local ? n_local : 1, w1 = L.n_words ? L.n_words : 1, k1 = n_kin ? n_kin : 1;
+  const uint64_t t1 = L.n_tiles ? L.n_tiles : 1;
+  L.keys = take(4 * n1);
+  L.elig = take(4 * (w1 + 1));
+  L.bm[0] = take(4 * (w1 + 1));
+  L.bm[1] = take(4 * (w1 + 1));
+  L.dint = take(4 * k1);
+  L.ilist_kin = take(16 * k1);
+  L.ilist_idx = take(4 * k1);
+  L.hist1 = take(8 * 4096);
+  L.mm1 = take(4 * 4096);
+  L.hist2 = take(8 * 1024);
+  L.mm2 = take(4 * 2048);
+  L.hist3 = take(8 * 1024);
+  L.state = take(sizeof(SelState));
+  L.header = take(8 * H_FIELDS);
+  L.gather = take(8 * (world + 8));
+  L.tile_tie = take(8 * t1);
+  L.tile_tie_excl = take(8 * t1);
+  L.tile_pf = take(4 * t1);
+  L.tile_ev = take(4 * t1);
+  L.tile_pf_excl = take(4 * t1);
+  L.tile_ev_excl = take(4 * t1);
+  L.tile_h2d = take(8 * t1);
+  L.tile_tiekept = take(8 * t1);
+  L.tile_elig = take(4 * t1);
+  L.pf_ids = take(4 * n1);
+  L.ev_ids = take(4 * n1);
+  L.sort_ka = take(4 * n1);
+  L.sort_va = take(4 * n1);
+  L.sort_kb = take(4 * n1);
+  L.sort_vb = take(4 * n1);
+  L.pfa_key = take(4 * n1);
+  L.pfa_val = take(4 * n1);
+  L.sort_cnt = take(4 * 2048 * L.max_sort_chunks);
+  L.exp_sum = take(8 * 4 * L.max_exp_chunks);
+  L.exp_excl = take(8 * 4 * L.max_exp_chunks);
+  L.page_first = take(8 * (n_blocks + 1));
+  L.page_table = take(4 * (L.n_block_pages ? L.n_block_pages : 1));
+  L.ring = take(4 * (L.n_dev_pages ? L.n_dev_pages : 1));
+  L.pool = take(16);
+  L.desc[0] = take(16 + 32 * (L.desc_cap ? L.desc_cap : 1));
+  L.desc[1] = take(16 + 32 * (L.desc_cap ? L.desc_cap : 1));
+  L.total = off;
+  return L;
+}
+
+Dev make_dev(void *ws, const Layout &L) {
+  Dev d = {};
+  uint8_t *b = static_cast<uint8_t *>(ws);
+  d.base = b;
+  d.keys = (uint32_t *)(b + L.keys);
+  d.elig = (uint32_t *)(b + L.elig);
+  d.bm[0] = (uint32_t *)(b + L.bm[0]);
+  d.bm[1] = (uint32_t *)(b + L.bm[1]);
+  d.dint = (float *)(b + L.dint);
+  d.ilist_kin = (float4 *)(b + L.ilist_kin);
+  d.ilist_idx = (uint32_t *)(b + L.ilist_idx);
+  d.hist1 = (unsigned long long *)(b + L.hist1);
+  d.mm1 = (uint32_t *)(b + L.mm1);
+  d.hist2 = (unsigned long long *)(b + L.hist2);
+  d.mm2 = (uint32_t *)(b + L.mm2);
+  d.hist3 = (unsigned long long *)(b + L.hist3);
+  d.state = (SelState *)(b + L.state);
+  d.header = (unsigned long long *)(b + L.header);
+  d.gather = (unsigned long long *)(b + L.gather);
+  d.tile_tie = (unsigned long long *)(b + L.tile_tie);
+  d.tile_tie_excl = (unsigned long long *)(b + L.tile_tie_excl);
+  d.tile_pf = (uint32_t *)(b + L.tile_pf);
+  d.tile_ev = (uint32_t *)(b + L.tile_ev);
+  d.tile_pf_excl = (uint32_t *)(b + L.tile_pf_excl);
+  d.tile_ev_excl = (uint32_t *)(b + L.tile_ev_excl);
+  d.tile_h2d = (unsigned long long *)(b + L.tile_h2d);
+  d.tile_tiekept = (unsigned long long *)(b + L.tile_tiekept);
+  d.tile_elig = (uint32_t *)(b + L.tile_elig);
+  d.pf_ids = (uint32_t *)(b + L.pf_ids);
+  d.ev_ids = (uint32_t *)(b + L.ev_ids);
+  d.sort_ka = (uint32_t *)(b + L.sort_ka);
+  d.sort_va = (uint32_t *)(b + L.sort_va);
+  d.sort_kb = (uint32_t *)(b + L.sort_kb);
+  d.sort_vb = (uint32_t *)(b + L.sort_vb);
+  d.pfa_key = (uint32_t *)(b + L.pfa_key);
+  d.pfa_val = (uint32_t *)(b + L.pfa_val);
+  d.sort_cnt = (uint32_t *)(b + L.sort_cnt);
+  d.exp_sum = (unsigned long long *)(b + L.exp_sum);
+  d.exp_excl = (unsigned long long *)(b + L.exp_excl);
+  d.page_first = (unsigned long long *)(b + L.page_first);
+  d.page_table = (uint32_t *)(b + L.page_table);
+  d.ring = (uint32_t *)(b + L.ring);
+  d.pool = (unsigned long long *)(b + L.pool);
+  d.desc[0] = (unsigned long long *)(b + L.desc[0]);
+  d.desc[1] = (unsigned long long *)(b + L.desc[1]);
+  return d;
+}
+
+void launch_init_page_table(const Params &p, uint64_t n_block_pages, const uint32_t *res, uint64_t *cnt_dev,
+                            cudaStream_t s);
+int launch_fix_kept(const Params &p, cudaStream_t s);
+int launch_mask_tail(const Params &p, cudaStream_t s);
+
+// ---- NCCL, loaded lazily so the library has no link-time NCCL dependency ----
+struct Nccl {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    return GetUniqueId && CommInitRank && CommDestroy && AllReduce && AllGather;
+  }
+};
+static Nccl g_nccl;
+
+}  // namespace ss
+
+using namespace ss;
+
+struct scalesim_ctx {
+  scalesim_config cfg;
+  scalesim_tables tab;
+  Layout L;
+  Params p;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  cudaEvent_t ev_plan = nullptr, ev_xfer[2] = {nullptr, nullptr};
+  bool transfer = false;
+  int grid = 592;
+  int copy_ctas = 64;
+  uint64_t step = 0;        // plans made
+  bool scored = false, planned = false, transferred = true;
+  uint64_t launches = 0;
+  ncclComm_t comm = nullptr;
+  int last_buf = 0;
+  bool xfer_pending = false;
+};
+
+static scalesim_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SCALESIM_OK : SCALESIM_E_CUDA; }
+
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t _e = (x);                                                           \
+    if (_e != cudaSuccess) {                                                        \
+      if (getenv("SCALESIM_VERBOSE")) fprintf(stderr, "scalesim: %s: %s\n", #x, cudaGetErrorString(_e)); \
+      return SCALESIM_E_CUDA;                                                       \
+    }                                                                               \
+  } while (0)
+
+#define NK(x)                                  \
+  do {                                         \
+    if ((x) != ncclSuccess) return SCALESIM_E_NCCL; \
+  } while (0)
+
+static bool aligned(const void *p, uint64_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+static scalesim_status validate_config(const scalesim_config *c) {
+  if (!c || c->abi_version != SCALESIM_ABI_VERSION) return SCALESIM_E_INVALID;
+  if (c->shard_begin > c->shard_end || c->shard_end > c->n_agents) return SCALESIM_E_INVALID;
+  if (c->n_agents > 0xFFFFFFFFull) return SCALESIM_E_INVALID;  // ids are uint32
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return SCALESIM_E_INVALID;
+  if (c->world == 1 && (c->shard_begin != 0 || c->shard_end != c->n_agents)) return SCALESIM_E_INVALID;
+  if (c->world > 1 && c->n_kin > 0) return SCALESIM_E_INVALID;  // interaction agents: single rank
+  for (int k = 0; k < 3; ++k)
+    if (std::isnan(c->theta[k]) || c->theta[k] < 0.0f) return SCALESIM_E_INVALID;
+  if (!(c->hop_scale > 0.0f) || std::isinf(c->hop_scale)) return SCALESIM_E_INVALID;
+  if (!(c->flags & SCALESIM_F_NO_TRANSFER)) {
+    if (c->page_bytes == 0 || c->page_bytes % 4096 != 0) return SCALESIM_E_INVALID;
+  }
+  return SCALESIM_OK;
+}
+
+extern "C" uint64_t scalesim_workspace_bytes(const scalesim_config *cfg, const scalesim_tables *t) {
+  if (validate_config(cfg) != SCALESIM_OK || !t) return 0;
+  const bool transfer = !(cfg->flags & SCALESIM_F_NO_TRANSFER);
+  const uint64_t n_local = cfg->shard_end - cfg->shard_begin;
+  const uint64_t n_dev_pages = transfer ? t->dev_bytes / cfg->page_bytes : 0;
+  Layout L = make_layout(n_local, cfg->n_kin, t->n_blocks, t->n_block_pages, n_dev_pages, cfg->world, transfer);
+  return L.total;
+}
+
+extern "C" const char *scalesim_strerror(scalesim_status s) {
+  switch (s) {
+    case SCALESIM_OK: return "ok";
+    case SCALESIM_E_INVALID: return "invalid argument";
+    case SCALESIM_E_INSUFFICIENT: return "insufficient memory: active agents exceed the budget";
+    case SCALESIM_E_NOT_RESTORABLE: return "block not restorable (no host backing)";
+    case SCALESIM_E_ORDER: return "calls out of order";
+    case SCALESIM_E_CUDA: return "CUDA error";
+    case SCALESIM_E_NCCL: return "NCCL error";
+    case SCALESIM_E_INVARIANT: return "invariant violation";
+    case SCALESIM_E_BAD_INPUT: return "malformed agent record or kinematics";
+  }
+  return "unknown status";
+}
+
+extern "C" scalesim_status scalesim_nccl_unique_id(void *out128) {
+  if (!out128) return SCALESIM_E_INVALID;
+  if (!g_nccl.load()) return SCALESIM_E_NCCL;
+  ncclUniqueId id;
+  NK(g_nccl.GetUniqueId(&id));
+  memcpy(out128, &id, sizeof(id));
+  return SCALESIM_OK;
+}
+
+extern "C" uint64_t scalesim_launch_count(const scalesim_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scalesim_tables *t, scalesim_ctx **out) {
+  if (!out) return SCALESIM_E_INVALID;
+  *out = nullptr;
+  scalesim_status st = validate_config(cfg);
+  if (st != SCALESIM_OK || !t) return SCALESIM_E_INVALID;
+  const bool transfer = !(cfg->flags & SCALESIM_F_NO_TRANSFER);
+  const uint64_t n_local = cfg->shard_end - cfg->shard_begin;
+  if (n_local > 0 && (!t->agent_rec || !aligned(t->agent_rec, 16))) return SCALESIM_E_INVALID;
+  if (cfg->n_kin > 0 && (!t->agent_kin || !aligned(t->agent_kin, 16))) return SCALESIM_E_INVALID;
+  if (!t->blk_ptr || (t->n_blocks > 0 && (!t->blk_size || !t->blk_kind || !t->blk_host_off))) return SCALESIM_E_INVALID;
+  if (!t->workspace || !aligned(t->workspace, 256)) return SCALESIM_E_INVALID;
+  uint64_t n_dev_pages = 0;
+  if (transfer) {
+    if (!t->dev_arena || !t->host_arena) return SCALESIM_E_INVALID;
+    if (!aligned(t->dev_arena, 16) || !aligned(t->host_arena, 16)) return SCALESIM_E_INVALID;
+    n_dev_pages = t->dev_bytes / cfg->page_bytes;
+    const uint64_t need = (cfg->budget_bytes + cfg->page_bytes - 1) / cfg->page_bytes;
+    if (n_dev_pages < need || n_dev_pages > 0xFFFFFFFFull) return SCALESIM_E_INVALID;
+  }
+  Layout L = make_layout(n_local, cfg->n_kin, t->n_blocks, t->n_block_pages, n_dev_pages, cfg->world, transfer);
+  if (t->workspace_bytes < L.total) return SCALESIM_E_INVALID;
+
+  CK(cudaSetDevice(cfg->device));
+  scalesim_ctx *c = new (std::nothrow) scalesim_ctx();
+  if (!c) return SCALESIM_E_INVALID;
+  c->cfg = *cfg;
+  c->tab = *t;
+  c->L = L;
+  c->transfer = transfer;
+  c->stream = static_cast<cudaStream_t>(cfg->stream);
+  c->copy_stream = cfg->copy_stream ? static_cast<cudaStream_t>(cfg->copy_stream) : c->stream;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  c->grid = sms * 4;
+  c->copy_ctas = sms / 2;
+  auto fail = [&](scalesim_status s) {
+    scalesim_destroy(c);
+    return s;
+  };
+  if (cudaEventCreateWithFlags(&c->ev_plan, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_xfer[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_xfer[1], cudaEventDisableTiming) != cudaSuccess)
+    return fail(SCALESIM_E_CUDA);
+
+  Params &p = c->p;
+  p.n_local = n_local;
+  p.n_words = L.n_words;
+  p.n_kin = cfg->n_kin;
+  p.n_tiles = L.n_tiles;
+  p.shard_begin = cfg->shard_begin;
+  p.budget = cfg->budget_bytes;
+  p.page_bytes = cfg->page_bytes;
+  p.n_dev_pages = n_dev_pages;
+  p.desc_cap = L.desc_cap;
+  for (int k = 0; k < 3; ++k) p.theta[k] = cfg->theta[k];
+  p.hop_scale = cfg->hop_scale;
+  p.rank = cfg->rank;
+  p.world = cfg->world;
+  p.rec = reinterpret_cast<const uint4 *>(t->agent_rec);
+  p.kin = reinterpret_cast<const float4 *>(t->agent_kin);
+  p.blk_ptr = reinterpret_cast<const unsigned long long *>(t->blk_ptr);
+  p.blk_size = t->blk_size;
+  p.blk_host_off = reinterpret_cast<const unsigned long long *>(t->blk_host_off);
+  p.blk_kind = t->blk_kind;
+  p.host_arena = static_cast<uint8_t *>(t->host_arena);
+  p.dev_arena = static_cast<uint8_t *>(t->dev_arena);
+  p.cur = 0;
+  p.desc_buf = 0;
+  p.d = make_dev(t->workspace, L);
+
+  // Host-side validation of the block table: sizes are page multiples, CSR is monotone,
+  // n_block_pages matches; page_first (prefix of pages per block) goes to the workspace.
+  std::vector<uint64_t> bp(n_local + 1);
+  if (cudaMemcpy(bp.data(), t->blk_ptr, 8 * (n_local + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SCALESIM_E_CUDA);
+  if (bp[0] != 0 || bp[n_local] != t->n_blocks) return fail(SCALESIM_E_INVALID);
+  for (uint64_t a = 0; a < n_local; ++a)
+    if (bp[a + 1] < bp[a]) return fail(SCALESIM_E_INVALID);
+  std::vector<uint64_t> pf(t->n_blocks + 1, 0);
+  if (t->n_blocks > 0) {
+    std::vector<uint32_t> bs(t->n_blocks);
+    std::vector<uint8_t> bk(t->n_blocks);
+    std::vector<uint64_t> bo(t->n_blocks);
+    if (cudaMemcpy(bs.data(), t->blk_size, 4 * t->n_blocks, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(bk.data(), t->blk_kind, t->n_blocks, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(bo.data(), t->blk_host_off, 8 * t->n_blocks, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(SCALESIM_E_CUDA);
+    const uint64_t pb = transfer ? cfg->page_bytes : 0;
+    for (uint64_t b = 0; b < t->n_blocks; ++b) {
+      if (bk[b] > 2) return fail(SCALESIM_E_INVALID);
+      if (transfer) {
+        if (bs[b] % pb != 0 || bo[b] % 16 != 0 || bo[b] + bs[b] > t->host_bytes) return fail(SCALESIM_E_INVALID);
+        pf[b + 1] = pf[b] + bs[b] / pb;
+      }
+    }
+  }
+  if (transfer && pf[t->n_blocks] != t->n_block_pages) return fail(SCALESIM_E_INVALID);
+  if (cudaMemsetAsync(t->workspace, 0, L.total, c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
+  if (cudaMemcpyAsync(p.d.page_first, pf.data(), 8 * (t->n_blocks + 1), cudaMemcpyHostToDevice, c->stream) !=
+      cudaSuccess)
+    return fail(SCALESIM_E_CUDA);
+  c->launches += launch_init_pages(p, t->resident_init, c->stream);
+  c->launches += launch_mask_tail(p, c->stream);
+  if (transfer) {
+    uint64_t *cnt = reinterpret_cast<uint64_t *>(p.d.gather);
+    launch_init_page_table(p, L.n_block_pages, t->resident_init, cnt, c->stream);
+    c->launches += 2;
+    if (t->resident_init) {
+      // load the initially resident blocks (synchronous, init time)
+      std::vector<uint32_t> pt(L.n_block_pages ? L.n_block_pages : 1);
+      if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
+      if (L.n_block_pages &&
+          cudaMemcpy(pt.data(), p.d.page_table, 4 * L.n_block_pages, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(SCALESIM_E_CUDA);
+      std::vector<uint64_t> bo(t->n_blocks ? t->n_blocks : 1);
+      if (t->n_blocks && cudaMemcpy(bo.data(), t->blk_host_off, 8 * t->n_blocks, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(SCALESIM_E_CUDA);
+      std::vector<uint64_t> desc(2);
+      uint64_t nh = 0;
+      for (uint64_t b = 0; b < t->n_blocks; ++b)
+        for (uint64_t q = pf[b]; q < pf[b + 1]; ++q)
+          if (pt[q] != PAGE_NONE) {
+            desc.push_back(bo[b] + (q - pf[b]) * cfg->page_bytes);
+            desc.push_back(pt[q]);
+            ++nh;
+          }
+      // layout of a descriptor buffer: [n_d2h, n_h2d, d2h pairs (desc_cap), h2d pairs]
+      std::vector<uint64_t> buf(2 + 4 * (L.desc_cap ? L.desc_cap : 1), 0);
+      buf[0] = 0;
+      buf[1] = nh;
+      if (nh > L.desc_cap) return fail(SCALESIM_E_INVALID);
+      for (uint64_t k = 0; k < 2 * nh; ++k) buf[2 + 2 * L.desc_cap + k] = desc[2 + k];
+      if (cudaMemcpy(p.d.desc[0], buf.data(), 8 * buf.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(SCALESIM_E_CUDA);
+      p.desc_buf = 0;
+      c->launches += launch_transfer(p, c->stream, c->copy_ctas);
+    }
+  }
+  c->launches += launch_plan_init(p, c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
+  if (cfg->world > 1) {
+    if (!cfg->nccl_unique_id || !g_nccl.load()) return fail(SCALESIM_E_NCCL);
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+    if (g_nccl.CommInitRank(&c->comm, cfg->world, id, cfg->rank) != ncclSuccess) return fail(SCALESIM_E_NCCL);
+  }
+  *out = c;
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_set_inputs(scalesim_ctx *c, const uint32_t *rec, const float *kin) {
+  if (!c) return SCALESIM_E_INVALID;
+  if (c->p.n_local > 0 && (!rec || !aligned(rec, 16))) return SCALESIM_E_INVALID;
+  if (c->p.n_kin > 0 && (!kin || !aligned(kin, 16))) return SCALESIM_E_INVALID;
+  c->p.rec = reinterpret_cast<const uint4 *>(rec);
+  c->p.kin = reinterpret_cast<const float4 *>(kin);
+  c->tab.agent_rec = rec;
+  c->tab.agent_kin = kin;
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_score(scalesim_ctx *c, int64_t now, float *dist_out) {
+  if (!c) return SCALESIM_E_INVALID;
+  CK(cudaGetLastError());
+  // the accumulators were cleared at the end of the previous plan (or at init); a repeated
+  // score without a plan clears them again
+  if (c->scored) c->launches += launch_plan_init(c->p, c->stream);
+  c->launches += launch_score(c->p, now, dist_out, c->stream, c->grid);
+  CK(cudaGetLastError());
+  c->scored = true;
+  return SCALESIM_OK;
+}
+
+static scalesim_status allreduce(scalesim_ctx *c, void *buf, size_t n, ncclDataType_t t, ncclRedOp_t op) {
+  NK(g_nccl.AllReduce(buf, buf, n, t, op, c->comm, c->stream));
+  return SCALESIM_OK;
+}
+
+static void fill_plan(scalesim_ctx *c, scalesim_plan_view *out) {
+  if (!out) return;
+  const Params &p = c->p;
+  out->prefetch_ids = p.d.pf_ids;
+  out->evict_ids = p.d.ev_ids;
+  out->resident_bitmap = p.d.bm[p.cur];  // after the flip: the new residency
+  out->dist = reinterpret_cast<const float *>(p.d.keys);
+  out->page_table = p.d.page_table;
+  out->d2h_desc = reinterpret_cast<const uint64_t *>(p.d.desc[c->last_buf] + 2);
+  out->h2d_desc = reinterpret_cast<const uint64_t *>(p.d.desc[c->last_buf] + 2 + 2 * p.desc_cap);
+  out->header = reinterpret_cast<const uint64_t *>(p.d.header);
+  out->done_event = c->ev_xfer[c->last_buf];
+}
+
+extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *out) {
+  if (!c) return SCALESIM_E_INVALID;
+  if (!c->scored) return SCALESIM_E_ORDER;
+  Params &p = c->p;
+  const bool multi = c->cfg.world > 1;
+  if (multi) {
+    scalesim_status s;
+    if ((s = allreduce(c, p.d.hist1, 2049, ncclUint64, ncclSum)) != SCALESIM_OK) return s;
+    if ((s = allreduce(c, p.d.mm1, 4096, ncclUint32, ncclMin)) != SCALESIM_OK) return s;
+  }
+  c->launches += launch_select(p, 1, c->stream);
+  c->launches += launch_hist(p, 2, c->stream, c->grid);
+  if (multi) {
+    scalesim_status s;
+    if ((s = allreduce(c, p.d.hist2, 1024, ncclUint64, ncclSum)) != SCALESIM_OK) return s;
+    if ((s = allreduce(c, p.d.mm2, 2048, ncclUint32, ncclMin)) != SCALESIM_OK) return s;
+  }
+  c->launches += launch_select(p, 2, c->stream);
+  c->launches += launch_hist(p, 3, c->stream, c->grid);
+  if (multi) {
+    scalesim_status s;
+    if ((s = allreduce(c, p.d.hist3, 1024, ncclUint64, ncclSum)) != SCALESIM_OK) return s;
+  }
+  c->launches += launch_select(p, 3, c->stream);
+  c->launches += launch_tie(p, c->stream);
+  if (multi) {
+    NK(g_nccl.AllGather(&p.d.state->tie_local, p.d.gather, 1, ncclUint64, c->comm, c->stream));
+  }
+  c->launches += launch_emit(p, c->stream);
+  if (multi) {
+    scalesim_status s;
+    if ((s = allreduce(c, &p.d.state->tie_kept, 1, ncclUint64, ncclSum)) != SCALESIM_OK) return s;
+    c->launches += launch_fix_kept(p, c->stream);
+  }
+  c->launches += launch_lists(p, c->stream);
+  const int buf = (int)(c->step & 1);
+  p.desc_buf = buf;
+  if (c->transfer) {
+    // the descriptor buffer `buf` was last read by the transfer of plan step-2
+    CK(cudaStreamWaitEvent(c->stream, c->ev_xfer[buf], 0));
+    if (buf == c->last_buf) c->xfer_pending = false;
+  }
+  c->launches += launch_expand(p, c->stream);  // byte accounting always; pages only with transfer
+  CK(cudaEventRecord(c->ev_plan, c->stream));
+  c->launches += launch_plan_init(p, c->stream);  // clear the accumulators for the next step
+  CK(cudaGetLastError());
+  c->last_buf = buf;
+  p.cur ^= 1;  // the new residency becomes current
+  c->step++;
+  c->scored = false;
+  c->planned = true;
+  c->transferred = false;
+  fill_plan(c, out);
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_transfer(scalesim_ctx *c, const scalesim_plan_view *plan) {
+  if (!c) return SCALESIM_E_INVALID;
+  if (!c->planned || c->transferred) return SCALESIM_E_ORDER;
+  if (plan && plan->header != reinterpret_cast<const uint64_t *>(c->p.d.header)) return SCALESIM_E_ORDER;
+  const int buf = c->last_buf;
+  if (c->transfer) {
+    CK(cudaStreamWaitEvent(c->copy_stream, c->ev_plan, 0));
+    Params q = c->p;
+    q.desc_buf = buf;
+    c->launches += launch_transfer(q, c->copy_stream, c->copy_ctas);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_xfer[buf], c->copy_stream));
+    c->xfer_pending = true;
+  }
+  c->transferred = true;
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_join(scalesim_ctx *c) {
+  if (!c) return SCALESIM_E_INVALID;
+  if (c->xfer_pending) {
+    CK(cudaStreamWaitEvent(c->stream, c->ev_xfer[c->last_buf], 0));
+    c->xfer_pending = false;
+  }
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_step(scalesim_ctx *c, int64_t now, scalesim_plan_view *out) {
+  scalesim_status s = scalesim_score(c, now, nullptr);
+  if (s != SCALESIM_OK) return s;
+  scalesim_plan_view pl;
+  if ((s = scalesim_plan(c, &pl)) != SCALESIM_OK) return s;
+  if ((s = scalesim_transfer(c, &pl)) != SCALESIM_OK) return s;
+  if (out) *out = pl;
+  return SCALESIM_OK;
+}
+
+static scalesim_status status_of_header(uint64_t st) {
+  if (st & (SCALESIM_ST_BAD_RECORD | SCALESIM_ST_BAD_KIN)) return SCALESIM_E_BAD_INPUT;
+  if (st & SCALESIM_ST_NO_PAGES) return SCALESIM_E_INVARIANT;
+  if (st & SCALESIM_ST_INSUFFICIENT) return SCALESIM_E_INSUFFICIENT;
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_sync(scalesim_ctx *c, scalesim_plan_host *out) {
+  if (!c) return SCALESIM_E_INVALID;
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->copy_stream));
+  scalesim_plan_host h;
+  CK(cudaMemcpy(h.f, c->p.d.header, sizeof(h.f), cudaMemcpyDeviceToHost));
+  if (out) *out = h;
+  return c->planned ? status_of_header(h.f[SCALESIM_H_STATUS]) : SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, const uint32_t *host_rec,
+                                              const float *host_kin, scalesim_plan_host *out, uint32_t *pf_out,
+                                              uint32_t *ev_out) {
+  if (!c || !host_rec) return SCALESIM_E_INVALID;
+  if (c->p.n_kin > 0 && !host_kin) return SCALESIM_E_INVALID;
+  CK(cudaMemcpyAsync(const_cast<uint4 *>(c->p.rec), host_rec, 16 * c->p.n_local, cudaMemcpyHostToDevice, c->stream));
+  if (c->p.n_kin > 0)
+    CK(cudaMemcpyAsync(const_cast<float4 *>(c->p.kin), host_kin, 16 * c->p.n_kin, cudaMemcpyHostToDevice, c->stream));
+  scalesim_status s = scalesim_step(c, now, nullptr);
+  if (s != SCALESIM_OK) return s;
+  scalesim_plan_host h;
+  CK(cudaMemcpyAsync(h.f, c->p.d.header, sizeof(h.f), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (pf_out && h.f[SCALESIM_H_N_PREFETCH])
+    CK(cudaMemcpyAsync(pf_out, c->p.d.pf_ids, 4 * h.f[SCALESIM_H_N_PREFETCH], cudaMemcpyDeviceToHost, c->stream));
+  if (ev_out && h.f[SCALESIM_H_N_EVICT])
+    CK(cudaMemcpyAsync(ev_out, c->p.d.ev_ids, 4 * h.f[SCALESIM_H_N_EVICT], cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->copy_stream));
+  if (out) *out = h;
+  return status_of_header(h.f[SCALESIM_H_STATUS]);
+}
+
+extern "C" void scalesim_destroy(scalesim_ctx *c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->ev_plan) cudaEventDestroy(c->ev_plan);
+  for (int k = 0; k < 2; ++k)
+    if (c->ev_xfer[k]) cudaEventDestroy(c->ev_xfer[k]);
+  delete c;
+}

@@ -1,0 +1,115 @@
+// internal.h — shared between api.cpp (host, C ABI) and kernels.cu (device).  Not installed.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ss {
+
+constexpr int NT = 256;                   // threads per block of the agent-scan kernels
+constexpr uint32_t TILE = 2048;           // agents per tile (id-ordered kernels); multiple of 32
+constexpr uint32_t SORT_CH = 8192;        // list elements per sort chunk
+constexpr uint32_t EXP_CH = 256;          // list entries per expansion chunk
+constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;
+constexpr uint32_t PAGE_NONE = 0xFFFFFFFFu;
+constexpr int L1_BITS = 11, L2_BITS = 10, L3_BITS = 10;  // distance-bit digits [30:20] [19:10] [9:0]
+
+// status bits (mirror include/scalesim.h)
+constexpr uint32_t ST_INSUFFICIENT = 1u, ST_BAD_RECORD = 2u, ST_BAD_KIN = 4u, ST_NO_PAGES = 8u;
+
+// header fields (mirror SCALESIM_H_*)
+enum { H_N_PF = 0, H_N_EV, H_H2D, H_D2H, H_CUT_BITS, H_CUT_REM, H_STATUS, H_N_D2H, H_N_H2D,
+       H_KEPT, H_N_ELIG, H_POOL_HEAD, H_POOL_TAIL, H_FIELDS = 16 };
+
+// Device-side selection state of one plan (radix select of the boundary distance).
+struct SelState {
+  unsigned long long below;      // bytes of eligible agents with key < prefix range (global)
+  unsigned long long rem;        // B - bytes(d < D*)
+  unsigned long long total;      // total eligible bytes (global)
+  unsigned long long tie_local;  // this rank's bytes at d == D*
+  unsigned long long tie_kept;   // this rank's kept bytes at d == D*
+  unsigned long long zero_bytes; // bytes of d == 0 agents (global after exchange)
+  unsigned int prefix;           // distance bits fixed so far
+  unsigned int level;            // next histogram level to build (1..3), 4 = resolved
+  unsigned int done;             // D* resolved
+  unsigned int all_fit;          // every eligible agent fits
+  unsigned int dstar;            // boundary distance bits
+  unsigned int status;           // SCALESIM_ST_* of this plan
+  unsigned int int_count;        // interaction participants
+  unsigned int sort_or[2], sort_and[2];  // varying-bit analysis of the two lists
+  unsigned int pad[3];
+};
+
+// Workspace carve-up (byte offsets from the workspace base, 256-B aligned).
+struct Layout {
+  uint64_t n_local, n_words, n_kin, n_tiles, n_blocks, n_block_pages, n_dev_pages, desc_cap, world;
+  uint64_t max_sort_chunks, max_exp_chunks;
+  uint64_t keys, elig, bm[2], dint, ilist_kin, ilist_idx;
+  uint64_t hist1, mm1, hist2, mm2, hist3, state, header, gather;
+  uint64_t tile_tie, tile_tie_excl, tile_pf, tile_ev, tile_pf_excl, tile_ev_excl, tile_h2d, tile_tiekept, tile_elig;
+  uint64_t pf_ids, ev_ids, sort_ka, sort_va, sort_kb, sort_vb, sort_cnt, pfa_key, pfa_val;
+  uint64_t exp_sum, exp_excl;
+  uint64_t page_first, page_table, ring, pool, desc[2];
+  uint64_t total;
+};
+
+Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t n_block_pages,
+                   uint64_t n_dev_pages, uint64_t world, bool transfer);
+
+// Pointers derived from the layout.
+struct Dev {
+  uint8_t *base;
+  uint32_t *keys, *elig, *bm[2];
+  float *dint;
+  float4 *ilist_kin;
+  uint32_t *ilist_idx;
+  unsigned long long *hist1, *hist2, *hist3;
+  uint32_t *mm1, *mm2;  // [0, 2^w) min of bits, [2^w, 2^(w+1)) min of ~bits (= ~max)
+  SelState *state;
+  unsigned long long *header, *gather;
+  unsigned long long *tile_tie, *tile_tie_excl, *tile_h2d, *tile_tiekept;
+  uint32_t *tile_pf, *tile_ev, *tile_pf_excl, *tile_ev_excl, *tile_elig;
+  uint32_t *pf_ids, *ev_ids;
+  uint32_t *sort_ka, *sort_va, *sort_kb, *sort_vb, *sort_cnt, *pfa_key, *pfa_val;
+  unsigned long long *exp_sum, *exp_excl;
+  unsigned long long *page_first;
+  uint32_t *page_table, *ring;
+  unsigned long long *pool;  // [0] head, [1] tail
+  unsigned long long *desc[2];  // each: d2h [desc_cap pairs] then h2d [desc_cap pairs]
+};
+
+Dev make_dev(void *ws, const Layout &L);
+
+struct Params {
+  // sizes
+  uint64_t n_local, n_words, n_kin, n_tiles, shard_begin, budget, page_bytes, n_dev_pages, desc_cap;
+  float theta[3];
+  float hop_scale;
+  int rank, world;
+  // inputs
+  const uint4 *rec;
+  const float4 *kin;
+  const unsigned long long *blk_ptr;
+  const uint32_t *blk_size;
+  const unsigned long long *blk_host_off;
+  const uint8_t *blk_kind;
+  uint8_t *host_arena, *dev_arena;
+  // state
+  int cur;  // index of the residency bitmap holding the residency before this plan
+  int desc_buf;
+  Dev d;
+};
+
+// Launchers (kernels.cu).  Each returns the number of kernels it enqueued.
+int launch_plan_init(const Params &p, cudaStream_t s);
+int launch_score(const Params &p, int64_t now, float *dist_out, cudaStream_t s, int grid);
+int launch_select(const Params &p, int level, cudaStream_t s);
+int launch_hist(const Params &p, int level, cudaStream_t s, int grid);
+int launch_tie(const Params &p, cudaStream_t s);
+int launch_emit(const Params &p, cudaStream_t s);
+int launch_lists(const Params &p, cudaStream_t s);
+int launch_expand(const Params &p, cudaStream_t s);
+int launch_transfer(const Params &p, cudaStream_t s, int ctas);
+int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s);
+int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s);
+
+}  // namespace ss

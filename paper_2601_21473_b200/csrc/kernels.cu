@@ -1,0 +1,1076 @@
+// kernels.cu — sm_100a kernels of the ScaleSim planner (multi-kernel path, v1).
+//
+// Step = score (a1, a1', a2) -> radix select of the boundary distance (a3) -> id-order tie
+// scan and emit (a4, a5) -> list compaction + stable radix sort by distance (a5) -> block
+// expansion / page assignment (a5) -> page copies pinned host <-> HBM (a6).
+// See DESIGN.md §7 for the kernel list, the data layout and the roofline of each kernel.
+//
+// Floating point: the distance arithmetic uses explicit round-to-nearest intrinsics so
+// that nvcc cannot contract into FMA; the same op sequence as PAPER Eq. 2 reading R7.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace ss {
+
+#define FULL 0xFFFFFFFFu
+
+// ------------------------------------------------------------------------------------
+// small helpers
+
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan (blockDim.x == NT).  *total (shared memory) receives the sum;
+// it is valid after the call.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T *total) {
+  __shared__ T sh[NT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T incl = warp_incl_scan(v);
+  if (lane == 31) sh[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const T w = lane < NT / 32 ? sh[lane] : T(0);
+    const T wi = warp_incl_scan(w);
+    if (lane < NT / 32) sh[lane] = wi - w;
+    if (lane == NT / 32 - 1) *total = wi;
+  }
+  __syncthreads();
+  const T r = sh[warp] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+// Block-wide sum; the result is valid in every thread.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v) {
+  __shared__ T sh[NT / 32 + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T t = T(0);
+    for (int w = 0; w < NT / 32; ++w) t += sh[w];
+    sh[NT / 32] = t;
+  }
+  __syncthreads();
+  const T r = sh[NT / 32];
+  __syncthreads();
+  return r;
+}
+
+// 64-bit sum over the lanes in `mask` of a 32-bit value (exact: split in 16-bit halves).
+__device__ __forceinline__ unsigned long long warp_sum_u32_exact(uint32_t v) {
+  uint32_t lo = __reduce_add_sync(FULL, v & 0xFFFFu);
+  uint32_t hi = __reduce_add_sync(FULL, v >> 16);
+  return ((unsigned long long)hi << 16) + lo;
+}
+
+__device__ __forceinline__ uint32_t phase_of(uint4 r) { return r.z & 3u; }
+__device__ __forceinline__ uint32_t class_of(uint4 r) { return (r.z >> 2) & 3u; }
+
+// ------------------------------------------------------------------------------------
+// a1: invocation distance of one agent (readings R5, R8, R9)
+
+__device__ __forceinline__ float distance_of(uint4 r, int64_t now, float hop_scale, const float *dint,
+                                             uint64_t n_kin, uint32_t &st) {
+  const uint32_t ph = phase_of(r), cl = class_of(r);
+  float d;
+  if (cl == 3u) st |= ST_BAD_RECORD;
+  if (ph == 1u || ph == 2u) {
+    d = 0.0f;                                  // WAITING / GENERATING
+  } else if (ph == 3u) {
+    d = __int_as_float(0x7F800000);            // IDLE: +inf
+  } else if (cl == 0u || cl == 1u) {
+    const int64_t remain = (int64_t)r.x - now; // D_action
+    const float d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
+    d = d_action;
+    if (cl == 1u) {                            // Eq. 1: D = min(D_action, D_interaction)
+      float d_int = __int_as_float(0x7F800000);
+      if (r.w < n_kin) d_int = dint[r.w];
+      else st |= ST_BAD_RECORD;
+      if (d_int < d_action) d = d_int;
+    }
+  } else if (cl == 2u) {                       // hop count x hop_scale (R5)
+    d = (r.x == 0xFFFFFFFFu) ? __int_as_float(0x7F800000) : __fmul_rn(__uint2float_rn(r.x), hop_scale);
+  } else {
+    d = __int_as_float(0x7F800000);
+  }
+  if (d == 0.0f) d = 0.0f;  // canonical +0 (R8)
+  return d;
+}
+
+__device__ __forceinline__ float theta_of(const Params &p, uint32_t cl) {
+  return cl == 0u ? p.theta[0] : cl == 1u ? p.theta[1] : cl == 2u ? p.theta[2] : 0.0f;
+}
+
+// ------------------------------------------------------------------------------------
+// plan init: clear per-plan accumulators
+
+__global__ void k_plan_init(Params p) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 2048) {
+    p.d.hist1[t] = 0;
+    p.d.mm1[t] = 0xFFFFFFFFu;
+    p.d.mm1[2048 + t] = 0xFFFFFFFFu;
+  }
+  if (t < 1024) {
+    p.d.hist2[t] = 0;
+    p.d.hist3[t] = 0;
+    p.d.mm2[t] = 0xFFFFFFFFu;
+    p.d.mm2[1024 + t] = 0xFFFFFFFFu;
+  }
+  if (t == 0) {
+    SelState z = {};
+    z.level = 1;
+    z.sort_and[0] = z.sort_and[1] = 0xFFFFFFFFu;
+    *p.d.state = z;
+    p.d.hist1[2048] = 0;  // zero-distance bytes slot (exchanged with the histogram)
+  }
+  // the header is not cleared: every field is rewritten by the plan that owns it
+}
+
+// ------------------------------------------------------------------------------------
+// a1': interaction participants (ACTING INT agents with finite kinematics) and pair-min
+
+__global__ void __launch_bounds__(NT) k_int_compact(Params p) {
+  uint32_t st = 0;
+  for (uint64_t k = blockIdx.x * (uint64_t)NT + threadIdx.x; k < p.n_kin; k += (uint64_t)gridDim.x * NT)
+    p.d.dint[k] = __int_as_float(0x7F800000);
+  for (uint64_t base = blockIdx.x * (uint64_t)NT; base < p.n_local; base += (uint64_t)gridDim.x * NT) {
+    const uint64_t i = base + threadIdx.x;
+    bool part = false;
+    float4 kv = make_float4(0, 0, 0, 0);
+    uint32_t ki = 0;
+    if (i < p.n_local) {
+      const uint4 r = ld_stream(p.rec + i);
+      if (phase_of(r) == 0u && class_of(r) == 1u) {
+        if (r.w >= p.n_kin) {
+          st |= ST_BAD_RECORD;
+        } else {
+          kv = p.kin[r.w];
+          ki = r.w;
+          if (isfinite(kv.x) && isfinite(kv.y) && isfinite(kv.z) && isfinite(kv.w)) part = true;
+          else st |= ST_BAD_KIN;
+        }
+      }
+    }
+    const uint32_t m = __ballot_sync(FULL, part);
+    if (m) {
+      const int lane = threadIdx.x & 31;
+      uint32_t base_slot = 0;
+      if (lane == __ffs(m) - 1) base_slot = atomicAdd(&p.d.state->int_count, __popc(m));
+      base_slot = __shfl_sync(FULL, base_slot, __ffs(m) - 1);
+      if (part) {
+        const uint32_t slot = base_slot + __popc(m & lanemask_lt());
+        p.d.ilist_kin[slot] = kv;
+        p.d.ilist_idx[slot] = ki;
+      }
+    }
+  }
+  st = __reduce_or_sync(FULL, st);
+  if ((threadIdx.x & 31) == 0 && st) atomicOr(&p.d.state->status, st);
+}
+
+// Eq. 2, reading R6/R7: t_ij = (r.r) / (-(r.w)), r = p_j - p_i, w = v_j - v_i,
+// only for approaching pairs (r.w < 0).  min_j over other participants.  The division is
+// skipped only when it provably cannot lower the running minimum (g2 > RU(best * den)
+// implies fl(g2/den) >= best), so the result is the exact min of the rounded quotients.
+__global__ void __launch_bounds__(NT) k_pairmin(Params p) {
+  __shared__ float4 tile[NT];
+  const uint32_t count = p.d.state->int_count;
+  const uint32_t i = blockIdx.x * NT + threadIdx.x;
+  if (blockIdx.x * NT >= count) return;
+  const bool mine = i < count;
+  const float4 ki = mine ? p.d.ilist_kin[i] : make_float4(0, 0, 0, 0);
+  float best = __int_as_float(0x7F800000);
+  for (uint32_t j0 = 0; j0 < count; j0 += NT) {
+    __syncthreads();
+    if (j0 + threadIdx.x < count) tile[threadIdx.x] = p.d.ilist_kin[j0 + threadIdx.x];
+    __syncthreads();
+    const uint32_t jn = min((uint32_t)NT, count - j0);
+    if (mine) {
+      for (uint32_t jj = 0; jj < jn; ++jj) {
+        const float4 kj = tile[jj];
+        const float dx = __fsub_rn(kj.x, ki.x);
+        const float dy = __fsub_rn(kj.y, ki.y);
+        const float dvx = __fsub_rn(kj.z, ki.z);
+        const float dvy = __fsub_rn(kj.w, ki.w);
+        const float rw = __fadd_rn(__fmul_rn(dx, dvx), __fmul_rn(dy, dvy));
+        if (rw < 0.0f && (j0 + jj) != i) {
+          const float g2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+          const float den = -rw;
+          if (!(g2 > __fmul_ru(best, den))) {
+            const float t = __fdiv_rn(g2, den);
+            if (t < best) best = t;
+          }
+        }
+      }
+    }
+  }
+  if (mine) p.d.dint[p.d.ilist_idx[i]] = best;
+}
+
+// ------------------------------------------------------------------------------------
+// a1 + a2: score, key, eligibility, byte-weighted level-1 histogram with per-bucket min/max
+
+__global__ void __launch_bounds__(NT) k_score(Params p, int64_t now) {
+  __shared__ unsigned long long sh_hist[2048];
+  __shared__ uint32_t sh_min[2048], sh_nmax[2048];
+  for (int b = threadIdx.x; b < 2048; b += NT) {
+    sh_hist[b] = 0;
+    sh_min[b] = 0xFFFFFFFFu;
+    sh_nmax[b] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint32_t st = 0;
+  unsigned long long zero_bytes = 0;
+  const uint32_t *bm_old = p.d.bm[p.cur];
+  for (uint64_t base = blockIdx.x * (uint64_t)NT; base < p.n_local; base += (uint64_t)gridDim.x * NT) {
+    const uint64_t i = base + threadIdx.x;
+    const bool valid = i < p.n_local;
+    uint4 r = make_uint4(0, 0, 0, 0);
+    uint32_t word = 0;
+    if (valid) {
+      r = ld_stream(p.rec + i);
+      word = bm_old[i >> 5];
+    }
+    const bool res = valid && ((word >> (i & 31)) & 1u);
+    const float d = valid ? distance_of(r, now, p.hop_scale, p.d.dint, p.n_kin, st) : 0.0f;
+    const uint32_t bits = __float_as_uint(d);
+    const bool elig = valid && (res || d == 0.0f || d < theta_of(p, class_of(r)));
+    if (valid) p.d.keys[i] = bits;
+    const uint32_t eb = __ballot_sync(FULL, elig);
+    if (lane == 0 && (i >> 5) < p.n_words) p.d.elig[i >> 5] = eb;
+    if (valid && d == 0.0f) zero_bytes += r.y;
+    // warp-aggregated histogram update: one smem atomic per distinct bucket in the warp
+    uint32_t pending = eb;
+    const uint32_t bucket = bits >> 20;
+    while (pending) {
+      const int leader = __ffs(pending) - 1;
+      const uint32_t lb = __shfl_sync(FULL, bucket, leader);
+      const uint32_t grp = __ballot_sync(FULL, elig && bucket == lb);
+      const bool in = (grp >> lane) & 1u;
+      const unsigned long long s = warp_sum_u32_exact(in ? r.y : 0u);
+      const uint32_t mn = __reduce_min_sync(FULL, in ? bits : 0xFFFFFFFFu);
+      const uint32_t nmx = __reduce_min_sync(FULL, in ? ~bits : 0xFFFFFFFFu);
+      if (lane == leader) {
+        atomicAdd(&sh_hist[lb], s);
+        atomicMin(&sh_min[lb], mn);
+        atomicMin(&sh_nmax[lb], nmx);
+      }
+      pending &= ~grp;
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 2048; b += NT) {
+    if (sh_hist[b] != 0 || sh_min[b] != 0xFFFFFFFFu) {
+      atomicAdd(&p.d.hist1[b], sh_hist[b]);
+      atomicMin(&p.d.mm1[b], sh_min[b]);
+      atomicMin(&p.d.mm1[2048 + b], sh_nmax[b]);
+    }
+  }
+  const unsigned long long zb = block_sum(zero_bytes);
+  if (threadIdx.x == 0 && zb) atomicAdd(&p.d.hist1[2048], zb);
+  st = __reduce_or_sync(FULL, st);
+  if (lane == 0 && st) atomicOr(&p.d.state->status, st);
+}
+
+__global__ void k_copy_keys(Params p, float *out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.n_local; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = __uint_as_float(p.d.keys[i]);
+}
+
+// ------------------------------------------------------------------------------------
+// a3: select.  One block of NT threads scans the 2^w buckets of the current level and finds
+// the first bucket b with below + cum(<=b) > B (the boundary of the budget).
+
+__global__ void __launch_bounds__(NT) k_select(Params p, int level) {
+  SelState *S = p.d.state;
+  if (S->done) return;
+  const int w = level == 1 ? L1_BITS : (level == 2 ? L2_BITS : L3_BITS);
+  const int shift = level == 1 ? 20 : (level == 2 ? 10 : 0);
+  const uint32_t nb = 1u << w;
+  const unsigned long long *h = level == 1 ? p.d.hist1 : (level == 2 ? p.d.hist2 : p.d.hist3);
+  const uint32_t *mm = level == 1 ? p.d.mm1 : (level == 2 ? p.d.mm2 : nullptr);
+  const unsigned long long below = S->below;
+  __shared__ unsigned long long sh_total, sh_prev;
+  __shared__ uint32_t sh_first;
+  if (threadIdx.x == 0) sh_first = 0xFFFFFFFFu;
+  __syncthreads();
+  // each thread owns nb/NT consecutive buckets
+  const uint32_t per = nb / NT;
+  unsigned long long loc = 0;
+  for (uint32_t k = 0; k < per; ++k) loc += h[threadIdx.x * per + k];
+  unsigned long long tot;
+  const unsigned long long ex = block_excl_scan(loc, &sh_total);
+  tot = sh_total;
+  unsigned long long run = below + ex;
+  for (uint32_t k = 0; k < per; ++k) {
+    const uint32_t b = threadIdx.x * per + k;
+    const unsigned long long prev = run;
+    run += h[b];
+    if (run > p.budget && prev <= p.budget) {  // exactly one bucket crosses (sums are monotone)
+      sh_first = b;
+      sh_prev = prev;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (level == 1) {
+      S->total = tot;
+      if (p.d.hist1[2048] > p.budget) S->status |= ST_INSUFFICIENT;
+      S->zero_bytes = p.d.hist1[2048];
+    }
+    const uint32_t b = sh_first;
+    if (b == 0xFFFFFFFFu) {
+      // level 1 only: everything eligible fits
+      S->all_fit = 1;
+      S->done = 1;
+      S->dstar = 0xFFFFFFFFu;
+      S->rem = p.budget - (below + tot);
+      S->level = 4;
+    } else {
+      const unsigned long long cum_before = sh_prev;
+      S->below = cum_before;
+      S->prefix |= b << shift;
+      const bool single = mm != nullptr && mm[b] == ~mm[nb + b];
+      if (level == 3 || single) {
+        S->dstar = (level == 3) ? S->prefix : mm[b];
+        S->rem = p.budget - cum_before;
+        S->done = 1;
+        S->level = 4;
+      } else {
+        S->level = level + 1;
+      }
+    }
+  }
+}
+
+// Histogram of the next digit over the keys inside the boundary bucket (levels 2 and 3).
+__global__ void __launch_bounds__(NT) k_hist(Params p, int level) {
+  const SelState *S = p.d.state;
+  if (S->done || S->level != (unsigned)level) return;
+  __shared__ unsigned long long sh_hist[1024];
+  __shared__ uint32_t sh_min[1024], sh_nmax[1024];
+  for (int b = threadIdx.x; b < 1024; b += NT) {
+    sh_hist[b] = 0;
+    sh_min[b] = 0xFFFFFFFFu;
+    sh_nmax[b] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  const int hi_shift = level == 2 ? 20 : 10;
+  const int shift = level == 2 ? 10 : 0;
+  const uint32_t want = S->prefix >> hi_shift;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)NT; base < p.n_local; base += (uint64_t)gridDim.x * NT) {
+    const uint64_t i = base + threadIdx.x;
+    bool in_b = false;
+    uint32_t bits = 0, fp = 0;
+    if (i < p.n_local) {
+      const bool el = (p.d.elig[i >> 5] >> (i & 31)) & 1u;
+      bits = p.d.keys[i];
+      in_b = el && (bits >> hi_shift) == want;
+      if (in_b) fp = p.rec[i].y;
+    }
+    uint32_t pending = __ballot_sync(FULL, in_b);
+    const uint32_t bucket = (bits >> shift) & 1023u;
+    while (pending) {
+      const int leader = __ffs(pending) - 1;
+      const uint32_t lb = __shfl_sync(FULL, bucket, leader);
+      const uint32_t grp = __ballot_sync(FULL, in_b && bucket == lb);
+      const bool in = (grp >> lane) & 1u;
+      const unsigned long long s = warp_sum_u32_exact(in ? fp : 0u);
+      const uint32_t mn = __reduce_min_sync(FULL, in ? bits : 0xFFFFFFFFu);
+      const uint32_t nmx = __reduce_min_sync(FULL, in ? ~bits : 0xFFFFFFFFu);
+      if (lane == leader) {
+        atomicAdd(&sh_hist[lb], s);
+        atomicMin(&sh_min[lb], mn);
+        atomicMin(&sh_nmax[lb], nmx);
+      }
+      pending &= ~grp;
+    }
+  }
+  __syncthreads();
+  unsigned long long *gh = level == 2 ? p.d.hist2 : p.d.hist3;
+  for (int b = threadIdx.x; b < 1024; b += NT) {
+    if (sh_hist[b] != 0 || sh_min[b] != 0xFFFFFFFFu) {
+      atomicAdd(&gh[b], sh_hist[b]);
+      if (level == 2) {
+        atomicMin(&p.d.mm2[b], sh_min[b]);
+        atomicMin(&p.d.mm2[1024 + b], sh_nmax[b]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// a4: tie group (d == D*) bytes per tile, in id order, then the exclusive scan over tiles
+
+__global__ void __launch_bounds__(NT) k_tie_partial(Params p) {
+  const SelState *S = p.d.state;
+  const uint64_t t0 = (uint64_t)blockIdx.x * TILE;
+  unsigned long long s = 0;
+  if (!S->all_fit) {
+    const uint32_t dstar = S->dstar;
+    for (uint32_t k = threadIdx.x; k < TILE; k += NT) {
+      const uint64_t i = t0 + k;
+      if (i < p.n_local && ((p.d.elig[i >> 5] >> (i & 31)) & 1u) && p.d.keys[i] == dstar) s += p.rec[i].y;
+    }
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) p.d.tile_tie[blockIdx.x] = s;
+}
+
+// single block: exclusive scan of u64/u32 arrays of length n (NT threads, chunked)
+template <typename T>
+__device__ void block_scan_array(const T *in, T *out, uint64_t n, T *total_out) {
+  __shared__ T sh_tot;
+  T carry = 0;
+  for (uint64_t base = 0; base < n; base += NT) {
+    const uint64_t i = base + threadIdx.x;
+    const T v = i < n ? in[i] : T(0);
+    const T ex = block_excl_scan(v, &sh_tot);
+    __syncthreads();
+    const T tot = sh_tot;
+    if (i < n) out[i] = carry + ex;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = carry;
+}
+
+__global__ void __launch_bounds__(NT) k_tie_scan(Params p) {
+  __shared__ unsigned long long tot;
+  block_scan_array<unsigned long long>(p.d.tile_tie, p.d.tile_tie_excl, p.n_tiles, &tot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    p.d.state->tie_local = tot;
+    if (p.world == 1) p.d.gather[0] = tot;
+  }
+}
+
+// a4 + a5: kept decision, new residency bitmap, per-tile change counts.
+__global__ void __launch_bounds__(NT) k_emit(Params p) {
+  const SelState *S = p.d.state;
+  const uint64_t t0 = (uint64_t)blockIdx.x * TILE;
+  const bool all_fit = S->all_fit;
+  const uint32_t dstar = S->dstar;
+  const unsigned long long rem = S->rem;
+  unsigned long long rank_excl = 0;
+  for (int r = 0; r < p.rank; ++r) rank_excl += p.d.gather[r];
+  unsigned long long carry = p.d.tile_tie_excl[blockIdx.x] + rank_excl;
+  const uint32_t *bm_old = p.d.bm[p.cur];
+  uint32_t *bm_new = p.d.bm[p.cur ^ 1];
+  uint32_t n_pf = 0, n_ev = 0, n_el = 0;
+  unsigned long long h2d = 0, tie_kept = 0;
+  __shared__ unsigned long long sh_tot;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k0 = 0; k0 < TILE; k0 += NT) {
+    const uint64_t i = t0 + k0 + threadIdx.x;
+    const bool valid = i < p.n_local;
+    bool el = false, tie = false;
+    uint32_t key = KEY_NONE, fp = 0;
+    if (valid) {
+      el = (p.d.elig[i >> 5] >> (i & 31)) & 1u;
+      key = p.d.keys[i];
+      tie = el && !all_fit && key == dstar;
+      if (tie) fp = p.rec[i].y;
+    }
+    const unsigned long long ex = block_excl_scan((unsigned long long)fp, &sh_tot);
+    __syncthreads();
+    const unsigned long long incl = carry + ex + fp;
+    carry += sh_tot;
+    const bool kept = el && (all_fit || key < dstar || (tie && incl <= rem));
+    if (tie && kept) tie_kept += fp;
+    const uint32_t kw = __ballot_sync(FULL, kept);
+    const uint32_t ew = __ballot_sync(FULL, el);
+    const uint64_t wi = i >> 5;
+    uint32_t old = 0;
+    if (wi < p.n_words) old = bm_old[wi];
+    if (lane == 0 && wi < p.n_words && (t0 + k0 + (threadIdx.x & ~31u)) < p.n_local) {
+      bm_new[wi] = kw;
+      n_pf += __popc(kw & ~old);
+      n_ev += __popc(old & ~kw);
+      n_el += __popc(ew);
+    }
+    const bool pf = kept && !((old >> lane) & 1u);
+    if (pf) h2d += p.rec[i].y;
+    __syncthreads();
+  }
+  n_pf = block_sum(n_pf);
+  n_ev = block_sum(n_ev);
+  n_el = block_sum(n_el);
+  h2d = block_sum(h2d);
+  tie_kept = block_sum(tie_kept);
+  if (threadIdx.x == 0) {
+    p.d.tile_pf[blockIdx.x] = n_pf;
+    p.d.tile_ev[blockIdx.x] = n_ev;
+    p.d.tile_elig[blockIdx.x] = n_el;
+    p.d.tile_h2d[blockIdx.x] = h2d;
+    p.d.tile_tiekept[blockIdx.x] = tie_kept;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_count_scan(Params p) {
+  __shared__ uint32_t tot_pf, tot_ev, tot_el;
+  __shared__ unsigned long long tot_h2d, tot_tk;
+  block_scan_array<uint32_t>(p.d.tile_pf, p.d.tile_pf_excl, p.n_tiles, &tot_pf);
+  __syncthreads();
+  block_scan_array<uint32_t>(p.d.tile_ev, p.d.tile_ev_excl, p.n_tiles, &tot_ev);
+  __syncthreads();
+  unsigned long long a = 0, b = 0;
+  uint32_t c = 0;
+  for (uint64_t t = threadIdx.x; t < p.n_tiles; t += NT) {
+    a += p.d.tile_h2d[t];
+    b += p.d.tile_tiekept[t];
+    c += p.d.tile_elig[t];
+  }
+  a = block_sum(a);
+  b = block_sum(b);
+  c = block_sum(c);
+  if (threadIdx.x == 0) {
+    tot_h2d = a;
+    tot_tk = b;
+    tot_el = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    SelState *S = p.d.state;
+    S->tie_kept = tot_tk;
+    unsigned long long *H = p.d.header;
+    H[H_N_PF] = tot_pf;
+    H[H_N_EV] = tot_ev;
+    H[H_H2D] = tot_h2d;
+    H[H_CUT_BITS] = S->all_fit ? 0xFFFFFFFFull : S->dstar;
+    H[H_CUT_REM] = S->rem;
+    H[H_KEPT] = S->all_fit ? (p.budget - S->rem) : (p.budget - S->rem) + tot_tk;
+    H[H_N_ELIG] = tot_el;
+    H[H_STATUS] = S->status;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// a5: list compaction in id order (prefetch ascending id, evict descending id), then a
+// stable LSD radix sort by distance bits (prefetch: ascending d; evict: descending d via
+// the complemented key) -> ascending / descending (d, id) order.
+
+__global__ void __launch_bounds__(64) k_compact(Params p) {
+  const uint64_t w0 = (uint64_t)blockIdx.x * (TILE / 32);
+  const uint64_t wi = w0 + threadIdx.x;
+  const uint32_t *bm_old = p.d.bm[p.cur];
+  const uint32_t *bm_new = p.d.bm[p.cur ^ 1];
+  uint32_t pfw = 0, evw = 0;
+  if (wi < p.n_words) {
+    const uint32_t o = bm_old[wi], n = bm_new[wi];
+    pfw = n & ~o;
+    evw = o & ~n;
+  }
+  __shared__ uint32_t sh_pf[64], sh_ev[64];
+  sh_pf[threadIdx.x] = __popc(pfw);
+  sh_ev[threadIdx.x] = __popc(evw);
+  __syncthreads();
+  uint32_t epf = 0, eev = 0;
+  for (uint32_t k = 0; k < threadIdx.x; ++k) {
+    epf += sh_pf[k];
+    eev += sh_ev[k];
+  }
+  uint32_t pos = p.d.tile_pf_excl[blockIdx.x] + epf;
+  const uint32_t n_ev_tot = (uint32_t)p.d.header[H_N_EV];
+  uint32_t epos = p.d.tile_ev_excl[blockIdx.x] + eev;
+  SelState *S = p.d.state;
+  uint32_t or_pf = 0, and_pf = 0xFFFFFFFFu, or_ev = 0, and_ev = 0xFFFFFFFFu;
+  while (pfw) {
+    const int b = __ffs(pfw) - 1;
+    pfw &= pfw - 1;
+    const uint32_t i = (uint32_t)(wi * 32 + b);
+    const uint32_t key = p.d.keys[i];
+    p.d.sort_ka[pos] = key;
+    p.d.sort_va[pos] = i;
+    or_pf |= key;
+    and_pf &= key;
+    ++pos;
+  }
+  while (evw) {
+    const int b = __ffs(evw) - 1;
+    evw &= evw - 1;
+    const uint32_t i = (uint32_t)(wi * 32 + b);
+    const uint32_t key = ~p.d.keys[i];
+    const uint32_t slot = n_ev_tot - 1 - epos;
+    p.d.pfa_key[slot] = key;  // evict list staging (second buffer set)
+    p.d.pfa_val[slot] = i;
+    or_ev |= key;
+    and_ev &= key;
+    ++epos;
+  }
+  or_pf = __reduce_or_sync(FULL, or_pf);
+  and_pf = __reduce_and_sync(FULL, and_pf);
+  or_ev = __reduce_or_sync(FULL, or_ev);
+  and_ev = __reduce_and_sync(FULL, and_ev);
+  if ((threadIdx.x & 31) == 0) {
+    if (or_pf) atomicOr(&S->sort_or[0], or_pf);
+    if (and_pf != 0xFFFFFFFFu) atomicAnd(&S->sort_and[0], and_pf);
+    if (or_ev) atomicOr(&S->sort_or[1], or_ev);
+    if (and_ev != 0xFFFFFFFFu) atomicAnd(&S->sort_and[1], and_ev);
+  }
+}
+
+// digit d of pass q: bits [0,11), [11,22), [22,32)
+__device__ __forceinline__ uint32_t digit_of(uint32_t key, int pass) {
+  return pass == 0 ? (key & 2047u) : pass == 1 ? ((key >> 11) & 2047u) : (key >> 22);
+}
+__device__ __forceinline__ uint32_t digit_mask(int pass) {
+  return pass == 0 ? 0x7FFu : pass == 1 ? (0x7FFu << 11) : (0x3FFu << 22);
+}
+__device__ __forceinline__ bool pass_needed(const SelState *S, int list, int pass) {
+  const uint32_t varying = S->sort_or[list] ^ S->sort_and[list];
+  return (varying & digit_mask(pass)) != 0;
+}
+
+struct SortIO {
+  const uint32_t *kin, *vin;
+  uint32_t *kout, *vout;
+};
+
+__global__ void __launch_bounds__(NT) k_sort_hist(Params p, int list, int pass, SortIO io) {
+  const uint32_t count = (uint32_t)p.d.header[list == 0 ? H_N_PF : H_N_EV];
+  const uint32_t n_chunks = (count + SORT_CH - 1) / SORT_CH;
+  if (blockIdx.x >= n_chunks || !pass_needed(p.d.state, list, pass)) return;
+  __shared__ uint32_t h[2048];
+  for (int b = threadIdx.x; b < 2048; b += NT) h[b] = 0;
+  __syncthreads();
+  const uint32_t c0 = blockIdx.x * SORT_CH;
+  for (uint32_t k = threadIdx.x; k < SORT_CH; k += NT) {
+    const uint32_t e = c0 + k;
+    if (e < count) atomicAdd(&h[digit_of(io.kin[e], pass)], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 2048; b += NT) p.d.sort_cnt[(uint64_t)b * n_chunks + blockIdx.x] = h[b];
+}
+
+__global__ void __launch_bounds__(NT) k_sort_scan(Params p, int list, int pass) {
+  const uint32_t count = (uint32_t)p.d.header[list == 0 ? H_N_PF : H_N_EV];
+  const uint32_t n_chunks = (count + SORT_CH - 1) / SORT_CH;
+  if (n_chunks == 0 || !pass_needed(p.d.state, list, pass)) return;
+  block_scan_array<uint32_t>(p.d.sort_cnt, p.d.sort_cnt, (uint64_t)2048 * n_chunks, nullptr);
+}
+
+__global__ void __launch_bounds__(NT) k_sort_scatter(Params p, int list, int pass, SortIO io) {
+  const uint32_t count = (uint32_t)p.d.header[list == 0 ? H_N_PF : H_N_EV];
+  const uint32_t n_chunks = (count + SORT_CH - 1) / SORT_CH;
+  if (blockIdx.x >= n_chunks) return;
+  const uint32_t c0 = blockIdx.x * SORT_CH;
+  if (!pass_needed(p.d.state, list, pass)) {  // identity copy keeps the buffer schedule static
+    for (uint32_t k = threadIdx.x; k < SORT_CH; k += NT) {
+      const uint32_t e = c0 + k;
+      if (e < count) {
+        io.kout[e] = io.kin[e];
+        io.vout[e] = io.vin[e];
+      }
+    }
+    return;
+  }
+  __shared__ uint32_t run[2048];
+  for (int b = threadIdx.x; b < 2048; b += NT) run[b] = p.d.sort_cnt[(uint64_t)b * n_chunks + blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t k0 = 0; k0 < SORT_CH; k0 += NT) {
+    const uint32_t e = c0 + k0 + threadIdx.x;
+    const bool valid = e < count;
+    const uint32_t key = valid ? io.kin[e] : 0u;
+    const uint32_t val = valid ? io.vin[e] : 0u;
+    const uint32_t dg = valid ? digit_of(key, pass) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(FULL, dg);
+    const uint32_t rank = __popc(peers & lanemask_lt());
+    const bool leader = (peers & lanemask_lt()) == 0;
+    for (int w = 0; w < NT / 32; ++w) {
+      if (warp == w && valid) {
+        const uint32_t pos = run[dg] + rank;
+        io.kout[pos] = key;
+        io.vout[pos] = val;
+      }
+      __syncwarp();
+      if (warp == w && valid && leader) run[dg] += __popc(peers);
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void k_sort_finish(Params p, int list, const uint32_t *vals) {
+  const uint32_t count = (uint32_t)p.d.header[list == 0 ? H_N_PF : H_N_EV];
+  uint32_t *out = list == 0 ? p.d.pf_ids : p.d.ev_ids;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x)
+    out[e] = (uint32_t)(vals[e] + p.shard_begin);
+}
+
+// ------------------------------------------------------------------------------------
+// a5: block expansion and deterministic page assignment.
+// Chunk c of a list covers entries [c*EXP_CH, (c+1)*EXP_CH).  exp_sum layout:
+//   [0][chunk] evict pages, [1][chunk] evict write-back pages, [2][chunk] prefetch pages
+
+__device__ __forceinline__ void agent_pages(const Params &p, uint32_t a, bool dirty, uint32_t &pages,
+                                            uint32_t &wb_pages) {
+  const uint64_t b0 = p.blk_ptr[a], b1 = p.blk_ptr[a + 1];
+  pages = (uint32_t)(p.d.page_first[b1] - p.d.page_first[b0]);
+  wb_pages = 0;
+  if (dirty)
+    for (uint64_t b = b0; b < b1; ++b)
+      if (p.blk_kind[b] != 0) wb_pages += (uint32_t)(p.d.page_first[b + 1] - p.d.page_first[b]);
+}
+
+__global__ void __launch_bounds__(NT) k_exp_count(Params p, uint64_t max_chunks) {
+  const uint32_t n_pf = (uint32_t)p.d.header[H_N_PF], n_ev = (uint32_t)p.d.header[H_N_EV];
+  const uint32_t e = blockIdx.x * EXP_CH + threadIdx.x;
+  uint32_t evp = 0, evw = 0, pfp = 0;
+  unsigned long long wb_bytes = 0;
+  if (e < n_ev) {
+    const uint32_t a = p.d.ev_ids[e] - (uint32_t)p.shard_begin;
+    const bool dirty = (p.rec[a].z >> 4) & 1u;
+    agent_pages(p, a, dirty, evp, evw);
+    if (dirty)  // R13: KV + HIST blocks of a dirty evicted agent are written back
+      for (uint64_t b = p.blk_ptr[a]; b < p.blk_ptr[a + 1]; ++b)
+        if (p.blk_kind[b] != 0) wb_bytes += p.blk_size[b];
+  }
+  if (e < n_pf) {
+    const uint32_t a = p.d.pf_ids[e] - (uint32_t)p.shard_begin;
+    uint32_t dummy;
+    agent_pages(p, a, false, pfp, dummy);
+  }
+  const unsigned long long s0 = block_sum((unsigned long long)evp);
+  const unsigned long long s1 = block_sum((unsigned long long)evw);
+  const unsigned long long s2 = block_sum((unsigned long long)pfp);
+  const unsigned long long s3 = block_sum(wb_bytes);
+  if (threadIdx.x == 0) {
+    p.d.exp_sum[blockIdx.x] = s0;
+    p.d.exp_sum[max_chunks + blockIdx.x] = s1;
+    p.d.exp_sum[2 * max_chunks + blockIdx.x] = s2;
+    p.d.exp_sum[3 * max_chunks + blockIdx.x] = s3;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_exp_scan(Params p, uint64_t max_chunks) {
+  const uint32_t n_pf = (uint32_t)p.d.header[H_N_PF], n_ev = (uint32_t)p.d.header[H_N_EV];
+  const uint64_t nc = (max(n_pf, n_ev) + EXP_CH - 1) / EXP_CH;
+  __shared__ unsigned long long t0, t1, t2, t3;
+  block_scan_array<unsigned long long>(p.d.exp_sum, p.d.exp_excl, nc, &t0);
+  __syncthreads();
+  block_scan_array<unsigned long long>(p.d.exp_sum + max_chunks, p.d.exp_excl + max_chunks, nc, &t1);
+  __syncthreads();
+  block_scan_array<unsigned long long>(p.d.exp_sum + 2 * max_chunks, p.d.exp_excl + 2 * max_chunks, nc, &t2);
+  __syncthreads();
+  block_scan_array<unsigned long long>(p.d.exp_sum + 3 * max_chunks, p.d.exp_excl + 3 * max_chunks, nc, &t3);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long *H = p.d.header;
+    H[H_D2H] = t3;
+    if (p.n_dev_pages == 0) return;  // logical sizes (NO_TRANSFER): byte accounting only
+    unsigned long long *desc = p.d.desc[p.desc_buf];
+    const unsigned long long head = p.d.pool[0], tail = p.d.pool[1];
+    H[H_N_D2H] = t1;
+    H[H_N_H2D] = t2;
+    desc[0] = t1;
+    desc[1] = t2;
+    // free pages after releasing = tail + t0 - head; the prefetch must fit (always true when
+    // dev pages >= budget pages; flagged otherwise)
+    if (t2 > tail + t0 - head) {
+      p.d.state->status |= ST_NO_PAGES;
+      H[H_STATUS] |= ST_NO_PAGES;
+    }
+    H[H_POOL_HEAD] = head + t2;
+    H[H_POOL_TAIL] = tail + t0;
+  }
+}
+
+// release (evict) or assign (prefetch) the pages of one list chunk
+template <bool RELEASE>
+__global__ void __launch_bounds__(NT) k_pages(Params p, uint64_t max_chunks) {
+  const uint32_t count = (uint32_t)p.d.header[RELEASE ? H_N_EV : H_N_PF];
+  const uint32_t c0 = blockIdx.x * EXP_CH;
+  if (c0 >= count || (p.d.header[H_STATUS] & ST_NO_PAGES)) return;
+  __shared__ unsigned long long sh_off[EXP_CH], sh_wb[EXP_CH];
+  __shared__ unsigned long long sh_t;
+  const uint32_t e = c0 + threadIdx.x;
+  uint32_t a = 0, pages = 0, wb = 0;
+  bool dirty = false;
+  if (e < count) {
+    a = (RELEASE ? p.d.ev_ids[e] : p.d.pf_ids[e]) - (uint32_t)p.shard_begin;
+    dirty = RELEASE && ((p.rec[a].z >> 4) & 1u);
+    agent_pages(p, a, dirty, pages, wb);
+  }
+  const unsigned long long ex = block_excl_scan((unsigned long long)pages, &sh_t);
+  __syncthreads();
+  const unsigned long long exw = block_excl_scan((unsigned long long)wb, &sh_t);
+  __syncthreads();
+  const unsigned long long chunk_off = p.d.exp_excl[(RELEASE ? 0 : 2 * max_chunks) + blockIdx.x];
+  sh_off[threadIdx.x] = chunk_off + ex;
+  sh_wb[threadIdx.x] = (RELEASE ? p.d.exp_excl[max_chunks + blockIdx.x] : 0ull) + exw;
+  __syncthreads();
+  const unsigned long long head = p.d.pool[0], tail = p.d.pool[1];
+  const unsigned long long npg = p.n_dev_pages;
+  unsigned long long *desc = p.d.desc[p.desc_buf] + 2;  // pairs after the two counters
+  unsigned long long *d2h = desc;
+  unsigned long long *h2d = desc + 2 * p.desc_cap;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t n_here = min(count - c0, EXP_CH);
+  for (uint32_t k = warp; k < n_here; k += NT / 32) {
+    const uint32_t ag = (RELEASE ? p.d.ev_ids[c0 + k] : p.d.pf_ids[c0 + k]) - (uint32_t)p.shard_begin;
+    const bool dty = RELEASE && ((p.rec[ag].z >> 4) & 1u);
+    unsigned long long off = sh_off[k];
+    unsigned long long woff = sh_wb[k];
+    for (uint64_t b = p.blk_ptr[ag]; b < p.blk_ptr[ag + 1]; ++b) {
+      const unsigned long long pf0 = p.d.page_first[b];
+      const uint32_t np = (uint32_t)(p.d.page_first[b + 1] - pf0);
+      const bool wbk = dty && p.blk_kind[b] != 0;
+      const unsigned long long hoff = p.blk_host_off[b];
+      for (uint32_t q = lane; q < np; q += 32) {
+        if (RELEASE) {
+          const uint32_t pg = p.d.page_table[pf0 + q];
+          p.d.ring[(tail + off + q) % npg] = pg;
+          p.d.page_table[pf0 + q] = PAGE_NONE;
+          if (wbk) {
+            d2h[2 * (woff + q)] = hoff + (unsigned long long)q * p.page_bytes;
+            d2h[2 * (woff + q) + 1] = pg;
+          }
+        } else {
+          const uint32_t pg = p.d.ring[(head + off + q) % npg];
+          p.d.page_table[pf0 + q] = pg;
+          h2d[2 * (off + q)] = hoff + (unsigned long long)q * p.page_bytes;
+          h2d[2 * (off + q) + 1] = pg;
+        }
+      }
+      off += np;
+      if (wbk) woff += np;
+    }
+  }
+}
+
+__global__ void k_pool_update(Params p) {
+  p.d.pool[0] = p.d.header[H_POOL_HEAD];
+  p.d.pool[1] = p.d.header[H_POOL_TAIL];
+}
+
+// init: pages for the initially resident agents in id order (block order, page order)
+__global__ void k_init_pages_count(Params p, const uint32_t *res, uint64_t *cnt) {
+  // serial over agents in a single thread: init-time only
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned long long head = 0;
+  for (uint64_t a = 0; a < p.n_local; ++a) {
+    if (!((res[a >> 5] >> (a & 31)) & 1u)) continue;
+    for (uint64_t b = p.blk_ptr[a]; b < p.blk_ptr[a + 1]; ++b)
+      for (unsigned long long q = p.d.page_first[b]; q < p.d.page_first[b + 1]; ++q) {
+        p.d.page_table[q] = p.d.ring[head % p.n_dev_pages];
+        ++head;
+      }
+  }
+  p.d.pool[0] = head;
+  p.d.pool[1] = p.n_dev_pages;
+  *cnt = head;
+}
+
+__global__ void k_init_ring(Params p, const uint32_t *res) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < p.n_dev_pages; q += (uint64_t)gridDim.x * blockDim.x)
+    p.d.ring[q] = (uint32_t)q;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < p.n_words; w += (uint64_t)gridDim.x * blockDim.x) {
+    p.d.bm[0][w] = res ? res[w] : 0u;
+    p.d.bm[1][w] = 0u;
+  }
+}
+
+__global__ void k_init_page_table(Params p, uint64_t n_block_pages) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n_block_pages; q += (uint64_t)gridDim.x * blockDim.x)
+    p.d.page_table[q] = PAGE_NONE;
+}
+
+// ------------------------------------------------------------------------------------
+// a6: page copies.  One CTA per 64 KiB page per iteration: every thread issues all its
+// 128-bit loads (16 per thread for 64 KiB) before its stores, so a CTA keeps a whole page
+// in flight across PCIe; the grid is small (the copy overlaps the next plan).
+
+template <bool D2H>
+__global__ void __launch_bounds__(NT) k_copy_pages(const unsigned long long *desc_base, uint8_t *host, uint8_t *dev,
+                                                  uint64_t page_bytes, uint64_t desc_cap) {
+  const unsigned long long n = desc_base[D2H ? 0 : 1];
+  const unsigned long long *desc = desc_base + 2 + (D2H ? 0 : 2 * desc_cap);
+  const uint32_t vec_per_page = (uint32_t)(page_bytes / 16);
+  for (unsigned long long k = blockIdx.x; k < n; k += gridDim.x) {
+    const unsigned long long hoff = desc[2 * k];
+    const unsigned long long pg = desc[2 * k + 1];
+    const uint4 *src = reinterpret_cast<const uint4 *>(D2H ? dev + pg * page_bytes : host + hoff);
+    uint4 *dst = reinterpret_cast<uint4 *>(D2H ? host + hoff : dev + pg * page_bytes);
+    for (uint32_t v0 = 0; v0 < vec_per_page; v0 += NT * 16) {
+      uint4 buf[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const uint32_t v = v0 + u * NT + threadIdx.x;
+        if (v < vec_per_page) buf[u] = ld_stream(src + v);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const uint32_t v = v0 + u * NT + threadIdx.x;
+        if (v < vec_per_page) dst[v] = buf[u];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// launchers
+
+static inline int ceil_div(uint64_t a, uint64_t b) { return (int)((a + b - 1) / b); }
+static inline int tiles_grid(const Params &p) { return p.n_tiles > 0 ? (int)p.n_tiles : 1; }
+
+int launch_plan_init(const Params &p, cudaStream_t s) {
+  k_plan_init<<<8, NT, 0, s>>>(p);
+  return 1;
+}
+
+int launch_score(const Params &p, int64_t now, float *dist_out, cudaStream_t s, int grid) {
+  int n = 0;
+  if (p.n_kin > 0) {
+    const int g = min(grid, max(1, ceil_div(max(p.n_local, p.n_kin), NT)));
+    k_int_compact<<<g, NT, 0, s>>>(p);
+    k_pairmin<<<max(1, ceil_div(p.n_kin, NT)), NT, 0, s>>>(p);
+    n += 2;
+  }
+  const int g = min(grid, max(1, ceil_div(p.n_local, NT)));
+  k_score<<<g, NT, 0, s>>>(p, now);
+  ++n;
+  if (dist_out) {
+    k_copy_keys<<<min(grid, max(1, ceil_div(p.n_local, NT))), NT, 0, s>>>(p, dist_out);
+    ++n;
+  }
+  return n;
+}
+
+int launch_select(const Params &p, int level, cudaStream_t s) {
+  k_select<<<1, NT, 0, s>>>(p, level);
+  return 1;
+}
+
+int launch_hist(const Params &p, int level, cudaStream_t s, int grid) {
+  k_hist<<<min(grid, max(1, ceil_div(p.n_local, NT))), NT, 0, s>>>(p, level);
+  return 1;
+}
+
+int launch_tie(const Params &p, cudaStream_t s) {
+  k_tie_partial<<<tiles_grid(p), NT, 0, s>>>(p);
+  k_tie_scan<<<1, NT, 0, s>>>(p);
+  return 2;
+}
+
+int launch_emit(const Params &p, cudaStream_t s) {
+  k_emit<<<tiles_grid(p), NT, 0, s>>>(p);
+  k_count_scan<<<1, NT, 0, s>>>(p);
+  return 2;
+}
+
+int launch_lists(const Params &p, cudaStream_t s) {
+  int n = 0;
+  k_compact<<<tiles_grid(p), 64, 0, s>>>(p);
+  ++n;
+  const int max_chunks = max(1, ceil_div(p.n_local, SORT_CH));
+  for (int list = 0; list < 2; ++list) {
+    uint32_t *ka = list == 0 ? p.d.sort_ka : p.d.pfa_key;
+    uint32_t *va = list == 0 ? p.d.sort_va : p.d.pfa_val;
+    uint32_t *kb = p.d.sort_kb, *vb = p.d.sort_vb;
+    // A -> B -> A -> B
+    for (int pass = 0; pass < 3; ++pass) {
+      SortIO io;
+      if (pass == 1) io = SortIO{kb, vb, ka, va};
+      else io = SortIO{ka, va, kb, vb};
+      k_sort_hist<<<max_chunks, NT, 0, s>>>(p, list, pass, io);
+      k_sort_scan<<<1, NT, 0, s>>>(p, list, pass);
+      k_sort_scatter<<<max_chunks, NT, 0, s>>>(p, list, pass, io);
+      n += 3;
+    }
+    k_sort_finish<<<min(1184, max_chunks * 8), NT, 0, s>>>(p, list, vb);
+    ++n;
+  }
+  return n;
+}
+
+int launch_expand(const Params &p, cudaStream_t s) {
+  const uint64_t max_chunks = (uint64_t)max(1, ceil_div(p.n_local, EXP_CH));
+  k_exp_count<<<(int)max_chunks, NT, 0, s>>>(p, max_chunks);
+  k_exp_scan<<<1, NT, 0, s>>>(p, max_chunks);
+  if (p.n_dev_pages == 0) return 2;
+  k_pages<true><<<(int)max_chunks, NT, 0, s>>>(p, max_chunks);
+  k_pages<false><<<(int)max_chunks, NT, 0, s>>>(p, max_chunks);
+  k_pool_update<<<1, 1, 0, s>>>(p);
+  return 5;
+}
+
+int launch_transfer(const Params &p, cudaStream_t s, int ctas) {
+  const unsigned long long *desc = p.d.desc[p.desc_buf];
+  k_copy_pages<true><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  k_copy_pages<false><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  return 2;
+}
+
+int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s) {
+  k_init_ring<<<256, NT, 0, s>>>(p, resident_init);
+  if (p.n_dev_pages == 0) return 1;
+  return 1;
+}
+
+int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s) {
+  k_copy_keys<<<256, NT, 0, s>>>(p, dist_out);
+  return 1;
+}
+
+__global__ void k_fix_kept(Params p) {
+  const SelState *S = p.d.state;
+  p.d.header[H_KEPT] = S->all_fit ? (p.budget - S->rem) : (p.budget - S->rem) + S->tie_kept;
+}
+
+__global__ void k_mask_tail(Params p) {
+  if (p.n_local % 32 != 0 && p.n_words > 0) p.d.bm[0][p.n_words - 1] &= (1u << (p.n_local % 32)) - 1u;
+}
+
+int launch_fix_kept(const Params &p, cudaStream_t s) {
+  k_fix_kept<<<1, 1, 0, s>>>(p);
+  return 1;
+}
+
+int launch_mask_tail(const Params &p, cudaStream_t s) {
+  k_mask_tail<<<1, 1, 0, s>>>(p);
+  return 1;
+}
+
+// exported for api.cpp (init-time page table)
+void launch_init_page_table(const Params &p, uint64_t n_block_pages, const uint32_t *res, uint64_t *cnt_dev,
+                            cudaStream_t s) {
+  k_init_page_table<<<256, NT, 0, s>>>(p, n_block_pages);
+  if (res) k_init_pages_count<<<1, 1, 0, s>>>(p, res, cnt_dev);
+}
+
+void launch_init_transfer(const Params &p, cudaStream_t s, int ctas) { launch_transfer(p, s, ctas); }
+
+}  // namespace ss

@@ -1,0 +1,231 @@
+"""Thin Python binding of the C ABI.  PyTorch provides device / pinned memory and streams
+only; every step of the planner runs in libscalesim.so's kernels.  Names follow
+include/scalesim.h (score / plan / transfer / step / sync)."""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _dev_bytes(arr: np.ndarray, device) -> torch.Tensor:
+    a = np.ascontiguousarray(arr)
+    t = torch.from_numpy(a.view(np.uint8).reshape(-1)) if a.nbytes else torch.zeros(16, dtype=torch.uint8)
+    return t.to(device)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class Planner:
+    """One planner context (one rank's shard).
+
+    blk_ptr/blk_size/blk_host_off/blk_kind: numpy CSR block table of the local agents.
+    host_arena: pinned uint8 torch tensor (or None: allocated, size host_bytes).
+    dev_bytes: HBM arena size (default: ceil(budget / page) pages).
+    """
+
+    def __init__(self, n_agents: int, blk_ptr, blk_size, blk_host_off, blk_kind, budget: int, theta,
+                 hop_scale: float = 1.0, n_kin: int = 0, page_bytes: int = 65536, transfer: bool = True,
+                 host_arena: Optional[torch.Tensor] = None, host_bytes: Optional[int] = None,
+                 dev_bytes: Optional[int] = None, resident_init=None, device: int = 0,
+                 shard: Optional[tuple] = None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None):
+        self.lib = L.lib()
+        self.device = torch.device("cuda", device)
+        torch.cuda.set_device(self.device)
+        lo, hi = shard if shard is not None else (0, n_agents)
+        self.n_agents, self.lo, self.hi = int(n_agents), int(lo), int(hi)
+        self.n_local = self.hi - self.lo
+        self.n_kin = int(n_kin)
+        self.page_bytes = int(page_bytes)
+        self.transfer_enabled = bool(transfer)
+        self.stream = stream or torch.cuda.Stream(self.device)
+        self.copy_stream = copy_stream or torch.cuda.Stream(self.device)
+        dev = self.device
+        # inputs
+        self.rec = torch.zeros(max(self.n_local, 1) * 16, dtype=torch.uint8, device=dev)
+        self.kin = torch.zeros(max(self.n_kin, 1) * 16, dtype=torch.uint8, device=dev)
+        blk_ptr = np.ascontiguousarray(blk_ptr, dtype=np.uint64)
+        blk_size = np.ascontiguousarray(blk_size, dtype=np.uint32)
+        self.n_blocks = int(blk_ptr[-1]) if len(blk_ptr) else 0
+        self.blk_ptr = _dev_bytes(blk_ptr, dev)
+        self.blk_size = _dev_bytes(blk_size, dev)
+        self.blk_host_off = _dev_bytes(np.ascontiguousarray(blk_host_off, dtype=np.uint64), dev)
+        self.blk_kind = _dev_bytes(np.ascontiguousarray(blk_kind, dtype=np.uint8), dev)
+        self.n_block_pages = int((blk_size.astype(np.uint64) // np.uint64(page_bytes)).sum()) if transfer else 0
+        self.blk_size_np = blk_size
+        self.budget = int(budget)
+        # arenas
+        self.host_arena = None
+        self.dev_arena = None
+        if transfer:
+            if host_arena is None:
+                hb = int(host_bytes) if host_bytes is not None else int(np.asarray(blk_host_off, np.uint64).max(
+                    initial=0) + page_bytes + (int(blk_size.max()) if len(blk_size) else 0))
+                host_arena = torch.zeros(hb, dtype=torch.uint8).pin_memory()
+            self.host_arena = host_arena
+            if dev_bytes is None:
+                dev_bytes = (self.budget + page_bytes - 1) // page_bytes * page_bytes
+            self.dev_arena = torch.empty(max(int(dev_bytes), page_bytes), dtype=torch.uint8, device=dev)
+        self.res_init = None
+        if resident_init is not None:
+            ri = np.ascontiguousarray(resident_init).astype(bool)
+            words = np.packbits(ri, bitorder="little")
+            pad = (-len(words)) % 4
+            words = np.concatenate([words, np.zeros(pad, np.uint8)])
+            self.res_init = _dev_bytes(words, dev)
+        self._nccl_id = None
+        if world > 1:
+            self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
+        cfg = L.Config()
+        cfg.abi_version = L.ABI_VERSION
+        cfg.flags = 0 if transfer else L.F_NO_TRANSFER
+        cfg.n_agents = self.n_agents
+        cfg.shard_begin = self.lo
+        cfg.shard_end = self.hi
+        cfg.n_kin = self.n_kin
+        cfg.budget_bytes = self.budget
+        th = np.asarray(theta, dtype=np.float32)
+        cfg.theta[0], cfg.theta[1], cfg.theta[2] = float(th[0]), float(th[1]), float(th[2])
+        cfg.hop_scale = float(hop_scale)
+        cfg.page_bytes = self.page_bytes
+        cfg.device = int(device)
+        cfg.rank = int(rank)
+        cfg.world = int(world)
+        cfg.nccl_unique_id = C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None
+        cfg.stream = self.stream.cuda_stream
+        cfg.copy_stream = self.copy_stream.cuda_stream
+        self.cfg = cfg
+        tab = L.Tables()
+        tab.agent_rec = _ptr(self.rec)
+        tab.agent_kin = _ptr(self.kin)
+        tab.blk_ptr = _ptr(self.blk_ptr)
+        tab.blk_size = _ptr(self.blk_size)
+        tab.blk_host_off = _ptr(self.blk_host_off)
+        tab.blk_kind = _ptr(self.blk_kind)
+        tab.n_blocks = self.n_blocks
+        tab.n_block_pages = self.n_block_pages
+        tab.host_arena = _ptr(self.host_arena)
+        tab.host_bytes = 0 if self.host_arena is None else self.host_arena.numel()
+        tab.dev_arena = _ptr(self.dev_arena)
+        tab.dev_bytes = 0 if self.dev_arena is None else self.dev_arena.numel()
+        tab.resident_init = _ptr(self.res_init)
+        ws = int(self.lib.scalesim_workspace_bytes(C.byref(cfg), C.byref(tab)))
+        if ws == 0:
+            raise L.ScaleSimError(L.E_INVALID, "scalesim_workspace_bytes")
+        self.workspace = torch.empty(ws + 256, dtype=torch.uint8, device=dev)
+        base = self.workspace.data_ptr()
+        tab.workspace = (base + 255) // 256 * 256
+        tab.workspace_bytes = ws
+        self.tab = tab
+        self.ctx = C.c_void_p()
+        torch.cuda.synchronize(self.device)
+        L.check(self.lib.scalesim_init(C.byref(cfg), C.byref(tab), C.byref(self.ctx)), "scalesim_init")
+        self.view = L.PlanView()
+
+    # ---- inputs ------------------------------------------------------------------
+    def set_records(self, rec, kin=None):
+        """Copy this step's agent records (n_local, 4) uint32 and kinematics to the device
+        buffers the context reads (on the planner stream)."""
+        with torch.cuda.stream(self.stream):
+            r = np.ascontiguousarray(rec, dtype=np.uint32)
+            assert r.size == 4 * self.n_local
+            if self.n_local:
+                self.rec[:r.nbytes].copy_(torch.from_numpy(r.view(np.uint8).reshape(-1)), non_blocking=False)
+            if kin is not None and self.n_kin:
+                k = np.ascontiguousarray(kin, dtype=np.float32)
+                self.kin[:k.nbytes].copy_(torch.from_numpy(k.view(np.uint8).reshape(-1)), non_blocking=False)
+
+    def set_inputs_ptr(self, rec_ptr: int, kin_ptr: Optional[int] = None):
+        L.check(self.lib.scalesim_set_inputs(self.ctx, rec_ptr, kin_ptr or _ptr(self.kin)), "scalesim_set_inputs")
+
+    # ---- the four calls ------------------------------------------------------------
+    def score(self, now: int, dist_out: Optional[torch.Tensor] = None):
+        L.check(self.lib.scalesim_score(self.ctx, int(now), _ptr(dist_out)), "scalesim_score")
+
+    def plan(self):
+        L.check(self.lib.scalesim_plan(self.ctx, C.byref(self.view)), "scalesim_plan")
+        return self.view
+
+    def transfer(self):
+        L.check(self.lib.scalesim_transfer(self.ctx, C.byref(self.view)), "scalesim_transfer")
+
+    def step(self, now: int):
+        L.check(self.lib.scalesim_step(self.ctx, int(now), C.byref(self.view)), "scalesim_step")
+        return self.view
+
+    def step_host(self, now: int, rec_host: np.ndarray, kin_host: Optional[np.ndarray] = None,
+                  pf_out: Optional[np.ndarray] = None, ev_out: Optional[np.ndarray] = None):
+        """End-to-end step from host buffers (host->device copy, step, header + lists back)."""
+        h = L.PlanHost()
+        rp = rec_host.ctypes.data
+        kp = kin_host.ctypes.data if kin_host is not None else None
+        st = self.lib.scalesim_step_host(self.ctx, int(now), rp, kp, C.byref(h),
+                                         None if pf_out is None else pf_out.ctypes.data,
+                                         None if ev_out is None else ev_out.ctypes.data)
+        L.check(st, "scalesim_step_host", allow=(L.OK, L.E_INSUFFICIENT))
+        return h.as_dict()
+
+    def join(self):
+        L.check(self.lib.scalesim_join(self.ctx), "scalesim_join")
+
+    def sync(self):
+        h = L.PlanHost()
+        st = self.lib.scalesim_sync(self.ctx, C.byref(h))
+        L.check(st, "scalesim_sync", allow=(L.OK, L.E_INSUFFICIENT, L.E_BAD_INPUT))
+        d = h.as_dict()
+        d["rc"] = st
+        return d
+
+    def launch_count(self) -> int:
+        return int(self.lib.scalesim_launch_count(self.ctx))
+
+    # ---- readbacks (tests / tools) --------------------------------------------------
+    def _read(self, ptr: int, nbytes: int) -> np.ndarray:
+        """Copy nbytes at a view pointer (always inside the workspace) to the host."""
+        off = int(ptr) - self.workspace.data_ptr()
+        assert 0 <= off and off + nbytes <= self.workspace.numel()
+        torch.cuda.synchronize(self.device)
+        return self.workspace[off:off + nbytes].cpu().numpy()
+
+    def lists(self, hdr=None):
+        hdr = hdr or self.sync()
+        pf = self._read(self.view.prefetch_ids, 4 * hdr["n_prefetch"]).view(np.uint32)
+        ev = self._read(self.view.evict_ids, 4 * hdr["n_evict"]).view(np.uint32)
+        return pf, ev
+
+    def resident(self) -> np.ndarray:
+        nw = (self.n_local + 31) // 32
+        words = self._read(self.view.resident_bitmap, 4 * nw)
+        return np.unpackbits(words, bitorder="little")[:self.n_local].astype(np.uint8)
+
+    def distances(self) -> np.ndarray:
+        return self._read(self.view.dist, 4 * self.n_local).view(np.float32)
+
+    def page_table(self) -> np.ndarray:
+        return self._read(self.view.page_table, 4 * self.n_block_pages).view(np.uint32)
+
+    def descriptors(self, hdr=None):
+        hdr = hdr or self.sync()
+        d2h = self._read(self.view.d2h_desc, 16 * hdr["n_d2h"]).view(np.uint64).reshape(-1, 2)
+        h2d = self._read(self.view.h2d_desc, 16 * hdr["n_h2d"]).view(np.uint64).reshape(-1, 2)
+        return d2h, h2d
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None and self.ctx.value:
+            self.lib.scalesim_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+

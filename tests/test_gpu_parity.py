@@ -1,0 +1,139 @@
+"""GPU parity: the CUDA planner (through the C ABI) against the CPU oracle, element by
+element, on seeded workloads of every BASELINE config shape."""
+import numpy as np
+import pytest
+
+import oracle
+import tracegen as tg
+from helpers import rec_of
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2601_21473_b200 import build
+    build.build()
+
+
+def test_c1_all_variants():
+    from gpu_harness import run_parity
+    for variant in ("ind", "int", "diff", "diff-star"):
+        for th in (0.0, 3.0, np.inf):
+            for seed in (1, 2, 3):
+                w = tg.config_c1(seed=seed, theta=(th, th, th), variant=variant)
+                run_parity(w)
+
+
+def test_c2_mini_physical_transfer():
+    from gpu_harness import run_parity
+    w = tg.config_c2(seed=2, steps=40, n=3001, lora=4 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
+    out = run_parity(w)
+    assert sum(o["n_evict"] for o in out) > 0
+
+
+def test_c3_mini_all_classes():
+    from gpu_harness import run_parity
+    w = tg.config_c3(seed=1, steps=6, n=9001, budget=int(9001 * 3.41e6 * 0.235))
+    run_parity(w)
+
+
+def test_c2_full_size():
+    """BASELINE configs[1]: 10k agents, rank-16 7B LoRA + 917,504 B KV pages, budget 25%."""
+    from gpu_harness import run_parity
+    w = tg.config_c2(seed=1, steps=24, host_bytes=16 << 30)
+    run_parity(w, stamp_writes=False, content_pages=16)
+
+
+def test_c3_full_size():
+    """BASELINE configs[2]: 100k agents, three classes, 80 GB budget (2 steps: the oracle's
+    O(n^2) interaction scan takes ~10 s per step)."""
+    from gpu_harness import run_parity
+    w = tg.config_c3(seed=1, steps=2, host_bytes=8 << 30)
+    run_parity(w, stamp_writes=False, content_pages=16)
+
+
+def test_c4_full_size_logical():
+    """BASELINE configs[3] at G=1: 1M agents, logical sizes (no arena), the bench's launch
+    configuration."""
+    from gpu_harness import run_parity
+    w = tg.config_c4(seed=1, steps=6)
+    run_parity(w, transfer=False)
+
+
+def test_edge_cases():
+    from gpu_harness import run_parity
+    PG = tg.PAGE_BYTES
+
+    def wl(agents, budget, theta=(4.0, 4.0, 4.0), kin=None, now=0, resident=None):
+        n = len(agents)
+        for a in agents:
+            a.setdefault("fp", PG)
+        blocks = tg.make_blocks([[tg.KIND_KV] if a["fp"] else [] for a in agents],
+                                [[a["fp"]] if a["fp"] else [] for a in agents])
+        rec = rec_of(agents, now)[None]
+        k = None if kin is None else np.asarray(kin, np.float32)[None]
+        return tg.Workload("edge", n, np.array([now]), rec, k, blocks, budget, np.asarray(theta, np.float32))
+
+    # single agent, fits / does not fit
+    run_parity(wl([dict(d=1)], PG))
+    run_parity(wl([dict(d=1)], PG - 1))
+    # ragged word (33 agents), everything fits
+    run_parity(wl([dict(d=i % 5) for i in range(33)], 40 * PG))
+    # budget 0 with active agents -> INSUFFICIENT
+    run_parity(wl([dict(phase=tg.PH_GENERATING), dict(d=2)], 0))
+    # theta 0 and inf, idle agents, unreachable diffusion, zero-footprint agents
+    ag = [dict(d=3), dict(phase=tg.PH_IDLE), dict(cls=tg.CL_DIFF, hop=tg.UNREACHABLE), dict(d=1, fp=0),
+          dict(cls=tg.CL_DIFF, hop=2), dict(phase=tg.PH_WAITING)]
+    for th in (0.0, np.inf):
+        run_parity(wl([dict(a) for a in ag], 3 * PG, theta=(th, th, th)))
+    # malformed records: class 3, kin index out of range, non-finite kinematics
+    ag = [dict(cls=3, d=2), dict(cls=tg.CL_INT, d=5, kin=9), dict(cls=tg.CL_INT, d=5, kin=0),
+          dict(cls=tg.CL_INT, d=5, kin=1)]
+    run_parity(wl(ag, 10 * PG, kin=[[0, 0, np.nan, 0], [1, 0, -1, 0]]))
+    # resident at init, then evicted
+    w = wl([dict(d=9), dict(d=1), dict(phase=tg.PH_GENERATING)], 2 * PG)
+    run_parity(w, resident_init=np.array([1, 1, 0], np.uint8))
+
+
+def test_large_tie_group_spans_tiles():
+    """Heavy integer ties: 20,000 agents at the same distance, budget cutting inside the tie
+    group across several 2048-agent tiles (id-order prefix, R1/R3)."""
+    from gpu_harness import run_parity
+    n = 20000
+    rng = np.random.default_rng(3)
+    fp = rng.choice([1, 2, 3], n) * tg.PAGE_BYTES
+    agents = [dict(d=5, fp=int(fp[i])) for i in range(n)]
+    blocks = tg.make_blocks([[tg.KIND_KV]] * n, [[int(f)] for f in fp])
+    rec = rec_of(agents)[None]
+    budget = int(fp.sum() * 0.37)
+    w = tg.Workload("ties", n, np.array([0]), rec, None, blocks, budget, np.full(3, 9.0, np.float32))
+    run_parity(w)
+    run_parity(w, transfer=False)
+
+
+def test_call_order_and_host_step():
+    from paper_2601_21473_b200 import _lib as L
+    from gpu_harness import make_planner
+    w = tg.config_c2(seed=4, steps=3, n=500, lora=2 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
+    pl = make_planner(w, transfer=True)
+    with pytest.raises(L.ScaleSimError) as e:
+        pl.plan()
+    assert e.value.status == L.E_ORDER
+    pl.set_records(w.rec[0])
+    pl.score(int(w.now[0]))
+    pl.plan()
+    pl.transfer()
+    with pytest.raises(L.ScaleSimError):
+        pl.transfer()
+    hdr = pl.sync()
+    # the end-to-end host entry point gives the same plan as the device one
+    pl2 = make_planner(w, transfer=True)
+    pf = np.zeros(w.n, np.uint32)
+    ev = np.zeros(w.n, np.uint32)
+    h2 = pl2.step_host(int(w.now[0]), np.ascontiguousarray(w.rec[0]), None, pf, ev)
+    pf1, ev1 = pl.lists(hdr)
+    assert h2["n_prefetch"] == hdr["n_prefetch"] and np.array_equal(pf[:h2["n_prefetch"]], pf1)
+    assert h2["cut_bits"] == hdr["cut_bits"] and h2["bytes_h2d"] == hdr["bytes_h2d"]
+    pl.close()
+    pl2.close()
