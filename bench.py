@@ -162,9 +162,9 @@ def run_reference(args, rank, world):
 
 def link_peak(torch, dev):
     n = 1 << 30
-    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(n, dtype=torch.uint8, device=dev)
-    h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     d2 = torch.empty(n, dtype=torch.uint8, device=dev)
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
@@ -197,7 +197,7 @@ def transfer_leg(torch, dev, seed):
     from paper_2601_21473_b200.planner import Planner
     w = tg.config_c2(seed=seed, steps=24, host_bytes=8 << 30)
     b = w.blocks
-    host = torch.empty(int(b.host_bytes), dtype=torch.uint8).pin_memory()
+    host = torch.empty(int(b.host_bytes), dtype=torch.uint8, pin_memory=True)
     pl = Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
                  page_bytes=w.page_bytes, transfer=True, host_arena=host, device=dev.index)
     tot_b, tot_t, steps = 0, 0.0, 0
@@ -291,8 +291,9 @@ def main():
         eager_step(s)
     pl.sync()
 
-    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    # external=True: inside a graph capture these become event-record nodes that keep timing
+    ev_s = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(K)]
     t_base = WARM_IN + W
 
     def timed_steps():

@@ -95,6 +95,25 @@ __device__ __forceinline__ unsigned long long warp_sum_u32_exact(uint32_t v) {
 __device__ __forceinline__ uint32_t phase_of(uint4 r) { return r.z & 3u; }
 __device__ __forceinline__ uint32_t class_of(uint4 r) { return (r.z >> 2) & 3u; }
 
+// Warp-aggregated byte-weighted histogram update: lanes with the same bucket form a group
+// (match.any); each group reduces its bytes (exact, 16-bit halves), min and max key, and its
+// lowest lane issues one shared-memory atomic per field.
+__device__ __forceinline__ void hist_add(unsigned long long *h, uint32_t *mn, uint32_t *nmx, bool on,
+                                         uint32_t bucket, uint32_t bits, uint32_t bytes) {
+  const uint32_t grp = __match_any_sync(FULL, on ? bucket : 0xFFFFFFFFu);
+  if (on) {
+    const uint32_t lo = __reduce_add_sync(grp, bytes & 0xFFFFu);
+    const uint32_t hi = __reduce_add_sync(grp, bytes >> 16);
+    const uint32_t kmin = __reduce_min_sync(grp, bits);
+    const uint32_t knmx = __reduce_min_sync(grp, ~bits);
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(grp) - 1)) {
+      atomicAdd(&h[bucket], ((unsigned long long)hi << 16) + lo);
+      atomicMin(&mn[bucket], kmin);
+      atomicMin(&nmx[bucket], knmx);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // a1: invocation distance of one agent (readings R5, R8, R9)
 
@@ -271,23 +290,7 @@ __global__ void __launch_bounds__(NT) k_score(Params p, int64_t now) {
     if (lane == 0 && (i >> 5) < p.n_words) p.d.elig[i >> 5] = eb;
     if (valid && d == 0.0f) zero_bytes += r.y;
     // warp-aggregated histogram update: one smem atomic per distinct bucket in the warp
-    uint32_t pending = eb;
-    const uint32_t bucket = bits >> 20;
-    while (pending) {
-      const int leader = __ffs(pending) - 1;
-      const uint32_t lb = __shfl_sync(FULL, bucket, leader);
-      const uint32_t grp = __ballot_sync(FULL, elig && bucket == lb);
-      const bool in = (grp >> lane) & 1u;
-      const unsigned long long s = warp_sum_u32_exact(in ? r.y : 0u);
-      const uint32_t mn = __reduce_min_sync(FULL, in ? bits : 0xFFFFFFFFu);
-      const uint32_t nmx = __reduce_min_sync(FULL, in ? ~bits : 0xFFFFFFFFu);
-      if (lane == leader) {
-        atomicAdd(&sh_hist[lb], s);
-        atomicMin(&sh_min[lb], mn);
-        atomicMin(&sh_nmax[lb], nmx);
-      }
-      pending &= ~grp;
-    }
+    hist_add(sh_hist, sh_min, sh_nmax, elig, bits >> 20, bits, r.y);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < 2048; b += NT) {
@@ -400,23 +403,7 @@ __global__ void __launch_bounds__(NT) k_hist(Params p, int level) {
       in_b = el && (bits >> hi_shift) == want;
       if (in_b) fp = p.rec[i].y;
     }
-    uint32_t pending = __ballot_sync(FULL, in_b);
-    const uint32_t bucket = (bits >> shift) & 1023u;
-    while (pending) {
-      const int leader = __ffs(pending) - 1;
-      const uint32_t lb = __shfl_sync(FULL, bucket, leader);
-      const uint32_t grp = __ballot_sync(FULL, in_b && bucket == lb);
-      const bool in = (grp >> lane) & 1u;
-      const unsigned long long s = warp_sum_u32_exact(in ? fp : 0u);
-      const uint32_t mn = __reduce_min_sync(FULL, in ? bits : 0xFFFFFFFFu);
-      const uint32_t nmx = __reduce_min_sync(FULL, in ? ~bits : 0xFFFFFFFFu);
-      if (lane == leader) {
-        atomicAdd(&sh_hist[lb], s);
-        atomicMin(&sh_min[lb], mn);
-        atomicMin(&sh_nmax[lb], nmx);
-      }
-      pending &= ~grp;
-    }
+    hist_add(sh_hist, sh_min, sh_nmax, in_b, (bits >> shift) & 1023u, bits, fp);
   }
   __syncthreads();
   unsigned long long *gh = level == 2 ? p.d.hist2 : p.d.hist3;
@@ -895,6 +882,10 @@ __global__ void k_init_pages_count(Params p, const uint32_t *res, uint64_t *cnt)
 }
 
 __global__ void k_init_ring(Params p, const uint32_t *res) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.d.pool[0] = 0;              // FIFO of free pages: all pages, in index order
+    p.d.pool[1] = p.n_dev_pages;
+  }
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < p.n_dev_pages; q += (uint64_t)gridDim.x * blockDim.x)
     p.d.ring[q] = (uint32_t)q;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < p.n_words; w += (uint64_t)gridDim.x * blockDim.x) {

@@ -68,7 +68,7 @@ class Planner:
             if host_arena is None:
                 hb = int(host_bytes) if host_bytes is not None else int(np.asarray(blk_host_off, np.uint64).max(
                     initial=0) + page_bytes + (int(blk_size.max()) if len(blk_size) else 0))
-                host_arena = torch.zeros(hb, dtype=torch.uint8).pin_memory()
+                host_arena = torch.zeros(hb, dtype=torch.uint8, pin_memory=True)
             self.host_arena = host_arena
             if dev_bytes is None:
                 dev_bytes = (self.budget + page_bytes - 1) // page_bytes * page_bytes

@@ -17,15 +17,25 @@ import tracegen as tg
 ST_MASK = oracle.ST_INSUFFICIENT | oracle.ST_BAD_RECORD | oracle.ST_BAD_KIN | oracle.ST_NO_PAGES
 
 
+def fill_pattern(host, chunk=1 << 28):
+    """Per-offset pattern into a pinned host tensor, chunk by chunk (bounded host memory)."""
+    hb = host.numel()
+    words = host[: hb // 4 * 4].view(torch.int32)
+    for o in range(0, hb // 4, chunk // 4):
+        n = min(chunk // 4, hb // 4 - o)
+        pat = tg.host_pattern(4 * n, seed=0, word_offset=o)
+        words[o:o + n].copy_(torch.from_numpy(pat.view(np.int32)))
+
+
 def make_planner(w: tg.Workload, transfer: bool, resident_init=None, host_pattern=True, dev_pages=None):
     from paper_2601_21473_b200.planner import Planner
     b = w.blocks
     host = None
     if transfer:
         hb = int(b.host_bytes)
-        host = torch.empty(hb, dtype=torch.uint8).pin_memory()
+        host = torch.empty(hb, dtype=torch.uint8, pin_memory=True)
         if host_pattern:
-            host.view(torch.int32)[: hb // 4].copy_(torch.from_numpy(tg.host_pattern(hb).view(np.int32)))
+            fill_pattern(host)
     pages = dev_pages if dev_pages is not None else (w.budget + w.page_bytes - 1) // w.page_bytes
     return Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
                    hop_scale=w.hop_scale, n_kin=w.n_kin, page_bytes=w.page_bytes, transfer=transfer,

@@ -34,8 +34,8 @@ def test_c2_mini_physical_transfer():
 
 def test_c3_mini_all_classes():
     from gpu_harness import run_parity
-    w = tg.config_c3(seed=1, steps=6, n=9001, budget=int(9001 * 3.41e6 * 0.235))
-    run_parity(w)
+    w = tg.config_c3(seed=1, steps=6, n=9001, budget=int(9001 * 3.41e6 * 0.235), host_bytes=4 << 30)
+    run_parity(w, stamp_writes=False)
 
 
 def test_c2_full_size():

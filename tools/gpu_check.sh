@@ -9,5 +9,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout ${BENCH_TIMEOUT:-900} python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2> gpurun_out/bench.err
 echo "bench rc=$?" >> gpurun_out/bench.err
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/bench.err
+tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/bench.err
 tail -c 3000 gpurun_out/bench.log

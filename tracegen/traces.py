@@ -400,9 +400,9 @@ def gen_diffusion(n: int, steps: int, seed: int, adj=None, sources=None, n_sourc
     return P, T, D
 
 
-def host_pattern(n_bytes: int, seed: int = 0) -> np.ndarray:
+def host_pattern(n_bytes: int, seed: int = 0, word_offset: int = 0) -> np.ndarray:
     """Deterministic per-offset byte pattern for the host arena (uint32 words)."""
-    w = np.arange(n_bytes // 4, dtype=np.uint64)
+    w = np.arange(word_offset, word_offset + n_bytes // 4, dtype=np.uint64)
     x = (w * np.uint64(0x9E3779B1) + np.uint64(seed * 0x85EBCA77 + 1)) & np.uint64(0xFFFFFFFF)
     x ^= x >> np.uint64(15)
     return x.astype(np.uint32)
