@@ -68,6 +68,9 @@ typedef enum {
 #define SCALESIM_F_NO_TRANSFER 1u   /* plan + byte accounting only: no arena, no pages, no copies
                                        (logical sizes, BASELINE configs 4 and 5) */
 #define SCALESIM_F_KEEP_DIST 2u     /* keep per-agent distances readable after plan (dist view) */
+#define SCALESIM_F_MULTI_KERNEL 4u  /* force the multi-kernel plan path (otherwise, at world == 1 and
+                                       <= 16384 agents per SM, one persistent cooperative kernel
+                                       scores and plans the step; both paths give identical plans) */
 
 /* Agent record: 4 x uint32 per agent, 16-byte aligned, one 128-bit load.
  *   [0] t_next : action-end tick (ACTING independent / interaction agents), or remaining hop
@@ -206,6 +209,10 @@ scalesim_status scalesim_nccl_unique_id(void *out128);
  * caller's stream: required before reading arena pages on cfg.stream, and before ending a
  * CUDA-graph capture that contains scalesim_transfer). */
 scalesim_status scalesim_join(scalesim_ctx *ctx);
+
+/* 1 if this context plans each step with the single persistent kernel, 0 if with the
+ * multi-kernel path (world > 1, SCALESIM_F_MULTI_KERNEL, or tiles too large), -1 on NULL. */
+int scalesim_fused(const scalesim_ctx *ctx);
 
 /* Launches of library kernels enqueued so far (for the bench's gpu_launches). */
 uint64_t scalesim_launch_count(const scalesim_ctx *ctx);

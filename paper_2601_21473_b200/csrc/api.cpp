@@ -81,6 +81,22 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.pool = take(16);
   L.desc[0] = take(16 + 32 * (L.desc_cap ? L.desc_cap : 1));
   L.desc[1] = take(16 + 32 * (L.desc_cap ? L.desc_cap : 1));
+  L.f_hist1 = take(8 * 2 * 2048);
+  L.f_mm1 = take(4 * 2 * 4096);
+  L.f_hist2 = take(8 * 2 * 1024);
+  L.f_mm2 = take(4 * 2 * 2048);
+  L.f_hist3 = take(8 * 2 * 1024);
+  L.f_cta_h1 = take(8 * (uint64_t)FUSED_MAX_CTAS * 2048);
+  L.f_cta_h2 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
+  L.f_cta_h3 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
+  L.f_cta_cpf = take(4 * (uint64_t)FUSED_MAX_CTAS * 2048);
+  L.f_cta_cev = take(4 * (uint64_t)FUSED_MAX_CTAS * 2048);
+  L.f_tot = take(4 * 2 * 2 * 2048);
+  L.f_acc = take(8 * 2 * 8);
+  L.f_sk2 = take(4 * n1);
+  L.f_sv2 = take(4 * n1);
+  L.f_sk3 = take(4 * n1);
+  L.f_sv3 = take(4 * n1);
   L.total = off;
   return L;
 }
@@ -130,6 +146,22 @@ Dev make_dev(void *ws, const Layout &L) {
   d.pool = (unsigned long long *)(b + L.pool);
   d.desc[0] = (unsigned long long *)(b + L.desc[0]);
   d.desc[1] = (unsigned long long *)(b + L.desc[1]);
+  d.f_hist1 = (unsigned long long *)(b + L.f_hist1);
+  d.f_mm1 = (uint32_t *)(b + L.f_mm1);
+  d.f_hist2 = (unsigned long long *)(b + L.f_hist2);
+  d.f_mm2 = (uint32_t *)(b + L.f_mm2);
+  d.f_hist3 = (unsigned long long *)(b + L.f_hist3);
+  d.f_cta_h1 = (unsigned long long *)(b + L.f_cta_h1);
+  d.f_cta_h2 = (unsigned long long *)(b + L.f_cta_h2);
+  d.f_cta_h3 = (unsigned long long *)(b + L.f_cta_h3);
+  d.f_cta_cpf = (uint32_t *)(b + L.f_cta_cpf);
+  d.f_cta_cev = (uint32_t *)(b + L.f_cta_cev);
+  d.f_tot = (uint32_t *)(b + L.f_tot);
+  d.f_acc = (unsigned long long *)(b + L.f_acc);
+  d.f_sk2 = (uint32_t *)(b + L.f_sk2);
+  d.f_sv2 = (uint32_t *)(b + L.f_sv2);
+  d.f_sk3 = (uint32_t *)(b + L.f_sk3);
+  d.f_sv3 = (uint32_t *)(b + L.f_sv3);
   return d;
 }
 
@@ -185,6 +217,13 @@ struct scalesim_ctx {
   ncclComm_t comm = nullptr;
   int last_buf = 0;
   bool xfer_pending = false;
+  // fused single-kernel plan (world == 1)
+  bool fused = false;
+  uint32_t fused_tile = 0;
+  int fused_grid = 0;
+  uint64_t fused_steps = 0;
+  bool deferred = false;  // score deferred into the fused plan kernel
+  int64_t deferred_now = 0;
 };
 
 static scalesim_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SCALESIM_OK : SCALESIM_E_CUDA; }
@@ -255,6 +294,8 @@ extern "C" scalesim_status scalesim_nccl_unique_id(void *out128) {
 }
 
 extern "C" uint64_t scalesim_launch_count(const scalesim_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" int scalesim_fused(const scalesim_ctx *ctx) { return ctx ? (ctx->fused ? 1 : 0) : -1; }
 
 extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scalesim_tables *t, scalesim_ctx **out) {
   if (!out) return SCALESIM_E_INVALID;
@@ -395,6 +436,18 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
     }
   }
   c->launches += launch_plan_init(p, c->stream);
+  // fused path: one CTA per SM, co-resident (cooperative launch)
+  if (cfg->world == 1 && !(cfg->flags & SCALESIM_F_MULTI_KERNEL)) {
+    uint32_t tile = 0;
+    if (fused_supported(p, sms, &tile)) {
+      c->fused = true;
+      c->fused_tile = tile;
+      c->fused_grid = sms;
+      if (cudaMemsetAsync(p.d.f_mm1, 0xFF, 4 * 2 * 4096, c->stream) != cudaSuccess ||
+          cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2048, c->stream) != cudaSuccess)
+        return fail(SCALESIM_E_CUDA);
+    }
+  }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
   if (cfg->world > 1) {
     if (!cfg->nccl_unique_id || !g_nccl.load()) return fail(SCALESIM_E_NCCL);
@@ -423,7 +476,16 @@ extern "C" scalesim_status scalesim_score(scalesim_ctx *c, int64_t now, float *d
   // the accumulators were cleared at the end of the previous plan (or at init); a repeated
   // score without a plan clears them again
   if (c->scored) c->launches += launch_plan_init(c->p, c->stream);
-  c->launches += launch_score(c->p, now, dist_out, c->stream, c->grid);
+  if (c->fused && !dist_out) {
+    // the fused plan kernel scores the agents itself (phase P1); only the interaction
+    // pair scan (which needs every participant before any agent is scored) runs here
+    c->launches += launch_interaction(c->p, c->stream, c->grid);
+    c->deferred = true;
+    c->deferred_now = now;
+  } else {
+    c->launches += launch_score(c->p, now, dist_out, c->stream, c->grid);
+    c->deferred = false;
+  }
   CK(cudaGetLastError());
   c->scored = true;
   return SCALESIM_OK;
@@ -448,11 +510,20 @@ static void fill_plan(scalesim_ctx *c, scalesim_plan_view *out) {
   out->done_event = c->ev_xfer[c->last_buf];
 }
 
+static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out);
+
 extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *out) {
   if (!c) return SCALESIM_E_INVALID;
   if (!c->scored) return SCALESIM_E_ORDER;
   Params &p = c->p;
   const bool multi = c->cfg.world > 1;
+  if (c->deferred) {
+    c->launches += launch_fused_plan(p, c->deferred_now, (int)(c->fused_steps & 1), c->fused_grid, c->fused_tile,
+                                     c->stream);
+    c->fused_steps++;
+    c->deferred = false;
+    return finish_plan(c, out);
+  }
   if (multi) {
     scalesim_status s;
     if ((s = allreduce(c, p.d.hist1, 2049, ncclUint64, ncclSum)) != SCALESIM_OK) return s;
@@ -483,6 +554,11 @@ extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *ou
     c->launches += launch_fix_kept(p, c->stream);
   }
   c->launches += launch_lists(p, c->stream);
+  return finish_plan(c, out);
+}
+
+static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out) {
+  Params &p = c->p;
   const int buf = (int)(c->step & 1);
   p.desc_buf = buf;
   if (c->transfer) {
@@ -492,7 +568,8 @@ extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *ou
   }
   c->launches += launch_expand(p, c->stream);  // byte accounting always; pages only with transfer
   CK(cudaEventRecord(c->ev_plan, c->stream));
-  c->launches += launch_plan_init(p, c->stream);  // clear the accumulators for the next step
+  if (!c->fused || p.n_kin > 0 || c->cfg.world > 1)
+    c->launches += launch_plan_init(p, c->stream);  // clear the multi-kernel accumulators for the next step
   CK(cudaGetLastError());
   c->last_buf = buf;
   p.cur ^= 1;  // the new residency becomes current

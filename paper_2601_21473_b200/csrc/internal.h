@@ -12,6 +12,8 @@ constexpr uint32_t EXP_CH = 256;          // list entries per expansion chunk
 constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;
 constexpr uint32_t PAGE_NONE = 0xFFFFFFFFu;
 constexpr int L1_BITS = 11, L2_BITS = 10, L3_BITS = 10;  // distance-bit digits [30:20] [19:10] [9:0]
+constexpr int FUSED_MAX_CTAS = 160;       // fused path: one CTA per SM (B200: 148)
+constexpr uint32_t FUSED_MAX_TILE = 16384;  // fused path: agents per CTA held in shared memory
 
 // status bits (mirror include/scalesim.h)
 constexpr uint32_t ST_INSUFFICIENT = 1u, ST_BAD_RECORD = 2u, ST_BAD_KIN = 4u, ST_NO_PAGES = 8u;
@@ -49,6 +51,9 @@ struct Layout {
   uint64_t pf_ids, ev_ids, sort_ka, sort_va, sort_kb, sort_vb, sort_cnt, pfa_key, pfa_val;
   uint64_t exp_sum, exp_excl;
   uint64_t page_first, page_table, ring, pool, desc[2];
+  // fused path (double-buffered by fused-step parity where noted)
+  uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_h1, f_cta_h2, f_cta_h3, f_cta_cpf, f_cta_cev, f_tot, f_acc;
+  uint64_t f_sk2, f_sv2, f_sk3, f_sv3;
   uint64_t total;
 };
 
@@ -75,6 +80,17 @@ struct Dev {
   uint32_t *page_table, *ring;
   unsigned long long *pool;  // [0] head, [1] tail
   unsigned long long *desc[2];  // each: d2h [desc_cap pairs] then h2d [desc_cap pairs]
+  // fused path
+  unsigned long long *f_hist1;  // [2][2048]
+  uint32_t *f_mm1;              // [2][4096]
+  unsigned long long *f_hist2;  // [2][1024]
+  uint32_t *f_mm2;              // [2][2048]
+  unsigned long long *f_hist3;  // [2][1024]
+  unsigned long long *f_cta_h1, *f_cta_h2, *f_cta_h3;  // [CTAS][2048] / [CTAS][1024] / [CTAS][1024]
+  uint32_t *f_cta_cpf, *f_cta_cev;                      // [CTAS][2048]
+  uint32_t *f_tot;                                      // [2][2][2048]
+  unsigned long long *f_acc;                            // [2][8]
+  uint32_t *f_sk2, *f_sv2, *f_sk3, *f_sv3;              // [n_local] evict-segment sort scratch
 };
 
 Dev make_dev(void *ws, const Layout &L);
@@ -102,6 +118,7 @@ struct Params {
 // Launchers (kernels.cu).  Each returns the number of kernels it enqueued.
 int launch_plan_init(const Params &p, cudaStream_t s);
 int launch_score(const Params &p, int64_t now, float *dist_out, cudaStream_t s, int grid);
+int launch_interaction(const Params &p, cudaStream_t s, int grid);
 int launch_select(const Params &p, int level, cudaStream_t s);
 int launch_hist(const Params &p, int level, cudaStream_t s, int grid);
 int launch_tie(const Params &p, cudaStream_t s);
@@ -111,5 +128,8 @@ int launch_expand(const Params &p, cudaStream_t s);
 int launch_transfer(const Params &p, cudaStream_t s, int ctas);
 int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s);
 int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s);
+bool fused_supported(const Params &p, int grid, uint32_t *tile_out);
+int launch_fused_plan(const Params &p, int64_t now, int parity, int grid, uint32_t tile, cudaStream_t s);
+size_t fused_smem_bytes(uint32_t tile);
 
 }  // namespace ss

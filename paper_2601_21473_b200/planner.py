@@ -35,7 +35,8 @@ class Planner:
                  host_arena: Optional[torch.Tensor] = None, host_bytes: Optional[int] = None,
                  dev_bytes: Optional[int] = None, resident_init=None, device: int = 0,
                  shard: Optional[tuple] = None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None):
+                 stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None,
+                 multi_kernel: bool = False):
         self.lib = L.lib()
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
@@ -85,7 +86,7 @@ class Planner:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
         cfg = L.Config()
         cfg.abi_version = L.ABI_VERSION
-        cfg.flags = 0 if transfer else L.F_NO_TRANSFER
+        cfg.flags = (0 if transfer else L.F_NO_TRANSFER) | (L.F_MULTI_KERNEL if multi_kernel else 0)
         cfg.n_agents = self.n_agents
         cfg.shard_begin = self.lo
         cfg.shard_end = self.hi
@@ -182,6 +183,10 @@ class Planner:
         d = h.as_dict()
         d["rc"] = st
         return d
+
+    @property
+    def fused(self) -> bool:
+        return int(self.lib.scalesim_fused(self.ctx)) == 1
 
     def launch_count(self) -> int:
         return int(self.lib.scalesim_launch_count(self.ctx))

@@ -27,7 +27,8 @@ def fill_pattern(host, chunk=1 << 28):
         words[o:o + n].copy_(torch.from_numpy(pat.view(np.int32)))
 
 
-def make_planner(w: tg.Workload, transfer: bool, resident_init=None, host_pattern=True, dev_pages=None):
+def make_planner(w: tg.Workload, transfer: bool, resident_init=None, host_pattern=True, dev_pages=None,
+                 multi_kernel=False):
     from paper_2601_21473_b200.planner import Planner
     b = w.blocks
     host = None
@@ -39,14 +40,18 @@ def make_planner(w: tg.Workload, transfer: bool, resident_init=None, host_patter
     pages = dev_pages if dev_pages is not None else (w.budget + w.page_bytes - 1) // w.page_bytes
     return Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
                    hop_scale=w.hop_scale, n_kin=w.n_kin, page_bytes=w.page_bytes, transfer=transfer,
-                   host_arena=host, dev_bytes=max(pages, 1) * w.page_bytes, resident_init=resident_init)
+                   host_arena=host, dev_bytes=max(pages, 1) * w.page_bytes, resident_init=resident_init,
+                   multi_kernel=multi_kernel)
 
 
 def run_parity(w: tg.Workload, steps=None, transfer=True, resident_init=None, content_pages=64,
-               check_dist=True, stamp_writes=True, seed=0):
+               check_dist=True, stamp_writes=True, seed=0, multi_kernel=False, expect_fused=None):
     """Step the GPU planner and the oracle through the workload; assert parity every step.
     Returns per-step summaries."""
-    pl = make_planner(w, transfer, resident_init)
+    pl = make_planner(w, transfer, resident_init, multi_kernel=multi_kernel)
+    if expect_fused is None:
+        expect_fused = not multi_kernel
+    assert pl.fused == expect_fused
     res = np.zeros(w.n, np.uint8) if resident_init is None else np.asarray(resident_init, np.uint8).copy()
     om = None
     if transfer:

@@ -16,26 +16,32 @@ def built():
     build.build()
 
 
-def test_c1_all_variants():
+PATHS = [pytest.param(False, id="fused"), pytest.param(True, id="multikernel")]
+
+
+@pytest.mark.parametrize("mk", PATHS)
+def test_c1_all_variants(mk):
     from gpu_harness import run_parity
     for variant in ("ind", "int", "diff", "diff-star"):
         for th in (0.0, 3.0, np.inf):
             for seed in (1, 2, 3):
                 w = tg.config_c1(seed=seed, theta=(th, th, th), variant=variant)
-                run_parity(w)
+                run_parity(w, multi_kernel=mk)
 
 
-def test_c2_mini_physical_transfer():
+@pytest.mark.parametrize("mk", PATHS)
+def test_c2_mini_physical_transfer(mk):
     from gpu_harness import run_parity
     w = tg.config_c2(seed=2, steps=40, n=3001, lora=4 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
-    out = run_parity(w)
+    out = run_parity(w, multi_kernel=mk)
     assert sum(o["n_evict"] for o in out) > 0
 
 
-def test_c3_mini_all_classes():
+@pytest.mark.parametrize("mk", PATHS)
+def test_c3_mini_all_classes(mk):
     from gpu_harness import run_parity
     w = tg.config_c3(seed=1, steps=6, n=9001, budget=int(9001 * 3.41e6 * 0.235), host_bytes=4 << 30)
-    run_parity(w, stamp_writes=False)
+    run_parity(w, stamp_writes=False, multi_kernel=mk)
 
 
 def test_c2_full_size():
@@ -53,16 +59,21 @@ def test_c3_full_size():
     run_parity(w, stamp_writes=False, content_pages=16)
 
 
-def test_c4_full_size_logical():
+@pytest.mark.parametrize("mk", PATHS)
+def test_c4_full_size_logical(mk):
     """BASELINE configs[3] at G=1: 1M agents, logical sizes (no arena), the bench's launch
     configuration."""
     from gpu_harness import run_parity
-    w = tg.config_c4(seed=1, steps=6)
-    run_parity(w, transfer=False)
+    w = tg.config_c4(seed=1, steps=6 if mk else 20)
+    run_parity(w, transfer=False, multi_kernel=mk)
 
 
-def test_edge_cases():
-    from gpu_harness import run_parity
+@pytest.mark.parametrize("mk", PATHS)
+def test_edge_cases(mk):
+    from gpu_harness import run_parity as _rp
+
+    def run_parity(w, **kw):
+        return _rp(w, multi_kernel=mk, **kw)
     PG = tg.PAGE_BYTES
 
     def wl(agents, budget, theta=(4.0, 4.0, 4.0), kin=None, now=0, resident=None):
@@ -96,10 +107,14 @@ def test_edge_cases():
     run_parity(w, resident_init=np.array([1, 1, 0], np.uint8))
 
 
-def test_large_tie_group_spans_tiles():
+@pytest.mark.parametrize("mk", PATHS)
+def test_large_tie_group_spans_tiles(mk):
     """Heavy integer ties: 20,000 agents at the same distance, budget cutting inside the tie
     group across several 2048-agent tiles (id-order prefix, R1/R3)."""
-    from gpu_harness import run_parity
+    from gpu_harness import run_parity as _rp
+
+    def run_parity(w, **kw):
+        return _rp(w, multi_kernel=mk, **kw)
     n = 20000
     rng = np.random.default_rng(3)
     fp = rng.choice([1, 2, 3], n) * tg.PAGE_BYTES
@@ -137,3 +152,24 @@ def test_call_order_and_host_step():
     assert h2["cut_bits"] == hdr["cut_bits"] and h2["bytes_h2d"] == hdr["bytes_h2d"]
     pl.close()
     pl2.close()
+
+
+def test_fused_multi_level_select_and_segments():
+    """Distances spread over many values (boundary bucket with several distances: select
+    levels 2 and 3; evict segments that need the re-sort by full key), fused vs oracle."""
+    from gpu_harness import run_parity
+    n = 50000
+    rng = np.random.default_rng(9)
+    d = rng.integers(1, 5000, n)
+    fp = rng.choice([1, 2], n) * tg.PAGE_BYTES
+    agents = [dict(d=int(d[i]), fp=int(fp[i])) for i in range(n)]
+    blocks = tg.make_blocks([[tg.KIND_KV]] * n, [[int(f)] for f in fp])
+    rec0 = rec_of(agents)
+    # second step: everyone's distance changes (large evict list over many distances)
+    agents2 = [dict(d=int(x), fp=int(fp[i])) for i, x in enumerate(rng.integers(1, 5000, n))]
+    rec = np.stack([rec0, rec_of(agents2)])
+    budget = int(fp.sum() * 0.3)
+    w = tg.Workload("spread", n, np.array([0, 0]), rec, None, blocks, budget, np.full(3, np.inf, np.float32))
+    run_parity(w, transfer=False)
+    run_parity(w, transfer=False, multi_kernel=True)
+    run_parity(w)
