@@ -141,6 +141,7 @@ enum {
   SCALESIM_H_N_ELIGIBLE = 10,/* eligible agents on this rank */
   SCALESIM_H_POOL_HEAD = 11, /* free-page FIFO counters after this plan */
   SCALESIM_H_POOL_TAIL = 12,
+  SCALESIM_H_SEQ = 13,       /* plans completed on the device so far (integrity check for graphs) */
   SCALESIM_H_FIELDS = 16
 };
 

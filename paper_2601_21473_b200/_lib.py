@@ -23,10 +23,10 @@ ST_NO_PAGES = 8
 OK, E_INVALID, E_INSUFFICIENT, E_NOT_RESTORABLE, E_ORDER, E_CUDA, E_NCCL, E_INVARIANT, E_BAD_INPUT = range(9)
 
 H_N_PREFETCH, H_N_EVICT, H_BYTES_H2D, H_BYTES_D2H, H_CUT_BITS, H_CUT_REM, H_STATUS, H_N_D2H, H_N_H2D, \
-    H_KEPT_BYTES, H_N_ELIGIBLE, H_POOL_HEAD, H_POOL_TAIL = range(13)
+    H_KEPT_BYTES, H_N_ELIGIBLE, H_POOL_HEAD, H_POOL_TAIL, H_SEQ = range(14)
 H_FIELDS = 16
 HEADER_NAMES = ["n_prefetch", "n_evict", "bytes_h2d", "bytes_d2h", "cut_bits", "cut_rem", "status",
-                "n_d2h", "n_h2d", "kept_bytes", "n_eligible", "pool_head", "pool_tail"]
+                "n_d2h", "n_h2d", "kept_bytes", "n_eligible", "pool_head", "pool_tail", "seq"]
 
 # Every symbol include/scalesim.h declares (checked by tests/test_abi.py).
 EXPORTS = ["scalesim_workspace_bytes", "scalesim_init", "scalesim_score", "scalesim_plan",

@@ -97,6 +97,7 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_sv2 = take(4 * n1);
   L.f_sk3 = take(4 * n1);
   L.f_sv3 = take(4 * n1);
+  L.f_bar = take(64);
   L.total = off;
   return L;
 }
@@ -162,6 +163,7 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_sv2 = (uint32_t *)(b + L.f_sv2);
   d.f_sk3 = (uint32_t *)(b + L.f_sk3);
   d.f_sv3 = (uint32_t *)(b + L.f_sv3);
+  d.f_bar = (unsigned int *)(b + L.f_bar);
   return d;
 }
 
@@ -439,7 +441,7 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
   // fused path: one CTA per SM, co-resident (cooperative launch)
   if (cfg->world == 1 && !(cfg->flags & SCALESIM_F_MULTI_KERNEL)) {
     uint32_t tile = 0;
-    if (fused_supported(p, sms, &tile)) {
+    if (fused_supported(p, sms, &tile) && fused_prepare(sms, tile)) {
       c->fused = true;
       c->fused_tile = tile;
       c->fused_grid = sms;
@@ -519,7 +521,8 @@ extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *ou
   const bool multi = c->cfg.world > 1;
   if (c->deferred) {
     c->launches += launch_fused_plan(p, c->deferred_now, (int)(c->fused_steps & 1), c->fused_grid, c->fused_tile,
-                                     c->stream);
+                                     p.d.f_bar, c->stream);
+    CK(cudaGetLastError());
     c->fused_steps++;
     c->deferred = false;
     return finish_plan(c, out);

@@ -21,24 +21,48 @@
 //
 // Every decision uses the same definitions as the multi-kernel path (kernels.cu), DESIGN.md
 // §3; the two paths give bit-identical plans (tests/test_gpu_parity.py runs both).
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "common.cuh"
 #include "internal.h"
 
-namespace cg = cooperative_groups;
-
 namespace ss {
 
 constexpr int FT = 1024;  // threads per CTA
 constexpr int FWARPS = FT / 32;
 
+// Grid barrier for a grid of co-resident CTAs (one per SM, checked with the occupancy API
+// at init).  bar counts arrivals monotonically within one launch; the k-th barrier waits for
+// k * gridDim.x arrivals.  Launch L uses bar[L & 1]; launch L-1 reset it (same stream, so
+// every CTA of launch L-2 had finished).
+struct GridBar {
+  unsigned int *bar;
+  unsigned int k;
+  __device__ __forceinline__ void sync() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ++k;
+      __threadfence();
+      atomicAdd(bar, 1u);
+      const unsigned int target = k * gridDim.x;
+      unsigned int v;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        if (v >= target) break;
+        __nanosleep(20);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+};
+
 struct FusedArgs {
   Params p;
   int64_t now;
   int parity;
+  unsigned int *bar;  // [2] barrier counters
   uint32_t tile;   // agents per CTA, multiple of 32
   uint32_t tw;     // tile / 32
 };
@@ -254,7 +278,8 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
 }
 
 __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
-  cg::grid_group grid = cg::this_grid();
+  GridBar grid{A.bar + A.parity, 0u};
+  if (blockIdx.x == 0 && threadIdx.x == 0) A.bar[A.parity ^ 1] = 0u;  // for launch L+1
   const Params &p = A.p;
   const Dev &d = p.d;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -529,9 +554,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     H[H_CUT_REM] = sel.rem;
     H[H_KEPT] = (p.budget - sel.rem) + (all_fit ? 0ull : acc[3]);
     H[H_N_ELIG] = acc[4];
-    uint32_t status = (uint32_t)acc[5];
+    uint32_t status = (uint32_t)acc[5] | d.state->status;  // + BAD_KIN/BAD_RECORD of k_int_compact
     if (acc[0] > p.budget) status |= ST_INSUFFICIENT;
     H[H_STATUS] = status;
+    H[H_SEQ] += 1;
   }
 
   // ---------------- P6: re-sort list segments whose bucket holds several distances
@@ -547,40 +573,69 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
   __syncthreads();
   if (!sh_need) return;
   grid.sync();
-  // segment k (in bucket order, prefetch list first) is sorted by CTA k mod G
-  uint32_t seg = 0;
-  for (int list = 0; list < 2; ++list) {
-    const uint32_t *tot = list == 0 ? tot_pf : tot_ev;
-    uint32_t *ids = list == 0 ? d.pf_ids : d.ev_ids;
-    // bucket start recomputed from the totals (g_* were advanced in place)
-    uint32_t start = 0;
-    for (int bb = 0; bb < 2048; ++bb) {
-      const int b = list == 0 ? bb : 2047 - bb;
-      const uint32_t t = tot[b];
-      const bool multi = mm1[b] != ~mm1[2048 + b];
-      if (t > 1 && multi) {
-        if (seg % G == c) {
-          // gather (key, id), sort by key ascending (evict: complemented key), write back ids
-          const bool fits = t <= A.tile;
-          uint32_t *ka = fits ? s.keys : (list == 0 ? d.sort_ka : d.f_sk2) + start;
-          uint32_t *ia = fits ? s.memb : (list == 0 ? d.sort_va : d.f_sv2) + start;
-          uint32_t *kb = (list == 0 ? d.sort_kb : d.f_sk3) + start;
-          uint32_t *ib = (list == 0 ? d.sort_vb : d.f_sv3) + start;
-          for (uint32_t e = threadIdx.x; e < t; e += FT) {
-            const uint32_t id = ids[start + e];
-            const uint32_t key = d.keys[id - p.shard_begin];
-            ka[e] = list == 0 ? key : ~key;
-            ia[e] = id;
-          }
-          __syncthreads();
-          cta_sort_pairs(ka, ia, kb, ib, t, s.h_lo);
-          for (uint32_t e = threadIdx.x; e < t; e += FT) ids[start + e] = ia[e];
-          __syncthreads();
-        }
-        ++seg;
-      }
-      start += t;
+  // segment k (bucket order, prefetch list first) is re-sorted by CTA k mod G, in rounds
+  // of up to 64 segments per CTA
+  __shared__ uint32_t q_n, q_start[64], q_len[64], q_list[64];
+  __shared__ uint32_t seg_base, tot_tmp, seg_tmp;
+  for (uint32_t round = 0;; ++round) {
+    if (threadIdx.x == 0) {
+      q_n = 0;
+      seg_base = 0;
     }
+    __syncthreads();
+    for (int list = 0; list < 2; ++list) {
+      const uint32_t *tot = list == 0 ? tot_pf : tot_ev;
+      uint32_t len[2], need[2];
+      for (int k = 0; k < 2; ++k) {
+        const uint32_t r = 2 * threadIdx.x + k;  // position in list order
+        const uint32_t b = list == 0 ? r : 2047 - r;
+        len[k] = tot[b];
+        need[k] = (len[k] > 1 && mm1[b] != ~mm1[2048 + b]) ? 1u : 0u;
+      }
+      const uint32_t st_ex = block_excl_scan<uint32_t, FT>(len[0] + len[1], &tot_tmp);
+      const uint32_t sg_ex = block_excl_scan<uint32_t, FT>(need[0] + need[1], &seg_tmp);
+      uint32_t start = st_ex, sg = seg_base + sg_ex;
+      for (int k = 0; k < 2; ++k) {
+        if (need[k]) {
+          const uint32_t j = sg / G;  // this segment's index among CTA (sg % G)'s segments
+          if (sg % G == c && j >= round * 64 && j < (round + 1) * 64) {
+            const uint32_t slot = j - round * 64;
+            q_start[slot] = start;
+            q_len[slot] = len[k];
+            q_list[slot] = list;
+            atomicAdd(&q_n, 1u);
+          }
+          ++sg;
+        }
+        start += len[k];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) seg_base += seg_tmp;
+      __syncthreads();
+    }
+    const uint32_t nq = q_n;  // the CTA's segments of this round occupy slots [0, nq)
+    for (uint32_t qi = 0; qi < nq; ++qi) {
+      const uint32_t list = q_list[qi], start = q_start[qi], t = q_len[qi];
+      uint32_t *ids = list == 0 ? d.pf_ids : d.ev_ids;
+      const bool fits = t <= A.tile;
+      uint32_t *ka = fits ? s.keys : (list == 0 ? d.sort_ka : d.f_sk2) + start;
+      uint32_t *ia = fits ? s.memb : (list == 0 ? d.sort_va : d.f_sv2) + start;
+      uint32_t *kb = (list == 0 ? d.sort_kb : d.f_sk3) + start;
+      uint32_t *ib = (list == 0 ? d.sort_vb : d.f_sv3) + start;
+      for (uint32_t e = threadIdx.x; e < t; e += FT) {
+        const uint32_t id = ids[start + e];
+        const uint32_t key = d.keys[id - p.shard_begin];
+        ka[e] = list == 0 ? key : ~key;
+        ia[e] = id;
+      }
+      __syncthreads();
+      cta_sort_pairs(ka, ia, kb, ib, t, s.h_lo);
+      for (uint32_t e = threadIdx.x; e < t; e += FT) ids[start + e] = ia[e];
+      __syncthreads();
+    }
+    const uint32_t total_segs = seg_base;
+    __syncthreads();
+    if ((round + 1) * 64 * G >= total_segs) break;  // uniform: every CTA sees the same totals
   }
 }
 
@@ -595,21 +650,27 @@ bool fused_supported(const Params &p, int grid, uint32_t *tile_out) {
   return true;
 }
 
-int launch_fused_plan(const Params &p, int64_t now, int parity, int grid, uint32_t tile, cudaStream_t s) {
-  static bool attr_set = false;
-  const size_t smem = fused_smem_bytes(tile);
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_fused_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem_bytes(FUSED_MAX_TILE));
-    attr_set = true;
-  }
+// 1 CTA of FT threads per SM must be resident for the whole grid (grid barrier).
+bool fused_prepare(int grid, uint32_t tile) {
+  if (cudaFuncSetAttribute(k_fused_plan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)fused_smem_bytes(FUSED_MAX_TILE)) != cudaSuccess)
+    return false;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_plan, FT, fused_smem_bytes(tile)) != cudaSuccess)
+    return false;
+  return per_sm >= 1 && grid >= 1;
+}
+
+int launch_fused_plan(const Params &p, int64_t now, int parity, int grid, uint32_t tile, unsigned int *bar,
+                      cudaStream_t s) {
   FusedArgs A;
   A.p = p;
   A.now = now;
   A.parity = parity;
+  A.bar = bar;
   A.tile = tile;
   A.tw = tile / 32;
-  void *args[] = {&A};
-  cudaLaunchCooperativeKernel((const void *)k_fused_plan, dim3(grid), dim3(FT), args, smem, s);
+  k_fused_plan<<<grid, FT, fused_smem_bytes(tile), s>>>(A);
   return 1;
 }
 

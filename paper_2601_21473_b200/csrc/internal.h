@@ -20,7 +20,7 @@ constexpr uint32_t ST_INSUFFICIENT = 1u, ST_BAD_RECORD = 2u, ST_BAD_KIN = 4u, ST
 
 // header fields (mirror SCALESIM_H_*)
 enum { H_N_PF = 0, H_N_EV, H_H2D, H_D2H, H_CUT_BITS, H_CUT_REM, H_STATUS, H_N_D2H, H_N_H2D,
-       H_KEPT, H_N_ELIG, H_POOL_HEAD, H_POOL_TAIL, H_FIELDS = 16 };
+       H_KEPT, H_N_ELIG, H_POOL_HEAD, H_POOL_TAIL, H_SEQ, H_FIELDS = 16 };
 
 // Device-side selection state of one plan (radix select of the boundary distance).
 struct SelState {
@@ -53,7 +53,7 @@ struct Layout {
   uint64_t page_first, page_table, ring, pool, desc[2];
   // fused path (double-buffered by fused-step parity where noted)
   uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_h1, f_cta_h2, f_cta_h3, f_cta_cpf, f_cta_cev, f_tot, f_acc;
-  uint64_t f_sk2, f_sv2, f_sk3, f_sv3;
+  uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar;
   uint64_t total;
 };
 
@@ -91,6 +91,7 @@ struct Dev {
   uint32_t *f_tot;                                      // [2][2][2048]
   unsigned long long *f_acc;                            // [2][8]
   uint32_t *f_sk2, *f_sv2, *f_sk3, *f_sv3;              // [n_local] evict-segment sort scratch
+  unsigned int *f_bar;                                  // [2] grid-barrier counters
 };
 
 Dev make_dev(void *ws, const Layout &L);
@@ -129,7 +130,9 @@ int launch_transfer(const Params &p, cudaStream_t s, int ctas);
 int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s);
 int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s);
 bool fused_supported(const Params &p, int grid, uint32_t *tile_out);
-int launch_fused_plan(const Params &p, int64_t now, int parity, int grid, uint32_t tile, cudaStream_t s);
+int launch_fused_plan(const Params &p, int64_t now, int parity, int grid, uint32_t tile, unsigned int *bar,
+                      cudaStream_t s);
+bool fused_prepare(int grid, uint32_t tile);
 size_t fused_smem_bytes(uint32_t tile);
 
 }  // namespace ss

@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(NT) k_count_scan(Params p) {
     H[H_KEPT] = S->all_fit ? (p.budget - S->rem) : (p.budget - S->rem) + tot_tk;
     H[H_N_ELIG] = tot_el;
     H[H_STATUS] = S->status;
+    H[H_SEQ] += 1;
   }
 }
 
