@@ -330,9 +330,10 @@ def main():
     sampler = ClockSampler(local)
     with sampler:
         if graph is not None:
-            t0.record(pl.stream)
-            graph.replay()
-            t1.record(pl.stream)
+            with torch.cuda.stream(pl.stream):  # replay on the stream the events are recorded on
+                t0.record(pl.stream)
+                graph.replay()
+                t1.record(pl.stream)
         else:
             with torch.cuda.stream(pl.stream):
                 torch.cuda._sleep(int(2e9 * 0.05 + K * 2e5))

@@ -81,23 +81,24 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.pool = take(16);
   L.desc[0] = take(16 + 32 * (L.desc_cap ? L.desc_cap : 1));
   L.desc[1] = take(16 + 32 * (L.desc_cap ? L.desc_cap : 1));
-  L.f_hist1 = take(8 * 2 * 2048);
-  L.f_mm1 = take(4 * 2 * 4096);
+  L.f_hist1 = take(8 * 2 * 4096);
+  L.f_mm1 = take(4 * 2 * 2 * 4096);
   L.f_hist2 = take(8 * 2 * 1024);
-  L.f_mm2 = take(4 * 2 * 2048);
+  L.f_mm2 = take(4 * 2 * 2 * 1024);
   L.f_hist3 = take(8 * 2 * 1024);
-  L.f_cta_h1 = take(8 * (uint64_t)FUSED_MAX_CTAS * 2048);
-  L.f_cta_h2 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
-  L.f_cta_h3 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
-  L.f_cta_cpf = take(4 * (uint64_t)FUSED_MAX_CTAS * 2048);
-  L.f_cta_cev = take(4 * (uint64_t)FUSED_MAX_CTAS * 2048);
-  L.f_tot = take(4 * 2 * 2 * 2048);
+  L.f_cta_cpf = take(4 * (uint64_t)FUSED_MAX_CTAS * 1024);
+  L.f_cta_cev = take(4 * (uint64_t)FUSED_MAX_CTAS * 1024);
+  L.f_tot = take(4 * 2 * 2 * 1024);
   L.f_acc = take(8 * 2 * 8);
+  L.f_tie_val = take(8 * (uint64_t)FUSED_MAX_CTAS);
+  L.f_tie_flag = take(4 * (uint64_t)FUSED_MAX_CTAS);
+  L.wb_bytes = take(4 * n1);
   L.f_sk2 = take(4 * n1);
   L.f_sv2 = take(4 * n1);
   L.f_sk3 = take(4 * n1);
   L.f_sv3 = take(4 * n1);
   L.f_bar = take(64);
+  L.f_prof = take(128);
   L.total = off;
   return L;
 }
@@ -152,18 +153,19 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_hist2 = (unsigned long long *)(b + L.f_hist2);
   d.f_mm2 = (uint32_t *)(b + L.f_mm2);
   d.f_hist3 = (unsigned long long *)(b + L.f_hist3);
-  d.f_cta_h1 = (unsigned long long *)(b + L.f_cta_h1);
-  d.f_cta_h2 = (unsigned long long *)(b + L.f_cta_h2);
-  d.f_cta_h3 = (unsigned long long *)(b + L.f_cta_h3);
   d.f_cta_cpf = (uint32_t *)(b + L.f_cta_cpf);
   d.f_cta_cev = (uint32_t *)(b + L.f_cta_cev);
   d.f_tot = (uint32_t *)(b + L.f_tot);
   d.f_acc = (unsigned long long *)(b + L.f_acc);
+  d.f_tie_val = (unsigned long long *)(b + L.f_tie_val);
+  d.f_tie_flag = (unsigned int *)(b + L.f_tie_flag);
+  d.wb_bytes = (uint32_t *)(b + L.wb_bytes);
   d.f_sk2 = (uint32_t *)(b + L.f_sk2);
   d.f_sv2 = (uint32_t *)(b + L.f_sv2);
   d.f_sk3 = (uint32_t *)(b + L.f_sk3);
   d.f_sv3 = (uint32_t *)(b + L.f_sv3);
   d.f_bar = (unsigned int *)(b + L.f_bar);
+  d.f_prof = (unsigned long long *)(b + L.f_prof);
   return d;
 }
 
@@ -225,6 +227,7 @@ struct scalesim_ctx {
   int fused_grid = 0;
   uint64_t fused_steps = 0;
   bool deferred = false;  // score deferred into the fused plan kernel
+  bool last_fused = false;
   int64_t deferred_now = 0;
 };
 
@@ -298,6 +301,10 @@ extern "C" scalesim_status scalesim_nccl_unique_id(void *out128) {
 extern "C" uint64_t scalesim_launch_count(const scalesim_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
 extern "C" int scalesim_fused(const scalesim_ctx *ctx) { return ctx ? (ctx->fused ? 1 : 0) : -1; }
+
+extern "C" const uint64_t *scalesim_profile_stamps(const scalesim_ctx *ctx) {
+  return ctx ? reinterpret_cast<const uint64_t *>(ctx->p.d.f_prof) : nullptr;
+}
 
 extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scalesim_tables *t, scalesim_ctx **out) {
   if (!out) return SCALESIM_E_INVALID;
@@ -396,9 +403,27 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
     }
   }
   if (transfer && pf[t->n_blocks] != t->n_block_pages) return fail(SCALESIM_E_INVALID);
+  // per-agent write-back bytes (KV + HIST blocks, R13) for the fused path's d2h accounting
+  std::vector<uint32_t> wb(n_local ? n_local : 1, 0);
+  if (t->n_blocks > 0) {
+    std::vector<uint32_t> bs(t->n_blocks);
+    std::vector<uint8_t> bk(t->n_blocks);
+    if (cudaMemcpy(bs.data(), t->blk_size, 4 * t->n_blocks, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(bk.data(), t->blk_kind, t->n_blocks, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(SCALESIM_E_CUDA);
+    for (uint64_t a = 0; a < n_local; ++a) {
+      uint64_t s = 0;
+      for (uint64_t b = bp[a]; b < bp[a + 1]; ++b)
+        if (bk[b] != 0) s += bs[b];
+      if (s > 0xFFFFFFFFull) return fail(SCALESIM_E_INVALID);
+      wb[a] = (uint32_t)s;
+    }
+  }
   if (cudaMemsetAsync(t->workspace, 0, L.total, c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
   if (cudaMemcpyAsync(p.d.page_first, pf.data(), 8 * (t->n_blocks + 1), cudaMemcpyHostToDevice, c->stream) !=
       cudaSuccess)
+    return fail(SCALESIM_E_CUDA);
+  if (cudaMemcpyAsync(p.d.wb_bytes, wb.data(), 4 * wb.size(), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
     return fail(SCALESIM_E_CUDA);
   c->launches += launch_init_pages(p, t->resident_init, c->stream);
   c->launches += launch_mask_tail(p, c->stream);
@@ -445,8 +470,8 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
       c->fused = true;
       c->fused_tile = tile;
       c->fused_grid = sms;
-      if (cudaMemsetAsync(p.d.f_mm1, 0xFF, 4 * 2 * 4096, c->stream) != cudaSuccess ||
-          cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2048, c->stream) != cudaSuccess)
+      if (cudaMemsetAsync(p.d.f_mm1, 0xFF, 4 * 2 * 2 * 4096, c->stream) != cudaSuccess ||
+          cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2 * 1024, c->stream) != cudaSuccess)
         return fail(SCALESIM_E_CUDA);
     }
   }
@@ -520,11 +545,12 @@ extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *ou
   Params &p = c->p;
   const bool multi = c->cfg.world > 1;
   if (c->deferred) {
-    c->launches += launch_fused_plan(p, c->deferred_now, (int)(c->fused_steps & 1), c->fused_grid, c->fused_tile,
-                                     p.d.f_bar, c->stream);
+    c->launches += launch_fused_plan(p, c->deferred_now, (int)(c->fused_steps & 1),
+                                     (unsigned int)(c->fused_steps + 1), c->fused_grid, c->fused_tile, c->stream);
     CK(cudaGetLastError());
     c->fused_steps++;
     c->deferred = false;
+    c->last_fused = true;
     return finish_plan(c, out);
   }
   if (multi) {
@@ -557,6 +583,7 @@ extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *ou
     c->launches += launch_fix_kept(p, c->stream);
   }
   c->launches += launch_lists(p, c->stream);
+  c->last_fused = false;
   return finish_plan(c, out);
 }
 
@@ -569,7 +596,9 @@ static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out) {
     CK(cudaStreamWaitEvent(c->stream, c->ev_xfer[buf], 0));
     if (buf == c->last_buf) c->xfer_pending = false;
   }
-  c->launches += launch_expand(p, c->stream);  // byte accounting always; pages only with transfer
+  // byte accounting (multi-kernel path) and page assignment (transfers); the fused kernel
+  // accounts the write-back bytes itself
+  if (c->transfer || !c->last_fused) c->launches += launch_expand(p, c->stream);
   CK(cudaEventRecord(c->ev_plan, c->stream));
   if (!c->fused || p.n_kin > 0 || c->cfg.world > 1)
     c->launches += launch_plan_init(p, c->stream);  // clear the multi-kernel accumulators for the next step

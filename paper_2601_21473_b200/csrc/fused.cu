@@ -1,26 +1,28 @@
-// fused.cu — one persistent cooperative kernel per planning step (world == 1).
+// fused.cu — one persistent kernel per planning step (world == 1).
 //
-// One CTA per SM (1024 threads); CTA c owns the contiguous agent tile [c*T, (c+1)*T), so
-// CTA order is id order.  Phases, separated by grid barriers (cooperative launch):
-//   P1  score the tile (a1, a2): 128-bit record loads, distance, eligibility; keys stay in
-//       shared memory; byte-weighted level-1 histogram of the distance bits [30:20] with
-//       per-bucket min/max key -> published per CTA (dense) and summed globally (atomics)
-//   --- barrier
-//   P2  every CTA resolves the boundary distance D* redundantly from the global histogram
-//       (a3; levels 2/3 of the radix select, each behind a barrier, only when the boundary
-//       bucket holds several distances)
-//   P3  exclusive prefix of the tie-group bytes over the preceding CTAs, read from the
-//       published per-CTA histograms (no extra barrier)
-//   P4  emit (a4, a5): kept bits, new residency, byte totals; per-CTA counts of the
-//       prefetch / evict members per level-1 bucket, published (dense) + global totals
-//   --- barrier
-//   P5  bucket (counting) sort of the lists: position = bucket start + members of the same
-//       bucket in preceding CTAs + in-CTA id-order rank -> lists sorted by (bucket, id)
-//   --- barrier (only when a list has members in a bucket holding several distances)
-//   P6  each such segment is stably re-sorted by the full distance key by one CTA
-//
-// Every decision uses the same definitions as the multi-kernel path (kernels.cu), DESIGN.md
-// §3; the two paths give bit-identical plans (tests/test_gpu_parity.py runs both).
+// One CTA per SM (1024 threads, co-residency checked at init); CTA c owns the contiguous
+// agent tile [c*T, (c+1)*T), so CTA order is id order.  Phases:
+//   P1  score the tile (a1, a2): batched 128-bit record loads, distance, eligibility; keys,
+//       footprints and residency/eligibility/dirty bits stay in shared memory; byte-weighted
+//       histogram of distance bits [30:19] (4096 buckets) with per-bucket min/max key, added
+//       to the global histogram with atomics
+//   --- grid barrier
+//   P2  every CTA resolves the boundary distance D* from the global histogram (a3); levels
+//       2 ([18:9]) and 3 ([8:0]) run, each behind a barrier, only when the boundary bucket
+//       holds several distances
+//   P3  tie group: each CTA publishes its bytes at d == D*, then sums the preceding CTAs'
+//       values (per-CTA flags tagged with the launch epoch: no barrier)
+//   P4  emit (a4, a5): kept bits, new residency words, byte totals; per-CTA member counts of
+//       the two lists per 1024-bucket of distance bits [30:21] (dense rows) + global totals
+//   --- grid barrier
+//   P5  stable bucket sort of the lists: slot = bucket start + members of that bucket in the
+//       preceding CTAs (prefetch: ascending id) or following CTAs (evict: descending id) +
+//       in-CTA rank
+//   --- grid barrier (only when a list bucket holds several distances)
+//   P6  such segments are re-sorted by (distance, id) — stable rank sort in shared memory
+//       for short segments, radix sort otherwise — one CTA per segment
+// Decisions follow DESIGN.md §3 exactly as the multi-kernel path (kernels.cu) does; both give
+// bit-identical plans (tests/test_gpu_parity.py runs both).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,11 +33,25 @@ namespace ss {
 
 constexpr int FT = 1024;  // threads per CTA
 constexpr int FWARPS = FT / 32;
+constexpr int NB1 = 4096;  // level-1 buckets: distance bits [30:19]
+constexpr int NBL = 1024;  // list-sort buckets: distance bits [30:21]
+constexpr int LOAD_BATCH = 8;  // records in flight per thread in P1
 
-// Grid barrier for a grid of co-resident CTAs (one per SM, checked with the occupancy API
-// at init).  bar counts arrivals monotonically within one launch; the k-th barrier waits for
-// k * gridDim.x arrivals.  Launch L uses bar[L & 1]; launch L-1 reset it (same stream, so
-// every CTA of launch L-2 had finished).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid barrier for a grid of co-resident CTAs.  bar counts arrivals within one launch; the
+// k-th barrier waits for k * gridDim.x arrivals.  Launch L uses bar[L & 1]; launch L-1 reset it
+// (same stream, so every CTA of launch L-2 had finished).
 struct GridBar {
   unsigned int *bar;
   unsigned int k;
@@ -46,11 +62,7 @@ struct GridBar {
       __threadfence();
       atomicAdd(bar, 1u);
       const unsigned int target = k * gridDim.x;
-      unsigned int v;
-      while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-        if (v >= target) break;
-        __nanosleep(20);
+      while (ld_acquire(bar) < target) {
       }
       __threadfence();
     }
@@ -62,18 +74,18 @@ struct FusedArgs {
   Params p;
   int64_t now;
   int parity;
-  unsigned int *bar;  // [2] barrier counters
-  uint32_t tile;   // agents per CTA, multiple of 32
-  uint32_t tw;     // tile / 32
+  unsigned int epoch;  // launch number (>= 1), tags the per-CTA tie flags
+  uint32_t tile;       // agents per CTA, multiple of 32
+  uint32_t tw;         // tile / 32
 };
 
 // dynamic shared memory carve-up
 struct FSmem {
-  uint32_t *keys;    // [tile] distance bits of the tile's agents
-  uint32_t *memb;    // [tile] member list scratch (ids local to the tile) / sort scratch
-  uint32_t *old_w, *elig_w, *pf_w, *ev_w;  // [tw]
-  uint32_t *h_lo, *h_hi, *h_min, *h_nmax;  // [2048] histogram (16-bit halves of bytes)
-  unsigned long long *scratch;             // [64]
+  uint32_t *keys;  // [tile] distance bits
+  uint32_t *fp;    // [tile] footprint bytes; P5: in-CTA ranks
+  uint32_t *memb;  // [tile] scratch: word prefixes (u64), member lists, sort buffers
+  uint32_t *old_w, *elig_w, *dirty_w, *pf_w, *ev_w;  // [tw]
+  uint32_t *h;     // [4 * NB1]: histogram lo/hi/min/nmax, later list counters and starts
 };
 
 __device__ __forceinline__ FSmem carve(uint8_t *base, uint32_t tile, uint32_t tw) {
@@ -81,62 +93,55 @@ __device__ __forceinline__ FSmem carve(uint8_t *base, uint32_t tile, uint32_t tw
   uint32_t *w = reinterpret_cast<uint32_t *>(base);
   s.keys = w;
   w += tile;
+  s.fp = w;
+  w += tile;
   s.memb = w;
   w += tile;
   s.old_w = w;
   w += tw;
   s.elig_w = w;
   w += tw;
+  s.dirty_w = w;
+  w += tw;
   s.pf_w = w;
   w += tw;
   s.ev_w = w;
   w += tw;
-  s.h_lo = w;
-  w += 2048;
-  s.h_hi = w;
-  w += 2048;
-  s.h_min = w;
-  w += 2048;
-  s.h_nmax = w;
-  w += 2048;
-  uintptr_t a = (reinterpret_cast<uintptr_t>(w) + 15) & ~uintptr_t(15);
-  s.scratch = reinterpret_cast<unsigned long long *>(a);
+  s.h = w;
   return s;
 }
 
 size_t fused_smem_bytes(uint32_t tile) {
   const uint32_t tw = tile / 32;
-  return (size_t)4 * (2 * tile + 4 * tw + 4 * 2048) + 16 + 64 * 8;
+  return (size_t)4 * (3 * tile + 5 * tw + 4 * NB1);
 }
 
-__device__ __forceinline__ void clear_hist(const FSmem &s, int nb) {
+__device__ __forceinline__ void clear_hist(uint32_t *h, int nb) {
   for (int b = threadIdx.x; b < nb; b += FT) {
-    s.h_lo[b] = 0;
-    s.h_hi[b] = 0;
-    s.h_min[b] = 0xFFFFFFFFu;
-    s.h_nmax[b] = 0xFFFFFFFFu;
+    h[b] = 0;
+    h[nb + b] = 0;
+    h[2 * nb + b] = 0xFFFFFFFFu;
+    h[3 * nb + b] = 0xFFFFFFFFu;
   }
 }
 
 // one lane's contribution to the byte-weighted histogram (native 32-bit shared atomics)
-__device__ __forceinline__ void hist_lane(const FSmem &s, uint32_t b, uint32_t bits, uint32_t bytes) {
-  atomicAdd(&s.h_lo[b], bytes & 0xFFFFu);
-  atomicAdd(&s.h_hi[b], bytes >> 16);
-  atomicMin(&s.h_min[b], bits);
-  atomicMin(&s.h_nmax[b], ~bits);
+__device__ __forceinline__ void hist_lane(uint32_t *h, int nb, uint32_t b, uint32_t bits, uint32_t bytes) {
+  atomicAdd(&h[b], bytes & 0xFFFFu);
+  atomicAdd(&h[nb + b], bytes >> 16);
+  atomicMin(&h[2 * nb + b], bits);
+  atomicMin(&h[3 * nb + b], ~bits);
 }
 
-// publish this CTA's histogram (dense, for the tie prefix) and add it to the global one
-__device__ __forceinline__ void publish_hist(const FSmem &s, int nb, unsigned long long *cta_row,
-                                             unsigned long long *g_hist, uint32_t *g_mm) {
+// add this CTA's histogram to the global one (nonzero buckets only)
+__device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned long long *g_hist, uint32_t *g_mm) {
   for (int b = threadIdx.x; b < nb; b += FT) {
-    const unsigned long long v = ((unsigned long long)s.h_hi[b] << 16) + s.h_lo[b];
-    cta_row[b] = v;
+    const unsigned long long v = ((unsigned long long)h[nb + b] << 16) + h[b];
     if (v != 0) {
       atomicAdd(&g_hist[b], v);
       if (g_mm) {
-        atomicMin(&g_mm[b], s.h_min[b]);
-        atomicMin(&g_mm[nb + b], s.h_nmax[b]);
+        atomicMin(&g_mm[b], h[2 * nb + b]);
+        atomicMin(&g_mm[nb + b], h[3 * nb + b]);
       }
     }
   }
@@ -145,46 +150,44 @@ __device__ __forceinline__ void publish_hist(const FSmem &s, int nb, unsigned lo
 struct Sel {
   uint32_t prefix;
   unsigned long long below, rem;
-  uint32_t dstar, all_fit, done, level_res, b_res;
+  uint32_t dstar, all_fit, done;
 };
 
-// Find the boundary bucket of histogram level `level` (every CTA computes the same result).
-__device__ void select_level(const FSmem &s, const unsigned long long *g_hist, const uint32_t *g_mm, int level,
+// Boundary bucket of histogram level `level` (every CTA computes the same result).
+__device__ void select_level(const unsigned long long *g_hist, const uint32_t *g_mm, int level,
                              unsigned long long budget, Sel &sel) {
-  const int nb = level == 1 ? 2048 : 1024;
-  const int shift = level == 1 ? 20 : (level == 2 ? 10 : 0);
-  const int per = nb / FT;  // 2 or 1
-  unsigned long long *sh = s.scratch;
+  const int nb = level == 1 ? NB1 : (level == 2 ? 1024 : 512);
+  const int shift = level == 1 ? 19 : (level == 2 ? 9 : 0);
+  const int per = nb / FT;  // 4, 1 or 0 (level 3: threads < 512)
   __shared__ unsigned long long sh_tot, sh_prev;
   __shared__ uint32_t sh_b;
   if (threadIdx.x == 0) sh_b = 0xFFFFFFFFu;
+  unsigned long long hv[4] = {0, 0, 0, 0};
   unsigned long long loc = 0;
-  unsigned long long hv[2];
-  for (int k = 0; k < per; ++k) {
-    hv[k] = g_hist[threadIdx.x * per + k];
+  const int mine = per > 0 ? per : ((int)threadIdx.x < nb ? 1 : 0);
+  const int b0 = per > 0 ? threadIdx.x * per : threadIdx.x;
+  for (int k = 0; k < mine; ++k) {
+    hv[k] = g_hist[b0 + k];
     loc += hv[k];
   }
   const unsigned long long ex = block_excl_scan<unsigned long long, FT>(loc, &sh_tot);
   __syncthreads();
   unsigned long long run = sel.below + ex;
-  for (int k = 0; k < per; ++k) {
+  for (int k = 0; k < mine; ++k) {
     const unsigned long long prev = run;
     run += hv[k];
-    if (run > budget && prev <= budget) {
-      sh_b = threadIdx.x * per + k;
+    if (run > budget && prev <= budget) {  // exactly one bucket crosses (sums are monotone)
+      sh_b = b0 + k;
       sh_prev = prev;
     }
   }
   __syncthreads();
   const uint32_t b = sh_b;
-  (void)sh;
   if (b == 0xFFFFFFFFu) {  // level 1 only: every eligible agent fits
     sel.all_fit = 1;
     sel.done = 1;
     sel.dstar = 0xFFFFFFFFu;
     sel.rem = budget - (sel.below + sh_tot);
-    sel.level_res = level;
-    sel.b_res = 0;
   } else {
     sel.below = sh_prev;
     sel.prefix |= b << shift;
@@ -193,18 +196,46 @@ __device__ void select_level(const FSmem &s, const unsigned long long *g_hist, c
       sel.dstar = (level == 3) ? sel.prefix : g_mm[b];
       sel.rem = budget - sel.below;
       sel.done = 1;
-      sel.level_res = level;
-      sel.b_res = b;
     }
   }
   __syncthreads();
 }
 
-// Stable LSD radix sort of n (key, id) pairs by key (ascending) for one CTA.  Buffers may
-// be shared or global memory (generic pointers).  Digits [0,11) [11,22) [22,32); constant
-// digits are skipped.  Result in (ka, ia).
+// Stable sort of a segment of n (key, id) pairs by key, ascending, for one CTA.
+// n <= 2048: rank sort in place (rank = #smaller keys + #equal keys before).
+// Larger: LSD radix sort (digits [0,11) [11,22) [22,32), constant digits skipped) on the
+// caller's buffers (shared or global), warp-serialised stable scatter.  Result in (ka, ia).
 __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_t *ib, uint32_t n, uint32_t *cnt) {
-  __shared__ uint32_t sh_or, sh_and;
+  if (n <= 1) return;
+  if (n <= 2 * FT) {
+    uint32_t k0 = 0, k1 = 0, i0 = 0, i1 = 0, r0 = 0, r1 = 0;
+    const uint32_t e0 = threadIdx.x, e1 = threadIdx.x + FT;
+    if (e0 < n) {
+      k0 = ka[e0];
+      i0 = ia[e0];
+    }
+    if (e1 < n) {
+      k1 = ka[e1];
+      i1 = ia[e1];
+    }
+    for (uint32_t j = 0; j < n; ++j) {
+      const uint32_t kj = ka[j];
+      r0 += (kj < k0) || (kj == k0 && j < e0);
+      r1 += (kj < k1) || (kj == k1 && j < e1);
+    }
+    __syncthreads();
+    if (e0 < n) {
+      ka[r0] = k0;
+      ia[r0] = i0;
+    }
+    if (e1 < n) {
+      ka[r1] = k1;
+      ia[r1] = i1;
+    }
+    __syncthreads();
+    return;
+  }
+  __shared__ uint32_t sh_or, sh_and, sh_tot;
   if (threadIdx.x == 0) {
     sh_or = 0;
     sh_and = 0xFFFFFFFFu;
@@ -223,7 +254,7 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
   }
   __syncthreads();
   const uint32_t varying = sh_or ^ sh_and;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5;
   for (int pass = 0; pass < 3; ++pass) {
     const int shift = pass == 0 ? 0 : (pass == 1 ? 11 : 22);
     const uint32_t mask = pass == 2 ? 0x3FFu : 0x7FFu;
@@ -232,10 +263,9 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
     __syncthreads();
     for (uint32_t e = threadIdx.x; e < n; e += FT) atomicAdd(&cnt[(ka[e] >> shift) & mask], 1u);
     __syncthreads();
-    {  // exclusive scan of the 2048 counters, 2 per thread
-      __shared__ uint32_t tot;
+    {
       const uint32_t c0 = cnt[2 * threadIdx.x], c1 = cnt[2 * threadIdx.x + 1];
-      const uint32_t ex = block_excl_scan<uint32_t, FT>(c0 + c1, &tot);
+      const uint32_t ex = block_excl_scan<uint32_t, FT>(c0 + c1, &sh_tot);
       __syncthreads();
       cnt[2 * threadIdx.x] = ex;
       cnt[2 * threadIdx.x + 1] = ex + c0;
@@ -261,79 +291,94 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
         __syncthreads();
       }
     }
-    __syncthreads();
-    uint32_t *t;
-    t = ka; ka = kb; kb = t;
-    t = ia; ia = ib; ib = t;
-    // keep the caller's view: results must end in the original (ka, ia) buffers
-    for (uint32_t e = threadIdx.x; e < n; e += FT) {
-      kb[e] = ka[e];
-      ib[e] = ia[e];
+    for (uint32_t e = threadIdx.x; e < n; e += FT) {  // back into (ka, ia)
+      ka[e] = kb[e];
+      ia[e] = ib[e];
     }
     __syncthreads();
-    t = ka; ka = kb; kb = t;
-    t = ia; ia = ib; ib = t;
   }
-  (void)lane;
 }
 
 __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
-  GridBar grid{A.bar + A.parity, 0u};
-  if (blockIdx.x == 0 && threadIdx.x == 0) A.bar[A.parity ^ 1] = 0u;  // for launch L+1
   const Params &p = A.p;
   const Dev &d = p.d;
+  GridBar grid{d.f_bar + A.parity, 0u};
+  unsigned long long *prof = d.f_prof;
+  if (threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    atomicMin(&prof[0], t);
+    if (blockIdx.x == 0) prof[2] = t;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.f_bar[A.parity ^ 1] = 0u;  // for launch L+1
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const FSmem s = carve(smem_raw, A.tile, A.tw);
   const uint32_t c = blockIdx.x, G = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = (uint64_t)c * A.tile;
-  const uint32_t n_here = base >= p.n_local ? 0u : (uint32_t)((p.n_local - base) < A.tile ? (p.n_local - base) : A.tile);
+  const uint32_t n_here =
+      base >= p.n_local ? 0u : (uint32_t)((p.n_local - base) < A.tile ? (p.n_local - base) : A.tile);
   const uint32_t tw_here = (n_here + 31) / 32;
   const int par = A.parity;
-  unsigned long long *acc = d.f_acc + 8 * par;  // [0] zero bytes [1] h2d [2] d2h [3] tie kept [4] n_elig [5] status
+  // accumulators of this launch: [0] zero-distance bytes [1] h2d [2] d2h [3] tie kept
+  // [4] eligible agents [5] status
+  unsigned long long *acc = d.f_acc + 8 * par;
   const uint32_t *bm_old = d.bm[p.cur];
   uint32_t *bm_new = d.bm[p.cur ^ 1];
 
   // ---------------- P1: score + level-1 histogram
-  clear_hist(s, 2048);
+  clear_hist(s.h, NB1);
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_old[base / 32 + w] : 0u;
   __syncthreads();
   uint32_t st = 0;
   unsigned long long zero_b = 0;
-  for (uint32_t k = threadIdx.x; k < A.tw * 32; k += FT) {
-    const bool valid = k < n_here;
-    const uint64_t i = base + k;
-    uint4 r = make_uint4(0, 0, 0, 0);
-    if (valid) r = ld_stream(p.rec + i);
-    const bool res = (s.old_w[k >> 5] >> (k & 31)) & 1u;
-    const float dist = valid ? distance_of(r, A.now, p.hop_scale, d.dint, p.n_kin, st) : 0.0f;
-    const uint32_t bits = __float_as_uint(dist);
-    const bool elig = valid && (res || dist == 0.0f || dist < theta_of(p, class_of(r)));
-    s.keys[k] = bits;
-    if (valid) d.keys[i] = bits;
-    const uint32_t eb = __ballot_sync(0xFFFFFFFFu, elig);
-    if (lane == 0) s.elig_w[k >> 5] = eb;
-    if (elig) hist_lane(s, bits >> 20, bits, r.y);
-    if (valid && dist == 0.0f) zero_b += r.y;
+  for (uint32_t k0 = 0; k0 < A.tw * 32; k0 += LOAD_BATCH * FT) {
+    uint4 r[LOAD_BATCH];
+#pragma unroll
+    for (int j = 0; j < LOAD_BATCH; ++j) {  // all loads in flight before any use
+      const uint32_t k = k0 + j * FT + threadIdx.x;
+      r[j] = k < n_here ? ld_stream(p.rec + base + k) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < LOAD_BATCH; ++j) {
+      const uint32_t k = k0 + j * FT + threadIdx.x;
+      if (k0 + j * FT >= A.tw * 32) break;  // uniform
+      const bool valid = k < n_here;
+      const bool res = (s.old_w[k >> 5] >> (k & 31)) & 1u;
+      const float dist = valid ? distance_of(r[j], A.now, p.hop_scale, d.dint, p.n_kin, st) : 0.0f;
+      const uint32_t bits = __float_as_uint(dist);
+      const bool elig = valid && (res || dist == 0.0f || dist < theta_of(p, class_of(r[j])));
+      s.keys[k] = bits;
+      s.fp[k] = r[j].y;
+      if (valid) d.keys[base + k] = bits;
+      const uint32_t eb = __ballot_sync(0xFFFFFFFFu, elig);
+      const uint32_t db = __ballot_sync(0xFFFFFFFFu, valid && ((r[j].z >> 4) & 1u));
+      if (lane == 0) {
+        s.elig_w[k >> 5] = eb;
+        s.dirty_w[k >> 5] = db;
+      }
+      if (elig) hist_lane(s.h, NB1, bits >> 19, bits, r[j].y);
+      if (valid && dist == 0.0f) zero_b += r[j].y;
+    }
   }
   __syncthreads();
-  publish_hist(s, 2048, d.f_cta_h1 + (uint64_t)c * 2048, d.f_hist1 + 2048 * par, d.f_mm1 + 4096 * par);
+  publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, d.f_mm1 + 2 * NB1 * par);
   zero_b = block_sum<unsigned long long, FT>(zero_b);
   st = __reduce_or_sync(0xFFFFFFFFu, st);
   if (lane == 0 && st) atomicOr(reinterpret_cast<unsigned int *>(&acc[5]), st);
   if (threadIdx.x == 0 && zero_b) atomicAdd(&acc[0], zero_b);
+  if (c == 0 && threadIdx.x == 0) prof[3] = gtimer();
   grid.sync();
+  if (c == 0 && threadIdx.x == 0) prof[4] = gtimer();
 
   // ---------------- P2: select
-  if (c == 0) {  // clear the other parity's accumulators for the next step
+  if (c == 0) {  // clear the other parity's accumulators for the next launch
     const int q = par ^ 1;
-    for (int b = threadIdx.x; b < 2048; b += FT) {
-      d.f_hist1[2048 * q + b] = 0;
-      d.f_mm1[4096 * q + b] = 0xFFFFFFFFu;
-      d.f_mm1[4096 * q + 2048 + b] = 0xFFFFFFFFu;
-      d.f_tot[4096 * q + b] = 0;
-      d.f_tot[4096 * q + 2048 + b] = 0;
+    for (int b = threadIdx.x; b < NB1; b += FT) {
+      d.f_hist1[NB1 * q + b] = 0;
+      d.f_mm1[2 * NB1 * q + b] = 0xFFFFFFFFu;
+      d.f_mm1[2 * NB1 * q + NB1 + b] = 0xFFFFFFFFu;
     }
+    for (int b = threadIdx.x; b < 2 * NBL; b += FT) d.f_tot[2 * NBL * q + b] = 0;
     for (int b = threadIdx.x; b < 1024; b += FT) {
       d.f_hist2[1024 * q + b] = 0;
       d.f_hist3[1024 * q + b] = 0;
@@ -342,85 +387,94 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     }
     if (threadIdx.x < 8) d.f_acc[8 * q + threadIdx.x] = 0;
   }
-  Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 0, 0};
-  select_level(s, d.f_hist1 + 2048 * par, d.f_mm1 + 4096 * par, 1, p.budget, sel);
+  Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0};
+  select_level(d.f_hist1 + NB1 * par, d.f_mm1 + 2 * NB1 * par, 1, p.budget, sel);
   for (int level = 2; level <= 3 && !sel.done; ++level) {
-    const int hi_shift = level == 2 ? 20 : 10, shift = level == 2 ? 10 : 0;
+    const int hi_shift = level == 2 ? 19 : 9, shift = level == 2 ? 9 : 0;
+    const int nb = level == 2 ? 1024 : 512;
     const uint32_t want = sel.prefix >> hi_shift;
-    clear_hist(s, 1024);
+    clear_hist(s.h, nb);
     __syncthreads();
     for (uint32_t k = threadIdx.x; k < n_here; k += FT) {
       const uint32_t bits = s.keys[k];
       if (((s.elig_w[k >> 5] >> (k & 31)) & 1u) && (bits >> hi_shift) == want)
-        hist_lane(s, (bits >> shift) & 1023u, bits, p.rec[base + k].y);
+        hist_lane(s.h, nb, (bits >> shift) & (nb - 1), bits, s.fp[k]);
     }
     __syncthreads();
     unsigned long long *gh = level == 2 ? d.f_hist2 + 1024 * par : d.f_hist3 + 1024 * par;
     uint32_t *gm = level == 2 ? d.f_mm2 + 2048 * par : nullptr;
-    publish_hist(s, 1024, (level == 2 ? d.f_cta_h2 : d.f_cta_h3) + (uint64_t)c * 1024, gh, gm);
+    publish_hist(s.h, nb, gh, gm);
     grid.sync();
-    select_level(s, gh, gm, level, p.budget, sel);
+    select_level(gh, gm, level, p.budget, sel);
   }
+  const bool all_fit = sel.all_fit;
+  const uint32_t dstar = sel.dstar;
 
-  // ---------------- P3: tie-group prefix over the preceding CTAs
-  __shared__ unsigned long long sh_tie_excl;
-  if (warp == 0) {
-    unsigned long long t = 0;
-    if (!sel.all_fit) {
-      const unsigned long long *col = sel.level_res == 1 ? d.f_cta_h1 : (sel.level_res == 2 ? d.f_cta_h2 : d.f_cta_h3);
-      const uint32_t stride = sel.level_res == 1 ? 2048 : 1024;
-      for (uint32_t q = lane; q < c; q += 32) t += col[(uint64_t)q * stride + sel.b_res];
+  // ---------------- P3: tie group — this CTA's bytes at d == D*, prefix over preceding CTAs
+  unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw]
+  for (uint32_t w = warp; w < A.tw; w += FWARPS) {
+    const uint32_t k = w * 32 + lane;
+    const bool tie = !all_fit && ((s.elig_w[w] >> lane) & 1u) && s.keys[k] == dstar;
+    unsigned long long v = tie ? s.fp[k] : 0u;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) word_tie[w] = v;
+  }
+  __syncthreads();
+  __shared__ unsigned long long sh_tie_excl, sh_tie_total, sh_chunk;
+  {  // exclusive scan over the tile's words
+    unsigned long long carry = 0;
+    for (uint32_t w0 = 0; w0 < A.tw; w0 += FT) {
+      const uint32_t w = w0 + threadIdx.x;
+      const unsigned long long v = w < A.tw ? word_tie[w] : 0ull;
+      const unsigned long long ex = block_excl_scan<unsigned long long, FT>(v, &sh_chunk);
+      __syncthreads();
+      if (w < A.tw) word_tie[w] = carry + ex;
+      carry += sh_chunk;
+      __syncthreads();
     }
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
-    if (lane == 0) sh_tie_excl = t;
+    if (threadIdx.x == 0) sh_tie_total = carry;
+  }
+  __syncthreads();
+  if (!all_fit) {
+    if (threadIdx.x == 0) {  // publish: value, then the epoch flag (release)
+      d.f_tie_val[c] = sh_tie_total;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(d.f_tie_flag + c), "r"(A.epoch) : "memory");
+    }
+    if (warp == 0) {
+      unsigned long long t = 0;
+      for (uint32_t q = lane; q < c; q += 32) {
+        while (ld_acquire(d.f_tie_flag + q) != A.epoch) {
+        }
+        t += *(volatile unsigned long long *)(d.f_tie_val + q);
+      }
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+      if (lane == 0) sh_tie_excl = t;
+    }
+  } else if (threadIdx.x == 0) {
+    sh_tie_excl = 0;
   }
   __syncthreads();
 
   // ---------------- P4: emit
-  // tie bytes per word (id order), then word-level exclusive scan
-  const bool all_fit = sel.all_fit;
-  const uint32_t dstar = sel.dstar;
-  uint32_t *word_tie = s.memb;  // [tw] scratch (u32 is enough? bytes per word can exceed 2^32: use 2 words)
-  unsigned long long *word_tie64 = reinterpret_cast<unsigned long long *>(s.memb);
-  for (uint32_t w = warp; w < A.tw; w += FWARPS) {
-    const uint32_t k = w * 32 + lane;
-    const bool tie = !all_fit && ((s.elig_w[w] >> lane) & 1u) && s.keys[k] == dstar && k < n_here;
-    const uint32_t fp = tie ? p.rec[base + k].y : 0u;
-    unsigned long long v = fp;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    if (lane == 0) word_tie64[w] = v;
-  }
-  (void)word_tie;
+  uint32_t *cnt_pf = s.h, *cnt_ev = s.h + NBL;  // per-CTA list members per list bucket
+  for (int b = threadIdx.x; b < 2 * NBL; b += FT) s.h[b] = 0;
   __syncthreads();
-  {  // exclusive scan over the tile's words (tw <= 1024*? ; loop in chunks of FT)
-    __shared__ unsigned long long tot;
-    unsigned long long carry = 0;
-    for (uint32_t w0 = 0; w0 < A.tw; w0 += FT) {
-      const uint32_t w = w0 + threadIdx.x;
-      const unsigned long long v = w < A.tw ? word_tie64[w] : 0ull;
-      const unsigned long long ex = block_excl_scan<unsigned long long, FT>(v, &tot);
-      __syncthreads();
-      if (w < A.tw) word_tie64[w] = carry + ex;
-      carry += tot;
-      __syncthreads();
-    }
-  }
   unsigned long long h2d = 0, d2h = 0, tie_kept = 0;
   uint32_t n_el = 0;
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
-    const bool valid = k < n_here;
-    const bool el = (s.elig_w[w] >> lane) & 1u;
+    const bool el = (s.elig_w[w] >> lane) & 1u;  // 0 beyond n_here
     const uint32_t key = s.keys[k];
-    const bool tie = valid && el && !all_fit && key == dstar;
-    const uint32_t fp = tie ? p.rec[base + k].y : 0u;
-    unsigned long long incl = fp;
+    const bool tie = el && !all_fit && key == dstar;
+    const uint32_t fp = s.fp[k];
+    unsigned long long incl = tie ? fp : 0u;
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
       if (lane >= o) incl += t;
     }
-    incl += sh_tie_excl + word_tie64[w];
-    const bool kept = valid && el && (all_fit || key < dstar || (tie && incl <= sel.rem));
+    incl += sh_tie_excl + word_tie[w];
+    const bool kept = el && (all_fit || key < dstar || (tie && incl <= sel.rem));
     if (tie && kept) tie_kept += fp;
     const uint32_t kw = __ballot_sync(0xFFFFFFFFu, kept);
     const uint32_t old = s.old_w[w];
@@ -431,32 +485,20 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
       s.ev_w[w] = evw;
       n_el += __popc(s.elig_w[w]);
     }
-    if ((pfw >> lane) & 1u) h2d += p.rec[base + k].y;
+    if ((pfw >> lane) & 1u) {
+      h2d += fp;
+      atomicAdd(&cnt_pf[key >> 21], 1u);
+    }
     if ((evw >> lane) & 1u) {
-      const uint4 r = p.rec[base + k];
-      if ((r.z >> 4) & 1u) {  // R13: KV + HIST blocks of a dirty evicted agent
-        for (uint64_t b = p.blk_ptr[base + k]; b < p.blk_ptr[base + k + 1]; ++b)
-          if (p.blk_kind[b] != 0) d2h += p.blk_size[b];
-      }
+      if ((s.dirty_w[w] >> lane) & 1u) d2h += d.wb_bytes[base + k];  // R13
+      atomicAdd(&cnt_ev[key >> 21], 1u);
     }
   }
   __syncthreads();
-  // list members per level-1 bucket (reuse the histogram arrays as counters)
-  for (int b = threadIdx.x; b < 2048; b += FT) {
-    s.h_lo[b] = 0;  // prefetch count
-    s.h_hi[b] = 0;  // evict count
-  }
-  __syncthreads();
-  for (uint32_t w = warp; w < A.tw; w += FWARPS) {
-    const uint32_t k = w * 32 + lane;
-    if ((s.pf_w[w] >> lane) & 1u) atomicAdd(&s.h_lo[s.keys[k] >> 20], 1u);
-    if ((s.ev_w[w] >> lane) & 1u) atomicAdd(&s.h_hi[s.keys[k] >> 20], 1u);
-  }
-  __syncthreads();
-  uint32_t *cpf = d.f_cta_cpf + (uint64_t)c * 2048, *cev = d.f_cta_cev + (uint64_t)c * 2048;
-  uint32_t *tot_pf = d.f_tot + 4096 * par, *tot_ev = d.f_tot + 4096 * par + 2048;
-  for (int b = threadIdx.x; b < 2048; b += FT) {
-    const uint32_t a = s.h_lo[b], e = s.h_hi[b];
+  uint32_t *cpf = d.f_cta_cpf + (uint64_t)c * NBL, *cev = d.f_cta_cev + (uint64_t)c * NBL;
+  uint32_t *tot_pf = d.f_tot + 2 * NBL * par, *tot_ev = d.f_tot + 2 * NBL * par + NBL;
+  for (int b = threadIdx.x; b < NBL; b += FT) {
+    const uint32_t a = cnt_pf[b], e = cnt_ev[b];
     cpf[b] = a;
     cev[b] = e;
     if (a) atomicAdd(&tot_pf[b], a);
@@ -472,76 +514,113 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     if (tie_kept) atomicAdd(&acc[3], tie_kept);
     if (n_el) atomicAdd(&acc[4], (unsigned long long)n_el);
   }
+  if (c == 0 && threadIdx.x == 0) prof[5] = gtimer();
   grid.sync();
+  if (c == 0 && threadIdx.x == 0) prof[6] = gtimer();
 
-  // ---------------- P5: bucket sort of the lists
-  // bucket starts (prefetch ascending buckets, evict descending buckets)
-  uint32_t *g_pf = s.h_min, *g_ev = s.h_nmax;  // [2048] starts
-  __shared__ uint32_t sh_npf, sh_nev;
+  // ---------------- P5: stable bucket sort of the lists
+  uint32_t *g_pf = s.h + 2 * NBL, *g_ev = s.h + 3 * NBL;  // first slot of this CTA's members per bucket
+  __shared__ uint32_t sh_npf, sh_nev, sh_mpf, sh_mev;
   {
-    const uint32_t a0 = tot_pf[2 * threadIdx.x], a1 = tot_pf[2 * threadIdx.x + 1];
-    const uint32_t ex = block_excl_scan<uint32_t, FT>(a0 + a1, &sh_npf);
-    g_pf[2 * threadIdx.x] = ex;
-    g_pf[2 * threadIdx.x + 1] = ex + a0;
-    // evict: scan over reversed bucket order r = 2047 - b
-    const uint32_t r0 = 2 * threadIdx.x, r1 = r0 + 1;
-    const uint32_t e0 = tot_ev[2047 - r0], e1 = tot_ev[2047 - r1];
-    const uint32_t exe = block_excl_scan<uint32_t, FT>(e0 + e1, &sh_nev);
-    g_ev[2047 - r0] = exe;
-    g_ev[2047 - r1] = exe + e0;
+    const uint32_t b = threadIdx.x;  // NBL == FT: one bucket per thread
+    const uint32_t a = tot_pf[b];
+    const uint32_t xa = block_excl_scan<uint32_t, FT>(a, &sh_npf);
+    g_pf[b] = xa;
+    const uint32_t rb = NBL - 1 - b;  // evict: descending buckets
+    const uint32_t e = tot_ev[rb];
+    const uint32_t xe = block_excl_scan<uint32_t, FT>(e, &sh_nev);
+    g_ev[rb] = xe;
   }
-  __syncthreads();
-  // preceding-CTA counts of the buckets this CTA has members in
-  for (int b = warp; b < 2048; b += FWARPS) {
-    const uint32_t mine_pf = s.h_lo[b], mine_ev = s.h_hi[b];
-    if (mine_pf == 0 && mine_ev == 0) continue;  // warp-uniform
-    uint32_t ppf = 0, pev = 0;
-    for (uint32_t q = lane; q < G; q += 32) {
-      if (mine_pf && q < c) ppf += d.f_cta_cpf[(uint64_t)q * 2048 + b];
-      if (mine_ev && q > c) pev += d.f_cta_cev[(uint64_t)q * 2048 + b];
+  {  // member counts of this CTA
+    uint32_t m_pf = 0, m_ev = 0;
+    for (uint32_t w = threadIdx.x; w < A.tw; w += FT) {
+      m_pf += __popc(s.pf_w[w]);
+      m_ev += __popc(s.ev_w[w]);
     }
-    ppf = __reduce_add_sync(0xFFFFFFFFu, ppf);
-    pev = __reduce_add_sync(0xFFFFFFFFu, pev);
-    if (lane == 0) {
-      g_pf[b] += ppf;  // now: first output slot of this CTA's members of bucket b
-      g_ev[b] += pev;
+    m_pf = block_sum<uint32_t, FT>(m_pf);
+    m_ev = block_sum<uint32_t, FT>(m_ev);
+    if (threadIdx.x == 0) {
+      sh_mpf = m_pf;
+      sh_mev = m_ev;
     }
   }
   __syncthreads();
-  // in-CTA ranks: warp 0 walks the prefetch members in ascending id order, warp 1 the
-  // evict members in descending id order
-  if (warp == 0) {
-    for (uint32_t w = 0; w < A.tw; ++w) {
-      const uint32_t m = s.pf_w[w];
-      if (m == 0) continue;
-      const bool on = (m >> lane) & 1u;
-      const uint32_t b = on ? (s.keys[w * 32 + lane] >> 20) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
-      if (on) {
-        const uint32_t pos = g_pf[b] + __popc(peers & lanemask_lt());
-        d.pf_ids[pos] = (uint32_t)(p.shard_begin + base + w * 32 + lane);
+  const uint32_t m_pf = sh_mpf, m_ev = sh_mev;
+  uint32_t *mem_pf = s.memb, *mem_ev = s.memb + m_pf;  // members in list order (tile-local indices)
+  {
+    uint32_t carry_pf = 0, carry_ev = 0;
+    __shared__ uint32_t t_pf, t_ev;
+    for (uint32_t w0 = 0; w0 < A.tw; w0 += FT) {
+      const uint32_t w = w0 + threadIdx.x;
+      const uint32_t a = w < A.tw ? __popc(s.pf_w[w]) : 0u, e = w < A.tw ? __popc(s.ev_w[w]) : 0u;
+      const uint32_t xa = block_excl_scan<uint32_t, FT>(a, &t_pf);
+      const uint32_t xe = block_excl_scan<uint32_t, FT>(e, &t_ev);
+      if (w < A.tw) {
+        uint32_t m = s.pf_w[w], o = carry_pf + xa;
+        while (m) {
+          const int bit = __ffs(m) - 1;
+          m &= m - 1;
+          mem_pf[o++] = w * 32 + bit;
+        }
+        m = s.ev_w[w];
+        o = m_ev - 1 - (carry_ev + xe);  // descending id
+        while (m) {
+          const int bit = __ffs(m) - 1;
+          m &= m - 1;
+          mem_ev[o--] = w * 32 + bit;
+        }
       }
-      __syncwarp();
-      if (on && (peers & lanemask_lt()) == 0) g_pf[b] += __popc(peers);
-      __syncwarp();
+      carry_pf += t_pf;
+      carry_ev += t_ev;
+      __syncthreads();
     }
-  } else if (warp == 1) {
-    for (uint32_t w = A.tw; w-- > 0;) {
-      const uint32_t m = s.ev_w[w];
-      if (m == 0) continue;
-      // descending id: lane j handles bit 31 - j
-      const uint32_t bit = 31 - lane;
-      const bool on = (m >> bit) & 1u;
-      const uint32_t b = on ? (s.keys[w * 32 + bit] >> 20) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
-      if (on) {
-        const uint32_t pos = g_ev[b] + __popc(peers & lanemask_lt());
-        d.ev_ids[pos] = (uint32_t)(p.shard_begin + base + w * 32 + bit);
+  }
+  __syncthreads();
+  // (a) warps 0/1: in-CTA rank of every member within its bucket (list order), into fp[]
+  // (b) other warps: members of the same bucket in the preceding (prefetch) / following
+  //     (evict) CTAs, added to the bucket starts
+  if (warp < 2) {
+    const uint32_t *mem = warp == 0 ? mem_pf : mem_ev;
+    const uint32_t m = warp == 0 ? m_pf : m_ev;
+    uint32_t *run = warp == 0 ? s.h : s.h + NBL;  // reuse the member counters as running ranks
+    for (uint32_t b = lane; b < NBL; b += 32) run[b] = 0;
+    __syncwarp();
+    for (uint32_t e0 = 0; e0 < m; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      const bool on = e < m;
+      const uint32_t bk = on ? (s.keys[mem[e]] >> 21) : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, bk);
+      uint32_t r = 0;
+      if (on) r = run[bk] + __popc(peers & lanemask_lt());
+      __syncwarp();
+      if (on && (peers & lanemask_lt()) == 0) run[bk] += __popc(peers);
+      __syncwarp();
+      if (on) s.fp[(warp == 0 ? 0 : m_pf) + e] = r;
+    }
+  } else {
+    for (uint32_t b = warp - 2; b < NBL; b += FWARPS - 2) {
+      const bool has_pf = cpf[b] != 0, has_ev = cev[b] != 0;  // this CTA's own rows (L2)
+      if (!has_pf && !has_ev) continue;
+      uint32_t ppf = 0, pev = 0;
+      for (uint32_t q = lane; q < G; q += 32) {
+        if (has_pf && q < c) ppf += d.f_cta_cpf[(uint64_t)q * NBL + b];
+        if (has_ev && q > c) pev += d.f_cta_cev[(uint64_t)q * NBL + b];
       }
-      __syncwarp();
-      if (on && (peers & lanemask_lt()) == 0) g_ev[b] += __popc(peers);
-      __syncwarp();
+      ppf = __reduce_add_sync(0xFFFFFFFFu, ppf);
+      pev = __reduce_add_sync(0xFFFFFFFFu, pev);
+      if (lane == 0) {
+        g_pf[b] += ppf;
+        g_ev[b] += pev;
+      }
     }
+  }
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e < m_pf + m_ev; e += FT) {
+    const uint32_t k = s.memb[e];
+    const uint32_t bk = s.keys[k] >> 21;
+    const uint32_t id = (uint32_t)(p.shard_begin + base + k);
+    if (e < m_pf) d.pf_ids[g_pf[bk] + s.fp[e]] = id;
+    else d.ev_ids[g_ev[bk] + s.fp[e]] = id;
   }
   // header (CTA 0): all accumulators are complete after the last barrier
   if (c == 0 && threadIdx.x == 0) {
@@ -561,22 +640,37 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
   }
 
   // ---------------- P6: re-sort list segments whose bucket holds several distances
-  // (decided identically by every CTA from global data)
-  const uint32_t *mm1 = d.f_mm1 + 4096 * par;
+  // (decided identically by every CTA from the global totals and the level-1 min/max)
+  const uint32_t *mm1 = d.f_mm1 + 2 * NB1 * par;
   __shared__ uint32_t sh_need;
   if (threadIdx.x == 0) sh_need = 0;
   __syncthreads();
-  for (int b = threadIdx.x; b < 2048; b += FT) {
-    const bool multi = mm1[b] != ~mm1[2048 + b];
-    if (multi && (tot_pf[b] > 1 || tot_ev[b] > 1)) atomicOr(&sh_need, 1u);
+  // list bucket lb (bits [30:21]) = level-1 buckets 4lb .. 4lb+3 (bits [30:19]); it holds
+  // several distances iff the min and max key over those buckets differ
+  auto multi_valued = [&](uint32_t lb) {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    for (uint32_t q = 4 * lb; q < 4 * lb + 4; ++q) {
+      if (mm1[q] == 0xFFFFFFFFu) continue;  // empty level-1 bucket
+      lo = min(lo, mm1[q]);
+      hi = max(hi, ~mm1[NB1 + q]);
+    }
+    return lo != 0xFFFFFFFFu && lo != hi;
+  };
+  {
+    const uint32_t b = threadIdx.x;
+    if ((tot_pf[b] > 1 || tot_ev[b] > 1) && multi_valued(b)) atomicOr(&sh_need, 1u);
   }
   __syncthreads();
-  if (!sh_need) return;
+  if (c == 0 && threadIdx.x == 0) prof[7] = gtimer();
+  if (!sh_need) {
+    if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
+    return;
+  }
   grid.sync();
-  // segment k (bucket order, prefetch list first) is re-sorted by CTA k mod G, in rounds
-  // of up to 64 segments per CTA
-  __shared__ uint32_t q_n, q_start[64], q_len[64], q_list[64];
+  if (c == 0 && threadIdx.x == 0) prof[8] = gtimer();
+  // segment j (bucket order, prefetch list first) is re-sorted by CTA j mod G
   __shared__ uint32_t seg_base, tot_tmp, seg_tmp;
+  __shared__ uint32_t q_n, q_start[64], q_len[64], q_list[64];
   for (uint32_t round = 0;; ++round) {
     if (threadIdx.x == 0) {
       q_n = 0;
@@ -585,58 +679,51 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     __syncthreads();
     for (int list = 0; list < 2; ++list) {
       const uint32_t *tot = list == 0 ? tot_pf : tot_ev;
-      uint32_t len[2], need[2];
-      for (int k = 0; k < 2; ++k) {
-        const uint32_t r = 2 * threadIdx.x + k;  // position in list order
-        const uint32_t b = list == 0 ? r : 2047 - r;
-        len[k] = tot[b];
-        need[k] = (len[k] > 1 && mm1[b] != ~mm1[2048 + b]) ? 1u : 0u;
-      }
-      const uint32_t st_ex = block_excl_scan<uint32_t, FT>(len[0] + len[1], &tot_tmp);
-      const uint32_t sg_ex = block_excl_scan<uint32_t, FT>(need[0] + need[1], &seg_tmp);
-      uint32_t start = st_ex, sg = seg_base + sg_ex;
-      for (int k = 0; k < 2; ++k) {
-        if (need[k]) {
-          const uint32_t j = sg / G;  // this segment's index among CTA (sg % G)'s segments
-          if (sg % G == c && j >= round * 64 && j < (round + 1) * 64) {
-            const uint32_t slot = j - round * 64;
-            q_start[slot] = start;
-            q_len[slot] = len[k];
-            q_list[slot] = list;
-            atomicAdd(&q_n, 1u);
-          }
-          ++sg;
+      const uint32_t r = threadIdx.x;  // position in list order
+      const uint32_t b = list == 0 ? r : NBL - 1 - r;
+      const uint32_t len = tot[b];
+      const uint32_t need = (len > 1 && multi_valued(b)) ? 1u : 0u;
+      const uint32_t start = block_excl_scan<uint32_t, FT>(len, &tot_tmp);
+      const uint32_t sg = seg_base + block_excl_scan<uint32_t, FT>(need, &seg_tmp);
+      if (need) {
+        const uint32_t j = sg / G;  // this segment's index among CTA (sg % G)'s segments
+        if (sg % G == c && j >= round * 64 && j < (round + 1) * 64) {
+          const uint32_t slot = j - round * 64;
+          q_start[slot] = start;
+          q_len[slot] = len;
+          q_list[slot] = list;
+          atomicAdd(&q_n, 1u);
         }
-        start += len[k];
       }
       __syncthreads();
       if (threadIdx.x == 0) seg_base += seg_tmp;
       __syncthreads();
     }
-    const uint32_t nq = q_n;  // the CTA's segments of this round occupy slots [0, nq)
+    const uint32_t nq = q_n;  // this round's segments occupy slots [0, nq)
     for (uint32_t qi = 0; qi < nq; ++qi) {
       const uint32_t list = q_list[qi], start = q_start[qi], t = q_len[qi];
       uint32_t *ids = list == 0 ? d.pf_ids : d.ev_ids;
       const bool fits = t <= A.tile;
       uint32_t *ka = fits ? s.keys : (list == 0 ? d.sort_ka : d.f_sk2) + start;
-      uint32_t *ia = fits ? s.memb : (list == 0 ? d.sort_va : d.f_sv2) + start;
-      uint32_t *kb = (list == 0 ? d.sort_kb : d.f_sk3) + start;
+      uint32_t *ia = fits ? s.fp : (list == 0 ? d.sort_va : d.f_sv2) + start;
+      uint32_t *kb = fits ? s.memb : (list == 0 ? d.sort_kb : d.f_sk3) + start;
       uint32_t *ib = (list == 0 ? d.sort_vb : d.f_sv3) + start;
       for (uint32_t e = threadIdx.x; e < t; e += FT) {
         const uint32_t id = ids[start + e];
         const uint32_t key = d.keys[id - p.shard_begin];
-        ka[e] = list == 0 ? key : ~key;
+        ka[e] = list == 0 ? key : ~key;  // evict: descending (distance, id) = ascending complement
         ia[e] = id;
       }
       __syncthreads();
-      cta_sort_pairs(ka, ia, kb, ib, t, s.h_lo);
+      cta_sort_pairs(ka, ia, kb, ib, t, s.h);
       for (uint32_t e = threadIdx.x; e < t; e += FT) ids[start + e] = ia[e];
       __syncthreads();
     }
     const uint32_t total_segs = seg_base;
     __syncthreads();
-    if ((round + 1) * 64 * G >= total_segs) break;  // uniform: every CTA sees the same totals
+    if ((round + 1) * 64 * G >= total_segs) break;  // uniform
   }
+  if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
 }
 
 // host side
@@ -661,13 +748,13 @@ bool fused_prepare(int grid, uint32_t tile) {
   return per_sm >= 1 && grid >= 1;
 }
 
-int launch_fused_plan(const Params &p, int64_t now, int parity, int grid, uint32_t tile, unsigned int *bar,
+int launch_fused_plan(const Params &p, int64_t now, int parity, unsigned int epoch, int grid, uint32_t tile,
                       cudaStream_t s) {
   FusedArgs A;
   A.p = p;
   A.now = now;
   A.parity = parity;
-  A.bar = bar;
+  A.epoch = epoch;
   A.tile = tile;
   A.tw = tile / 32;
   k_fused_plan<<<grid, FT, fused_smem_bytes(tile), s>>>(A);

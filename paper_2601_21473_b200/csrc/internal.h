@@ -13,7 +13,7 @@ constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;
 constexpr uint32_t PAGE_NONE = 0xFFFFFFFFu;
 constexpr int L1_BITS = 11, L2_BITS = 10, L3_BITS = 10;  // distance-bit digits [30:20] [19:10] [9:0]
 constexpr int FUSED_MAX_CTAS = 160;       // fused path: one CTA per SM (B200: 148)
-constexpr uint32_t FUSED_MAX_TILE = 16384;  // fused path: agents per CTA held in shared memory
+constexpr uint32_t FUSED_MAX_TILE = 12288;  // fused path: agents per CTA held in shared memory
 
 // status bits (mirror include/scalesim.h)
 constexpr uint32_t ST_INSUFFICIENT = 1u, ST_BAD_RECORD = 2u, ST_BAD_KIN = 4u, ST_NO_PAGES = 8u;
@@ -52,8 +52,8 @@ struct Layout {
   uint64_t exp_sum, exp_excl;
   uint64_t page_first, page_table, ring, pool, desc[2];
   // fused path (double-buffered by fused-step parity where noted)
-  uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_h1, f_cta_h2, f_cta_h3, f_cta_cpf, f_cta_cev, f_tot, f_acc;
-  uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar;
+  uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_cpf, f_cta_cev, f_tot, f_acc, f_tie_val, f_tie_flag;
+  uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes;
   uint64_t total;
 };
 
@@ -80,18 +80,21 @@ struct Dev {
   uint32_t *page_table, *ring;
   unsigned long long *pool;  // [0] head, [1] tail
   unsigned long long *desc[2];  // each: d2h [desc_cap pairs] then h2d [desc_cap pairs]
-  // fused path
-  unsigned long long *f_hist1;  // [2][2048]
-  uint32_t *f_mm1;              // [2][4096]
+  // fused path (parity = launch number & 1)
+  unsigned long long *f_hist1;  // [2][4096] level-1 byte histogram
+  uint32_t *f_mm1;              // [2][2][4096] per-bucket min key, min complemented key
   unsigned long long *f_hist2;  // [2][1024]
-  uint32_t *f_mm2;              // [2][2048]
+  uint32_t *f_mm2;              // [2][2][1024]
   unsigned long long *f_hist3;  // [2][1024]
-  unsigned long long *f_cta_h1, *f_cta_h2, *f_cta_h3;  // [CTAS][2048] / [CTAS][1024] / [CTAS][1024]
-  uint32_t *f_cta_cpf, *f_cta_cev;                      // [CTAS][2048]
-  uint32_t *f_tot;                                      // [2][2][2048]
+  uint32_t *f_cta_cpf, *f_cta_cev;                      // [CTAS][1024] list members per bucket
+  uint32_t *f_tot;                                      // [2][2][1024] list bucket totals
   unsigned long long *f_acc;                            // [2][8]
+  unsigned long long *f_tie_val;                        // [CTAS] tie bytes per CTA
+  unsigned int *f_tie_flag;                             // [CTAS] launch epoch of f_tie_val
+  uint32_t *wb_bytes;                                   // [n_local] KV+HIST bytes per agent (R13)
   uint32_t *f_sk2, *f_sv2, *f_sk3, *f_sv3;              // [n_local] evict-segment sort scratch
   unsigned int *f_bar;                                  // [2] grid-barrier counters
+  unsigned long long *f_prof;                           // [16] globaltimer stamps of the last fused launch
 };
 
 Dev make_dev(void *ws, const Layout &L);
@@ -130,7 +133,7 @@ int launch_transfer(const Params &p, cudaStream_t s, int ctas);
 int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s);
 int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s);
 bool fused_supported(const Params &p, int grid, uint32_t *tile_out);
-int launch_fused_plan(const Params &p, int64_t now, int parity, int grid, uint32_t tile, unsigned int *bar,
+int launch_fused_plan(const Params &p, int64_t now, int parity, unsigned int epoch, int grid, uint32_t tile,
                       cudaStream_t s);
 bool fused_prepare(int grid, uint32_t tile);
 size_t fused_smem_bytes(uint32_t tile);
