@@ -201,40 +201,12 @@ __device__ void select_level(const unsigned long long *g_hist, const uint32_t *g
   __syncthreads();
 }
 
-// Stable sort of a segment of n (key, id) pairs by key, ascending, for one CTA.
-// n <= 2048: rank sort in place (rank = #smaller keys + #equal keys before).
-// Larger: LSD radix sort (digits [0,11) [11,22) [22,32), constant digits skipped) on the
-// caller's buffers (shared or global), warp-serialised stable scatter.  Result in (ka, ia).
+// Stable sort of a segment of n (key, id) pairs by key, ascending, for one CTA: LSD radix
+// sort with 8-bit digits over the varying bits only.  Warp w owns the contiguous range
+// [w*L, (w+1)*L) of the input, so (digit, warp, position) order is stable.  cnt: 8192 words
+// of shared memory.  Buffers may be shared or global memory.  Result in (ka, ia).
 __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_t *ib, uint32_t n, uint32_t *cnt) {
   if (n <= 1) return;
-  if (n <= 2 * FT) {
-    uint32_t k0 = 0, k1 = 0, i0 = 0, i1 = 0, r0 = 0, r1 = 0;
-    const uint32_t e0 = threadIdx.x, e1 = threadIdx.x + FT;
-    if (e0 < n) {
-      k0 = ka[e0];
-      i0 = ia[e0];
-    }
-    if (e1 < n) {
-      k1 = ka[e1];
-      i1 = ia[e1];
-    }
-    for (uint32_t j = 0; j < n; ++j) {
-      const uint32_t kj = ka[j];
-      r0 += (kj < k0) || (kj == k0 && j < e0);
-      r1 += (kj < k1) || (kj == k1 && j < e1);
-    }
-    __syncthreads();
-    if (e0 < n) {
-      ka[r0] = k0;
-      ia[r0] = i0;
-    }
-    if (e1 < n) {
-      ka[r1] = k1;
-      ia[r1] = i1;
-    }
-    __syncthreads();
-    return;
-  }
   __shared__ uint32_t sh_or, sh_and, sh_tot;
   if (threadIdx.x == 0) {
     sh_or = 0;
@@ -254,43 +226,47 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
   }
   __syncthreads();
   const uint32_t varying = sh_or ^ sh_and;
-  const int warp = threadIdx.x >> 5;
-  for (int pass = 0; pass < 3; ++pass) {
-    const int shift = pass == 0 ? 0 : (pass == 1 ? 11 : 22);
-    const uint32_t mask = pass == 2 ? 0x3FFu : 0x7FFu;
-    if (((varying >> shift) & mask) == 0) continue;
-    for (int b = threadIdx.x; b < 2048; b += FT) cnt[b] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t L = (n + FWARPS - 1) / FWARPS;
+  const uint32_t lo = min(n, warp * L), hi = min(n, lo + L);
+  for (int shift = 0; shift < 32; shift += 8) {
+    if (((varying >> shift) & 0xFFu) == 0) continue;
+    // cnt[d * 32 + w]: members of digit d in warp w's range
+    for (int b = threadIdx.x; b < 256 * FWARPS; b += FT) cnt[b] = 0;
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < n; e += FT) atomicAdd(&cnt[(ka[e] >> shift) & mask], 1u);
+    for (uint32_t e = lo + lane; e < hi; e += 32) atomicAdd(&cnt[((ka[e] >> shift) & 0xFFu) * FWARPS + warp], 1u);
     __syncthreads();
-    {
-      const uint32_t c0 = cnt[2 * threadIdx.x], c1 = cnt[2 * threadIdx.x + 1];
-      const uint32_t ex = block_excl_scan<uint32_t, FT>(c0 + c1, &sh_tot);
-      __syncthreads();
-      cnt[2 * threadIdx.x] = ex;
-      cnt[2 * threadIdx.x + 1] = ex + c0;
-      __syncthreads();
-    }
-    for (uint32_t c0 = 0; c0 < n; c0 += FT) {
-      const uint32_t e = c0 + threadIdx.x;
-      const bool valid = e < n;
-      const uint32_t k = valid ? ka[e] : 0u, id = valid ? ia[e] : 0u;
-      const uint32_t dg = valid ? ((k >> shift) & mask) : 0xFFFFFFFFu;
-      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dg);
-      const uint32_t rank = __popc(peers & lanemask_lt());
-      const bool leader = (peers & lanemask_lt()) == 0;
-      const uint32_t nw = (min(n - c0, (uint32_t)FT) + 31) / 32;
-      for (uint32_t w = 0; w < nw; ++w) {
-        if ((uint32_t)warp == w && valid) {
-          const uint32_t pos = cnt[dg] + rank;
-          kb[pos] = k;
-          ib[pos] = id;
-        }
-        __syncwarp();
-        if ((uint32_t)warp == w && valid && leader) cnt[dg] += __popc(peers);
-        __syncthreads();
+    {  // exclusive scan in (digit, warp) order: 8 consecutive entries per thread
+      uint32_t v[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[j] = cnt[threadIdx.x * 8 + j];
+        sum += v[j];
+      }
+      uint32_t ex = block_excl_scan<uint32_t, FT>(sum, &sh_tot);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[threadIdx.x * 8 + j] = ex;
+        ex += v[j];
       }
     }
+    __syncthreads();
+    for (uint32_t e0 = lo; e0 < hi; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      const bool valid = e < hi;
+      const uint32_t k = valid ? ka[e] : 0u, id = valid ? ia[e] : 0u;
+      const uint32_t dg = valid ? ((k >> shift) & 0xFFu) : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dg);
+      if (valid) {
+        const uint32_t pos = cnt[dg * FWARPS + warp] + __popc(peers & lanemask_lt());
+        kb[pos] = k;
+        ib[pos] = id;
+      }
+      __syncwarp();
+      if (valid && (peers & lanemask_lt()) == 0) cnt[dg * FWARPS + warp] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
     for (uint32_t e = threadIdx.x; e < n; e += FT) {  // back into (ka, ia)
       ka[e] = kb[e];
       ia[e] = ib[e];
@@ -341,7 +317,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
 #pragma unroll
     for (int j = 0; j < LOAD_BATCH; ++j) {
       const uint32_t k = k0 + j * FT + threadIdx.x;
-      if (k0 + j * FT >= A.tw * 32) break;  // uniform
+      if (k >= A.tw * 32) continue;  // warp-uniform (tw * 32 is a multiple of 32)
       const bool valid = k < n_here;
       const bool res = (s.old_w[k >> 5] >> (k & 31)) & 1u;
       const float dist = valid ? distance_of(r[j], A.now, p.hop_scale, d.dint, p.n_kin, st) : 0.0f;
@@ -371,21 +347,22 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
   if (c == 0 && threadIdx.x == 0) prof[4] = gtimer();
 
   // ---------------- P2: select
-  if (c == 0) {  // clear the other parity's accumulators for the next launch
+  {  // clear the other parity's accumulators for the next launch, spread over the CTAs
     const int q = par ^ 1;
-    for (int b = threadIdx.x; b < NB1; b += FT) {
+    const uint32_t gt = c * FT + threadIdx.x, gs = G * FT;
+    for (uint32_t b = gt; b < NB1; b += gs) {
       d.f_hist1[NB1 * q + b] = 0;
       d.f_mm1[2 * NB1 * q + b] = 0xFFFFFFFFu;
       d.f_mm1[2 * NB1 * q + NB1 + b] = 0xFFFFFFFFu;
     }
-    for (int b = threadIdx.x; b < 2 * NBL; b += FT) d.f_tot[2 * NBL * q + b] = 0;
-    for (int b = threadIdx.x; b < 1024; b += FT) {
+    for (uint32_t b = gt; b < 2 * NBL; b += gs) d.f_tot[2 * NBL * q + b] = 0;
+    for (uint32_t b = gt; b < 1024; b += gs) {
       d.f_hist2[1024 * q + b] = 0;
       d.f_hist3[1024 * q + b] = 0;
       d.f_mm2[2048 * q + b] = 0xFFFFFFFFu;
       d.f_mm2[2048 * q + 1024 + b] = 0xFFFFFFFFu;
     }
-    if (threadIdx.x < 8) d.f_acc[8 * q + threadIdx.x] = 0;
+    if (gt < 8) d.f_acc[8 * q + gt] = 0;
   }
   Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0};
   select_level(d.f_hist1 + NB1 * par, d.f_mm1 + 2 * NB1 * par, 1, p.budget, sel);
@@ -409,6 +386,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
   }
   const bool all_fit = sel.all_fit;
   const uint32_t dstar = sel.dstar;
+  if (c == 0 && threadIdx.x == 0) prof[9] = gtimer();
 
   // ---------------- P3: tie group — this CTA's bytes at d == D*, prefix over preceding CTAs
   unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw]
@@ -455,6 +433,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     sh_tie_excl = 0;
   }
   __syncthreads();
+  if (c == 0 && threadIdx.x == 0) prof[10] = gtimer();
 
   // ---------------- P4: emit
   uint32_t *cnt_pf = s.h, *cnt_ev = s.h + NBL;  // per-CTA list members per list bucket
@@ -576,13 +555,20 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     }
   }
   __syncthreads();
+  // own nonzero list buckets (for the column prefix)
+  uint32_t *own_b = s.h + 6 * NBL;  // [NBL]
+  __shared__ uint32_t sh_nown;
+  if (threadIdx.x == 0) sh_nown = 0;
+  __syncthreads();
+  if (cnt_pf[threadIdx.x] || cnt_ev[threadIdx.x]) own_b[atomicAdd(&sh_nown, 1u)] = threadIdx.x;  // NBL == FT
+  __syncthreads();
   // (a) warps 0/1: in-CTA rank of every member within its bucket (list order), into fp[]
   // (b) other warps: members of the same bucket in the preceding (prefetch) / following
   //     (evict) CTAs, added to the bucket starts
   if (warp < 2) {
     const uint32_t *mem = warp == 0 ? mem_pf : mem_ev;
     const uint32_t m = warp == 0 ? m_pf : m_ev;
-    uint32_t *run = warp == 0 ? s.h : s.h + NBL;  // reuse the member counters as running ranks
+    uint32_t *run = warp == 0 ? s.h + 4 * NBL : s.h + 5 * NBL;
     for (uint32_t b = lane; b < NBL; b += 32) run[b] = 0;
     __syncwarp();
     for (uint32_t e0 = 0; e0 < m; e0 += 32) {
@@ -598,9 +584,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
       if (on) s.fp[(warp == 0 ? 0 : m_pf) + e] = r;
     }
   } else {
-    for (uint32_t b = warp - 2; b < NBL; b += FWARPS - 2) {
-      const bool has_pf = cpf[b] != 0, has_ev = cev[b] != 0;  // this CTA's own rows (L2)
-      if (!has_pf && !has_ev) continue;
+    const uint32_t nown = sh_nown;
+    for (uint32_t j = warp - 2; j < nown; j += FWARPS - 2) {
+      const uint32_t b = own_b[j];
+      const bool has_pf = cnt_pf[b] != 0, has_ev = cnt_ev[b] != 0;
       uint32_t ppf = 0, pev = 0;
       for (uint32_t q = lane; q < G; q += 32) {
         if (has_pf && q < c) ppf += d.f_cta_cpf[(uint64_t)q * NBL + b];
@@ -707,7 +694,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
       uint32_t *ka = fits ? s.keys : (list == 0 ? d.sort_ka : d.f_sk2) + start;
       uint32_t *ia = fits ? s.fp : (list == 0 ? d.sort_va : d.f_sv2) + start;
       uint32_t *kb = fits ? s.memb : (list == 0 ? d.sort_kb : d.f_sk3) + start;
-      uint32_t *ib = (list == 0 ? d.sort_vb : d.f_sv3) + start;
+      uint32_t *ib = t <= 8192 ? s.h + 8192 : (list == 0 ? d.sort_vb : d.f_sv3) + start;
       for (uint32_t e = threadIdx.x; e < t; e += FT) {
         const uint32_t id = ids[start + e];
         const uint32_t key = d.keys[id - p.shard_begin];

@@ -34,7 +34,7 @@ for mode in ("eager", "graph", "eager_sync"):
         torch.cuda.synchronize()
         st = pl.stamps().astype(np.int64)
         print("graph stamps: span of all launches (us)", (st[1]-st[0])/1e3, "last launch cta0 phases",
-              [(st[i]-st[2])/1e3 if st[i] else None for i in range(3, 9)])
+              [(st[i]-st[2])/1e3 if st[i] else None for i in range(3, 11)])
     elif mode == "eager":
         with torch.cuda.stream(pl.stream):
             torch.cuda._sleep(int(1e8))
@@ -54,7 +54,7 @@ for mode in ("eager", "graph", "eager_sync"):
             st = pl.stamps().astype(np.int64)
             if k < 4:
                 print("stamps(us rel. to min start): end", (st[1]-st[0])/1e3, "cta0 start", (st[2]-st[0])/1e3,
-                      "phases", [(st[i]-st[0])/1e3 if st[i] else None for i in range(3, 9)])
+                      "phases", [(st[i]-st[0])/1e3 if st[i] else None for i in range(3, 11)])
         print("eager_sync per-step ms", np.round(ts, 4))
         t0.record(pl.stream); t1.record(pl.stream)
     torch.cuda.synchronize()
