@@ -62,8 +62,7 @@ struct GridBar {
       __threadfence();
       atomicAdd(bar, 1u);
       const unsigned int target = k * gridDim.x;
-      while (ld_acquire(bar) < target) {
-      }
+      while (ld_acquire(bar) < target) __nanosleep(40);  // back off: 148 CTAs poll one line
       __threadfence();
     }
     __syncthreads();
@@ -342,6 +341,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
   st = __reduce_or_sync(0xFFFFFFFFu, st);
   if (lane == 0 && st) atomicOr(reinterpret_cast<unsigned int *>(&acc[5]), st);
   if (threadIdx.x == 0 && zero_b) atomicAdd(&acc[0], zero_b);
+  if (threadIdx.x == 0) atomicMax(&prof[11], gtimer());
   if (c == 0 && threadIdx.x == 0) prof[3] = gtimer();
   grid.sync();
   if (c == 0 && threadIdx.x == 0) prof[4] = gtimer();
@@ -393,8 +393,11 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
     const bool tie = !all_fit && ((s.elig_w[w] >> lane) & 1u) && s.keys[k] == dstar;
-    unsigned long long v = tie ? s.fp[k] : 0u;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    unsigned long long v = 0;
+    if (__ballot_sync(0xFFFFFFFFu, tie)) {  // most words hold no tie agent: skip the reduction
+      v = tie ? s.fp[k] : 0u;
+      v = warp_sum_u32_exact(tie ? s.fp[k] : 0u);
+    }
     if (lane == 0) word_tie[w] = v;
   }
   __syncthreads();
@@ -419,13 +422,17 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
       __threadfence();
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(d.f_tie_flag + c), "r"(A.epoch) : "memory");
     }
-    if (warp == 0) {
+    if (warp == 0) {  // lane j reads the flags of CTAs j, j+32, ...: loads issued together
       unsigned long long t = 0;
-      for (uint32_t q = lane; q < c; q += 32) {
-        while (ld_acquire(d.f_tie_flag + q) != A.epoch) {
-        }
-        t += *(volatile unsigned long long *)(d.f_tie_val + q);
+      uint32_t pending = 0;
+      for (uint32_t q = lane, j = 0; q < c; q += 32, ++j)
+        if (ld_acquire(d.f_tie_flag + q) != A.epoch) pending |= 1u << j;
+      while (pending) {
+        __nanosleep(40);
+        for (uint32_t q = lane, j = 0; q < c; q += 32, ++j)
+          if (((pending >> j) & 1u) && ld_acquire(d.f_tie_flag + q) == A.epoch) pending &= ~(1u << j);
       }
+      for (uint32_t q = lane; q < c; q += 32) t += *(volatile unsigned long long *)(d.f_tie_val + q);
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
       if (lane == 0) sh_tie_excl = t;
     }
@@ -434,6 +441,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
   }
   __syncthreads();
   if (c == 0 && threadIdx.x == 0) prof[10] = gtimer();
+  if (threadIdx.x == 0) atomicMax(&prof[14], gtimer());
 
   // ---------------- P4: emit
   uint32_t *cnt_pf = s.h, *cnt_ev = s.h + NBL;  // per-CTA list members per list bucket
@@ -447,13 +455,17 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     const uint32_t key = s.keys[k];
     const bool tie = el && !all_fit && key == dstar;
     const uint32_t fp = s.fp[k];
-    unsigned long long incl = tie ? fp : 0u;
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= o) incl += t;
+    bool tie_ok = false;
+    if (__ballot_sync(0xFFFFFFFFu, tie)) {  // id-order inclusive prefix of the tie bytes
+      unsigned long long incl = tie ? fp : 0u;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      incl += sh_tie_excl + word_tie[w];
+      tie_ok = tie && incl <= sel.rem;
     }
-    incl += sh_tie_excl + word_tie[w];
-    const bool kept = el && (all_fit || key < dstar || (tie && incl <= sel.rem));
+    const bool kept = el && (all_fit || key < dstar || tie_ok);
     if (tie && kept) tie_kept += fp;
     const uint32_t kw = __ballot_sync(0xFFFFFFFFu, kept);
     const uint32_t old = s.old_w[w];
@@ -493,6 +505,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     if (tie_kept) atomicAdd(&acc[3], tie_kept);
     if (n_el) atomicAdd(&acc[4], (unsigned long long)n_el);
   }
+  if (threadIdx.x == 0) atomicMax(&prof[12], gtimer());
   if (c == 0 && threadIdx.x == 0) prof[5] = gtimer();
   grid.sync();
   if (c == 0 && threadIdx.x == 0) prof[6] = gtimer();
@@ -648,6 +661,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
     if ((tot_pf[b] > 1 || tot_ev[b] > 1) && multi_valued(b)) atomicOr(&sh_need, 1u);
   }
   __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&prof[13], gtimer());
   if (c == 0 && threadIdx.x == 0) prof[7] = gtimer();
   if (!sh_need) {
     if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
@@ -687,6 +701,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
       __syncthreads();
     }
     const uint32_t nq = q_n;  // this round's segments occupy slots [0, nq)
+    if (round == 0 && threadIdx.x == 0) atomicMax(&prof[15], gtimer());
     for (uint32_t qi = 0; qi < nq; ++qi) {
       const uint32_t list = q_list[qi], start = q_start[qi], t = q_len[qi];
       uint32_t *ids = list == 0 ? d.pf_ids : d.ev_ids;

@@ -53,8 +53,10 @@ for mode in ("eager", "graph", "eager_sync"):
             ts.append(e0.elapsed_time(e1))
             st = pl.stamps().astype(np.int64)
             if k < 4:
-                print("stamps(us rel. to min start): end", (st[1]-st[0])/1e3, "cta0 start", (st[2]-st[0])/1e3,
-                      "phases", [(st[i]-st[0])/1e3 if st[i] else None for i in range(3, 11)])
+                r = lambda q: round((int(st[q]) - int(st[0])) / 1e3, 2) if st[q] else None
+                print("us: cta0 P1end", r(3), "B1", r(4), "sel", r(9), "P3", r(10), "P4end", r(5), "B4", r(6),
+                      "P5end", r(7), "B5", r(8), "| max over CTAs: P1end", r(11), "P3end", r(14), "P4end", r(12),
+                      "P5end", r(13), "P6enum", r(15), "end", r(1))
         print("eager_sync per-step ms", np.round(ts, 4))
         t0.record(pl.stream); t1.record(pl.stream)
     torch.cuda.synchronize()
