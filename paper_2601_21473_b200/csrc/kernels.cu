@@ -126,10 +126,12 @@ __global__ void __launch_bounds__(NT) k_pairmin(Params p) {
 // a1 + a2: score, key, eligibility, byte-weighted level-1 histogram with per-bucket min/max
 
 __global__ void __launch_bounds__(NT) k_score(Params p, int64_t now) {
-  __shared__ unsigned long long sh_hist[2048];
-  __shared__ uint32_t sh_min[2048], sh_nmax[2048];
+  // byte-weighted level-1 histogram in shared memory as 16-bit halves (native 32-bit
+  // shared atomics, exact), with per-bucket min key and min complemented key
+  __shared__ uint32_t sh_lo[2048], sh_hi[2048], sh_min[2048], sh_nmax[2048];
   for (int b = threadIdx.x; b < 2048; b += NT) {
-    sh_hist[b] = 0;
+    sh_lo[b] = 0;
+    sh_hi[b] = 0;
     sh_min[b] = 0xFFFFFFFFu;
     sh_nmax[b] = 0xFFFFFFFFu;
   }
@@ -155,13 +157,19 @@ __global__ void __launch_bounds__(NT) k_score(Params p, int64_t now) {
     const uint32_t eb = __ballot_sync(FULL, elig);
     if (lane == 0 && (i >> 5) < p.n_words) p.d.elig[i >> 5] = eb;
     if (valid && d == 0.0f) zero_bytes += r.y;
-    // warp-aggregated histogram update: one smem atomic per distinct bucket in the warp
-    hist_add(sh_hist, sh_min, sh_nmax, elig, bits >> 20, bits, r.y);
+    if (elig) {
+      const uint32_t b = bits >> 20;
+      atomicAdd(&sh_lo[b], r.y & 0xFFFFu);
+      atomicAdd(&sh_hi[b], r.y >> 16);
+      atomicMin(&sh_min[b], bits);
+      atomicMin(&sh_nmax[b], ~bits);
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < 2048; b += NT) {
-    if (sh_hist[b] != 0 || sh_min[b] != 0xFFFFFFFFu) {
-      atomicAdd(&p.d.hist1[b], sh_hist[b]);
+    const unsigned long long v = ((unsigned long long)sh_hi[b] << 16) + sh_lo[b];
+    if (v != 0 || sh_min[b] != 0xFFFFFFFFu) {
+      atomicAdd(&p.d.hist1[b], v);
       atomicMin(&p.d.mm1[b], sh_min[b]);
       atomicMin(&p.d.mm1[2048 + b], sh_nmax[b]);
     }
@@ -247,10 +255,10 @@ __global__ void __launch_bounds__(NT) k_select(Params p, int level) {
 __global__ void __launch_bounds__(NT) k_hist(Params p, int level) {
   const SelState *S = p.d.state;
   if (S->done || S->level != (unsigned)level) return;
-  __shared__ unsigned long long sh_hist[1024];
-  __shared__ uint32_t sh_min[1024], sh_nmax[1024];
+  __shared__ uint32_t sh_lo[1024], sh_hi[1024], sh_min[1024], sh_nmax[1024];
   for (int b = threadIdx.x; b < 1024; b += NT) {
-    sh_hist[b] = 0;
+    sh_lo[b] = 0;
+    sh_hi[b] = 0;
     sh_min[b] = 0xFFFFFFFFu;
     sh_nmax[b] = 0xFFFFFFFFu;
   }
@@ -258,24 +266,24 @@ __global__ void __launch_bounds__(NT) k_hist(Params p, int level) {
   const int hi_shift = level == 2 ? 20 : 10;
   const int shift = level == 2 ? 10 : 0;
   const uint32_t want = S->prefix >> hi_shift;
-  const int lane = threadIdx.x & 31;
-  for (uint64_t base = blockIdx.x * (uint64_t)NT; base < p.n_local; base += (uint64_t)gridDim.x * NT) {
-    const uint64_t i = base + threadIdx.x;
-    bool in_b = false;
-    uint32_t bits = 0, fp = 0;
-    if (i < p.n_local) {
-      const bool el = (p.d.elig[i >> 5] >> (i & 31)) & 1u;
-      bits = p.d.keys[i];
-      in_b = el && (bits >> hi_shift) == want;
-      if (in_b) fp = p.rec[i].y;
+  for (uint64_t i = blockIdx.x * (uint64_t)NT + threadIdx.x; i < p.n_local; i += (uint64_t)gridDim.x * NT) {
+    const bool el = (p.d.elig[i >> 5] >> (i & 31)) & 1u;
+    const uint32_t bits = p.d.keys[i];
+    if (el && (bits >> hi_shift) == want) {
+      const uint32_t fp = p.rec[i].y;
+      const uint32_t b = (bits >> shift) & 1023u;
+      atomicAdd(&sh_lo[b], fp & 0xFFFFu);
+      atomicAdd(&sh_hi[b], fp >> 16);
+      atomicMin(&sh_min[b], bits);
+      atomicMin(&sh_nmax[b], ~bits);
     }
-    hist_add(sh_hist, sh_min, sh_nmax, in_b, (bits >> shift) & 1023u, bits, fp);
   }
   __syncthreads();
   unsigned long long *gh = level == 2 ? p.d.hist2 : p.d.hist3;
   for (int b = threadIdx.x; b < 1024; b += NT) {
-    if (sh_hist[b] != 0 || sh_min[b] != 0xFFFFFFFFu) {
-      atomicAdd(&gh[b], sh_hist[b]);
+    const unsigned long long v = ((unsigned long long)sh_hi[b] << 16) + sh_lo[b];
+    if (v != 0 || sh_min[b] != 0xFFFFFFFFu) {
+      atomicAdd(&gh[b], v);
       if (level == 2) {
         atomicMin(&p.d.mm2[b], sh_min[b]);
         atomicMin(&p.d.mm2[1024 + b], sh_nmax[b]);
@@ -819,7 +827,7 @@ int launch_interaction(const Params &p, cudaStream_t s, int grid) {
 
 int launch_score(const Params &p, int64_t now, float *dist_out, cudaStream_t s, int grid) {
   int n = launch_interaction(p, s, grid);
-  const int g = min(grid, max(1, ceil_div(p.n_local, NT)));
+  const int g = min(grid / 2, max(1, ceil_div(p.n_local, NT)));  // 2 blocks per SM: fewer histogram flushes
   k_score<<<g, NT, 0, s>>>(p, now);
   ++n;
   if (dist_out) {
