@@ -188,6 +188,13 @@ scalesim_status scalesim_transfer(scalesim_ctx *ctx, const scalesim_plan_view *p
 /* score + plan + transfer of one step. */
 scalesim_status scalesim_step(scalesim_ctx *ctx, int64_t now_tick, scalesim_plan_view *out);
 
+/* One step of several independent contexts (simulation replicas / parameter sweeps, C5) in
+ * as few launches as possible: each context is planned by its own group of CTAs of one
+ * persistent kernel.  All contexts must use the single-kernel plan path (scalesim_fused == 1)
+ * on the same device and the same cfg.stream; each context's inputs are its own tables.
+ * Equivalent to scalesim_step on every context in turn (same plans). */
+scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32_t n, int64_t now_tick);
+
 /* End-to-end step from HOST buffers: copies host_rec (4*n_local uint32) and host_kin
  * (4*n_kin float, may be NULL) to the device, runs scalesim_step, waits, and copies the
  * plan header and lists back (prefetch_out/evict_out: host, n_local capacity each, may be

@@ -30,7 +30,7 @@ HEADER_NAMES = ["n_prefetch", "n_evict", "bytes_h2d", "bytes_d2h", "cut_bits", "
 
 # Every symbol include/scalesim.h declares (checked by tests/test_abi.py).
 EXPORTS = ["scalesim_workspace_bytes", "scalesim_init", "scalesim_score", "scalesim_plan",
-           "scalesim_transfer", "scalesim_step", "scalesim_step_host", "scalesim_set_inputs",
+           "scalesim_transfer", "scalesim_step", "scalesim_step_batch", "scalesim_step_host", "scalesim_set_inputs",
            "scalesim_sync", "scalesim_join", "scalesim_nccl_unique_id", "scalesim_fused", "scalesim_profile_stamps", "scalesim_launch_count", "scalesim_destroy",
            "scalesim_strerror"]
 
@@ -104,6 +104,8 @@ def lib():
         L.scalesim_transfer.restype = C.c_int
         L.scalesim_step.argtypes = [vp, i64, C.POINTER(PlanView)]
         L.scalesim_step.restype = C.c_int
+        L.scalesim_step_batch.argtypes = [C.POINTER(vp), C.c_uint32, i64]
+        L.scalesim_step_batch.restype = C.c_int
         L.scalesim_step_host.argtypes = [vp, i64, vp, vp, C.POINTER(PlanHost), vp, vp]
         L.scalesim_step_host.restype = C.c_int
         L.scalesim_set_inputs.argtypes = [vp, vp, vp]

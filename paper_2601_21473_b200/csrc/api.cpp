@@ -93,6 +93,7 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_tie_val = take(8 * (uint64_t)FUSED_MAX_CTAS);
   L.f_tie_flag = take(4 * (uint64_t)FUSED_MAX_CTAS);
   L.wb_bytes = take(4 * n1);
+  L.params_dev = take(sizeof(Params));
   L.f_sk2 = take(4 * n1);
   L.f_sv2 = take(4 * n1);
   L.f_sk3 = take(4 * n1);
@@ -160,6 +161,7 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_tie_val = (unsigned long long *)(b + L.f_tie_val);
   d.f_tie_flag = (unsigned int *)(b + L.f_tie_flag);
   d.wb_bytes = (uint32_t *)(b + L.wb_bytes);
+  d.params_dev = (uint8_t *)(b + L.params_dev);
   d.f_sk2 = (uint32_t *)(b + L.f_sk2);
   d.f_sv2 = (uint32_t *)(b + L.f_sv2);
   d.f_sk3 = (uint32_t *)(b + L.f_sk3);
@@ -228,6 +230,7 @@ struct scalesim_ctx {
   uint64_t fused_steps = 0;
   bool deferred = false;  // score deferred into the fused plan kernel
   bool last_fused = false;
+  int sms = 148;
   int64_t deferred_now = 0;
 };
 
@@ -470,11 +473,15 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
       c->fused = true;
       c->fused_tile = tile;
       c->fused_grid = sms;
+      c->sms = sms;
       if (cudaMemsetAsync(p.d.f_mm1, 0xFF, 4 * 2 * 2 * 4096, c->stream) != cudaSuccess ||
           cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2 * 1024, c->stream) != cudaSuccess)
         return fail(SCALESIM_E_CUDA);
     }
   }
+  // device copy of the parameters for the fused kernel (per-launch fields are overridden)
+  if (cudaMemcpyAsync(p.d.params_dev, &p, sizeof(Params), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    return fail(SCALESIM_E_CUDA);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
   if (cfg->world > 1) {
     if (!cfg->nccl_unique_id || !g_nccl.load()) return fail(SCALESIM_E_NCCL);
@@ -539,14 +546,27 @@ static void fill_plan(scalesim_ctx *c, scalesim_plan_view *out) {
 
 static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out);
 
+static FusedInst fused_inst(const scalesim_ctx *c, uint32_t tile) {
+  FusedInst f;
+  f.params = reinterpret_cast<const Params *>(c->p.d.params_dev);
+  f.rec = c->p.rec;
+  f.kin = c->p.kin;
+  f.now = c->deferred_now;
+  f.cur = (uint32_t)c->p.cur;
+  f.parity = (uint32_t)(c->fused_steps & 1);
+  f.epoch = (uint32_t)(c->fused_steps + 1);
+  f.tile = tile;
+  return f;
+}
+
 extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *out) {
   if (!c) return SCALESIM_E_INVALID;
   if (!c->scored) return SCALESIM_E_ORDER;
   Params &p = c->p;
   const bool multi = c->cfg.world > 1;
   if (c->deferred) {
-    c->launches += launch_fused_plan(p, c->deferred_now, (int)(c->fused_steps & 1),
-                                     (unsigned int)(c->fused_steps + 1), c->fused_grid, c->fused_tile, c->stream);
+    const FusedInst inst = fused_inst(c, c->fused_tile);
+    c->launches += launch_fused_batch(&inst, 1, (uint32_t)c->fused_grid, c->stream);
     CK(cudaGetLastError());
     c->fused_steps++;
     c->deferred = false;
@@ -647,6 +667,55 @@ extern "C" scalesim_status scalesim_step(scalesim_ctx *c, int64_t now, scalesim_
   if ((s = scalesim_plan(c, &pl)) != SCALESIM_OK) return s;
   if ((s = scalesim_transfer(c, &pl)) != SCALESIM_OK) return s;
   if (out) *out = pl;
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32_t n, int64_t now) {
+  if (!ctxs || n == 0) return SCALESIM_E_INVALID;
+  scalesim_ctx *c0 = ctxs[0];
+  if (!c0) return SCALESIM_E_INVALID;
+  for (uint32_t i = 0; i < n; ++i) {
+    scalesim_ctx *c = ctxs[i];
+    if (!c || !c->fused || c->stream != c0->stream || c->cfg.device != c0->cfg.device) return SCALESIM_E_INVALID;
+  }
+  // (1) score: interaction pair scans (if any) and the deferred score of every instance
+  for (uint32_t i = 0; i < n; ++i) {
+    scalesim_status s = scalesim_score(ctxs[i], now, nullptr);
+    if (s != SCALESIM_OK) return s;
+  }
+  // (2) plan: chunks of instances, each instance on its own group of CTAs, one launch each
+  const uint32_t sms = (uint32_t)c0->sms;
+  uint32_t i0 = 0;
+  while (i0 < n) {
+    uint32_t k = n - i0 < sms ? n - i0 : sms;
+    if (k > (uint32_t)FUSED_MAX_BATCH) k = FUSED_MAX_BATCH;
+    uint32_t gsize, tile;
+    while (true) {
+      gsize = sms / k;
+      uint64_t nm = 0;
+      for (uint32_t i = i0; i < i0 + k; ++i) nm = ctxs[i]->p.n_local > nm ? ctxs[i]->p.n_local : nm;
+      uint64_t t = (nm + gsize - 1) / gsize;
+      t = (t + 31) / 32 * 32;
+      tile = (uint32_t)(t ? t : 32);
+      if (tile <= FUSED_MAX_TILE || k == 1) break;
+      k = k / 2;  // fewer instances per launch, more CTAs each
+    }
+    if (tile > FUSED_MAX_TILE || !fused_prepare((int)(k * gsize), tile)) return SCALESIM_E_INVALID;
+    FusedInst insts[FUSED_MAX_BATCH];
+    for (uint32_t i = 0; i < k; ++i) insts[i] = fused_inst(ctxs[i0 + i], tile);
+    c0->launches += launch_fused_batch(insts, k, gsize, c0->stream);
+    CK(cudaGetLastError());
+    for (uint32_t i = i0; i < i0 + k; ++i) {
+      scalesim_ctx *c = ctxs[i];
+      c->fused_steps++;
+      c->deferred = false;
+      c->last_fused = true;
+      scalesim_status s = finish_plan(c, nullptr);
+      if (s != SCALESIM_OK) return s;
+      if ((s = scalesim_transfer(c, nullptr)) != SCALESIM_OK) return s;
+    }
+    i0 += k;
+  }
   return SCALESIM_OK;
 }
 

@@ -50,18 +50,19 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
 }
 
 // Grid barrier for a grid of co-resident CTAs.  bar counts arrivals within one launch; the
-// k-th barrier waits for k * gridDim.x arrivals.  Launch L uses bar[L & 1]; launch L-1 reset it
+// k-th barrier waits for k * n arrivals (n = CTAs of the instance).  Launch L uses bar[L & 1]; launch L-1 reset it
 // (same stream, so every CTA of launch L-2 had finished).
 struct GridBar {
   unsigned int *bar;
   unsigned int k;
+  unsigned int n;  // CTAs of this instance
   __device__ __forceinline__ void sync() {
     __syncthreads();
     if (threadIdx.x == 0) {
       ++k;
       __threadfence();
       atomicAdd(bar, 1u);
-      const unsigned int target = k * gridDim.x;
+      const unsigned int target = k * n;
       while (ld_acquire(bar) < target) __nanosleep(40);  // back off: 148 CTAs poll one line
       __threadfence();
     }
@@ -69,11 +70,18 @@ struct GridBar {
   }
 };
 
+// Kernel arguments: a batch of independent planner instances (one per context; C5's
+// replicas x budgets), each planned by its own group of B.gsize CTAs.  A single context is
+// a batch of one whose group spans every SM.
 struct FusedArgs {
-  Params p;
+  uint32_t n_inst, gsize;
+  FusedInst inst[FUSED_MAX_BATCH];
+};
+
+struct InstArgs {
   int64_t now;
   int parity;
-  unsigned int epoch;  // launch number (>= 1), tags the per-CTA tie flags
+  unsigned int epoch;  // launch number of the instance (>= 1), tags the per-CTA tie flags
   uint32_t tile;       // agents per CTA, multiple of 32
   uint32_t tw;         // tile / 32
 };
@@ -274,20 +282,36 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
   }
 }
 
-__global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
-  const Params &p = A.p;
+__global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ FusedArgs B) {
+  const uint32_t gi = blockIdx.x / B.gsize;
+  const uint32_t c = blockIdx.x % B.gsize, G = B.gsize;
+  const FusedInst &I = B.inst[gi];
+  __shared__ __align__(16) Params sp;  // the instance's parameters (device copy + per-launch fields)
+  {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(I.params);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(&sp);
+    for (uint32_t q = threadIdx.x; q < sizeof(Params) / 4; q += FT) dst[q] = src[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sp.rec = I.rec;
+    sp.kin = I.kin;
+    sp.cur = (int)I.cur;
+  }
+  __syncthreads();
+  const Params &p = sp;
+  const InstArgs A = {I.now, (int)I.parity, I.epoch, I.tile, I.tile / 32};
   const Dev &d = p.d;
-  GridBar grid{d.f_bar + A.parity, 0u};
+  GridBar grid{d.f_bar + A.parity, 0u, G};
   unsigned long long *prof = d.f_prof;
   if (threadIdx.x == 0) {
     const unsigned long long t = gtimer();
     atomicMin(&prof[0], t);
-    if (blockIdx.x == 0) prof[2] = t;
+    if (c == 0) prof[2] = t;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) d.f_bar[A.parity ^ 1] = 0u;  // for launch L+1
+  if (c == 0 && threadIdx.x == 0) d.f_bar[A.parity ^ 1] = 0u;  // for launch L+1
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const FSmem s = carve(smem_raw, A.tile, A.tw);
-  const uint32_t c = blockIdx.x, G = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = (uint64_t)c * A.tile;
   const uint32_t n_here =
@@ -731,7 +755,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(FusedArgs A) {
 // host side
 bool fused_supported(const Params &p, int grid, uint32_t *tile_out) {
   if (p.world != 1 || grid <= 0 || grid > FUSED_MAX_CTAS) return false;
-  uint64_t tile = (p.n_local + grid - 1) / grid;
+  uint64_t tile = (p.n_local + grid - 1) / grid;  // grid = CTAs of the instance
   tile = (tile + 31) / 32 * 32;
   if (tile == 0) tile = 32;
   if (tile > FUSED_MAX_TILE) return false;
@@ -750,16 +774,16 @@ bool fused_prepare(int grid, uint32_t tile) {
   return per_sm >= 1 && grid >= 1;
 }
 
-int launch_fused_plan(const Params &p, int64_t now, int parity, unsigned int epoch, int grid, uint32_t tile,
-                      cudaStream_t s) {
-  FusedArgs A;
-  A.p = p;
-  A.now = now;
-  A.parity = parity;
-  A.epoch = epoch;
-  A.tile = tile;
-  A.tw = tile / 32;
-  k_fused_plan<<<grid, FT, fused_smem_bytes(tile), s>>>(A);
+int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s) {
+  FusedArgs B;
+  B.n_inst = n;
+  B.gsize = gsize;
+  uint32_t tile = 32;
+  for (uint32_t i = 0; i < n; ++i) {
+    B.inst[i] = insts[i];
+    tile = insts[i].tile > tile ? insts[i].tile : tile;
+  }
+  k_fused_plan<<<n * gsize, FT, fused_smem_bytes(tile), s>>>(B);
   return 1;
 }
 

@@ -53,7 +53,7 @@ struct Layout {
   uint64_t page_first, page_table, ring, pool, desc[2];
   // fused path (double-buffered by fused-step parity where noted)
   uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_cpf, f_cta_cev, f_tot, f_acc, f_tie_val, f_tie_flag;
-  uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes;
+  uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes, params_dev;
   uint64_t total;
 };
 
@@ -92,6 +92,7 @@ struct Dev {
   unsigned long long *f_tie_val;                        // [CTAS] tie bytes per CTA
   unsigned int *f_tie_flag;                             // [CTAS] launch epoch of f_tie_val
   uint32_t *wb_bytes;                                   // [n_local] KV+HIST bytes per agent (R13)
+  uint8_t *params_dev;                                  // device copy of the context's Params (fused path)
   uint32_t *f_sk2, *f_sv2, *f_sk3, *f_sv3;              // [n_local] evict-segment sort scratch
   unsigned int *f_bar;                                  // [2] grid-barrier counters
   unsigned long long *f_prof;                           // [16] globaltimer stamps of the last fused launch
@@ -133,8 +134,16 @@ int launch_transfer(const Params &p, cudaStream_t s, int ctas);
 int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s);
 int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s);
 bool fused_supported(const Params &p, int grid, uint32_t *tile_out);
-int launch_fused_plan(const Params &p, int64_t now, int parity, unsigned int epoch, int grid, uint32_t tile,
-                      cudaStream_t s);
+// one instance of a fused launch (see fused.cu)
+struct FusedInst {
+  const Params *params;  // device copy of the context's Params (static fields)
+  const uint4 *rec;
+  const float4 *kin;
+  int64_t now;
+  uint32_t cur, parity, epoch, tile;
+};
+constexpr int FUSED_MAX_BATCH = 160;
+int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s);
 bool fused_prepare(int grid, uint32_t tile);
 size_t fused_smem_bytes(uint32_t tile);
 

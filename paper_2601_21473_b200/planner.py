@@ -246,3 +246,13 @@ class Planner:
             pass
 
 
+
+
+def step_batch(planners, now: int):
+    """One step of several independent planners (replicas / sweep points) sharing one stream:
+    scalesim_step_batch plans them in as few launches as possible."""
+    if not planners:
+        return
+    lib = planners[0].lib
+    arr = (C.c_void_p * len(planners))(*[pl.ctx.value for pl in planners])
+    L.check(lib.scalesim_step_batch(arr, len(planners), int(now)), "scalesim_step_batch")

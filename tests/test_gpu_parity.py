@@ -173,3 +173,40 @@ def test_fused_multi_level_select_and_segments():
     run_parity(w, transfer=False)
     run_parity(w, transfer=False, multi_kernel=True)
     run_parity(w)
+
+
+def test_c5_batch_replicas_vs_oracle():
+    """BASELINE configs[4] shape: independent replicas x budgets planned by one batched
+    launch (scalesim_step_batch); every instance equals its own oracle run."""
+    import torch
+    from paper_2601_21473_b200.planner import Planner, step_batch
+    replicas, budgets, n, steps = 3, (10, 40, 90), 2000, 10
+    ws = [tg.config_c5(replica=r, budget_pct=10, steps=steps, n=n) for r in range(replicas)]
+    stream = torch.cuda.Stream()
+    inst = []
+    for r, w in enumerate(ws):
+        total = int(w.footprint.sum())
+        for pct in budgets:
+            b = w.blocks
+            budget = total * pct // 100
+            pl = Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, w.theta,
+                         transfer=False, stream=stream)
+            assert pl.fused
+            inst.append(dict(pl=pl, w=w, budget=budget, res=np.zeros(n, np.uint8)))
+    for s in range(steps):
+        for it in inst:
+            it["pl"].set_records(it["w"].rec[s])
+        step_batch([it["pl"] for it in inst], int(ws[0].now[s]))
+        for it in inst:
+            w = it["w"]
+            hdr = it["pl"].sync()
+            d, _ = oracle.score(w.rec[s], None, int(w.now[s]))
+            p = oracle.plan(w.rec[s], d, it["res"], w.theta, it["budget"])
+            pf, ev = it["pl"].lists(hdr)
+            assert np.array_equal(pf, p["prefetch"]) and np.array_equal(ev, p["evict"]), s
+            assert np.array_equal(it["pl"].resident(), p["resident"])
+            assert hdr["cut_bits"] == p["cut_bits"] and hdr["cut_rem"] == p["cut_rem"]
+            assert hdr["kept_bytes"] == p["kept_bytes"] and hdr["bytes_h2d"] == p["bytes_h2d"]
+            it["res"] = p["resident"]
+    for it in inst:
+        it["pl"].close()
