@@ -227,6 +227,51 @@ def transfer_leg(torch, dev, seed):
                                         "host arena 8 GiB (offsets aliased), SM-driven page copies"}
 
 
+def c5_leg(torch, dev, rank, world, replicas=64, budgets=tuple(range(10, 100, 10)), steps=8, warm=8, seed_base=100):
+    """C5: independent simulation replicas x budget sizes, instances sharded over the ranks
+    (instance i on rank i % world), all of a rank's instances stepped by scalesim_step_batch.
+    Returns this rank's agent-plans and the device time of the timed steps."""
+    from paper_2601_21473_b200.planner import Planner, step_batch
+    T = warm + steps
+    mine = [(r, pct) for i, (r, pct) in enumerate((r, p) for r in range(replicas) for p in budgets) if i % world == rank]
+    reps = sorted({r for r, _ in mine})
+    traces = {r: tg.config_c5(replica=r, budget_pct=10, seed_base=seed_base, steps=T) for r in reps}
+    recs = {r: torch.from_numpy(np.ascontiguousarray(traces[r].rec).view(np.uint8).reshape(T, -1)).to(dev) for r in reps}
+    stream = torch.cuda.Stream(dev)
+    pls = []
+    for r, pct in mine:
+        w = traces[r]
+        b = w.blocks
+        budget = int(w.footprint.sum()) * pct // 100
+        pls.append((r, Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, w.theta,
+                               transfer=False, device=dev.index, stream=stream)))
+
+    def one(s):
+        for r, pl in pls:
+            pl.set_inputs_ptr(recs[r][s].data_ptr())
+        step_batch([pl for _, pl in pls], int(traces[reps[0]].now[s]))
+
+    for s in range(warm):
+        one(s)
+    torch.cuda.synchronize(dev)
+    lc0 = sum(pl.launch_count() for _, pl in pls)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(2e8))
+    e0.record(stream)
+    for s in range(warm, T):
+        one(s)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    launches = sum(pl.launch_count() for _, pl in pls) - lc0
+    n_agents = sum(traces[r].n for r, _ in pls)
+    for _, pl in pls:
+        pl.close()
+    return {"instances": len(pls), "agents_per_step": n_agents, "steps": steps, "ms": ms,
+            "launches": launches}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -239,6 +284,8 @@ def main():
     ap.add_argument("--no-transfer-leg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=32)
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 replicas x budgets leg")
+    ap.add_argument("--c5-replicas", type=int, default=64)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -394,8 +441,25 @@ def main():
            "d2h_bytes_per_step": d2h_b // e2e_k, "steps": e2e_k,
            "api": "scalesim_step_host (pinned host records in, header + lists out, synchronous)"}
 
+    pl.close()
+    c5 = None
+    if not args.no_c5:
+        if world > 1:
+            dist.barrier()
+        r5 = c5_leg(torch, dev, rank, world, replicas=args.c5_replicas)
+        if world > 1:
+            t = torch.tensor([r5["ms"], r5["agents_per_step"]], dtype=torch.float64, device=dev)
+            mx = t.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = t.clone()
+            dist.all_reduce(sm)
+            r5["ms"], r5["agents_per_step"] = float(mx[0].item()), int(sm[1].item())
+        c5 = {"value": r5["agents_per_step"] * r5["steps"] / (r5["ms"] / 1e3), "unit": "agent-plans/s",
+              "workload": f"c5: {args.c5_replicas} replicas x 9 budgets (10..90%) of the C2 shape (10k agents), "
+                          f"instances sharded over {world} GPU(s), scalesim_step_batch",
+              "instances_per_gpu": r5["instances"], "steps": r5["steps"], "ms_per_step": r5["ms"] / r5["steps"],
+              "gpu_launches": r5["launches"]}
     if rank != 0:
-        pl.close()
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
@@ -437,7 +501,8 @@ def main():
                        "l2": f"{K} distinct 16 MB record buffers (> 126 MB L2)", "timing": mode,
                        "last_plan": {k: hdr[k] for k in ("n_prefetch", "n_evict", "cut_bits", "status")}},
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": sampler.result()}
-    pl.close()
+    if c5 is not None:
+        line["c5"] = c5
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     if not args.no_transfer_leg:
