@@ -185,6 +185,9 @@ scalesim_status scalesim_plan(scalesim_ctx *ctx, scalesim_plan_view *out);
  * done_event.  Requires the most recent plan. */
 scalesim_status scalesim_transfer(scalesim_ctx *ctx, const scalesim_plan_view *plan);
 
+/* Fill *out with the views of the context's latest plan (e.g. after scalesim_step_batch). */
+scalesim_status scalesim_view(scalesim_ctx *ctx, scalesim_plan_view *out);
+
 /* score + plan + transfer of one step. */
 scalesim_status scalesim_step(scalesim_ctx *ctx, int64_t now_tick, scalesim_plan_view *out);
 

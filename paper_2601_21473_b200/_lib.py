@@ -30,7 +30,7 @@ HEADER_NAMES = ["n_prefetch", "n_evict", "bytes_h2d", "bytes_d2h", "cut_bits", "
 
 # Every symbol include/scalesim.h declares (checked by tests/test_abi.py).
 EXPORTS = ["scalesim_workspace_bytes", "scalesim_init", "scalesim_score", "scalesim_plan",
-           "scalesim_transfer", "scalesim_step", "scalesim_step_batch", "scalesim_step_host", "scalesim_set_inputs",
+           "scalesim_transfer", "scalesim_view", "scalesim_step", "scalesim_step_batch", "scalesim_step_host", "scalesim_set_inputs",
            "scalesim_sync", "scalesim_join", "scalesim_nccl_unique_id", "scalesim_fused", "scalesim_profile_stamps", "scalesim_launch_count", "scalesim_destroy",
            "scalesim_strerror"]
 
@@ -102,6 +102,8 @@ def lib():
         L.scalesim_plan.restype = C.c_int
         L.scalesim_transfer.argtypes = [vp, C.POINTER(PlanView)]
         L.scalesim_transfer.restype = C.c_int
+        L.scalesim_view.argtypes = [vp, C.POINTER(PlanView)]
+        L.scalesim_view.restype = C.c_int
         L.scalesim_step.argtypes = [vp, i64, C.POINTER(PlanView)]
         L.scalesim_step.restype = C.c_int
         L.scalesim_step_batch.argtypes = [C.POINTER(vp), C.c_uint32, i64]

@@ -633,6 +633,13 @@ static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out) {
   return SCALESIM_OK;
 }
 
+extern "C" scalesim_status scalesim_view(scalesim_ctx *c, scalesim_plan_view *out) {
+  if (!c || !out) return SCALESIM_E_INVALID;
+  if (!c->planned) return SCALESIM_E_ORDER;
+  fill_plan(c, out);
+  return SCALESIM_OK;
+}
+
 extern "C" scalesim_status scalesim_transfer(scalesim_ctx *c, const scalesim_plan_view *plan) {
   if (!c) return SCALESIM_E_INVALID;
   if (!c->planned || c->transferred) return SCALESIM_E_ORDER;

@@ -256,3 +256,5 @@ def step_batch(planners, now: int):
     lib = planners[0].lib
     arr = (C.c_void_p * len(planners))(*[pl.ctx.value for pl in planners])
     L.check(lib.scalesim_step_batch(arr, len(planners), int(now)), "scalesim_step_batch")
+    for pl in planners:
+        L.check(lib.scalesim_view(pl.ctx, C.byref(pl.view)), "scalesim_view")
