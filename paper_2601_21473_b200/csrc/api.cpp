@@ -79,8 +79,8 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.page_table = take(4 * (L.n_block_pages ? L.n_block_pages : 1));
   L.ring = take(4 * (L.n_dev_pages ? L.n_dev_pages : 1));
   L.pool = take(16);
-  L.desc[0] = take(16 + 32 * (L.desc_cap ? L.desc_cap : 1));
-  L.desc[1] = take(16 + 32 * (L.desc_cap ? L.desc_cap : 1));
+  L.desc[0] = take(8 * DESC_HDR + 32 * (L.desc_cap ? L.desc_cap : 1));
+  L.desc[1] = take(8 * DESC_HDR + 32 * (L.desc_cap ? L.desc_cap : 1));
   L.f_hist1 = take(8 * 2 * 4096);
   L.f_mm1 = take(4 * 2 * 2 * 4096);
   L.f_hist2 = take(8 * 2 * 1024);
@@ -213,7 +213,8 @@ struct scalesim_ctx {
   Layout L;
   Params p;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
-  cudaEvent_t ev_plan = nullptr, ev_xfer[2] = {nullptr, nullptr};
+  cudaEvent_t ev_plan = nullptr, ev_xfer[2] = {nullptr, nullptr}, ev_side = nullptr;
+  cudaStream_t copy_stream2 = nullptr;  // library-owned: loads that do not wait for write-backs
   bool transfer = false;
   int grid = 592;
   int copy_ctas = 64;
@@ -348,6 +349,9 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
     scalesim_destroy(c);
     return s;
   };
+  if (cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy_stream2, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(SCALESIM_E_CUDA);
   if (cudaEventCreateWithFlags(&c->ev_plan, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_xfer[0], cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_xfer[1], cudaEventDisableTiming) != cudaSuccess)
@@ -454,11 +458,12 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
             ++nh;
           }
       // layout of a descriptor buffer: [n_d2h, n_h2d, d2h pairs (desc_cap), h2d pairs]
-      std::vector<uint64_t> buf(2 + 4 * (L.desc_cap ? L.desc_cap : 1), 0);
+      std::vector<uint64_t> buf(DESC_HDR + 4 * (L.desc_cap ? L.desc_cap : 1), 0);
       buf[0] = 0;
       buf[1] = nh;
+      buf[2] = nh;  // every initial load is independent
       if (nh > L.desc_cap) return fail(SCALESIM_E_INVALID);
-      for (uint64_t k = 0; k < 2 * nh; ++k) buf[2 + 2 * L.desc_cap + k] = desc[2 + k];
+      for (uint64_t k = 0; k < 2 * nh; ++k) buf[DESC_HDR + 2 * L.desc_cap + k] = desc[2 + k];
       if (cudaMemcpy(p.d.desc[0], buf.data(), 8 * buf.size(), cudaMemcpyHostToDevice) != cudaSuccess)
         return fail(SCALESIM_E_CUDA);
       p.desc_buf = 0;
@@ -538,8 +543,8 @@ static void fill_plan(scalesim_ctx *c, scalesim_plan_view *out) {
   out->resident_bitmap = p.d.bm[p.cur];  // after the flip: the new residency
   out->dist = reinterpret_cast<const float *>(p.d.keys);
   out->page_table = p.d.page_table;
-  out->d2h_desc = reinterpret_cast<const uint64_t *>(p.d.desc[c->last_buf] + 2);
-  out->h2d_desc = reinterpret_cast<const uint64_t *>(p.d.desc[c->last_buf] + 2 + 2 * p.desc_cap);
+  out->d2h_desc = reinterpret_cast<const uint64_t *>(p.d.desc[c->last_buf] + DESC_HDR);
+  out->h2d_desc = reinterpret_cast<const uint64_t *>(p.d.desc[c->last_buf] + DESC_HDR + 2 * p.desc_cap);
   out->header = reinterpret_cast<const uint64_t *>(p.d.header);
   out->done_event = c->ev_xfer[c->last_buf];
 }
@@ -647,10 +652,13 @@ extern "C" scalesim_status scalesim_transfer(scalesim_ctx *c, const scalesim_pla
   const int buf = c->last_buf;
   if (c->transfer) {
     CK(cudaStreamWaitEvent(c->copy_stream, c->ev_plan, 0));
+    CK(cudaStreamWaitEvent(c->copy_stream2, c->ev_plan, 0));
     Params q = c->p;
     q.desc_buf = buf;
-    c->launches += launch_transfer(q, c->copy_stream, c->copy_ctas);
+    c->launches += launch_transfer_split(q, c->copy_stream, c->copy_stream2, c->copy_ctas);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_side, c->copy_stream2));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->ev_side, 0));
     CK(cudaEventRecord(c->ev_xfer[buf], c->copy_stream));
     c->xfer_pending = true;
   }
@@ -771,6 +779,11 @@ extern "C" void scalesim_destroy(scalesim_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->copy_stream2) {
+    cudaStreamSynchronize(c->copy_stream2);
+    cudaStreamDestroy(c->copy_stream2);
+  }
+  if (c->ev_side) cudaEventDestroy(c->ev_side);
   if (c->ev_plan) cudaEventDestroy(c->ev_plan);
   for (int k = 0; k < 2; ++k)
     if (c->ev_xfer[k]) cudaEventDestroy(c->ev_xfer[k]);

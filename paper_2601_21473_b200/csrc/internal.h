@@ -10,6 +10,7 @@ constexpr uint32_t TILE = 2048;           // agents per tile (id-ordered kernels
 constexpr uint32_t SORT_CH = 8192;        // list elements per sort chunk
 constexpr uint32_t EXP_CH = 256;          // list entries per expansion chunk
 constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;
+constexpr int DESC_HDR = 4;  // descriptor buffer: n_d2h, n_h2d, n_h2d_independent, 0, then pairs
 constexpr uint32_t PAGE_NONE = 0xFFFFFFFFu;
 constexpr int L1_BITS = 11, L2_BITS = 10, L3_BITS = 10;  // distance-bit digits [30:20] [19:10] [9:0]
 constexpr int FUSED_MAX_CTAS = 160;       // fused path: one CTA per SM (B200: 148)
@@ -131,6 +132,7 @@ int launch_emit(const Params &p, cudaStream_t s);
 int launch_lists(const Params &p, cudaStream_t s);
 int launch_expand(const Params &p, cudaStream_t s);
 int launch_transfer(const Params &p, cudaStream_t s, int ctas);
+int launch_transfer_split(const Params &p, cudaStream_t s, cudaStream_t s2, int ctas);
 int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s);
 int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s);
 bool fused_supported(const Params &p, int grid, uint32_t *tile_out);

@@ -659,6 +659,10 @@ __global__ void __launch_bounds__(NT) k_exp_scan(Params p, uint64_t max_chunks) 
     H[H_N_H2D] = t2;
     desc[0] = t1;
     desc[1] = t2;
+    // prefetched pages popped below the old tail were free before this step's releases: their
+    // loads do not wait for the write-backs (D2H and H2D then run concurrently)
+    desc[2] = t2 < tail - head ? t2 : tail - head;
+    desc[3] = 0;
     // free pages after releasing = tail + t0 - head; the prefetch must fit (always true when
     // dev pages >= budget pages; flagged otherwise)
     if (t2 > tail + t0 - head) {
@@ -696,7 +700,7 @@ __global__ void __launch_bounds__(NT) k_pages(Params p, uint64_t max_chunks) {
   __syncthreads();
   const unsigned long long head = p.d.pool[0], tail = p.d.pool[1];
   const unsigned long long npg = p.n_dev_pages;
-  unsigned long long *desc = p.d.desc[p.desc_buf] + 2;  // pairs after the two counters
+  unsigned long long *desc = p.d.desc[p.desc_buf] + DESC_HDR;  // pairs after the counters
   unsigned long long *d2h = desc;
   unsigned long long *h2d = desc + 2 * p.desc_cap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -779,13 +783,17 @@ __global__ void k_init_page_table(Params p, uint64_t n_block_pages) {
 // 128-bit loads (16 per thread for 64 KiB) before its stores, so a CTA keeps a whole page
 // in flight across PCIe; the grid is small (the copy overlaps the next plan).
 
-template <bool D2H>
+// MODE 0: write-backs (device page -> host), all; MODE 1: loads (host -> device page)
+// [0, n_indep); MODE 2: loads [n_indep, n_h2d) (after the write-backs).
+template <int MODE>
 __global__ void __launch_bounds__(NT) k_copy_pages(const unsigned long long *desc_base, uint8_t *host, uint8_t *dev,
                                                   uint64_t page_bytes, uint64_t desc_cap) {
-  const unsigned long long n = desc_base[D2H ? 0 : 1];
-  const unsigned long long *desc = desc_base + 2 + (D2H ? 0 : 2 * desc_cap);
+  constexpr bool D2H = MODE == 0;
+  const unsigned long long lo = MODE == 2 ? desc_base[2] : 0ull;
+  const unsigned long long hi = MODE == 0 ? desc_base[0] : (MODE == 1 ? desc_base[2] : desc_base[1]);
+  const unsigned long long *desc = desc_base + DESC_HDR + (D2H ? 0 : 2 * desc_cap);
   const uint32_t vec_per_page = (uint32_t)(page_bytes / 16);
-  for (unsigned long long k = blockIdx.x; k < n; k += gridDim.x) {
+  for (unsigned long long k = lo + blockIdx.x; k < hi; k += gridDim.x) {
     const unsigned long long hoff = desc[2 * k];
     const unsigned long long pg = desc[2 * k + 1];
     const uint4 *src = reinterpret_cast<const uint4 *>(D2H ? dev + pg * page_bytes : host + hoff);
@@ -897,9 +905,20 @@ int launch_expand(const Params &p, cudaStream_t s) {
 
 int launch_transfer(const Params &p, cudaStream_t s, int ctas) {
   const unsigned long long *desc = p.d.desc[p.desc_buf];
-  k_copy_pages<true><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
-  k_copy_pages<false><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
-  return 2;
+  k_copy_pages<0><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  k_copy_pages<1><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  k_copy_pages<2><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  return 3;
+}
+
+// write-backs on s, independent loads concurrently on s2, dependent loads on s after the
+// write-backs; the caller joins s2 back into s
+int launch_transfer_split(const Params &p, cudaStream_t s, cudaStream_t s2, int ctas) {
+  const unsigned long long *desc = p.d.desc[p.desc_buf];
+  k_copy_pages<0><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  k_copy_pages<1><<<ctas, NT, 0, s2>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  k_copy_pages<2><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  return 3;
 }
 
 int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s) {
