@@ -513,7 +513,7 @@ def main():
         # (full-duplex PCIe), each at the cudaMemcpy peak measured in this run
         ideal_s = max(tl["h2d_bytes_per_step"] / (lp["h2d_GBs"] * 1e9), tl["d2h_bytes_per_step"] / (lp["d2h_GBs"] * 1e9))
         tl["frac_of_link"] = ideal_s / max(tl["bytes_per_step"] / (tl["GBs"] * 1e9), 1e-12)
-        tl["frac_definition"] = "max(h2d/h2d_peak, d2h/d2h_peak) / measured transfer time per step
+        tl["frac_definition"] = "max(h2d/h2d_peak, d2h/d2h_peak) / measured transfer time per step"
         line["transfer"] = tl
     line["cpu"] = {"cores": os.cpu_count()}
     print(json.dumps(line), flush=True)
