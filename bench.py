@@ -244,7 +244,7 @@ def c5_leg(torch, dev, rank, world, replicas=64, budgets=tuple(range(10, 100, 10
         b = w.blocks
         budget = int(w.footprint.sum()) * pct // 100
         pls.append((r, Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, w.theta,
-                               transfer=False, device=dev.index, stream=stream)))
+                               transfer=False, device=dev.index, stream=stream, keep_dist=False)))
 
     def one(s):
         for r, pl in pls:
@@ -325,7 +325,7 @@ def main():
     b = w.blocks
     pl = Planner(n * world, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, w.theta,
                  transfer=False, device=local, shard=(rank * n, (rank + 1) * n), rank=rank, world=world,
-                 nccl_id=nccl_id)
+                 nccl_id=nccl_id, keep_dist=False)
     # all step records resident in HBM (T distinct 16 MB buffers, > L2)
     recs = torch.from_numpy(np.ascontiguousarray(w.rec).view(np.uint8).reshape(T, -1)).to(dev)
     ptr = [recs[s].data_ptr() for s in range(T)]

@@ -67,7 +67,8 @@ typedef enum {
 /* Config flags. */
 #define SCALESIM_F_NO_TRANSFER 1u   /* plan + byte accounting only: no arena, no pages, no copies
                                        (logical sizes, BASELINE configs 4 and 5) */
-#define SCALESIM_F_KEEP_DIST 2u     /* keep per-agent distances readable after plan (dist view) */
+#define SCALESIM_F_KEEP_DIST 2u     /* keep per-agent distances readable after plan (dist view); the
+                                       single-kernel path skips writing them otherwise */
 #define SCALESIM_F_MULTI_KERNEL 4u  /* force the multi-kernel plan path (otherwise, at world == 1 and
                                        <= 16384 agents per SM, one persistent cooperative kernel
                                        scores and plans the step; both paths give identical plans) */

@@ -92,6 +92,9 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_acc = take(8 * 2 * 8);
   L.f_tie_val = take(8 * (uint64_t)FUSED_MAX_CTAS);
   L.f_tie_flag = take(4 * (uint64_t)FUSED_MAX_CTAS);
+  L.f_rows1 = take(8 * (uint64_t)FUSED_MAX_CTAS * 4096);
+  L.f_rows2 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
+  L.f_rows3 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
   L.wb_bytes = take(4 * n1);
   L.params_dev = take(sizeof(Params));
   L.f_sk2 = take(4 * n1);
@@ -160,6 +163,9 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_acc = (unsigned long long *)(b + L.f_acc);
   d.f_tie_val = (unsigned long long *)(b + L.f_tie_val);
   d.f_tie_flag = (unsigned int *)(b + L.f_tie_flag);
+  d.f_rows1 = (unsigned long long *)(b + L.f_rows1);
+  d.f_rows2 = (unsigned long long *)(b + L.f_rows2);
+  d.f_rows3 = (unsigned long long *)(b + L.f_rows3);
   d.wb_bytes = (uint32_t *)(b + L.wb_bytes);
   d.params_dev = (uint8_t *)(b + L.params_dev);
   d.f_sk2 = (uint32_t *)(b + L.f_sk2);
@@ -381,6 +387,7 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
   p.dev_arena = static_cast<uint8_t *>(t->dev_arena);
   p.cur = 0;
   p.desc_buf = 0;
+  p.keep_dist = (cfg->flags & SCALESIM_F_KEEP_DIST) ? 1 : 0;
   p.d = make_dev(t->workspace, L);
 
   // Host-side validation of the block table: sizes are page multiples, CSR is monotone,

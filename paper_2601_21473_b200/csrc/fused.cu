@@ -36,6 +36,7 @@ constexpr int FWARPS = FT / 32;
 constexpr int NB1 = 4096;  // level-1 buckets: distance bits [30:19]
 constexpr int NBL = 1024;  // list-sort buckets: distance bits [30:21]
 constexpr int LOAD_BATCH = 8;  // records in flight per thread in P1
+constexpr uint32_t RANK_MAX = 4096;  // P6: longer segments are radix-sorted by one CTA
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -140,10 +141,13 @@ __device__ __forceinline__ void hist_lane(uint32_t *h, int nb, uint32_t b, uint3
   atomicMin(&h[3 * nb + b], ~bits);
 }
 
-// add this CTA's histogram to the global one (nonzero buckets only)
-__device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned long long *g_hist, uint32_t *g_mm) {
+// this CTA's histogram: dense row (row[b] = bytes) and added to the global one (nonzero
+// buckets only)
+__device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned long long *g_hist, uint32_t *g_mm,
+                                             unsigned long long *row) {
   for (int b = threadIdx.x; b < nb; b += FT) {
     const unsigned long long v = ((unsigned long long)h[nb + b] << 16) + h[b];
+    row[b] = v;
     if (v != 0) {
       atomicAdd(&g_hist[b], v);
       if (g_mm) {
@@ -157,7 +161,7 @@ __device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned
 struct Sel {
   uint32_t prefix;
   unsigned long long below, rem;
-  uint32_t dstar, all_fit, done;
+  uint32_t dstar, all_fit, done, level_res, b_res;  // bucket (and level) holding the agents at D*
 };
 
 // Boundary bucket of histogram level `level` (every CTA computes the same result).
@@ -203,15 +207,18 @@ __device__ void select_level(const unsigned long long *g_hist, const uint32_t *g
       sel.dstar = (level == 3) ? sel.prefix : g_mm[b];
       sel.rem = budget - sel.below;
       sel.done = 1;
+      sel.level_res = level;
+      sel.b_res = b;
     }
   }
   __syncthreads();
 }
 
 // Stable sort of a segment of n (key, id) pairs by key, ascending, for one CTA: LSD radix
-// sort with 8-bit digits over the varying bits only.  Warp w owns the contiguous range
-// [w*L, (w+1)*L) of the input, so (digit, warp, position) order is stable.  cnt: 8192 words
-// of shared memory.  Buffers may be shared or global memory.  Result in (ka, ia).
+// sort with 8-bit digits over the varying bits only.  Warp w < SW owns the contiguous range
+// [w*L, (w+1)*L) of the input, so (digit, warp, position) order is stable.  cnt: 256 * SW
+// words of shared memory.  Buffers may be shared or global memory.  Result in (ka, ia).
+constexpr int SW = 16;
 __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_t *ib, uint32_t n, uint32_t *cnt) {
   if (n <= 1) return;
   __shared__ uint32_t sh_or, sh_and, sh_tot;
@@ -234,26 +241,26 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
   __syncthreads();
   const uint32_t varying = sh_or ^ sh_and;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t L = (n + FWARPS - 1) / FWARPS;
-  const uint32_t lo = min(n, warp * L), hi = min(n, lo + L);
+  const uint32_t L = (n + SW - 1) / SW;
+  const uint32_t lo = warp < SW ? min(n, warp * L) : n, hi = warp < SW ? min(n, lo + L) : n;
   for (int shift = 0; shift < 32; shift += 8) {
     if (((varying >> shift) & 0xFFu) == 0) continue;
-    // cnt[d * 32 + w]: members of digit d in warp w's range
-    for (int b = threadIdx.x; b < 256 * FWARPS; b += FT) cnt[b] = 0;
+    // cnt[d * SW + w]: members of digit d in warp w's range
+    for (int b = threadIdx.x; b < 256 * SW; b += FT) cnt[b] = 0;
     __syncthreads();
-    for (uint32_t e = lo + lane; e < hi; e += 32) atomicAdd(&cnt[((ka[e] >> shift) & 0xFFu) * FWARPS + warp], 1u);
+    for (uint32_t e = lo + lane; e < hi; e += 32) atomicAdd(&cnt[((ka[e] >> shift) & 0xFFu) * SW + warp], 1u);
     __syncthreads();
-    {  // exclusive scan in (digit, warp) order: 8 consecutive entries per thread
-      uint32_t v[8], sum = 0;
+    {  // exclusive scan in (digit, warp) order: 4 consecutive entries per thread
+      uint32_t v[4], sum = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        v[j] = cnt[threadIdx.x * 8 + j];
+      for (int j = 0; j < 4; ++j) {
+        v[j] = cnt[threadIdx.x * 4 + j];
         sum += v[j];
       }
       uint32_t ex = block_excl_scan<uint32_t, FT>(sum, &sh_tot);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        cnt[threadIdx.x * 8 + j] = ex;
+      for (int j = 0; j < 4; ++j) {
+        cnt[threadIdx.x * 4 + j] = ex;
         ex += v[j];
       }
     }
@@ -265,12 +272,12 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
       const uint32_t dg = valid ? ((k >> shift) & 0xFFu) : 0xFFFFFFFFu;
       const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dg);
       if (valid) {
-        const uint32_t pos = cnt[dg * FWARPS + warp] + __popc(peers & lanemask_lt());
+        const uint32_t pos = cnt[dg * SW + warp] + __popc(peers & lanemask_lt());
         kb[pos] = k;
         ib[pos] = id;
       }
       __syncwarp();
-      if (valid && (peers & lanemask_lt()) == 0) cnt[dg * FWARPS + warp] += __popc(peers);
+      if (valid && (peers & lanemask_lt()) == 0) cnt[dg * SW + warp] += __popc(peers);
       __syncwarp();
     }
     __syncthreads();
@@ -325,6 +332,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   uint32_t *bm_new = d.bm[p.cur ^ 1];
 
   // ---------------- P1: score + level-1 histogram
+  // per-thread copies of the parameters used per agent (Params lives in shared memory)
+  const float th0 = p.theta[0], th1 = p.theta[1], th2 = p.theta[2], hop_scale = p.hop_scale;
+  const uint64_t n_kin = p.n_kin;
+  const float *dint = d.dint;
+  const uint4 *rec = p.rec + base;
+  uint32_t *gkeys = p.keep_dist ? d.keys + base : nullptr;
+  const int64_t now = A.now;
   clear_hist(s.h, NB1);
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_old[base / 32 + w] : 0u;
   __syncthreads();
@@ -335,7 +349,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
 #pragma unroll
     for (int j = 0; j < LOAD_BATCH; ++j) {  // all loads in flight before any use
       const uint32_t k = k0 + j * FT + threadIdx.x;
-      r[j] = k < n_here ? ld_stream(p.rec + base + k) : make_uint4(0, 0, 0, 0);
+      r[j] = k < n_here ? ld_stream(rec + k) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int j = 0; j < LOAD_BATCH; ++j) {
@@ -343,12 +357,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       if (k >= A.tw * 32) continue;  // warp-uniform (tw * 32 is a multiple of 32)
       const bool valid = k < n_here;
       const bool res = (s.old_w[k >> 5] >> (k & 31)) & 1u;
-      const float dist = valid ? distance_of(r[j], A.now, p.hop_scale, d.dint, p.n_kin, st) : 0.0f;
+      const float dist = valid ? distance_of(r[j], now, hop_scale, dint, n_kin, st) : 0.0f;
       const uint32_t bits = __float_as_uint(dist);
-      const bool elig = valid && (res || dist == 0.0f || dist < theta_of(p, class_of(r[j])));
+      const uint32_t cl = class_of(r[j]);
+      const float th = cl == 0u ? th0 : cl == 1u ? th1 : cl == 2u ? th2 : 0.0f;
+      const bool elig = valid && (res || dist == 0.0f || dist < th);
       s.keys[k] = bits;
       s.fp[k] = r[j].y;
-      if (valid) d.keys[base + k] = bits;
+      if (gkeys && valid) gkeys[k] = bits;
       const uint32_t eb = __ballot_sync(0xFFFFFFFFu, elig);
       const uint32_t db = __ballot_sync(0xFFFFFFFFu, valid && ((r[j].z >> 4) & 1u));
       if (lane == 0) {
@@ -360,7 +376,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
-  publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, d.f_mm1 + 2 * NB1 * par);
+  // this CTA's level-1 bytes: dense row (its column entry gives the tie prefix in P3) and
+  // the global sum
+  publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, d.f_mm1 + 2 * NB1 * par, d.f_rows1 + (uint64_t)c * NB1);
   zero_b = block_sum<unsigned long long, FT>(zero_b);
   st = __reduce_or_sync(0xFFFFFFFFu, st);
   if (lane == 0 && st) atomicOr(reinterpret_cast<unsigned int *>(&acc[5]), st);
@@ -388,8 +406,25 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
     if (gt < 8) d.f_acc[8 * q + gt] = 0;
   }
-  Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0};
-  select_level(d.f_hist1 + NB1 * par, d.f_mm1 + 2 * NB1 * par, 1, p.budget, sel);
+  const uint32_t *mm1 = d.f_mm1 + 2 * NB1 * par;
+  // list bucket lb (bits [30:21]) = level-1 buckets 4lb..4lb+3 (bits [30:19]); it holds several
+  // distances iff the min and max key over those buckets differ (list members are eligible)
+  uint32_t *lmulti = s.h + 7 * NBL;  // written after the histogram is no longer needed
+  uint32_t my_multi;
+  {
+    const uint32_t lb = threadIdx.x;  // NBL == FT
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+#pragma unroll
+    for (uint32_t q = 4 * lb; q < 4 * lb + 4; ++q) {
+      const uint32_t m = mm1[q];
+      if (m == 0xFFFFFFFFu) continue;  // empty level-1 bucket
+      lo = min(lo, m);
+      hi = max(hi, ~mm1[NB1 + q]);
+    }
+    my_multi = (lo != 0xFFFFFFFFu && lo != hi) ? 1u : 0u;
+  }
+  Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 1, 0};
+  select_level(d.f_hist1 + NB1 * par, mm1, 1, p.budget, sel);
   for (int level = 2; level <= 3 && !sel.done; ++level) {
     const int hi_shift = level == 2 ? 19 : 9, shift = level == 2 ? 9 : 0;
     const int nb = level == 2 ? 1024 : 512;
@@ -404,28 +439,26 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     __syncthreads();
     unsigned long long *gh = level == 2 ? d.f_hist2 + 1024 * par : d.f_hist3 + 1024 * par;
     uint32_t *gm = level == 2 ? d.f_mm2 + 2048 * par : nullptr;
-    publish_hist(s.h, nb, gh, gm);
+    publish_hist(s.h, nb, gh, gm, (level == 2 ? d.f_rows2 : d.f_rows3) + (uint64_t)c * 1024);
     grid.sync();
     select_level(gh, gm, level, p.budget, sel);
   }
   const bool all_fit = sel.all_fit;
   const uint32_t dstar = sel.dstar;
+  lmulti[threadIdx.x] = my_multi;  // s.h no longer holds a histogram
   if (c == 0 && threadIdx.x == 0) prof[9] = gtimer();
 
-  // ---------------- P3: tie group — this CTA's bytes at d == D*, prefix over preceding CTAs
+  // ---------------- P3: tie group: id-order prefix of the bytes at d == D*
   unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw]
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
     const bool tie = !all_fit && ((s.elig_w[w] >> lane) & 1u) && s.keys[k] == dstar;
     unsigned long long v = 0;
-    if (__ballot_sync(0xFFFFFFFFu, tie)) {  // most words hold no tie agent: skip the reduction
-      v = tie ? s.fp[k] : 0u;
-      v = warp_sum_u32_exact(tie ? s.fp[k] : 0u);
-    }
+    if (__ballot_sync(0xFFFFFFFFu, tie)) v = warp_sum_u32_exact(tie ? s.fp[k] : 0u);  // most words: no tie
     if (lane == 0) word_tie[w] = v;
   }
   __syncthreads();
-  __shared__ unsigned long long sh_tie_excl, sh_tie_total, sh_chunk;
+  __shared__ unsigned long long sh_tie_excl, sh_chunk;
   {  // exclusive scan over the tile's words
     unsigned long long carry = 0;
     for (uint32_t w0 = 0; w0 < A.tw; w0 += FT) {
@@ -437,31 +470,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       carry += sh_chunk;
       __syncthreads();
     }
-    if (threadIdx.x == 0) sh_tie_total = carry;
   }
-  __syncthreads();
-  if (!all_fit) {
-    if (threadIdx.x == 0) {  // publish: value, then the epoch flag (release)
-      d.f_tie_val[c] = sh_tie_total;
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(d.f_tie_flag + c), "r"(A.epoch) : "memory");
+  {  // preceding CTAs: their bytes in the resolving bucket (published rows; one load each)
+    unsigned long long t = 0;
+    if (!all_fit && threadIdx.x < c) {
+      const unsigned long long *rows = sel.level_res == 1 ? d.f_rows1 : (sel.level_res == 2 ? d.f_rows2 : d.f_rows3);
+      const uint32_t stride = sel.level_res == 1 ? NB1 : 1024;
+      t = rows[(uint64_t)threadIdx.x * stride + sel.b_res];
     }
-    if (warp == 0) {  // lane j reads the flags of CTAs j, j+32, ...: loads issued together
-      unsigned long long t = 0;
-      uint32_t pending = 0;
-      for (uint32_t q = lane, j = 0; q < c; q += 32, ++j)
-        if (ld_acquire(d.f_tie_flag + q) != A.epoch) pending |= 1u << j;
-      while (pending) {
-        __nanosleep(40);
-        for (uint32_t q = lane, j = 0; q < c; q += 32, ++j)
-          if (((pending >> j) & 1u) && ld_acquire(d.f_tie_flag + q) == A.epoch) pending &= ~(1u << j);
-      }
-      for (uint32_t q = lane; q < c; q += 32) t += *(volatile unsigned long long *)(d.f_tie_val + q);
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
-      if (lane == 0) sh_tie_excl = t;
-    }
-  } else if (threadIdx.x == 0) {
-    sh_tie_excl = 0;
+    t = block_sum<unsigned long long, FT>(t);
+    if (threadIdx.x == 0) sh_tie_excl = t;
   }
   __syncthreads();
   if (c == 0 && threadIdx.x == 0) prof[10] = gtimer();
@@ -512,7 +530,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   __syncthreads();
   uint32_t *cpf = d.f_cta_cpf + (uint64_t)c * NBL, *cev = d.f_cta_cev + (uint64_t)c * NBL;
   uint32_t *tot_pf = d.f_tot + 2 * NBL * par, *tot_ev = d.f_tot + 2 * NBL * par + NBL;
-  for (int b = threadIdx.x; b < NBL; b += FT) {
+  {
+    const int b = threadIdx.x;  // NBL == FT
     const uint32_t a = cnt_pf[b], e = cnt_ev[b];
     cpf[b] = a;
     cev[b] = e;
@@ -536,18 +555,21 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
 
   // ---------------- P5: stable bucket sort of the lists
   uint32_t *g_pf = s.h + 2 * NBL, *g_ev = s.h + 3 * NBL;  // first slot of this CTA's members per bucket
-  __shared__ uint32_t sh_npf, sh_nev, sh_mpf, sh_mev;
+  uint32_t *tpf = s.h + 8 * NBL, *tev = s.h + 9 * NBL;    // list bucket totals (shared copy)
+  __shared__ uint32_t sh_npf, sh_nev, sh_mpf, sh_mev, sh_need;
   {
     const uint32_t b = threadIdx.x;  // NBL == FT: one bucket per thread
     const uint32_t a = tot_pf[b];
+    tpf[b] = a;
     const uint32_t xa = block_excl_scan<uint32_t, FT>(a, &sh_npf);
     g_pf[b] = xa;
     const uint32_t rb = NBL - 1 - b;  // evict: descending buckets
     const uint32_t e = tot_ev[rb];
+    tev[rb] = e;
     const uint32_t xe = block_excl_scan<uint32_t, FT>(e, &sh_nev);
     g_ev[rb] = xe;
   }
-  {  // member counts of this CTA
+  {  // member counts of this CTA; does any list bucket need the re-sort (P6)?
     uint32_t m_pf = 0, m_ev = 0;
     for (uint32_t w = threadIdx.x; w < A.tw; w += FT) {
       m_pf += __popc(s.pf_w[w]);
@@ -555,9 +577,11 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
     m_pf = block_sum<uint32_t, FT>(m_pf);
     m_ev = block_sum<uint32_t, FT>(m_ev);
+    const uint32_t need = __syncthreads_or(lmulti[threadIdx.x] && (tpf[threadIdx.x] > 1 || tev[threadIdx.x] > 1));
     if (threadIdx.x == 0) {
       sh_mpf = m_pf;
       sh_mev = m_ev;
+      sh_need = need;
     }
   }
   __syncthreads();
@@ -591,13 +615,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       __syncthreads();
     }
   }
-  __syncthreads();
   // own nonzero list buckets (for the column prefix)
-  uint32_t *own_b = s.h + 6 * NBL;  // [NBL]
+  uint32_t *own_b = s.h + 6 * NBL;
   __shared__ uint32_t sh_nown;
   if (threadIdx.x == 0) sh_nown = 0;
   __syncthreads();
-  if (cnt_pf[threadIdx.x] || cnt_ev[threadIdx.x]) own_b[atomicAdd(&sh_nown, 1u)] = threadIdx.x;  // NBL == FT
+  if (cnt_pf[threadIdx.x] || cnt_ev[threadIdx.x]) own_b[atomicAdd(&sh_nown, 1u)] = threadIdx.x;
   __syncthreads();
   // (a) warps 0/1: in-CTA rank of every member within its bucket (list order), into fp[]
   // (b) other warps: members of the same bucket in the preceding (prefetch) / following
@@ -639,12 +662,27 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
+  // members of buckets holding several distances are also staged (key, id) by slot for P6
   for (uint32_t e = threadIdx.x; e < m_pf + m_ev; e += FT) {
     const uint32_t k = s.memb[e];
-    const uint32_t bk = s.keys[k] >> 21;
+    const uint32_t key = s.keys[k];
+    const uint32_t bk = key >> 21;
     const uint32_t id = (uint32_t)(p.shard_begin + base + k);
-    if (e < m_pf) d.pf_ids[g_pf[bk] + s.fp[e]] = id;
-    else d.ev_ids[g_ev[bk] + s.fp[e]] = id;
+    if (e < m_pf) {
+      const uint32_t slot = g_pf[bk] + s.fp[e];
+      d.pf_ids[slot] = id;
+      if (lmulti[bk]) {
+        d.sort_ka[slot] = key;
+        d.sort_va[slot] = id;
+      }
+    } else {
+      const uint32_t slot = g_ev[bk] + s.fp[e];
+      d.ev_ids[slot] = id;
+      if (lmulti[bk]) {
+        d.f_sk2[slot] = ~key;  // evict: descending (distance, id) = ascending complement
+        d.f_sv2[slot] = id;
+      }
+    }
   }
   // header (CTA 0): all accumulators are complete after the last barrier
   if (c == 0 && threadIdx.x == 0) {
@@ -662,92 +700,97 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     H[H_STATUS] = status;
     H[H_SEQ] += 1;
   }
-
-  // ---------------- P6: re-sort list segments whose bucket holds several distances
-  // (decided identically by every CTA from the global totals and the level-1 min/max)
-  const uint32_t *mm1 = d.f_mm1 + 2 * NB1 * par;
-  __shared__ uint32_t sh_need;
-  if (threadIdx.x == 0) sh_need = 0;
-  __syncthreads();
-  // list bucket lb (bits [30:21]) = level-1 buckets 4lb .. 4lb+3 (bits [30:19]); it holds
-  // several distances iff the min and max key over those buckets differ
-  auto multi_valued = [&](uint32_t lb) {
-    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-    for (uint32_t q = 4 * lb; q < 4 * lb + 4; ++q) {
-      if (mm1[q] == 0xFFFFFFFFu) continue;  // empty level-1 bucket
-      lo = min(lo, mm1[q]);
-      hi = max(hi, ~mm1[NB1 + q]);
-    }
-    return lo != 0xFFFFFFFFu && lo != hi;
-  };
-  {
-    const uint32_t b = threadIdx.x;
-    if ((tot_pf[b] > 1 || tot_ev[b] > 1) && multi_valued(b)) atomicOr(&sh_need, 1u);
-  }
-  __syncthreads();
   if (threadIdx.x == 0) atomicMax(&prof[13], gtimer());
   if (c == 0 && threadIdx.x == 0) prof[7] = gtimer();
-  if (!sh_need) {
+  if (!sh_need) {  // uniform: every CTA computed it from the same global totals
     if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
     return;
   }
   grid.sync();
   if (c == 0 && threadIdx.x == 0) prof[8] = gtimer();
-  // segment j (bucket order, prefetch list first) is re-sorted by CTA j mod G
-  __shared__ uint32_t seg_base, tot_tmp, seg_tmp;
-  __shared__ uint32_t q_n, q_start[64], q_len[64], q_list[64];
-  for (uint32_t round = 0;; ++round) {
-    if (threadIdx.x == 0) {
-      q_n = 0;
-      seg_base = 0;
+
+  // ---------------- P6: order the segments of buckets that hold several distances by
+  // (distance, id).  Segment table in list order (prefetch list first); short segments
+  // (<= RANK_MAX) are spread element-wise over all CTAs (rank = smaller keys + equal keys
+  // earlier in the id-ordered segment), long ones are radix-sorted by one CTA each.
+  uint32_t *seg_start = s.h + 10 * NBL, *seg_len = s.h + 12 * NBL, *seg_off = s.h + 14 * NBL;  // [2 * NBL]
+  uint32_t *big_list = s.h + 4 * NBL;                                                          // [2 * NBL]
+  __shared__ uint32_t sh_nsmall, sh_nbig, sh_tmp;
+  {
+    // thread t owns the (list, bucket) positions 2t, 2t+1 of the 2048 in list order
+    // (prefetch buckets ascending, then evict buckets descending)
+    uint32_t len[2], small[2], big[2];
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t gp = 2 * threadIdx.x + q;
+      const int list = gp < NBL ? 0 : 1;
+      const uint32_t b = list == 0 ? gp : (2 * NBL - 1 - gp);
+      len[q] = list == 0 ? tpf[b] : tev[b];
+      const bool mv = lmulti[b] && len[q] > 1;
+      small[q] = (mv && len[q] <= RANK_MAX) ? 1u : 0u;
+      big[q] = (mv && len[q] > RANK_MAX) ? 1u : 0u;
     }
+    // segment start within its list (the evict list starts at position NBL)
+    const uint32_t lx = block_excl_scan<uint32_t, FT>(len[0] + len[1], &sh_tmp);
+    const uint32_t start0 = (2 * threadIdx.x < NBL) ? lx : lx - sh_npf;
+    const uint32_t start1 = (2 * threadIdx.x + 1 < NBL) ? lx + len[0] : lx + len[0] - sh_npf;
+    const uint32_t sx = block_excl_scan<uint32_t, FT>(small[0] * len[0] + small[1] * len[1], &sh_nsmall);
+    const uint32_t bx = block_excl_scan<uint32_t, FT>(big[0] + big[1], &sh_nbig);
+    seg_start[2 * threadIdx.x] = start0;
+    seg_start[2 * threadIdx.x + 1] = start1;
+    seg_len[2 * threadIdx.x] = small[0] ? len[0] : 0u;
+    seg_len[2 * threadIdx.x + 1] = small[1] ? len[1] : 0u;
+    seg_off[2 * threadIdx.x] = sx;
+    seg_off[2 * threadIdx.x + 1] = sx + small[0] * len[0];
+    if (big[0]) big_list[bx] = 2 * threadIdx.x;
+    if (big[1]) big_list[bx + big[0]] = 2 * threadIdx.x + 1;
+  }
+  __syncthreads();
+  const uint32_t small_total = sh_nsmall, nbig = sh_nbig;
+  // long segments (rare): segment j is radix-sorted by CTA j % G
+  for (uint32_t j = c; j < nbig; j += G) {
+    const uint32_t gp = big_list[j];
+    const int list = gp < NBL ? 0 : 1;
+    const uint32_t b = list == 0 ? gp : (2 * NBL - 1 - gp);
+    const uint32_t t = list == 0 ? tpf[b] : tev[b];
+    const uint32_t start = seg_start[gp];
+    uint32_t *ids = list == 0 ? d.pf_ids : d.ev_ids;
+    uint32_t *ka = (list == 0 ? d.sort_ka : d.f_sk2) + start;
+    uint32_t *ia = (list == 0 ? d.sort_va : d.f_sv2) + start;
+    uint32_t *kb = (list == 0 ? d.sort_kb : d.f_sk3) + start;
+    uint32_t *ib = (list == 0 ? d.sort_vb : d.f_sv3) + start;
+    cta_sort_pairs(ka, ia, kb, ib, t, s.h);  // counters in s.h[0, 4096): not needed any more
+    for (uint32_t e = threadIdx.x; e < t; e += FT) ids[start + e] = ia[e];
     __syncthreads();
-    for (int list = 0; list < 2; ++list) {
-      const uint32_t *tot = list == 0 ? tot_pf : tot_ev;
-      const uint32_t r = threadIdx.x;  // position in list order
-      const uint32_t b = list == 0 ? r : NBL - 1 - r;
-      const uint32_t len = tot[b];
-      const uint32_t need = (len > 1 && multi_valued(b)) ? 1u : 0u;
-      const uint32_t start = block_excl_scan<uint32_t, FT>(len, &tot_tmp);
-      const uint32_t sg = seg_base + block_excl_scan<uint32_t, FT>(need, &seg_tmp);
-      if (need) {
-        const uint32_t j = sg / G;  // this segment's index among CTA (sg % G)'s segments
-        if (sg % G == c && j >= round * 64 && j < (round + 1) * 64) {
-          const uint32_t slot = j - round * 64;
-          q_start[slot] = start;
-          q_len[slot] = len;
-          q_list[slot] = list;
-          atomicAdd(&q_n, 1u);
-        }
+  }
+  // short segments: element e of the concatenation (in list order) -> its segment by binary
+  // search of seg_off; one warp per element
+  {
+    const uint32_t e_lo = (uint32_t)((uint64_t)small_total * c / G);
+    const uint32_t e_hi = (uint32_t)((uint64_t)small_total * (c + 1) / G);
+    for (uint32_t e = e_lo + warp; e < e_hi; e += FWARPS) {
+      // the largest gp with seg_off[gp] <= e is e's segment (empty entries before it share its
+      // offset, entries after it start beyond e)
+      uint32_t lo = 0, hi = 2 * NBL;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (seg_off[mid] <= e) lo = mid;
+        else hi = mid;
       }
-      __syncthreads();
-      if (threadIdx.x == 0) seg_base += seg_tmp;
-      __syncthreads();
-    }
-    const uint32_t nq = q_n;  // this round's segments occupy slots [0, nq)
-    if (round == 0 && threadIdx.x == 0) atomicMax(&prof[15], gtimer());
-    for (uint32_t qi = 0; qi < nq; ++qi) {
-      const uint32_t list = q_list[qi], start = q_start[qi], t = q_len[qi];
-      uint32_t *ids = list == 0 ? d.pf_ids : d.ev_ids;
-      const bool fits = t <= A.tile;
-      uint32_t *ka = fits ? s.keys : (list == 0 ? d.sort_ka : d.f_sk2) + start;
-      uint32_t *ia = fits ? s.fp : (list == 0 ? d.sort_va : d.f_sv2) + start;
-      uint32_t *kb = fits ? s.memb : (list == 0 ? d.sort_kb : d.f_sk3) + start;
-      uint32_t *ib = t <= 8192 ? s.h + 8192 : (list == 0 ? d.sort_vb : d.f_sv3) + start;
-      for (uint32_t e = threadIdx.x; e < t; e += FT) {
-        const uint32_t id = ids[start + e];
-        const uint32_t key = d.keys[id - p.shard_begin];
-        ka[e] = list == 0 ? key : ~key;  // evict: descending (distance, id) = ascending complement
-        ia[e] = id;
+      const uint32_t gp = lo;
+      const int list = gp < NBL ? 0 : 1;
+      const uint32_t start = seg_start[gp], t = seg_len[gp];
+      const uint32_t x = start + (e - seg_off[gp]);
+      const uint32_t *sk = list == 0 ? d.sort_ka : d.f_sk2;
+      const uint32_t *si = list == 0 ? d.sort_va : d.f_sv2;
+      const uint32_t kx = sk[x];
+      uint32_t rank = 0;
+      for (uint32_t j = start + lane; j < start + t; j += 32) {
+        const uint32_t kj = sk[j];
+        rank += (kj < kx) || (kj == kx && j < x);
       }
-      __syncthreads();
-      cta_sort_pairs(ka, ia, kb, ib, t, s.h);
-      for (uint32_t e = threadIdx.x; e < t; e += FT) ids[start + e] = ia[e];
-      __syncthreads();
+      rank = __reduce_add_sync(0xFFFFFFFFu, rank);
+      if (lane == 0) (list == 0 ? d.pf_ids : d.ev_ids)[start + rank] = si[x];
     }
-    const uint32_t total_segs = seg_base;
-    __syncthreads();
-    if ((round + 1) * 64 * G >= total_segs) break;  // uniform
   }
   if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
 }

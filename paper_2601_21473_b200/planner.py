@@ -36,7 +36,7 @@ class Planner:
                  dev_bytes: Optional[int] = None, resident_init=None, device: int = 0,
                  shard: Optional[tuple] = None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None,
-                 multi_kernel: bool = False):
+                 multi_kernel: bool = False, keep_dist: bool = True):
         self.lib = L.lib()
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
@@ -86,7 +86,8 @@ class Planner:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
         cfg = L.Config()
         cfg.abi_version = L.ABI_VERSION
-        cfg.flags = (0 if transfer else L.F_NO_TRANSFER) | (L.F_MULTI_KERNEL if multi_kernel else 0)
+        cfg.flags = (0 if transfer else L.F_NO_TRANSFER) | (L.F_MULTI_KERNEL if multi_kernel else 0) | \
+            (L.F_KEEP_DIST if keep_dist else 0)
         cfg.n_agents = self.n_agents
         cfg.shard_begin = self.lo
         cfg.shard_end = self.hi

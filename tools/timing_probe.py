@@ -13,7 +13,8 @@ ptr = [recs[s].data_ptr() for s in range(w.steps)]
 b = w.blocks
 res = {}
 for mode in ("eager", "graph", "eager_sync"):
-    pl = Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta, transfer=False)
+    pl = Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta, transfer=False,
+                 keep_dist=False)
     for s in range(16):
         pl.set_inputs_ptr(ptr[s]); pl.step(int(w.now[s]))
     pl.sync()
