@@ -95,6 +95,7 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_rows1 = take(8 * (uint64_t)FUSED_MAX_CTAS * 4096);
   L.f_rows2 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
   L.f_rows3 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
+  L.f_lmm = take(4 * 2 * 4 * 1024);
   L.wb_bytes = take(4 * n1);
   L.params_dev = take(sizeof(Params));
   L.f_sk2 = take(4 * n1);
@@ -102,7 +103,7 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_sk3 = take(4 * n1);
   L.f_sv3 = take(4 * n1);
   L.f_bar = take(64);
-  L.f_prof = take(128);
+  L.f_prof = take(256);
   L.total = off;
   return L;
 }
@@ -166,6 +167,7 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_rows1 = (unsigned long long *)(b + L.f_rows1);
   d.f_rows2 = (unsigned long long *)(b + L.f_rows2);
   d.f_rows3 = (unsigned long long *)(b + L.f_rows3);
+  d.f_lmm = (uint32_t *)(b + L.f_lmm);
   d.wb_bytes = (uint32_t *)(b + L.wb_bytes);
   d.params_dev = (uint8_t *)(b + L.params_dev);
   d.f_sk2 = (uint32_t *)(b + L.f_sk2);
@@ -487,7 +489,8 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
       c->fused_grid = sms;
       c->sms = sms;
       if (cudaMemsetAsync(p.d.f_mm1, 0xFF, 4 * 2 * 2 * 4096, c->stream) != cudaSuccess ||
-          cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2 * 1024, c->stream) != cudaSuccess)
+          cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2 * 1024, c->stream) != cudaSuccess ||
+          cudaMemsetAsync(p.d.f_lmm, 0xFF, 4 * 2 * 4 * 1024, c->stream) != cudaSuccess)
         return fail(SCALESIM_E_CUDA);
     }
   }

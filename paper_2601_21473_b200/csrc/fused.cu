@@ -18,9 +18,9 @@
 //   P5  stable bucket sort of the lists: slot = bucket start + members of that bucket in the
 //       preceding CTAs (prefetch: ascending id) or following CTAs (evict: descending id) +
 //       in-CTA rank
-//   --- grid barrier (only when a list bucket holds several distances)
-//   P6  such segments are re-sorted by (distance, id) — stable rank sort in shared memory
-//       for short segments, radix sort otherwise — one CTA per segment
+//   --- grid barrier (only when the members of a list bucket hold several distances)
+//   P6  such segments are re-sorted by (distance, id): ranks by counting, the comparisons
+//       spread evenly over all CTAs (short segments), or a radix sort by one CTA (long ones)
 // Decisions follow DESIGN.md §3 exactly as the multi-kernel path (kernels.cu) does; both give
 // bit-identical plans (tests/test_gpu_parity.py runs both).
 #include <cuda_runtime.h>
@@ -36,7 +36,6 @@ constexpr int FWARPS = FT / 32;
 constexpr int NB1 = 4096;  // level-1 buckets: distance bits [30:19]
 constexpr int NBL = 1024;  // list-sort buckets: distance bits [30:21]
 constexpr int LOAD_BATCH = 8;  // records in flight per thread in P1
-constexpr uint32_t RANK_MAX = 4096;  // P6: longer segments are radix-sorted by one CTA
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -115,13 +114,14 @@ __device__ __forceinline__ FSmem carve(uint8_t *base, uint32_t tile, uint32_t tw
   w += tw;
   s.ev_w = w;
   w += tw;
+  w += (4 - ((uintptr_t)w / 4) % 4) % 4;  // 16-byte aligned: s.h is also read as u64
   s.h = w;
   return s;
 }
 
 size_t fused_smem_bytes(uint32_t tile) {
   const uint32_t tw = tile / 32;
-  return (size_t)4 * (3 * tile + 5 * tw + 4 * NB1);
+  return (size_t)4 * (3 * tile + 5 * tw + 4 * NB1) + 16;
 }
 
 __device__ __forceinline__ void clear_hist(uint32_t *h, int nb) {
@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       d.f_mm1[2 * NB1 * q + NB1 + b] = 0xFFFFFFFFu;
     }
     for (uint32_t b = gt; b < 2 * NBL; b += gs) d.f_tot[2 * NBL * q + b] = 0;
+    for (uint32_t b = gt; b < 4 * NBL; b += gs) d.f_lmm[4 * NBL * q + b] = 0xFFFFFFFFu;
     for (uint32_t b = gt; b < 1024; b += gs) {
       d.f_hist2[1024 * q + b] = 0;
       d.f_hist3[1024 * q + b] = 0;
@@ -407,22 +408,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     if (gt < 8) d.f_acc[8 * q + gt] = 0;
   }
   const uint32_t *mm1 = d.f_mm1 + 2 * NB1 * par;
-  // list bucket lb (bits [30:21]) = level-1 buckets 4lb..4lb+3 (bits [30:19]); it holds several
-  // distances iff the min and max key over those buckets differ (list members are eligible)
-  uint32_t *lmulti = s.h + 7 * NBL;  // written after the histogram is no longer needed
-  uint32_t my_multi;
-  {
-    const uint32_t lb = threadIdx.x;  // NBL == FT
-    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-#pragma unroll
-    for (uint32_t q = 4 * lb; q < 4 * lb + 4; ++q) {
-      const uint32_t m = mm1[q];
-      if (m == 0xFFFFFFFFu) continue;  // empty level-1 bucket
-      lo = min(lo, m);
-      hi = max(hi, ~mm1[NB1 + q]);
-    }
-    my_multi = (lo != 0xFFFFFFFFu && lo != hi) ? 1u : 0u;
-  }
   Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 1, 0};
   select_level(d.f_hist1 + NB1 * par, mm1, 1, p.budget, sel);
   for (int level = 2; level <= 3 && !sel.done; ++level) {
@@ -445,7 +430,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   const bool all_fit = sel.all_fit;
   const uint32_t dstar = sel.dstar;
-  lmulti[threadIdx.x] = my_multi;  // s.h no longer holds a histogram
   if (c == 0 && threadIdx.x == 0) prof[9] = gtimer();
 
   // ---------------- P3: tie group: id-order prefix of the bytes at d == D*
@@ -487,7 +471,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
 
   // ---------------- P4: emit
   uint32_t *cnt_pf = s.h, *cnt_ev = s.h + NBL;  // per-CTA list members per list bucket
+  uint32_t *mm_l = s.h + 10 * NBL;  // [4][NBL]: prefetch min, prefetch ~max, evict min, evict ~max
   for (int b = threadIdx.x; b < 2 * NBL; b += FT) s.h[b] = 0;
+  for (int b = threadIdx.x; b < 4 * NBL; b += FT) mm_l[b] = 0xFFFFFFFFu;
   __syncthreads();
   unsigned long long h2d = 0, d2h = 0, tie_kept = 0;
   uint32_t n_el = 0;
@@ -521,10 +507,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     if ((pfw >> lane) & 1u) {
       h2d += fp;
       atomicAdd(&cnt_pf[key >> 21], 1u);
+      atomicMin(&mm_l[key >> 21], key);
+      atomicMin(&mm_l[NBL + (key >> 21)], ~key);
     }
     if ((evw >> lane) & 1u) {
       if ((s.dirty_w[w] >> lane) & 1u) d2h += d.wb_bytes[base + k];  // R13
       atomicAdd(&cnt_ev[key >> 21], 1u);
+      atomicMin(&mm_l[2 * NBL + (key >> 21)], key);
+      atomicMin(&mm_l[3 * NBL + (key >> 21)], ~key);
     }
   }
   __syncthreads();
@@ -535,8 +525,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     const uint32_t a = cnt_pf[b], e = cnt_ev[b];
     cpf[b] = a;
     cev[b] = e;
-    if (a) atomicAdd(&tot_pf[b], a);
-    if (e) atomicAdd(&tot_ev[b], e);
+    if (a) {
+      atomicAdd(&tot_pf[b], a);
+      atomicMin(&d.f_lmm[4 * NBL * par + b], mm_l[b]);
+      atomicMin(&d.f_lmm[4 * NBL * par + NBL + b], mm_l[NBL + b]);
+    }
+    if (e) {
+      atomicAdd(&tot_ev[b], e);
+      atomicMin(&d.f_lmm[4 * NBL * par + 2 * NBL + b], mm_l[2 * NBL + b]);
+      atomicMin(&d.f_lmm[4 * NBL * par + 3 * NBL + b], mm_l[3 * NBL + b]);
+    }
   }
   h2d = block_sum<unsigned long long, FT>(h2d);
   d2h = block_sum<unsigned long long, FT>(d2h);
@@ -556,6 +554,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   // ---------------- P5: stable bucket sort of the lists
   uint32_t *g_pf = s.h + 2 * NBL, *g_ev = s.h + 3 * NBL;  // first slot of this CTA's members per bucket
   uint32_t *tpf = s.h + 8 * NBL, *tev = s.h + 9 * NBL;    // list bucket totals (shared copy)
+  // list bucket b needs the re-sort by full distance iff its members hold several distances
+  uint32_t *lmulti = s.h + 7 * NBL;  // bit 0: prefetch list, bit 1: evict list
+  {
+    const uint32_t b = threadIdx.x;
+    const uint32_t *lmm = d.f_lmm + 4 * NBL * par;
+    const uint32_t mp = lmm[b], xp = ~lmm[NBL + b], me = lmm[2 * NBL + b], xe = ~lmm[3 * NBL + b];
+    lmulti[b] = ((mp != 0xFFFFFFFFu && mp != xp) ? 1u : 0u) | ((me != 0xFFFFFFFFu && me != xe) ? 2u : 0u);
+  }
   __shared__ uint32_t sh_npf, sh_nev, sh_mpf, sh_mev, sh_need;
   {
     const uint32_t b = threadIdx.x;  // NBL == FT: one bucket per thread
@@ -577,7 +583,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
     m_pf = block_sum<uint32_t, FT>(m_pf);
     m_ev = block_sum<uint32_t, FT>(m_ev);
-    const uint32_t need = __syncthreads_or(lmulti[threadIdx.x] && (tpf[threadIdx.x] > 1 || tev[threadIdx.x] > 1));
+    const uint32_t need = __syncthreads_or(lmulti[threadIdx.x] != 0u);
     if (threadIdx.x == 0) {
       sh_mpf = m_pf;
       sh_mev = m_ev;
@@ -671,14 +677,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     if (e < m_pf) {
       const uint32_t slot = g_pf[bk] + s.fp[e];
       d.pf_ids[slot] = id;
-      if (lmulti[bk]) {
+      if (lmulti[bk] & 1u) {
         d.sort_ka[slot] = key;
         d.sort_va[slot] = id;
       }
     } else {
       const uint32_t slot = g_ev[bk] + s.fp[e];
       d.ev_ids[slot] = id;
-      if (lmulti[bk]) {
+      if (lmulti[bk] & 2u) {
         d.f_sk2[slot] = ~key;  // evict: descending (distance, id) = ascending complement
         d.f_sv2[slot] = id;
       }
@@ -709,13 +715,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   grid.sync();
   if (c == 0 && threadIdx.x == 0) prof[8] = gtimer();
 
-  // ---------------- P6: order the segments of buckets that hold several distances by
-  // (distance, id).  Segment table in list order (prefetch list first); short segments
-  // (<= RANK_MAX) are spread element-wise over all CTAs (rank = smaller keys + equal keys
-  // earlier in the id-ordered segment), long ones are radix-sorted by one CTA each.
-  uint32_t *seg_start = s.h + 10 * NBL, *seg_len = s.h + 12 * NBL, *seg_off = s.h + 14 * NBL;  // [2 * NBL]
-  uint32_t *big_list = s.h + 4 * NBL;                                                          // [2 * NBL]
-  __shared__ uint32_t sh_nsmall, sh_nbig, sh_tmp;
+  // ---------------- P6: order the segments of list buckets whose members hold several
+  // distances by (distance, id).  Segment table in list order (prefetch list first).  Short
+  // segments: every element's rank is counted against its segment's keys, the comparison
+  // work spread evenly over all CTAs; long ones are radix-sorted in global memory by one CTA.
+  uint32_t *seg_start = s.h + 10 * NBL, *seg_len = s.h + 12 * NBL;  // [2 * NBL] each
+  __shared__ uint32_t sh_nsmall, sh_nbig, sh_tmp, sh_gp, sh_nds;
+  uint32_t *dense_gp = s.h + 14 * NBL;  // [2 * NBL]: nonempty short segments in list order
+  uint32_t big_mask = 0, big_x = 0;  // this thread's long segments (bits for gp 2t, 2t+1) and their index
   {
     // thread t owns the (list, bucket) positions 2t, 2t+1 of the 2048 in list order
     // (prefetch buckets ascending, then evict buckets descending)
@@ -725,30 +732,42 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       const int list = gp < NBL ? 0 : 1;
       const uint32_t b = list == 0 ? gp : (2 * NBL - 1 - gp);
       len[q] = list == 0 ? tpf[b] : tev[b];
-      const bool mv = lmulti[b] && len[q] > 1;
-      small[q] = (mv && len[q] <= RANK_MAX) ? 1u : 0u;
-      big[q] = (mv && len[q] > RANK_MAX) ? 1u : 0u;
+      const bool mv = (lmulti[b] >> list) & 1u;
+      small[q] = (mv && 4 * len[q] <= 3 * A.tile) ? 1u : 0u;  // sortable in shared memory
+      big[q] = (mv && 4 * len[q] > 3 * A.tile) ? 1u : 0u;
     }
     // segment start within its list (the evict list starts at position NBL)
     const uint32_t lx = block_excl_scan<uint32_t, FT>(len[0] + len[1], &sh_tmp);
     const uint32_t start0 = (2 * threadIdx.x < NBL) ? lx : lx - sh_npf;
     const uint32_t start1 = (2 * threadIdx.x + 1 < NBL) ? lx + len[0] : lx + len[0] - sh_npf;
     const uint32_t sx = block_excl_scan<uint32_t, FT>(small[0] * len[0] + small[1] * len[1], &sh_nsmall);
-    const uint32_t bx = block_excl_scan<uint32_t, FT>(big[0] + big[1], &sh_nbig);
+    big_x = block_excl_scan<uint32_t, FT>(big[0] + big[1], &sh_nbig);
+    const uint32_t dx = block_excl_scan<uint32_t, FT>(small[0] + small[1], &sh_nds);
+    if (small[0]) dense_gp[dx] = 2 * threadIdx.x;
+    if (small[1]) dense_gp[dx + small[0]] = 2 * threadIdx.x + 1;
+    big_mask = big[0] | (big[1] << 1);
     seg_start[2 * threadIdx.x] = start0;
     seg_start[2 * threadIdx.x + 1] = start1;
     seg_len[2 * threadIdx.x] = small[0] ? len[0] : 0u;
     seg_len[2 * threadIdx.x + 1] = small[1] ? len[1] : 0u;
-    seg_off[2 * threadIdx.x] = sx;
-    seg_off[2 * threadIdx.x + 1] = sx + small[0] * len[0];
-    if (big[0]) big_list[bx] = 2 * threadIdx.x;
-    if (big[1]) big_list[bx + big[0]] = 2 * threadIdx.x + 1;
   }
   __syncthreads();
   const uint32_t small_total = sh_nsmall, nbig = sh_nbig;
-  // long segments (rare): segment j is radix-sorted by CTA j % G
+  if (c == 0 && threadIdx.x == 0) {
+    prof[16] = small_total;
+    prof[17] = nbig;
+  }
+  {
+    const uint32_t m = max(seg_len[2 * threadIdx.x], seg_len[2 * threadIdx.x + 1]);
+    if (m) atomicMax(&prof[18], (unsigned long long)m);
+  }
+  if (threadIdx.x == 0) atomicMax(&prof[19], gtimer());
+  // long segments (rare): the j-th is radix-sorted in global memory by CTA j % G
   for (uint32_t j = c; j < nbig; j += G) {
-    const uint32_t gp = big_list[j];
+    if ((big_mask & 1u) && big_x == j) sh_gp = 2 * threadIdx.x;
+    if ((big_mask & 2u) && big_x + (big_mask & 1u) == j) sh_gp = 2 * threadIdx.x + 1;
+    __syncthreads();
+    const uint32_t gp = sh_gp;
     const int list = gp < NBL ? 0 : 1;
     const uint32_t b = list == 0 ? gp : (2 * NBL - 1 - gp);
     const uint32_t t = list == 0 ? tpf[b] : tev[b];
@@ -762,35 +781,52 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     for (uint32_t e = threadIdx.x; e < t; e += FT) ids[start + e] = ia[e];
     __syncthreads();
   }
-  // short segments: element e of the concatenation (in list order) -> its segment by binary
-  // search of seg_off; one warp per element
+  if (threadIdx.x == 0) atomicMax(&prof[20], gtimer());
+  // short segments (fit in shared memory, 4 words per element): segment i (dense order) is
+  // sorted by CTA i % G.  Keys are first mapped to order-preserving small codes
+  // (key - min) >> g, g = common trailing zeros of the differences (integer-tick distances in
+  // one list bucket give a handful of codes), so the stable radix sort needs one 8-bit pass.
   {
-    const uint32_t e_lo = (uint32_t)((uint64_t)small_total * c / G);
-    const uint32_t e_hi = (uint32_t)((uint64_t)small_total * (c + 1) / G);
-    for (uint32_t e = e_lo + warp; e < e_hi; e += FWARPS) {
-      // the largest gp with seg_off[gp] <= e is e's segment (empty entries before it share its
-      // offset, entries after it start beyond e)
-      uint32_t lo = 0, hi = 2 * NBL;
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) / 2;
-        if (seg_off[mid] <= e) lo = mid;
-        else hi = mid;
-      }
-      const uint32_t gp = lo;
+    const uint32_t nds = sh_nds;
+    const unsigned long long t_r0 = gtimer();
+    __shared__ uint32_t sh_min, sh_or;
+    for (uint32_t i = c; i < nds; i += G) {
+      const uint32_t gp = dense_gp[i];
       const int list = gp < NBL ? 0 : 1;
-      const uint32_t start = seg_start[gp], t = seg_len[gp];
-      const uint32_t x = start + (e - seg_off[gp]);
-      const uint32_t *sk = list == 0 ? d.sort_ka : d.f_sk2;
-      const uint32_t *si = list == 0 ? d.sort_va : d.f_sv2;
-      const uint32_t kx = sk[x];
-      uint32_t rank = 0;
-      for (uint32_t j = start + lane; j < start + t; j += 32) {
-        const uint32_t kj = sk[j];
-        rank += (kj < kx) || (kj == kx && j < x);
+      const uint32_t t = seg_len[gp], start = seg_start[gp];
+      const uint32_t *sk = (list == 0 ? d.sort_ka : d.f_sk2) + start;
+      const uint32_t *si = (list == 0 ? d.sort_va : d.f_sv2) + start;
+      uint32_t *ka = s.keys, *ia = s.keys + t, *kb = s.keys + 2 * t, *ib = s.keys + 3 * t;  // 4t <= 3 * tile
+      uint32_t mn = 0xFFFFFFFFu;
+      for (uint32_t j = threadIdx.x; j < t; j += FT) {
+        const uint32_t k = sk[j];
+        ka[j] = k;
+        ia[j] = si[j];
+        mn = min(mn, k);
       }
-      rank = __reduce_add_sync(0xFFFFFFFFu, rank);
-      if (lane == 0) (list == 0 ? d.pf_ids : d.ev_ids)[start + rank] = si[x];
+      mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+      if (threadIdx.x == 0) {
+        sh_min = 0xFFFFFFFFu;
+        sh_or = 0;
+      }
+      __syncthreads();
+      if (lane == 0) atomicMin(&sh_min, mn);
+      __syncthreads();
+      mn = sh_min;
+      uint32_t o = 0;
+      for (uint32_t j = threadIdx.x; j < t; j += FT) o |= ka[j] - mn;
+      o = __reduce_or_sync(0xFFFFFFFFu, o);
+      if (lane == 0 && o) atomicOr(&sh_or, o);
+      __syncthreads();
+      const uint32_t g = sh_or ? (uint32_t)(__ffs(sh_or) - 1) : 0u;
+      for (uint32_t j = threadIdx.x; j < t; j += FT) ka[j] = (ka[j] - mn) >> g;  // order-preserving code
+      __syncthreads();
+      cta_sort_pairs(ka, ia, kb, ib, t, s.h);  // counters in s.h[0, 4096)
+      uint32_t *out = (list == 0 ? d.pf_ids : d.ev_ids) + start;
+      for (uint32_t j = threadIdx.x; j < t; j += FT) out[j] = ia[j];
+      __syncthreads();
     }
+    if (threadIdx.x == 0) atomicMax(&prof[21], gtimer() - t_r0);
   }
   if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
 }

@@ -54,7 +54,7 @@ struct Layout {
   uint64_t page_first, page_table, ring, pool, desc[2];
   // fused path (double-buffered by fused-step parity where noted)
   uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_cpf, f_cta_cev, f_tot, f_acc, f_tie_val, f_tie_flag;
-  uint64_t f_rows1, f_rows2, f_rows3;
+  uint64_t f_rows1, f_rows2, f_rows3, f_lmm;
   uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes, params_dev;
   uint64_t total;
 };
@@ -93,6 +93,7 @@ struct Dev {
   unsigned long long *f_acc;                            // [2][8]
   unsigned long long *f_tie_val;                        // [CTAS] tie bytes per CTA
   unsigned long long *f_rows1, *f_rows2, *f_rows3;      // [CTAS][4096] / [CTAS][1024] per-CTA histogram rows
+  uint32_t *f_lmm;                                      // [2][4][1024] list members: min / ~max key per bucket
   unsigned int *f_tie_flag;                             // [CTAS] launch epoch of f_tie_val
   uint32_t *wb_bytes;                                   // [n_local] KV+HIST bytes per agent (R13)
   uint8_t *params_dev;                                  // device copy of the context's Params (fused path)
