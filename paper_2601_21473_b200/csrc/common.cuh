@@ -67,15 +67,74 @@ __device__ __forceinline__ T block_sum(T v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   if (lane == 0) sh[warp] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    T t = T(0);
-    for (int w = 0; w < BT / 32; ++w) t += sh[w];
-    sh[BT / 32] = t;
+  if (warp == 0) {
+    T t = lane < BT / 32 ? sh[lane] : T(0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+    if (lane == 0) sh[BT / 32] = t;
   }
   __syncthreads();
   const T r = sh[BT / 32];
   __syncthreads();
   return r;
+}
+
+// Block-wide sums of N values per thread at once (one pair of barriers); results in v[].
+template <typename T, int N, int BT = NT>
+__device__ __forceinline__ void block_sum_v(T (&v)[N]) {
+  __shared__ T sh[N][BT / 32 + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(FULL, v[i], o);
+    if (lane == 0) sh[i][warp] = v[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      T t = lane < BT / 32 ? sh[i][lane] : T(0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+      if (lane == 0) sh[i][BT / 32] = t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = sh[i][BT / 32];
+  __syncthreads();
+}
+
+// Block-wide exclusive scans of N values per thread at once; v[] becomes the exclusive
+// prefixes, tot[] (any memory) receives the totals in every thread.
+template <typename T, int N, int BT = NT>
+__device__ __forceinline__ void block_excl_scan_v(T (&v)[N], T (&tot)[N]) {
+  __shared__ T sh[N][BT / 32 + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T incl[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    incl[i] = warp_incl_scan(v[i]);
+    if (lane == 31) sh[i][warp] = incl[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const T w = lane < BT / 32 ? sh[i][lane] : T(0);
+      const T wi = warp_incl_scan(w);
+      if (lane < BT / 32) sh[i][lane] = wi - w;
+      if (lane == BT / 32 - 1) sh[i][BT / 32] = wi;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    v[i] = sh[i][warp] + incl[i] - v[i];
+    tot[i] = sh[i][BT / 32];
+  }
+  __syncthreads();
 }
 
 // 64-bit sum over the lanes in `mask` of a 32-bit value (exact: split in 16-bit halves).

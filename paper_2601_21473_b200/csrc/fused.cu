@@ -443,17 +443,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   __syncthreads();
   __shared__ unsigned long long sh_tie_excl, sh_chunk;
-  {  // exclusive scan over the tile's words
-    unsigned long long carry = 0;
-    for (uint32_t w0 = 0; w0 < A.tw; w0 += FT) {
-      const uint32_t w = w0 + threadIdx.x;
-      const unsigned long long v = w < A.tw ? word_tie[w] : 0ull;
-      const unsigned long long ex = block_excl_scan<unsigned long long, FT>(v, &sh_chunk);
-      __syncthreads();
-      if (w < A.tw) word_tie[w] = carry + ex;
-      carry += sh_chunk;
-      __syncthreads();
-    }
+  {  // exclusive scan over the tile's words (tw <= FUSED_MAX_TILE / 32 <= FT: one word per thread)
+    const uint32_t w = threadIdx.x;
+    const unsigned long long v = w < A.tw ? word_tie[w] : 0ull;
+    const unsigned long long ex = block_excl_scan<unsigned long long, FT>(v, &sh_chunk);
+    if (w < A.tw) word_tie[w] = ex;
+    __syncthreads();
   }
   {  // preceding CTAs: their bytes in the resolving bucket (published rows; one load each)
     unsigned long long t = 0;
@@ -536,15 +531,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       atomicMin(&d.f_lmm[4 * NBL * par + 3 * NBL + b], mm_l[3 * NBL + b]);
     }
   }
-  h2d = block_sum<unsigned long long, FT>(h2d);
-  d2h = block_sum<unsigned long long, FT>(d2h);
-  tie_kept = block_sum<unsigned long long, FT>(tie_kept);
-  n_el = block_sum<uint32_t, FT>(n_el);
-  if (threadIdx.x == 0) {
-    if (h2d) atomicAdd(&acc[1], h2d);
-    if (d2h) atomicAdd(&acc[2], d2h);
-    if (tie_kept) atomicAdd(&acc[3], tie_kept);
-    if (n_el) atomicAdd(&acc[4], (unsigned long long)n_el);
+  {
+    unsigned long long sums[4] = {h2d, d2h, tie_kept, (unsigned long long)n_el};
+    block_sum_v<unsigned long long, 4, FT>(sums);
+    if (threadIdx.x < 4 && sums[threadIdx.x]) atomicAdd(&acc[1 + threadIdx.x], sums[threadIdx.x]);
   }
   if (threadIdx.x == 0) atomicMax(&prof[12], gtimer());
   if (c == 0 && threadIdx.x == 0) prof[5] = gtimer();
@@ -564,63 +554,48 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   __shared__ uint32_t sh_npf, sh_nev, sh_mpf, sh_mev, sh_need;
   {
-    const uint32_t b = threadIdx.x;  // NBL == FT: one bucket per thread
-    const uint32_t a = tot_pf[b];
-    tpf[b] = a;
-    const uint32_t xa = block_excl_scan<uint32_t, FT>(a, &sh_npf);
-    g_pf[b] = xa;
-    const uint32_t rb = NBL - 1 - b;  // evict: descending buckets
-    const uint32_t e = tot_ev[rb];
-    tev[rb] = e;
-    const uint32_t xe = block_excl_scan<uint32_t, FT>(e, &sh_nev);
-    g_ev[rb] = xe;
-  }
-  {  // member counts of this CTA; does any list bucket need the re-sort (P6)?
-    uint32_t m_pf = 0, m_ev = 0;
-    for (uint32_t w = threadIdx.x; w < A.tw; w += FT) {
-      m_pf += __popc(s.pf_w[w]);
-      m_ev += __popc(s.ev_w[w]);
+    const uint32_t b = threadIdx.x, rb = NBL - 1 - b;  // NBL == FT; evict: descending buckets
+    uint32_t v[2] = {tot_pf[b], tot_ev[rb]}, tt[2];
+    tpf[b] = v[0];
+    tev[rb] = v[1];
+    block_excl_scan_v<uint32_t, 2, FT>(v, tt);
+    g_pf[b] = v[0];
+    g_ev[rb] = v[1];
+    if (threadIdx.x == 0) {
+      sh_npf = tt[0];
+      sh_nev = tt[1];
     }
-    m_pf = block_sum<uint32_t, FT>(m_pf);
-    m_ev = block_sum<uint32_t, FT>(m_ev);
+  }
+  // members in list order (prefetch ascending id, evict descending id; tile-local indices)
+  // into memb; one word per thread (tw <= FT)
+  {
+    const uint32_t w = threadIdx.x;
+    const uint32_t pw = w < A.tw ? s.pf_w[w] : 0u, ew = w < A.tw ? s.ev_w[w] : 0u;
+    uint32_t v[2] = {(uint32_t)__popc(pw), (uint32_t)__popc(ew)}, tt[2];
+    block_excl_scan_v<uint32_t, 2, FT>(v, tt);
     const uint32_t need = __syncthreads_or(lmulti[threadIdx.x] != 0u);
     if (threadIdx.x == 0) {
-      sh_mpf = m_pf;
-      sh_mev = m_ev;
+      sh_mpf = tt[0];
+      sh_mev = tt[1];
       sh_need = need;
+    }
+    uint32_t m = pw, o = v[0];
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      s.memb[o++] = w * 32 + bit;
+    }
+    m = ew;
+    o = tt[0] + tt[1] - 1 - v[1];
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      s.memb[o--] = w * 32 + bit;
     }
   }
   __syncthreads();
   const uint32_t m_pf = sh_mpf, m_ev = sh_mev;
-  uint32_t *mem_pf = s.memb, *mem_ev = s.memb + m_pf;  // members in list order (tile-local indices)
-  {
-    uint32_t carry_pf = 0, carry_ev = 0;
-    __shared__ uint32_t t_pf, t_ev;
-    for (uint32_t w0 = 0; w0 < A.tw; w0 += FT) {
-      const uint32_t w = w0 + threadIdx.x;
-      const uint32_t a = w < A.tw ? __popc(s.pf_w[w]) : 0u, e = w < A.tw ? __popc(s.ev_w[w]) : 0u;
-      const uint32_t xa = block_excl_scan<uint32_t, FT>(a, &t_pf);
-      const uint32_t xe = block_excl_scan<uint32_t, FT>(e, &t_ev);
-      if (w < A.tw) {
-        uint32_t m = s.pf_w[w], o = carry_pf + xa;
-        while (m) {
-          const int bit = __ffs(m) - 1;
-          m &= m - 1;
-          mem_pf[o++] = w * 32 + bit;
-        }
-        m = s.ev_w[w];
-        o = m_ev - 1 - (carry_ev + xe);  // descending id
-        while (m) {
-          const int bit = __ffs(m) - 1;
-          m &= m - 1;
-          mem_ev[o--] = w * 32 + bit;
-        }
-      }
-      carry_pf += t_pf;
-      carry_ev += t_ev;
-      __syncthreads();
-    }
-  }
+  uint32_t *mem_pf = s.memb, *mem_ev = s.memb + m_pf;
   // own nonzero list buckets (for the column prefix)
   uint32_t *own_b = s.h + 6 * NBL;
   __shared__ uint32_t sh_nown;
@@ -737,12 +712,18 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       big[q] = (mv && 4 * len[q] > 3 * A.tile) ? 1u : 0u;
     }
     // segment start within its list (the evict list starts at position NBL)
-    const uint32_t lx = block_excl_scan<uint32_t, FT>(len[0] + len[1], &sh_tmp);
+    uint32_t v[4] = {len[0] + len[1], small[0] * len[0] + small[1] * len[1], big[0] + big[1], small[0] + small[1]};
+    uint32_t tt[4];
+    block_excl_scan_v<uint32_t, 4, FT>(v, tt);
+    const uint32_t lx = v[0], dx = v[3];
+    big_x = v[2];
+    if (threadIdx.x == 0) {
+      sh_nsmall = tt[1];
+      sh_nbig = tt[2];
+      sh_nds = tt[3];
+    }
     const uint32_t start0 = (2 * threadIdx.x < NBL) ? lx : lx - sh_npf;
     const uint32_t start1 = (2 * threadIdx.x + 1 < NBL) ? lx + len[0] : lx + len[0] - sh_npf;
-    const uint32_t sx = block_excl_scan<uint32_t, FT>(small[0] * len[0] + small[1] * len[1], &sh_nsmall);
-    big_x = block_excl_scan<uint32_t, FT>(big[0] + big[1], &sh_nbig);
-    const uint32_t dx = block_excl_scan<uint32_t, FT>(small[0] + small[1], &sh_nds);
     if (small[0]) dense_gp[dx] = 2 * threadIdx.x;
     if (small[1]) dense_gp[dx + small[0]] = 2 * threadIdx.x + 1;
     big_mask = big[0] | (big[1] << 1);
