@@ -333,7 +333,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
 
   // ---------------- P1: score + level-1 histogram
   // per-thread copies of the parameters used per agent (Params lives in shared memory)
-  const float th0 = p.theta[0], th1 = p.theta[1], th2 = p.theta[2], hop_scale = p.hop_scale;
+  const float hop_scale = p.hop_scale;
+  __shared__ float thv[4];  // prefetch threshold per class (class 3: malformed, never prefetched)
+  if (threadIdx.x < 4) thv[threadIdx.x] = threadIdx.x < 3 ? p.theta[threadIdx.x] : 0.0f;
   const uint64_t n_kin = p.n_kin;
   const float *dint = d.dint;
   const uint4 *rec = p.rec + base;
@@ -357,10 +359,20 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       if (k >= A.tw * 32) continue;  // warp-uniform (tw * 32 is a multiple of 32)
       const bool valid = k < n_here;
       const bool res = (s.old_w[k >> 5] >> (k & 31)) & 1u;
-      const float dist = valid ? distance_of(r[j], now, hop_scale, dint, n_kin, st) : 0.0f;
+      const uint32_t ph = r[j].z & 3u, cl = (r[j].z >> 2) & 3u;
+      float dist;
+      if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {
+        // the warp holds interaction / diffusion / malformed records: general definition
+        dist = valid ? distance_of(r[j], now, hop_scale, dint, n_kin, st) : 0.0f;
+      } else {
+        // independent agents only: remaining action ticks, 0 while in an LLM
+        // phase, +inf when idle — the same values distance_of gives for class 0
+        const int64_t remain = (int64_t)r[j].x - now;
+        const float d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
+        dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
+      }
       const uint32_t bits = __float_as_uint(dist);
-      const uint32_t cl = class_of(r[j]);
-      const float th = cl == 0u ? th0 : cl == 1u ? th1 : cl == 2u ? th2 : 0.0f;
+      const float th = thv[cl];
       const bool elig = valid && (res || dist == 0.0f || dist < th);
       s.keys[k] = bits;
       s.fp[k] = r[j].y;
@@ -472,6 +484,11 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   __syncthreads();
   unsigned long long h2d = 0, d2h = 0, tie_kept = 0;
   uint32_t n_el = 0;
+  constexpr uint32_t WB_CAP = 5 * NBL;
+  uint32_t *wb_list = s.h + 2 * NBL;  // evicted dirty agents of this tile (s.h[2NBL, 7NBL) is free here)
+  __shared__ uint32_t sh_nwb;
+  if (threadIdx.x == 0) sh_nwb = 0;
+  __syncthreads();
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
     const bool el = (s.elig_w[w] >> lane) & 1u;  // 0 beyond n_here
@@ -506,13 +523,18 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       atomicMin(&mm_l[NBL + (key >> 21)], ~key);
     }
     if ((evw >> lane) & 1u) {
-      if ((s.dirty_w[w] >> lane) & 1u) d2h += d.wb_bytes[base + k];  // R13
+      if ((s.dirty_w[w] >> lane) & 1u) {  // R13: write-back bytes, loaded after the loop
+        const uint32_t slot = atomicAdd(&sh_nwb, 1u);
+        if (slot < WB_CAP) wb_list[slot] = k;
+        else d2h += d.wb_bytes[base + k];
+      }
       atomicAdd(&cnt_ev[key >> 21], 1u);
       atomicMin(&mm_l[2 * NBL + (key >> 21)], key);
       atomicMin(&mm_l[3 * NBL + (key >> 21)], ~key);
     }
   }
   __syncthreads();
+  for (uint32_t q = threadIdx.x; q < min(sh_nwb, WB_CAP); q += FT) d2h += d.wb_bytes[base + wb_list[q]];
   uint32_t *cpf = d.f_cta_cpf + (uint64_t)c * NBL, *cev = d.f_cta_cev + (uint64_t)c * NBL;
   uint32_t *tot_pf = d.f_tot + 2 * NBL * par, *tot_ev = d.f_tot + 2 * NBL * par + NBL;
   {
