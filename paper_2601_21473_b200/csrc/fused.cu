@@ -388,9 +388,11 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&prof[25], gtimer());  // P1 loop done
   // this CTA's level-1 bytes: dense row (its column entry gives the tie prefix in P3) and
   // the global sum
   publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, d.f_mm1 + 2 * NB1 * par, d.f_rows1 + (uint64_t)c * NB1);
+  if (threadIdx.x == 0) atomicMax(&prof[26], gtimer());  // published
   zero_b = block_sum<unsigned long long, FT>(zero_b);
   st = __reduce_or_sync(0xFFFFFFFFu, st);
   if (lane == 0 && st) atomicOr(reinterpret_cast<unsigned int *>(&acc[5]), st);
@@ -534,6 +536,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&prof[27], gtimer());  // P4 word loop done
   for (uint32_t q = threadIdx.x; q < min(sh_nwb, WB_CAP); q += FT) d2h += d.wb_bytes[base + wb_list[q]];
   uint32_t *cpf = d.f_cta_cpf + (uint64_t)c * NBL, *cev = d.f_cta_cev + (uint64_t)c * NBL;
   uint32_t *tot_pf = d.f_tot + 2 * NBL * par, *tot_ev = d.f_tot + 2 * NBL * par + NBL;
@@ -553,6 +556,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       atomicMin(&d.f_lmm[4 * NBL * par + 3 * NBL + b], mm_l[3 * NBL + b]);
     }
   }
+  if (threadIdx.x == 0) atomicMax(&prof[28], gtimer());  // rows published
   {
     unsigned long long sums[4] = {h2d, d2h, tie_kept, (unsigned long long)n_el};
     block_sum_v<unsigned long long, 4, FT>(sums);

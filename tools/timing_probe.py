@@ -59,7 +59,7 @@ for mode in ("eager", "graph", "eager_sync"):
                       "P5end", r(7), "B5", r(8), "| max over CTAs: P1end", r(11), "P3end", r(14), "P4end", r(12),
                       "P5end", r(13), "P6tables", r(19), "P6big", r(20), "end", r(1),
                       "| small", int(st[16]), "nbig", int(st[17]), "maxseg", int(st[18]),
-                      "rank_ns_max", int(st[21]), "work_max", int(st[22]), "iters_max", int(st[23]), "W", int(st[24]))
+                      "rank_ns_max", int(st[21]), "work_max", int(st[22]), "iters_max", int(st[23]), "W", int(st[24]), "| P1loop", r(25), "P1pub", r(26), "P4loop", r(27), "P4rows", r(28))
         print("eager_sync per-step ms", np.round(ts, 4))
         t0.record(pl.stream); t1.record(pl.stream)
     torch.cuda.synchronize()
