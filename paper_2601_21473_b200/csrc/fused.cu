@@ -35,7 +35,7 @@ constexpr int FT = 1024;  // threads per CTA
 constexpr int FWARPS = FT / 32;
 constexpr int NB1 = 4096;  // level-1 buckets: distance bits [30:19]
 constexpr int NBL = 1024;  // list-sort buckets: distance bits [30:21]
-constexpr int LOAD_BATCH = 8;  // records in flight per thread in P1
+constexpr int LOAD_BATCH = 4;  // records in flight per thread in P1
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -333,9 +333,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
 
   // ---------------- P1: score + level-1 histogram
   // per-thread copies of the parameters used per agent (Params lives in shared memory)
-  const float hop_scale = p.hop_scale;
-  __shared__ float thv[4];  // prefetch threshold per class (class 3: malformed, never prefetched)
-  if (threadIdx.x < 4) thv[threadIdx.x] = threadIdx.x < 3 ? p.theta[threadIdx.x] : 0.0f;
+  const float hop_scale = p.hop_scale, th0 = p.theta[0], th1 = p.theta[1], th2 = p.theta[2];
   const uint64_t n_kin = p.n_kin;
   const float *dint = d.dint;
   const uint4 *rec = p.rec + base;
@@ -360,19 +358,20 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       const bool valid = k < n_here;
       const bool res = (s.old_w[k >> 5] >> (k & 31)) & 1u;
       const uint32_t ph = r[j].z & 3u, cl = (r[j].z >> 2) & 3u;
-      float dist;
+      float dist, th;
       if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {
         // the warp holds interaction / diffusion / malformed records: general definition
         dist = valid ? distance_of(r[j], now, hop_scale, dint, n_kin, st) : 0.0f;
+        th = (cl & 2u) ? ((cl & 1u) ? 0.0f : th2) : ((cl & 1u) ? th1 : th0);
       } else {
         // independent agents only: remaining action ticks, 0 while in an LLM
         // phase, +inf when idle — the same values distance_of gives for class 0
         const int64_t remain = (int64_t)r[j].x - now;
         const float d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
         dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
+        th = th0;
       }
       const uint32_t bits = __float_as_uint(dist);
-      const float th = thv[cl];
       const bool elig = valid && (res || dist == 0.0f || dist < th);
       s.keys[k] = bits;
       s.fp[k] = r[j].y;
