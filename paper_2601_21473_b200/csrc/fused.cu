@@ -73,9 +73,12 @@ struct GridBar {
 // Kernel arguments: a batch of independent planner instances (one per context; C5's
 // replicas x budgets), each planned by its own group of B.gsize CTAs.  A single context is
 // a batch of one whose group spans every SM.
+// MAXB = 1 for a single context keeps the kernel parameter block small (48 B of instance
+// data instead of 7.7 KB): graph replays of the single-context step pay per launch for it.
+template <int MAXB>
 struct FusedArgs {
   uint32_t n_inst, gsize;
-  FusedInst inst[FUSED_MAX_BATCH];
+  FusedInst inst[MAXB];
 };
 
 struct InstArgs {
@@ -289,7 +292,8 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
   }
 }
 
-__global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ FusedArgs B) {
+template <int MAXB>
+__global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ FusedArgs<MAXB> B) {
   const uint32_t gi = blockIdx.x / B.gsize;
   const uint32_t c = blockIdx.x % B.gsize, G = B.gsize;
   const FusedInst &I = B.inst[gi];
@@ -849,18 +853,25 @@ bool fused_supported(const Params &p, int grid, uint32_t *tile_out) {
 }
 
 // 1 CTA of FT threads per SM must be resident for the whole grid (grid barrier).
-bool fused_prepare(int grid, uint32_t tile) {
-  if (cudaFuncSetAttribute(k_fused_plan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int MAXB>
+static bool prepare_one(uint32_t tile) {
+  if (cudaFuncSetAttribute(k_fused_plan<MAXB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)fused_smem_bytes(FUSED_MAX_TILE)) != cudaSuccess)
     return false;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_plan, FT, fused_smem_bytes(tile)) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_plan<MAXB>, FT, fused_smem_bytes(tile)) !=
+      cudaSuccess)
     return false;
-  return per_sm >= 1 && grid >= 1;
+  return per_sm >= 1;
 }
 
-int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s) {
-  FusedArgs B;
+bool fused_prepare(int grid, uint32_t tile) {
+  return grid >= 1 && prepare_one<1>(tile) && prepare_one<FUSED_MAX_BATCH>(tile);
+}
+
+template <int MAXB>
+static void launch_t(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s) {
+  FusedArgs<MAXB> B;
   B.n_inst = n;
   B.gsize = gsize;
   uint32_t tile = 32;
@@ -868,7 +879,12 @@ int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaS
     B.inst[i] = insts[i];
     tile = insts[i].tile > tile ? insts[i].tile : tile;
   }
-  k_fused_plan<<<n * gsize, FT, fused_smem_bytes(tile), s>>>(B);
+  k_fused_plan<MAXB><<<n * gsize, FT, fused_smem_bytes(tile), s>>>(B);
+}
+
+int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s) {
+  if (n == 1) launch_t<1>(insts, n, gsize, s);
+  else launch_t<FUSED_MAX_BATCH>(insts, n, gsize, s);
   return 1;
 }
 
