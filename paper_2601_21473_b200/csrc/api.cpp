@@ -90,12 +90,10 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_cta_cev = take(4 * (uint64_t)FUSED_MAX_CTAS * 1024);
   L.f_tot = take(4 * 2 * 2 * 1024);
   L.f_acc = take(8 * 2 * 8);
-  L.f_tie_val = take(8 * (uint64_t)FUSED_MAX_CTAS);
-  L.f_tie_flag = take(4 * (uint64_t)FUSED_MAX_CTAS);
   L.f_rows1 = take(8 * (uint64_t)FUSED_MAX_CTAS * 4096);
   L.f_rows2 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
   L.f_rows3 = take(8 * (uint64_t)FUSED_MAX_CTAS * 1024);
-  L.f_lmm = take(4 * 2 * 4 * 1024);
+  L.f_cta_lmm = take(4 * (uint64_t)FUSED_MAX_CTAS * 6 * 1024);
   L.wb_bytes = take(4 * n1);
   L.params_dev = take(sizeof(Params));
   L.f_sk2 = take(4 * n1);
@@ -162,12 +160,10 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_cta_cev = (uint32_t *)(b + L.f_cta_cev);
   d.f_tot = (uint32_t *)(b + L.f_tot);
   d.f_acc = (unsigned long long *)(b + L.f_acc);
-  d.f_tie_val = (unsigned long long *)(b + L.f_tie_val);
-  d.f_tie_flag = (unsigned int *)(b + L.f_tie_flag);
   d.f_rows1 = (unsigned long long *)(b + L.f_rows1);
   d.f_rows2 = (unsigned long long *)(b + L.f_rows2);
   d.f_rows3 = (unsigned long long *)(b + L.f_rows3);
-  d.f_lmm = (uint32_t *)(b + L.f_lmm);
+  d.f_cta_lmm = (uint32_t *)(b + L.f_cta_lmm);
   d.wb_bytes = (uint32_t *)(b + L.wb_bytes);
   d.params_dev = (uint8_t *)(b + L.params_dev);
   d.f_sk2 = (uint32_t *)(b + L.f_sk2);
@@ -377,6 +373,7 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
   p.desc_cap = L.desc_cap;
   for (int k = 0; k < 3; ++k) p.theta[k] = cfg->theta[k];
   p.hop_scale = cfg->hop_scale;
+  p.int_mode = (cfg->n_kin == 0 && cfg->hop_scale == std::floor(cfg->hop_scale)) ? 1 : 0;
   p.rank = cfg->rank;
   p.world = cfg->world;
   p.rec = reinterpret_cast<const uint4 *>(t->agent_rec);
@@ -489,8 +486,7 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
       c->fused_grid = sms;
       c->sms = sms;
       if (cudaMemsetAsync(p.d.f_mm1, 0xFF, 4 * 2 * 2 * 4096, c->stream) != cudaSuccess ||
-          cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2 * 1024, c->stream) != cudaSuccess ||
-          cudaMemsetAsync(p.d.f_lmm, 0xFF, 4 * 2 * 4 * 1024, c->stream) != cudaSuccess)
+          cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2 * 1024, c->stream) != cudaSuccess)
         return fail(SCALESIM_E_CUDA);
     }
   }
@@ -567,6 +563,7 @@ static FusedInst fused_inst(const scalesim_ctx *c, uint32_t tile) {
   f.rec = c->p.rec;
   f.kin = c->p.kin;
   f.now = c->deferred_now;
+  f.n_local = c->p.n_local;
   f.cur = (uint32_t)c->p.cur;
   f.parity = (uint32_t)(c->fused_steps & 1);
   f.epoch = (uint32_t)(c->fused_steps + 1);

@@ -49,9 +49,16 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
   return v;
 }
 
-// Grid barrier for a grid of co-resident CTAs.  bar counts arrivals within one launch; the
-// k-th barrier waits for k * n arrivals (n = CTAs of the instance).  Launch L uses bar[L & 1]; launch L-1 reset it
-// (same stream, so every CTA of launch L-2 had finished).
+__device__ __forceinline__ void red_release(unsigned int *p, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid barrier for a grid of co-resident CTAs (arrive: release reduction on a counter; wait:
+// acquire polling; the CTA barriers order the other threads' accesses).  bar counts arrivals
+// within one launch; the k-th barrier waits for k * n arrivals (n = CTAs of the instance).
+// Launch L uses bar[L & 1]; launch L-1 reset it (same stream, so every CTA of launch L-2 had
+// finished).  Measured on B200 (tools/bar_bench.cu, 148 CTAs x 1024 threads): 1.22 us per
+// barrier; per-CTA flags polled by a warp: 2.4 us.
 struct GridBar {
   unsigned int *bar;
   unsigned int k;
@@ -60,11 +67,10 @@ struct GridBar {
     __syncthreads();
     if (threadIdx.x == 0) {
       ++k;
-      __threadfence();
-      atomicAdd(bar, 1u);
+      red_release(bar, 1u);
       const unsigned int target = k * n;
-      while (ld_acquire(bar) < target) __nanosleep(40);  // back off: 148 CTAs poll one line
-      __threadfence();
+      while (ld_acquire(bar) < target) {
+      }
     }
     __syncthreads();
   }
@@ -84,7 +90,7 @@ struct FusedArgs {
 struct InstArgs {
   int64_t now;
   int parity;
-  unsigned int epoch;  // launch number of the instance (>= 1), tags the per-CTA tie flags
+  unsigned int epoch;  // launch number of the instance (>= 1)
   uint32_t tile;       // agents per CTA, multiple of 32
   uint32_t tw;         // tile / 32
 };
@@ -136,6 +142,11 @@ __device__ __forceinline__ void clear_hist(uint32_t *h, int nb) {
   }
 }
 
+// Level-1 histogram slot of bucket b: the bucket's low two bits go to the top, so buckets
+// that differ by multiples of 4 (consecutive small integer distances: bits [22:21] fixed)
+// fall in different shared-memory banks.
+__device__ __forceinline__ uint32_t slot1(uint32_t b) { return (b >> 2) | ((b & 3u) << 10); }
+
 // one lane's contribution to the byte-weighted histogram (native 32-bit shared atomics)
 __device__ __forceinline__ void hist_lane(uint32_t *h, int nb, uint32_t b, uint32_t bits, uint32_t bytes) {
   atomicAdd(&h[b], bytes & 0xFFFFu);
@@ -149,13 +160,14 @@ __device__ __forceinline__ void hist_lane(uint32_t *h, int nb, uint32_t b, uint3
 __device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned long long *g_hist, uint32_t *g_mm,
                                              unsigned long long *row) {
   for (int b = threadIdx.x; b < nb; b += FT) {
-    const unsigned long long v = ((unsigned long long)h[nb + b] << 16) + h[b];
+    const uint32_t q = nb == NB1 ? slot1(b) : (uint32_t)b;
+    const unsigned long long v = ((unsigned long long)h[nb + q] << 16) + h[q];
     row[b] = v;
     if (v != 0) {
       atomicAdd(&g_hist[b], v);
       if (g_mm) {
-        atomicMin(&g_mm[b], h[2 * nb + b]);
-        atomicMin(&g_mm[nb + b], h[3 * nb + b]);
+        atomicMin(&g_mm[b], h[2 * nb + q]);
+        atomicMin(&g_mm[nb + b], h[3 * nb + q]);
       }
     }
   }
@@ -169,21 +181,30 @@ struct Sel {
 
 // Boundary bucket of histogram level `level` (every CTA computes the same result).
 __device__ void select_level(const unsigned long long *g_hist, const uint32_t *g_mm, int level,
-                             unsigned long long budget, Sel &sel) {
+                             unsigned long long budget, Sel &sel, bool imode = false) {
   const int nb = level == 1 ? NB1 : (level == 2 ? 1024 : 512);
   const int shift = level == 1 ? 19 : (level == 2 ? 9 : 0);
   const int per = nb / FT;  // 4, 1 or 0 (level 3: threads < 512)
   __shared__ unsigned long long sh_tot, sh_prev;
-  __shared__ uint32_t sh_b;
+  __shared__ uint32_t sh_b, sh_min, sh_nmax;
   if (threadIdx.x == 0) sh_b = 0xFFFFFFFFu;
   unsigned long long hv[4] = {0, 0, 0, 0};
+  uint32_t mnv[4] = {0, 0, 0, 0}, nmxv[4] = {0, 0, 0, 0};
   unsigned long long loc = 0;
   const int mine = per > 0 ? per : ((int)threadIdx.x < nb ? 1 : 0);
   const int b0 = per > 0 ? threadIdx.x * per : threadIdx.x;
-  for (int k = 0; k < mine; ++k) {
-    hv[k] = g_hist[b0 + k];
-    loc += hv[k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {  // all loads at once (min / max with the bytes: no second round trip)
+    if (k < mine) {
+      hv[k] = g_hist[b0 + k];
+      if (g_mm) {
+        mnv[k] = g_mm[b0 + k];
+        nmxv[k] = g_mm[nb + b0 + k];
+      }
+    }
   }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) loc += hv[k];
   const unsigned long long ex = block_excl_scan<unsigned long long, FT>(loc, &sh_tot);
   __syncthreads();
   unsigned long long run = sel.below + ex;
@@ -193,6 +214,8 @@ __device__ void select_level(const unsigned long long *g_hist, const uint32_t *g
     if (run > budget && prev <= budget) {  // exactly one bucket crosses (sums are monotone)
       sh_b = b0 + k;
       sh_prev = prev;
+      sh_min = mnv[k];
+      sh_nmax = nmxv[k];
     }
   }
   __syncthreads();
@@ -205,9 +228,12 @@ __device__ void select_level(const unsigned long long *g_hist, const uint32_t *g
   } else {
     sel.below = sh_prev;
     sel.prefix |= b << shift;
-    const bool single = g_mm != nullptr && g_mm[b] == ~g_mm[nb + b];
+    // integer distances (level 1, no min / max kept): a bucket of exponent <= 4 (d < 32),
+    // the zero bucket and the +inf bucket each hold one value, bits = b << 19
+    const bool int_single = imode && level == 1 && ((b >> 4) <= 131u || b == 0xFF0u);
+    const bool single = int_single || (g_mm != nullptr && sh_min == ~sh_nmax);
     if (level == 3 || single) {
-      sel.dstar = (level == 3) ? sel.prefix : g_mm[b];
+      sel.dstar = (level == 3) ? sel.prefix : (int_single ? (b << 19) : sh_min);
       sel.rem = budget - sel.below;
       sel.done = 1;
       sel.level_res = level;
@@ -297,6 +323,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   const uint32_t gi = blockIdx.x / B.gsize;
   const uint32_t c = blockIdx.x % B.gsize, G = B.gsize;
   const FusedInst &I = B.inst[gi];
+  if (threadIdx.x == 0) {  // this tile's records into L2 while the parameters are fetched
+    const uint64_t b0 = (uint64_t)c * I.tile;
+    if (b0 < I.n_local) {
+      const uint64_t nb = 16 * (I.n_local - b0 < I.tile ? I.n_local - b0 : I.tile);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(I.rec + b0), "r"((uint32_t)nb) : "memory");
+    }
+  }
   __shared__ __align__(16) Params sp;  // the instance's parameters (device copy + per-launch fields)
   {
     const uint32_t *src = reinterpret_cast<const uint32_t *>(I.params);
@@ -314,13 +347,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   const InstArgs A = {I.now, (int)I.parity, I.epoch, I.tile, I.tile / 32};
   const Dev &d = p.d;
   GridBar grid{d.f_bar + A.parity, 0u, G};
+  if (c == 0 && threadIdx.x == 0) d.f_bar[A.parity ^ 1] = 0u;  // for launch L+1
   unsigned long long *prof = d.f_prof;
   if (threadIdx.x == 0) {
     const unsigned long long t = gtimer();
     atomicMin(&prof[0], t);
     if (c == 0) prof[2] = t;
   }
-  if (c == 0 && threadIdx.x == 0) d.f_bar[A.parity ^ 1] = 0u;  // for launch L+1
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const FSmem s = carve(smem_raw, A.tile, A.tw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -343,6 +376,11 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   const uint4 *rec = p.rec + base;
   uint32_t *gkeys = p.keep_dist ? d.keys + base : nullptr;
   const int64_t now = A.now;
+  const bool imode = p.int_mode != 0;
+  // remaining ticks in 32-bit arithmetic when now fits (t_next is 32-bit): exact for < 2^24,
+  // rounded to nearest as __ll2float_rn above
+  const bool now32 = now >= 0 && now <= 0xFFFFFFFFll;
+  const uint32_t nowl = (uint32_t)now;
   clear_hist(s.h, NB1);
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_old[base / 32 + w] : 0u;
   __syncthreads();
@@ -370,8 +408,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       } else {
         // independent agents only: remaining action ticks, 0 while in an LLM
         // phase, +inf when idle — the same values distance_of gives for class 0
-        const int64_t remain = (int64_t)r[j].x - now;
-        const float d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
+        float d_action;
+        if (now32) {
+          d_action = r[j].x > nowl ? __uint2float_rn(r[j].x - nowl) : 0.0f;
+        } else {
+          const int64_t remain = (int64_t)r[j].x - now;
+          d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
+        }
         dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
         th = th0;
       }
@@ -386,7 +429,15 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         s.elig_w[k >> 5] = eb;
         s.dirty_w[k >> 5] = db;
       }
-      if (elig) hist_lane(s.h, NB1, bits >> 19, bits, r[j].y);
+      if (elig) {
+        const uint32_t q = slot1(bits >> 19);
+        atomicAdd(&s.h[q], r[j].y & 0xFFFFu);
+        atomicAdd(&s.h[NB1 + q], r[j].y >> 16);
+        if (!imode) {  // min / max key only where a bucket can hold several distances
+          atomicMin(&s.h[2 * NB1 + q], bits);
+          atomicMin(&s.h[3 * NB1 + q], ~bits);
+        }
+      }
       if (valid && dist == 0.0f) zero_b += r[j].y;
     }
   }
@@ -394,7 +445,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   if (threadIdx.x == 0) atomicMax(&prof[25], gtimer());  // P1 loop done
   // this CTA's level-1 bytes: dense row (its column entry gives the tie prefix in P3) and
   // the global sum
-  publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, d.f_mm1 + 2 * NB1 * par, d.f_rows1 + (uint64_t)c * NB1);
+  publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, imode ? nullptr : d.f_mm1 + 2 * NB1 * par,
+               d.f_rows1 + (uint64_t)c * NB1);
   if (threadIdx.x == 0) atomicMax(&prof[26], gtimer());  // published
   zero_b = block_sum<unsigned long long, FT>(zero_b);
   st = __reduce_or_sync(0xFFFFFFFFu, st);
@@ -415,7 +467,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       d.f_mm1[2 * NB1 * q + NB1 + b] = 0xFFFFFFFFu;
     }
     for (uint32_t b = gt; b < 2 * NBL; b += gs) d.f_tot[2 * NBL * q + b] = 0;
-    for (uint32_t b = gt; b < 4 * NBL; b += gs) d.f_lmm[4 * NBL * q + b] = 0xFFFFFFFFu;
     for (uint32_t b = gt; b < 1024; b += gs) {
       d.f_hist2[1024 * q + b] = 0;
       d.f_hist3[1024 * q + b] = 0;
@@ -426,7 +477,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   const uint32_t *mm1 = d.f_mm1 + 2 * NB1 * par;
   Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 1, 0};
-  select_level(d.f_hist1 + NB1 * par, mm1, 1, p.budget, sel);
+  select_level(d.f_hist1 + NB1 * par, imode ? nullptr : mm1, 1, p.budget, sel, imode);
   for (int level = 2; level <= 3 && !sel.done; ++level) {
     const int hi_shift = level == 2 ? 19 : 9, shift = level == 2 ? 9 : 0;
     const int nb = level == 2 ? 1024 : 512;
@@ -450,6 +501,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   if (c == 0 && threadIdx.x == 0) prof[9] = gtimer();
 
   // ---------------- P3: tie group: id-order prefix of the bytes at d == D*
+  unsigned long long t_rows = 0;  // preceding CTAs' bytes in the resolving bucket (published rows)
+  if (!all_fit && threadIdx.x < c) {
+    const unsigned long long *rows = sel.level_res == 1 ? d.f_rows1 : (sel.level_res == 2 ? d.f_rows2 : d.f_rows3);
+    const uint32_t stride = sel.level_res == 1 ? NB1 : 1024;
+    t_rows = rows[(uint64_t)threadIdx.x * stride + sel.b_res];
+  }
   unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw]
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
@@ -467,14 +524,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     if (w < A.tw) word_tie[w] = ex;
     __syncthreads();
   }
-  {  // preceding CTAs: their bytes in the resolving bucket (published rows; one load each)
-    unsigned long long t = 0;
-    if (!all_fit && threadIdx.x < c) {
-      const unsigned long long *rows = sel.level_res == 1 ? d.f_rows1 : (sel.level_res == 2 ? d.f_rows2 : d.f_rows3);
-      const uint32_t stride = sel.level_res == 1 ? NB1 : 1024;
-      t = rows[(uint64_t)threadIdx.x * stride + sel.b_res];
-    }
-    t = block_sum<unsigned long long, FT>(t);
+  {
+    const unsigned long long t = block_sum<unsigned long long, FT>(t_rows);
     if (threadIdx.x == 0) sh_tie_excl = t;
   }
   __syncthreads();
@@ -483,130 +534,104 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
 
   // ---------------- P4: emit
   uint32_t *cnt_pf = s.h, *cnt_ev = s.h + NBL;  // per-CTA list members per list bucket
+  uint32_t *lor_l = s.h + 6 * NBL;   // [2][NBL]: OR of the key bits below the list bucket
   uint32_t *mm_l = s.h + 10 * NBL;  // [4][NBL]: prefetch min, prefetch ~max, evict min, evict ~max
-  for (int b = threadIdx.x; b < 2 * NBL; b += FT) s.h[b] = 0;
+  for (int b = threadIdx.x; b < 2 * NBL; b += FT) {
+    s.h[b] = 0;
+    lor_l[b] = 0;
+  }
   for (int b = threadIdx.x; b < 4 * NBL; b += FT) mm_l[b] = 0xFFFFFFFFu;
   __syncthreads();
   unsigned long long h2d = 0, d2h = 0, tie_kept = 0;
-  uint32_t n_el = 0;
-  constexpr uint32_t WB_CAP = 5 * NBL;
-  uint32_t *wb_list = s.h + 2 * NBL;  // evicted dirty agents of this tile (s.h[2NBL, 7NBL) is free here)
-  __shared__ uint32_t sh_nwb;
-  if (threadIdx.x == 0) sh_nwb = 0;
-  __syncthreads();
+  uint32_t n_el = 0, wb_pend = 0;  // wb_pend: write-back bytes load in flight (added one use later)
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
-    const bool el = (s.elig_w[w] >> lane) & 1u;  // 0 beyond n_here
+    const uint32_t elw = s.elig_w[w];  // 0 beyond n_here
     const uint32_t key = s.keys[k];
-    const bool tie = el && !all_fit && key == dstar;
-    const uint32_t fp = s.fp[k];
-    bool tie_ok = false;
-    if (__ballot_sync(0xFFFFFFFFu, tie)) {  // id-order inclusive prefix of the tie bytes
-      unsigned long long incl = tie ? fp : 0u;
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += t;
+    uint32_t kw = elw;  // kept agents of the word
+    if (!all_fit) {
+      kw = __ballot_sync(0xFFFFFFFFu, key < dstar) & elw;
+      const uint32_t tiew = __ballot_sync(0xFFFFFFFFu, key == dstar) & elw;
+      if (tiew) {  // id-order inclusive prefix of the tie bytes
+        const bool tie = (tiew >> lane) & 1u;
+        const uint32_t fp = s.fp[k];
+        unsigned long long incl = tie ? fp : 0u;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        incl += sh_tie_excl + word_tie[w];
+        const bool ok = tie && incl <= sel.rem;
+        if (ok) tie_kept += fp;
+        kw |= __ballot_sync(0xFFFFFFFFu, ok);
       }
-      incl += sh_tie_excl + word_tie[w];
-      tie_ok = tie && incl <= sel.rem;
     }
-    const bool kept = el && (all_fit || key < dstar || tie_ok);
-    if (tie && kept) tie_kept += fp;
-    const uint32_t kw = __ballot_sync(0xFFFFFFFFu, kept);
     const uint32_t old = s.old_w[w];
     const uint32_t pfw = kw & ~old, evw = old & ~kw;
     if (lane == 0) {
       if (w < tw_here) bm_new[base / 32 + w] = kw;
       s.pf_w[w] = pfw;
       s.ev_w[w] = evw;
-      n_el += __popc(s.elig_w[w]);
+      n_el += __popc(elw);
     }
-    if ((pfw >> lane) & 1u) {
-      h2d += fp;
-      atomicAdd(&cnt_pf[key >> 21], 1u);
-      atomicMin(&mm_l[key >> 21], key);
-      atomicMin(&mm_l[NBL + (key >> 21)], ~key);
-    }
-    if ((evw >> lane) & 1u) {
-      if ((s.dirty_w[w] >> lane) & 1u) {  // R13: write-back bytes, loaded after the loop
-        const uint32_t slot = atomicAdd(&sh_nwb, 1u);
-        if (slot < WB_CAP) wb_list[slot] = k;
-        else d2h += d.wb_bytes[base + k];
+    if (pfw | evw) {  // list members in this word
+      const uint32_t bk = key >> 21;
+      if ((pfw >> lane) & 1u) {
+        h2d += s.fp[k];
+        atomicAdd(&cnt_pf[bk], 1u);
+        atomicMin(&mm_l[bk], key);
+        atomicMin(&mm_l[NBL + bk], ~key);
+        atomicOr(&lor_l[bk], key & 0x1FFFFFu);
       }
-      atomicAdd(&cnt_ev[key >> 21], 1u);
-      atomicMin(&mm_l[2 * NBL + (key >> 21)], key);
-      atomicMin(&mm_l[3 * NBL + (key >> 21)], ~key);
+      if ((evw >> lane) & 1u) {
+        if ((s.dirty_w[w] >> lane) & 1u) {  // R13: write-back bytes of a dirty evicted agent
+          d2h += wb_pend;
+          wb_pend = d.wb_bytes[base + k];
+        }
+        atomicAdd(&cnt_ev[bk], 1u);
+        atomicMin(&mm_l[2 * NBL + bk], key);
+        atomicMin(&mm_l[3 * NBL + bk], ~key);
+        atomicOr(&lor_l[NBL + bk], key & 0x1FFFFFu);
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&prof[27], gtimer());  // P4 word loop done
-  for (uint32_t q = threadIdx.x; q < min(sh_nwb, WB_CAP); q += FT) d2h += d.wb_bytes[base + wb_list[q]];
-  uint32_t *cpf = d.f_cta_cpf + (uint64_t)c * NBL, *cev = d.f_cta_cev + (uint64_t)c * NBL;
-  uint32_t *tot_pf = d.f_tot + 2 * NBL * par, *tot_ev = d.f_tot + 2 * NBL * par + NBL;
+  // list bucket totals (global atomics, issued now: they drain while the members are
+  // staged); the CTA's min / max key and OR of the low key bits per bucket go to its rows
   {
+    uint32_t *tot_pf = d.f_tot + 2 * NBL * par, *tot_ev = d.f_tot + 2 * NBL * par + NBL;
+    uint32_t *rm = d.f_cta_lmm + (uint64_t)c * 6 * NBL;
     const int b = threadIdx.x;  // NBL == FT
     const uint32_t a = cnt_pf[b], e = cnt_ev[b];
-    cpf[b] = a;
-    cev[b] = e;
     if (a) {
       atomicAdd(&tot_pf[b], a);
-      atomicMin(&d.f_lmm[4 * NBL * par + b], mm_l[b]);
-      atomicMin(&d.f_lmm[4 * NBL * par + NBL + b], mm_l[NBL + b]);
+      rm[b] = mm_l[b];
+      rm[NBL + b] = mm_l[NBL + b];
+      rm[2 * NBL + b] = lor_l[b];
     }
     if (e) {
       atomicAdd(&tot_ev[b], e);
-      atomicMin(&d.f_lmm[4 * NBL * par + 2 * NBL + b], mm_l[2 * NBL + b]);
-      atomicMin(&d.f_lmm[4 * NBL * par + 3 * NBL + b], mm_l[3 * NBL + b]);
+      rm[3 * NBL + b] = mm_l[2 * NBL + b];
+      rm[4 * NBL + b] = mm_l[3 * NBL + b];
+      rm[5 * NBL + b] = lor_l[NBL + b];
     }
   }
-  if (threadIdx.x == 0) atomicMax(&prof[28], gtimer());  // rows published
-  {
-    unsigned long long sums[4] = {h2d, d2h, tie_kept, (unsigned long long)n_el};
-    block_sum_v<unsigned long long, 4, FT>(sums);
-    if (threadIdx.x < 4 && sums[threadIdx.x]) atomicAdd(&acc[1 + threadIdx.x], sums[threadIdx.x]);
-  }
-  if (threadIdx.x == 0) atomicMax(&prof[12], gtimer());
-  if (c == 0 && threadIdx.x == 0) prof[5] = gtimer();
-  grid.sync();
-  if (c == 0 && threadIdx.x == 0) prof[6] = gtimer();
-
-  // ---------------- P5: stable bucket sort of the lists
-  uint32_t *g_pf = s.h + 2 * NBL, *g_ev = s.h + 3 * NBL;  // first slot of this CTA's members per bucket
-  uint32_t *tpf = s.h + 8 * NBL, *tev = s.h + 9 * NBL;    // list bucket totals (shared copy)
-  // list bucket b needs the re-sort by full distance iff its members hold several distances
-  uint32_t *lmulti = s.h + 7 * NBL;  // bit 0: prefetch list, bit 1: evict list
-  {
-    const uint32_t b = threadIdx.x;
-    const uint32_t *lmm = d.f_lmm + 4 * NBL * par;
-    const uint32_t mp = lmm[b], xp = ~lmm[NBL + b], me = lmm[2 * NBL + b], xe = ~lmm[3 * NBL + b];
-    lmulti[b] = ((mp != 0xFFFFFFFFu && mp != xp) ? 1u : 0u) | ((me != 0xFFFFFFFFu && me != xe) ? 2u : 0u);
-  }
-  __shared__ uint32_t sh_npf, sh_nev, sh_mpf, sh_mev, sh_need;
-  {
-    const uint32_t b = threadIdx.x, rb = NBL - 1 - b;  // NBL == FT; evict: descending buckets
-    uint32_t v[2] = {tot_pf[b], tot_ev[rb]}, tt[2];
-    tpf[b] = v[0];
-    tev[rb] = v[1];
-    block_excl_scan_v<uint32_t, 2, FT>(v, tt);
-    g_pf[b] = v[0];
-    g_ev[rb] = v[1];
-    if (threadIdx.x == 0) {
-      sh_npf = tt[0];
-      sh_nev = tt[1];
-    }
-  }
-  // members in list order (prefetch ascending id, evict descending id; tile-local indices)
-  // into memb; one word per thread (tw <= FT)
+  // This tile's list members in list order (prefetch ascending id, evict descending id) into
+  // memb, and the bucket-major offsets of the staging area (one word / bucket per thread:
+  // tw <= FT == NBL)
+  uint32_t *off_pf = s.h + 2 * NBL, *off_ev = s.h + 3 * NBL;
+  __shared__ uint32_t sh_mpf, sh_mev;
   {
     const uint32_t w = threadIdx.x;
     const uint32_t pw = w < A.tw ? s.pf_w[w] : 0u, ew = w < A.tw ? s.ev_w[w] : 0u;
-    uint32_t v[2] = {(uint32_t)__popc(pw), (uint32_t)__popc(ew)}, tt[2];
-    block_excl_scan_v<uint32_t, 2, FT>(v, tt);
-    const uint32_t need = __syncthreads_or(lmulti[threadIdx.x] != 0u);
+    uint32_t v[4] = {(uint32_t)__popc(pw), (uint32_t)__popc(ew), cnt_pf[w], cnt_ev[w]}, tt[4];
+    block_excl_scan_v<uint32_t, 4, FT>(v, tt);
+    off_pf[w] = v[2];
+    off_ev[w] = v[3];
     if (threadIdx.x == 0) {
       sh_mpf = tt[0];
       sh_mev = tt[1];
-      sh_need = need;
     }
     uint32_t m = pw, o = v[0];
     while (m) {
@@ -624,19 +649,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   __syncthreads();
   const uint32_t m_pf = sh_mpf, m_ev = sh_mev;
-  uint32_t *mem_pf = s.memb, *mem_ev = s.memb + m_pf;
-  // own nonzero list buckets (for the column prefix)
-  uint32_t *own_b = s.h + 6 * NBL;
-  __shared__ uint32_t sh_nown;
-  if (threadIdx.x == 0) sh_nown = 0;
-  __syncthreads();
-  if (cnt_pf[threadIdx.x] || cnt_ev[threadIdx.x]) own_b[atomicAdd(&sh_nown, 1u)] = threadIdx.x;
-  __syncthreads();
-  // (a) warps 0/1: in-CTA rank of every member within its bucket (list order), into fp[]
-  // (b) other warps: members of the same bucket in the preceding (prefetch) / following
-  //     (evict) CTAs, added to the bucket starts
+  // in-CTA rank of every member within its bucket (list order), warp 0 prefetch, warp 1
+  // evict, into fp[]
   if (warp < 2) {
-    const uint32_t *mem = warp == 0 ? mem_pf : mem_ev;
+    const uint32_t *mem = s.memb + (warp == 0 ? 0 : m_pf);
     const uint32_t m = warp == 0 ? m_pf : m_ev;
     uint32_t *run = warp == 0 ? s.h + 4 * NBL : s.h + 5 * NBL;
     for (uint32_t b = lane; b < NBL; b += 32) run[b] = 0;
@@ -653,190 +669,291 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       __syncwarp();
       if (on) s.fp[(warp == 0 ? 0 : m_pf) + e] = r;
     }
-  } else {
-    const uint32_t nown = sh_nown;
-    for (uint32_t j = warp - 2; j < nown; j += FWARPS - 2) {
-      const uint32_t b = own_b[j];
-      const bool has_pf = cnt_pf[b] != 0, has_ev = cnt_ev[b] != 0;
-      uint32_t ppf = 0, pev = 0;
-      for (uint32_t q = lane; q < G; q += 32) {
-        if (has_pf && q < c) ppf += d.f_cta_cpf[(uint64_t)q * NBL + b];
-        if (has_ev && q > c) pev += d.f_cta_cev[(uint64_t)q * NBL + b];
-      }
-      ppf = __reduce_add_sync(0xFFFFFFFFu, ppf);
-      pev = __reduce_add_sync(0xFFFFFFFFu, pev);
-      if (lane == 0) {
-        g_pf[b] += ppf;
-        g_ev[b] += pev;
-      }
-    }
   }
   __syncthreads();
-  // members of buckets holding several distances are also staged (key, id) by slot for P6
+  // stage (key, id) bucket-major in this tile's range of the staging arrays: bucket b's
+  // members at base + off[b] + rank, in list order
   for (uint32_t e = threadIdx.x; e < m_pf + m_ev; e += FT) {
     const uint32_t k = s.memb[e];
     const uint32_t key = s.keys[k];
     const uint32_t bk = key >> 21;
     const uint32_t id = (uint32_t)(p.shard_begin + base + k);
     if (e < m_pf) {
-      const uint32_t slot = g_pf[bk] + s.fp[e];
-      d.pf_ids[slot] = id;
-      if (lmulti[bk] & 1u) {
-        d.sort_ka[slot] = key;
-        d.sort_va[slot] = id;
-      }
+      const uint64_t slot = base + off_pf[bk] + s.fp[e];
+      d.sort_ka[slot] = key;
+      d.sort_va[slot] = id;
     } else {
-      const uint32_t slot = g_ev[bk] + s.fp[e];
-      d.ev_ids[slot] = id;
-      if (lmulti[bk] & 2u) {
-        d.f_sk2[slot] = ~key;  // evict: descending (distance, id) = ascending complement
-        d.f_sv2[slot] = id;
-      }
+      const uint64_t slot = base + off_ev[bk] + s.fp[e];
+      d.f_sk2[slot] = key;
+      d.f_sv2[slot] = id;
     }
   }
-  // header (CTA 0): all accumulators are complete after the last barrier
-  if (c == 0 && threadIdx.x == 0) {
+  {  // rows: offset << 16 | count (tile <= FUSED_MAX_TILE < 2^16)
+    const int b = threadIdx.x;  // NBL == FT
+    d.f_cta_cpf[(uint64_t)c * NBL + b] = (off_pf[b] << 16) | cnt_pf[b];
+    d.f_cta_cev[(uint64_t)c * NBL + b] = (off_ev[b] << 16) | cnt_ev[b];
+  }
+  d2h += wb_pend;
+  if (threadIdx.x == 0) atomicMax(&prof[28], gtimer());  // staged, rows published
+  {
+    unsigned long long sums[4] = {h2d, d2h, tie_kept, (unsigned long long)n_el};
+    block_sum_v<unsigned long long, 4, FT>(sums);
+    if (threadIdx.x < 4 && sums[threadIdx.x]) atomicAdd(&acc[1 + threadIdx.x], sums[threadIdx.x]);
+  }
+  if (threadIdx.x == 0) atomicMax(&prof[12], gtimer());
+  if (c == 0 && threadIdx.x == 0) prof[5] = gtimer();
+  grid.sync();
+  if (c == 0 && threadIdx.x == 0) prof[6] = gtimer();
+  if (c == 0 && threadIdx.x == 32) {  // header (CTA 0, warp 1): the accumulators are complete; loads first
+    const unsigned long long a0 = acc[0], a1 = acc[1], a2 = acc[2], a3 = acc[3], a4 = acc[4], a5 = acc[5];
+    const uint32_t st0 = d.state->status;  // + BAD_KIN/BAD_RECORD of k_int_compact
     unsigned long long *H = d.header;
-    H[H_N_PF] = sh_npf;
-    H[H_N_EV] = sh_nev;
-    H[H_H2D] = acc[1];
-    H[H_D2H] = acc[2];
+    const unsigned long long seq = H[H_SEQ];
+    H[H_H2D] = a1;
+    H[H_D2H] = a2;
     H[H_CUT_BITS] = all_fit ? 0xFFFFFFFFull : dstar;
     H[H_CUT_REM] = sel.rem;
-    H[H_KEPT] = (p.budget - sel.rem) + (all_fit ? 0ull : acc[3]);
-    H[H_N_ELIG] = acc[4];
-    uint32_t status = (uint32_t)acc[5] | d.state->status;  // + BAD_KIN/BAD_RECORD of k_int_compact
-    if (acc[0] > p.budget) status |= ST_INSUFFICIENT;
+    H[H_KEPT] = (p.budget - sel.rem) + (all_fit ? 0ull : a3);
+    H[H_N_ELIG] = a4;
+    uint32_t status = (uint32_t)a5 | st0;
+    if (a0 > p.budget) status |= ST_INSUFFICIENT;
     H[H_STATUS] = status;
-    H[H_SEQ] += 1;
+    H[H_SEQ] = seq + 1;
   }
-  if (threadIdx.x == 0) atomicMax(&prof[13], gtimer());
-  if (c == 0 && threadIdx.x == 0) prof[7] = gtimer();
-  if (!sh_need) {  // uniform: every CTA computed it from the same global totals
-    if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
-    return;
-  }
-  grid.sync();
-  if (c == 0 && threadIdx.x == 0) prof[8] = gtimer();
+  if (threadIdx.x == 0) atomicMax(&prof[30], gtimer());  // B4 passed (last CTA)
 
-  // ---------------- P6: order the segments of list buckets whose members hold several
-  // distances by (distance, id).  Segment table in list order (prefetch list first).  Short
-  // segments: every element's rank is counted against its segment's keys, the comparison
-  // work spread evenly over all CTAs; long ones are radix-sorted in global memory by one CTA.
-  uint32_t *seg_start = s.h + 10 * NBL, *seg_len = s.h + 12 * NBL;  // [2 * NBL] each
-  __shared__ uint32_t sh_nsmall, sh_nbig, sh_tmp, sh_gp, sh_nds;
-  uint32_t *dense_gp = s.h + 14 * NBL;  // [2 * NBL]: nonempty short segments in list order
-  uint32_t big_mask = 0, big_x = 0;  // this thread's long segments (bits for gp 2t, 2t+1) and their index
+  // ---------------- P5: list order.  A segment is the members of one list bucket, in list
+  // order (prefetch: ascending key; evict: descending key); its position in the list follows
+  // from the bucket totals.  Segments are cut into slices of CH elements, one slice per slot,
+  // slots dealt round-robin to the CTAs.  A slot gathers its segment from the CTAs' staging
+  // areas (CTA order = id order) and places
+  //   SINGLE  (one distance in the segment): its slice as is (already in (distance, id) order);
+  //   COUNT   (codes (key - min) >> g span <= RMAX values): its slice by a stable counting
+  //           sort whose counts cover the whole segment;
+  //   SORT1 / BIG (wider codes): the whole segment by a stable radix sort in shared / global
+  //           memory (one slot).
+  constexpr uint32_t RMAX = 2 * NBL;
+  enum { M_NONE = 0, M_SINGLE, M_COUNT, M_SORT1, M_BIG };
+  // per segment (index gp in list order: prefetch buckets ascending, then evict buckets
+  // descending): first slot, list position, length
+  uint32_t *slot_base = s.h + 6 * NBL, *seg_start = s.h + 8 * NBL, *seg_len = s.h + 10 * NBL;
+  uint32_t npf, nev, CH;  // list lengths, slice length (every thread)
+  __shared__ uint32_t sh_ns;
   {
-    // thread t owns the (list, bucket) positions 2t, 2t+1 of the 2048 in list order
-    // (prefetch buckets ascending, then evict buckets descending)
-    uint32_t len[2], small[2], big[2];
+    // thread t: segments 2t, 2t+1 (never on both lists: NBL is even)
+    const uint32_t list = 2 * threadIdx.x < NBL ? 0u : 1u;
+    const uint32_t *tot = d.f_tot + 2 * NBL * par + list * NBL;
+    uint32_t len[2];
+#pragma unroll
     for (int q = 0; q < 2; ++q) {
       const uint32_t gp = 2 * threadIdx.x + q;
-      const int list = gp < NBL ? 0 : 1;
-      const uint32_t b = list == 0 ? gp : (2 * NBL - 1 - gp);
-      len[q] = list == 0 ? tpf[b] : tev[b];
-      const bool mv = (lmulti[b] >> list) & 1u;
-      small[q] = (mv && 4 * len[q] <= 3 * A.tile) ? 1u : 0u;  // sortable in shared memory
-      big[q] = (mv && 4 * len[q] > 3 * A.tile) ? 1u : 0u;
+      len[q] = tot[list == 0 ? gp : 2 * NBL - 1 - gp];
     }
-    // segment start within its list (the evict list starts at position NBL)
-    uint32_t v[4] = {len[0] + len[1], small[0] * len[0] + small[1] * len[1], big[0] + big[1], small[0] + small[1]};
-    uint32_t tt[4];
-    block_excl_scan_v<uint32_t, 4, FT>(v, tt);
-    const uint32_t lx = v[0], dx = v[3];
-    big_x = v[2];
-    if (threadIdx.x == 0) {
-      sh_nsmall = tt[1];
-      sh_nbig = tt[2];
-      sh_nds = tt[3];
-    }
-    const uint32_t start0 = (2 * threadIdx.x < NBL) ? lx : lx - sh_npf;
-    const uint32_t start1 = (2 * threadIdx.x + 1 < NBL) ? lx + len[0] : lx + len[0] - sh_npf;
-    if (small[0]) dense_gp[dx] = 2 * threadIdx.x;
-    if (small[1]) dense_gp[dx + small[0]] = 2 * threadIdx.x + 1;
-    big_mask = big[0] | (big[1] << 1);
-    seg_start[2 * threadIdx.x] = start0;
-    seg_start[2 * threadIdx.x + 1] = start1;
-    seg_len[2 * threadIdx.x] = small[0] ? len[0] : 0u;
-    seg_len[2 * threadIdx.x + 1] = small[1] ? len[1] : 0u;
+    uint32_t v[2] = {list == 0 ? len[0] + len[1] : 0u, list == 1 ? len[0] + len[1] : 0u}, tt[2];
+    block_excl_scan_v<uint32_t, 2, FT>(v, tt);
+    if (threadIdx.x == 0) atomicMax(&prof[31], gtimer());  // totals loaded and scanned
+    npf = tt[0];
+    nev = tt[1];
+    // slice length: about two slots per CTA, 256..1024 elements
+    uint32_t ch = (2 * (npf + nev) / G + 31) / 32 * 32;
+    CH = ch < 256 ? 256 : (ch > 1024 ? 1024 : ch);
+    const uint32_t ns0 = (len[0] + CH - 1) / CH, ns1 = (len[1] + CH - 1) / CH;
+    seg_start[2 * threadIdx.x] = v[list];
+    seg_start[2 * threadIdx.x + 1] = v[list] + len[0];
+    seg_len[2 * threadIdx.x] = len[0];
+    seg_len[2 * threadIdx.x + 1] = len[1];
+    uint32_t w[1] = {ns0 + ns1}, wt[1];
+    block_excl_scan_v<uint32_t, 1, FT>(w, wt);
+    slot_base[2 * threadIdx.x] = w[0];
+    slot_base[2 * threadIdx.x + 1] = w[0] + ns0;
+    if (threadIdx.x == 0) sh_ns = wt[0];
+  }
+  if (c == 0 && threadIdx.x == 0) {
+    d.header[H_N_PF] = npf;
+    d.header[H_N_EV] = nev;
   }
   __syncthreads();
-  const uint32_t small_total = sh_nsmall, nbig = sh_nbig;
-  if (c == 0 && threadIdx.x == 0) {
-    prof[16] = small_total;
-    prof[17] = nbig;
-  }
-  {
-    const uint32_t m = max(seg_len[2 * threadIdx.x], seg_len[2 * threadIdx.x + 1]);
-    if (m) atomicMax(&prof[18], (unsigned long long)m);
-  }
-  if (threadIdx.x == 0) atomicMax(&prof[19], gtimer());
-  // long segments (rare): the j-th is radix-sorted in global memory by CTA j % G
-  for (uint32_t j = c; j < nbig; j += G) {
-    if ((big_mask & 1u) && big_x == j) sh_gp = 2 * threadIdx.x;
-    if ((big_mask & 2u) && big_x + (big_mask & 1u) == j) sh_gp = 2 * threadIdx.x + 1;
+  const uint32_t n_slots = sh_ns;
+  if (c == 0 && threadIdx.x == 0) prof[16] = n_slots;
+  if (threadIdx.x == 0) atomicMax(&prof[13], gtimer());  // P5 tables
+  if (c == 0 && threadIdx.x == 0) prof[7] = gtimer();
+  __shared__ uint32_t col_pre[FUSED_MAX_CTAS], col_src[FUSED_MAX_CTAS];
+  __shared__ uint32_t sh_gp, sh_tmp, sh_mm[3];
+  const unsigned long long t_s0 = gtimer();
+  unsigned long long dt[4] = {0, 0, 0, 0};  // slot sections (thread 0): segment + columns, gather, scan, place
+  for (uint32_t j = c; j < n_slots; j += G) {
+    unsigned long long tq = gtimer();
+    {  // the segment holding slot j
+      const uint32_t g0 = 2 * threadIdx.x;
+      const uint32_t a = slot_base[g0], m = slot_base[g0 + 1], z = g0 + 2 < 2 * NBL ? slot_base[g0 + 2] : n_slots;
+      if (a <= j && j < m) sh_gp = g0;
+      if (m <= j && j < z) sh_gp = g0 + 1;
+    }
     __syncthreads();
     const uint32_t gp = sh_gp;
-    const int list = gp < NBL ? 0 : 1;
-    const uint32_t b = list == 0 ? gp : (2 * NBL - 1 - gp);
-    const uint32_t t = list == 0 ? tpf[b] : tev[b];
-    const uint32_t start = seg_start[gp];
-    uint32_t *ids = list == 0 ? d.pf_ids : d.ev_ids;
-    uint32_t *ka = (list == 0 ? d.sort_ka : d.f_sk2) + start;
-    uint32_t *ia = (list == 0 ? d.sort_va : d.f_sv2) + start;
-    uint32_t *kb = (list == 0 ? d.sort_kb : d.f_sk3) + start;
-    uint32_t *ib = (list == 0 ? d.sort_vb : d.f_sv3) + start;
-    cta_sort_pairs(ka, ia, kb, ib, t, s.h);  // counters in s.h[0, 4096): not needed any more
-    for (uint32_t e = threadIdx.x; e < t; e += FT) ids[start + e] = ia[e];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) atomicMax(&prof[20], gtimer());
-  // short segments (fit in shared memory, 4 words per element): segment i (dense order) is
-  // sorted by CTA i % G.  Keys are first mapped to order-preserving small codes
-  // (key - min) >> g, g = common trailing zeros of the differences (integer-tick distances in
-  // one list bucket give a handful of codes), so the stable radix sort needs one 8-bit pass.
-  {
-    const uint32_t nds = sh_nds;
-    const unsigned long long t_r0 = gtimer();
-    __shared__ uint32_t sh_min, sh_or;
-    for (uint32_t i = c; i < nds; i += G) {
-      const uint32_t gp = dense_gp[i];
-      const int list = gp < NBL ? 0 : 1;
-      const uint32_t t = seg_len[gp], start = seg_start[gp];
-      const uint32_t *sk = (list == 0 ? d.sort_ka : d.f_sk2) + start;
-      const uint32_t *si = (list == 0 ? d.sort_va : d.f_sv2) + start;
-      uint32_t *ka = s.keys, *ia = s.keys + t, *kb = s.keys + 2 * t, *ib = s.keys + 3 * t;  // 4t <= 3 * tile
-      uint32_t mn = 0xFFFFFFFFu;
-      for (uint32_t j = threadIdx.x; j < t; j += FT) {
-        const uint32_t k = sk[j];
-        ka[j] = k;
-        ia[j] = si[j];
-        mn = min(mn, k);
+    const uint32_t list = gp < NBL ? 0u : 1u, b = list == 0 ? gp : 2 * NBL - 1 - gp;
+    const uint32_t len = seg_len[gp];
+    const uint32_t si = j - slot_base[gp];
+    // the segment's members in each CTA (list order of the CTAs: prefetch ascending, evict
+    // descending): first position and staging address; the segment's min / max key and OR of
+    // the low key bits
+    if (threadIdx.x == 0) {
+      sh_mm[0] = 0xFFFFFFFFu;
+      sh_mm[1] = 0xFFFFFFFFu;
+      sh_mm[2] = 0u;
+    }
+    {
+      uint32_t cnt = 0, src = 0, mn = 0xFFFFFFFFu, nmx = 0xFFFFFFFFu, lo = 0;
+      if ((int)threadIdx.x < (int)G) {
+        const uint32_t q = list == 0 ? threadIdx.x : G - 1 - threadIdx.x;
+        const uint32_t pk = (list == 0 ? d.f_cta_cpf : d.f_cta_cev)[(uint64_t)q * NBL + b];
+        const uint32_t *rm = d.f_cta_lmm + (uint64_t)q * 6 * NBL + 3 * list * NBL + b;
+        const uint32_t m0 = rm[0], m1 = rm[NBL], m2 = rm[2 * NBL];
+        cnt = pk & 0xFFFFu;
+        src = q * A.tile + (pk >> 16);
+        if (cnt) {
+          mn = m0;
+          nmx = m1;
+          lo = m2;
+        }
       }
       mn = __reduce_min_sync(0xFFFFFFFFu, mn);
-      if (threadIdx.x == 0) {
-        sh_min = 0xFFFFFFFFu;
-        sh_or = 0;
+      nmx = __reduce_min_sync(0xFFFFFFFFu, nmx);
+      lo = __reduce_or_sync(0xFFFFFFFFu, lo);
+      const uint32_t pre = block_excl_scan<uint32_t, FT>(cnt, &sh_tmp);  // (its barriers order sh_mm's init)
+      if (lane == 0 && (int)threadIdx.x < (int)G) {
+        atomicMin(&sh_mm[0], mn);
+        atomicMin(&sh_mm[1], nmx);
+        atomicOr(&sh_mm[2], lo);
+      }
+      if ((int)threadIdx.x < (int)G) {
+        col_pre[threadIdx.x] = pre;
+        col_src[threadIdx.x] = src - pre;  // staging index of segment element e: col_src[o] + e
       }
       __syncthreads();
-      if (lane == 0) atomicMin(&sh_min, mn);
-      __syncthreads();
-      mn = sh_min;
-      uint32_t o = 0;
-      for (uint32_t j = threadIdx.x; j < t; j += FT) o |= ka[j] - mn;
-      o = __reduce_or_sync(0xFFFFFFFFu, o);
-      if (lane == 0 && o) atomicOr(&sh_or, o);
-      __syncthreads();
-      const uint32_t g = sh_or ? (uint32_t)(__ffs(sh_or) - 1) : 0u;
-      for (uint32_t j = threadIdx.x; j < t; j += FT) ka[j] = (ka[j] - mn) >> g;  // order-preserving code
-      __syncthreads();
-      cta_sort_pairs(ka, ia, kb, ib, t, s.h);  // counters in s.h[0, 4096)
-      uint32_t *out = (list == 0 ? d.pf_ids : d.ev_ids) + start;
-      for (uint32_t j = threadIdx.x; j < t; j += FT) out[j] = ia[j];
-      __syncthreads();
     }
-    if (threadIdx.x == 0) atomicMax(&prof[21], gtimer() - t_r0);
+    const uint32_t smin = sh_mm[0], smax = ~sh_mm[1];
+    uint32_t mode, g = 0;
+    if (smin == smax) mode = M_SINGLE;
+    else {
+      g = __ffs(sh_mm[2]) - 1;  // every key - min is a multiple of 2^g (same bits [31:21])
+      mode = ((smax - smin) >> g) < RMAX ? M_COUNT : (4 * len <= 3 * A.tile ? M_SORT1 : M_BIG);
+    }
+    const uint32_t org = list == 0 ? smin : smax;  // code origin
+    if (mode >= M_SORT1 && si > 0) {  // the segment's first slot sorts all of it
+      __syncthreads();
+      continue;
+    }
+    // staging index of segment element e: the last CTA o whose first position is <= e
+    auto src_of = [&](uint32_t e) -> uint32_t {
+      uint32_t lo = 0, hi = G;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (col_pre[mid] <= e) lo = mid;
+        else hi = mid;
+      }
+      return col_src[lo] + e;
+    };
+    const uint32_t *sk = list == 0 ? d.sort_ka : d.f_sk2, *sv = list == 0 ? d.sort_va : d.f_sv2;
+    uint32_t *out = (list == 0 ? d.pf_ids : d.ev_ids) + seg_start[gp];
+    auto lap = [&](int i) {
+      const unsigned long long t = gtimer();
+      dt[i] += t - tq;
+      tq = t;
+    };
+    lap(0);
+    const uint32_t e0 = si * CH, e1 = min(len, e0 + CH);
+    if (mode == M_SINGLE) {
+      for (uint32_t e = e0 + threadIdx.x; e < e1; e += FT) out[e] = sv[src_of(e)];
+    } else if (mode == M_COUNT) {
+      uint32_t *h_all = s.h, *h_bef = s.h + 2 * NBL, *sc = s.h + 4 * NBL, *sid = s.h + 5 * NBL;
+      const uint32_t R = RMAX;
+      for (uint32_t x = threadIdx.x; x < R; x += FT) {
+        h_all[x] = 0;
+        h_bef[x] = 0;
+      }
+      __syncthreads();
+      for (uint32_t e00 = 0; e00 < len; e00 += 4 * FT) {
+        uint32_t key[4], id[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // loads first
+          const uint32_t e = e00 + q * FT + threadIdx.x;
+          if (e < len) {
+            const uint32_t sidx = src_of(e);
+            key[q] = sk[sidx];
+            id[q] = (e >= e0 && e < e1) ? sv[sidx] : 0u;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t e = e00 + q * FT + threadIdx.x;
+          if (e < len) {
+            const uint32_t code = (list == 0 ? key[q] - org : org - key[q]) >> g;
+            atomicAdd(&h_all[code], 1u);
+            if (e < e0) atomicAdd(&h_bef[code], 1u);
+            else if (e < e1) {
+              sc[e - e0] = code;
+              sid[e - e0] = id[q];
+            }
+          }
+        }
+      }
+      __syncthreads();
+      lap(1);
+      {  // exclusive scan of the code counts (2 bins per thread)
+        const uint32_t v0 = h_all[2 * threadIdx.x], v1 = h_all[2 * threadIdx.x + 1];
+        const uint32_t ex = block_excl_scan<uint32_t, FT>(v0 + v1, &sh_tmp);
+        h_all[2 * threadIdx.x] = ex;
+        h_all[2 * threadIdx.x + 1] = ex + v0;
+      }
+      __syncthreads();
+      lap(2);
+      if (warp == 0) {  // the slice in order: position = start + earlier members with the same code
+        for (uint32_t x0 = 0; x0 < e1 - e0; x0 += 32) {
+          const uint32_t x = x0 + lane;
+          const bool on = x < e1 - e0;
+          const uint32_t code = on ? sc[x] : 0xFFFFFFFFu;
+          const uint32_t peers = __match_any_sync(0xFFFFFFFFu, code);
+          if (on) out[h_all[code] + h_bef[code] + __popc(peers & lanemask_lt())] = sid[x];
+          __syncwarp();
+          if (on && (peers & lanemask_lt()) == 0) h_bef[code] += __popc(peers);
+          __syncwarp();
+        }
+      }
+    } else {  // M_SORT1 / M_BIG: the whole segment
+      uint32_t *ka, *ia, *kb, *ib;
+      if (mode == M_SORT1) {  // 4 * len <= 3 * tile words of keys / fp / memb
+        ka = s.keys;
+        ia = ka + len;
+        kb = ka + 2 * len;
+        ib = ka + 3 * len;
+      } else {  // disjoint global ranges: prefetch [0, npf), evict [npf, npf + nev)
+        const uint32_t at = (list == 0 ? 0u : npf) + seg_start[gp];
+        ka = d.sort_kb + at;
+        ia = d.sort_vb + at;
+        kb = d.f_sk3 + at;
+        ib = d.f_sv3 + at;
+      }
+      for (uint32_t e = threadIdx.x; e < len; e += FT) {
+        const uint32_t sidx = src_of(e);
+        const uint32_t key = sk[sidx];
+        ka[e] = (list == 0 ? key - org : org - key) >> g;  // order-preserving code
+        ia[e] = sv[sidx];
+      }
+      __syncthreads();
+      cta_sort_pairs(ka, ia, kb, ib, len, s.h);  // counters in s.h[0, 4096)
+      for (uint32_t e = threadIdx.x; e < len; e += FT) out[e] = ia[e];
+      if (threadIdx.x == 0) atomicMax(&prof[18], (unsigned long long)len);
+    }
+    __syncthreads();
+    lap(3);
+  }
+  if (threadIdx.x == 0) {
+    atomicMax(&prof[21], gtimer() - t_s0);
+    atomicMax(&prof[22], dt[0]);
+    atomicMax(&prof[23], dt[1]);
+    atomicMax(&prof[24], dt[2]);
+    atomicMax(&prof[29], dt[3]);
   }
   if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
 }

@@ -53,8 +53,8 @@ struct Layout {
   uint64_t exp_sum, exp_excl;
   uint64_t page_first, page_table, ring, pool, desc[2];
   // fused path (double-buffered by fused-step parity where noted)
-  uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_cpf, f_cta_cev, f_tot, f_acc, f_tie_val, f_tie_flag;
-  uint64_t f_rows1, f_rows2, f_rows3, f_lmm;
+  uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_cpf, f_cta_cev, f_tot, f_acc;
+  uint64_t f_rows1, f_rows2, f_rows3, f_cta_lmm;
   uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes, params_dev;
   uint64_t total;
 };
@@ -88,13 +88,14 @@ struct Dev {
   unsigned long long *f_hist2;  // [2][1024]
   uint32_t *f_mm2;              // [2][2][1024]
   unsigned long long *f_hist3;  // [2][1024]
-  uint32_t *f_cta_cpf, *f_cta_cev;                      // [CTAS][1024] list members per bucket
+  uint32_t *f_cta_cpf, *f_cta_cev;                      // [CTAS][1024] (offset << 16) | count of the CTA's
+                                                        // list members per bucket (staged bucket-major)
   uint32_t *f_tot;                                      // [2][2][1024] list bucket totals
   unsigned long long *f_acc;                            // [2][8]
-  unsigned long long *f_tie_val;                        // [CTAS] tie bytes per CTA
   unsigned long long *f_rows1, *f_rows2, *f_rows3;      // [CTAS][4096] / [CTAS][1024] per-CTA histogram rows
-  uint32_t *f_lmm;                                      // [2][4][1024] list members: min / ~max key per bucket
-  unsigned int *f_tie_flag;                             // [CTAS] launch epoch of f_tie_val
+  uint32_t *f_cta_lmm;                                  // [CTAS][2 lists][3][1024] the CTA's list members per
+                                                        // bucket: min key, ~max key, OR of key bits [20:0]
+                                                        // (valid where the row count is nonzero)
   uint32_t *wb_bytes;                                   // [n_local] KV+HIST bytes per agent (R13)
   uint8_t *params_dev;                                  // device copy of the context's Params (fused path)
   uint32_t *f_sk2, *f_sv2, *f_sk3, *f_sv3;              // [n_local] evict-segment sort scratch
@@ -120,6 +121,7 @@ struct Params {
   uint8_t *host_arena, *dev_arena;
   // state
   int keep_dist;  // fused path: also write the distances to the workspace (dist view)
+  int int_mode;   // every distance is an integer or +inf (no interaction class, integral hop_scale)
   int cur;  // index of the residency bitmap holding the residency before this plan
   int desc_buf;
   Dev d;
@@ -146,6 +148,7 @@ struct FusedInst {
   const uint4 *rec;
   const float4 *kin;
   int64_t now;
+  uint64_t n_local;  // agents of the instance (the kernel prefetches its records before reading params)
   uint32_t cur, parity, epoch, tile;
 };
 constexpr int FUSED_MAX_BATCH = 160;

@@ -210,3 +210,23 @@ def test_c5_batch_replicas_vs_oracle():
             it["res"] = p["resident"]
     for it in inst:
         it["pl"].close()
+
+
+def test_fused_wide_code_segments():
+    """Large integer distances (2^17..2^24 ticks: one list bucket spans up to 2^19 distinct
+    values) so the list segments need the full radix sort: whole-list changes give long
+    segments sorted in global memory, a 3% change gives short ones sorted in shared memory."""
+    from gpu_harness import run_parity
+    n = 50000
+    rng = np.random.default_rng(17)
+    fp = rng.choice([1, 2, 3], n) * tg.PAGE_BYTES
+    d0 = rng.integers(1 << 17, 1 << 24, n)
+    d1 = d0.copy()
+    ch = rng.choice(n, n * 3 // 100, replace=False)
+    d1[ch] = rng.integers(1 << 17, 1 << 24, len(ch))
+    recs = [rec_of([dict(d=int(x), fp=int(fp[i])) for i, x in enumerate(dd)]) for dd in (d0, d1, d0)]
+    blocks = tg.make_blocks([[tg.KIND_KV]] * n, [[int(f)] for f in fp])
+    w = tg.Workload("wide", n, np.zeros(3, np.int64), np.stack(recs), None, blocks, int(fp.sum() * 0.3),
+                    np.full(3, np.inf, np.float32))
+    run_parity(w, transfer=False)
+    run_parity(w, transfer=False, multi_kernel=True)
