@@ -564,6 +564,7 @@ static FusedInst fused_inst(const scalesim_ctx *c, uint32_t tile) {
   f.kin = c->p.kin;
   f.now = c->deferred_now;
   f.n_local = c->p.n_local;
+  f.bm_old = c->p.d.bm[c->p.cur];
   f.cur = (uint32_t)c->p.cur;
   f.parity = (uint32_t)(c->fused_steps & 1);
   f.epoch = (uint32_t)(c->fused_steps + 1);

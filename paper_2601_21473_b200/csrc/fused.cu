@@ -328,6 +328,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     if (b0 < I.n_local) {
       const uint64_t nb = 16 * (I.n_local - b0 < I.tile ? I.n_local - b0 : I.tile);
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(I.rec + b0), "r"((uint32_t)nb) : "memory");
+      const uint64_t wb0 = b0 / 32, nw = (nb / 16 + 31) / 32;  // residency words of the tile
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(I.bm_old + wb0 - (wb0 & 3)),
+                   "r"((uint32_t)(((nw + (wb0 & 3)) * 4 + 15) / 16 * 16)) : "memory");
     }
   }
   __shared__ __align__(16) Params sp;  // the instance's parameters (device copy + per-launch fields)

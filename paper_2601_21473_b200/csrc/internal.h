@@ -149,6 +149,7 @@ struct FusedInst {
   const float4 *kin;
   int64_t now;
   uint64_t n_local;  // agents of the instance (the kernel prefetches its records before reading params)
+  const uint32_t *bm_old;  // residency bitmap before this plan (prefetched likewise)
   uint32_t cur, parity, epoch, tile;
 };
 constexpr int FUSED_MAX_BATCH = 160;
