@@ -72,6 +72,12 @@ typedef enum {
 #define SCALESIM_F_MULTI_KERNEL 4u  /* force the multi-kernel plan path (otherwise, at world == 1 and
                                        <= 16384 agents per SM, one persistent cooperative kernel
                                        scores and plans the step; both paths give identical plans) */
+#define SCALESIM_F_EXPLICIT_DIST 8u /* records carry their distance (reading R19): word [0] = f32 bits
+                                       of d >= 0 or +inf (NaN / negative: ST_BAD_RECORD, d = +inf;
+                                       -0 -> +0); phase, class and kinematics are not used, every
+                                       record is eligible below theta[0].  Plans shared memory
+                                       objects from scalesim_object_min.  Requires
+                                       n_kin == 0. */
 
 /* Agent record: 4 x uint32 per agent, 16-byte aligned, one 128-bit load.
  *   [0] t_next : action-end tick (ACTING independent / interaction agents), or remaining hop
@@ -231,6 +237,29 @@ int scalesim_fused(const scalesim_ctx *ctx);
  * seen by CTA 0.  The caller resets [0] to UINT64_MAX and [1] to 0 between launches it wants
  * to time.  Profiling aid; NULL for a NULL context. */
 const uint64_t *scalesim_profile_stamps(const scalesim_ctx *ctx);
+
+/* Fine-grained distance assignment for shared memory objects ("the invocation
+ * distance of a memory object as the minimum invocation distance among all agents that
+ * currently reference it"; S:263-271 recompute_object_distances; reading R19):
+ *   dist(o) = min { agent_dist[a] : a in ref_agent[ref_ptr[o] .. ref_ptr[o+1]) },  +inf if empty.
+ * Writes one record per object for a context created with SCALESIM_F_EXPLICIT_DIST
+ * (word [0] = f32 bits of dist(o), [1] = obj_bytes[o], [2] = obj_flags[o] (0 if NULL), [3] = 0),
+ * so the objects are ranked, cut and transferred by the same planner.
+ *   agent_dist   device f32 [n_agents], >= 0 or +inf (e.g. the dist view of an agent context
+ *                created with SCALESIM_F_KEEP_DIST, after its plan)
+ *   ref_ptr      device u64 [n_objects + 1], non-decreasing CSR offsets into ref_agent
+ *   ref_agent    device u32 [ref_ptr[n_objects]], agent indices; an index >= n_agents is skipped
+ *                and sets SCALESIM_ST_BAD_RECORD in *status_out
+ *   obj_bytes    device u32 [n_objects]; obj_flags device u32 [n_objects] or NULL
+ *   obj_rec_out  device, 16-byte aligned, 4 x u32 per object; obj_dist_out device f32 [n_objects]
+ *                or NULL; status_out device u32 (ORed) or NULL
+ *   stream       cudaStream_t (NULL: legacy default stream)
+ * Asynchronous (stream-ordered, graph-capturable).  Returns SCALESIM_E_INVALID for NULL or
+ * misaligned required pointers, SCALESIM_E_CUDA on a launch error.  n_objects == 0 is a no-op. */
+scalesim_status scalesim_object_min(const float *agent_dist, uint64_t n_agents, const uint64_t *ref_ptr,
+                                    const uint32_t *ref_agent, uint64_t n_objects, const uint32_t *obj_bytes,
+                                    const uint32_t *obj_flags, void *obj_rec_out, float *obj_dist_out,
+                                    uint32_t *status_out, void *stream);
 
 /* Launches of library kernels enqueued so far (for the bench's gpu_launches). */
 uint64_t scalesim_launch_count(const scalesim_ctx *ctx);

@@ -320,3 +320,46 @@ extern "C" void oracle_mem_pool(const oracle_mem *m, uint64_t *head, uint64_t *t
   *tail = m->tail;
   if (ring) std::copy(m->ring.begin(), m->ring.end(), ring);
 }
+
+// ---------------------------------------------------------------------------------------
+// Shared memory objects: P:459-463 (fine-grained distance assignment), R19.
+
+void oracle_object_min(uint64_t n_agents, const float *agent_dist, uint64_t n_obj, const uint64_t *ref_ptr,
+                       const uint32_t *ref_agent, float *d_obj, uint32_t *status) {
+  uint32_t st = 0;
+  for (uint64_t o = 0; o < n_obj; ++o) {
+    // "the minimum invocation distance among all agents that currently reference it"
+    float m = std::numeric_limits<float>::infinity();  // no referrer: +inf
+    for (uint64_t k = ref_ptr[o]; k < ref_ptr[o + 1]; ++k) {
+      const uint32_t a = ref_agent[k];
+      if (a >= n_agents) {
+        st |= ORACLE_ST_BAD_RECORD;
+        continue;
+      }
+      float x = agent_dist[a];
+      if (std::isnan(x) || x < 0.0f) {
+        st |= ORACLE_ST_BAD_RECORD;
+        x = std::numeric_limits<float>::infinity();
+      }
+      if (x < m) m = x;
+    }
+    if (m == 0.0f) m = 0.0f;  // -0 -> +0
+    d_obj[o] = m;
+  }
+  *status |= st;
+}
+
+void oracle_explicit_dist(uint64_t n, const uint32_t *rec, float *d_out, uint32_t *status) {
+  uint32_t st = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    float x;
+    std::memcpy(&x, &rec[4 * i], sizeof(float));
+    if (std::isnan(x) || x < 0.0f) {
+      st |= ORACLE_ST_BAD_RECORD;
+      x = std::numeric_limits<float>::infinity();
+    }
+    if (x == 0.0f) x = 0.0f;
+    d_out[i] = x;
+  }
+  *status |= st;
+}

@@ -42,6 +42,19 @@ extern "C" {
 void oracle_score(uint64_t n, const uint32_t *rec, const float *kin, uint64_t n_kin,
                   int64_t now, float hop_scale, float *d_out, uint32_t *status);
 
+/* Fine-grained distance assignment for shared memory objects ("the invocation
+ * distance of a memory object as the minimum invocation distance among all agents that
+ * currently reference it"; reading R19):
+ *   d_obj[o] = min { agent_dist[a] : a in ref_agent[ref_ptr[o] .. ref_ptr[o+1]) },  +inf if none.
+ * An agent index >= n_agents is skipped and a NaN / negative agent distance is read as +inf
+ * (*status |= ORACLE_ST_BAD_RECORD for either); -0 reads as +0. */
+void oracle_object_min(uint64_t n_agents, const float *agent_dist, uint64_t n_obj, const uint64_t *ref_ptr,
+                       const uint32_t *ref_agent, float *d_obj, uint32_t *status);
+
+/* Explicit distances (reading R19): d_out[i] = the float whose bits are rec word 0 of record i;
+ * NaN or negative -> +inf and ORACLE_ST_BAD_RECORD; -0 -> +0. */
+void oracle_explicit_dist(uint64_t n, const uint32_t *rec, float *d_out, uint32_t *status);
+
 /* Interaction component only (Eq. 2): dint[k] = min over other ACTING INT agents j of
  * (r.r)/(-r.w) for approaching pairs, +inf otherwise; indexed by kin index.  Exposed so
  * the tests can pin Eq. 2 separately.  Entries of kin not owned by an ACTING INT agent

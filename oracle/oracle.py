@@ -49,6 +49,10 @@ def lib():
             L.oracle_score.restype = None
             L.oracle_interaction.argtypes = [u64, u32p, f32p, u64, f32p, u32p]
             L.oracle_interaction.restype = None
+            L.oracle_object_min.argtypes = [u64, f32p, u64, u64p, u32p, f32p, u32p]
+            L.oracle_object_min.restype = None
+            L.oracle_explicit_dist.argtypes = [u64, u32p, f32p, u32p]
+            L.oracle_explicit_dist.restype = None
             L.oracle_plan.argtypes = [u64, u32p, f32p, u8p, f32p, u64, u8p, u32p, u64p, u32p, u64p,
                                       u64p, u32p]
             L.oracle_plan.restype = None
@@ -109,6 +113,31 @@ def interaction(rec, kin):
     lib().oracle_interaction(rec.shape[0], _p(rec, C.c_uint32), _p(kin, C.c_float), n_kin,
                              _p(dint, C.c_float), _p(st, C.c_uint32))
     return dint[:n_kin], int(st[0])
+
+
+def object_min(agent_dist, ref_ptr, ref_agent):
+    """Shared-object distances: float32 [n_objects] and the status bits."""
+    ad = np.ascontiguousarray(agent_dist, dtype=np.float32)
+    rp = np.ascontiguousarray(ref_ptr, dtype=np.uint64)
+    ra = np.ascontiguousarray(ref_agent, dtype=np.uint32)
+    n_obj = rp.shape[0] - 1
+    out = np.empty(max(n_obj, 1), dtype=np.float32)
+    st = np.zeros(1, dtype=np.uint32)
+    lib().oracle_object_min(ad.shape[0], _p(ad if ad.size else np.zeros(1, np.float32), C.c_float), n_obj,
+                            _p(rp, C.c_uint64), _p(ra if ra.size else np.zeros(1, np.uint32), C.c_uint32),
+                            _p(out, C.c_float), _p(st, C.c_uint32))
+    return out[:n_obj], int(st[0])
+
+
+def explicit_dist(rec):
+    """Explicit distances of records (reading R19) and the status bits."""
+    rec = _rec(rec)
+    n = rec.shape[0]
+    d = np.empty(max(n, 1), dtype=np.float32)
+    st = np.zeros(1, dtype=np.uint32)
+    lib().oracle_explicit_dist(n, _p(rec if n else np.zeros((1, 4), np.uint32), C.c_uint32), _p(d, C.c_float),
+                               _p(st, C.c_uint32))
+    return d[:n], int(st[0])
 
 
 def plan(rec, d, resident, theta, budget: int):

@@ -264,6 +264,10 @@ static scalesim_status validate_config(const scalesim_config *c) {
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return SCALESIM_E_INVALID;
   if (c->world == 1 && (c->shard_begin != 0 || c->shard_end != c->n_agents)) return SCALESIM_E_INVALID;
   if (c->world > 1 && c->n_kin > 0) return SCALESIM_E_INVALID;  // interaction agents: single rank
+  if ((c->flags & SCALESIM_F_EXPLICIT_DIST) && c->n_kin > 0) return SCALESIM_E_INVALID;
+  if (c->flags & ~(uint32_t)(SCALESIM_F_NO_TRANSFER | SCALESIM_F_KEEP_DIST | SCALESIM_F_MULTI_KERNEL |
+                             SCALESIM_F_EXPLICIT_DIST))
+    return SCALESIM_E_INVALID;
   for (int k = 0; k < 3; ++k)
     if (std::isnan(c->theta[k]) || c->theta[k] < 0.0f) return SCALESIM_E_INVALID;
   if (!(c->hop_scale > 0.0f) || std::isinf(c->hop_scale)) return SCALESIM_E_INVALID;
@@ -373,7 +377,8 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
   p.desc_cap = L.desc_cap;
   for (int k = 0; k < 3; ++k) p.theta[k] = cfg->theta[k];
   p.hop_scale = cfg->hop_scale;
-  p.int_mode = (cfg->n_kin == 0 && cfg->hop_scale == std::floor(cfg->hop_scale)) ? 1 : 0;
+  p.explicit_dist = (cfg->flags & SCALESIM_F_EXPLICIT_DIST) ? 1 : 0;
+  p.int_mode = (!p.explicit_dist && cfg->n_kin == 0 && cfg->hop_scale == std::floor(cfg->hop_scale)) ? 1 : 0;
   p.rank = cfg->rank;
   p.world = cfg->world;
   p.rec = reinterpret_cast<const uint4 *>(t->agent_rec);

@@ -197,6 +197,18 @@ __device__ __forceinline__ float distance_of(uint4 r, int64_t now, float hop_sca
   return d;
 }
 
+// Explicit distance (SCALESIM_F_EXPLICIT_DIST, reading R19): word 0 holds the f32 bits;
+// NaN or negative -> BAD_RECORD and +inf; -0 -> +0.
+__device__ __forceinline__ float explicit_distance_of(uint4 r, uint32_t &st) {
+  float d = __uint_as_float(r.x);
+  if (!(d >= 0.0f)) {  // NaN or < 0 (-0 compares equal to 0 and passes)
+    st |= ST_BAD_RECORD;
+    d = __int_as_float(0x7F800000);
+  }
+  if (d == 0.0f) d = 0.0f;
+  return d;
+}
+
 __device__ __forceinline__ float theta_of(const Params &p, uint32_t cl) {
   return cl == 0u ? p.theta[0] : cl == 1u ? p.theta[1] : cl == 2u ? p.theta[2] : 0.0f;
 }

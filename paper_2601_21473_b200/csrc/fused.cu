@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   const uint4 *rec = p.rec + base;
   uint32_t *gkeys = p.keep_dist ? d.keys + base : nullptr;
   const int64_t now = A.now;
-  const bool imode = p.int_mode != 0;
+  const bool imode = p.int_mode != 0, xdist = p.explicit_dist != 0;
   // remaining ticks in 32-bit arithmetic when now fits (t_next is 32-bit): exact for < 2^24,
   // rounded to nearest as __ll2float_rn above
   const bool now32 = now >= 0 && now <= 0xFFFFFFFFll;
@@ -404,7 +404,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       const bool res = (s.old_w[k >> 5] >> (k & 31)) & 1u;
       const uint32_t ph = r[j].z & 3u, cl = (r[j].z >> 2) & 3u;
       float dist, th;
-      if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {
+      if (xdist) {  // explicit distances (R19)
+        dist = valid ? explicit_distance_of(r[j], st) : 0.0f;
+        th = th0;
+      } else if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {
         // the warp holds interaction / diffusion / malformed records: general definition
         dist = valid ? distance_of(r[j], now, hop_scale, dint, n_kin, st) : 0.0f;
         th = (cl & 2u) ? ((cl & 1u) ? 0.0f : th2) : ((cl & 1u) ? th1 : th0);

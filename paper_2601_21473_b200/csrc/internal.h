@@ -122,6 +122,7 @@ struct Params {
   // state
   int keep_dist;  // fused path: also write the distances to the workspace (dist view)
   int int_mode;   // every distance is an integer or +inf (no interaction class, integral hop_scale)
+  int explicit_dist;  // SCALESIM_F_EXPLICIT_DIST: record word 0 holds the distance bits (R19)
   int cur;  // index of the residency bitmap holding the residency before this plan
   int desc_buf;
   Dev d;

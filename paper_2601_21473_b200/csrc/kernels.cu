@@ -150,9 +150,11 @@ __global__ void __launch_bounds__(NT) k_score(Params p, int64_t now) {
       word = bm_old[i >> 5];
     }
     const bool res = valid && ((word >> (i & 31)) & 1u);
-    const float d = valid ? distance_of(r, now, p.hop_scale, p.d.dint, p.n_kin, st) : 0.0f;
+    const float d = !valid ? 0.0f
+                    : (p.explicit_dist ? explicit_distance_of(r, st)
+                                       : distance_of(r, now, p.hop_scale, p.d.dint, p.n_kin, st));
     const uint32_t bits = __float_as_uint(d);
-    const bool elig = valid && (res || d == 0.0f || d < theta_of(p, class_of(r)));
+    const bool elig = valid && (res || d == 0.0f || d < (p.explicit_dist ? p.theta[0] : theta_of(p, class_of(r))));
     if (valid) p.d.keys[i] = bits;
     const uint32_t eb = __ballot_sync(FULL, elig);
     if (lane == 0 && (i >> 5) < p.n_words) p.d.elig[i >> 5] = eb;

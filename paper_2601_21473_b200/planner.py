@@ -36,7 +36,7 @@ class Planner:
                  dev_bytes: Optional[int] = None, resident_init=None, device: int = 0,
                  shard: Optional[tuple] = None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None,
-                 multi_kernel: bool = False, keep_dist: bool = True):
+                 multi_kernel: bool = False, keep_dist: bool = True, explicit_dist: bool = False):
         self.lib = L.lib()
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
@@ -87,7 +87,7 @@ class Planner:
         cfg = L.Config()
         cfg.abi_version = L.ABI_VERSION
         cfg.flags = (0 if transfer else L.F_NO_TRANSFER) | (L.F_MULTI_KERNEL if multi_kernel else 0) | \
-            (L.F_KEEP_DIST if keep_dist else 0)
+            (L.F_KEEP_DIST if keep_dist else 0) | (L.F_EXPLICIT_DIST if explicit_dist else 0)
         cfg.n_agents = self.n_agents
         cfg.shard_begin = self.lo
         cfg.shard_end = self.hi
@@ -226,6 +226,11 @@ class Planner:
     def distances(self) -> np.ndarray:
         return self._read(self.view.dist, 4 * self.n_local).view(np.float32)
 
+    def dist_tensor(self) -> torch.Tensor:
+        """Device view (float32, n_local) of the distances of the last plan (keep_dist)."""
+        off = int(self.view.dist) - self.workspace.data_ptr()
+        return self.workspace[off: off + 4 * self.n_local].view(torch.float32)
+
     def page_table(self) -> np.ndarray:
         return self._read(self.view.page_table, 4 * self.n_block_pages).view(np.uint32)
 
@@ -247,6 +252,20 @@ class Planner:
             pass
 
 
+
+def object_min(agent_dist: torch.Tensor, ref_ptr: torch.Tensor, ref_agent: torch.Tensor, obj_bytes: torch.Tensor,
+               rec_out: torch.Tensor, obj_flags: Optional[torch.Tensor] = None, dist_out: Optional[torch.Tensor] = None,
+               status: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None):
+    """scalesim_object_min: shared-object distances (min over referencing agents)
+    written as explicit-distance records into rec_out (uint8 device tensor, 16 B per object).
+    All tensors on the same CUDA device; ref_ptr int64/uint64 [n_objects + 1], ref_agent,
+    obj_bytes, obj_flags 32-bit."""
+    lib = L.lib()
+    n_obj = ref_ptr.numel() - 1
+    st = stream if stream is not None else torch.cuda.current_stream(agent_dist.device)
+    L.check(lib.scalesim_object_min(_ptr(agent_dist), agent_dist.numel(), _ptr(ref_ptr), _ptr(ref_agent), n_obj,
+                                    _ptr(obj_bytes), _ptr(obj_flags), _ptr(rec_out), _ptr(dist_out), _ptr(status),
+                                    st.cuda_stream), "scalesim_object_min")
 
 
 def step_batch(planners, now: int):

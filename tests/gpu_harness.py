@@ -28,7 +28,7 @@ def fill_pattern(host, chunk=1 << 28):
 
 
 def make_planner(w: tg.Workload, transfer: bool, resident_init=None, host_pattern=True, dev_pages=None,
-                 multi_kernel=False):
+                 multi_kernel=False, explicit=False):
     from paper_2601_21473_b200.planner import Planner
     b = w.blocks
     host = None
@@ -41,14 +41,14 @@ def make_planner(w: tg.Workload, transfer: bool, resident_init=None, host_patter
     return Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
                    hop_scale=w.hop_scale, n_kin=w.n_kin, page_bytes=w.page_bytes, transfer=transfer,
                    host_arena=host, dev_bytes=max(pages, 1) * w.page_bytes, resident_init=resident_init,
-                   multi_kernel=multi_kernel)
+                   multi_kernel=multi_kernel, explicit_dist=explicit)
 
 
 def run_parity(w: tg.Workload, steps=None, transfer=True, resident_init=None, content_pages=64,
-               check_dist=True, stamp_writes=True, seed=0, multi_kernel=False, expect_fused=None):
+               check_dist=True, stamp_writes=True, seed=0, multi_kernel=False, expect_fused=None, explicit=False):
     """Step the GPU planner and the oracle through the workload; assert parity every step.
     Returns per-step summaries."""
-    pl = make_planner(w, transfer, resident_init, multi_kernel=multi_kernel)
+    pl = make_planner(w, transfer, resident_init, multi_kernel=multi_kernel, explicit=explicit)
     if expect_fused is None:
         expect_fused = not multi_kernel
     assert pl.fused == expect_fused
@@ -86,7 +86,10 @@ def run_parity(w: tg.Workload, steps=None, transfer=True, resident_init=None, co
         pl.step(int(w.now[s]))
         hdr = pl.sync()
         # --- score parity
-        d_or, st_or = oracle.score(rec, kin, int(w.now[s]), w.hop_scale)
+        if explicit:  # records carry their distances (R19)
+            d_or, st_or = oracle.explicit_dist(rec)
+        else:
+            d_or, st_or = oracle.score(rec, kin, int(w.now[s]), w.hop_scale)
         if check_dist:
             d_gpu = pl.distances()
             bad = np.nonzero(d_gpu.view(np.uint32) != d_or.view(np.uint32))[0]

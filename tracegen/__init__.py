@@ -12,3 +12,4 @@ from .traces import (  # noqa: F401
     gen_independent, gen_interaction, gen_diffusion,
     config_c1, config_c2, config_c3, config_c4, config_c5, config_by_name, host_pattern,
 )
+from .objects import Objects, gen_objects, object_records  # noqa: F401,E402
