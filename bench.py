@@ -272,6 +272,81 @@ def c5_leg(torch, dev, rank, world, replicas=64, budgets=tuple(range(10, 100, 10
             "launches": launches}
 
 
+def objects_leg(torch, dev, n=1_000_000, steps=8, warm=8, seed=5):
+    """NEXT #1: 1M C4 agents + shared memory objects (a system prompt shared by
+    all, n/100 persona adapters, private KV pages): per step the agent plan (distances kept),
+    scalesim_object_min, and the object plan (explicit distances), all on one stream."""
+    from paper_2601_21473_b200.planner import Planner, object_min
+    T = warm + steps
+    w = tg.config_c4(seed=seed, steps=T, n=n)
+    ob = tg.gen_objects(n, seed=seed)
+    recs = torch.from_numpy(np.ascontiguousarray(w.rec).view(np.uint8).reshape(T, -1)).to(dev)
+    flags = torch.from_numpy(np.stack([ob.flags(w.rec[s]) for s in range(T)])).to(dev)
+    stream = torch.cuda.Stream(dev)
+    b = w.blocks
+    agents = Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta, transfer=False,
+                     device=dev.index, stream=stream, keep_dist=True)
+    bo = ob.blocks
+    ob_budget = int(ob.obj_bytes.astype(np.int64).sum()) // 4
+    objs = Planner(ob.n, bo.blk_ptr, bo.blk_size, bo.blk_host_off, bo.blk_kind, ob_budget, w.theta, transfer=False,
+                   device=dev.index, stream=stream, keep_dist=False, explicit_dist=True)
+    ptr_t = torch.from_numpy(ob.ref_ptr).to(dev)
+    ag_t = torch.from_numpy(ob.ref_agent).to(dev)
+    by_t = torch.from_numpy(ob.obj_bytes).to(dev)
+    ev = []
+    dist_t = []
+
+    def one(s, timed):
+        agents.set_inputs_ptr(recs[s].data_ptr())
+        agents.step(int(w.now[s]))
+        if not dist_t:
+            dist_t.append(agents.dist_tensor())  # the view exists after the first plan
+        if timed:
+            e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                 torch.cuda.Event(enable_timing=True))
+            e[0].record(stream)
+        object_min(dist_t[0], ptr_t, ag_t, by_t, objs.rec, obj_flags=flags[s], stream=stream)
+        if timed:
+            e[1].record(stream)
+        objs.step(int(w.now[s]))
+        if timed:
+            e[2].record(stream)
+            ev.append(e)
+
+    for s in range(warm):
+        one(s, False)
+    torch.cuda.synchronize(dev)
+    lc0 = agents.launch_count() + objs.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(2e8))
+    t0.record(stream)
+    for s in range(warm, T):
+        one(s, True)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    om = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    op = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    hdr = objs.sync()
+    launches = agents.launch_count() + objs.launch_count() - lc0 + steps  # + one object_min launch per step
+    refs = int(ob.ref_ptr[-1])
+    # object_min algorithmic bytes: CSR offsets 8 B + size 4 B + flags 4 B + record 16 B per object,
+    # 4 B agent index + 4 B agent distance per reference
+    om_bytes = 32 * ob.n + 8 * refs
+    agents.close()
+    objs.close()
+    return {"value": ob.n * steps / (ms / 1e3), "unit": "object-plans/s",
+            "workload": f"NEXT#1 shared objects: {n} C4 agents, {ob.n} objects (1 prompt prefix shared by all, "
+                        f"{ob.n - 1 - n} persona adapters, {n} private KV-page objects), {refs} references",
+            "ms_per_step": ms / steps, "includes": "agent plan + scalesim_object_min + object plan per step",
+            "object_min_ms": om, "object_plan_ms": op,
+            "object_min_GBs": om_bytes / (om / 1e3) / 1e9, "object_min_bytes": om_bytes,
+            "last_object_plan": {"n_prefetch": hdr["n_prefetch"], "n_evict": hdr["n_evict"],
+                                 "status": hdr["status"]},
+            "gpu_launches": launches, "steps": steps}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -286,6 +361,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=32)
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 replicas x budgets leg")
     ap.add_argument("--c5-replicas", type=int, default=64)
+    ap.add_argument("--no-objects", action="store_true", help="skip the shared-object leg (NEXT #1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -459,6 +535,9 @@ def main():
                           f"instances sharded over {world} GPU(s), scalesim_step_batch",
               "instances_per_gpu": r5["instances"], "steps": r5["steps"], "ms_per_step": r5["ms"] / r5["steps"],
               "gpu_launches": r5["launches"]}
+    objects = None
+    if not args.no_objects and rank == 0:
+        objects = objects_leg(torch, dev)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -503,6 +582,8 @@ def main():
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": sampler.result()}
     if c5 is not None:
         line["c5"] = c5
+    if objects is not None:
+        line["objects"] = objects
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     if not args.no_transfer_leg:
