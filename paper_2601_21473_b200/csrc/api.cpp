@@ -47,6 +47,13 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.dint = take(4 * k1);
   L.ilist_kin = take(16 * k1);
   L.ilist_idx = take(4 * k1);
+  L.ilist_dact = take(4 * k1);
+  L.grid_hdr = take(64);
+  L.cell_cnt = take(4 * (n_kin ? (uint64_t)GRID_MAX_SIDE * GRID_MAX_SIDE : 1));
+  L.cell_start = take(4 * (n_kin ? (uint64_t)GRID_MAX_SIDE * GRID_MAX_SIDE + 1 : 1));
+  L.g_cell = take(4 * k1);
+  L.g_kin = take(16 * k1);
+  L.g_ent = take(4 * k1);
   L.hist1 = take(8 * 4096);
   L.mm1 = take(4 * 4096);
   L.hist2 = take(8 * 1024);
@@ -117,6 +124,13 @@ Dev make_dev(void *ws, const Layout &L) {
   d.dint = (float *)(b + L.dint);
   d.ilist_kin = (float4 *)(b + L.ilist_kin);
   d.ilist_idx = (uint32_t *)(b + L.ilist_idx);
+  d.ilist_dact = (float *)(b + L.ilist_dact);
+  d.grid_hdr = (uint8_t *)(b + L.grid_hdr);
+  d.cell_cnt = (uint32_t *)(b + L.cell_cnt);
+  d.cell_start = (uint32_t *)(b + L.cell_start);
+  d.g_cell = (uint32_t *)(b + L.g_cell);
+  d.g_kin = (float4 *)(b + L.g_kin);
+  d.g_ent = (uint32_t *)(b + L.g_ent);
   d.hist1 = (unsigned long long *)(b + L.hist1);
   d.mm1 = (uint32_t *)(b + L.mm1);
   d.hist2 = (unsigned long long *)(b + L.hist2);
@@ -529,7 +543,7 @@ extern "C" scalesim_status scalesim_score(scalesim_ctx *c, int64_t now, float *d
   if (c->fused && !dist_out) {
     // the fused plan kernel scores the agents itself (phase P1); only the interaction
     // pair scan (which needs every participant before any agent is scored) runs here
-    c->launches += launch_interaction(c->p, c->stream, c->grid);
+    c->launches += launch_interaction(c->p, now, c->stream, c->grid);
     c->deferred = true;
     c->deferred_now = now;
   } else {

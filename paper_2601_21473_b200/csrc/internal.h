@@ -13,6 +13,8 @@ constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;
 constexpr int DESC_HDR = 4;  // descriptor buffer: n_d2h, n_h2d, n_h2d_independent, 0, then pairs
 constexpr uint32_t PAGE_NONE = 0xFFFFFFFFu;
 constexpr int L1_BITS = 11, L2_BITS = 10, L3_BITS = 10;  // distance-bit digits [30:20] [19:10] [9:0]
+constexpr uint32_t GRID_MAX_SIDE = 256;   // a1' spatial grid: at most 256 x 256 cells
+constexpr uint64_t GRID_MIN_PARTICIPANTS = 2048;  // below: tiled all-pairs scan
 constexpr int FUSED_MAX_CTAS = 160;       // fused path: one CTA per SM (B200: 148)
 constexpr uint32_t FUSED_MAX_TILE = 12288;  // fused path: agents per CTA held in shared memory
 
@@ -46,7 +48,7 @@ struct SelState {
 struct Layout {
   uint64_t n_local, n_words, n_kin, n_tiles, n_blocks, n_block_pages, n_dev_pages, desc_cap, world;
   uint64_t max_sort_chunks, max_exp_chunks;
-  uint64_t keys, elig, bm[2], dint, ilist_kin, ilist_idx;
+  uint64_t keys, elig, bm[2], dint, ilist_kin, ilist_idx, ilist_dact, grid_hdr, cell_cnt, cell_start, g_cell, g_kin, g_ent;
   uint64_t hist1, mm1, hist2, mm2, hist3, state, header, gather;
   uint64_t tile_tie, tile_tie_excl, tile_pf, tile_ev, tile_pf_excl, tile_ev_excl, tile_h2d, tile_tiekept, tile_elig;
   uint64_t pf_ids, ev_ids, sort_ka, sort_va, sort_kb, sort_vb, sort_cnt, pfa_key, pfa_val;
@@ -69,6 +71,11 @@ struct Dev {
   float *dint;
   float4 *ilist_kin;
   uint32_t *ilist_idx;
+  float *ilist_dact;                 // D_action of each participant (a1' pruning bound)
+  uint8_t *grid_hdr;                 // a1' grid: bounding box, cell size, shape (interaction.cu)
+  uint32_t *cell_cnt, *cell_start;   // [GRID_MAX_SIDE^2 (+1)]
+  uint32_t *g_cell, *g_ent;          // [n_kin] cell of each participant; participant of each sorted slot
+  float4 *g_kin;                     // [n_kin] kinematics in cell order
   unsigned long long *hist1, *hist2, *hist3;
   uint32_t *mm1, *mm2;  // [0, 2^w) min of bits, [2^w, 2^(w+1)) min of ~bits (= ~max)
   SelState *state;
@@ -131,7 +138,8 @@ struct Params {
 // Launchers (kernels.cu).  Each returns the number of kernels it enqueued.
 int launch_plan_init(const Params &p, cudaStream_t s);
 int launch_score(const Params &p, int64_t now, float *dist_out, cudaStream_t s, int grid);
-int launch_interaction(const Params &p, cudaStream_t s, int grid);
+int launch_interaction(const Params &p, int64_t now, cudaStream_t s, int grid);
+int launch_grid_pairmin(const Params &p, cudaStream_t s, int grid);
 int launch_select(const Params &p, int level, cudaStream_t s);
 int launch_hist(const Params &p, int level, cudaStream_t s, int grid);
 int launch_tie(const Params &p, cudaStream_t s);

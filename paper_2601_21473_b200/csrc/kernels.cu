@@ -44,7 +44,7 @@ __global__ void k_plan_init(Params p) {
 // ------------------------------------------------------------------------------------
 // a1': interaction participants (ACTING INT agents with finite kinematics) and pair-min
 
-__global__ void __launch_bounds__(NT) k_int_compact(Params p) {
+__global__ void __launch_bounds__(NT) k_int_compact(Params p, int64_t now) {
   uint32_t st = 0;
   for (uint64_t k = blockIdx.x * (uint64_t)NT + threadIdx.x; k < p.n_kin; k += (uint64_t)gridDim.x * NT)
     p.d.dint[k] = __int_as_float(0x7F800000);
@@ -53,8 +53,11 @@ __global__ void __launch_bounds__(NT) k_int_compact(Params p) {
     bool part = false;
     float4 kv = make_float4(0, 0, 0, 0);
     uint32_t ki = 0;
+    float dact = 0.0f;
     if (i < p.n_local) {
       const uint4 r = ld_stream(p.rec + i);
+      const int64_t remain = (int64_t)r.x - now;  // D_action, as in distance_of
+      dact = remain <= 0 ? 0.0f : __ll2float_rn(remain);
       if (phase_of(r) == 0u && class_of(r) == 1u) {
         if (r.w >= p.n_kin) {
           st |= ST_BAD_RECORD;
@@ -76,6 +79,7 @@ __global__ void __launch_bounds__(NT) k_int_compact(Params p) {
         const uint32_t slot = base_slot + __popc(m & lanemask_lt());
         p.d.ilist_kin[slot] = kv;
         p.d.ilist_idx[slot] = ki;
+        p.d.ilist_dact[slot] = dact;
       }
     }
   }
@@ -827,16 +831,17 @@ int launch_plan_init(const Params &p, cudaStream_t s) {
   return 1;
 }
 
-int launch_interaction(const Params &p, cudaStream_t s, int grid) {
+int launch_interaction(const Params &p, int64_t now, cudaStream_t s, int grid) {
   if (p.n_kin == 0) return 0;
   const int g = min(grid, max(1, ceil_div(max(p.n_local, p.n_kin), NT)));
-  k_int_compact<<<g, NT, 0, s>>>(p);
+  k_int_compact<<<g, NT, 0, s>>>(p, now);
+  if (p.n_kin >= GRID_MIN_PARTICIPANTS) return 1 + launch_grid_pairmin(p, s, grid);
   k_pairmin<<<max(1, ceil_div(p.n_kin, NT)), NT, 0, s>>>(p);
   return 2;
 }
 
 int launch_score(const Params &p, int64_t now, float *dist_out, cudaStream_t s, int grid) {
-  int n = launch_interaction(p, s, grid);
+  int n = launch_interaction(p, now, s, grid);
   const int g = min(grid / 2, max(1, ceil_div(p.n_local, NT)));  // 2 blocks per SM: fewer histogram flushes
   k_score<<<g, NT, 0, s>>>(p, now);
   ++n;

@@ -230,3 +230,36 @@ def test_fused_wide_code_segments():
                     np.full(3, np.inf, np.float32))
     run_parity(w, transfer=False)
     run_parity(w, transfer=False, multi_kernel=True)
+
+
+@pytest.mark.parametrize("mk", PATHS)
+def test_interaction_grid_pruning_exact(mk):
+    """a1' with the spatial grid (>= 2048 participants): clusters far denser than the grid,
+    agents on cell boundaries and at identical positions, stationary agents, fast agents,
+    D_action from 0 to 10^6 ticks; distances bit-identical to the oracle's all-pairs scan."""
+    from gpu_harness import run_parity
+    rng = np.random.default_rng(21)
+    n = 6000
+    pos = rng.uniform(0, 3000, (n, 2))
+    pos[:1500] = rng.normal(1500, 3.0, (1500, 2))               # one dense cluster
+    pos[1500:1700] = np.round(pos[1500:1700] / 50.0) * 50.0      # grid-aligned coordinates
+    pos[1700:1710] = pos[1700]                                   # identical positions
+    vel = rng.normal(0, 1, (n, 2))
+    vel[2000:2500] = 0.0                                         # stationary
+    vel[2500:2600] *= 40.0                                       # fast
+    kin = np.concatenate([pos, vel], axis=1).astype(np.float32)
+    d_action = rng.integers(0, 60, n)
+    d_action[:100] = 0
+    d_action[100:200] = 10 ** 6
+    steps = []
+    for s in range(2):
+        k = kin.copy()
+        k[:, :2] += s * k[:, 2:]
+        agents = [dict(cls=tg.CL_INT, d=int(d_action[i]), kin=i, fp=tg.PAGE_BYTES) for i in range(n)]
+        for i in rng.choice(n, 300, replace=False):
+            agents[i]["phase"] = tg.PH_GENERATING
+        steps.append((rec_of(agents), k))
+    blocks = tg.make_blocks([[tg.KIND_KV]] * n, [[tg.PAGE_BYTES]] * n)
+    w = tg.Workload("grid", n, np.zeros(2, np.int64), np.stack([r for r, _ in steps]),
+                    np.stack([k for _, k in steps]), blocks, n * tg.PAGE_BYTES // 3, np.full(3, 30.0, np.float32))
+    run_parity(w, transfer=False, multi_kernel=mk)
