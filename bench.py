@@ -227,6 +227,91 @@ def transfer_leg(torch, dev, seed):
                                         "host arena 8 GiB (offsets aliased), SM-driven page copies"}
 
 
+def c3_leg(torch, dev, seed=1, warm=4, steps=8):
+    """C3 (BASELINE configs[2]: 100k agents of all three classes, 80 GB budget, Qwen2.5-0.5B
+    sizes): planning (with the interaction pair scan on the spatial grid) and physical
+    transfers, then the same steps with each step's transfer overlapped with the next step's
+    planning.  overlap efficiency = (t_plan + t_transfer) / t_overlapped."""
+    from paper_2601_21473_b200.planner import Planner
+    T = warm + steps
+    w = tg.config_c3(seed=seed, steps=T, host_bytes=8 << 30)
+    b = w.blocks
+    recs = torch.from_numpy(np.ascontiguousarray(w.rec).view(np.uint8).reshape(T, -1)).to(dev)
+    kins = torch.from_numpy(np.ascontiguousarray(w.kin).view(np.uint8).reshape(T, -1)).to(dev)
+
+    def mk(transfer, host=None):
+        return Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
+                       hop_scale=w.hop_scale, n_kin=w.n_kin, page_bytes=w.page_bytes, transfer=transfer,
+                       host_arena=host, device=dev.index, keep_dist=False)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    # (1) planning alone (score = the a1' pair scan + deferral; plan = the fused kernel)
+    pl = mk(False)
+    t_score, t_plan = [], []
+    for s in range(T):
+        pl.set_inputs_ptr(recs[s].data_ptr(), kins[s].data_ptr())
+        e = [ev() for _ in range(3)]
+        e[0].record(pl.stream)
+        pl.score(int(w.now[s]))
+        e[1].record(pl.stream)
+        pl.plan()
+        e[2].record(pl.stream)
+        torch.cuda.synchronize(dev)
+        if s >= warm:
+            t_score.append(e[0].elapsed_time(e[1]))
+            t_plan.append(e[0].elapsed_time(e[2]))
+    pl.close()
+    host = torch.empty(int(b.host_bytes), dtype=torch.uint8, pin_memory=True)
+    # (2) the same steps, each transfer timed alone (plan, wait, transfer, wait)
+    pl = mk(True, host)
+    t_x, moved = [], []
+    for s in range(T):
+        pl.set_inputs_ptr(recs[s].data_ptr(), kins[s].data_ptr())
+        pl.score(int(w.now[s]))
+        pl.plan()
+        pl.stream.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(pl.copy_stream)
+        pl.transfer()
+        e1.record(pl.copy_stream)
+        hdr = pl.sync()
+        if s >= warm:
+            t_x.append(e0.elapsed_time(e1))
+            moved.append((hdr["n_h2d"] + hdr["n_d2h"]) * w.page_bytes)
+    pl.close()
+    torch.cuda.empty_cache()
+    # (3) the same steps back to back: transfer t runs on the copy stream under plan t+1
+    pl = mk(True, host)
+    for s in range(warm):
+        pl.set_inputs_ptr(recs[s].data_ptr(), kins[s].data_ptr())
+        pl.step(int(w.now[s]))
+    pl.sync()
+    e0, e1 = ev(), ev()
+    with torch.cuda.stream(pl.stream):
+        torch.cuda._sleep(int(1e8))
+    e0.record(pl.stream)
+    for s in range(warm, T):
+        pl.set_inputs_ptr(recs[s].data_ptr(), kins[s].data_ptr())
+        pl.step(int(w.now[s]))
+    pl.join()
+    e1.record(pl.stream)
+    torch.cuda.synchronize(dev)
+    t_over = e0.elapsed_time(e1) / steps
+    pl.close()
+    del host
+    torch.cuda.empty_cache()
+    tp, tx = float(np.mean(t_plan)), float(np.mean(t_x))
+    return {"workload": f"c3: {w.n} agents (independent / interaction / diffusion thirds), 80 GB budget, "
+                        "0.5B LoRA + KV pages + history, host arena 8 GiB (offsets aliased)",
+            "plan_ms": tp, "score_ms": float(np.mean(t_score)), "transfer_ms": tx,
+            "bytes_per_step": float(np.mean(moved)), "transfer_GBs": float(np.mean(moved)) / (tx / 1e3) / 1e9,
+            "step_ms_overlapped": t_over, "overlap_efficiency": (tp + tx) / t_over,
+            "value": w.n / (t_over / 1e3), "unit": "agent-plans/s (planning + transfer, overlapped)",
+            "steps": steps}
+
+
 def c5_leg(torch, dev, rank, world, replicas=64, budgets=tuple(range(10, 100, 10)), steps=8, warm=8, seed_base=100):
     """C5: independent simulation replicas x budget sizes, instances sharded over the ranks
     (instance i on rank i % world), all of a rank's instances stepped by scalesim_step_batch.
@@ -362,6 +447,7 @@ def main():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 replicas x budgets leg")
     ap.add_argument("--c5-replicas", type=int, default=64)
     ap.add_argument("--no-objects", action="store_true", help="skip the shared-object leg (NEXT #1)")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 planning + transfer overlap leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -538,6 +624,9 @@ def main():
     objects = None
     if not args.no_objects and rank == 0:
         objects = objects_leg(torch, dev)
+    c3 = None
+    if not args.no_c3 and rank == 0:
+        c3 = c3_leg(torch, dev)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -584,6 +673,8 @@ def main():
         line["c5"] = c5
     if objects is not None:
         line["objects"] = objects
+    if c3 is not None:
+        line["c3"] = c3
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     if not args.no_transfer_leg:

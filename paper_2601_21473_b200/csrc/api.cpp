@@ -48,7 +48,8 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.ilist_kin = take(16 * k1);
   L.ilist_idx = take(4 * k1);
   L.ilist_dact = take(4 * k1);
-  L.grid_hdr = take(64);
+  L.grid_hdr = take(sizeof(GridHdr));
+  L.heavy = take(4 * k1);
   L.cell_cnt = take(4 * (n_kin ? (uint64_t)GRID_MAX_SIDE * GRID_MAX_SIDE : 1));
   L.cell_start = take(4 * (n_kin ? (uint64_t)GRID_MAX_SIDE * GRID_MAX_SIDE + 1 : 1));
   L.g_cell = take(4 * k1);
@@ -126,6 +127,7 @@ Dev make_dev(void *ws, const Layout &L) {
   d.ilist_idx = (uint32_t *)(b + L.ilist_idx);
   d.ilist_dact = (float *)(b + L.ilist_dact);
   d.grid_hdr = (uint8_t *)(b + L.grid_hdr);
+  d.heavy = (uint32_t *)(b + L.heavy);
   d.cell_cnt = (uint32_t *)(b + L.cell_cnt);
   d.cell_start = (uint32_t *)(b + L.cell_start);
   d.g_cell = (uint32_t *)(b + L.g_cell);
@@ -452,6 +454,12 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
     }
   }
   if (cudaMemsetAsync(t->workspace, 0, L.total, c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
+  GridHdr gh = {};  // a1' grid accumulators start empty (k_grid_setup re-arms them every step)
+  gh.acc_x0 = gh.acc_y0 = 0x7FFFFFFF;
+  gh.acc_x1 = gh.acc_y1 = (int32_t)0x80000000;
+  if (cfg->n_kin > 0 &&
+      cudaMemcpyAsync(p.d.grid_hdr, &gh, sizeof(gh), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    return fail(SCALESIM_E_CUDA);
   if (cudaMemcpyAsync(p.d.page_first, pf.data(), 8 * (t->n_blocks + 1), cudaMemcpyHostToDevice, c->stream) !=
       cudaSuccess)
     return fail(SCALESIM_E_CUDA);

@@ -197,6 +197,13 @@ __device__ __forceinline__ float distance_of(uint4 r, int64_t now, float hop_sca
   return d;
 }
 
+// Order-preserving integer key of a finite float (signed-integer order = float order).
+__device__ __forceinline__ int32_t fkey(float f) {
+  const int32_t i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float fkey_inv(int32_t k) { return __int_as_float(k >= 0 ? k : k ^ 0x7FFFFFFF); }
+
 // Explicit distance (SCALESIM_F_EXPLICIT_DIST, reading R19): word 0 holds the f32 bits;
 // NaN or negative -> BAD_RECORD and +inf; -0 -> +0.
 __device__ __forceinline__ float explicit_distance_of(uint4 r, uint32_t &st) {

@@ -13,7 +13,7 @@ constexpr uint32_t KEY_NONE = 0xFFFFFFFFu;
 constexpr int DESC_HDR = 4;  // descriptor buffer: n_d2h, n_h2d, n_h2d_independent, 0, then pairs
 constexpr uint32_t PAGE_NONE = 0xFFFFFFFFu;
 constexpr int L1_BITS = 11, L2_BITS = 10, L3_BITS = 10;  // distance-bit digits [30:20] [19:10] [9:0]
-constexpr uint32_t GRID_MAX_SIDE = 256;   // a1' spatial grid: at most 256 x 256 cells
+constexpr uint32_t GRID_MAX_SIDE = 128;   // a1' spatial grid: at most 128 x 128 cells
 constexpr uint64_t GRID_MIN_PARTICIPANTS = 2048;  // below: tiled all-pairs scan
 constexpr int FUSED_MAX_CTAS = 160;       // fused path: one CTA per SM (B200: 148)
 constexpr uint32_t FUSED_MAX_TILE = 12288;  // fused path: agents per CTA held in shared memory
@@ -44,11 +44,21 @@ struct SelState {
   unsigned int pad[3];
 };
 
+// a1' spatial grid header (workspace, interaction.cu).  The bounding-box / speed accumulators
+// are filled by k_int_compact with atomics and reset by k_grid_setup for the next step.
+struct GridHdr {
+  double xmin, ymin, h, vmax;
+  uint32_t ncx, ncy, count, n_heavy;
+  int32_t acc_x0, acc_y0, acc_x1, acc_y1;  // order-preserving integer keys of the coordinates
+  uint32_t acc_vmax;                        // float bits of the largest speed (non-negative)
+  uint32_t pad[3];
+};
+
 // Workspace carve-up (byte offsets from the workspace base, 256-B aligned).
 struct Layout {
   uint64_t n_local, n_words, n_kin, n_tiles, n_blocks, n_block_pages, n_dev_pages, desc_cap, world;
   uint64_t max_sort_chunks, max_exp_chunks;
-  uint64_t keys, elig, bm[2], dint, ilist_kin, ilist_idx, ilist_dact, grid_hdr, cell_cnt, cell_start, g_cell, g_kin, g_ent;
+  uint64_t keys, elig, bm[2], dint, ilist_kin, ilist_idx, ilist_dact, grid_hdr, heavy, cell_cnt, cell_start, g_cell, g_kin, g_ent;
   uint64_t hist1, mm1, hist2, mm2, hist3, state, header, gather;
   uint64_t tile_tie, tile_tie_excl, tile_pf, tile_ev, tile_pf_excl, tile_ev_excl, tile_h2d, tile_tiekept, tile_elig;
   uint64_t pf_ids, ev_ids, sort_ka, sort_va, sort_kb, sort_vb, sort_cnt, pfa_key, pfa_val;
@@ -72,7 +82,8 @@ struct Dev {
   float4 *ilist_kin;
   uint32_t *ilist_idx;
   float *ilist_dact;                 // D_action of each participant (a1' pruning bound)
-  uint8_t *grid_hdr;                 // a1' grid: bounding box, cell size, shape (interaction.cu)
+  uint8_t *grid_hdr;                 // a1' grid: GridHdr
+  uint32_t *heavy;                   // [n_kin] participants whose search continues warp-wide
   uint32_t *cell_cnt, *cell_start;   // [GRID_MAX_SIDE^2 (+1)]
   uint32_t *g_cell, *g_ent;          // [n_kin] cell of each participant; participant of each sorted slot
   float4 *g_kin;                     // [n_kin] kinematics in cell order

@@ -46,6 +46,9 @@ __global__ void k_plan_init(Params p) {
 
 __global__ void __launch_bounds__(NT) k_int_compact(Params p, int64_t now) {
   uint32_t st = 0;
+  // bounding box and largest speed of the participants, for the a1' grid (interaction.cu)
+  int32_t bx0 = 0x7FFFFFFF, by0 = 0x7FFFFFFF, bx1 = (int32_t)0x80000000, by1 = (int32_t)0x80000000;
+  uint32_t bvm = 0;
   for (uint64_t k = blockIdx.x * (uint64_t)NT + threadIdx.x; k < p.n_kin; k += (uint64_t)gridDim.x * NT)
     p.d.dint[k] = __int_as_float(0x7F800000);
   for (uint64_t base = blockIdx.x * (uint64_t)NT; base < p.n_local; base += (uint64_t)gridDim.x * NT) {
@@ -80,11 +83,47 @@ __global__ void __launch_bounds__(NT) k_int_compact(Params p, int64_t now) {
         p.d.ilist_kin[slot] = kv;
         p.d.ilist_idx[slot] = ki;
         p.d.ilist_dact[slot] = dact;
+        bx0 = min(bx0, fkey(kv.x));
+        by0 = min(by0, fkey(kv.y));
+        bx1 = max(bx1, fkey(kv.x));
+        by1 = max(by1, fkey(kv.y));
+        bvm = max(bvm, __float_as_uint(sqrtf(kv.z * kv.z + kv.w * kv.w)));
       }
     }
   }
   st = __reduce_or_sync(FULL, st);
   if ((threadIdx.x & 31) == 0 && st) atomicOr(&p.d.state->status, st);
+  if (p.n_kin >= GRID_MIN_PARTICIPANTS) {
+    __shared__ int32_t sb[4];
+    __shared__ uint32_t svm;
+    if (threadIdx.x == 0) {
+      sb[0] = sb[1] = 0x7FFFFFFF;
+      sb[2] = sb[3] = (int32_t)0x80000000;
+      svm = 0;
+    }
+    __syncthreads();
+    bx0 = __reduce_min_sync(FULL, bx0);
+    by0 = __reduce_min_sync(FULL, by0);
+    bx1 = __reduce_max_sync(FULL, bx1);
+    by1 = __reduce_max_sync(FULL, by1);
+    bvm = __reduce_max_sync(FULL, bvm);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&sb[0], bx0);
+      atomicMin(&sb[1], by0);
+      atomicMax(&sb[2], bx1);
+      atomicMax(&sb[3], by1);
+      atomicMax(&svm, bvm);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && sb[0] != 0x7FFFFFFF) {
+      GridHdr *g = reinterpret_cast<GridHdr *>(p.d.grid_hdr);
+      atomicMin(&g->acc_x0, sb[0]);
+      atomicMin(&g->acc_y0, sb[1]);
+      atomicMax(&g->acc_x1, sb[2]);
+      atomicMax(&g->acc_y1, sb[3]);
+      atomicMax(&g->acc_vmax, svm);
+    }
+  }
 }
 
 // Eq. 2, reading R6/R7: t_ij = (r.r) / (-(r.w)), r = p_j - p_i, w = v_j - v_i,
