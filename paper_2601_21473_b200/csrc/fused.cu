@@ -914,7 +914,35 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       }
       __syncthreads();
       lap(2);
-      if (warp == 0) {  // the slice in order: position = start + earlier members with the same code
+      const uint32_t rseg = ((smax - smin) >> g) + 1, nsl = e1 - e0;
+      if (rseg <= 128) {
+        // position = start of the code + members before the slice + members of earlier warps
+        // of the slice + earlier lanes of the warp (all warps at once: per-warp code counts)
+        uint32_t *hw = s.h + 12 * NBL;  // [32 warps][128 codes]
+        const uint32_t nw = (nsl + 31) / 32;
+        for (uint32_t x = threadIdx.x; x < nw * 128; x += FT) hw[x] = 0;
+        __syncthreads();
+        const uint32_t x = warp * 32 + lane;
+        const bool on = x < nsl;
+        uint32_t code = 0xFFFFFFFFu, rin = 0;
+        if (warp < nw) {
+          code = on ? sc[x] : 0xFFFFFFFFu;
+          const uint32_t peers = __match_any_sync(0xFFFFFFFFu, code);
+          rin = __popc(peers & lanemask_lt());
+          if (on && rin == 0) hw[warp * 128 + code] = __popc(peers);
+        }
+        __syncthreads();
+        for (uint32_t c2 = threadIdx.x; c2 < rseg; c2 += FT) {  // exclusive prefix over the warps
+          uint32_t run = 0;
+          for (uint32_t w2 = 0; w2 < nw; ++w2) {
+            const uint32_t v = hw[w2 * 128 + c2];
+            hw[w2 * 128 + c2] = run;
+            run += v;
+          }
+        }
+        __syncthreads();
+        if (on) out[h_all[code] + h_bef[code] + hw[warp * 128 + code] + rin] = sid[x];
+      } else if (warp == 0) {  // the slice in order, one warp: position = start + earlier members with the same code
         for (uint32_t x0 = 0; x0 < e1 - e0; x0 += 32) {
           const uint32_t x = x0 + lane;
           const bool on = x < e1 - e0;
