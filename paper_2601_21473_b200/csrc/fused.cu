@@ -346,6 +346,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     sp.cur = (int)I.cur;
   }
   __syncthreads();
+  // Programmatic dependent launch: everything above (parameter copy, L2 prefetch of the
+  // inputs) overlaps the tail of the previous kernel on the stream; from here on this launch
+  // sees all of its writes.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // ... and the next launch may be scheduled right away: its CTAs take SMs as this grid's CTAs
+  // exit and wait (above) for this grid's completion before touching any state
+  asm volatile("griddepcontrol.launch_dependents;");
   const Params &p = sp;
   const InstArgs A = {I.now, (int)I.parity, I.epoch, I.tile, I.tile / 32};
   const Dev &d = p.d;
@@ -1030,7 +1037,17 @@ static void launch_t(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStr
     B.inst[i] = insts[i];
     tile = insts[i].tile > tile ? insts[i].tile : tile;
   }
-  k_fused_plan<MAXB><<<n * gsize, FT, fused_smem_bytes(tile), s>>>(B);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n * gsize);
+  cfg.blockDim = dim3(FT);
+  cfg.dynamicSmemBytes = fused_smem_bytes(tile);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_fused_plan<MAXB>, B);
 }
 
 int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s) {
