@@ -312,6 +312,28 @@ def c3_leg(torch, dev, seed=1, warm=4, steps=8):
             "steps": steps}
 
 
+def closed_loop_leg(dev, steps=64, seed=1):
+    """NEXT #3: C2 (10k agents, 7B LoRA + KV pages, budget 25%) stepped in closed loop under
+    the invocation-distance policy and the reactive LRU baseline (reading R20)."""
+    from paper_2601_21473_b200 import closed_loop
+    w = tg.config_c2(seed=seed, steps=steps)
+    b = w.blocks
+    res = {}
+    for pol in ("distance", "lru"):
+        o = closed_loop.run(w.rec, w.now, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
+                            policy=pol, device=dev.index)
+        warm = 8  # the first steps fill the empty GPU under both policies
+        res[pol] = {"demand_misses": int(o["misses"][warm:].sum()), "demand_miss_GB": float(o["miss_bytes"][warm:].sum()) / 1e9,
+                    "loaded_GB": float(o["loaded_bytes"][warm:].sum()) / 1e9,
+                    "written_back_GB": float(o["writeback_bytes"][warm:].sum()) / 1e9}
+    d, l = res["distance"], res["lru"]
+    return {"workload": f"c2 closed loop: {w.n} agents, {steps} steps (first 8 excluded), budget 25%, theta 4",
+            "distance_policy": d, "lru_baseline": l,
+            "demand_miss_reduction": 1.0 - d["demand_misses"] / max(l["demand_misses"], 1),
+            "note": "demand miss = an agent needed now (distance 0) that was not resident before the step's plan: "
+                    "a load on the critical path (P:87, P:373-375)"}
+
+
 def c5_leg(torch, dev, rank, world, replicas=64, budgets=tuple(range(10, 100, 10)), steps=8, warm=8, seed_base=100):
     """C5: independent simulation replicas x budget sizes, instances sharded over the ranks
     (instance i on rank i % world), all of a rank's instances stepped by scalesim_step_batch.
@@ -448,6 +470,7 @@ def main():
     ap.add_argument("--c5-replicas", type=int, default=64)
     ap.add_argument("--no-objects", action="store_true", help="skip the shared-object leg (NEXT #1)")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 planning + transfer overlap leg")
+    ap.add_argument("--no-closed-loop", action="store_true", help="skip the closed-loop policy comparison (NEXT #3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -627,6 +650,9 @@ def main():
     c3 = None
     if not args.no_c3 and rank == 0:
         c3 = c3_leg(torch, dev)
+    cl = None
+    if not args.no_closed_loop and rank == 0:
+        cl = closed_loop_leg(dev)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -675,6 +701,8 @@ def main():
         line["objects"] = objects
     if c3 is not None:
         line["c3"] = c3
+    if cl is not None:
+        line["closed_loop"] = cl
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     if not args.no_transfer_leg:

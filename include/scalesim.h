@@ -261,6 +261,21 @@ scalesim_status scalesim_object_min(const float *agent_dist, uint64_t n_agents, 
                                     const uint32_t *obj_flags, void *obj_rec_out, float *obj_dist_out,
                                     uint32_t *status_out, void *stream);
 
+/* Reactive LRU baseline (the paper's SGLang-style comparison policy; S:330-338;
+ * reading R20), as explicit-distance records for a context created with
+ * SCALESIM_F_EXPLICIT_DIST and planned with theta = 0: an agent in an LLM phase (WAITING /
+ * GENERATING) gets distance 0 and last_use[i] = now_tick; any other agent gets
+ * now_tick - last_use[i] (+inf while last_use[i] == 0xFFFFFFFF, never used).  Record word
+ * [1] = the agent's footprint, [2] = its dirty bit.
+ *   agent_rec   device, 16-byte aligned, 4 x u32 per agent (the planner's record layout)
+ *   last_use    device u32 [n_agents], caller-initialised to 0xFFFFFFFF; updated in place
+ *   rec_out     device, 16-byte aligned, 4 x u32 per agent
+ *   now_tick    0 <= now_tick < 2^32 - 1, non-decreasing across calls
+ * Asynchronous on `stream`.  Returns SCALESIM_E_INVALID for NULL / misaligned pointers or a
+ * tick out of range. */
+scalesim_status scalesim_lru_records(const uint32_t *agent_rec, uint64_t n_agents, int64_t now_tick,
+                                     uint32_t *last_use, void *rec_out, void *stream);
+
 /* Launches of library kernels enqueued so far (for the bench's gpu_launches). */
 uint64_t scalesim_launch_count(const scalesim_ctx *ctx);
 

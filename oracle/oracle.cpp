@@ -363,3 +363,27 @@ void oracle_explicit_dist(uint64_t n, const uint32_t *rec, float *d_out, uint32_
   }
   *status |= st;
 }
+
+// ---------------------------------------------------------------------------------------
+// LRU baseline (R20): recency as a distance.
+
+void oracle_lru_records(uint64_t n, const uint32_t *rec, int64_t now, uint32_t *last_use, uint32_t *rec_out) {
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t phase = rec[4 * i + 2] & 3u;
+    float d;
+    if (phase == PH_WAITING || phase == PH_GENERATING) {  // the agent's memory is in use now
+      last_use[i] = (uint32_t)now;
+      d = 0.0f;
+    } else if (last_use[i] == 0xFFFFFFFFu) {
+      d = std::numeric_limits<float>::infinity();  // never used
+    } else {
+      d = (float)(uint32_t)((uint32_t)now - last_use[i]);  // steps since the last use
+    }
+    uint32_t bits;
+    std::memcpy(&bits, &d, sizeof(bits));
+    rec_out[4 * i + 0] = bits;
+    rec_out[4 * i + 1] = rec[4 * i + 1];
+    rec_out[4 * i + 2] = rec[4 * i + 2] & 0x10u;
+    rec_out[4 * i + 3] = 0;
+  }
+}

@@ -55,6 +55,12 @@ void oracle_object_min(uint64_t n_agents, const float *agent_dist, uint64_t n_ob
  * NaN or negative -> +inf and ORACLE_ST_BAD_RECORD; -0 -> +0. */
 void oracle_explicit_dist(uint64_t n, const uint32_t *rec, float *d_out, uint32_t *status);
 
+/* Reactive LRU baseline as explicit distances (P:303 SGLang-style on-demand loading with LRU
+ * eviction; reading R20): agent i in WAITING or GENERATING gets distance 0 and
+ * last_use[i] = now; any other agent gets now - last_use[i], or +inf while last_use[i] is
+ * 0xFFFFFFFF (never used).  rec_out[i] = {f32 bits of the distance, footprint, dirty bit, 0}. */
+void oracle_lru_records(uint64_t n, const uint32_t *rec, int64_t now, uint32_t *last_use, uint32_t *rec_out);
+
 /* Interaction component only (Eq. 2): dint[k] = min over other ACTING INT agents j of
  * (r.r)/(-r.w) for approaching pairs, +inf otherwise; indexed by kin index.  Exposed so
  * the tests can pin Eq. 2 separately.  Entries of kin not owned by an ACTING INT agent

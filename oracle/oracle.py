@@ -53,6 +53,8 @@ def lib():
             L.oracle_object_min.restype = None
             L.oracle_explicit_dist.argtypes = [u64, u32p, f32p, u32p]
             L.oracle_explicit_dist.restype = None
+            L.oracle_lru_records.argtypes = [u64, u32p, C.c_int64, u32p, u32p]
+            L.oracle_lru_records.restype = None
             L.oracle_plan.argtypes = [u64, u32p, f32p, u8p, f32p, u64, u8p, u32p, u64p, u32p, u64p,
                                       u64p, u32p]
             L.oracle_plan.restype = None
@@ -138,6 +140,16 @@ def explicit_dist(rec):
     lib().oracle_explicit_dist(n, _p(rec if n else np.zeros((1, 4), np.uint32), C.c_uint32), _p(d, C.c_float),
                                _p(st, C.c_uint32))
     return d[:n], int(st[0])
+
+
+def lru_records(rec, now: int, last_use):
+    """LRU-baseline records (reading R20); last_use (uint32, n) is updated in place."""
+    rec = _rec(rec)
+    n = rec.shape[0]
+    assert last_use.dtype == np.uint32 and last_use.flags.c_contiguous and last_use.shape[0] == n
+    out = np.zeros((max(n, 1), 4), dtype=np.uint32)
+    lib().oracle_lru_records(n, _p(rec, C.c_uint32), int(now), _p(last_use, C.c_uint32), _p(out, C.c_uint32))
+    return out[:n]
 
 
 def plan(rec, d, resident, theta, budget: int):

@@ -407,3 +407,40 @@ def test_config1_traces_all_variants():
                     kept, _ = brute_force_cut(d, w.rec[s, :, 1], res, w.theta, cls, w.budget)
                     assert set(np.nonzero(p["resident"])[0].tolist()) == kept
                     res = p["resident"]
+
+
+# ----------------------------------------------------------------------------------------
+# LRU baseline as explicit distances (reading R20): pinned to the textbook LRU
+
+
+def lru_closed_loop(requests, n_agents, capacity):
+    """Closed loop of the planner on LRU records (theta = 0): misses = requested agents not
+    resident before the plan."""
+    res = np.zeros(n_agents, np.uint8)
+    last = np.full(n_agents, 0xFFFFFFFF, np.uint32)
+    misses = 0
+    for t, req in enumerate(requests):
+        agents = [dict(phase=tg.PH_WAITING) if a in req else dict(d=1) for a in range(n_agents)]
+        rec = oracle.lru_records(rec_of(agents), t, last)
+        d, _ = oracle.explicit_dist(rec)
+        misses += sum(1 for a in req if not res[a])
+        p = oracle.plan(rec, d, res, np.zeros(3, np.float32), capacity)
+        res = p["resident"]
+    return misses
+
+
+def test_lru_reading_canonical_trace():
+    g = gold("canonical_trace.json")
+    reqs = [frozenset([a]) for a in g["trace"]]
+    assert lru_closed_loop(reqs, 4, g["capacity"]) == g["expected_lru_misses"]
+
+
+def test_lru_reading_equals_textbook_lru():
+    """Single requests, uniform sizes: the planner on LRU records is LRU (misses equal the
+    textbook list-based LRU on random traces)."""
+    rng = np.random.default_rng(77)
+    for trial in range(150):
+        n_agents = int(rng.integers(2, 8))
+        cap = int(rng.integers(1, n_agents + 1))
+        trace = [int(x) for x in rng.integers(0, n_agents, int(rng.integers(1, 25)))]
+        assert lru_closed_loop([frozenset([a]) for a in trace], n_agents, cap) == lru_misses(trace, cap), trial
