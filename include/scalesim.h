@@ -276,6 +276,21 @@ scalesim_status scalesim_object_min(const float *agent_dist, uint64_t n_agents, 
 scalesim_status scalesim_lru_records(const uint32_t *agent_rec, uint64_t n_agents, int64_t now_tick,
                                      uint32_t *last_use, void *rec_out, void *stream);
 
+/* Hop counts for the diffusion class ("hop count from the information source", R9):
+ * breadth-first levels from a source set over a CSR graph, on the GPU (an initialisation-time
+ * computation: the caller turns them into the records' remaining-hop words).
+ *   row_ptr   device u64 [n_vertices + 1], col device u32 [row_ptr[n_vertices]] (neighbours;
+ *             indices >= n_vertices are ignored)
+ *   sources   device u32 [n_sources] (out-of-range entries ignored, duplicates allowed)
+ *   hops_out  device u32 [n_vertices]: BFS level, 0xFFFFFFFF where unreachable
+ *   scratch   device, 16-byte aligned, >= scalesim_bfs_scratch_bytes(n_vertices) bytes
+ * Synchronous on `stream` (the host reads each level's frontier size).  Returns
+ * SCALESIM_E_INVALID for NULL / misaligned / undersized arguments or n_vertices >= 2^32 - 1. */
+uint64_t scalesim_bfs_scratch_bytes(uint64_t n_vertices);
+scalesim_status scalesim_bfs_hops(const uint64_t *row_ptr, const uint32_t *col, uint64_t n_vertices,
+                                  const uint32_t *sources, uint64_t n_sources, uint32_t *hops_out, void *scratch,
+                                  uint64_t scratch_bytes, void *stream);
+
 /* Launches of library kernels enqueued so far (for the bench's gpu_launches). */
 uint64_t scalesim_launch_count(const scalesim_ctx *ctx);
 

@@ -387,3 +387,29 @@ void oracle_lru_records(uint64_t n, const uint32_t *rec, int64_t now, uint32_t *
     rec_out[4 * i + 3] = 0;
   }
 }
+
+// ---------------------------------------------------------------------------------------
+// Diffusion hop counts: P:229, R9 (plain FIFO breadth-first search).
+
+void oracle_bfs_hops(uint64_t n, const uint64_t *row_ptr, const uint32_t *col, const uint32_t *sources,
+                     uint64_t n_sources, uint32_t *hops) {
+  for (uint64_t v = 0; v < n; ++v) hops[v] = 0xFFFFFFFFu;
+  std::vector<uint32_t> queue;
+  for (uint64_t k = 0; k < n_sources; ++k) {
+    const uint32_t s = sources[k];
+    if (s < n && hops[s] == 0xFFFFFFFFu) {
+      hops[s] = 0;
+      queue.push_back(s);
+    }
+  }
+  for (size_t head = 0; head < queue.size(); ++head) {
+    const uint32_t u = queue[head];
+    for (uint64_t k = row_ptr[u]; k < row_ptr[u + 1]; ++k) {
+      const uint32_t w = col[k];
+      if (w < n && hops[w] == 0xFFFFFFFFu) {
+        hops[w] = hops[u] + 1;
+        queue.push_back(w);
+      }
+    }
+  }
+}

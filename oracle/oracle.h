@@ -61,6 +61,12 @@ void oracle_explicit_dist(uint64_t n, const uint32_t *rec, float *d_out, uint32_
  * 0xFFFFFFFF (never used).  rec_out[i] = {f32 bits of the distance, footprint, dirty bit, 0}. */
 void oracle_lru_records(uint64_t n, const uint32_t *rec, int64_t now, uint32_t *last_use, uint32_t *rec_out);
 
+/* Diffusion hop counts ("hop count from the information source", R9): breadth-first
+ * levels from the source set over a CSR graph (row_ptr [n+1], col); 0xFFFFFFFF unreachable.
+ * Out-of-range neighbour / source indices are ignored. */
+void oracle_bfs_hops(uint64_t n, const uint64_t *row_ptr, const uint32_t *col, const uint32_t *sources,
+                     uint64_t n_sources, uint32_t *hops);
+
 /* Interaction component only (Eq. 2): dint[k] = min over other ACTING INT agents j of
  * (r.r)/(-r.w) for approaching pairs, +inf otherwise; indexed by kin index.  Exposed so
  * the tests can pin Eq. 2 separately.  Entries of kin not owned by an ACTING INT agent

@@ -55,6 +55,8 @@ def lib():
             L.oracle_explicit_dist.restype = None
             L.oracle_lru_records.argtypes = [u64, u32p, C.c_int64, u32p, u32p]
             L.oracle_lru_records.restype = None
+            L.oracle_bfs_hops.argtypes = [u64, u64p, u32p, u32p, u64, u32p]
+            L.oracle_bfs_hops.restype = None
             L.oracle_plan.argtypes = [u64, u32p, f32p, u8p, f32p, u64, u8p, u32p, u64p, u32p, u64p,
                                       u64p, u32p]
             L.oracle_plan.restype = None
@@ -149,6 +151,18 @@ def lru_records(rec, now: int, last_use):
     assert last_use.dtype == np.uint32 and last_use.flags.c_contiguous and last_use.shape[0] == n
     out = np.zeros((max(n, 1), 4), dtype=np.uint32)
     lib().oracle_lru_records(n, _p(rec, C.c_uint32), int(now), _p(last_use, C.c_uint32), _p(out, C.c_uint32))
+    return out[:n]
+
+
+def bfs_hops(row_ptr, col, sources):
+    """Diffusion hop counts (R9): uint32 BFS levels, 0xFFFFFFFF unreachable."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+    cl = np.ascontiguousarray(col, dtype=np.uint32)
+    sr = np.ascontiguousarray(sources, dtype=np.uint32)
+    n = rp.shape[0] - 1
+    out = np.zeros(max(n, 1), dtype=np.uint32)
+    lib().oracle_bfs_hops(n, _p(rp, C.c_uint64), _p(cl if cl.size else np.zeros(1, np.uint32), C.c_uint32),
+                          _p(sr if sr.size else np.zeros(1, np.uint32), C.c_uint32), sr.shape[0], _p(out, C.c_uint32))
     return out[:n]
 
 

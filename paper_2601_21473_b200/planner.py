@@ -268,6 +268,22 @@ def object_min(agent_dist: torch.Tensor, ref_ptr: torch.Tensor, ref_agent: torch
                                     st.cuda_stream), "scalesim_object_min")
 
 
+def bfs_hops(row_ptr: torch.Tensor, col: torch.Tensor, sources: torch.Tensor,
+             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """scalesim_bfs_hops: BFS level of every vertex from the sources (uint32 as int32 tensor,
+    -1 = unreachable).  row_ptr int64 [n + 1], col / sources 32-bit, all on one CUDA device."""
+    lib = L.lib()
+    n = row_ptr.numel() - 1
+    dev = row_ptr.device
+    hops = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    nb = int(lib.scalesim_bfs_scratch_bytes(n))
+    scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    L.check(lib.scalesim_bfs_hops(_ptr(row_ptr), _ptr(col), n, _ptr(sources), sources.numel(), _ptr(hops),
+                                  _ptr(scratch), nb, st.cuda_stream), "scalesim_bfs_hops")
+    return hops[:n]
+
+
 def step_batch(planners, now: int):
     """One step of several independent planners (replicas / sweep points) sharing one stream:
     scalesim_step_batch plans them in as few launches as possible."""

@@ -131,3 +131,22 @@ def test_explicit_records_with_transfers():
                     int(fp.sum() * 0.3), np.full(3, 5.0, np.float32))
     run_parity(w, explicit=True)
     run_parity(w, explicit=True, multi_kernel=True)
+
+
+def test_bfs_hops_vs_oracle():
+    """scalesim_bfs_hops (R9, NEXT #4): BFS levels on a 100k-vertex Barabasi-Albert graph
+    (C3's diffusion graph shape) from 8 sources, plus a graph with unreachable parts, equal
+    the oracle's FIFO BFS."""
+    from paper_2601_21473_b200.planner import bfs_hops
+    for n, m, extra in ((100_000, 4, 0), (5000, 2, 300)):
+        adj = tg.ba_graph(n, m, seed=n)
+        adj = adj + [[] for _ in range(extra)]  # isolated vertices
+        ptr = np.zeros(len(adj) + 1, np.uint64)
+        ptr[1:] = np.cumsum([len(a) for a in adj])
+        col = np.array([w for a in adj for w in a], np.uint32)
+        src = np.random.default_rng(n).choice(n, 8, replace=False).astype(np.uint32)
+        exp = oracle.bfs_hops(ptr, col, src)
+        got = bfs_hops(_dev(ptr), _dev(col), _dev(src)).cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, exp)
+        assert np.array_equal(exp.astype(np.int64), np.where(tg.bfs_hops(adj, src) == tg.UNREACHABLE, 0xFFFFFFFF,
+                                                             tg.bfs_hops(adj, src)))

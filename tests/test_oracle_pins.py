@@ -444,3 +444,38 @@ def test_lru_reading_equals_textbook_lru():
         cap = int(rng.integers(1, n_agents + 1))
         trace = [int(x) for x in rng.integers(0, n_agents, int(rng.integers(1, 25)))]
         assert lru_closed_loop([frozenset([a]) for a in trace], n_agents, cap) == lru_misses(trace, cap), trial
+
+
+# ----------------------------------------------------------------------------------------
+# Diffusion hop counts (R9): closed forms
+
+
+def _csr(adj):
+    ptr = np.zeros(len(adj) + 1, np.uint64)
+    ptr[1:] = np.cumsum([len(a) for a in adj])
+    col = np.array([w for a in adj for w in a], np.uint32)
+    return ptr, col
+
+
+def test_bfs_closed_forms():
+    # path 0-1-2-...-9 from 0: hop = index; star from the centre: 1; from a leaf: 2
+    path = [[i - 1] * (i > 0) + [i + 1] * (i < 9) for i in range(10)]
+    assert oracle.bfs_hops(*_csr(path), [0]).tolist() == list(range(10))
+    star = [list(range(1, 6))] + [[0]] * 5
+    assert oracle.bfs_hops(*_csr(star), [0]).tolist() == [0, 1, 1, 1, 1, 1]
+    assert oracle.bfs_hops(*_csr(star), [3]).tolist() == [1, 2, 2, 0, 2, 2]
+    # W x H grid graph from the corner: Manhattan distance; two sources: the nearer one
+    W, H = 13, 7
+    grid = [[] for _ in range(W * H)]
+    for y in range(H):
+        for x in range(W):
+            v = y * W + x
+            for dx, dy in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+                if 0 <= x + dx < W and 0 <= y + dy < H:
+                    grid[v].append((y + dy) * W + x + dx)
+    h = oracle.bfs_hops(*_csr(grid), [0])
+    assert all(h[y * W + x] == x + y for y in range(H) for x in range(W))
+    h2 = oracle.bfs_hops(*_csr(grid), [0, W * H - 1])
+    assert all(h2[y * W + x] == min(x + y, (W - 1 - x) + (H - 1 - y)) for y in range(H) for x in range(W))
+    # unreachable vertices, out-of-range source ignored
+    assert oracle.bfs_hops(*_csr([[1], [0], []]), [0, 99]).tolist() == [0, 1, 0xFFFFFFFF]
