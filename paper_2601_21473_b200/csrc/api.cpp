@@ -659,7 +659,10 @@ static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out) {
   // byte accounting (multi-kernel path) and page assignment (transfers); the fused kernel
   // accounts the write-back bytes itself
   if (c->transfer || !c->last_fused) c->launches += launch_expand(p, c->stream);
-  CK(cudaEventRecord(c->ev_plan, c->stream));
+  // the transfer's copy streams wait on this event (plan-only contexts record nothing: in a
+  // captured graph consecutive plan kernels then stay directly linked, so their programmatic
+  // launch overlap is kept)
+  if (c->transfer) CK(cudaEventRecord(c->ev_plan, c->stream));
   if (!c->fused || p.n_kin > 0 || c->cfg.world > 1)
     c->launches += launch_plan_init(p, c->stream);  // clear the multi-kernel accumulators for the next step
   CK(cudaGetLastError());
