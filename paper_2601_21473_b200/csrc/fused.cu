@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     t_rows = rows[(uint64_t)threadIdx.x * stride + sel.b_res];
   }
   unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw]
+#pragma unroll 2
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
     const bool tie = !all_fit && ((s.elig_w[w] >> lane) & 1u) && s.keys[k] == dstar;
@@ -529,17 +530,15 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     if (lane == 0) word_tie[w] = v;
   }
   __syncthreads();
-  __shared__ unsigned long long sh_tie_excl, sh_chunk;
-  {  // exclusive scan over the tile's words (tw <= FUSED_MAX_TILE / 32 <= FT: one word per thread)
-    const uint32_t w = threadIdx.x;
-    const unsigned long long v = w < A.tw ? word_tie[w] : 0ull;
-    const unsigned long long ex = block_excl_scan<unsigned long long, FT>(v, &sh_chunk);
-    if (w < A.tw) word_tie[w] = ex;
-    __syncthreads();
-  }
+  // exclusive scan over the tile's words (tw <= FUSED_MAX_TILE / 32 <= FT: one word per
+  // thread) and, in the same pass, the preceding CTAs' total
+  unsigned long long sh_tie_excl;
   {
-    const unsigned long long t = block_sum<unsigned long long, FT>(t_rows);
-    if (threadIdx.x == 0) sh_tie_excl = t;
+    const uint32_t w = threadIdx.x;
+    unsigned long long v[2] = {w < A.tw ? word_tie[w] : 0ull, t_rows}, tt[2];
+    block_excl_scan_v<unsigned long long, 2, FT>(v, tt);
+    if (w < A.tw) word_tie[w] = v[0];
+    sh_tie_excl = tt[1];
   }
   __syncthreads();
   if (c == 0 && threadIdx.x == 0) prof[10] = gtimer();
@@ -557,6 +556,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   __syncthreads();
   unsigned long long h2d = 0, d2h = 0, tie_kept = 0;
   uint32_t n_el = 0, wb_pend = 0;  // wb_pend: write-back bytes load in flight (added one use later)
+#pragma unroll 2
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
     const uint32_t elw = s.elig_w[w];  // 0 beyond n_here
