@@ -173,6 +173,22 @@ __device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned
   }
 }
 
+// Exact CTA-wide sum of a 64-bit value without a block reduction: each warp reduces the
+// value's four 16-bit chunks with REDUX (a warp sums < 2^21 per chunk) and lane 0 adds them to
+// four shared 32-bit counters (a CTA sums < 2^26 per chunk); after the next barrier the CTA
+// total is parts_u64(acc4).  Block-wide shuffle reductions cost ~1.5 us on 1024 threads.
+__device__ __forceinline__ void warp_add_u64(unsigned long long v, uint32_t *acc4) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t part = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(v >> (16 * k)) & 0xFFFFu);
+    if ((threadIdx.x & 31) == 0 && part) atomicAdd(&acc4[k], part);
+  }
+}
+__device__ __forceinline__ unsigned long long parts_u64(const uint32_t *acc4) {
+  return (unsigned long long)acc4[0] + ((unsigned long long)acc4[1] << 16) + ((unsigned long long)acc4[2] << 32) +
+         ((unsigned long long)acc4[3] << 48);
+}
+
 struct Sel {
   uint32_t prefix;
   unsigned long long below, rem;
@@ -393,6 +409,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   const uint32_t nowl = (uint32_t)now;
   clear_hist(s.h, NB1);
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_old[base / 32 + w] : 0u;
+  __shared__ uint32_t sacc[20];  // 16-bit chunk counters: [0,4) zero-distance bytes, [4,20) P4 sums
+  if (threadIdx.x < 20) sacc[threadIdx.x] = 0;
   __syncthreads();
   uint32_t st = 0;
   unsigned long long zero_b = 0;
@@ -454,6 +472,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       if (valid && dist == 0.0f) zero_b += r[j].y;
     }
   }
+  warp_add_u64(zero_b, sacc);
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&prof[25], gtimer());  // P1 loop done
   // this CTA's level-1 bytes: dense row (its column entry gives the tie prefix in P3) and
@@ -461,10 +480,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, imode ? nullptr : d.f_mm1 + 2 * NB1 * par,
                d.f_rows1 + (uint64_t)c * NB1);
   if (threadIdx.x == 0) atomicMax(&prof[26], gtimer());  // published
-  zero_b = block_sum<unsigned long long, FT>(zero_b);
   st = __reduce_or_sync(0xFFFFFFFFu, st);
   if (lane == 0 && st) atomicOr(reinterpret_cast<unsigned int *>(&acc[5]), st);
-  if (threadIdx.x == 0 && zero_b) atomicAdd(&acc[0], zero_b);
+  if (threadIdx.x == 0) {
+    const unsigned long long zb = parts_u64(sacc);
+    if (zb) atomicAdd(&acc[0], zb);
+  }
   if (threadIdx.x == 0) atomicMax(&prof[11], gtimer());
   if (c == 0 && threadIdx.x == 0) prof[3] = gtimer();
   grid.sync();
@@ -635,6 +656,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   // tw <= FT == NBL)
   uint32_t *off_pf = s.h + 2 * NBL, *off_ev = s.h + 3 * NBL;
   __shared__ uint32_t sh_mpf, sh_mev;
+  d2h += wb_pend;
+  warp_add_u64(h2d, sacc + 4);  // (the scan's barriers complete them)
+  warp_add_u64(d2h, sacc + 8);
+  warp_add_u64(tie_kept, sacc + 12);
+  warp_add_u64(n_el, sacc + 16);
+  // This tile's list members in list order (prefetch ascending id, evict descending id) into
+  // memb, and the bucket-major offsets of the staging area (one word / bucket per thread:
+  // tw <= FT == NBL)
   {
     const uint32_t w = threadIdx.x;
     const uint32_t pw = w < A.tw ? s.pf_w[w] : 0u, ew = w < A.tw ? s.ev_w[w] : 0u;
@@ -706,12 +735,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     d.f_cta_cpf[(uint64_t)c * NBL + b] = (off_pf[b] << 16) | cnt_pf[b];
     d.f_cta_cev[(uint64_t)c * NBL + b] = (off_ev[b] << 16) | cnt_ev[b];
   }
-  d2h += wb_pend;
   if (threadIdx.x == 0) atomicMax(&prof[28], gtimer());  // staged, rows published
-  {
-    unsigned long long sums[4] = {h2d, d2h, tie_kept, (unsigned long long)n_el};
-    block_sum_v<unsigned long long, 4, FT>(sums);
-    if (threadIdx.x < 4 && sums[threadIdx.x]) atomicAdd(&acc[1 + threadIdx.x], sums[threadIdx.x]);
+  if (threadIdx.x < 4) {
+    const unsigned long long v = parts_u64(sacc + 4 + 4 * threadIdx.x);
+    if (v) atomicAdd(&acc[1 + threadIdx.x], v);
   }
   if (threadIdx.x == 0) atomicMax(&prof[12], gtimer());
   if (c == 0 && threadIdx.x == 0) prof[5] = gtimer();
@@ -762,24 +789,21 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       const uint32_t gp = 2 * threadIdx.x + q;
       len[q] = tot[list == 0 ? gp : 2 * NBL - 1 - gp];
     }
-    uint32_t v[2] = {list == 0 ? len[0] + len[1] : 0u, list == 1 ? len[0] + len[1] : 0u}, tt[2];
-    block_excl_scan_v<uint32_t, 2, FT>(v, tt);
+    // one scan: list positions of the segments and their first slots (slices of CH = 512)
+    CH = 512;
+    const uint32_t ns0 = (len[0] + CH - 1) / CH, ns1 = (len[1] + CH - 1) / CH;
+    uint32_t v[3] = {list == 0 ? len[0] + len[1] : 0u, list == 1 ? len[0] + len[1] : 0u, ns0 + ns1}, tt[3];
+    block_excl_scan_v<uint32_t, 3, FT>(v, tt);
     if (threadIdx.x == 0) atomicMax(&prof[31], gtimer());  // totals loaded and scanned
     npf = tt[0];
     nev = tt[1];
-    // slice length: about two slots per CTA, 256..1024 elements
-    uint32_t ch = (2 * (npf + nev) / G + 31) / 32 * 32;
-    CH = ch < 256 ? 256 : (ch > 1024 ? 1024 : ch);
-    const uint32_t ns0 = (len[0] + CH - 1) / CH, ns1 = (len[1] + CH - 1) / CH;
     seg_start[2 * threadIdx.x] = v[list];
     seg_start[2 * threadIdx.x + 1] = v[list] + len[0];
     seg_len[2 * threadIdx.x] = len[0];
     seg_len[2 * threadIdx.x + 1] = len[1];
-    uint32_t w[1] = {ns0 + ns1}, wt[1];
-    block_excl_scan_v<uint32_t, 1, FT>(w, wt);
-    slot_base[2 * threadIdx.x] = w[0];
-    slot_base[2 * threadIdx.x + 1] = w[0] + ns0;
-    if (threadIdx.x == 0) sh_ns = wt[0];
+    slot_base[2 * threadIdx.x] = v[2];
+    slot_base[2 * threadIdx.x + 1] = v[2] + ns0;
+    if (threadIdx.x == 0) sh_ns = tt[2];
   }
   if (c == 0 && threadIdx.x == 0) {
     d.header[H_N_PF] = npf;
