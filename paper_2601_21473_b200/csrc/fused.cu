@@ -667,8 +667,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   {
     const uint32_t w = threadIdx.x;
     const uint32_t pw = w < A.tw ? s.pf_w[w] : 0u, ew = w < A.tw ? s.ev_w[w] : 0u;
-    uint32_t v[4] = {(uint32_t)__popc(pw), (uint32_t)__popc(ew), cnt_pf[w], cnt_ev[w]}, tt[4];
-    block_excl_scan_v<uint32_t, 4, FT>(v, tt);
+    // four scans in one: 16-bit fields of a 64-bit value (every prefix <= tile < 2^16)
+    const unsigned long long pk = (unsigned long long)__popc(pw) | ((unsigned long long)__popc(ew) << 16) |
+                                  ((unsigned long long)cnt_pf[w] << 32) | ((unsigned long long)cnt_ev[w] << 48);
+    unsigned long long pv[1] = {pk}, pt[1];
+    block_excl_scan_v<unsigned long long, 1, FT>(pv, pt);
+    const uint32_t v[4] = {(uint32_t)(pv[0] & 0xFFFFu), (uint32_t)((pv[0] >> 16) & 0xFFFFu),
+                           (uint32_t)((pv[0] >> 32) & 0xFFFFu), (uint32_t)(pv[0] >> 48)};
+    const uint32_t tt[2] = {(uint32_t)(pt[0] & 0xFFFFu), (uint32_t)((pt[0] >> 16) & 0xFFFFu)};
     off_pf[w] = v[2];
     off_ev[w] = v[3];
     if (threadIdx.x == 0) {
@@ -792,8 +798,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     // one scan: list positions of the segments and their first slots (slices of CH = 512)
     CH = 512;
     const uint32_t ns0 = (len[0] + CH - 1) / CH, ns1 = (len[1] + CH - 1) / CH;
-    uint32_t v[3] = {list == 0 ? len[0] + len[1] : 0u, list == 1 ? len[0] + len[1] : 0u, ns0 + ns1}, tt[3];
-    block_excl_scan_v<uint32_t, 3, FT>(v, tt);
+    // three scans in one: 21-bit fields of a 64-bit value (fused path: n_local <= 148 x 12288
+    // < 2^21, slots <= n_local / 512 + 2048)
+    const unsigned long long pk = (unsigned long long)(list == 0 ? len[0] + len[1] : 0u) |
+                                  ((unsigned long long)(list == 1 ? len[0] + len[1] : 0u) << 21) |
+                                  ((unsigned long long)(ns0 + ns1) << 42);
+    unsigned long long pv[1] = {pk}, pt[1];
+    block_excl_scan_v<unsigned long long, 1, FT>(pv, pt);
+    const uint32_t M21 = (1u << 21) - 1;
+    const uint32_t v[3] = {(uint32_t)(pv[0] & M21), (uint32_t)((pv[0] >> 21) & M21), (uint32_t)(pv[0] >> 42)};
+    const uint32_t tt[3] = {(uint32_t)(pt[0] & M21), (uint32_t)((pt[0] >> 21) & M21), (uint32_t)(pt[0] >> 42)};
     if (threadIdx.x == 0) atomicMax(&prof[31], gtimer());  // totals loaded and scanned
     npf = tt[0];
     nev = tt[1];
