@@ -409,8 +409,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   const uint32_t nowl = (uint32_t)now;
   clear_hist(s.h, NB1);
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_old[base / 32 + w] : 0u;
-  __shared__ uint32_t sacc[20];  // 16-bit chunk counters: [0,4) zero-distance bytes, [4,20) P4 sums
-  if (threadIdx.x < 20) sacc[threadIdx.x] = 0;
+  // 16-bit chunk counters: [0,4) zero-distance bytes, [4,20) P4 sums, [20,24) P3 tie prefix
+  __shared__ uint32_t sacc[24];
+  if (threadIdx.x < 24) sacc[threadIdx.x] = 0;
   __syncthreads();
   uint32_t st = 0;
   unsigned long long zero_b = 0;
@@ -553,14 +554,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   __syncthreads();
   // exclusive scan over the tile's words (tw <= FUSED_MAX_TILE / 32 <= FT: one word per
   // thread) and, in the same pass, the preceding CTAs' total
-  unsigned long long sh_tie_excl;
+  if (warp * 32 < c) warp_add_u64(t_rows, sacc + 20);  // preceding CTAs' total (threads < c)
   {
     const uint32_t w = threadIdx.x;
-    unsigned long long v[2] = {w < A.tw ? word_tie[w] : 0ull, t_rows}, tt[2];
-    block_excl_scan_v<unsigned long long, 2, FT>(v, tt);
+    unsigned long long v[1] = {w < A.tw ? word_tie[w] : 0ull}, tt[1];
+    block_excl_scan_v<unsigned long long, 1, FT>(v, tt);  // (its barriers complete the sum)
     if (w < A.tw) word_tie[w] = v[0];
-    sh_tie_excl = tt[1];
   }
+  const unsigned long long sh_tie_excl = parts_u64(sacc + 20);
   __syncthreads();
   if (c == 0 && threadIdx.x == 0) prof[10] = gtimer();
   if (threadIdx.x == 0) atomicMax(&prof[14], gtimer());
