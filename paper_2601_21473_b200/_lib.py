@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libscalesim.so")
+SO_PATH = os.environ.get("SCALESIM_SO") or os.path.join(HERE, "libscalesim.so")  # override: tools/ A/B runs only
 
 ABI_VERSION = 1
 F_NO_TRANSFER = 1

@@ -89,7 +89,7 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.pool = take(16);
   L.desc[0] = take(8 * DESC_HDR + 32 * (L.desc_cap ? L.desc_cap : 1));
   L.desc[1] = take(8 * DESC_HDR + 32 * (L.desc_cap ? L.desc_cap : 1));
-  L.f_hist1 = take(8 * 2 * 4096);
+  L.f_hist1 = take(8 * 2 * (4096 + 64));  // + [2][64] coarse sums
   L.f_mm1 = take(4 * 2 * 2 * 4096);
   L.f_hist2 = take(8 * 2 * 1024);
   L.f_mm2 = take(4 * 2 * 2 * 1024);

@@ -35,7 +35,10 @@ constexpr int FT = 1024;  // threads per CTA
 constexpr int FWARPS = FT / 32;
 constexpr int NB1 = 4096;  // level-1 buckets: distance bits [30:19]
 constexpr int NBL = 1024;  // list-sort buckets: distance bits [30:21]
-constexpr int LOAD_BATCH = 4;  // records in flight per thread in P1
+#ifndef LOAD_BATCH_V
+#define LOAD_BATCH_V 4
+#endif
+constexpr int LOAD_BATCH = LOAD_BATCH_V;  // records in flight per thread in P1
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -157,8 +160,10 @@ __device__ __forceinline__ void hist_lane(uint32_t *h, int nb, uint32_t b, uint3
 
 // this CTA's histogram: dense row (row[b] = bytes) and added to the global one (nonzero
 // buckets only)
+// g_coarse (level 1 only): sums over 64 consecutive buckets, one warp-reduced atomic per warp
+// and bucket group that holds bytes
 __device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned long long *g_hist, uint32_t *g_mm,
-                                             unsigned long long *row) {
+                                             unsigned long long *row, unsigned long long *g_coarse = nullptr) {
   for (int b = threadIdx.x; b < nb; b += FT) {
     const uint32_t q = nb == NB1 ? slot1(b) : (uint32_t)b;
     const unsigned long long v = ((unsigned long long)h[nb + q] << 16) + h[q];
@@ -169,6 +174,12 @@ __device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned
         atomicMin(&g_mm[b], h[2 * nb + q]);
         atomicMin(&g_mm[nb + b], h[3 * nb + q]);
       }
+    }
+    if (g_coarse && __ballot_sync(0xFFFFFFFFu, v != 0)) {  // warp-uniform (FT is a multiple of 32)
+      unsigned long long t = v;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&g_coarse[b >> 6], t);
     }
   }
 }
@@ -194,6 +205,75 @@ struct Sel {
   unsigned long long below, rem;
   uint32_t dstar, all_fit, done, level_res, b_res;  // bucket (and level) holding the agents at D*
 };
+
+// Level 1 of the select by one warp and two dependent loads: the 64 coarse sums (buckets
+// b >> 6), then the 64 buckets of the coarse bucket where the running byte sum crosses the
+// budget.  Same result as select_level(level 1); no block-wide scan.
+__device__ void select_level1_warp(const unsigned long long *g_hist, const unsigned long long *g_coarse,
+                                   const uint32_t *g_mm, unsigned long long budget, Sel &sel, bool imode) {
+  __shared__ unsigned long long s1_prev, s1_tot;
+  __shared__ uint32_t s1_b, s1_min, s1_nmax;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const ulonglong2 cc = reinterpret_cast<const ulonglong2 *>(g_coarse)[lane];
+    const unsigned long long incl = warp_incl_scan(cc.x + cc.y), ex = incl - cc.x - cc.y;
+    const uint32_t m1 = __ballot_sync(0xFFFFFFFFu, incl > budget);
+    const uint32_t m0 = __ballot_sync(0xFFFFFFFFu, ex + cc.x > budget);
+    if (m1 == 0) {  // every eligible agent fits
+      if (lane == 31) {
+        s1_b = 0xFFFFFFFFu;
+        s1_tot = incl;
+      }
+    } else {
+      const int L = __ffs(m1) - 1;
+      const bool even = (m0 >> L) & 1u;
+      const uint32_t C = 2 * L + (even ? 0 : 1);
+      const unsigned long long below = __shfl_sync(0xFFFFFFFFu, even ? ex : ex + cc.x, L);
+      const ulonglong2 f = reinterpret_cast<const ulonglong2 *>(g_hist + 64 * C)[lane];
+      uint32_t mn0 = 0, mn1 = 0, nx0 = 0, nx1 = 0;
+      if (g_mm) {
+        const uint2 mn = reinterpret_cast<const uint2 *>(g_mm + 64 * C)[lane];
+        const uint2 nx = reinterpret_cast<const uint2 *>(g_mm + NB1 + 64 * C)[lane];
+        mn0 = mn.x;
+        mn1 = mn.y;
+        nx0 = nx.x;
+        nx1 = nx.y;
+      }
+      const unsigned long long fi = below + warp_incl_scan(f.x + f.y), fe = fi - f.x - f.y;
+      const uint32_t n1 = __ballot_sync(0xFFFFFFFFu, fi > budget);  // nonzero: the coarse bucket crosses
+      const uint32_t n0 = __ballot_sync(0xFFFFFFFFu, fe + f.x > budget);
+      const int Lf = __ffs(n1) - 1;
+      if (lane == Lf) {
+        const bool ev = (n0 >> Lf) & 1u;
+        s1_b = 64 * C + 2 * Lf + (ev ? 0 : 1);
+        s1_prev = ev ? fe : fe + f.x;
+        s1_min = ev ? mn0 : mn1;
+        s1_nmax = ev ? nx0 : nx1;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t b = s1_b;
+  if (b == 0xFFFFFFFFu) {
+    sel.all_fit = 1;
+    sel.done = 1;
+    sel.dstar = 0xFFFFFFFFu;
+    sel.rem = budget - s1_tot;
+  } else {
+    sel.below = s1_prev;
+    sel.prefix |= b << 19;
+    const bool int_single = imode && ((b >> 4) <= 131u || b == 0xFF0u);
+    const bool single = int_single || (g_mm != nullptr && s1_min == ~s1_nmax);
+    if (single) {
+      sel.dstar = int_single ? (b << 19) : s1_min;
+      sel.rem = budget - sel.below;
+      sel.done = 1;
+      sel.level_res = 1;
+      sel.b_res = b;
+    }
+  }
+  __syncthreads();
+}
 
 // Boundary bucket of histogram level `level` (every CTA computes the same result).
 __device__ void select_level(const unsigned long long *g_hist, const uint32_t *g_mm, int level,
@@ -336,8 +416,9 @@ __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, uint32_
 
 template <int MAXB>
 __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ FusedArgs<MAXB> B) {
-  const uint32_t gi = blockIdx.x / B.gsize;
-  const uint32_t c = blockIdx.x % B.gsize, G = B.gsize;
+  // (single context: instance 0 at constant offsets, so its fields stay in uniform registers)
+  const uint32_t gi = MAXB == 1 ? 0u : blockIdx.x / B.gsize;
+  const uint32_t c = MAXB == 1 ? blockIdx.x : blockIdx.x % B.gsize, G = B.gsize;
   const FusedInst &I = B.inst[gi];
   if (threadIdx.x == 0) {  // this tile's records into L2 while the parameters are fetched
     const uint64_t b0 = (uint64_t)c * I.tile;
@@ -378,6 +459,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   if (threadIdx.x == 0) {
     const unsigned long long t = gtimer();
     atomicMin(&prof[0], t);
+    atomicMax(&prof[15], t);  // last CTA past the dependency wait
     if (c == 0) prof[2] = t;
   }
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -407,84 +489,101 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   // rounded to nearest as __ll2float_rn above
   const bool now32 = now >= 0 && now <= 0xFFFFFFFFll;
   const uint32_t nowl = (uint32_t)now;
+  // The tile is streamed in batches of LOAD_BATCH records per thread, all loads of a batch in
+  // flight before any use (measured on B200: 2-4 per thread, within noise; deeper batches and a rolling
+  // refill, profiles/r01_v8_ab.log).  Lanes past the tile's end load its last record (no
+  // zero-fill) and are masked by `valid`.
+  const uint32_t last = n_here ? n_here - 1 : 0u;
+  uint4 r[LOAD_BATCH];
+  auto load_batch = [&](uint32_t k0) {
+#pragma unroll
+    for (int j = 0; j < LOAD_BATCH; ++j)  // all loads in flight before any use
+      r[j] = n_here ? ld_stream(rec + min(k0 + j * FT + threadIdx.x, last)) : make_uint4(0, 0, 0, 0);
+  };
+#ifndef EARLY_V
+#define EARLY_V 1
+#endif
+#if EARLY_V
+  load_batch(0);  // the first batch goes out before the residency words and the shared set-up
+#endif
+  const uint32_t *bm_tile = bm_old + base / 32;
+  for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_tile[w] : 0u;
   clear_hist(s.h, NB1);
-  for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_old[base / 32 + w] : 0u;
   // 16-bit chunk counters: [0,4) zero-distance bytes, [4,20) P4 sums, [20,24) P3 tie prefix
   __shared__ uint32_t sacc[24];
   if (threadIdx.x < 24) sacc[threadIdx.x] = 0;
   __syncthreads();
   uint32_t st = 0;
-  unsigned long long zero_b = 0;
+  unsigned long long zero_b = 0;  // (integer mode: bucket 0 of the histogram instead)
   for (uint32_t k0 = 0; k0 < A.tw * 32; k0 += LOAD_BATCH * FT) {
-    uint4 r[LOAD_BATCH];
-#pragma unroll
-    for (int j = 0; j < LOAD_BATCH; ++j) {  // all loads in flight before any use
-      const uint32_t k = k0 + j * FT + threadIdx.x;
-      r[j] = k < n_here ? ld_stream(rec + k) : make_uint4(0, 0, 0, 0);
-    }
+    if (k0 != 0 || !EARLY_V) load_batch(k0);
 #pragma unroll
     for (int j = 0; j < LOAD_BATCH; ++j) {
-      const uint32_t k = k0 + j * FT + threadIdx.x;
-      if (k >= A.tw * 32) continue;  // warp-uniform (tw * 32 is a multiple of 32)
+      const uint32_t wd = (k0 + j * FT) / 32 + warp;  // this warp's residency word (k & 31 == lane)
+      if (wd >= A.tw) continue;  // warp-uniform
+      const uint32_t k = wd * 32 + lane;
       const bool valid = k < n_here;
-      const bool res = (s.old_w[k >> 5] >> (k & 31)) & 1u;
-      const uint32_t ph = r[j].z & 3u, cl = (r[j].z >> 2) & 3u;
+      const uint4 rj = r[j];
+      const bool res = (s.old_w[wd] >> lane) & 1u;
+      const uint32_t ph = rj.z & 3u, cl = (rj.z >> 2) & 3u;
       float dist, th;
       if (xdist) {  // explicit distances (R19)
-        dist = valid ? explicit_distance_of(r[j], st) : 0.0f;
+        dist = valid ? explicit_distance_of(rj, st) : 0.0f;
         th = th0;
       } else if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {
         // the warp holds interaction / diffusion / malformed records: general definition
-        dist = valid ? distance_of(r[j], now, hop_scale, dint, n_kin, st) : 0.0f;
+        dist = valid ? distance_of(rj, now, hop_scale, dint, n_kin, st) : 0.0f;
         th = (cl & 2u) ? ((cl & 1u) ? 0.0f : th2) : ((cl & 1u) ? th1 : th0);
       } else {
         // independent agents only: remaining action ticks, 0 while in an LLM
         // phase, +inf when idle — the same values distance_of gives for class 0
         float d_action;
         if (now32) {
-          d_action = r[j].x > nowl ? __uint2float_rn(r[j].x - nowl) : 0.0f;
+          d_action = rj.x > nowl ? __uint2float_rn(rj.x - nowl) : 0.0f;
         } else {
-          const int64_t remain = (int64_t)r[j].x - now;
+          const int64_t remain = (int64_t)rj.x - now;
           d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
         }
         dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
         th = th0;
       }
-      const uint32_t bits = __float_as_uint(dist);
+      const uint32_t bits = valid ? __float_as_uint(dist) : 0u;
       const bool elig = valid && (res || dist == 0.0f || dist < th);
       s.keys[k] = bits;
-      s.fp[k] = r[j].y;
+      s.fp[k] = valid ? rj.y : 0u;
       if (gkeys && valid) gkeys[k] = bits;
       const uint32_t eb = __ballot_sync(0xFFFFFFFFu, elig);
-      const uint32_t db = __ballot_sync(0xFFFFFFFFu, valid && ((r[j].z >> 4) & 1u));
+      const uint32_t db = __ballot_sync(0xFFFFFFFFu, valid && ((rj.z >> 4) & 1u));
       if (lane == 0) {
-        s.elig_w[k >> 5] = eb;
-        s.dirty_w[k >> 5] = db;
+        s.elig_w[wd] = eb;
+        s.dirty_w[wd] = db;
       }
       if (elig) {
         const uint32_t q = slot1(bits >> 19);
-        atomicAdd(&s.h[q], r[j].y & 0xFFFFu);
-        atomicAdd(&s.h[NB1 + q], r[j].y >> 16);
+        atomicAdd(&s.h[q], rj.y & 0xFFFFu);
+        atomicAdd(&s.h[NB1 + q], rj.y >> 16);
         if (!imode) {  // min / max key only where a bucket can hold several distances
           atomicMin(&s.h[2 * NB1 + q], bits);
           atomicMin(&s.h[3 * NB1 + q], ~bits);
         }
       }
-      if (valid && dist == 0.0f) zero_b += r[j].y;
+      if (!imode && valid && dist == 0.0f) zero_b += rj.y;
     }
   }
-  warp_add_u64(zero_b, sacc);
+  if (!imode) warp_add_u64(zero_b, sacc);
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&prof[25], gtimer());  // P1 loop done
   // this CTA's level-1 bytes: dense row (its column entry gives the tie prefix in P3) and
   // the global sum
   publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, imode ? nullptr : d.f_mm1 + 2 * NB1 * par,
-               d.f_rows1 + (uint64_t)c * NB1);
+               d.f_rows1 + (uint64_t)c * NB1, d.f_hist1 + 2 * NB1 + 64 * par);
   if (threadIdx.x == 0) atomicMax(&prof[26], gtimer());  // published
   st = __reduce_or_sync(0xFFFFFFFFu, st);
   if (lane == 0 && st) atomicOr(reinterpret_cast<unsigned int *>(&acc[5]), st);
   if (threadIdx.x == 0) {
-    const unsigned long long zb = parts_u64(sacc);
+    // integer mode: every distance is an integer or +inf, so level-1 bucket 0 (bits < 2^19)
+    // holds exactly the d == 0 agents, all eligible (slot1(0) == 0)
+    const unsigned long long zb = imode ? ((unsigned long long)s.h[NB1] << 16) + s.h[0] : parts_u64(sacc);
     if (zb) atomicAdd(&acc[0], zb);
   }
   if (threadIdx.x == 0) atomicMax(&prof[11], gtimer());
@@ -498,6 +597,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     const uint32_t gt = c * FT + threadIdx.x, gs = G * FT;
     for (uint32_t b = gt; b < NB1; b += gs) {
       d.f_hist1[NB1 * q + b] = 0;
+      if (b < 64) d.f_hist1[2 * NB1 + 64 * q + b] = 0;  // coarse sums
       d.f_mm1[2 * NB1 * q + b] = 0xFFFFFFFFu;
       d.f_mm1[2 * NB1 * q + NB1 + b] = 0xFFFFFFFFu;
     }
@@ -512,7 +612,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   const uint32_t *mm1 = d.f_mm1 + 2 * NB1 * par;
   Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 1, 0};
-  select_level(d.f_hist1 + NB1 * par, imode ? nullptr : mm1, 1, p.budget, sel, imode);
+  select_level1_warp(d.f_hist1 + NB1 * par, d.f_hist1 + 2 * NB1 + 64 * par, imode ? nullptr : mm1, p.budget, sel,
+                     imode);
   for (int level = 2; level <= 3 && !sel.done; ++level) {
     const int hi_shift = level == 2 ? 19 : 9, shift = level == 2 ? 9 : 0;
     const int nb = level == 2 ? 1024 : 512;
@@ -560,6 +661,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     unsigned long long v[1] = {w < A.tw ? word_tie[w] : 0ull}, tt[1];
     block_excl_scan_v<unsigned long long, 1, FT>(v, tt);  // (its barriers complete the sum)
     if (w < A.tw) word_tie[w] = v[0];
+    if (threadIdx.x == 0) word_tie[A.tw] = tt[0];  // (memb holds tile / 2 >= tw + 1 words of 64 bits)
   }
   const unsigned long long sh_tie_excl = parts_u64(sacc + 20);
   __syncthreads();
@@ -590,15 +692,23 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       if (tiew) {  // id-order inclusive prefix of the tie bytes
         const bool tie = (tiew >> lane) & 1u;
         const uint32_t fp = s.fp[k];
-        unsigned long long incl = tie ? fp : 0u;
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= o) incl += t;
+        // the word's tie bytes lie in (lo, hi]: every tie of the word fits when hi <= rem, none
+        // when lo > rem (one word of the grid straddles rem: only it needs the in-word prefix)
+        const unsigned long long lo = sh_tie_excl + word_tie[w], hi = sh_tie_excl + word_tie[w + 1];
+        if (hi <= sel.rem) {
+          if (tie) tie_kept += fp;
+          kw |= tiew;
+        } else if (lo <= sel.rem) {
+          unsigned long long incl = tie ? fp : 0u;
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          incl += lo;
+          const bool ok = tie && incl <= sel.rem;
+          if (ok) tie_kept += fp;
+          kw |= __ballot_sync(0xFFFFFFFFu, ok);
         }
-        incl += sh_tie_excl + word_tie[w];
-        const bool ok = tie && incl <= sel.rem;
-        if (ok) tie_kept += fp;
-        kw |= __ballot_sync(0xFFFFFFFFu, ok);
       }
     }
     const uint32_t old = s.old_w[w];
@@ -830,7 +940,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   if (threadIdx.x == 0) atomicMax(&prof[13], gtimer());  // P5 tables
   if (c == 0 && threadIdx.x == 0) prof[7] = gtimer();
   __shared__ uint32_t col_pre[FUSED_MAX_CTAS], col_src[FUSED_MAX_CTAS];
-  __shared__ uint32_t sh_gp, sh_tmp, sh_mm[3];
+  __shared__ uint32_t sh_gp, sh_tmp;
   const unsigned long long t_s0 = gtimer();
   unsigned long long dt[4] = {0, 0, 0, 0};  // slot sections (thread 0): segment + columns, gather, scan, place
   for (uint32_t j = c; j < n_slots; j += G) {
@@ -849,13 +959,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     // the segment's members in each CTA (list order of the CTAs: prefetch ascending, evict
     // descending): first position and staging address; the segment's min / max key and OR of
     // the low key bits
-    if (threadIdx.x == 0) {
-      sh_mm[0] = 0xFFFFFFFFu;
-      sh_mm[1] = 0xFFFFFFFFu;
-      sh_mm[2] = 0u;
-    }
+    // (warps holding CTA columns: G <= FUSED_MAX_CTAS <= 8 * 32; warp scans and REDUX, the
+    // warp totals combined by every thread: two CTA barriers)
+    uint32_t smin, smax, slo;
     {
-      uint32_t cnt = 0, src = 0, mn = 0xFFFFFFFFu, nmx = 0xFFFFFFFFu, lo = 0;
+      __shared__ uint32_t w_sum[8], w_mm[3][8];
+      uint32_t cnt = 0, src = 0, mn = 0xFFFFFFFFu, nmx = 0xFFFFFFFFu, lo = 0, incl = 0;
       if ((int)threadIdx.x < (int)G) {
         const uint32_t q = list == 0 ? threadIdx.x : G - 1 - threadIdx.x;
         const uint32_t pk = (list == 0 ? d.f_cta_cpf : d.f_cta_cev)[(uint64_t)q * NBL + b];
@@ -869,26 +978,41 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
           lo = m2;
         }
       }
-      mn = __reduce_min_sync(0xFFFFFFFFu, mn);
-      nmx = __reduce_min_sync(0xFFFFFFFFu, nmx);
-      lo = __reduce_or_sync(0xFFFFFFFFu, lo);
-      const uint32_t pre = block_excl_scan<uint32_t, FT>(cnt, &sh_tmp);  // (its barriers order sh_mm's init)
-      if (lane == 0 && (int)threadIdx.x < (int)G) {
-        atomicMin(&sh_mm[0], mn);
-        atomicMin(&sh_mm[1], nmx);
-        atomicOr(&sh_mm[2], lo);
+      const uint32_t nwg = (G + 31) / 32;
+      if ((uint32_t)warp < nwg) {
+        incl = warp_incl_scan(cnt);
+        mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+        nmx = __reduce_min_sync(0xFFFFFFFFu, nmx);
+        lo = __reduce_or_sync(0xFFFFFFFFu, lo);
+        if (lane == 31) {
+          w_sum[warp] = incl;
+          w_mm[0][warp] = mn;
+          w_mm[1][warp] = nmx;
+          w_mm[2][warp] = lo;
+        }
       }
+      __syncthreads();
+      uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, a2 = 0u, pre = incl - cnt;
+      for (uint32_t w2 = 0; w2 < nwg; ++w2) {
+        a0 = min(a0, w_mm[0][w2]);
+        a1 = min(a1, w_mm[1][w2]);
+        a2 |= w_mm[2][w2];
+        if (w2 < (uint32_t)warp) pre += w_sum[w2];
+      }
+      smin = a0;
+      smax = ~a1;
+      slo = a2;
       if ((int)threadIdx.x < (int)G) {
         col_pre[threadIdx.x] = pre;
         col_src[threadIdx.x] = src - pre;  // staging index of segment element e: col_src[o] + e
       }
       __syncthreads();
     }
-    const uint32_t smin = sh_mm[0], smax = ~sh_mm[1];
+
     uint32_t mode, g = 0;
     if (smin == smax) mode = M_SINGLE;
     else {
-      g = __ffs(sh_mm[2]) - 1;  // every key - min is a multiple of 2^g (same bits [31:21])
+      g = __ffs(slo) - 1;  // every key - min is a multiple of 2^g (same bits [31:21])
       mode = ((smax - smin) >> g) < RMAX ? M_COUNT : (4 * len <= 3 * A.tile ? M_SORT1 : M_BIG);
     }
     const uint32_t org = list == 0 ? smin : smax;  // code origin

@@ -101,7 +101,7 @@ struct Dev {
   unsigned long long *pool;  // [0] head, [1] tail
   unsigned long long *desc[2];  // each: d2h [desc_cap pairs] then h2d [desc_cap pairs]
   // fused path (parity = launch number & 1)
-  unsigned long long *f_hist1;  // [2][4096] level-1 byte histogram
+  unsigned long long *f_hist1;  // [2][4096] level-1 byte histogram, then [2][64] coarse sums
   uint32_t *f_mm1;              // [2][2][4096] per-bucket min key, min complemented key
   unsigned long long *f_hist2;  // [2][1024]
   uint32_t *f_mm2;              // [2][2][1024]

@@ -263,3 +263,28 @@ def test_interaction_grid_pruning_exact(mk):
     w = tg.Workload("grid", n, np.zeros(2, np.int64), np.stack([r for r, _ in steps]),
                     np.stack([k for _, k in steps]), blocks, n * tg.PAGE_BYTES // 3, np.full(3, 30.0, np.float32))
     run_parity(w, transfer=False, multi_kernel=mk)
+
+
+@pytest.mark.parametrize("mk", PATHS)
+def test_tie_cut_word_boundaries_and_writebacks(mk):
+    """The budget cut lands exactly on word / tile boundaries of the d == D* tie group, with
+    zero-size tie agents right at the cut (kept: inclusive prefix <= rem), and dirty resident
+    agents both beyond D* and inside the tie group past the cut (write-back bytes, R13)."""
+    from gpu_harness import run_parity as _rp
+    rng = np.random.default_rng(11)
+    n = 70000  # several fused tiles (~473 agents per CTA at 148 CTAs) and ragged words
+    PG = tg.PAGE_BYTES
+    d = np.where(rng.random(n) < 0.6, 5, rng.integers(1, 40, n))
+    fp = rng.choice([0, 1, 2], n, p=[0.1, 0.6, 0.3]) * PG
+    dirty = (rng.random(n) < 0.5).astype(int)
+    agents = [dict(d=int(d[i]), fp=int(fp[i]), dirty=int(dirty[i])) for i in range(n)]
+    blocks = tg.make_blocks([[tg.KIND_KV] if f else [] for f in fp], [[int(f)] if f else [] for f in fp])
+    rec = rec_of(agents)[None]
+    below = int(fp[(d < 5)].sum())
+    tie_ids = np.nonzero(d == 5)[0]
+    csum = np.cumsum(fp[tie_ids])
+    resident = (rng.random(n) < 0.5).astype(np.uint8)
+    for j in (31, 32 * 40 - 1, len(tie_ids) // 2):  # cut after the j-th tie agent (in id order)
+        budget = below + int(csum[j])
+        w = tg.Workload("tiecut", n, np.array([0]), rec, None, blocks, budget, np.full(3, 50.0, np.float32))
+        _rp(w, transfer=False, multi_kernel=mk, resident_init=resident)
