@@ -500,12 +500,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     for (int j = 0; j < LOAD_BATCH; ++j)  // all loads in flight before any use
       r[j] = n_here ? ld_stream(rec + min(k0 + j * FT + threadIdx.x, last)) : make_uint4(0, 0, 0, 0);
   };
-#ifndef EARLY_V
-#define EARLY_V 1
-#endif
-#if EARLY_V
-  load_batch(0);  // the first batch goes out before the residency words and the shared set-up
-#endif
   const uint32_t *bm_tile = bm_old + base / 32;
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_tile[w] : 0u;
   clear_hist(s.h, NB1);
@@ -516,7 +510,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   uint32_t st = 0;
   unsigned long long zero_b = 0;  // (integer mode: bucket 0 of the histogram instead)
   for (uint32_t k0 = 0; k0 < A.tw * 32; k0 += LOAD_BATCH * FT) {
-    if (k0 != 0 || !EARLY_V) load_batch(k0);
+    load_batch(k0);
 #pragma unroll
     for (int j = 0; j < LOAD_BATCH; ++j) {
       const uint32_t wd = (k0 + j * FT) / 32 + warp;  // this warp's residency word (k & 31 == lane)
