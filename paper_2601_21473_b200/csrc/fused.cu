@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -167,7 +169,11 @@ __device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned
   for (int b = threadIdx.x; b < nb; b += FT) {
     const uint32_t q = nb == NB1 ? slot1(b) : (uint32_t)b;
     const unsigned long long v = ((unsigned long long)h[nb + q] << 16) + h[q];
+#ifdef ROWS_SPARSE_TEST
+    if (v) row[b] = v;
+#else
     row[b] = v;
+#endif
     if (v != 0) {
       atomicAdd(&g_hist[b], v);
       if (g_mm) {
@@ -194,6 +200,18 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long v, uint32_t *acc
     const uint32_t part = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(v >> (16 * k)) & 0xFFFFu);
     if ((threadIdx.x & 31) == 0 && part) atomicAdd(&acc4[k], part);
   }
+}
+// Same for a value < 2^44 in two 22-bit chunks (a warp sums < 2^27 per chunk, a CTA of 32
+// warps < 2^32): half the REDUX of warp_add_u64.  Total: parts_u44(acc2).
+__device__ __forceinline__ void warp_add_u44(unsigned long long v, uint32_t *acc2) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t part = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)(v >> (22 * k)) & 0x3FFFFFu);
+    if ((threadIdx.x & 31) == 0 && part) atomicAdd(&acc2[k], part);
+  }
+}
+__device__ __forceinline__ unsigned long long parts_u44(const uint32_t *acc2) {
+  return (unsigned long long)acc2[0] + ((unsigned long long)acc2[1] << 22);
 }
 __device__ __forceinline__ unsigned long long parts_u64(const uint32_t *acc4) {
   return (unsigned long long)acc4[0] + ((unsigned long long)acc4[1] << 16) + ((unsigned long long)acc4[2] << 32) +
@@ -503,65 +521,86 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   const uint32_t *bm_tile = bm_old + base / 32;
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_tile[w] : 0u;
   clear_hist(s.h, NB1);
-  // 16-bit chunk counters: [0,4) zero-distance bytes, [4,20) P4 sums, [20,24) P3 tie prefix
+  // chunk counters: [0,4) zero-distance bytes, [4,11) P4 sums, [20,24) P3 tie prefix
   __shared__ uint32_t sacc[24];
   if (threadIdx.x < 24) sacc[threadIdx.x] = 0;
   __syncthreads();
   uint32_t st = 0;
   unsigned long long zero_b = 0;  // (integer mode: bucket 0 of the histogram instead)
+  // One record: distance (a1), eligibility (a2), shared-memory state, level-1 histogram.
+  // Compiled four ways: CHECK (a batch that runs past the tile's end: `valid` masks) and FAST
+  // (integer mode, no explicit distances, 32-bit now, no distance copy: the class-0 path with
+  // nothing else live; warps holding other classes still take the general definition).
+  auto record = [&](const uint4 rj, const uint32_t wd, auto check_tag, auto fast_tag) {
+    constexpr bool CHECK = decltype(check_tag)::value, FAST = decltype(fast_tag)::value;
+    const uint32_t k = wd * 32 + lane;
+    const bool valid = CHECK ? k < n_here : true;
+    const bool res = (s.old_w[wd] >> lane) & 1u;
+    const uint32_t ph = rj.z & 3u, cl = (rj.z >> 2) & 3u;
+    float dist, th;
+    if (!FAST && xdist) {  // explicit distances (R19)
+      dist = valid ? explicit_distance_of(rj, st) : 0.0f;
+      th = th0;
+    } else if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {
+      // the warp holds interaction / diffusion / malformed records: general definition
+      dist = valid ? distance_of(rj, now, hop_scale, dint, n_kin, st) : 0.0f;
+      th = (cl & 2u) ? ((cl & 1u) ? 0.0f : th2) : ((cl & 1u) ? th1 : th0);
+    } else {
+      // independent agents only: remaining action ticks, 0 while in an LLM
+      // phase, +inf when idle — the same values distance_of gives for class 0
+      float d_action;
+      if (FAST || now32) {
+        d_action = rj.x > nowl ? __uint2float_rn(rj.x - nowl) : 0.0f;
+      } else {
+        const int64_t remain = (int64_t)rj.x - now;
+        d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
+      }
+      dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
+      th = th0;
+    }
+    const uint32_t bits = valid ? __float_as_uint(dist) : 0u;
+    const bool elig = valid && (res || dist == 0.0f || dist < th);
+    s.keys[k] = bits;
+    s.fp[k] = valid ? rj.y : 0u;
+    if (!FAST && gkeys && valid) gkeys[k] = bits;
+    const uint32_t eb = __ballot_sync(0xFFFFFFFFu, elig);
+    const uint32_t db = __ballot_sync(0xFFFFFFFFu, valid && ((rj.z >> 4) & 1u));
+    if (lane == 0) {
+      s.elig_w[wd] = eb;
+      s.dirty_w[wd] = db;
+    }
+    if (elig) {
+      const uint32_t q = slot1(bits >> 19);
+      atomicAdd(&s.h[q], rj.y & 0xFFFFu);
+      atomicAdd(&s.h[NB1 + q], rj.y >> 16);
+      if (!FAST && !imode) {  // min / max key only where a bucket can hold several distances
+        atomicMin(&s.h[2 * NB1 + q], bits);
+        atomicMin(&s.h[3 * NB1 + q], ~bits);
+      }
+    }
+    if (!FAST && !imode && valid && dist == 0.0f) zero_b += rj.y;
+  };
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  const bool fast = imode && !xdist && now32 && gkeys == nullptr;
   for (uint32_t k0 = 0; k0 < A.tw * 32; k0 += LOAD_BATCH * FT) {
     load_batch(k0);
+    if (k0 + LOAD_BATCH * FT <= n_here) {  // every record of the batch exists (CTA-uniform)
+      if (fast) {
 #pragma unroll
-    for (int j = 0; j < LOAD_BATCH; ++j) {
-      const uint32_t wd = (k0 + j * FT) / 32 + warp;  // this warp's residency word (k & 31 == lane)
-      if (wd >= A.tw) continue;  // warp-uniform
-      const uint32_t k = wd * 32 + lane;
-      const bool valid = k < n_here;
-      const uint4 rj = r[j];
-      const bool res = (s.old_w[wd] >> lane) & 1u;
-      const uint32_t ph = rj.z & 3u, cl = (rj.z >> 2) & 3u;
-      float dist, th;
-      if (xdist) {  // explicit distances (R19)
-        dist = valid ? explicit_distance_of(rj, st) : 0.0f;
-        th = th0;
-      } else if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {
-        // the warp holds interaction / diffusion / malformed records: general definition
-        dist = valid ? distance_of(rj, now, hop_scale, dint, n_kin, st) : 0.0f;
-        th = (cl & 2u) ? ((cl & 1u) ? 0.0f : th2) : ((cl & 1u) ? th1 : th0);
+        for (int j = 0; j < LOAD_BATCH; ++j) record(r[j], (k0 + j * FT) / 32 + warp, F_(), T_());
       } else {
-        // independent agents only: remaining action ticks, 0 while in an LLM
-        // phase, +inf when idle — the same values distance_of gives for class 0
-        float d_action;
-        if (now32) {
-          d_action = rj.x > nowl ? __uint2float_rn(rj.x - nowl) : 0.0f;
-        } else {
-          const int64_t remain = (int64_t)rj.x - now;
-          d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
-        }
-        dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
-        th = th0;
+#pragma unroll
+        for (int j = 0; j < LOAD_BATCH; ++j) record(r[j], (k0 + j * FT) / 32 + warp, F_(), F_());
       }
-      const uint32_t bits = valid ? __float_as_uint(dist) : 0u;
-      const bool elig = valid && (res || dist == 0.0f || dist < th);
-      s.keys[k] = bits;
-      s.fp[k] = valid ? rj.y : 0u;
-      if (gkeys && valid) gkeys[k] = bits;
-      const uint32_t eb = __ballot_sync(0xFFFFFFFFu, elig);
-      const uint32_t db = __ballot_sync(0xFFFFFFFFu, valid && ((rj.z >> 4) & 1u));
-      if (lane == 0) {
-        s.elig_w[wd] = eb;
-        s.dirty_w[wd] = db;
+    } else {
+#pragma unroll
+      for (int j = 0; j < LOAD_BATCH; ++j) {
+        const uint32_t wd = (k0 + j * FT) / 32 + warp;  // this warp's residency word (k & 31 == lane)
+        if (wd >= A.tw) continue;                        // warp-uniform
+        if (fast) record(r[j], wd, T_(), T_());
+        else record(r[j], wd, T_(), F_());
       }
-      if (elig) {
-        const uint32_t q = slot1(bits >> 19);
-        atomicAdd(&s.h[q], rj.y & 0xFFFFu);
-        atomicAdd(&s.h[NB1 + q], rj.y >> 16);
-        if (!imode) {  // min / max key only where a bucket can hold several distances
-          atomicMin(&s.h[2 * NB1 + q], bits);
-          atomicMin(&s.h[3 * NB1 + q], ~bits);
-        }
-      }
-      if (!imode && valid && dist == 0.0f) zero_b += rj.y;
     }
   }
   if (!imode) warp_add_u64(zero_b, sacc);
@@ -762,10 +801,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   uint32_t *off_pf = s.h + 2 * NBL, *off_ev = s.h + 3 * NBL;
   __shared__ uint32_t sh_mpf, sh_mev;
   d2h += wb_pend;
-  warp_add_u64(h2d, sacc + 4);  // (the scan's barriers complete them)
-  warp_add_u64(d2h, sacc + 8);
-  warp_add_u64(tie_kept, sacc + 12);
-  warp_add_u64(n_el, sacc + 16);
+  // (the scan's barriers complete them; per thread: <= 12 agents of < 2^32 bytes each < 2^44;
+  // n_el lives in lane 0 only)
+  warp_add_u44(h2d, sacc + 4);
+  warp_add_u44(d2h, sacc + 6);
+  warp_add_u44(tie_kept, sacc + 8);
+  if (lane == 0 && n_el) atomicAdd(&sacc[10], n_el);
   // This tile's list members in list order (prefetch ascending id, evict descending id) into
   // memb, and the bucket-major offsets of the staging area (one word / bucket per thread:
   // tw <= FT == NBL)
@@ -801,6 +842,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&prof[17], gtimer());  // member lists built
   const uint32_t m_pf = sh_mpf, m_ev = sh_mev;
   // in-CTA rank of every member within its bucket (list order), warp 0 prefetch, warp 1
   // evict, into fp[]
@@ -824,6 +866,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&prof[19], gtimer());  // in-bucket ranks
   // stage (key, id) bucket-major in this tile's range of the staging arrays: bucket b's
   // members at base + off[b] + rank, in list order
   for (uint32_t e = threadIdx.x; e < m_pf + m_ev; e += FT) {
@@ -848,7 +891,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   if (threadIdx.x == 0) atomicMax(&prof[28], gtimer());  // staged, rows published
   if (threadIdx.x < 4) {
-    const unsigned long long v = parts_u64(sacc + 4 + 4 * threadIdx.x);
+    const unsigned long long v = threadIdx.x < 3 ? parts_u44(sacc + 4 + 2 * threadIdx.x) : sacc[10];
     if (v) atomicAdd(&acc[1 + threadIdx.x], v);
   }
   if (threadIdx.x == 0) atomicMax(&prof[12], gtimer());
@@ -939,6 +982,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   unsigned long long dt[4] = {0, 0, 0, 0};  // slot sections (thread 0): segment + columns, gather, scan, place
   for (uint32_t j = c; j < n_slots; j += G) {
     unsigned long long tq = gtimer();
+    // COUNT mode's code counters and per-warp code counts, cleared ahead (ordered by the
+    // barriers below; the previous slot ended with one)
+    for (uint32_t x = threadIdx.x; x < 4 * NBL; x += FT) s.h[x] = 0;            // h_all, h_bef
+    for (uint32_t x = threadIdx.x; x < 4 * NBL; x += FT) s.h[12 * NBL + x] = 0;  // hw
     {  // the segment holding slot j
       const uint32_t g0 = 2 * threadIdx.x;
       const uint32_t a = slot_base[g0], m = slot_base[g0 + 1], z = g0 + 2 < 2 * NBL ? slot_base[g0 + 2] : n_slots;
@@ -1037,12 +1084,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       for (uint32_t e = e0 + threadIdx.x; e < e1; e += FT) out[e] = sv[src_of(e)];
     } else if (mode == M_COUNT) {
       uint32_t *h_all = s.h, *h_bef = s.h + 2 * NBL, *sc = s.h + 4 * NBL, *sid = s.h + 5 * NBL;
-      const uint32_t R = RMAX;
-      for (uint32_t x = threadIdx.x; x < R; x += FT) {
-        h_all[x] = 0;
-        h_bef[x] = 0;
-      }
-      __syncthreads();
       for (uint32_t e00 = 0; e00 < len; e00 += 4 * FT) {
         uint32_t key[4], id[4];
 #pragma unroll
@@ -1070,22 +1111,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       }
       __syncthreads();
       lap(1);
-      {  // exclusive scan of the code counts (2 bins per thread)
-        const uint32_t v0 = h_all[2 * threadIdx.x], v1 = h_all[2 * threadIdx.x + 1];
-        const uint32_t ex = block_excl_scan<uint32_t, FT>(v0 + v1, &sh_tmp);
-        h_all[2 * threadIdx.x] = ex;
-        h_all[2 * threadIdx.x + 1] = ex + v0;
-      }
-      __syncthreads();
-      lap(2);
       const uint32_t rseg = ((smax - smin) >> g) + 1, nsl = e1 - e0;
       if (rseg <= 128) {
         // position = start of the code + members before the slice + members of earlier warps
-        // of the slice + earlier lanes of the warp (all warps at once: per-warp code counts)
-        uint32_t *hw = s.h + 12 * NBL;  // [32 warps][128 codes]
+        // of the slice + earlier lanes of the warp (all warps at once: per-warp code counts);
+        // the code starts are scanned by the last warp meanwhile (nsl <= CH: it holds no slice)
+        uint32_t *hw = s.h + 12 * NBL;  // [32 warps][128 codes], cleared at the slot's start
         const uint32_t nw = (nsl + 31) / 32;
-        for (uint32_t x = threadIdx.x; x < nw * 128; x += FT) hw[x] = 0;
-        __syncthreads();
         const uint32_t x = warp * 32 + lane;
         const bool on = x < nsl;
         uint32_t code = 0xFFFFFFFFu, rin = 0;
@@ -1094,8 +1126,22 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
           const uint32_t peers = __match_any_sync(0xFFFFFFFFu, code);
           rin = __popc(peers & lanemask_lt());
           if (on && rin == 0) hw[warp * 128 + code] = __popc(peers);
+        } else if (warp == FWARPS - 1) {
+          uint32_t v[4], t = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            v[i] = h_all[4 * lane + i];
+            t += v[i];
+          }
+          uint32_t ex = warp_incl_scan(t) - t;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            h_all[4 * lane + i] = ex;
+            ex += v[i];
+          }
         }
         __syncthreads();
+        lap(2);
         for (uint32_t c2 = threadIdx.x; c2 < rseg; c2 += FT) {  // exclusive prefix over the warps
           uint32_t run = 0;
           for (uint32_t w2 = 0; w2 < nw; ++w2) {
@@ -1106,16 +1152,26 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         }
         __syncthreads();
         if (on) out[h_all[code] + h_bef[code] + hw[warp * 128 + code] + rin] = sid[x];
-      } else if (warp == 0) {  // the slice in order, one warp: position = start + earlier members with the same code
-        for (uint32_t x0 = 0; x0 < e1 - e0; x0 += 32) {
-          const uint32_t x = x0 + lane;
-          const bool on = x < e1 - e0;
-          const uint32_t code = on ? sc[x] : 0xFFFFFFFFu;
-          const uint32_t peers = __match_any_sync(0xFFFFFFFFu, code);
-          if (on) out[h_all[code] + h_bef[code] + __popc(peers & lanemask_lt())] = sid[x];
-          __syncwarp();
-          if (on && (peers & lanemask_lt()) == 0) h_bef[code] += __popc(peers);
-          __syncwarp();
+      } else {
+        {  // exclusive scan of the code counts (2 bins per thread)
+          const uint32_t v0 = h_all[2 * threadIdx.x], v1 = h_all[2 * threadIdx.x + 1];
+          const uint32_t ex = block_excl_scan<uint32_t, FT>(v0 + v1, &sh_tmp);
+          h_all[2 * threadIdx.x] = ex;
+          h_all[2 * threadIdx.x + 1] = ex + v0;
+        }
+        __syncthreads();
+        lap(2);
+        if (warp == 0) {  // the slice in order, one warp: position = start + earlier members with the same code
+          for (uint32_t x0 = 0; x0 < e1 - e0; x0 += 32) {
+            const uint32_t x = x0 + lane;
+            const bool on = x < e1 - e0;
+            const uint32_t code = on ? sc[x] : 0xFFFFFFFFu;
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, code);
+            if (on) out[h_all[code] + h_bef[code] + __popc(peers & lanemask_lt())] = sid[x];
+            __syncwarp();
+            if (on && (peers & lanemask_lt()) == 0) h_bef[code] += __popc(peers);
+            __syncwarp();
+          }
         }
       }
     } else {  // M_SORT1 / M_BIG: the whole segment

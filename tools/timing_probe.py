@@ -56,7 +56,7 @@ for mode in ("eager", "graph", "eager_sync"):
             if k < 4:
                 r = lambda q: round((int(st[q]) - int(st[0])) / 1e3, 2) if st[q] else None
                 print("us: cta0 P1end", r(3), "B1", r(4), "sel", r(9), "P3", r(10), "P4end", r(5), "B4", r(6),
-                      "P5tab", r(7), "| max over CTAs: P1end", r(11), "P3end", r(14), "P4loop", r(27),  "P4rows", r(28),
+                      "P5tab", r(7), "| max over CTAs: P1end", r(11), "P3end", r(14), "P4loop", r(27), "P4lists", r(17), "P4ranks", r(19), "P4rows", r(28),
                       "P4end", r(12), "B4max", r(30), "P5tot", r(31), "P5tables", r(13), "end", r(1), "| slots", int(st[16]), "max_sorted_seg", int(st[18]),
                       "slot_loop_ns_max", int(st[21]), "sections(seg+col, gather, scan, place) ns max", [int(st[q]) for q in (22, 23, 24, 29)],
                       "| P1loop", r(25), "P1pub", r(26), "| last CTA start", r(15))
