@@ -38,7 +38,7 @@ constexpr int FWARPS = FT / 32;
 constexpr int NB1 = 4096;  // level-1 buckets: distance bits [30:19]
 constexpr int NBL = 1024;  // list-sort buckets: distance bits [30:21]
 #ifndef LOAD_BATCH_V
-#define LOAD_BATCH_V 4
+#define LOAD_BATCH_V 2
 #endif
 constexpr int LOAD_BATCH = LOAD_BATCH_V;  // records in flight per thread in P1
 
@@ -169,11 +169,7 @@ __device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned
   for (int b = threadIdx.x; b < nb; b += FT) {
     const uint32_t q = nb == NB1 ? slot1(b) : (uint32_t)b;
     const unsigned long long v = ((unsigned long long)h[nb + q] << 16) + h[q];
-#ifdef ROWS_SPARSE_TEST
-    if (v) row[b] = v;
-#else
     row[b] = v;
-#endif
     if (v != 0) {
       atomicAdd(&g_hist[b], v);
       if (g_mm) {
@@ -507,16 +503,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   // rounded to nearest as __ll2float_rn above
   const bool now32 = now >= 0 && now <= 0xFFFFFFFFll;
   const uint32_t nowl = (uint32_t)now;
-  // The tile is streamed in batches of LOAD_BATCH records per thread, all loads of a batch in
-  // flight before any use (measured on B200: 2-4 per thread, within noise; deeper batches and a rolling
-  // refill, profiles/r01_v8_ab.log).  Lanes past the tile's end load its last record (no
-  // zero-fill) and are masked by `valid`.
+  // The tile is streamed in batches of LOAD_BATCH records per thread, double-buffered (two
+  // batches in flight).  Measured on B200 (profiles/r01_v8_ab_*.log, r01_v9_ab_dbuf.log): a
+  // per-slot rolling refill and deeper single batches are slower.  Lanes past the tile's end
+  // load its last record (no zero-fill) and are masked by `valid`.
   const uint32_t last = n_here ? n_here - 1 : 0u;
   uint4 r[LOAD_BATCH];
-  auto load_batch = [&](uint32_t k0) {
+  auto load_into = [&](uint4 (&rr)[LOAD_BATCH], uint32_t k0) {
 #pragma unroll
-    for (int j = 0; j < LOAD_BATCH; ++j)  // all loads in flight before any use
-      r[j] = n_here ? ld_stream(rec + min(k0 + j * FT + threadIdx.x, last)) : make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < LOAD_BATCH; ++j)  // all loads of a batch in flight before any use
+      rr[j] = n_here ? ld_stream(rec + min(k0 + j * FT + threadIdx.x, last)) : make_uint4(0, 0, 0, 0);
   };
   const uint32_t *bm_tile = bm_old + base / 32;
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_tile[w] : 0u;
@@ -583,25 +579,36 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   using T_ = std::true_type;
   using F_ = std::false_type;
   const bool fast = imode && !xdist && now32 && gkeys == nullptr;
-  for (uint32_t k0 = 0; k0 < A.tw * 32; k0 += LOAD_BATCH * FT) {
-    load_batch(k0);
+  auto batch = [&](uint4 (&rr)[LOAD_BATCH], uint32_t k0) {
     if (k0 + LOAD_BATCH * FT <= n_here) {  // every record of the batch exists (CTA-uniform)
       if (fast) {
 #pragma unroll
-        for (int j = 0; j < LOAD_BATCH; ++j) record(r[j], (k0 + j * FT) / 32 + warp, F_(), T_());
+        for (int j = 0; j < LOAD_BATCH; ++j) record(rr[j], (k0 + j * FT) / 32 + warp, F_(), T_());
       } else {
 #pragma unroll
-        for (int j = 0; j < LOAD_BATCH; ++j) record(r[j], (k0 + j * FT) / 32 + warp, F_(), F_());
+        for (int j = 0; j < LOAD_BATCH; ++j) record(rr[j], (k0 + j * FT) / 32 + warp, F_(), F_());
       }
     } else {
 #pragma unroll
       for (int j = 0; j < LOAD_BATCH; ++j) {
         const uint32_t wd = (k0 + j * FT) / 32 + warp;  // this warp's residency word (k & 31 == lane)
         if (wd >= A.tw) continue;                        // warp-uniform
-        if (fast) record(r[j], wd, T_(), T_());
-        else record(r[j], wd, T_(), F_());
+        if (fast) record(rr[j], wd, T_(), T_());
+        else record(rr[j], wd, T_(), F_());
       }
     }
+  };
+  // two batches in flight: the next one's loads go out before the current one is processed
+  // (measured: P1 loop 6.0 vs 6.3 us with single batches, profiles/r01_v9_ab_dbuf.log)
+  uint4 r2[LOAD_BATCH];
+  const uint32_t BS = LOAD_BATCH * FT, nk = A.tw * 32;
+  load_into(r, 0);
+  for (uint32_t k0 = 0; k0 < nk; k0 += 2 * BS) {
+    if (k0 + BS < nk) load_into(r2, k0 + BS);
+    batch(r, k0);
+    if (k0 + BS >= nk) break;
+    if (k0 + 2 * BS < nk) load_into(r, k0 + 2 * BS);
+    batch(r2, k0 + BS);
   }
   if (!imode) warp_add_u64(zero_b, sacc);
   __syncthreads();
@@ -800,11 +807,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   // tw <= FT == NBL)
   uint32_t *off_pf = s.h + 2 * NBL, *off_ev = s.h + 3 * NBL;
   __shared__ uint32_t sh_mpf, sh_mev;
-  d2h += wb_pend;
   // (the scan's barriers complete them; per thread: <= 12 agents of < 2^32 bytes each < 2^44;
   // n_el lives in lane 0 only)
   warp_add_u44(h2d, sacc + 4);
-  warp_add_u44(d2h, sacc + 6);
   warp_add_u44(tie_kept, sacc + 8);
   if (lane == 0 && n_el) atomicAdd(&sacc[10], n_el);
   // This tile's list members in list order (prefetch ascending id, evict descending id) into
@@ -843,6 +848,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&prof[17], gtimer());  // member lists built
+  // the write-back bytes loads (issued in the word loop) were hidden behind the scan; the
+  // barrier after the ranks completes the sum
+  d2h += wb_pend;
+  warp_add_u44(d2h, sacc + 6);
   const uint32_t m_pf = sh_mpf, m_ev = sh_mev;
   // in-CTA rank of every member within its bucket (list order), warp 0 prefetch, warp 1
   // evict, into fp[]
@@ -982,10 +991,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   unsigned long long dt[4] = {0, 0, 0, 0};  // slot sections (thread 0): segment + columns, gather, scan, place
   for (uint32_t j = c; j < n_slots; j += G) {
     unsigned long long tq = gtimer();
-    // COUNT mode's code counters and per-warp code counts, cleared ahead (ordered by the
-    // barriers below; the previous slot ended with one)
-    for (uint32_t x = threadIdx.x; x < 4 * NBL; x += FT) s.h[x] = 0;            // h_all, h_bef
-    for (uint32_t x = threadIdx.x; x < 4 * NBL; x += FT) s.h[12 * NBL + x] = 0;  // hw
     {  // the segment holding slot j
       const uint32_t g0 = 2 * threadIdx.x;
       const uint32_t a = slot_base[g0], m = slot_base[g0 + 1], z = g0 + 2 < 2 * NBL ? slot_base[g0 + 2] : n_slots;
@@ -1019,6 +1024,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
           lo = m2;
         }
       }
+      // COUNT mode's code counters and per-warp code counts, cleared while the column loads
+      // are in flight (ordered by the barriers below; the previous slot ended with one)
+      for (uint32_t x = threadIdx.x; x < 4 * NBL; x += FT) s.h[x] = 0;            // h_all, h_bef
+      for (uint32_t x = threadIdx.x; x < 4 * NBL; x += FT) s.h[12 * NBL + x] = 0;  // hw
       const uint32_t nwg = (G + 31) / 32;
       if ((uint32_t)warp < nwg) {
         incl = warp_incl_scan(cnt);
