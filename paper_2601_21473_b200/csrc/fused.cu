@@ -718,8 +718,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   for (int b = threadIdx.x; b < 4 * NBL; b += FT) mm_l[b] = 0xFFFFFFFFu;
   __syncthreads();
-  unsigned long long h2d = 0, d2h = 0, tie_kept = 0;
-  uint32_t n_el = 0, wb_pend = 0;  // wb_pend: write-back bytes load in flight (added one use later)
+  unsigned long long h2d = 0, tie_kept = 0;
+  uint32_t n_el = 0;
 #pragma unroll 2
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
@@ -769,10 +769,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         atomicOr(&lor_l[bk], key & 0x1FFFFFu);
       }
       if ((evw >> lane) & 1u) {
-        if ((s.dirty_w[w] >> lane) & 1u) {  // R13: write-back bytes of a dirty evicted agent
-          d2h += wb_pend;
-          wb_pend = d.wb_bytes[base + k];
-        }
         atomicAdd(&cnt_ev[bk], 1u);
         atomicMin(&mm_l[2 * NBL + bk], key);
         atomicMin(&mm_l[3 * NBL + bk], ~key);
@@ -848,19 +844,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&prof[17], gtimer());  // member lists built
-  // the write-back bytes loads (issued in the word loop) were hidden behind the scan; the
-  // barrier after the ranks completes the sum
-  d2h += wb_pend;
-  warp_add_u44(d2h, sacc + 6);
   const uint32_t m_pf = sh_mpf, m_ev = sh_mev;
-  // in-CTA rank of every member within its bucket (list order), warp 0 prefetch, warp 1
-  // evict, into fp[]
+  // staging slot of every member (bucket start + rank within its bucket in list order), warp
+  // 0 prefetch, warp 1 evict, into fp[]; the bucket offsets serve as cursors (each ends at
+  // its bucket's end: start = off - cnt)
   if (warp < 2) {
     const uint32_t *mem = s.memb + (warp == 0 ? 0 : m_pf);
     const uint32_t m = warp == 0 ? m_pf : m_ev;
-    uint32_t *run = warp == 0 ? s.h + 4 * NBL : s.h + 5 * NBL;
-    for (uint32_t b = lane; b < NBL; b += 32) run[b] = 0;
-    __syncwarp();
+    uint32_t *run = warp == 0 ? off_pf : off_ev;
     for (uint32_t e0 = 0; e0 < m; e0 += 32) {
       const uint32_t e = e0 + lane;
       const bool on = e < m;
@@ -881,39 +872,38 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   for (uint32_t e = threadIdx.x; e < m_pf + m_ev; e += FT) {
     const uint32_t k = s.memb[e];
     const uint32_t key = s.keys[k];
-    const uint32_t bk = key >> 21;
     const uint32_t id = (uint32_t)(p.shard_begin + base + k);
     if (e < m_pf) {
-      const uint64_t slot = base + off_pf[bk] + s.fp[e];
+      const uint64_t slot = base + s.fp[e];
       d.sort_ka[slot] = key;
       d.sort_va[slot] = id;
     } else {
-      const uint64_t slot = base + off_ev[bk] + s.fp[e];
+      const uint64_t slot = base + s.fp[e];
       d.f_sk2[slot] = key;
       d.f_sv2[slot] = id;
     }
   }
   {  // rows: offset << 16 | count (tile <= FUSED_MAX_TILE < 2^16)
     const int b = threadIdx.x;  // NBL == FT
-    d.f_cta_cpf[(uint64_t)c * NBL + b] = (off_pf[b] << 16) | cnt_pf[b];
-    d.f_cta_cev[(uint64_t)c * NBL + b] = (off_ev[b] << 16) | cnt_ev[b];
+    d.f_cta_cpf[(uint64_t)c * NBL + b] = ((off_pf[b] - cnt_pf[b]) << 16) | cnt_pf[b];
+    d.f_cta_cev[(uint64_t)c * NBL + b] = ((off_ev[b] - cnt_ev[b]) << 16) | cnt_ev[b];
   }
   if (threadIdx.x == 0) atomicMax(&prof[28], gtimer());  // staged, rows published
   if (threadIdx.x < 4) {
     const unsigned long long v = threadIdx.x < 3 ? parts_u44(sacc + 4 + 2 * threadIdx.x) : sacc[10];
-    if (v) atomicAdd(&acc[1 + threadIdx.x], v);
+    if (v && threadIdx.x != 1) atomicAdd(&acc[1 + threadIdx.x], v);  // ([2] write-back bytes: end of P5)
   }
+  if (c == 0 && threadIdx.x == 0) d.header[H_D2H] = 0ull;  // (summed by every CTA after B4)
   if (threadIdx.x == 0) atomicMax(&prof[12], gtimer());
   if (c == 0 && threadIdx.x == 0) prof[5] = gtimer();
   grid.sync();
   if (c == 0 && threadIdx.x == 0) prof[6] = gtimer();
   if (c == 0 && threadIdx.x == 32) {  // header (CTA 0, warp 1): the accumulators are complete; loads first
-    const unsigned long long a0 = acc[0], a1 = acc[1], a2 = acc[2], a3 = acc[3], a4 = acc[4], a5 = acc[5];
+    const unsigned long long a0 = acc[0], a1 = acc[1], a3 = acc[3], a4 = acc[4], a5 = acc[5];
     const uint32_t st0 = d.state->status;  // + BAD_KIN/BAD_RECORD of k_int_compact
     unsigned long long *H = d.header;
     const unsigned long long seq = H[H_SEQ];
     H[H_H2D] = a1;
-    H[H_D2H] = a2;
     H[H_CUT_BITS] = all_fit ? 0xFFFFFFFFull : dstar;
     H[H_CUT_REM] = sel.rem;
     H[H_KEPT] = (p.budget - sel.rem) + (all_fit ? 0ull : a3);
@@ -982,6 +972,22 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   __syncthreads();
   const uint32_t n_slots = sh_ns;
+  // R13 write-back bytes of this tile's dirty evicted agents: loads issued now (up to two per
+  // word in registers), summed after the slot loop (their latency hides behind P5) and added
+  // to the header by a reduction
+  uint32_t wbm = 0, wb0 = 0, wb1 = 0;
+  if (threadIdx.x < A.tw) {
+    wbm = s.ev_w[threadIdx.x] & s.dirty_w[threadIdx.x];
+    const uint32_t *wbw = d.wb_bytes + base + 32 * threadIdx.x;
+    if (wbm) {
+      wb0 = wbw[__ffs(wbm) - 1];
+      wbm &= wbm - 1;
+    }
+    if (wbm) {
+      wb1 = wbw[__ffs(wbm) - 1];
+      wbm &= wbm - 1;
+    }
+  }
   if (c == 0 && threadIdx.x == 0) prof[16] = n_slots;
   if (threadIdx.x == 0) atomicMax(&prof[13], gtimer());  // P5 tables
   if (c == 0 && threadIdx.x == 0) prof[7] = gtimer();
@@ -1217,6 +1223,19 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     atomicMax(&prof[23], dt[1]);
     atomicMax(&prof[24], dt[2]);
     atomicMax(&prof[29], dt[3]);
+  }
+  {  // write-back bytes: the CTA's sum into acc[2]; the last CTA to arrive writes the header
+    unsigned long long d2h = (unsigned long long)wb0 + wb1;
+    while (wbm) {  // (rare: a word with more than two dirty evicted agents)
+      d2h += d.wb_bytes[base + 32 * threadIdx.x + __ffs(wbm) - 1];
+      wbm &= wbm - 1;
+    }
+    warp_add_u44(d2h, sacc + 6);  // (sacc[6, 8) are free since P4)
+    __syncthreads();
+    if (threadIdx.x == 0) {  // a reduction into the header (zeroed by CTA 0 before B4): no wait
+      const unsigned long long v = parts_u44(sacc + 6);
+      if (v) atomicAdd(&d.header[H_D2H], v);
+    }
   }
   if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
 }
