@@ -232,10 +232,12 @@ scalesim_status scalesim_join(scalesim_ctx *ctx);
  * multi-kernel path (world > 1, SCALESIM_F_MULTI_KERNEL, or tiles too large), -1 on NULL. */
 int scalesim_fused(const scalesim_ctx *ctx);
 
-/* Device pointer to 16 uint64 %globaltimer stamps (ns) written by the fused plan kernel:
- * [0] earliest CTA start (atomicMin), [1] latest CTA end (atomicMax), [2..8] phase boundaries
- * seen by CTA 0.  The caller resets [0] to UINT64_MAX and [1] to 0 between launches it wants
- * to time.  Profiling aid; NULL for a NULL context. */
+/* Device pointer to 64 uint64 %globaltimer stamps (ns) written by the fused plan kernel:
+ * [0] earliest CTA start past the dependency wait (atomicMin), [1] latest CTA end
+ * (atomicMax), [2..10] and [32..35] phase boundaries seen by CTA 0, [11..31] latest CTA per
+ * phase (atomicMax) and per-slot section times (tools/timing_probe.py names them).  The caller
+ * resets [0] to UINT64_MAX and the rest to 0 between launches it wants to time.  Profiling
+ * aid; NULL for a NULL context. */
 const uint64_t *scalesim_profile_stamps(const scalesim_ctx *ctx);
 
 /* Fine-grained distance assignment for shared memory objects ("the invocation

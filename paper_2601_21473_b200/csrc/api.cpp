@@ -109,7 +109,7 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_sk3 = take(4 * n1);
   L.f_sv3 = take(4 * n1);
   L.f_bar = take(64);
-  L.f_prof = take(256);
+  L.f_prof = take(512);
   L.total = off;
   return L;
 }

@@ -224,13 +224,15 @@ struct Sel {
 // b >> 6), then the 64 buckets of the coarse bucket where the running byte sum crosses the
 // budget.  Same result as select_level(level 1); no block-wide scan.
 __device__ void select_level1_warp(const unsigned long long *g_hist, const unsigned long long *g_coarse,
-                                   const uint32_t *g_mm, unsigned long long budget, Sel &sel, bool imode) {
+                                   const uint32_t *g_mm, unsigned long long budget, Sel &sel, bool imode,
+                                   unsigned long long *prof) {
   __shared__ unsigned long long s1_prev, s1_tot;
   __shared__ uint32_t s1_b, s1_min, s1_nmax;
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     const ulonglong2 cc = reinterpret_cast<const ulonglong2 *>(g_coarse)[lane];
     const unsigned long long incl = warp_incl_scan(cc.x + cc.y), ex = incl - cc.x - cc.y;
+    if (blockIdx.x == 0 && lane == 0) prof[33] = gtimer();  // coarse sums loaded and scanned
     const uint32_t m1 = __ballot_sync(0xFFFFFFFFu, incl > budget);
     const uint32_t m0 = __ballot_sync(0xFFFFFFFFu, ex + cc.x > budget);
     if (m1 == 0) {  // every eligible agent fits
@@ -254,6 +256,7 @@ __device__ void select_level1_warp(const unsigned long long *g_hist, const unsig
         nx1 = nx.y;
       }
       const unsigned long long fi = below + warp_incl_scan(f.x + f.y), fe = fi - f.x - f.y;
+      if (blockIdx.x == 0 && lane == 0) prof[34] = gtimer();  // fine buckets loaded and scanned
       const uint32_t n1 = __ballot_sync(0xFFFFFFFFu, fi > budget);  // nonzero: the coarse bucket crosses
       const uint32_t n0 = __ballot_sync(0xFFFFFFFFu, fe + f.x > budget);
       const int Lf = __ffs(n1) - 1;
@@ -267,6 +270,7 @@ __device__ void select_level1_warp(const unsigned long long *g_hist, const unsig
     }
   }
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) prof[35] = gtimer();  // select barrier passed
   const uint32_t b = s1_b;
   if (b == 0xFFFFFFFFu) {
     sel.all_fit = 1;
@@ -652,8 +656,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   const uint32_t *mm1 = d.f_mm1 + 2 * NB1 * par;
   Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 1, 0};
+  if (c == 0 && threadIdx.x == 0) prof[32] = gtimer();  // other parity cleared
   select_level1_warp(d.f_hist1 + NB1 * par, d.f_hist1 + 2 * NB1 + 64 * par, imode ? nullptr : mm1, p.budget, sel,
-                     imode);
+                     imode, prof);
   for (int level = 2; level <= 3 && !sel.done; ++level) {
     const int hi_shift = level == 2 ? 19 : 9, shift = level == 2 ? 9 : 0;
     const int nb = level == 2 ? 1024 : 512;

@@ -188,12 +188,12 @@ class Planner:
     def stamps(self, reset: bool = False) -> np.ndarray:
         """The fused kernel's %globaltimer stamps (ns), see scalesim_profile_stamps."""
         ptr = int(self.lib.scalesim_profile_stamps(self.ctx))
-        v = self._read(ptr, 256).view(np.uint64).copy()
+        v = self._read(ptr, 512).view(np.uint64).copy()
         if reset:
             off = ptr - self.workspace.data_ptr()
-            init = np.zeros(32, np.uint64)
+            init = np.zeros(64, np.uint64)
             init[0] = np.iinfo(np.uint64).max
-            self.workspace[off:off + 256].copy_(torch.from_numpy(init.view(np.uint8)))
+            self.workspace[off:off + 512].copy_(torch.from_numpy(init.view(np.uint8)))
             torch.cuda.synchronize(self.device)
         return v
 
