@@ -59,21 +59,34 @@ class ClockSampler:
         except Exception:
             self.N = None
 
-    def _run(self):
+    def sample(self):
         N = self.N
-        names = {getattr(N, k): k for k in dir(N) if k.startswith("nvmlClocksEventReason") or
-                 k.startswith("nvmlClocksThrottleReason")}
+        if N is None:
+            return
+        if not hasattr(self, "_names"):
+            self._names = {getattr(N, k): k for k in dir(N) if k.startswith("nvmlClocksEventReason") or
+                           k.startswith("nvmlClocksThrottleReason")}
+        try:
+            self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
+                N, "nvmlDeviceGetCurrentClocksEventReasons") else N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            for bit, name in self._names.items():
+                if isinstance(bit, int) and bit and (r & bit) == bit and bit & (bit - 1) == 0:
+                    self.reasons.add(name.replace("nvmlClocksEventReason", "").replace(
+                        "nvmlClocksThrottleReason", ""))
+        except Exception:
+            pass
+
+    def poll_until(self, event):
+        """Sample from the calling thread until `event` (recorded at the end of the timed
+        region) completes: the host enqueues ahead, so the GPU is still in the region."""
+        while not event.query():
+            self.sample()
+            time.sleep(0.0005)
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
-                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
-                    N, "nvmlDeviceGetCurrentClocksEventReasons") else N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                for bit, name in names.items():
-                    if isinstance(bit, int) and bit and (r & bit) == bit and bit & (bit - 1) == 0:
-                        self.reasons.add(name.replace("nvmlClocksEventReason", "").replace(
-                            "nvmlClocksThrottleReason", ""))
-            except Exception:
-                pass
+            self.sample()
             time.sleep(0.002)
 
     def __enter__(self):
@@ -555,6 +568,7 @@ def main():
         steps(t_base)
         t1.record(pl.stream)
         launches = pl.launch_count() - lc0
+        sampler.poll_until(t1)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()

@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -742,6 +743,11 @@ extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32
   while (i0 < n) {
     uint32_t k = n - i0 < sms ? n - i0 : sms;
     if (k > (uint32_t)FUSED_MAX_BATCH) k = FUSED_MAX_BATCH;
+    {  // experiment knob: cap on instances per launch (tools/ only)
+      static const char *cap_s = std::getenv("SCALESIM_BATCH_CAP");
+      const uint32_t cap = cap_s ? (uint32_t)std::atoi(cap_s) : 0u;
+      if (cap && k > cap) k = cap;
+    }
     uint32_t gsize, tile;
     while (true) {
       gsize = sms / k;
