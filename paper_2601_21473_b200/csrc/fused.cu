@@ -70,6 +70,7 @@ struct GridBar {
   unsigned int n;  // CTAs of this instance
   __device__ __forceinline__ void sync() {
     __syncthreads();
+    if (n == 1) return;  // a single-CTA group: the CTA barrier orders its global accesses
     if (threadIdx.x == 0) {
       ++k;
       red_release(bar, 1u);
@@ -976,7 +977,30 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     d.header[H_N_EV] = nev;
   }
   __syncthreads();
-  const uint32_t n_slots = sh_ns;
+  // A single-CTA instance (G == 1, the batched replicas of C5) holds every list member in its
+  // own staging area, bucket-major (buckets ascending) and in list order within a bucket: one
+  // stable radix sort per list by key (prefetch) or complemented key (evict) gives the
+  // (distance, id) order directly, instead of one slot per nonempty list bucket.
+  const bool one_cta = G == 1 && 4 * max(npf, nev) <= 3 * A.tile;
+  if (one_cta) {
+#pragma unroll 1
+    for (uint32_t list = 0; list < 2; ++list) {
+      const uint32_t len = list == 0 ? npf : nev;
+      if (len == 0) continue;
+      const uint32_t *sk = list == 0 ? d.sort_ka : d.f_sk2, *sv = list == 0 ? d.sort_va : d.f_sv2;
+      uint32_t *ka = s.keys, *ia = ka + len, *kb = ka + 2 * len, *ib = ka + 3 * len;  // 4 len <= 3 tile
+      for (uint32_t e = threadIdx.x; e < len; e += FT) {
+        ka[e] = list == 0 ? sk[e] : ~sk[e];
+        ia[e] = sv[e];
+      }
+      __syncthreads();
+      cta_sort_pairs(ka, ia, kb, ib, len, s.h);  // stable: ties keep the staging (list) order
+      uint32_t *out = list == 0 ? d.pf_ids : d.ev_ids;
+      for (uint32_t e = threadIdx.x; e < len; e += FT) out[e] = ia[e];
+      __syncthreads();
+    }
+  }
+  const uint32_t n_slots = one_cta ? 0u : sh_ns;
   // R13 write-back bytes of this tile's dirty evicted agents: loads issued now (up to two per
   // word in registers), summed after the slot loop (their latency hides behind P5) and added
   // to the header by a reduction

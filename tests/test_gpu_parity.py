@@ -288,3 +288,47 @@ def test_tie_cut_word_boundaries_and_writebacks(mk):
         budget = below + int(csum[j])
         w = tg.Workload("tiecut", n, np.array([0]), rec, None, blocks, budget, np.full(3, 50.0, np.float32))
         _rp(w, transfer=False, multi_kernel=mk, resident_init=resident)
+
+
+def test_batch_single_cta_instances():
+    """scalesim_step_batch with >= 75 instances gives each instance one CTA (the C5 launch
+    shape on one GPU): its lists come from the single-CTA radix-sort path, or from the slot
+    path when a list exceeds 3/4 of the tile (theta = inf, budget 90% at the first step)."""
+    import torch
+    from paper_2601_21473_b200.planner import Planner, step_batch
+    n, steps, k = 1500, 6, 80
+    ws = [tg.config_c5(replica=r, budget_pct=10, steps=steps, n=n) for r in range(8)]
+    stream = torch.cuda.Stream()
+    inst = []
+    for i in range(k):
+        w = ws[i % 8]
+        pct = 90 if i >= k - 2 else 10 * (1 + i % 9)
+        theta = np.full(3, np.inf, np.float32) if i >= k - 2 else w.theta
+        b = w.blocks
+        budget = int(w.footprint.sum()) * pct // 100
+        pl = Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, theta, transfer=False,
+                     stream=stream)
+        inst.append(dict(pl=pl, w=w, budget=budget, theta=theta, res=np.zeros(n, np.uint8)))
+    for s in range(steps):
+        for it in inst:
+            it["pl"].set_records(it["w"].rec[s])
+        step_batch([it["pl"] for it in inst], int(ws[0].now[s]))
+        for i, it in enumerate(inst):
+            w = it["w"]
+            hdr = it["pl"].sync()
+            d, _ = oracle.score(w.rec[s], None, int(w.now[s]))
+            p = oracle.plan(w.rec[s], d, it["res"], it["theta"], it["budget"])
+            pf, ev = it["pl"].lists(hdr)
+            assert np.array_equal(pf, p["prefetch"]) and np.array_equal(ev, p["evict"]), (s, i)
+            assert np.array_equal(it["pl"].resident(), p["resident"]), (s, i)
+            assert hdr["cut_bits"] == p["cut_bits"] and hdr["kept_bytes"] == p["kept_bytes"], (s, i)
+            assert hdr["bytes_h2d"] == p["bytes_h2d"], (s, i)
+            dirty = ((w.rec[s][:, 2] >> 4) & 1).astype(bool)  # R13 write-back bytes of dirty evicted agents
+            bl = w.blocks
+            wb = sum(int(bl.blk_size[int(bl.blk_ptr[a]):int(bl.blk_ptr[a + 1])][
+                bl.blk_kind[int(bl.blk_ptr[a]):int(bl.blk_ptr[a + 1])] != tg.KIND_LORA].astype(np.int64).sum())
+                for a in p["evict"] if dirty[a])
+            assert hdr["bytes_d2h"] == wb, (s, i)
+            it["res"] = p["resident"]
+    for it in inst:
+        it["pl"].close()
