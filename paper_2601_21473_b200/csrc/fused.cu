@@ -70,7 +70,9 @@ struct GridBar {
   unsigned int n;  // CTAs of this instance
   __device__ __forceinline__ void sync() {
     __syncthreads();
-    if (n == 1) return;  // a single-CTA group: the CTA barrier orders its global accesses
+    // a single-CTA group: the CTA barrier orders its threads' global accesses (its atomics
+    // happen before the loads after it in causality order, PTX memory model)
+    if (n == 1) return;
     if (threadIdx.x == 0) {
       ++k;
       red_release(bar, 1u);
@@ -921,6 +923,58 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   }
   if (threadIdx.x == 0) atomicMax(&prof[30], gtimer());  // B4 passed (last CTA)
 
+  // A single-CTA instance (G == 1, the batched replicas of C5) holds every list member in its
+  // own staging area, bucket-major (buckets ascending) and in list order within a bucket,
+  // with P4's per-bucket counts, end offsets and min / max keys still in s.h: each member's
+  // list position follows from its segment directly (single-valued segment: its staging
+  // rank; otherwise by counting within the segment when every such segment holds <= 128
+  // members), else one stable radix sort per list — instead of one P5 slot per nonempty
+  // list bucket (tools/c5_probe.py: 30 slots of ~2 us for 473 members).
+  // (batched launches only: a single context's group spans every SM)
+  const bool one_cta = MAXB > 1 && G == 1 && 4 * max(m_pf, m_ev) <= 3 * A.tile;
+  if constexpr (MAXB > 1) if (one_cta) {
+    const uint32_t *mm = s.h + 10 * NBL;  // [4][NBL]: prefetch min, ~max, evict min, ~max
+    bool big = false;
+    for (uint32_t b = threadIdx.x; b < NBL; b += FT)
+      big |= (s.h[b] > 128u && mm[b] != ~mm[NBL + b]) || (s.h[NBL + b] > 128u && mm[2 * NBL + b] != ~mm[3 * NBL + b]);
+    big = __syncthreads_or(big);
+#pragma unroll 1
+    for (uint32_t list = 0; list < 2; ++list) {
+      const uint32_t len = list == 0 ? m_pf : m_ev;
+      if (len == 0) continue;
+      const uint32_t *sk = list == 0 ? d.sort_ka : d.f_sk2, *sv = list == 0 ? d.sort_va : d.f_sv2;
+      uint32_t *ka = s.keys, *ia = ka + len, *kb = ka + 2 * len, *ib = ka + 3 * len;  // 4 len <= 3 tile
+      uint32_t *out = list == 0 ? d.pf_ids : d.ev_ids;
+      for (uint32_t e = threadIdx.x; e < len; e += FT) {
+        ka[e] = (list == 0 || !big) ? sk[e] : ~sk[e];
+        ia[e] = sv[e];
+      }
+      __syncthreads();
+      if (!big) {
+        // prefetch: position = segment start + members with a smaller key or an equal key
+        // earlier in staging (ascending id); evict (buckets and keys descending): members
+        // of higher buckets + members with a larger key or an equal key earlier (descending id)
+        for (uint32_t e = threadIdx.x; e < len; e += FT) {
+          const uint32_t k = ka[e], bk = k >> 21;
+          const uint32_t end = s.h[(2 + list) * NBL + bk], beg = end - s.h[list * NBL + bk];
+          uint32_t pos = (list == 0 ? beg : len - end) + (e - beg);
+          if (mm[2 * list * NBL + bk] != ~mm[(2 * list + 1) * NBL + bk]) {  // several distances
+            pos = list == 0 ? beg : len - end;
+            for (uint32_t x = beg; x < end; ++x) {
+              const uint32_t kx = ka[x];
+              pos += (list == 0 ? kx < k : kx > k) || (kx == k && x < e);
+            }
+          }
+          out[pos] = ia[e];
+        }
+      } else {
+        cta_sort_pairs(ka, ia, kb, ib, len, s.h);  // stable: ties keep the staging (list) order
+        for (uint32_t e = threadIdx.x; e < len; e += FT) out[e] = ia[e];
+      }
+      __syncthreads();
+    }
+  }
+
   // ---------------- P5: list order.  A segment is the members of one list bucket, in list
   // order (prefetch: ascending key; evict: descending key); its position in the list follows
   // from the bucket totals.  Segments are cut into slices of CH elements, one slice per slot,
@@ -977,29 +1031,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     d.header[H_N_EV] = nev;
   }
   __syncthreads();
-  // A single-CTA instance (G == 1, the batched replicas of C5) holds every list member in its
-  // own staging area, bucket-major (buckets ascending) and in list order within a bucket: one
-  // stable radix sort per list by key (prefetch) or complemented key (evict) gives the
-  // (distance, id) order directly, instead of one slot per nonempty list bucket.
-  const bool one_cta = G == 1 && 4 * max(npf, nev) <= 3 * A.tile;
-  if (one_cta) {
-#pragma unroll 1
-    for (uint32_t list = 0; list < 2; ++list) {
-      const uint32_t len = list == 0 ? npf : nev;
-      if (len == 0) continue;
-      const uint32_t *sk = list == 0 ? d.sort_ka : d.f_sk2, *sv = list == 0 ? d.sort_va : d.f_sv2;
-      uint32_t *ka = s.keys, *ia = ka + len, *kb = ka + 2 * len, *ib = ka + 3 * len;  // 4 len <= 3 tile
-      for (uint32_t e = threadIdx.x; e < len; e += FT) {
-        ka[e] = list == 0 ? sk[e] : ~sk[e];
-        ia[e] = sv[e];
-      }
-      __syncthreads();
-      cta_sort_pairs(ka, ia, kb, ib, len, s.h);  // stable: ties keep the staging (list) order
-      uint32_t *out = list == 0 ? d.pf_ids : d.ev_ids;
-      for (uint32_t e = threadIdx.x; e < len; e += FT) out[e] = ia[e];
-      __syncthreads();
-    }
-  }
   const uint32_t n_slots = one_cta ? 0u : sh_ns;
   // R13 write-back bytes of this tile's dirty evicted agents: loads issued now (up to two per
   // word in registers), summed after the slot loop (their latency hides behind P5) and added

@@ -292,20 +292,32 @@ def test_tie_cut_word_boundaries_and_writebacks(mk):
 
 def test_batch_single_cta_instances():
     """scalesim_step_batch with >= 75 instances gives each instance one CTA (the C5 launch
-    shape on one GPU): its lists come from the single-CTA radix-sort path, or from the slot
-    path when a list exceeds 3/4 of the tile (theta = inf, budget 90% at the first step)."""
+    shape on one GPU): its lists come from the single-CTA paths (per-segment counting when
+    every multi-valued list bucket holds <= 128 members, else a radix sort: the `wide`
+    workload), or from the slot path when a list exceeds 3/4 of the tile (theta = inf,
+    budget 90%)."""
     import torch
     from paper_2601_21473_b200.planner import Planner, step_batch
     n, steps, k = 1500, 6, 80
-    ws = [tg.config_c5(replica=r, budget_pct=10, steps=steps, n=n) for r in range(8)]
+    ws = [tg.config_c5(replica=r, budget_pct=10, steps=steps, n=n) for r in range(7)]
+    # one workload whose distances share one list bucket ([16, 32): several values per bucket,
+    # far more than 128 members): the radix-sort fallback
+    rng = np.random.default_rng(5)
+    fpw = rng.choice([1, 2], n) * tg.PAGE_BYTES
+    now = np.asarray(ws[0].now, np.int64)  # (one `now` per batched step for every instance)
+    recw = np.stack([rec_of([dict(d=int(rng.integers(16, 20)), fp=int(fpw[a]), dirty=int(rng.integers(0, 2)))
+                             for a in range(n)], now=int(now[t])) for t in range(steps)])
+    blw = tg.make_blocks([[tg.KIND_KV]] * n, [[int(f)] for f in fpw])
+    wide = tg.Workload("wide", n, now, recw, None, blw, int(fpw.sum()) // 2, np.full(3, 50.0, np.float32))
+    ws.append(wide)
     stream = torch.cuda.Stream()
     inst = []
     for i in range(k):
         w = ws[i % 8]
-        pct = 90 if i >= k - 2 else 10 * (1 + i % 9)
-        theta = np.full(3, np.inf, np.float32) if i >= k - 2 else w.theta
+        pct = 90 if i >= k - 2 else (40 if i >= k - 4 else 10 * (1 + i % 9))
+        theta = np.full(3, np.inf, np.float32) if i >= k - 4 else w.theta
         b = w.blocks
-        budget = int(w.footprint.sum()) * pct // 100
+        budget = int(b.blk_size.astype(np.int64).sum()) * pct // 100
         pl = Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, theta, transfer=False,
                      stream=stream)
         inst.append(dict(pl=pl, w=w, budget=budget, theta=theta, res=np.zeros(n, np.uint8)))
