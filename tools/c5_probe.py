@@ -37,7 +37,8 @@ for j, pl in enumerate(pls[:4]):
     st = pl.stamps().astype(np.int64)
     r = lambda q: round((int(st[q]) - int(st[0])) / 1e3, 2) if st[q] else None
     h = pl.sync()
-    print("inst", j, "npf", h["n_prefetch"], "nev", h["n_evict"], "| P1loop", r(25), "P1end", r(11), "P3end", r(14),
+    print("inst", j, "npf", h["n_prefetch"], "nev", h["n_evict"], "| B1", r(4), "cleared", r(32), "coarse", r(33),
+          "fine", r(34), "selbar", r(35), "sel", r(9), "P3", r(10), "| P1loop", r(25), "P1end", r(11), "P3end", r(14),
           "P4loop", r(27), "P4lists", r(17), "P4ranks", r(19), "P4rows", r(28), "P4end", r(12), "P5tables", r(13),
           "end", r(1), "| slots", int(st[16]), "slot_loop_ns", int(st[21]), "sections", [int(st[q]) for q in (22, 23, 24, 29)],
           "max_sorted_seg", int(st[18]))
