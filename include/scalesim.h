@@ -198,11 +198,15 @@ scalesim_status scalesim_view(scalesim_ctx *ctx, scalesim_plan_view *out);
 /* score + plan + transfer of one step. */
 scalesim_status scalesim_step(scalesim_ctx *ctx, int64_t now_tick, scalesim_plan_view *out);
 
-/* One step of several independent contexts (simulation replicas / parameter sweeps, C5) in
- * as few launches as possible: each context is planned by its own group of CTAs of one
- * persistent kernel.  All contexts must use the single-kernel plan path (scalesim_fused == 1)
- * on the same device and the same cfg.stream; each context's inputs are its own tables.
- * Equivalent to scalesim_step on every context in turn (same plans). */
+/* One step of several independent contexts (simulation replicas / parameter sweeps, C5,
+ * BASELINE configs[4]) in as few launches as possible: each context is planned by its
+ * own group of floor(SMs / k) CTAs of one persistent kernel (k <= SMs contexts per launch; a
+ * group of one CTA orders its lists in shared memory instead of the multi-CTA slot pass).
+ * All contexts must use the single-kernel plan path (scalesim_fused == 1) on the same device
+ * and the same cfg.stream; each context's inputs are its own tables; all share now_tick.
+ * Equivalent to scalesim_step on every context in turn (same plans, tests/test_gpu_parity.py).
+ * Errors: SCALESIM_E_INVALID for a NULL / non-fused / mixed-stream context or a context too
+ * large for its group's tile; otherwise the first failing context's status. */
 scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32_t n, int64_t now_tick);
 
 /* End-to-end step from HOST buffers: copies host_rec (4*n_local uint32) and host_kin
