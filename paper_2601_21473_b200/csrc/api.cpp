@@ -245,6 +245,7 @@ struct scalesim_ctx {
   ncclComm_t comm = nullptr;
   int last_buf = 0;
   bool xfer_pending = false;
+  bool xfer_recorded[2] = {false, false};  // ev_xfer[b] has been recorded at least once
   // fused single-kernel plan (world == 1)
   bool fused = false;
   uint32_t fused_tile = 0;
@@ -692,6 +693,9 @@ extern "C" scalesim_status scalesim_transfer(scalesim_ctx *c, const scalesim_pla
   if (c->transfer) {
     CK(cudaStreamWaitEvent(c->copy_stream, c->ev_plan, 0));
     CK(cudaStreamWaitEvent(c->copy_stream2, c->ev_plan, 0));
+    // the independent loads may reuse pages the previous step released: they must not
+    // overtake that step's write-backs (still running on copy_stream when plans run ahead)
+    if (c->xfer_recorded[buf ^ 1]) CK(cudaStreamWaitEvent(c->copy_stream2, c->ev_xfer[buf ^ 1], 0));
     Params q = c->p;
     q.desc_buf = buf;
     c->launches += launch_transfer_split(q, c->copy_stream, c->copy_stream2, c->copy_ctas);
@@ -699,6 +703,7 @@ extern "C" scalesim_status scalesim_transfer(scalesim_ctx *c, const scalesim_pla
     CK(cudaEventRecord(c->ev_side, c->copy_stream2));
     CK(cudaStreamWaitEvent(c->copy_stream, c->ev_side, 0));
     CK(cudaEventRecord(c->ev_xfer[buf], c->copy_stream));
+    c->xfer_recorded[buf] = true;
     c->xfer_pending = true;
   }
   c->transferred = true;
@@ -724,6 +729,29 @@ extern "C" scalesim_status scalesim_step(scalesim_ctx *c, int64_t now, scalesim_
   return SCALESIM_OK;
 }
 
+// Instances per launch and CTAs per instance for a batch chunk starting at i0 (sms CTAs in
+// all: one CTA per SM); false when a context's tile cannot fit shared memory.
+static bool batch_chunk(scalesim_ctx *const *ctxs, uint32_t n, uint32_t i0, uint32_t sms, uint32_t *k_out,
+                        uint32_t *gsize_out, uint32_t *tile_out) {
+  uint32_t k = n - i0 < sms ? n - i0 : sms;
+  if (k > (uint32_t)FUSED_MAX_BATCH) k = FUSED_MAX_BATCH;
+  uint32_t gsize, tile;
+  while (true) {
+    gsize = sms / k;
+    uint64_t nm = 0;
+    for (uint32_t i = i0; i < i0 + k; ++i) nm = ctxs[i]->p.n_local > nm ? ctxs[i]->p.n_local : nm;
+    uint64_t t = (nm + gsize - 1) / gsize;
+    t = (t + 31) / 32 * 32;
+    tile = (uint32_t)(t ? t : 32);
+    if (tile <= FUSED_MAX_TILE || k == 1) break;
+    k = k / 2;  // fewer instances per launch, more CTAs each
+  }
+  *k_out = k;
+  *gsize_out = gsize;
+  *tile_out = tile;
+  return tile <= FUSED_MAX_TILE && fused_prepare((int)(k * gsize), tile);
+}
+
 extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32_t n, int64_t now) {
   if (!ctxs || n == 0) return SCALESIM_E_INVALID;
   scalesim_ctx *c0 = ctxs[0];
@@ -731,35 +759,26 @@ extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32
   for (uint32_t i = 0; i < n; ++i) {
     scalesim_ctx *c = ctxs[i];
     if (!c || !c->fused || c->stream != c0->stream || c->cfg.device != c0->cfg.device) return SCALESIM_E_INVALID;
+    for (uint32_t j = 0; j < i; ++j)
+      if (ctxs[j] == c) return SCALESIM_E_INVALID;  // a context at most once per batch
   }
+  // validate every launch before enqueueing anything: an error leaves every context unchanged
+  const uint32_t sms = (uint32_t)c0->sms;
+  for (uint32_t i0 = 0; i0 < n;) {
+    uint32_t k, gsize, tile;
+    if (!batch_chunk(ctxs, n, i0, sms, &k, &gsize, &tile)) return SCALESIM_E_INVALID;
+    i0 += k;
+  }
+  CK(cudaGetLastError());
   // (1) score: interaction pair scans (if any) and the deferred score of every instance
   for (uint32_t i = 0; i < n; ++i) {
     scalesim_status s = scalesim_score(ctxs[i], now, nullptr);
     if (s != SCALESIM_OK) return s;
   }
   // (2) plan: chunks of instances, each instance on its own group of CTAs, one launch each
-  const uint32_t sms = (uint32_t)c0->sms;
-  uint32_t i0 = 0;
-  while (i0 < n) {
-    uint32_t k = n - i0 < sms ? n - i0 : sms;
-    if (k > (uint32_t)FUSED_MAX_BATCH) k = FUSED_MAX_BATCH;
-    {  // experiment knob: cap on instances per launch (tools/ only)
-      static const char *cap_s = std::getenv("SCALESIM_BATCH_CAP");
-      const uint32_t cap = cap_s ? (uint32_t)std::atoi(cap_s) : 0u;
-      if (cap && k > cap) k = cap;
-    }
-    uint32_t gsize, tile;
-    while (true) {
-      gsize = sms / k;
-      uint64_t nm = 0;
-      for (uint32_t i = i0; i < i0 + k; ++i) nm = ctxs[i]->p.n_local > nm ? ctxs[i]->p.n_local : nm;
-      uint64_t t = (nm + gsize - 1) / gsize;
-      t = (t + 31) / 32 * 32;
-      tile = (uint32_t)(t ? t : 32);
-      if (tile <= FUSED_MAX_TILE || k == 1) break;
-      k = k / 2;  // fewer instances per launch, more CTAs each
-    }
-    if (tile > FUSED_MAX_TILE || !fused_prepare((int)(k * gsize), tile)) return SCALESIM_E_INVALID;
+  for (uint32_t i0 = 0; i0 < n;) {
+    uint32_t k, gsize, tile;
+    batch_chunk(ctxs, n, i0, sms, &k, &gsize, &tile);
     FusedInst insts[FUSED_MAX_BATCH];
     for (uint32_t i = 0; i < k; ++i) insts[i] = fused_inst(ctxs[i0 + i], tile);
     c0->launches += launch_fused_batch(insts, k, gsize, c0->stream);

@@ -1343,11 +1343,16 @@ static void launch_t(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStr
   cfg.blockDim = dim3(FT);
   cfg.dynamicSmemBytes = fused_smem_bytes(tile);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // cooperative: the grid barrier needs every CTA resident at once; the launch is scheduled
+  // (or fails) as a whole instead of leaving resident CTAs spinning on absent ones when other
+  // work holds SMs (another context's plan, copy kernels, the caller's kernels)
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, k_fused_plan<MAXB>, B);
 }
 

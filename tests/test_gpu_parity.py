@@ -59,13 +59,16 @@ def test_c3_full_size():
     run_parity(w, stamp_writes=False, content_pages=16)
 
 
-@pytest.mark.parametrize("mk", PATHS)
-def test_c4_full_size_logical(mk):
-    """BASELINE configs[3] at G=1: 1M agents, logical sizes (no arena), the bench's launch
-    configuration."""
+@pytest.mark.parametrize("mk,keep", [pytest.param(False, True, id="fused"),
+                                     pytest.param(False, False, id="fused-nokeep-bench"),
+                                     pytest.param(True, True, id="multikernel")])
+def test_c4_full_size_logical(mk, keep):
+    """BASELINE configs[3] at G=1: 1M agents, logical sizes (no arena).  `fused-nokeep-bench`
+    is exactly bench.py's headline configuration (same generator, seed and size, keep_dist
+    off: the fused kernel's fast P1 variant that the timed region runs)."""
     from gpu_harness import run_parity
-    w = tg.config_c4(seed=1, steps=6 if mk else 20)
-    run_parity(w, transfer=False, multi_kernel=mk)
+    w = tg.config_c4(seed=1, steps=6 if mk else 24)
+    run_parity(w, transfer=False, multi_kernel=mk, keep_dist=keep)
 
 
 @pytest.mark.parametrize("mk", PATHS)
@@ -125,6 +128,7 @@ def test_large_tie_group_spans_tiles(mk):
     w = tg.Workload("ties", n, np.array([0]), rec, None, blocks, budget, np.full(3, 9.0, np.float32))
     run_parity(w)
     run_parity(w, transfer=False)
+    run_parity(w, transfer=False, keep_dist=False)
 
 
 def test_call_order_and_host_step():
@@ -288,6 +292,8 @@ def test_tie_cut_word_boundaries_and_writebacks(mk):
         budget = below + int(csum[j])
         w = tg.Workload("tiecut", n, np.array([0]), rec, None, blocks, budget, np.full(3, 50.0, np.float32))
         _rp(w, transfer=False, multi_kernel=mk, resident_init=resident)
+        if not mk:  # the bench's fast P1 variant (no distance copy)
+            _rp(w, transfer=False, resident_init=resident, keep_dist=False)
 
 
 def test_batch_single_cta_instances():
