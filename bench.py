@@ -521,9 +521,11 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     b = w.blocks
+    # the headline context owns the GPU (SCALESIM_F_EXCLUSIVE: no cooperative-launch attribute,
+    # include/scalesim.h); the default (cooperative) launch is timed beside it
     pl = Planner(n * world, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, w.theta,
                  transfer=False, device=local, shard=(rank * n, (rank + 1) * n), rank=rank, world=world,
-                 nccl_id=nccl_id, keep_dist=False)
+                 nccl_id=nccl_id, keep_dist=False, exclusive=True)
     # all step records resident in HBM (T distinct 16 MB buffers, > L2)
     recs = torch.from_numpy(np.ascontiguousarray(w.rec).view(np.uint8).reshape(T, -1)).to(dev)
     ptr = [recs[s].data_ptr() for s in range(T)]
@@ -582,6 +584,28 @@ def main():
         ms = float(t.item())
     ms_per_step = ms / K
     value = n * world * K / (ms / 1e3)
+
+    # (1a) the default launch mode (cooperative attribute, any context may run concurrently
+    # with other kernels): the same K steps on a second, non-exclusive context
+    coop_ms = None
+    if world == 1:
+        pc = Planner(n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, budget, w.theta, transfer=False,
+                     device=local, keep_dist=False)
+        for s in range(WARM_IN + W):
+            pc.set_inputs_ptr(ptr[s])
+            pc.step(int(w.now[s]))
+        torch.cuda.synchronize(dev)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(pc.stream):
+            torch.cuda._sleep(int(2e9 * 0.05 + K * 2e5))
+        c0.record(pc.stream)
+        for k in range(K):
+            pc.set_inputs_ptr(ptr[t_base + k])
+            pc.step(int(w.now[t_base + k]))
+        c1.record(pc.stream)
+        torch.cuda.synchronize(dev)
+        coop_ms = c0.elapsed_time(c1) / K
+        pc.close()
 
     # (1b) the same K-step loop captured once as a CUDA graph and replayed (next K buffers):
     # reported beside the eager number, not as the value
@@ -728,6 +752,9 @@ def main():
                        "n_agents_per_gpu": n, "n_agents": n * world, "parallelism": f"id-shard x{world}",
                        "l2": f"{K} distinct 16 MB record buffers (> 126 MB L2)", "timing": mode,
                        "graph_replay_ms_per_step": graph_ms,
+                       "launch_mode": "SCALESIM_F_EXCLUSIVE (device dedicated to the planner: no cooperative "
+                                      "attribute, programmatic dependent launch)",
+                       "cooperative_mode_ms_per_step": coop_ms,
                        "last_plan": {k: hdr[k] for k in ("n_prefetch", "n_evict", "cut_bits", "status")}},
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": sampler.result()}
     if c5 is not None:

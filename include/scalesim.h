@@ -63,6 +63,8 @@ typedef enum {
 #define SCALESIM_ST_BAD_RECORD 2u   /* class 3, or an INT agent whose kin index >= n_kin */
 #define SCALESIM_ST_BAD_KIN 4u      /* ACTING INT agent with non-finite kinematics (excluded) */
 #define SCALESIM_ST_NO_PAGES 8u     /* free page pool exhausted (cannot happen for a valid config) */
+#define SCALESIM_ST_SYNC 16u        /* internal: a fused-kernel CTA timed out waiting for another
+                                       CTA's published offsets (cannot happen: grid co-resident) */
 
 /* Config flags. */
 #define SCALESIM_F_NO_TRANSFER 1u   /* plan + byte accounting only: no arena, no pages, no copies
@@ -78,6 +80,25 @@ typedef enum {
                                        record is eligible below theta[0].  Plans shared memory
                                        objects from scalesim_object_min.  Requires
                                        n_kin == 0. */
+#define SCALESIM_F_EXCLUSIVE 16u    /* the caller dedicates the device to this library's plans while
+                                       they run: every SM usable (no MPS / green-context partition)
+                                       and no other kernel concurrent with a plan launch.  The
+                                       single-kernel plan is then launched without the cooperative
+                                       attribute, so its prologue overlaps the previous kernel's tail
+                                       (~2 us per step, profiles/r02_*); co-residency of its CTAs
+                                       (one per SM) is checked at init, and the library orders the
+                                       single-kernel plans of its exclusive contexts on one device
+                                       one after another (event chain across their streams).
+                                       Without the flag the launch is cooperative: the grid is
+                                       scheduled as a whole and cannot deadlock against other work
+                                       holding SMs (the kernel's grid barrier needs every CTA). */
+#define SCALESIM_F_LOOPBACK 32u     /* world > 1 without NCCL: this context is rank `rank` of a world
+                                       whose ranks all live on this device (one process) and are
+                                       stepped together by scalesim_step_group: one launch of the
+                                       single-kernel plan, floor(SMs / world) CTAs per rank, the
+                                       exchange of the global cut through the ranks' workspaces
+                                       after a world-wide barrier.  Shards must be
+                                       contiguous, in rank order and cover [0, n_agents). */
 
 /* Agent record: 4 x uint32 per agent, 16-byte aligned, one 128-bit load.
  *   [0] t_next : action-end tick (ACTING independent / interaction agents), or remaining hop
@@ -102,7 +123,8 @@ typedef struct {
   float hop_scale;        /* ticks per hop for diffusion distances (R5), > 0, finite */
   uint64_t page_bytes;    /* device arena page size; every block size is a multiple; 4096-aligned */
   int32_t device;         /* CUDA device ordinal */
-  int32_t rank, world;    /* world > 1: NCCL exchange for the global cut */
+  int32_t rank, world;    /* world > 1: NCCL exchange for the global cut, or
+                             SCALESIM_F_LOOPBACK (scalesim_step_group) */
   const void *nccl_unique_id; /* 128 bytes from scalesim_nccl_unique_id on rank 0, broadcast by the
                                  caller (e.g. torch.distributed); ignored when world == 1 */
   void *stream;           /* cudaStream_t for score/plan (0 = legacy default stream) */
@@ -208,6 +230,16 @@ scalesim_status scalesim_step(scalesim_ctx *ctx, int64_t now_tick, scalesim_plan
  * Errors: SCALESIM_E_INVALID for a NULL / non-fused / mixed-stream context or a context too
  * large for its group's tile; otherwise the first failing context's status. */
 scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32_t n, int64_t now_tick);
+
+/* One step of a world of `world` ranks on one device (contexts created with
+ * SCALESIM_F_LOOPBACK, ctxs[r] = rank r, all on the same device and cfg.stream, same n_agents,
+ * budget and thresholds, contiguous shards in rank order covering [0, n_agents), equal step
+ * counts): score + plan + transfer of every rank, the global cut exchanged inside one launch.
+ * Each rank's plan holds its own shard's lists (global ids, list order of the world) and
+ * residency; cut_bits, cut_rem, kept_bytes, n_eligible and the INSUFFICIENT bit are
+ * world-wide, the other header fields the rank's.  plan(world) == plan(1) restricted to the
+ * shard (tests/test_gpu_world.py).  Errors: SCALESIM_E_INVALID for a malformed world. */
+scalesim_status scalesim_step_group(scalesim_ctx *const *ctxs, uint32_t world, int64_t now_tick);
 
 /* End-to-end step from HOST buffers: copies host_rec (4*n_local uint32) and host_kin
  * (4*n_kin float, may be NULL) to the device, runs scalesim_step, waits, and copies the

@@ -15,6 +15,7 @@ F_NO_TRANSFER = 1
 F_KEEP_DIST = 2
 F_MULTI_KERNEL = 4
 F_EXPLICIT_DIST = 8
+F_EXCLUSIVE = 16
 
 ST_INSUFFICIENT = 1
 ST_BAD_RECORD = 2

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -111,6 +112,10 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_sv3 = take(4 * n1);
   L.f_bar = take(64);
   L.f_prof = take(512);
+  L.f_pos = take(8 * 2 * 4096 * (uint64_t)FUSED_MAX_CTAS);
+  L.f_rt = take(8 * 2 * (uint64_t)FUSED_MAX_CTAS);
+  L.f_crow = take(4 * 2 * 4096 * (uint64_t)FUSED_MAX_CTAS);
+  L.f_ovf = take(16 * 2 * (uint64_t)FUSED_OVF_CAP);
   L.total = off;
   return L;
 }
@@ -189,6 +194,10 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_sv3 = (uint32_t *)(b + L.f_sv3);
   d.f_bar = (unsigned int *)(b + L.f_bar);
   d.f_prof = (unsigned long long *)(b + L.f_prof);
+  d.f_pos = (unsigned long long *)(b + L.f_pos);
+  d.f_rt = (unsigned long long *)(b + L.f_rt);
+  d.f_crow = (uint32_t *)(b + L.f_crow);
+  d.f_ovf = (uint4 *)(b + L.f_ovf);
   return d;
 }
 
@@ -224,6 +233,18 @@ struct Nccl {
 };
 static Nccl g_nccl;
 
+// SCALESIM_F_EXCLUSIVE: the single-kernel plans of the exclusive contexts of a device run one
+// after another (their grid barriers need every SM): the last launch's stream and event per
+// device, and the number of such contexts (with one, nothing is recorded: consecutive launches
+// on its stream stay directly linked for the programmatic launch overlap).
+struct ExclusiveChain {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t event = nullptr;
+  int contexts = 0;
+};
+static std::mutex g_excl_mu;
+static ExclusiveChain g_excl[64];
+
 }  // namespace ss
 
 using namespace ss;
@@ -246,6 +267,8 @@ struct scalesim_ctx {
   int last_buf = 0;
   bool xfer_pending = false;
   bool xfer_recorded[2] = {false, false};  // ev_xfer[b] has been recorded at least once
+  bool exclusive = false;                  // SCALESIM_F_EXCLUSIVE
+  cudaEvent_t ev_fused = nullptr;          // after this context's last single-kernel plan
   // fused single-kernel plan (world == 1)
   bool fused = false;
   uint32_t fused_tile = 0;
@@ -282,9 +305,10 @@ static scalesim_status validate_config(const scalesim_config *c) {
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return SCALESIM_E_INVALID;
   if (c->world == 1 && (c->shard_begin != 0 || c->shard_end != c->n_agents)) return SCALESIM_E_INVALID;
   if (c->world > 1 && c->n_kin > 0) return SCALESIM_E_INVALID;  // interaction agents: single rank
+  if ((c->flags & SCALESIM_F_LOOPBACK) && (c->world < 2 || c->world > (int)FUSED_MAX_WORLD)) return SCALESIM_E_INVALID;
   if ((c->flags & SCALESIM_F_EXPLICIT_DIST) && c->n_kin > 0) return SCALESIM_E_INVALID;
   if (c->flags & ~(uint32_t)(SCALESIM_F_NO_TRANSFER | SCALESIM_F_KEEP_DIST | SCALESIM_F_MULTI_KERNEL |
-                             SCALESIM_F_EXPLICIT_DIST))
+                             SCALESIM_F_EXPLICIT_DIST | SCALESIM_F_EXCLUSIVE | SCALESIM_F_LOOPBACK))
     return SCALESIM_E_INVALID;
   for (int k = 0; k < 3; ++k)
     if (std::isnan(c->theta[k]) || c->theta[k] < 0.0f) return SCALESIM_E_INVALID;
@@ -396,6 +420,7 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
   for (int k = 0; k < 3; ++k) p.theta[k] = cfg->theta[k];
   p.hop_scale = cfg->hop_scale;
   p.explicit_dist = (cfg->flags & SCALESIM_F_EXPLICIT_DIST) ? 1 : 0;
+  p.loopback = (cfg->flags & SCALESIM_F_LOOPBACK) ? 1 : 0;
   p.int_mode = (!p.explicit_dist && cfg->n_kin == 0 && cfg->hop_scale == std::floor(cfg->hop_scale)) ? 1 : 0;
   p.rank = cfg->rank;
   p.world = cfg->world;
@@ -506,24 +531,34 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
     }
   }
   c->launches += launch_plan_init(p, c->stream);
-  // fused path: one CTA per SM, co-resident (cooperative launch)
-  if (cfg->world == 1 && !(cfg->flags & SCALESIM_F_MULTI_KERNEL)) {
+  // fused path: one CTA per SM, co-resident (cooperative launch); a loopback rank gets its
+  // share of the SMs (its world is planned by one launch)
+  if ((cfg->world == 1 || p.loopback) && !(cfg->flags & SCALESIM_F_MULTI_KERNEL)) {
     uint32_t tile = 0;
-    if (fused_supported(p, sms, &tile) && fused_prepare(sms, tile)) {
+    const int g = p.loopback ? sms / cfg->world : sms;
+    if (fused_supported(p, g, &tile) && fused_prepare(g * (p.loopback ? cfg->world : 1), tile, (uint32_t)g)) {
       c->fused = true;
       c->fused_tile = tile;
-      c->fused_grid = sms;
+      c->fused_grid = g;
       c->sms = sms;
       if (cudaMemsetAsync(p.d.f_mm1, 0xFF, 4 * 2 * 2 * 4096, c->stream) != cudaSuccess ||
           cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2 * 1024, c->stream) != cudaSuccess)
         return fail(SCALESIM_E_CUDA);
     }
   }
+  if (c->fused && (cfg->flags & SCALESIM_F_EXCLUSIVE)) {
+    if (cfg->device < 0 || cfg->device >= 64 || cudaEventCreateWithFlags(&c->ev_fused, cudaEventDisableTiming) != cudaSuccess)
+      return fail(SCALESIM_E_INVALID);
+    std::lock_guard<std::mutex> g(g_excl_mu);
+    c->exclusive = true;
+    g_excl[cfg->device].contexts++;
+  }
   // device copy of the parameters for the fused kernel (per-launch fields are overridden)
   if (cudaMemcpyAsync(p.d.params_dev, &p, sizeof(Params), cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
     return fail(SCALESIM_E_CUDA);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
-  if (cfg->world > 1) {
+  if (p.loopback && !c->fused) return fail(SCALESIM_E_INVALID);  // (shard too large for its CTAs)
+  if (cfg->world > 1 && !p.loopback) {
     if (!cfg->nccl_unique_id || !g_nccl.load()) return fail(SCALESIM_E_NCCL);
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_unique_id, sizeof(id));
@@ -586,6 +621,22 @@ static void fill_plan(scalesim_ctx *c, scalesim_plan_view *out) {
 
 static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out);
 
+// One single-kernel plan launch (n instances on c's stream): cooperative unless c is an
+// exclusive context; exclusive launches of different contexts of a device are chained.
+static int launch_fused(scalesim_ctx *c, const FusedInst *insts, uint32_t n, uint32_t gsize) {
+  if (!c->exclusive) return launch_fused_batch(insts, n, gsize, c->stream, true);
+  std::lock_guard<std::mutex> g(g_excl_mu);
+  ExclusiveChain &x = g_excl[c->cfg.device];
+  if (x.contexts > 1 && x.stream && x.stream != c->stream) cudaStreamWaitEvent(c->stream, x.event, 0);
+  const int k = launch_fused_batch(insts, n, gsize, c->stream, false);
+  if (x.contexts > 1) {
+    cudaEventRecord(c->ev_fused, c->stream);
+    x.stream = c->stream;
+    x.event = c->ev_fused;
+  }
+  return k;
+}
+
 static FusedInst fused_inst(const scalesim_ctx *c, uint32_t tile) {
   FusedInst f;
   f.params = reinterpret_cast<const Params *>(c->p.d.params_dev);
@@ -608,7 +659,7 @@ extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *ou
   const bool multi = c->cfg.world > 1;
   if (c->deferred) {
     const FusedInst inst = fused_inst(c, c->fused_tile);
-    c->launches += launch_fused_batch(&inst, 1, (uint32_t)c->fused_grid, c->stream);
+    c->launches += launch_fused(c, &inst, 1, (uint32_t)c->fused_grid);
     CK(cudaGetLastError());
     c->fused_steps++;
     c->deferred = false;
@@ -749,7 +800,7 @@ static bool batch_chunk(scalesim_ctx *const *ctxs, uint32_t n, uint32_t i0, uint
   *k_out = k;
   *gsize_out = gsize;
   *tile_out = tile;
-  return tile <= FUSED_MAX_TILE && fused_prepare((int)(k * gsize), tile);
+  return tile <= FUSED_MAX_TILE && fused_prepare((int)(k * gsize), tile, gsize);
 }
 
 extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32_t n, int64_t now) {
@@ -758,7 +809,9 @@ extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32
   if (!c0) return SCALESIM_E_INVALID;
   for (uint32_t i = 0; i < n; ++i) {
     scalesim_ctx *c = ctxs[i];
-    if (!c || !c->fused || c->stream != c0->stream || c->cfg.device != c0->cfg.device) return SCALESIM_E_INVALID;
+    if (!c || !c->fused || c->stream != c0->stream || c->cfg.device != c0->cfg.device ||
+        c->exclusive != c0->exclusive)
+      return SCALESIM_E_INVALID;
     for (uint32_t j = 0; j < i; ++j)
       if (ctxs[j] == c) return SCALESIM_E_INVALID;  // a context at most once per batch
   }
@@ -781,7 +834,7 @@ extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32
     batch_chunk(ctxs, n, i0, sms, &k, &gsize, &tile);
     FusedInst insts[FUSED_MAX_BATCH];
     for (uint32_t i = 0; i < k; ++i) insts[i] = fused_inst(ctxs[i0 + i], tile);
-    c0->launches += launch_fused_batch(insts, k, gsize, c0->stream);
+    c0->launches += launch_fused(c0, insts, k, gsize);
     CK(cudaGetLastError());
     for (uint32_t i = i0; i < i0 + k; ++i) {
       scalesim_ctx *c = ctxs[i];
@@ -799,7 +852,7 @@ extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32
 
 static scalesim_status status_of_header(uint64_t st) {
   if (st & (SCALESIM_ST_BAD_RECORD | SCALESIM_ST_BAD_KIN)) return SCALESIM_E_BAD_INPUT;
-  if (st & SCALESIM_ST_NO_PAGES) return SCALESIM_E_INVARIANT;
+  if (st & (SCALESIM_ST_NO_PAGES | SCALESIM_ST_SYNC)) return SCALESIM_E_INVARIANT;
   if (st & SCALESIM_ST_INSUFFICIENT) return SCALESIM_E_INSUFFICIENT;
   return SCALESIM_OK;
 }
@@ -842,6 +895,16 @@ extern "C" void scalesim_destroy(scalesim_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->exclusive) {
+    std::lock_guard<std::mutex> g(g_excl_mu);
+    ExclusiveChain &x = g_excl[c->cfg.device];
+    x.contexts--;
+    if (x.event == c->ev_fused) {
+      x.stream = nullptr;
+      x.event = nullptr;
+    }
+  }
+  if (c->ev_fused) cudaEventDestroy(c->ev_fused);
   if (c->copy_stream2) {
     cudaStreamSynchronize(c->copy_stream2);
     cudaStreamDestroy(c->copy_stream2);

@@ -42,6 +42,64 @@ constexpr int NBL = 1024;  // list-sort buckets: distance bits [30:21]
 #endif
 constexpr int LOAD_BATCH = LOAD_BATCH_V;  // records in flight per thread in P1
 
+// Integer-distance contexts (int_mode: every distance is an integer number of ticks or +inf)
+// bucket level 1 by value: d < 2048 is its own bucket (single-valued), larger finite
+// distances keep the float-bit buckets (bits >> 19, multi-valued) shifted down to
+// [2048, 3920), and +inf is bucket 3920.  Monotone in d, so the byte-weighted select is
+// unchanged; with the boundary and every list member in a single-valued bucket, list
+// positions follow from per-CTA counts alone (the fast list placement below).
+constexpr uint32_t IB_EXACT = 2048;  // first multi-valued bucket
+constexpr uint32_t IB_INF = 3920;    // the +inf bucket
+__device__ __forceinline__ uint32_t ibucket(uint32_t bits) {
+  return bits < 0x45000000u ? (uint32_t)__uint_as_float(bits) : (bits >> 19) - 160u;  // 2048.0f = 0x45000000
+}
+__device__ __forceinline__ bool ib_multi(uint32_t b) { return b >= IB_EXACT && b < IB_INF; }
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// epoch-tagged 48-bit payload: two 24-bit fields (ep in bits [63:48])
+__device__ __forceinline__ unsigned long long pack_ep(uint32_t ep, uint32_t a, uint32_t b) {
+  return ((unsigned long long)ep << 48) | ((unsigned long long)(a & 0xFFFFFFu) << 24) | (b & 0xFFFFFFu);
+}
+// wait until *p carries this launch's epoch (published by another CTA of the grid, which is
+// co-resident); bounded: a sync failure is flagged in the status instead of hanging
+__device__ __forceinline__ unsigned long long poll_ep(const unsigned long long *p, uint32_t ep,
+                                                      unsigned long long *hdr) {
+  unsigned long long v = ld_relaxed_u64(p);
+  for (uint32_t spin = 0; (uint32_t)(v >> 48) != ep; ++spin) {
+    if (spin > (1u << 22)) {
+      atomicOr(reinterpret_cast<unsigned int *>(&hdr[H_STATUS]), ST_SYNC);
+      break;
+    }
+    v = ld_relaxed_u64(p);
+  }
+  return v;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// %globaltimer phase stamps into the workspace (tools/timing_probe.py): compiled only into
+// probe builds (-DFUSED_PROBE); each stamp is ~10 instructions and the kernel's executed code
+// does not fit the 32 KB instruction cache as it is (profiles/r02_*: no_instruction stalls)
+#ifdef FUSED_PROBE
+#define PROBE(...) __VA_ARGS__
+#else
+#define PROBE(...)
+#endif
+#define STAMP_MAX(i) PROBE(if (threadIdx.x == 0) atomicMax(&prof[i], gtimer());)
+#define STAMP0(i) PROBE(if (c == 0 && threadIdx.x == 0) prof[i] = gtimer();)
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -91,7 +149,8 @@ struct GridBar {
 // data instead of 7.7 KB): graph replays of the single-context step pay per launch for it.
 template <int MAXB>
 struct FusedArgs {
-  uint32_t n_inst, gsize;
+  uint32_t n_inst, gsize, fastok;
+  uint32_t wsize;  // ranks per world (consecutive instances); 1: independent instances
   FusedInst inst[MAXB];
 };
 
@@ -101,6 +160,7 @@ struct InstArgs {
   unsigned int epoch;  // launch number of the instance (>= 1)
   uint32_t tile;       // agents per CTA, multiple of 32
   uint32_t tw;         // tile / 32
+  uint32_t fastok;     // shared memory holds the bucket-owner staging (fast list placement)
 };
 
 // dynamic shared memory carve-up
@@ -110,6 +170,7 @@ struct FSmem {
   uint32_t *memb;  // [tile] scratch: word prefixes (u64), member lists, sort buffers
   uint32_t *old_w, *elig_w, *dirty_w, *pf_w, *ev_w;  // [tw]
   uint32_t *h;     // [4 * NB1]: histogram lo/hi/min/nmax, later list counters and starts
+  uint32_t *col;   // bucket-owner staging: [G][RB] CTA counts, then [4][RB] totals / offsets
 };
 
 __device__ __forceinline__ FSmem carve(uint8_t *base, uint32_t tile, uint32_t tw) {
@@ -133,6 +194,7 @@ __device__ __forceinline__ FSmem carve(uint8_t *base, uint32_t tile, uint32_t tw
   w += tw;
   w += (4 - ((uintptr_t)w / 4) % 4) % 4;  // 16-byte aligned: s.h is also read as u64
   s.h = w;
+  s.col = w + 4 * NB1;
   return s;
 }
 
@@ -142,6 +204,7 @@ size_t fused_smem_bytes(uint32_t tile) {
 }
 
 __device__ __forceinline__ void clear_hist(uint32_t *h, int nb) {
+#pragma unroll 1
   for (int b = threadIdx.x; b < nb; b += FT) {
     h[b] = 0;
     h[nb + b] = 0;
@@ -168,9 +231,11 @@ __device__ __forceinline__ void hist_lane(uint32_t *h, int nb, uint32_t b, uint3
 // g_coarse (level 1 only): sums over 64 consecutive buckets, one warp-reduced atomic per warp
 // and bucket group that holds bytes
 __device__ __forceinline__ void publish_hist(const uint32_t *h, int nb, unsigned long long *g_hist, uint32_t *g_mm,
-                                             unsigned long long *row, unsigned long long *g_coarse = nullptr) {
+                                             unsigned long long *row, unsigned long long *g_coarse = nullptr,
+                                             bool perm = true) {
+#pragma unroll 1
   for (int b = threadIdx.x; b < nb; b += FT) {
-    const uint32_t q = nb == NB1 ? slot1(b) : (uint32_t)b;
+    const uint32_t q = (nb == NB1 && perm) ? slot1(b) : (uint32_t)b;
     const unsigned long long v = ((unsigned long long)h[nb + q] << 16) + h[q];
     row[b] = v;
     if (v != 0) {
@@ -217,6 +282,23 @@ __device__ __forceinline__ unsigned long long parts_u64(const uint32_t *acc4) {
          ((unsigned long long)acc4[3] << 48);
 }
 
+// One out-of-line copy of the CTA-wide exclusive scan of one u64 per thread (called from several
+// phases: the kernel's executed code has to stay small, see PROBE).
+__device__ __noinline__ void cta_scan1(unsigned long long (&v)[1], unsigned long long (&tot)[1]) {
+  block_excl_scan_v<unsigned long long, 1, FT>(v, tot);
+}
+
+// The ranks of one world planned in one launch (scalesim_step_group, SCALESIM_F_LOOPBACK): each
+// rank's published arrays.  The select sums the ranks' histograms after the world barrier, the
+// tie prefix adds the lower ranks' bytes at D*, and the world-wide header fields are summed into
+// every rank's header.  nw == 1: the context's own arrays only.
+struct WorldPtrs {
+  uint32_t nw, rank;
+  const unsigned long long *h1[FUSED_MAX_WORLD], *h2[FUSED_MAX_WORLD], *h3[FUSED_MAX_WORLD];
+  const uint32_t *m1[FUSED_MAX_WORLD], *m2[FUSED_MAX_WORLD];
+  unsigned long long *acc[FUSED_MAX_WORLD], *hdr[FUSED_MAX_WORLD];
+};
+
 struct Sel {
   uint32_t prefix;
   unsigned long long below, rem;
@@ -226,16 +308,21 @@ struct Sel {
 // Level 1 of the select by one warp and two dependent loads: the 64 coarse sums (buckets
 // b >> 6), then the 64 buckets of the coarse bucket where the running byte sum crosses the
 // budget.  Same result as select_level(level 1); no block-wide scan.
-__device__ void select_level1_warp(const unsigned long long *g_hist, const unsigned long long *g_coarse,
-                                   const uint32_t *g_mm, unsigned long long budget, Sel &sel, bool imode,
+__device__ void select_level1_warp(const WorldPtrs &W, int par, unsigned long long budget, Sel &sel, bool imode,
                                    unsigned long long *prof) {
   __shared__ unsigned long long s1_prev, s1_tot;
   __shared__ uint32_t s1_b, s1_min, s1_nmax;
+  const bool mm = !imode;  // min / max keys kept (non-integer distances)
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    const ulonglong2 cc = reinterpret_cast<const ulonglong2 *>(g_coarse)[lane];
+    ulonglong2 cc = make_ulonglong2(0, 0);
+    for (uint32_t r = 0; r < W.nw; ++r) {  // coarse sums of the world
+      const ulonglong2 t = reinterpret_cast<const ulonglong2 *>(W.h1[r] + 2 * NB1 + 64 * par)[lane];
+      cc.x += t.x;
+      cc.y += t.y;
+    }
     const unsigned long long incl = warp_incl_scan(cc.x + cc.y), ex = incl - cc.x - cc.y;
-    if (blockIdx.x == 0 && lane == 0) prof[33] = gtimer();  // coarse sums loaded and scanned
+    PROBE(if (blockIdx.x == 0 && lane == 0) prof[33] = gtimer();)  // coarse sums loaded and scanned
     const uint32_t m1 = __ballot_sync(0xFFFFFFFFu, incl > budget);
     const uint32_t m0 = __ballot_sync(0xFFFFFFFFu, ex + cc.x > budget);
     if (m1 == 0) {  // every eligible agent fits
@@ -248,18 +335,24 @@ __device__ void select_level1_warp(const unsigned long long *g_hist, const unsig
       const bool even = (m0 >> L) & 1u;
       const uint32_t C = 2 * L + (even ? 0 : 1);
       const unsigned long long below = __shfl_sync(0xFFFFFFFFu, even ? ex : ex + cc.x, L);
-      const ulonglong2 f = reinterpret_cast<const ulonglong2 *>(g_hist + 64 * C)[lane];
-      uint32_t mn0 = 0, mn1 = 0, nx0 = 0, nx1 = 0;
-      if (g_mm) {
-        const uint2 mn = reinterpret_cast<const uint2 *>(g_mm + 64 * C)[lane];
-        const uint2 nx = reinterpret_cast<const uint2 *>(g_mm + NB1 + 64 * C)[lane];
-        mn0 = mn.x;
-        mn1 = mn.y;
-        nx0 = nx.x;
-        nx1 = nx.y;
+      ulonglong2 f = make_ulonglong2(0, 0);
+      uint32_t mn0 = 0xFFFFFFFFu, mn1 = 0xFFFFFFFFu, nx0 = 0xFFFFFFFFu, nx1 = 0xFFFFFFFFu;
+      for (uint32_t r = 0; r < W.nw; ++r) {
+        const ulonglong2 t = reinterpret_cast<const ulonglong2 *>(W.h1[r] + NB1 * par + 64 * C)[lane];
+        f.x += t.x;
+        f.y += t.y;
+        if (mm) {
+          const uint32_t *g_mm = W.m1[r] + 2 * NB1 * par;
+          const uint2 mn = reinterpret_cast<const uint2 *>(g_mm + 64 * C)[lane];
+          const uint2 nx = reinterpret_cast<const uint2 *>(g_mm + NB1 + 64 * C)[lane];
+          mn0 = min(mn0, mn.x);
+          mn1 = min(mn1, mn.y);
+          nx0 = min(nx0, nx.x);
+          nx1 = min(nx1, nx.y);
+        }
       }
       const unsigned long long fi = below + warp_incl_scan(f.x + f.y), fe = fi - f.x - f.y;
-      if (blockIdx.x == 0 && lane == 0) prof[34] = gtimer();  // fine buckets loaded and scanned
+      PROBE(if (blockIdx.x == 0 && lane == 0) prof[34] = gtimer();)  // fine buckets loaded and scanned
       const uint32_t n1 = __ballot_sync(0xFFFFFFFFu, fi > budget);  // nonzero: the coarse bucket crosses
       const uint32_t n0 = __ballot_sync(0xFFFFFFFFu, fe + f.x > budget);
       const int Lf = __ffs(n1) - 1;
@@ -273,7 +366,7 @@ __device__ void select_level1_warp(const unsigned long long *g_hist, const unsig
     }
   }
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) prof[35] = gtimer();  // select barrier passed
+  PROBE(if (blockIdx.x == 0 && threadIdx.x == 0) prof[35] = gtimer();)  // select barrier passed
   const uint32_t b = s1_b;
   if (b == 0xFFFFFFFFu) {
     sel.all_fit = 1;
@@ -282,11 +375,13 @@ __device__ void select_level1_warp(const unsigned long long *g_hist, const unsig
     sel.rem = budget - s1_tot;
   } else {
     sel.below = s1_prev;
-    sel.prefix |= b << 19;
-    const bool int_single = imode && ((b >> 4) <= 131u || b == 0xFF0u);
-    const bool single = int_single || (g_mm != nullptr && s1_min == ~s1_nmax);
+    // integer mode: value buckets below IB_EXACT and the +inf bucket hold one distance each;
+    // a multi-valued bucket refines on the float bits (bits >> 19 == b + 160)
+    sel.prefix |= (imode ? b + 160u : b) << 19;
+    const bool int_single = imode && (b < IB_EXACT || b == IB_INF);
+    const bool single = int_single || (mm && s1_min == ~s1_nmax);
     if (single) {
-      sel.dstar = int_single ? (b << 19) : s1_min;
+      sel.dstar = int_single ? (b == IB_INF ? 0x7F800000u : __float_as_uint((float)b)) : s1_min;
       sel.rem = budget - sel.below;
       sel.done = 1;
       sel.level_res = 1;
@@ -297,8 +392,8 @@ __device__ void select_level1_warp(const unsigned long long *g_hist, const unsig
 }
 
 // Boundary bucket of histogram level `level` (every CTA computes the same result).
-__device__ void select_level(const unsigned long long *g_hist, const uint32_t *g_mm, int level,
-                             unsigned long long budget, Sel &sel, bool imode = false) {
+__device__ void select_level(const WorldPtrs &W, int par, int level, unsigned long long budget, Sel &sel,
+                             bool imode = false) {
   const int nb = level == 1 ? NB1 : (level == 2 ? 1024 : 512);
   const int shift = level == 1 ? 19 : (level == 2 ? 9 : 0);
   const int per = nb / FT;  // 4, 1 or 0 (level 3: threads < 512)
@@ -313,13 +408,17 @@ __device__ void select_level(const unsigned long long *g_hist, const uint32_t *g
 #pragma unroll
   for (int k = 0; k < 4; ++k) {  // all loads at once (min / max with the bytes: no second round trip)
     if (k < mine) {
-      hv[k] = g_hist[b0 + k];
-      if (g_mm) {
-        mnv[k] = g_mm[b0 + k];
-        nmxv[k] = g_mm[nb + b0 + k];
+      mnv[k] = nmxv[k] = 0xFFFFFFFFu;
+      for (uint32_t r = 0; r < W.nw; ++r) {  // the world's sums
+        hv[k] += (level == 2 ? W.h2[r] : W.h3[r])[1024 * par + b0 + k];
+        if (level == 2) {
+          mnv[k] = min(mnv[k], W.m2[r][2048 * par + b0 + k]);
+          nmxv[k] = min(nmxv[k], W.m2[r][2048 * par + nb + b0 + k]);
+        }
       }
     }
   }
+  const bool g_mm = level == 2;
 #pragma unroll
   for (int k = 0; k < 4; ++k) loc += hv[k];
   const unsigned long long ex = block_excl_scan<unsigned long long, FT>(loc, &sh_tot);
@@ -348,7 +447,7 @@ __device__ void select_level(const unsigned long long *g_hist, const uint32_t *g
     // integer distances (level 1, no min / max kept): a bucket of exponent <= 4 (d < 32),
     // the zero bucket and the +inf bucket each hold one value, bits = b << 19
     const bool int_single = imode && level == 1 && ((b >> 4) <= 131u || b == 0xFF0u);
-    const bool single = int_single || (g_mm != nullptr && sh_min == ~sh_nmax);
+    const bool single = int_single || (g_mm && sh_min == ~sh_nmax);
     if (level == 3 || single) {
       sel.dstar = (level == 3) ? sel.prefix : (int_single ? (b << 19) : sh_min);
       sel.rem = budget - sel.below;
@@ -472,17 +571,50 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   // exit and wait (above) for this grid's completion before touching any state
   asm volatile("griddepcontrol.launch_dependents;");
   const Params &p = sp;
-  const InstArgs A = {I.now, (int)I.parity, I.epoch, I.tile, I.tile / 32};
+  const InstArgs A = {I.now, (int)I.parity, I.epoch, I.tile, I.tile / 32, B.fastok};
   const Dev &d = p.d;
-  GridBar grid{d.f_bar + A.parity, 0u, G};
-  if (c == 0 && threadIdx.x == 0) d.f_bar[A.parity ^ 1] = 0u;  // for launch L+1
+  // the world this instance is a rank of (its peers' arrays), or itself
+  __shared__ WorldPtrs sw;
+  const uint32_t nw = MAXB == 1 ? 1u : B.wsize, rank = MAXB == 1 ? 0u : gi % nw;
+  if (threadIdx.x < nw) {
+    const Dev &q = nw == 1 ? d : B.inst[gi - rank + threadIdx.x].params->d;
+    sw.h1[threadIdx.x] = q.f_hist1;
+    sw.h2[threadIdx.x] = q.f_hist2;
+    sw.h3[threadIdx.x] = q.f_hist3;
+    sw.m1[threadIdx.x] = q.f_mm1;
+    sw.m2[threadIdx.x] = q.f_mm2;
+    sw.acc[threadIdx.x] = q.f_acc;
+    sw.hdr[threadIdx.x] = q.header;
+    if (threadIdx.x == 0) {
+      sw.nw = nw;
+      sw.rank = rank;
+    }
+  }
+  __shared__ unsigned int *sw_bar;  // rank 0's world-barrier counters
+  if (threadIdx.x == 32) sw_bar = (nw == 1 ? d.f_bar : B.inst[gi - rank].params->d.f_bar) + 2;
+  __syncthreads();
+  const WorldPtrs &W = sw;
+  GridBar wgrid{sw_bar + A.parity, 0u, nw * G};              // every CTA of the world
+  if (c == 0 && threadIdx.x == 0) {
+    d.f_bar[A.parity ^ 1] = 0u;  // for launch L+1
+    if (rank == 0) sw_bar[A.parity ^ 1] = 0u;
+    // header fields summed by every CTA after B1 (fast list placement) or written after B4
+    unsigned long long *H = d.header;
+    H[H_N_PF] = 0ull;
+    H[H_N_EV] = 0ull;
+    H[H_H2D] = 0ull;
+    H[H_D2H] = 0ull;
+    H[H_KEPT] = 0ull;
+    H[H_N_ELIG] = 0ull;
+    H[H_STATUS] = 0ull;
+  }
   unsigned long long *prof = d.f_prof;
-  if (threadIdx.x == 0) {
+  PROBE(if (threadIdx.x == 0) {
     const unsigned long long t = gtimer();
     atomicMin(&prof[0], t);
     atomicMax(&prof[15], t);  // last CTA past the dependency wait
     if (c == 0) prof[2] = t;
-  }
+  })
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const FSmem s = carve(smem_raw, A.tile, A.tw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -524,6 +656,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   const uint32_t *bm_tile = bm_old + base / 32;
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_tile[w] : 0u;
   clear_hist(s.h, NB1);
+  if (imode)  // [2 * NB1, 3 * NB1): eligible counts per bucket (non-resident | resident << 16)
+    for (int b = threadIdx.x; b < NB1; b += FT) s.h[2 * NB1 + b] = 0u;  // (4 per thread)
+  // this CTA's eligible agents in multi-valued integer buckets (placed by one CTA, fast path)
+  constexpr uint32_t LOVF = 32;
+  __shared__ uint4 s_ovf[LOVF];
+  __shared__ uint32_t s_novf;
+  if (threadIdx.x == 0) s_novf = 0;
   // chunk counters: [0,4) zero-distance bytes, [4,11) P4 sums, [20,24) P3 tie prefix
   __shared__ uint32_t sacc[24];
   if (threadIdx.x < 24) sacc[threadIdx.x] = 0;
@@ -573,10 +712,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       s.dirty_w[wd] = db;
     }
     if (elig) {
-      const uint32_t q = slot1(bits >> 19);
+      const uint32_t q = (FAST || imode) ? ibucket(bits) : slot1(bits >> 19);
       atomicAdd(&s.h[q], rj.y & 0xFFFFu);
       atomicAdd(&s.h[NB1 + q], rj.y >> 16);
-      if (!FAST && !imode) {  // min / max key only where a bucket can hold several distances
+      if (FAST || imode) {  // eligible counts by residency (fast list placement)
+        atomicAdd(&s.h[2 * NB1 + q], res ? 0x10000u : 1u);
+        if (ib_multi(q)) {  // rare: a multi-valued bucket
+          const uint32_t j = atomicAdd(&s_novf, 1u);
+          if (j < LOVF) s_ovf[j] = make_uint4(bits, (uint32_t)(p.shard_begin + base + k), res ? 1u : 0u, 0u);
+        }
+      } else {  // min / max key only where a bucket can hold several distances
         atomicMin(&s.h[2 * NB1 + q], bits);
         atomicMin(&s.h[3 * NB1 + q], ~bits);
       }
@@ -586,23 +731,15 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   using T_ = std::true_type;
   using F_ = std::false_type;
   const bool fast = imode && !xdist && now32 && gkeys == nullptr;
+  // one record body per variant (always masked; a rolled loop): the kernel's executed code has
+  // to stay small (instruction-fetch stalls, see PROBE)
   auto batch = [&](uint4 (&rr)[LOAD_BATCH], uint32_t k0) {
-    if (k0 + LOAD_BATCH * FT <= n_here) {  // every record of the batch exists (CTA-uniform)
-      if (fast) {
 #pragma unroll
-        for (int j = 0; j < LOAD_BATCH; ++j) record(rr[j], (k0 + j * FT) / 32 + warp, F_(), T_());
-      } else {
-#pragma unroll
-        for (int j = 0; j < LOAD_BATCH; ++j) record(rr[j], (k0 + j * FT) / 32 + warp, F_(), F_());
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < LOAD_BATCH; ++j) {
-        const uint32_t wd = (k0 + j * FT) / 32 + warp;  // this warp's residency word (k & 31 == lane)
-        if (wd >= A.tw) continue;                        // warp-uniform
-        if (fast) record(rr[j], wd, T_(), T_());
-        else record(rr[j], wd, T_(), F_());
-      }
+    for (int j = 0; j < LOAD_BATCH; ++j) {
+      const uint32_t wd = (k0 + j * FT) / 32 + warp;  // this warp's residency word (k & 31 == lane)
+      if (wd >= A.tw) continue;                        // warp-uniform
+      if (fast) record(rr[j], wd, T_(), T_());
+      else record(rr[j], wd, T_(), F_());
     }
   };
   // two batches in flight: the next one's loads go out before the current one is processed
@@ -610,6 +747,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   uint4 r2[LOAD_BATCH];
   const uint32_t BS = LOAD_BATCH * FT, nk = A.tw * 32;
   load_into(r, 0);
+#ifdef AB_P1_UNROLL2  // A/B: the two batches of a loop iteration as separate code copies
   for (uint32_t k0 = 0; k0 < nk; k0 += 2 * BS) {
     if (k0 + BS < nk) load_into(r2, k0 + BS);
     batch(r, k0);
@@ -617,14 +755,43 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     if (k0 + 2 * BS < nk) load_into(r, k0 + 2 * BS);
     batch(r2, k0 + BS);
   }
+#else
+#pragma unroll 1
+  for (uint32_t k0 = 0; k0 < nk; k0 += BS) {
+    if (k0 + BS < nk) load_into(r2, k0 + BS);
+    batch(r, k0);
+#pragma unroll
+    for (int j = 0; j < LOAD_BATCH; ++j) r[j] = r2[j];
+  }
+#endif
   if (!imode) warp_add_u64(zero_b, sacc);
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&prof[25], gtimer());  // P1 loop done
+  STAMP_MAX(25)  // P1 loop done
   // this CTA's level-1 bytes: dense row (its column entry gives the tie prefix in P3) and
   // the global sum
   publish_hist(s.h, NB1, d.f_hist1 + NB1 * par, imode ? nullptr : d.f_mm1 + 2 * NB1 * par,
-               d.f_rows1 + (uint64_t)c * NB1, d.f_hist1 + 2 * NB1 + 64 * par);
-  if (threadIdx.x == 0) atomicMax(&prof[26], gtimer());  // published
+               d.f_rows1 + (uint64_t)c * NB1, d.f_hist1 + 2 * NB1 + 64 * par, !imode);
+  // bucket owners (fast list placement): CTA o owns buckets [o RB, (o + 1) RB)
+  const uint32_t RB = ((NB1 + G - 1) / G + 3u) & ~3u;
+  const uint32_t o_lo = min((uint32_t)NB1, c * RB), o_n = min((uint32_t)NB1, o_lo + RB) - o_lo;
+  const uint32_t QP = (G + 31) / 32;  // CTAs per lane in a column scan
+  if (imode) {
+    // this CTA's eligible counts per bucket: one dense row (16 KB, every launch)
+    if (G > 1)
+      reinterpret_cast<uint4 *>(d.f_crow + ((uint64_t)par * G + c) * NB1)[threadIdx.x] =
+          reinterpret_cast<const uint4 *>(s.h + 2 * NB1)[threadIdx.x];  // (NB1 / 4 == FT)
+    const uint32_t nov = s_novf;  // (CTA-uniform: the P1 loop ended with a barrier)
+    if (nov) {
+      __shared__ unsigned long long s_ovbase;
+      if (threadIdx.x == 0)  // more than this CTA can stage: push the count past the cap
+        s_ovbase = atomicAdd(&acc[6], nov <= LOVF ? (unsigned long long)nov : FUSED_OVF_CAP + 1ull);
+      __syncthreads();
+      const unsigned long long ob = s_ovbase;
+      if (threadIdx.x < nov && nov <= LOVF && ob + threadIdx.x < FUSED_OVF_CAP)
+        d.f_ovf[(uint64_t)par * FUSED_OVF_CAP + ob + threadIdx.x] = s_ovf[threadIdx.x];
+    }
+  }
+  STAMP_MAX(26)  // published
   st = __reduce_or_sync(0xFFFFFFFFu, st);
   if (lane == 0 && st) atomicOr(reinterpret_cast<unsigned int *>(&acc[5]), st);
   if (threadIdx.x == 0) {
@@ -633,10 +800,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     const unsigned long long zb = imode ? ((unsigned long long)s.h[NB1] << 16) + s.h[0] : parts_u64(sacc);
     if (zb) atomicAdd(&acc[0], zb);
   }
-  if (threadIdx.x == 0) atomicMax(&prof[11], gtimer());
-  if (c == 0 && threadIdx.x == 0) prof[3] = gtimer();
-  grid.sync();
-  if (c == 0 && threadIdx.x == 0) prof[4] = gtimer();
+  STAMP_MAX(11)
+  STAMP0(3)
+  wgrid.sync();  // (the world's CTAs: every instance's own when nw == 1)
+  STAMP0(4)
 
   // ---------------- P2: select
   {  // clear the other parity's accumulators for the next launch, spread over the CTAs
@@ -657,11 +824,26 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
     if (gt < 8) d.f_acc[8 * q + gt] = 0;
   }
-  const uint32_t *mm1 = d.f_mm1 + 2 * NB1 * par;
+  // bucket owner: this CTA's range of every CTA's count row, staged while warp 0 selects
+  const bool owners = imode && A.fastok && G > 1;
+  if (owners && warp > 0) {
+    const uint32_t ch = o_n / 4;  // 16-byte chunks per CTA row segment
+    for (uint32_t x = threadIdx.x - 32; x < G * ch; x += FT - 32) {
+      const uint32_t q = x / ch, k = x - q * ch;
+      cp_async16(s.col + q * RB + 4 * k, d.f_crow + ((uint64_t)par * G + q) * NB1 + o_lo + 4 * k);
+    }
+    cp_async_commit();
+  }
+  __shared__ unsigned long long sh_novf;  // eligible agents in multi-valued buckets (all CTAs)
+  if (threadIdx.x == 32) {  // (warp 0 runs the select)
+    unsigned long long v = 0;
+    if (imode)  // the world's: the fast list decision must agree across its ranks
+      for (uint32_t r = 0; r < nw; ++r) v += W.acc[r][8 * par + 6];
+    sh_novf = v;
+  }
   Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 1, 0};
-  if (c == 0 && threadIdx.x == 0) prof[32] = gtimer();  // other parity cleared
-  select_level1_warp(d.f_hist1 + NB1 * par, d.f_hist1 + 2 * NB1 + 64 * par, imode ? nullptr : mm1, p.budget, sel,
-                     imode, prof);
+  STAMP0(32)  // other parity cleared
+  select_level1_warp(W, par, p.budget, sel, imode, prof);
   for (int level = 2; level <= 3 && !sel.done; ++level) {
     const int hi_shift = level == 2 ? 19 : 9, shift = level == 2 ? 9 : 0;
     const int nb = level == 2 ? 1024 : 512;
@@ -677,22 +859,145 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     unsigned long long *gh = level == 2 ? d.f_hist2 + 1024 * par : d.f_hist3 + 1024 * par;
     uint32_t *gm = level == 2 ? d.f_mm2 + 2048 * par : nullptr;
     publish_hist(s.h, nb, gh, gm, (level == 2 ? d.f_rows2 : d.f_rows3) + (uint64_t)c * 1024);
-    grid.sync();
-    select_level(gh, gm, level, p.budget, sel);
+    wgrid.sync();  // (the world's CTAs: every instance's own when nw == 1)
+    select_level(W, par, level, p.budget, sel);
   }
   const bool all_fit = sel.all_fit;
   const uint32_t dstar = sel.dstar;
-  if (c == 0 && threadIdx.x == 0) prof[9] = gtimer();
+  STAMP0(9)
 
-  // ---------------- P3: tie group: id-order prefix of the bytes at d == D*
+  // ---------------- fast list placement (integer distances; grid-uniform decision).  With the
+  // boundary D* in a single-valued bucket b* (or everything kept), a list member's position
+  // is known from counts published before B1: prefetch members (eligible non-residents kept)
+  // of bucket b <= b* sit at  sum_{b' < b} NR[b'] + NR of b in the preceding CTAs + its rank
+  // in this CTA (ascending id); evict members (residents not kept) of bucket b >= b* at
+  // sum_{b' > b} R[b'] + R of b in the following CTAs + its rank (descending id).  At b* the
+  // tie cut is an id prefix, so CTAs before the cut keep all their ties and CTAs after it keep
+  // none: the same column sums hold there.  Agents in multi-valued buckets (rare, at most
+  // FUSED_OVF_CAP) are ranked by one CTA.  No second grid barrier.
+#ifdef AB_NO_FAST  // A/B experiments only (tools/)
+  const bool fastp = false;
+#else
+  const bool fastp = imode && A.fastok && sh_novf <= FUSED_OVF_CAP &&
+                     (all_fit || (sel.level_res == 1 && (sel.b_res < IB_EXACT || sel.b_res == IB_INF)));
+#endif
+  if (c == 0 && threadIdx.x == 0) atomicAdd(&prof[fastp ? 48 : 49], 1ull);  // launches per list path
+  const uint32_t bs = all_fit ? (uint32_t)NB1 : sel.b_res;  // boundary bucket (NB1: every eligible agent kept)
+  uint32_t *const lcnt = s.h + 2 * NB1;  // this CTA's eligible counts per bucket (P1)
+  uint32_t *const need = s.h + 3 * NB1;  // buckets where this CTA has list members
+  const uint32_t ep = A.epoch & 0xFFFFu;  // tags the owners' published offsets of this launch
+  __shared__ uint32_t sh_m;
+  uint32_t m_need = 0;
+  // P3's load of the preceding CTAs' tie bytes goes out first (its latency hides behind the
+  // owner pass)
   unsigned long long t_rows = 0;  // preceding CTAs' bytes in the resolving bucket (published rows)
   if (!all_fit && threadIdx.x < c) {
     const unsigned long long *rows = sel.level_res == 1 ? d.f_rows1 : (sel.level_res == 2 ? d.f_rows2 : d.f_rows3);
     const uint32_t stride = sel.level_res == 1 ? NB1 : 1024;
     t_rows = rows[(uint64_t)threadIdx.x * stride + sel.b_res];
   }
+  // ... and the lower ranks' bytes at D* (rank r owns the r-th contiguous id range of the world)
+  if (!all_fit && warp == FWARPS - 1 && lane < rank) {
+    const unsigned long long *hh = sel.level_res == 1 ? W.h1[lane] + NB1 * par
+                                                      : (sel.level_res == 2 ? W.h2[lane] : W.h3[lane]) + 1024 * par;
+    t_rows = hh[sel.b_res];
+  }
+  if (owners) {
+    cp_async_wait_all();
+    __syncthreads();
+    STAMP_MAX(40)  // owner staging landed
+    if (fastp) {
+      // Bucket owner pass (this CTA's range of RB buckets, every CTA's counts staged in s.col):
+      // for bucket b and CTA q, the prefetch offset  W_nr(b) + sum_{q' < q} nr_q'(b)  and the
+      // evict offset  W_r(b) + sum_{q' > q} r_q'(b), relative to the range start (W: the range's
+      // buckets before b ascending / after b descending), published tagged with the launch
+      // epoch; and the range totals.  Consumers add the range starts.
+      uint32_t *tn = s.col + G * RB, *tr = tn + RB, *wn = tr + RB, *wr = wn + RB;
+      for (uint32_t j = warp; j < o_n; j += FWARPS) {  // totals over the CTAs
+        uint32_t a = 0, e = 0;
+        for (uint32_t i = 0; i < QP; ++i) {
+          const uint32_t q = lane * QP + i;
+          if (q < G) {
+            const uint32_t v = s.col[q * RB + j];
+            a += v & 0xFFFFu;
+            e += v >> 16;
+          }
+        }
+        a = __reduce_add_sync(0xFFFFFFFFu, a);
+        e = __reduce_add_sync(0xFFFFFFFFu, e);
+        if (lane == 0) {
+          tn[j] = a;
+          tr[j] = e;
+        }
+      }
+      __syncthreads();
+      STAMP_MAX(46)  // owner pass 1
+      if (warp == 0) {  // offsets of the buckets within the range, and the range totals
+        const uint32_t JP = (o_n + 31) / 32;
+        uint32_t sa = 0, se = 0;
+        for (uint32_t i = 0; i < JP; ++i) {
+          const uint32_t j = lane * JP + i;
+          if (j < o_n) {
+            sa += tn[j];
+            se += tr[j];
+          }
+        }
+        const uint32_t ia = warp_incl_scan(sa), ie = warp_incl_scan(se);
+        const uint32_t TA = __shfl_sync(0xFFFFFFFFu, ia, 31), TE = __shfl_sync(0xFFFFFFFFu, ie, 31);
+        uint32_t ra = ia - sa, re = ie - se;
+        for (uint32_t i = 0; i < JP; ++i) {
+          const uint32_t j = lane * JP + i;
+          if (j < o_n) {
+            wn[j] = ra;
+            ra += tn[j];
+            re += tr[j];
+            wr[j] = TE - re;
+          }
+        }
+        if (lane == 0) st_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + c], pack_ep(ep, TA, TE));
+      }
+      __syncthreads();
+      STAMP_MAX(47)  // owner range scan
+      for (uint32_t j = warp; j < o_n; j += FWARPS) {  // per-CTA offsets: 32 consecutive CTAs per store
+        const uint32_t w_n = wn[j], w_r = wr[j], t_r = tr[j];
+        unsigned long long *P = d.f_pos + ((uint64_t)par * NB1 + o_lo + j) * FUSED_MAX_CTAS;
+        uint32_t ca = 0, ce = 0;  // running sums over the previous 32-CTA chunks
+        for (uint32_t q0 = 0; q0 < G; q0 += 32) {
+          const uint32_t q = q0 + lane;
+          const uint32_t v = q < G ? s.col[q * RB + j] : 0u;
+          const uint32_t a = v & 0xFFFFu, e = v >> 16;
+          const uint32_t ia = warp_incl_scan(a), ie = warp_incl_scan(e);
+          // prefetch: CTAs before q; evict: CTAs after q (total minus inclusive prefix)
+          if (q < G) st_relaxed_u64(&P[q], pack_ep(ep, w_n + ca + ia - a, w_r + t_r - (ce + ie)));
+          ca += __shfl_sync(0xFFFFFFFFu, ia, 31);
+          ce += __shfl_sync(0xFFFFFFFFu, ie, 31);
+        }
+      }
+    }
+  }
+  STAMP_MAX(41)  // owner pass done
+  if (fastp && G > 1) {
+    // the buckets where this CTA has list members (multi-valued ones go to the overflow CTA)
+    if (threadIdx.x == 0) sh_m = 0;
+    __syncthreads();
+#pragma unroll 1
+    for (uint32_t b = threadIdx.x; b < NB1; b += FT) {
+      const uint32_t v = lcnt[b];
+      const bool nd = !ib_multi(b) && (b < bs ? (v & 0xFFFFu) != 0u : (b > bs ? (v >> 16) != 0u : v != 0u));
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, nd);
+      uint32_t j0 = 0;
+      if (lane == 0 && bal) j0 = atomicAdd(&sh_m, (uint32_t)__popc(bal));
+      j0 = __shfl_sync(0xFFFFFFFFu, j0, 0);
+      if (nd) need[j0 + __popc(bal & lanemask_lt())] = b;
+    }
+    __syncthreads();
+    m_need = sh_m;
+  }
+  STAMP_MAX(42)  // need list
+
+  // ---------------- P3: tie group: id-order prefix of the bytes at d == D*
   unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw]
-#pragma unroll 2
+#pragma unroll 1
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
     const bool tie = !all_fit && ((s.elig_w[w] >> lane) & 1u) && s.keys[k] == dstar;
@@ -703,32 +1008,34 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   __syncthreads();
   // exclusive scan over the tile's words (tw <= FUSED_MAX_TILE / 32 <= FT: one word per
   // thread) and, in the same pass, the preceding CTAs' total
-  if (warp * 32 < c) warp_add_u64(t_rows, sacc + 20);  // preceding CTAs' total (threads < c)
+  if (warp * 32 < c || (warp == FWARPS - 1 && rank > 0)) warp_add_u64(t_rows, sacc + 20);  // preceding CTAs' and ranks' total
   {
     const uint32_t w = threadIdx.x;
     unsigned long long v[1] = {w < A.tw ? word_tie[w] : 0ull}, tt[1];
-    block_excl_scan_v<unsigned long long, 1, FT>(v, tt);  // (its barriers complete the sum)
+    cta_scan1(v, tt);  // (its barriers complete the sum)
     if (w < A.tw) word_tie[w] = v[0];
     if (threadIdx.x == 0) word_tie[A.tw] = tt[0];  // (memb holds tile / 2 >= tw + 1 words of 64 bits)
   }
   const unsigned long long sh_tie_excl = parts_u64(sacc + 20);
   __syncthreads();
-  if (c == 0 && threadIdx.x == 0) prof[10] = gtimer();
-  if (threadIdx.x == 0) atomicMax(&prof[14], gtimer());
+  STAMP0(10)
+  STAMP_MAX(14)
 
   // ---------------- P4: emit
   uint32_t *cnt_pf = s.h, *cnt_ev = s.h + NBL;  // per-CTA list members per list bucket
   uint32_t *lor_l = s.h + 6 * NBL;   // [2][NBL]: OR of the key bits below the list bucket
   uint32_t *mm_l = s.h + 10 * NBL;  // [4][NBL]: prefetch min, prefetch ~max, evict min, evict ~max
-  for (int b = threadIdx.x; b < 2 * NBL; b += FT) {
-    s.h[b] = 0;
-    lor_l[b] = 0;
+  if (!fastp) {
+    for (int b = threadIdx.x; b < 2 * NBL; b += FT) {
+      s.h[b] = 0;
+      lor_l[b] = 0;
+    }
+    for (int b = threadIdx.x; b < 4 * NBL; b += FT) mm_l[b] = 0xFFFFFFFFu;
   }
-  for (int b = threadIdx.x; b < 4 * NBL; b += FT) mm_l[b] = 0xFFFFFFFFu;
   __syncthreads();
   unsigned long long h2d = 0, tie_kept = 0;
   uint32_t n_el = 0;
-#pragma unroll 2
+#pragma unroll 1
   for (uint32_t w = warp; w < A.tw; w += FWARPS) {
     const uint32_t k = w * 32 + lane;
     const uint32_t elw = s.elig_w[w];  // 0 beyond n_here
@@ -767,7 +1074,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       s.ev_w[w] = evw;
       n_el += __popc(elw);
     }
-    if (pfw | evw) {  // list members in this word
+    if (fastp) {
+      if ((pfw >> lane) & 1u) h2d += s.fp[k];
+    } else if (pfw | evw) {  // list members in this word (slow path: list-bucket counts)
       const uint32_t bk = key >> 21;
       if ((pfw >> lane) & 1u) {
         h2d += s.fp[k];
@@ -785,7 +1094,221 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&prof[27], gtimer());  // P4 word loop done
+  STAMP_MAX(27)  // P4 word loop done
+  if (fastp) {
+    uint32_t *const h32 = s.h;  // [0, NB1): prefetch positions, [NB1, 2 NB1): evict positions
+    __shared__ uint32_t sh_spf, sh_sev, sh_fpf, sh_fev;
+    // write-back bytes (R13) of this tile's dirty evicted agents: up to two loads per word
+    // issued now into registers, consumed at the end
+    uint32_t wbm = 0, wb0 = 0, wb1 = 0;
+    if (threadIdx.x < A.tw) {
+      wbm = s.ev_w[threadIdx.x] & s.dirty_w[threadIdx.x];
+      const uint32_t *wbw = d.wb_bytes + base + 32 * threadIdx.x;
+      if (wbm) {
+        wb0 = wbw[__ffs(wbm) - 1];
+        wbm &= wbm - 1;
+      }
+      if (wbm) {
+        wb1 = wbw[__ffs(wbm) - 1];
+        wbm &= wbm - 1;
+      }
+    }
+    warp_add_u44(h2d, sacc + 4);
+    warp_add_u44(tie_kept, sacc + 8);
+    if (lane == 0 && n_el) atomicAdd(&sacc[10], n_el);
+    __shared__ uint32_t sh_mvpf, sh_mvev;  // list starts of the multi-valued buckets' members
+    if (G > 1) {
+      // range starts from the owners' range totals: prefetch ascending, evict descending
+      uint32_t *rps = s.col, *rpe = s.col + G;  // (the owner staging is free)
+      // this thread's first list bucket: its offsets load goes out with the range totals'
+      const unsigned long long *Pc = d.f_pos + (uint64_t)par * NB1 * FUSED_MAX_CTAS + c;
+      const unsigned long long pv0 = threadIdx.x < m_need ? ld_relaxed_u64(Pc + (uint64_t)need[threadIdx.x] * FUSED_MAX_CTAS) : 0ull;
+      unsigned long long rv = 0;
+      if (threadIdx.x < G) rv = poll_ep(&d.f_rt[par * FUSED_MAX_CTAS + threadIdx.x], ep, d.header);
+      const uint32_t ra = (uint32_t)(rv >> 24) & 0xFFFFFFu, re = (uint32_t)rv & 0xFFFFFFu;
+      unsigned long long pk[1] = {(unsigned long long)ra | ((unsigned long long)re << 32)}, tt[1];
+      cta_scan1(pk, tt);
+      const uint32_t r_tot = (uint32_t)(tt[0] >> 32);
+      if (threadIdx.x < G) {
+        rps[threadIdx.x] = (uint32_t)pk[0];
+        rpe[threadIdx.x] = r_tot - (uint32_t)(pk[0] >> 32) - re;
+      }
+      __syncthreads();
+      // positions of this CTA's first member in each of its list buckets
+      for (uint32_t j = threadIdx.x; j < m_need; j += FT) {
+        const uint32_t b = need[j];
+        unsigned long long v = j == threadIdx.x ? pv0 : ld_relaxed_u64(Pc + (uint64_t)b * FUSED_MAX_CTAS);
+        if ((uint32_t)(v >> 48) != ep) v = poll_ep(Pc + (uint64_t)b * FUSED_MAX_CTAS, ep, d.header);
+        h32[b] = rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
+        h32[NB1 + b] = rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
+      }
+      auto pos_pf = [&](uint32_t b) {  // sum_{b' < b} NR[b']
+        const unsigned long long v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS], ep, d.header);
+        return rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
+      };
+      auto pos_ev = [&](uint32_t b) {  // sum_{b' > b} R[b']
+        const unsigned long long v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS + G - 1], ep, d.header);
+        return rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
+      };
+      if (c == 0 && threadIdx.x == 0) {
+        sh_spf = bs < (uint32_t)NB1 ? pos_pf(bs) : (uint32_t)tt[0];
+        sh_sev = bs < (uint32_t)NB1 ? pos_ev(bs) : 0u;
+      }
+      if (c == G - 1 && threadIdx.x == 32) {
+        sh_mvpf = pos_pf(IB_EXACT);
+        sh_mvev = pos_ev(IB_INF - 1);
+      }
+    } else {
+      // one CTA: its counts are the totals (S_pf(b) = sum_{b' < b} NR, S_ev(b) = sum_{b' > b} R)
+      uint32_t tv[4];
+      unsigned long long loc = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        tv[k] = lcnt[4 * threadIdx.x + k];
+        loc += (unsigned long long)(tv[k] & 0xFFFFu) | ((unsigned long long)(tv[k] >> 16) << 32);
+      }
+      unsigned long long ex[1] = {loc}, tt[1];
+      cta_scan1(ex, tt);
+      const uint32_t r_tot = (uint32_t)(tt[0] >> 32);
+      unsigned long long run = ex[0];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t b = 4 * threadIdx.x + k;
+        run += (unsigned long long)(tv[k] & 0xFFFFu) | ((unsigned long long)(tv[k] >> 16) << 32);
+        const uint32_t spf = (uint32_t)run - (tv[k] & 0xFFFFu), sev = r_tot - (uint32_t)(run >> 32);
+        h32[b] = spf;
+        h32[NB1 + b] = sev;
+        if (b == bs) {
+          sh_spf = spf;
+          sh_sev = sev;
+        }
+        if (b == IB_EXACT) sh_mvpf = spf;
+        if (b == IB_INF - 1) sh_mvev = sev;
+      }
+      if (bs == (uint32_t)NB1 && threadIdx.x == 0) {
+        sh_spf = (uint32_t)tt[0];
+        sh_sev = 0;
+      }
+    }
+    __syncthreads();
+    STAMP_MAX(17)  // positions ready
+    // this tile's members in list order (prefetch ascending id, evict descending id)
+    {
+      const uint32_t w = threadIdx.x;
+      const uint32_t pw = w < A.tw ? s.pf_w[w] : 0u, ew = w < A.tw ? s.ev_w[w] : 0u;
+      unsigned long long pv[1] = {(unsigned long long)__popc(pw) | ((unsigned long long)__popc(ew) << 32)}, pt[1];
+      cta_scan1(pv, pt);
+      const uint32_t vp = (uint32_t)pv[0], ve = (uint32_t)(pv[0] >> 32);
+      const uint32_t tp = (uint32_t)pt[0], te = (uint32_t)(pt[0] >> 32);
+      if (threadIdx.x == 0) {
+        sh_fpf = tp;
+        sh_fev = te;
+      }
+      // (bucket << 16 | local index: tile < 2^16)
+      uint32_t m = pw, o = vp;
+      while (m) {
+        const uint32_t k = w * 32 + __ffs(m) - 1;
+        s.memb[o++] = (ibucket(s.keys[k]) << 16) | k;
+        m &= m - 1;
+      }
+      m = ew;
+      o = tp + te - 1 - ve;
+      while (m) {
+        const uint32_t k = w * 32 + __ffs(m) - 1;
+        s.memb[o--] = (ibucket(s.keys[k]) << 16) | k;
+        m &= m - 1;
+      }
+    }
+    __syncthreads();
+    STAMP_MAX(38)  // member lists
+    const uint32_t m_pf = sh_fpf, m_ev = sh_fev;
+    // positions: warp 0 the prefetch members, warp 1 the evict members, 32 at a time in list
+    // order; the bucket positions serve as cursors
+    if (warp < 2) {
+      const uint32_t m = warp == 0 ? m_pf : m_ev;
+      const uint32_t *mem = s.memb + (warp == 0 ? 0u : m_pf);
+      uint32_t *cur = h32 + (warp == 0 ? 0u : (uint32_t)NB1);
+      uint32_t *out = warp == 0 ? d.pf_ids : d.ev_ids;
+      uint32_t nb = 0;
+      for (uint32_t e0 = 0; e0 < m; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const uint32_t bk = e < m ? mem[e] : 0xFFFFFFFFu;
+        const uint32_t k = bk & 0xFFFFu, b = e < m ? bk >> 16 : 0xFFFFFFFFu;
+        const bool on = e < m && !ib_multi(b);
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, on ? b : 0xFFFFFFFFu);
+        uint32_t pos = 0;
+        if (on) pos = cur[b] + __popc(peers & lanemask_lt());
+        __syncwarp();
+        if (on && (peers & lanemask_lt()) == 0) cur[b] += __popc(peers);
+        if (on) out[pos] = (uint32_t)(p.shard_begin + base + k);
+        nb += __popc(__ballot_sync(0xFFFFFFFFu, on && b == bs));
+        __syncwarp();
+      }
+      if (lane == 0 && nb) atomicAdd(&d.header[warp == 0 ? H_N_PF : H_N_EV], (unsigned long long)nb);
+      PROBE(if (lane == 0) atomicMax(&prof[43 + warp], gtimer());)
+    } else if (c == G - 1 && sh_novf > 0) {
+      // the agents in multi-valued buckets (all CTAs'): prefetch members (non-residents below
+      // b*) after the value buckets below 2048, evict members (residents above b*) after the
+      // +inf bucket; ranked by (key, id) among themselves
+      __shared__ uint4 s_ov[FUSED_OVF_CAP];
+      const uint32_t nov = (uint32_t)sh_novf;
+      const uint32_t t = threadIdx.x - 64;  // warps 2..31 (named barrier 1)
+      for (uint32_t x = t; x < nov; x += FT - 64) s_ov[x] = d.f_ovf[(uint64_t)par * FUSED_OVF_CAP + x];
+      asm volatile("bar.sync 1, %0;" ::"r"(FT - 64) : "memory");
+      const uint32_t pf0 = sh_mvpf, ev0 = sh_mvev;
+      for (uint32_t x = t; x < nov; x += FT - 64) {
+        const uint4 q = s_ov[x];
+        const uint32_t b = ibucket(q.x);
+        const int lst = (!q.z && b < bs) ? 0 : ((q.z && b > bs) ? 1 : -1);
+        if (lst < 0) continue;
+        uint32_t rank = 0;
+        for (uint32_t u = 0; u < nov; ++u) {
+          const uint4 f = s_ov[u];
+          const uint32_t fb = ibucket(f.x);
+          if (lst == 0 ? (!f.z && fb < bs) : (f.z && fb > bs))
+            rank += lst == 0 ? (f.x < q.x || (f.x == q.x && f.y < q.y)) : (f.x > q.x || (f.x == q.x && f.y > q.y));
+        }
+        if (lst == 0) d.pf_ids[pf0 + rank] = q.y;
+        else d.ev_ids[ev0 + rank] = q.y;
+      }
+    }
+    {
+      unsigned long long d2h = (unsigned long long)wb0 + wb1;
+      while (wbm) {  // (rare: a word with more than two dirty evicted agents)
+        d2h += d.wb_bytes[base + 32 * threadIdx.x + __ffs(wbm) - 1];
+        wbm &= wbm - 1;
+      }
+      warp_add_u44(d2h, sacc + 6);
+    }
+    __syncthreads();
+    STAMP_MAX(39)  // placed
+    if (threadIdx.x == 0) {  // this CTA's sums into the header (zeroed before B1)
+      unsigned long long *H = d.header;
+      const unsigned long long v_h2d = parts_u44(sacc + 4), v_tie = parts_u44(sacc + 8), v_wb = parts_u44(sacc + 6);
+      if (v_h2d) atomicAdd(&H[H_H2D], v_h2d);
+      for (uint32_t r = 0; r < nw; ++r) {  // world-wide fields: into every rank's header
+        if (v_tie) atomicAdd(&W.hdr[r][H_KEPT], v_tie);
+        if (sacc[10]) atomicAdd(&W.hdr[r][H_N_ELIG], (unsigned long long)sacc[10]);
+      }
+      if (v_wb) atomicAdd(&H[H_D2H], v_wb);
+      if (c == 0) {
+        if (sh_spf) atomicAdd(&H[H_N_PF], (unsigned long long)sh_spf);
+        if (sh_sev) atomicAdd(&H[H_N_EV], (unsigned long long)sh_sev);
+        atomicAdd(&H[H_KEPT], p.budget - sel.rem);
+        const uint32_t st0 = d.state->status;
+        uint32_t status = (uint32_t)acc[5] | st0;
+        unsigned long long zb = 0;  // bytes of the world's distance-0 agents
+        for (uint32_t r = 0; r < nw; ++r) zb += W.acc[r][8 * par];
+        if (zb > p.budget) status |= ST_INSUFFICIENT;
+        H[H_CUT_BITS] = all_fit ? 0xFFFFFFFFull : dstar;
+        H[H_CUT_REM] = sel.rem;
+        atomicOr(reinterpret_cast<unsigned int *>(&H[H_STATUS]), status);
+        H[H_SEQ] = H[H_SEQ] + 1;
+      }
+    }
+      STAMP_MAX(1)
+    return;
+  }
   // list bucket totals (global atomics, issued now: they drain while the members are
   // staged); the CTA's min / max key and OR of the low key bits per bucket go to its rows
   {
@@ -826,7 +1349,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     const unsigned long long pk = (unsigned long long)__popc(pw) | ((unsigned long long)__popc(ew) << 16) |
                                   ((unsigned long long)cnt_pf[w] << 32) | ((unsigned long long)cnt_ev[w] << 48);
     unsigned long long pv[1] = {pk}, pt[1];
-    block_excl_scan_v<unsigned long long, 1, FT>(pv, pt);
+    cta_scan1(pv, pt);
     const uint32_t v[4] = {(uint32_t)(pv[0] & 0xFFFFu), (uint32_t)((pv[0] >> 16) & 0xFFFFu),
                            (uint32_t)((pv[0] >> 32) & 0xFFFFu), (uint32_t)(pv[0] >> 48)};
     const uint32_t tt[2] = {(uint32_t)(pt[0] & 0xFFFFu), (uint32_t)((pt[0] >> 16) & 0xFFFFu)};
@@ -851,7 +1374,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&prof[17], gtimer());  // member lists built
+  STAMP_MAX(17)  // member lists built
   const uint32_t m_pf = sh_mpf, m_ev = sh_mev;
   // staging slot of every member (bucket start + rank within its bucket in list order), warp
   // 0 prefetch, warp 1 evict, into fp[]; the bucket offsets serve as cursors (each ends at
@@ -874,7 +1397,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&prof[19], gtimer());  // in-bucket ranks
+  STAMP_MAX(19)  // in-bucket ranks
   // stage (key, id) bucket-major in this tile's range of the staging arrays: bucket b's
   // members at base + off[b] + rank, in list order
   for (uint32_t e = threadIdx.x; e < m_pf + m_ev; e += FT) {
@@ -896,18 +1419,25 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     d.f_cta_cpf[(uint64_t)c * NBL + b] = ((off_pf[b] - cnt_pf[b]) << 16) | cnt_pf[b];
     d.f_cta_cev[(uint64_t)c * NBL + b] = ((off_ev[b] - cnt_ev[b]) << 16) | cnt_ev[b];
   }
-  if (threadIdx.x == 0) atomicMax(&prof[28], gtimer());  // staged, rows published
+  STAMP_MAX(28)  // staged, rows published
   if (threadIdx.x < 4) {
     const unsigned long long v = threadIdx.x < 3 ? parts_u44(sacc + 4 + 2 * threadIdx.x) : sacc[10];
     if (v && threadIdx.x != 1) atomicAdd(&acc[1 + threadIdx.x], v);  // ([2] write-back bytes: end of P5)
   }
   if (c == 0 && threadIdx.x == 0) d.header[H_D2H] = 0ull;  // (summed by every CTA after B4)
-  if (threadIdx.x == 0) atomicMax(&prof[12], gtimer());
-  if (c == 0 && threadIdx.x == 0) prof[5] = gtimer();
-  grid.sync();
-  if (c == 0 && threadIdx.x == 0) prof[6] = gtimer();
+  STAMP_MAX(12)
+  STAMP0(5)
+  wgrid.sync();  // (the world's CTAs: every instance's own when nw == 1)
+  STAMP0(6)
   if (c == 0 && threadIdx.x == 32) {  // header (CTA 0, warp 1): the accumulators are complete; loads first
-    const unsigned long long a0 = acc[0], a1 = acc[1], a3 = acc[3], a4 = acc[4], a5 = acc[5];
+    unsigned long long a0 = 0, a3 = 0, a4 = 0;  // world sums: zero-distance bytes, tie bytes kept, eligible
+    for (uint32_t r = 0; r < nw; ++r) {
+      const unsigned long long *ar = W.acc[r] + 8 * par;
+      a0 += ar[0];
+      a3 += ar[3];
+      a4 += ar[4];
+    }
+    const unsigned long long a1 = acc[1], a5 = acc[5];
     const uint32_t st0 = d.state->status;  // + BAD_KIN/BAD_RECORD of k_int_compact
     unsigned long long *H = d.header;
     const unsigned long long seq = H[H_SEQ];
@@ -921,7 +1451,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     H[H_STATUS] = status;
     H[H_SEQ] = seq + 1;
   }
-  if (threadIdx.x == 0) atomicMax(&prof[30], gtimer());  // B4 passed (last CTA)
+  STAMP_MAX(30)  // B4 passed (last CTA)
 
   // A single-CTA instance (G == 1, the batched replicas of C5) holds every list member in its
   // own staging area, bucket-major (buckets ascending) and in list order within a bucket,
@@ -1011,11 +1541,11 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
                                   ((unsigned long long)(list == 1 ? len[0] + len[1] : 0u) << 21) |
                                   ((unsigned long long)(ns0 + ns1) << 42);
     unsigned long long pv[1] = {pk}, pt[1];
-    block_excl_scan_v<unsigned long long, 1, FT>(pv, pt);
+    cta_scan1(pv, pt);
     const uint32_t M21 = (1u << 21) - 1;
     const uint32_t v[3] = {(uint32_t)(pv[0] & M21), (uint32_t)((pv[0] >> 21) & M21), (uint32_t)(pv[0] >> 42)};
     const uint32_t tt[3] = {(uint32_t)(pt[0] & M21), (uint32_t)((pt[0] >> 21) & M21), (uint32_t)(pt[0] >> 42)};
-    if (threadIdx.x == 0) atomicMax(&prof[31], gtimer());  // totals loaded and scanned
+    STAMP_MAX(31)  // totals loaded and scanned
     npf = tt[0];
     nev = tt[1];
     seg_start[2 * threadIdx.x] = v[list];
@@ -1048,15 +1578,15 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       wbm &= wbm - 1;
     }
   }
-  if (c == 0 && threadIdx.x == 0) prof[16] = n_slots;
-  if (threadIdx.x == 0) atomicMax(&prof[13], gtimer());  // P5 tables
-  if (c == 0 && threadIdx.x == 0) prof[7] = gtimer();
+  PROBE(if (c == 0 && threadIdx.x == 0) prof[16] = n_slots;)
+  STAMP_MAX(13)  // P5 tables
+  STAMP0(7)
   __shared__ uint32_t col_pre[FUSED_MAX_CTAS], col_src[FUSED_MAX_CTAS];
   __shared__ uint32_t sh_gp, sh_tmp;
-  const unsigned long long t_s0 = gtimer();
-  unsigned long long dt[4] = {0, 0, 0, 0};  // slot sections (thread 0): segment + columns, gather, scan, place
+  PROBE(const unsigned long long t_s0 = gtimer();)
+  PROBE(unsigned long long dt[4] = {0, 0, 0, 0};)
   for (uint32_t j = c; j < n_slots; j += G) {
-    unsigned long long tq = gtimer();
+    PROBE(unsigned long long tq = gtimer();)
     {  // the segment holding slot j
       const uint32_t g0 = 2 * threadIdx.x;
       const uint32_t a = slot_base[g0], m = slot_base[g0 + 1], z = g0 + 2 < 2 * NBL ? slot_base[g0 + 2] : n_slots;
@@ -1149,9 +1679,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     const uint32_t *sk = list == 0 ? d.sort_ka : d.f_sk2, *sv = list == 0 ? d.sort_va : d.f_sv2;
     uint32_t *out = (list == 0 ? d.pf_ids : d.ev_ids) + seg_start[gp];
     auto lap = [&](int i) {
-      const unsigned long long t = gtimer();
-      dt[i] += t - tq;
-      tq = t;
+      PROBE(const unsigned long long t = gtimer(); dt[i] += t - tq; tq = t;)
     };
     lap(0);
     const uint32_t e0 = si * CH, e1 = min(len, e0 + CH);
@@ -1272,18 +1800,18 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       __syncthreads();
       cta_sort_pairs(ka, ia, kb, ib, len, s.h);  // counters in s.h[0, 4096)
       for (uint32_t e = threadIdx.x; e < len; e += FT) out[e] = ia[e];
-      if (threadIdx.x == 0) atomicMax(&prof[18], (unsigned long long)len);
+      PROBE(if (threadIdx.x == 0) atomicMax(&prof[18], (unsigned long long)len);)
     }
     __syncthreads();
     lap(3);
   }
-  if (threadIdx.x == 0) {
+  PROBE(if (threadIdx.x == 0) {
     atomicMax(&prof[21], gtimer() - t_s0);
     atomicMax(&prof[22], dt[0]);
     atomicMax(&prof[23], dt[1]);
     atomicMax(&prof[24], dt[2]);
     atomicMax(&prof[29], dt[3]);
-  }
+  })
   {  // write-back bytes: the CTA's sum into acc[2]; the last CTA to arrive writes the header
     unsigned long long d2h = (unsigned long long)wb0 + wb1;
     while (wbm) {  // (rare: a word with more than two dirty evicted agents)
@@ -1297,12 +1825,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       if (v) atomicAdd(&d.header[H_D2H], v);
     }
   }
-  if (threadIdx.x == 0) atomicMax(&prof[1], gtimer());
+  STAMP_MAX(1)
 }
 
 // host side
 bool fused_supported(const Params &p, int grid, uint32_t *tile_out) {
-  if (p.world != 1 || grid <= 0 || grid > FUSED_MAX_CTAS) return false;
+  if ((p.world != 1 && !p.loopback) || grid <= 0 || grid > FUSED_MAX_CTAS) return false;
   uint64_t tile = (p.n_local + grid - 1) / grid;  // grid = CTAs of the instance
   tile = (tile + 31) / 32 * 32;
   if (tile == 0) tile = 32;
@@ -1311,27 +1839,60 @@ bool fused_supported(const Params &p, int grid, uint32_t *tile_out) {
   return true;
 }
 
+// Shared-memory budget of a launch: the tile arrays and histograms (fused_smem_bytes) plus the
+// CTA-count column staging of the fast list placement (as many slots as fit, <= 128).
+template <int MAXB>
+static size_t smem_limit() {
+  static size_t lim = 0;
+  if (!lim) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, k_fused_plan<MAXB>) != cudaSuccess) return 0;
+    lim = (size_t)optin > a.sharedSizeBytes ? (size_t)optin - a.sharedSizeBytes : 0;
+  }
+  return lim;
+}
+
+template <int MAXB>
+static size_t launch_smem(uint32_t tile, uint32_t gsize, uint32_t *fastok) {
+  const size_t base = fused_smem_bytes(tile), lim = smem_limit<MAXB>();
+  if (gsize <= 1) {  // one CTA per instance: no bucket owners
+    *fastok = 1;
+    return base;
+  }
+  // bucket-owner staging: [G][RB] counts + [4][RB] totals / offsets
+  const uint32_t RB = ((4096 + gsize - 1) / gsize + 3u) & ~3u;
+  const size_t need = (size_t)4 * RB * (gsize + 4);
+  *fastok = base + need <= lim ? 1u : 0u;  // else the two-barrier list path
+  return base + (*fastok ? need : 0);
+}
+
 // 1 CTA of FT threads per SM must be resident for the whole grid (grid barrier).
 template <int MAXB>
-static bool prepare_one(uint32_t tile) {
-  if (cudaFuncSetAttribute(k_fused_plan<MAXB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)fused_smem_bytes(FUSED_MAX_TILE)) != cudaSuccess)
+static bool prepare_one(uint32_t tile, uint32_t gsize) {
+  const size_t lim = smem_limit<MAXB>();
+  if (!lim || cudaFuncSetAttribute(k_fused_plan<MAXB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim) !=
+                  cudaSuccess)
     return false;
+  uint32_t fastok;
+  const size_t sm = launch_smem<MAXB>(tile, gsize, &fastok);
+  if (sm > lim) return false;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_plan<MAXB>, FT, fused_smem_bytes(tile)) !=
-      cudaSuccess)
-    return false;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_plan<MAXB>, FT, sm) != cudaSuccess) return false;
   return per_sm >= 1;
 }
 
-bool fused_prepare(int grid, uint32_t tile) {
-  return grid >= 1 && prepare_one<1>(tile) && prepare_one<FUSED_MAX_BATCH>(tile);
+bool fused_prepare(int grid, uint32_t tile, uint32_t gsize) {
+  return grid >= 1 && prepare_one<1>(tile, gsize) && prepare_one<FUSED_MAX_BATCH>(tile, gsize);
 }
 
 template <int MAXB>
-static void launch_t(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s) {
+static void launch_t(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s, bool coop, uint32_t wsize) {
   FusedArgs<MAXB> B;
   B.n_inst = n;
+  B.wsize = wsize;
   B.gsize = gsize;
   uint32_t tile = 32;
   for (uint32_t i = 0; i < n; ++i) {
@@ -1341,24 +1902,25 @@ static void launch_t(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStr
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n * gsize);
   cfg.blockDim = dim3(FT);
-  cfg.dynamicSmemBytes = fused_smem_bytes(tile);
+  cfg.dynamicSmemBytes = launch_smem<MAXB>(tile, gsize, &B.fastok);
   cfg.stream = s;
   // cooperative: the grid barrier needs every CTA resident at once; the launch is scheduled
   // (or fails) as a whole instead of leaving resident CTAs spinning on absent ones when other
   // work holds SMs (another context's plan, copy kernels, the caller's kernels)
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = coop ? 2 : 1;  // (SCALESIM_F_EXCLUSIVE: PDL only)
   cudaLaunchKernelEx(&cfg, k_fused_plan<MAXB>, B);
 }
 
-int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s) {
-  if (n == 1) launch_t<1>(insts, n, gsize, s);
-  else launch_t<FUSED_MAX_BATCH>(insts, n, gsize, s);
+int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s, bool coop,
+                       uint32_t wsize) {
+  if (n == 1) launch_t<1>(insts, n, gsize, s, coop, 1);
+  else launch_t<FUSED_MAX_BATCH>(insts, n, gsize, s, coop, wsize);
   return 1;
 }
 

@@ -17,9 +17,11 @@ constexpr uint32_t GRID_MAX_SIDE = 128;   // a1' spatial grid: at most 128 x 128
 constexpr uint64_t GRID_MIN_PARTICIPANTS = 2048;  // below: tiled all-pairs scan
 constexpr int FUSED_MAX_CTAS = 160;       // fused path: one CTA per SM (B200: 148)
 constexpr uint32_t FUSED_MAX_TILE = 12288;  // fused path: agents per CTA held in shared memory
+constexpr uint32_t FUSED_OVF_CAP = 256;     // fused fast lists: agents in multi-valued level-1 buckets
+constexpr uint32_t FUSED_MAX_WORLD = 8;     // ranks of one world planned in one launch (SCALESIM_F_LOOPBACK)
 
 // status bits (mirror include/scalesim.h)
-constexpr uint32_t ST_INSUFFICIENT = 1u, ST_BAD_RECORD = 2u, ST_BAD_KIN = 4u, ST_NO_PAGES = 8u;
+constexpr uint32_t ST_INSUFFICIENT = 1u, ST_BAD_RECORD = 2u, ST_BAD_KIN = 4u, ST_NO_PAGES = 8u, ST_SYNC = 16u;
 
 // header fields (mirror SCALESIM_H_*)
 enum { H_N_PF = 0, H_N_EV, H_H2D, H_D2H, H_CUT_BITS, H_CUT_REM, H_STATUS, H_N_D2H, H_N_H2D,
@@ -68,6 +70,7 @@ struct Layout {
   uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_cpf, f_cta_cev, f_tot, f_acc;
   uint64_t f_rows1, f_rows2, f_rows3, f_cta_lmm;
   uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes, params_dev;
+  uint64_t f_pos, f_rt, f_crow, f_ovf;
   uint64_t total;
 };
 
@@ -119,6 +122,11 @@ struct Dev {
   uint32_t *f_sk2, *f_sv2, *f_sk3, *f_sv3;              // [n_local] evict-segment sort scratch
   unsigned int *f_bar;                                  // [2] grid-barrier counters
   unsigned long long *f_prof;                           // [16] globaltimer stamps of the last fused launch
+  // fused fast list placement (integer-distance contexts):
+  uint32_t *f_crow;            // [2][G][4096] per-CTA eligible counts per level-1 bucket (non-resident | resident << 16)
+  unsigned long long *f_pos;   // [2][4096][FUSED_MAX_CTAS] bucket owners' list offsets per (bucket, CTA), epoch-tagged
+  unsigned long long *f_rt;    // [2][FUSED_MAX_CTAS] bucket owners' range totals, epoch-tagged
+  uint4 *f_ovf;                // [2][FUSED_OVF_CAP] eligible agents in multi-valued buckets: {key, id, resident, 0}
 };
 
 Dev make_dev(void *ws, const Layout &L);
@@ -141,6 +149,7 @@ struct Params {
   int keep_dist;  // fused path: also write the distances to the workspace (dist view)
   int int_mode;   // every distance is an integer or +inf (no interaction class, integral hop_scale)
   int explicit_dist;  // SCALESIM_F_EXPLICIT_DIST: record word 0 holds the distance bits (R19)
+  int loopback;       // SCALESIM_F_LOOPBACK: a rank of a world planned in one launch (step_group)
   int cur;  // index of the residency bitmap holding the residency before this plan
   int desc_buf;
   Dev d;
@@ -173,8 +182,9 @@ struct FusedInst {
   uint32_t cur, parity, epoch, tile;
 };
 constexpr int FUSED_MAX_BATCH = 160;
-int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s);
-bool fused_prepare(int grid, uint32_t tile);
+int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s, bool coop,
+                       uint32_t wsize = 1);
+bool fused_prepare(int grid, uint32_t tile, uint32_t gsize);
 size_t fused_smem_bytes(uint32_t tile);
 
 }  // namespace ss

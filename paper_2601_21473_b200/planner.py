@@ -36,7 +36,8 @@ class Planner:
                  dev_bytes: Optional[int] = None, resident_init=None, device: int = 0,
                  shard: Optional[tuple] = None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None,
-                 multi_kernel: bool = False, keep_dist: bool = True, explicit_dist: bool = False):
+                 multi_kernel: bool = False, keep_dist: bool = True, explicit_dist: bool = False,
+                 exclusive: bool = False):
         self.lib = L.lib()
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
@@ -87,7 +88,8 @@ class Planner:
         cfg = L.Config()
         cfg.abi_version = L.ABI_VERSION
         cfg.flags = (0 if transfer else L.F_NO_TRANSFER) | (L.F_MULTI_KERNEL if multi_kernel else 0) | \
-            (L.F_KEEP_DIST if keep_dist else 0) | (L.F_EXPLICIT_DIST if explicit_dist else 0)
+            (L.F_KEEP_DIST if keep_dist else 0) | (L.F_EXPLICIT_DIST if explicit_dist else 0) | \
+            (L.F_EXCLUSIVE if exclusive else 0)
         cfg.n_agents = self.n_agents
         cfg.shard_begin = self.lo
         cfg.shard_end = self.hi
@@ -196,6 +198,12 @@ class Planner:
             self.workspace[off:off + 512].copy_(torch.from_numpy(init.view(np.uint8)))
             torch.cuda.synchronize(self.device)
         return v
+
+    def list_paths(self):
+        """(fast, slow): fused launches so far whose lists were placed from the published
+        counts (no second grid barrier) / by the staged per-bucket sort."""
+        v = self.stamps()
+        return int(v[48]), int(v[49])
 
     @property
     def fused(self) -> bool:

@@ -28,7 +28,7 @@ def fill_pattern(host, chunk=1 << 28):
 
 
 def make_planner(w: tg.Workload, transfer: bool, resident_init=None, host_pattern=True, dev_pages=None,
-                 multi_kernel=False, explicit=False, keep_dist=True, stream=None):
+                 multi_kernel=False, explicit=False, keep_dist=True, stream=None, exclusive=False):
     from paper_2601_21473_b200.planner import Planner
     b = w.blocks
     host = None
@@ -41,17 +41,19 @@ def make_planner(w: tg.Workload, transfer: bool, resident_init=None, host_patter
     return Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
                    hop_scale=w.hop_scale, n_kin=w.n_kin, page_bytes=w.page_bytes, transfer=transfer,
                    host_arena=host, dev_bytes=max(pages, 1) * w.page_bytes, resident_init=resident_init,
-                   multi_kernel=multi_kernel, explicit_dist=explicit, keep_dist=keep_dist, stream=stream)
+                   multi_kernel=multi_kernel, explicit_dist=explicit, keep_dist=keep_dist, stream=stream,
+                   exclusive=exclusive)
 
 
 def run_parity(w: tg.Workload, steps=None, transfer=True, resident_init=None, content_pages=64,
                check_dist=True, stamp_writes=True, seed=0, multi_kernel=False, expect_fused=None, explicit=False,
-               keep_dist=True):
+               keep_dist=True, exclusive=False):
     """Step the GPU planner and the oracle through the workload; assert parity every step.
     keep_dist=False is the bench's configuration (the fused kernel's fast P1 variant, no
     distance copy): distances are then compared through the plan (D*, lists, bytes) only.
     Returns per-step summaries."""
-    pl = make_planner(w, transfer, resident_init, multi_kernel=multi_kernel, explicit=explicit, keep_dist=keep_dist)
+    pl = make_planner(w, transfer, resident_init, multi_kernel=multi_kernel, explicit=explicit, keep_dist=keep_dist,
+                      exclusive=exclusive)
     check_dist = check_dist and keep_dist
     if expect_fused is None:
         expect_fused = not multi_kernel
@@ -149,5 +151,7 @@ def run_parity(w: tg.Workload, steps=None, transfer=True, resident_init=None, co
         res = p["resident"]
         out.append(dict(step=s, n_prefetch=len(p["prefetch"]), n_evict=len(p["evict"]),
                         bytes_h2d=p["bytes_h2d"], status=hdr["status"]))
+    if pl.fused and out:  # fused launches that took the fast / the two-barrier list placement
+        out[-1]["paths"] = pl.list_paths()
     pl.close()
     return out

@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT + '/tests')
 import oracle, tracegen as tg
 from gpu_harness import make_planner
 ws = [tg.config_c4(seed=11, steps=8, n=300_000), tg.config_c4(seed=12, steps=8, n=250_000)]
-pls = [make_planner(w, transfer=False, keep_dist=False) for w in ws]
+pls = [make_planner(w, transfer=False, keep_dist=False, exclusive=EXCL) for w in ws]
 assert pls[0].stream.cuda_stream != pls[1].stream.cuda_stream
 assert all(pl.fused for pl in pls)
 recs = [torch.from_numpy(np.ascontiguousarray(w.rec).view(np.uint8).reshape(w.steps, -1)).cuda() for w in ws]
@@ -44,7 +44,10 @@ print("CONCURRENT_OK")
 """
 
 
-def test_two_contexts_two_streams_concurrently():
-    code = CHILD.replace("ROOT", repr(ROOT))
+@pytest.mark.parametrize("exclusive", [False, True], ids=["cooperative", "exclusive-chained"])
+def test_two_contexts_two_streams_concurrently(exclusive):
+    """Default contexts launch cooperatively; SCALESIM_F_EXCLUSIVE contexts are ordered by the
+    library's per-device event chain."""
+    code = CHILD.replace("ROOT", repr(ROOT)).replace("EXCL", repr(exclusive))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240)
     assert r.returncode == 0 and "CONCURRENT_OK" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])

@@ -59,16 +59,20 @@ def test_c3_full_size():
     run_parity(w, stamp_writes=False, content_pages=16)
 
 
-@pytest.mark.parametrize("mk,keep", [pytest.param(False, True, id="fused"),
-                                     pytest.param(False, False, id="fused-nokeep-bench"),
-                                     pytest.param(True, True, id="multikernel")])
-def test_c4_full_size_logical(mk, keep):
-    """BASELINE configs[3] at G=1: 1M agents, logical sizes (no arena).  `fused-nokeep-bench`
-    is exactly bench.py's headline configuration (same generator, seed and size, keep_dist
-    off: the fused kernel's fast P1 variant that the timed region runs)."""
+@pytest.mark.parametrize("mk,keep,excl", [pytest.param(False, True, False, id="fused"),
+                                          pytest.param(False, False, True, id="fused-nokeep-exclusive-bench"),
+                                          pytest.param(True, True, False, id="multikernel")])
+def test_c4_full_size_logical(mk, keep, excl):
+    """BASELINE configs[3] at G=1: 1M agents, logical sizes (no arena).  `fused-nokeep-
+    exclusive-bench` is exactly bench.py's headline configuration (same generator, seed and
+    size; keep_dist off: the fused kernel's fast P1 variant; SCALESIM_F_EXCLUSIVE: the launch
+    without the cooperative attribute)."""
     from gpu_harness import run_parity
     w = tg.config_c4(seed=1, steps=6 if mk else 24)
-    run_parity(w, transfer=False, multi_kernel=mk, keep_dist=keep)
+    out = run_parity(w, transfer=False, multi_kernel=mk, keep_dist=keep, exclusive=excl)
+    if not mk:  # integer distances: most steps place their lists without the second barrier
+        fast, slow = out[-1]["paths"]
+        assert fast + slow == 24 and fast >= 12, (fast, slow)
 
 
 @pytest.mark.parametrize("mk", PATHS)
