@@ -623,12 +623,12 @@ static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out);
 
 // One single-kernel plan launch (n instances on c's stream): cooperative unless c is an
 // exclusive context; exclusive launches of different contexts of a device are chained.
-static int launch_fused(scalesim_ctx *c, const FusedInst *insts, uint32_t n, uint32_t gsize) {
-  if (!c->exclusive) return launch_fused_batch(insts, n, gsize, c->stream, true);
+static int launch_fused(scalesim_ctx *c, const FusedInst *insts, uint32_t n, uint32_t gsize, uint32_t wsize = 1) {
+  if (!c->exclusive) return launch_fused_batch(insts, n, gsize, c->stream, true, wsize);
   std::lock_guard<std::mutex> g(g_excl_mu);
   ExclusiveChain &x = g_excl[c->cfg.device];
   if (x.contexts > 1 && x.stream && x.stream != c->stream) cudaStreamWaitEvent(c->stream, x.event, 0);
-  const int k = launch_fused_batch(insts, n, gsize, c->stream, false);
+  const int k = launch_fused_batch(insts, n, gsize, c->stream, false, wsize);
   if (x.contexts > 1) {
     cudaEventRecord(c->ev_fused, c->stream);
     x.stream = c->stream;
@@ -654,6 +654,7 @@ static FusedInst fused_inst(const scalesim_ctx *c, uint32_t tile) {
 
 extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *out) {
   if (!c) return SCALESIM_E_INVALID;
+  if (c->p.loopback) return SCALESIM_E_INVALID;  // a loopback rank is planned with its world (scalesim_step_group)
   if (!c->scored) return SCALESIM_E_ORDER;
   Params &p = c->p;
   const bool multi = c->cfg.world > 1;
@@ -846,6 +847,46 @@ extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32
       if ((s = scalesim_transfer(c, nullptr)) != SCALESIM_OK) return s;
     }
     i0 += k;
+  }
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_step_group(scalesim_ctx *const *ctxs, uint32_t world, int64_t now) {
+  if (!ctxs || world < 2 || world > FUSED_MAX_WORLD) return SCALESIM_E_INVALID;
+  scalesim_ctx *c0 = ctxs[0];
+  if (!c0) return SCALESIM_E_INVALID;
+  uint64_t next = 0;  // shards: contiguous, in rank order, covering [0, n_agents)
+  for (uint32_t r = 0; r < world; ++r) {
+    const scalesim_ctx *c = ctxs[r];
+    if (!c || !c->p.loopback || !c->fused || c->cfg.world != (int)world || c->cfg.rank != (int)r) return SCALESIM_E_INVALID;
+    if (c->stream != c0->stream || c->cfg.device != c0->cfg.device || c->exclusive != c0->exclusive ||
+        c->cfg.n_agents != c0->cfg.n_agents || c->cfg.budget_bytes != c0->cfg.budget_bytes ||
+        c->cfg.hop_scale != c0->cfg.hop_scale || c->fused_steps != c0->fused_steps ||
+        c->fused_grid != c0->fused_grid || c->p.int_mode != c0->p.int_mode)
+      return SCALESIM_E_INVALID;
+    for (int k = 0; k < 3; ++k)
+      if (c->cfg.theta[k] != c0->cfg.theta[k]) return SCALESIM_E_INVALID;
+    if (c->cfg.shard_begin != next) return SCALESIM_E_INVALID;
+    next = c->cfg.shard_end;
+  }
+  if (next != c0->cfg.n_agents) return SCALESIM_E_INVALID;
+  CK(cudaGetLastError());
+  for (uint32_t r = 0; r < world; ++r) {
+    scalesim_status s = scalesim_score(ctxs[r], now, nullptr);
+    if (s != SCALESIM_OK) return s;
+  }
+  FusedInst insts[FUSED_MAX_WORLD];
+  for (uint32_t r = 0; r < world; ++r) insts[r] = fused_inst(ctxs[r], ctxs[r]->fused_tile);
+  c0->launches += launch_fused(c0, insts, world, (uint32_t)c0->fused_grid, world);
+  CK(cudaGetLastError());
+  for (uint32_t r = 0; r < world; ++r) {
+    scalesim_ctx *c = ctxs[r];
+    c->fused_steps++;
+    c->deferred = false;
+    c->last_fused = true;
+    scalesim_status s = finish_plan(c, nullptr);
+    if (s != SCALESIM_OK) return s;
+    if ((s = scalesim_transfer(c, nullptr)) != SCALESIM_OK) return s;
   }
   return SCALESIM_OK;
 }

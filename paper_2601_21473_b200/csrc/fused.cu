@@ -834,12 +834,15 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
     cp_async_commit();
   }
-  __shared__ unsigned long long sh_novf;  // eligible agents in multi-valued buckets (all CTAs)
+  // eligible agents in multi-valued buckets: this instance's (placed by its overflow CTA) and
+  // the world's (the fast list decision must agree across the ranks)
+  __shared__ unsigned long long sh_novf, sh_novf_w;
   if (threadIdx.x == 32) {  // (warp 0 runs the select)
     unsigned long long v = 0;
-    if (imode)  // the world's: the fast list decision must agree across its ranks
+    if (imode)
       for (uint32_t r = 0; r < nw; ++r) v += W.acc[r][8 * par + 6];
-    sh_novf = v;
+    sh_novf_w = v;
+    sh_novf = imode ? acc[6] : 0ull;
   }
   Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 1, 0};
   STAMP0(32)  // other parity cleared
@@ -878,7 +881,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
 #ifdef AB_NO_FAST  // A/B experiments only (tools/)
   const bool fastp = false;
 #else
-  const bool fastp = imode && A.fastok && sh_novf <= FUSED_OVF_CAP &&
+  const bool fastp = imode && A.fastok && sh_novf_w <= FUSED_OVF_CAP &&
                      (all_fit || (sel.level_res == 1 && (sel.b_res < IB_EXACT || sel.b_res == IB_INF)));
 #endif
   if (c == 0 && threadIdx.x == 0) atomicAdd(&prof[fastp ? 48 : 49], 1ull);  // launches per list path

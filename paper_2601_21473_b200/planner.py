@@ -37,7 +37,7 @@ class Planner:
                  shard: Optional[tuple] = None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None,
                  multi_kernel: bool = False, keep_dist: bool = True, explicit_dist: bool = False,
-                 exclusive: bool = False):
+                 exclusive: bool = False, loopback: bool = False):
         self.lib = L.lib()
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
@@ -83,13 +83,13 @@ class Planner:
             words = np.concatenate([words, np.zeros(pad, np.uint8)])
             self.res_init = _dev_bytes(words, dev)
         self._nccl_id = None
-        if world > 1:
+        if world > 1 and not loopback:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
         cfg = L.Config()
         cfg.abi_version = L.ABI_VERSION
         cfg.flags = (0 if transfer else L.F_NO_TRANSFER) | (L.F_MULTI_KERNEL if multi_kernel else 0) | \
             (L.F_KEEP_DIST if keep_dist else 0) | (L.F_EXPLICIT_DIST if explicit_dist else 0) | \
-            (L.F_EXCLUSIVE if exclusive else 0)
+            (L.F_EXCLUSIVE if exclusive else 0) | (L.F_LOOPBACK if loopback else 0)
         cfg.n_agents = self.n_agents
         cfg.shard_begin = self.lo
         cfg.shard_end = self.hi
@@ -301,4 +301,15 @@ def step_batch(planners, now: int):
     arr = (C.c_void_p * len(planners))(*[pl.ctx.value for pl in planners])
     L.check(lib.scalesim_step_batch(arr, len(planners), int(now)), "scalesim_step_batch")
     for pl in planners:
+        L.check(lib.scalesim_view(pl.ctx, C.byref(pl.view)), "scalesim_view")
+
+
+def step_group(ranks, now: int):
+    """One step of a world whose ranks (Planner contexts created with loopback=True, rank r
+    = ranks[r]) all live on this device: scalesim_step_group plans them in one launch, the
+    global cut exchanged through device memory (include/scalesim.h)."""
+    lib = ranks[0].lib
+    arr = (C.c_void_p * len(ranks))(*[pl.ctx.value for pl in ranks])
+    L.check(lib.scalesim_step_group(arr, len(ranks), int(now)), "scalesim_step_group")
+    for pl in ranks:
         L.check(lib.scalesim_view(pl.ctx, C.byref(pl.view)), "scalesim_view")
