@@ -394,7 +394,7 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
   c->grid = sms * 4;
-  c->copy_ctas = sms / 2;
+  c->copy_ctas = COPY_CTAS;
   auto fail = [&](scalesim_status s) {
     scalesim_destroy(c);
     return s;
@@ -535,7 +535,8 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
   // share of the SMs (its world is planned by one launch)
   if ((cfg->world == 1 || p.loopback) && !(cfg->flags & SCALESIM_F_MULTI_KERNEL)) {
     uint32_t tile = 0;
-    const int g = p.loopback ? sms / cfg->world : sms;
+    // a transfer context leaves SMs to its page copies (they overlap the next plan)
+    const int g = (p.loopback ? sms / cfg->world : sms) - (transfer && !p.loopback ? 2 * COPY_CTAS : 0);
     if (fused_supported(p, g, &tile) && fused_prepare(g * (p.loopback ? cfg->world : 1), tile, (uint32_t)g)) {
       c->fused = true;
       c->fused_tile = tile;

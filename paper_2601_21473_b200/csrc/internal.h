@@ -16,6 +16,10 @@ constexpr int L1_BITS = 11, L2_BITS = 10, L3_BITS = 10;  // distance-bit digits 
 constexpr uint32_t GRID_MAX_SIDE = 128;   // a1' spatial grid: at most 128 x 128 cells
 constexpr uint64_t GRID_MIN_PARTICIPANTS = 2048;  // below: tiled all-pairs scan
 constexpr int FUSED_MAX_CTAS = 160;       // fused path: one CTA per SM (B200: 148)
+constexpr int COPY_CTAS = 8;              // a6: CTAs per page-copy launch (two run at once: write-backs and
+                                          // independent loads); the single-kernel plan of a transfer
+                                          // context leaves 2 * COPY_CTAS SMs to them, so the plan of step
+                                          // t+1 runs beside the copies of step t
 constexpr uint32_t FUSED_MAX_TILE = 12288;  // fused path: agents per CTA held in shared memory
 constexpr uint32_t FUSED_OVF_CAP = 256;     // fused fast lists: agents in multi-valued level-1 buckets
 constexpr uint32_t FUSED_MAX_WORLD = 8;     // ranks of one world planned in one launch (SCALESIM_F_LOOPBACK)

@@ -859,6 +859,68 @@ __global__ void __launch_bounds__(NT) k_copy_pages(const unsigned long long *des
   }
 }
 
+// TMA variant: one thread per CTA drives bulk copies (cp.async.bulk) through a ring of shared-
+// memory chunks: global (host-mapped or device) -> shared with an mbarrier completion, then
+// shared -> global as a bulk group; no register staging, 128 KB in flight per CTA.
+constexpr uint32_t TMA_CH = 16384, TMA_NB = 8;
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int MODE>
+__global__ void __launch_bounds__(32) k_copy_pages_tma(const unsigned long long *desc_base, uint8_t *host, uint8_t *dev,
+                                                      uint64_t page_bytes, uint64_t desc_cap) {
+  constexpr bool D2H = MODE == 0;
+  extern __shared__ __align__(128) uint8_t tbuf[];
+  __shared__ __align__(8) unsigned long long bar[TMA_NB];
+  if (threadIdx.x != 0) return;
+  const unsigned long long lo = MODE == 2 ? desc_base[2] : 0ull;
+  const unsigned long long hi = MODE == 0 ? desc_base[0] : (MODE == 1 ? desc_base[2] : desc_base[1]);
+  const unsigned long long *desc = desc_base + DESC_HDR + (D2H ? 0 : 2 * desc_cap);
+  const uint32_t cpp = (uint32_t)(page_bytes / TMA_CH);  // chunks per page (page_bytes % 16 KB == 0 here)
+  const unsigned long long mine = hi > lo + blockIdx.x ? (hi - lo - blockIdx.x + gridDim.x - 1) / gridDim.x : 0ull;
+  const unsigned long long n = mine * cpp;  // this CTA's chunks: its pages in order, chunks in order
+  if (n == 0) return;
+  for (uint32_t i = 0; i < TMA_NB; ++i)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto src_dst = [&](unsigned long long j, const uint8_t *&src, uint8_t *&dst) {
+    const unsigned long long k = lo + blockIdx.x + (j / cpp) * gridDim.x, off = (j % cpp) * TMA_CH;
+    const unsigned long long hoff = desc[2 * k], pg = desc[2 * k + 1];
+    src = (D2H ? dev + pg * page_bytes : host + hoff) + off;
+    dst = (D2H ? host + hoff : dev + pg * page_bytes) + off;
+  };
+  auto load = [&](unsigned long long j) {
+    const uint8_t *src;
+    uint8_t *dst;
+    src_dst(j, src, dst);
+    const uint32_t b = smem_u32(&bar[j % TMA_NB]), sm = smem_u32(tbuf + (j % TMA_NB) * TMA_CH);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(TMA_CH) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sm),
+                 "l"(src), "r"(TMA_CH), "r"(b)
+                 : "memory");
+  };
+  for (unsigned long long j = 0; j < n && j < TMA_NB; ++j) load(j);
+  for (unsigned long long j = 0; j < n; ++j) {
+    const uint32_t b = smem_u32(&bar[j % TMA_NB]), ph = (uint32_t)((j / TMA_NB) & 1);
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(ok)
+                   : "r"(b), "r"(ph)
+                   : "memory");
+    const uint8_t *src;
+    uint8_t *dst;
+    src_dst(j, src, dst);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(tbuf + (j % TMA_NB) * TMA_CH)), "r"(TMA_CH)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // the previous chunk's store has read its buffer: refill that buffer
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    if (j >= 1 && j - 1 + TMA_NB < n) load(j - 1 + TMA_NB);
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------------
 // launchers
 
@@ -961,6 +1023,23 @@ int launch_transfer(const Params &p, cudaStream_t s, int ctas) {
 // write-backs; the caller joins s2 back into s
 int launch_transfer_split(const Params &p, cudaStream_t s, cudaStream_t s2, int ctas) {
   const unsigned long long *desc = p.d.desc[p.desc_buf];
+  // bulk copies when pages are whole 16 KB chunks (A/B: the same link fraction as the
+  // register-staged copy, profiles/r02_copy_tma_ab.log, with one thread and no registers per CTA)
+#ifndef COPY_REGS
+  if (p.page_bytes % TMA_CH == 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_copy_pages_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_CH * TMA_NB);
+      cudaFuncSetAttribute(k_copy_pages_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_CH * TMA_NB);
+      cudaFuncSetAttribute(k_copy_pages_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_CH * TMA_NB);
+      attr = true;
+    }
+    k_copy_pages_tma<0><<<ctas, 32, TMA_CH * TMA_NB, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+    k_copy_pages_tma<1><<<ctas, 32, TMA_CH * TMA_NB, s2>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+    k_copy_pages_tma<2><<<ctas, 32, TMA_CH * TMA_NB, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+    return 3;
+  }
+#endif
   k_copy_pages<0><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
   k_copy_pages<1><<<ctas, NT, 0, s2>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
   k_copy_pages<2><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
