@@ -375,6 +375,62 @@ def closed_loop_leg(dev, steps=64, seed=1):
                     "a load on the critical path (P:87, P:373-375)"}
 
 
+def sched_leg(torch, dev, link=None, seed=3):
+    """NEXT #2: the preemptive load scheduler (scalesim_sched_run) moving C2-sized agents
+    (7B rank-16 LoRA + KV pages, ~24 MB each) in 16 MB chunks over the host link: 160 prefetch
+    tasks at distances 1..12 submitted at slot 0, an urgent (distance 0) task every 6 slots,
+    distance refreshes that cancel 10% of the waiting tasks; device-timed."""
+    from paper_2601_21473_b200.planner import LOAD_EVENT, sched_run
+    rng = np.random.default_rng(seed)
+    n_agents, chunk = 256, 16 << 20
+    per = 20_185_088 + 917_504 * 3
+    host_bytes = 2 << 30
+    host = torch.empty(host_bytes, dtype=torch.uint8, pin_memory=True)
+    devm = torch.empty(n_agents * per, dtype=torch.uint8, device=dev)
+    evs = []
+    for a in range(160):
+        evs.append((0, 0, a, float(rng.integers(1, 13)), (a * per) % (host_bytes - per) // 16 * 16, a * per, per))
+    for k, a in enumerate(range(160, 256)):
+        # (odd slots: the urgent task lands between the two chunks of a running prefetch)
+        evs.append((6 * (k + 1) + 1, 0, a, 0.0, (a * per) % (host_bytes - per) // 16 * 16, a * per, per))
+        if k % 2 == 0:
+            b = int(rng.integers(0, 160))
+            evs.append((6 * (k + 1) + 1, 1, b, 20.0, 0, 0, 0))
+    evs.sort(key=lambda e: e[0])
+    ev = np.array(evs, dtype=LOAD_EVENT)
+    sched_run(ev[:4], n_agents, 12.0, chunk, host, devm, 100_000)  # warm
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream(dev)
+    e0.record(st)
+    out = sched_run(ev, n_agents, 12.0, chunk, host, devm, 100_000, sync=False)
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    trace_t, tasks_t, counts_t = out[0], out[1], out[2]
+    c = counts_t.cpu().numpy().view(np.uint32)
+    tr = trace_t.cpu().numpy().view(np.uint32).reshape(-1, 2)[:c[0]]
+    tk = tasks_t.cpu().numpy()[:c[1] * 32].view(np.dtype([("agent", "<u4"), ("chunks", "<u4"), ("done", "<u4"),
+                                                          ("state", "<u4"), ("priority", "<f4"),
+                                                          ("preemptions", "<u4"), ("finish_slot", "<u4"), ("pad", "<u4")]))
+    moved = 0
+    for t, k in tr:
+        if t != 0xFFFFFFFF:
+            moved += min(chunk, per - int(k) * chunk)
+    ms = e0.elapsed_time(e1)
+    urgent = tk[tk["priority"] == 0.0]
+    wait = [int(u["finish_slot"]) for u in urgent]
+    r = {"workload": "C2-sized agents (20.2 MB LoRA + 3 KV pages), 160 prefetch tasks at distances 1..12 at slot 0, "
+                     "an urgent distance-0 task every 6 slots (96, landing mid-task: preemptions), distance refreshes cancelling "
+                     "waiting tasks",
+         "chunk_bytes": chunk, "slots": int(c[0]), "tasks": int(c[1]), "bytes_moved": moved, "ms": ms,
+         "GBs": moved / (ms / 1e3) / 1e9, "preemptions": int(tk["preemptions"].sum()),
+         "cancelled": int((tk["state"] == 4).sum()), "done": int((tk["state"] == 3).sum()),
+         "urgent_tasks": int(len(urgent))}
+    if link:
+        r["frac_of_h2d_link"] = r["GBs"] / link["h2d_GBs"]
+    del host, devm
+    return r
+
+
 def c5_leg(torch, dev, rank, world, replicas=64, budgets=tuple(range(10, 100, 10)), steps=8, warm=8, seed_base=100):
     """C5: independent simulation replicas x budget sizes, instances sharded over the ranks
     (instance i on rank i % world), all of a rank's instances stepped by scalesim_step_batch.
@@ -512,6 +568,7 @@ def main():
     ap.add_argument("--no-objects", action="store_true", help="skip the shared-object leg (NEXT #1)")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 planning + transfer overlap leg")
     ap.add_argument("--no-closed-loop", action="store_true", help="skip the closed-loop policy comparison (NEXT #3)")
+    ap.add_argument("--no-sched", action="store_true", help="skip the load scheduler leg (NEXT #2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -805,6 +862,8 @@ def main():
         tl["frac_of_link"] = ideal_s / max(tl["bytes_per_step"] / (tl["GBs"] * 1e9), 1e-12)
         tl["frac_definition"] = "max(h2d/h2d_peak, d2h/d2h_peak) / measured transfer time per step"
         line["transfer"] = tl
+        if not args.no_sched:
+            line["scheduler"] = sched_leg(torch, dev, lp)
     line["cpu"] = {"cores": os.cpu_count()}
     print(json.dumps(line), flush=True)
     if world > 1:

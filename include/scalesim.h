@@ -241,6 +241,50 @@ scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32_t n, int64
  * shard (tests/test_gpu_world.py).  Errors: SCALESIM_E_INVALID for a malformed world. */
 scalesim_status scalesim_step_group(scalesim_ctx *const *ctxs, uint32_t world, int64_t now_tick);
 
+/* ---- NEXT #2: the preemptive priority load scheduler (App. A "Load task scheduler"
+ * and "Preemption support"; SPEC.md S:291-293, S:324-327, S:348-356, S:366-374;
+ * readings R21-R23).  One channel moves one task's chunk per slot from
+ * the pinned host arena to the device arena; at every chunk boundary the boundary's events are
+ * admitted, then the most urgent waiting task runs, preempting the executing task when it is
+ * strictly more urgent (the preempted task resumes later with its completed chunks kept). */
+#define SCALESIM_LOAD_SUBMIT 0u   /* a load task for `agent` (coalesced into the agent's live task:
+                                     the smaller priority wins, no new task) */
+#define SCALESIM_LOAD_REFRESH 1u  /* the agent's refreshed distance: its waiting (queued or
+                                     preempted) task is cancelled when priority >= threshold; the
+                                     executing task never is */
+typedef struct {
+  uint32_t slot;      /* admitted at the boundary before chunk slot `slot`; events sorted by slot,
+                         same-slot events applied in array order */
+  uint32_t kind;      /* SCALESIM_LOAD_* */
+  uint32_t agent;     /* < n_agents */
+  float priority;     /* SUBMIT: invocation distance (>= 0, lower = more urgent, ties by task id);
+                         REFRESH: the agent's new distance */
+  uint64_t host_off;  /* SUBMIT: source bytes in the host arena (16-byte aligned) ... */
+  uint64_t dev_off;   /* ... destination in the device arena (16-byte aligned) */
+  uint64_t bytes;     /* ... length (chunks = ceil(bytes / chunk_bytes), at least 1) */
+} scalesim_load_event;
+typedef struct {
+  uint32_t task, chunk; /* what moved in a slot; task 0xFFFFFFFF = idle channel */
+} scalesim_load_slot;
+typedef struct {
+  uint32_t agent, chunks, done, state; /* state: 0 queued, 1 executing, 2 preempted, 3 done, 4 cancelled */
+  float priority;                      /* after coalescing */
+  uint32_t preemptions, finish_slot, pad;
+} scalesim_load_task;                  /* task ids = creation order (non-coalesced submissions) */
+
+uint64_t scalesim_sched_scratch_bytes(uint32_t n_events, uint32_t n_agents);
+/* Run a whole schedule on `stream` (asynchronous, one persistent launch): events (device,
+ * n_events), the prefetch threshold of REFRESH events, chunk_bytes (multiple of 16; the SPEC's
+ * default is 16 MB), host_arena (pinned, device-mapped) and dev_arena.  Outputs (device): trace
+ * (max_slots entries), tasks (n_events entries), counts[0] = slots run (the schedule stops when
+ * no task is live and no event is left, or at max_slots), counts[1] = tasks created.  scratch:
+ * 256-byte aligned device memory of scalesim_sched_scratch_bytes.  Errors: SCALESIM_E_INVALID
+ * for NULL / misaligned arguments or chunk_bytes % 16 != 0; SCALESIM_E_CUDA. */
+scalesim_status scalesim_sched_run(const scalesim_load_event *events, uint32_t n_events, uint32_t n_agents,
+                                   float threshold, uint64_t chunk_bytes, const void *host_arena, void *dev_arena,
+                                   uint32_t max_slots, scalesim_load_slot *trace, scalesim_load_task *tasks,
+                                   uint32_t *counts, void *scratch, uint64_t scratch_bytes, void *stream);
+
 /* End-to-end step from HOST buffers: copies host_rec (4*n_local uint32) and host_kin
  * (4*n_kin float, may be NULL) to the device, runs scalesim_step, waits, and copies the
  * plan header and lists back (prefetch_out/evict_out: host, n_local capacity each, may be

@@ -34,7 +34,7 @@ HEADER_NAMES = ["n_prefetch", "n_evict", "bytes_h2d", "bytes_d2h", "cut_bits", "
 # Every symbol include/scalesim.h declares (checked by tests/test_abi.py).
 EXPORTS = ["scalesim_workspace_bytes", "scalesim_init", "scalesim_score", "scalesim_plan",
            "scalesim_transfer", "scalesim_view", "scalesim_step", "scalesim_step_batch", "scalesim_step_group", "scalesim_step_host", "scalesim_set_inputs",
-           "scalesim_sync", "scalesim_join", "scalesim_nccl_unique_id", "scalesim_fused", "scalesim_profile_stamps", "scalesim_object_min", "scalesim_lru_records", "scalesim_bfs_scratch_bytes", "scalesim_bfs_hops", "scalesim_launch_count", "scalesim_destroy",
+           "scalesim_sync", "scalesim_join", "scalesim_nccl_unique_id", "scalesim_fused", "scalesim_profile_stamps", "scalesim_object_min", "scalesim_lru_records", "scalesim_bfs_scratch_bytes", "scalesim_bfs_hops", "scalesim_sched_scratch_bytes", "scalesim_sched_run", "scalesim_launch_count", "scalesim_destroy",
            "scalesim_strerror"]
 
 
@@ -135,6 +135,11 @@ def lib():
         L.scalesim_bfs_scratch_bytes.restype = u64
         L.scalesim_bfs_hops.argtypes = [vp, vp, u64, vp, u64, vp, vp, u64, vp]
         L.scalesim_bfs_hops.restype = C.c_int
+        L.scalesim_sched_scratch_bytes.argtypes = [C.c_uint32, C.c_uint32]
+        L.scalesim_sched_scratch_bytes.restype = u64
+        L.scalesim_sched_run.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_float, u64, vp, vp, C.c_uint32, vp, vp, vp,
+                                         vp, u64, vp]
+        L.scalesim_sched_run.restype = C.c_int
         L.scalesim_launch_count.argtypes = [vp]
         L.scalesim_launch_count.restype = u64
         L.scalesim_destroy.argtypes = [vp]

@@ -313,3 +313,38 @@ def step_group(ranks, now: int):
     L.check(lib.scalesim_step_group(arr, len(ranks), int(now)), "scalesim_step_group")
     for pl in ranks:
         L.check(lib.scalesim_view(pl.ctx, C.byref(pl.view)), "scalesim_view")
+
+
+# NEXT #2: the preemptive load scheduler (scalesim_sched_run, include/scalesim.h)
+LOAD_EVENT = np.dtype([("slot", "<u4"), ("kind", "<u4"), ("agent", "<u4"), ("priority", "<f4"),
+                       ("host_off", "<u8"), ("dev_off", "<u8"), ("bytes", "<u8")])
+LOAD_TASK = np.dtype([("agent", "<u4"), ("chunks", "<u4"), ("done", "<u4"), ("state", "<u4"), ("priority", "<f4"),
+                      ("preemptions", "<u4"), ("finish_slot", "<u4"), ("pad", "<u4")])
+
+
+def sched_run(events: np.ndarray, n_agents: int, threshold: float, chunk_bytes: int, host_arena: torch.Tensor,
+              dev_arena: torch.Tensor, max_slots: int, stream: Optional[torch.cuda.Stream] = None, sync: bool = True):
+    """Run a load schedule on the device.  events: numpy array of LOAD_EVENT sorted by slot.
+    Returns (trace (slots, 2) uint32, tasks LOAD_TASK array, n_slots) after a sync, or the
+    device tensors when sync is False."""
+    lib = L.lib()
+    dev = dev_arena.device
+    ev = torch.from_numpy(np.ascontiguousarray(events, dtype=LOAD_EVENT).view(np.uint8)).to(dev)
+    n_ev = len(events)
+    trace = torch.zeros(max(max_slots, 1) * 2, dtype=torch.int32, device=dev)
+    tasks = torch.zeros(max(n_ev, 1) * LOAD_TASK.itemsize, dtype=torch.uint8, device=dev)
+    counts = torch.zeros(2, dtype=torch.int32, device=dev)
+    nb = int(lib.scalesim_sched_scratch_bytes(n_ev, n_agents))
+    scratch = torch.empty(nb + 256, dtype=torch.uint8, device=dev)
+    sp = (scratch.data_ptr() + 255) // 256 * 256
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    L.check(lib.scalesim_sched_run(_ptr(ev) if n_ev else None, n_ev, n_agents, float(threshold), int(chunk_bytes),
+                                   _ptr(host_arena), _ptr(dev_arena), int(max_slots), _ptr(trace), _ptr(tasks),
+                                   _ptr(counts), sp, nb, st.cuda_stream), "scalesim_sched_run")
+    if not sync:
+        return trace, tasks, counts, (ev, scratch)
+    torch.cuda.synchronize(dev)
+    c = counts.cpu().numpy().view(np.uint32)
+    tr = trace.cpu().numpy().view(np.uint32).reshape(-1, 2)[:c[0]]
+    tk = tasks.cpu().numpy()[:c[1] * LOAD_TASK.itemsize].view(LOAD_TASK)
+    return tr, tk, int(c[0])
