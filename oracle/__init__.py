@@ -8,6 +8,6 @@ The arithmetic lives in ``oracle.cpp`` (plain single-threaded C++17); this modul
 builds it with g++ and marshals numpy arrays through ctypes.
 """
 from .oracle import (  # noqa: F401
-    build, lib, score, interaction, object_min, explicit_dist, lru_records, bfs_hops, plan, OracleMem, f32_bits,
+    build, lib, score, score_sampled, interaction, object_min, explicit_dist, lru_records, bfs_hops, plan, OracleMem, f32_bits,
     ST_INSUFFICIENT, ST_BAD_RECORD, ST_BAD_KIN, ST_NO_PAGES,
 )

@@ -94,43 +94,74 @@ extern "C" void oracle_interaction(uint64_t n, const uint32_t *rec, const float 
   }
 }
 
+/* Distance of agent i given the interaction times dint (indexed by kin index). */
+static float agent_distance(const uint32_t *rec, uint64_t i, uint64_t n_kin, int64_t now, float hop_scale,
+                            const float *dint, uint32_t *status) {
+  uint32_t ph = phase_of(rec, i), cl = class_of(rec, i);
+  if (cl == 3) *status |= ORACLE_ST_BAD_RECORD;
+  float d;
+  if (ph == PH_WAITING || ph == PH_GENERATING) {
+    d = 0.0f; /* S:170 "any agent in WaitingForMemory or Generating -> 0" */
+  } else if (ph == PH_IDLE) {
+    d = INF; /* S:124 "+infinity for agents that will never activate again" */
+  } else if (cl == CL_IND || cl == CL_INT) {
+    /* D_action: remaining duration of the current action, R8 clamp */
+    int64_t remain = (int64_t)rec[4 * i + 0] - now;
+    float d_action = remain <= 0 ? 0.0f : (float)remain;
+    d = d_action;
+    if (cl == CL_INT) {
+      /* Eq. 1: D = min(D_action, D_interaction) */
+      uint32_t k = rec[4 * i + 3];
+      float d_int = (k < n_kin) ? dint[k] : INF;
+      if (k >= n_kin) *status |= ORACLE_ST_BAD_RECORD;
+      if (d_int < d_action) d = d_int;
+    }
+  } else if (cl == CL_DIFF) {
+    /* hop count from the information source, R5/R9: hop * hop_scale */
+    uint32_t hop = rec[4 * i + 0];
+    if (hop == 0xFFFFFFFFu)
+      d = INF;
+    else
+      d = (float)hop * hop_scale;
+  } else {
+    d = INF; /* class 3: invalid record */
+  }
+  if (d == 0.0f) d = 0.0f; /* canonical +0 (R8) */
+  return d;
+}
+
 extern "C" void oracle_score(uint64_t n, const uint32_t *rec, const float *kin, uint64_t n_kin,
                              int64_t now, float hop_scale, float *d_out, uint32_t *status) {
   std::vector<float> dint(n_kin > 0 ? n_kin : 1, INF);
   if (n_kin > 0) oracle_interaction(n, rec, kin, n_kin, dint.data(), status);
-  for (uint64_t i = 0; i < n; ++i) {
-    uint32_t ph = phase_of(rec, i), cl = class_of(rec, i);
-    if (cl == 3) *status |= ORACLE_ST_BAD_RECORD;
-    float d;
-    if (ph == PH_WAITING || ph == PH_GENERATING) {
-      d = 0.0f; /* S:170 "any agent in WaitingForMemory or Generating -> 0" */
-    } else if (ph == PH_IDLE) {
-      d = INF; /* S:124 "+infinity for agents that will never activate again" */
-    } else if (cl == CL_IND || cl == CL_INT) {
-      /* D_action: remaining duration of the current action, R8 clamp */
-      int64_t remain = (int64_t)rec[4 * i + 0] - now;
-      float d_action = remain <= 0 ? 0.0f : (float)remain;
-      d = d_action;
-      if (cl == CL_INT) {
-        /* Eq. 1: D = min(D_action, D_interaction) */
-        uint32_t k = rec[4 * i + 3];
-        float d_int = (k < n_kin) ? dint[k] : INF;
-        if (k >= n_kin) *status |= ORACLE_ST_BAD_RECORD;
-        if (d_int < d_action) d = d_int;
-      }
-    } else if (cl == CL_DIFF) {
-      /* hop count from the information source, R5/R9: hop * hop_scale */
-      uint32_t hop = rec[4 * i + 0];
-      if (hop == 0xFFFFFFFFu)
-        d = INF;
-      else
-        d = (float)hop * hop_scale;
-    } else {
-      d = INF; /* class 3: invalid record */
+  for (uint64_t i = 0; i < n; ++i) d_out[i] = agent_distance(rec, i, n_kin, now, hop_scale, dint.data(), status);
+}
+
+extern "C" void oracle_score_sampled(uint64_t n, const uint32_t *rec, const float *kin, uint64_t n_kin, int64_t now,
+                                     float hop_scale, const uint64_t *agents, uint64_t n_sample, float *d_out,
+                                     uint32_t *status) {
+  /* the same definitions for a sample of agents: the Eq. 2 minimum of each sampled
+   * interaction participant over every other participant (the O(n^2) scan restricted to the
+   * sampled rows) */
+  std::vector<float> dint(n_kin > 0 ? n_kin : 1, INF);
+  std::vector<uint64_t> part;
+  for (uint64_t i = 0; i < n; ++i)
+    if (int_participant(rec, kin, n_kin, i, status)) part.push_back(i);
+  for (uint64_t s = 0; s < n_sample; ++s) {
+    const uint64_t i = agents[s];
+    if (!(i < n) || !int_participant(rec, kin, n_kin, i, status)) continue;
+    const float *ki = kin + 4 * (uint64_t)rec[4 * i + 3];
+    float best = INF;
+    for (uint64_t b = 0; b < part.size(); ++b) {
+      if (part[b] == i) continue;
+      const float *kj = kin + 4 * (uint64_t)rec[4 * part[b] + 3];
+      float t = pair_time(ki, kj);
+      if (t < best) best = t;
     }
-    if (d == 0.0f) d = 0.0f; /* canonical +0 (R8) */
-    d_out[i] = d;
+    dint[rec[4 * i + 3]] = best;
   }
+  for (uint64_t s = 0; s < n_sample; ++s)
+    d_out[s] = agents[s] < n ? agent_distance(rec, agents[s], n_kin, now, hop_scale, dint.data(), status) : INF;
 }
 
 extern "C" void oracle_plan(uint64_t n, const uint32_t *rec, const float *d, const uint8_t *resident_in,

@@ -71,6 +71,13 @@ void oracle_bfs_hops(uint64_t n, const uint64_t *row_ptr, const uint32_t *col, c
  * (r.r)/(-r.w) for approaching pairs, +inf otherwise; indexed by kin index.  Exposed so
  * the tests can pin Eq. 2 separately.  Entries of kin not owned by an ACTING INT agent
  * get +inf. */
+/* oracle_score's distances for a sample of agents only (agents[0..n_sample)): the same
+ * definitions, the Eq. 2 scan restricted to the sampled rows (full-size parity of the spatial
+ * grid at 10^6 interaction agents, where the full O(n^2) scan is out of reach). */
+void oracle_score_sampled(uint64_t n, const uint32_t *rec, const float *kin, uint64_t n_kin, int64_t now,
+                          float hop_scale, const uint64_t *agents, uint64_t n_sample, float *d_out,
+                          uint32_t *status);
+
 void oracle_interaction(uint64_t n, const uint32_t *rec, const float *kin, uint64_t n_kin,
                         float *dint, uint32_t *status);
 

@@ -47,6 +47,8 @@ def lib():
                 C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)
             L.oracle_score.argtypes = [u64, u32p, f32p, u64, C.c_int64, C.c_float, f32p, u32p]
             L.oracle_score.restype = None
+            L.oracle_score_sampled.argtypes = [u64, u32p, f32p, u64, C.c_int64, C.c_float, u64p, u64, f32p, u32p]
+            L.oracle_score_sampled.restype = None
             L.oracle_interaction.argtypes = [u64, u32p, f32p, u64, f32p, u32p]
             L.oracle_interaction.restype = None
             L.oracle_object_min.argtypes = [u64, f32p, u64, u64p, u32p, f32p, u32p]
@@ -107,6 +109,20 @@ def score(rec, kin, now: int, hop_scale: float = 1.0):
     lib().oracle_score(n, _p(rec, C.c_uint32), _p(kin, C.c_float), n_kin, int(now),
                        float(hop_scale), _p(d, C.c_float), _p(st, C.c_uint32))
     return d[:n], int(st[0])
+
+
+def score_sampled(rec, kin, now: int, agents, hop_scale: float = 1.0):
+    """oracle_score's distances of the given agents only (the Eq. 2 scan over every
+    participant for each sampled one)."""
+    rec = _rec(rec)
+    kin, n_kin = _kin(kin)
+    idx = np.ascontiguousarray(agents, dtype=np.uint64)
+    d = np.empty(max(len(idx), 1), dtype=np.float32)
+    st = np.zeros(1, dtype=np.uint32)
+    lib().oracle_score_sampled(rec.shape[0], _p(rec, C.c_uint32), _p(kin, C.c_float), n_kin, int(now),
+                               C.c_float(hop_scale), _p(idx, C.c_uint64), len(idx), _p(d, C.c_float),
+                               _p(st, C.c_uint32))
+    return d[:len(idx)], int(st[0])
 
 
 def interaction(rec, kin):

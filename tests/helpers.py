@@ -45,3 +45,25 @@ def round_f32(fr: Fraction) -> np.float32:
 def keys_of(d, ids):
     return (np.asarray(d, np.float32).view(np.uint32).astype(np.uint64) << np.uint64(32)) | \
         np.asarray(ids, np.uint64)
+
+
+def two_agent_overlap_records(F):
+    """SPEC acceptance #3 / P:174-185 timeline: agents A (0) and B (1), one slot.  A
+    calls the LLM at step 0, acts until step 7; B calls at step 1 and then acts for 19 steps,
+    longer than A's transfer: the distance policy reloads A while B acts."""
+    recs = []
+    for t in range(9):
+        if t == 0:
+            ag = [dict(phase=tg.PH_WAITING), dict(d=1)]
+        elif t == 1:
+            ag = [dict(d=6), dict(phase=tg.PH_WAITING)]
+        elif t < 7:
+            ag = [dict(d=7 - t), dict(d=20 - t)]
+        elif t == 7:
+            ag = [dict(phase=tg.PH_WAITING), dict(d=20 - t)]
+        else:
+            ag = [dict(phase=tg.PH_GENERATING), dict(d=20 - t)]
+        for a in ag:
+            a["fp"] = F
+        recs.append(rec_of(ag, now=t))
+    return np.stack(recs)

@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 import tracegen as tg
-from helpers import rec_of
+from helpers import rec_of, two_agent_overlap_records
 
 pytestmark = pytest.mark.gpu
 
@@ -85,3 +85,44 @@ def test_closed_loop_vs_oracle(policy):
     assert np.array_equal(got["miss_bytes"], exp[:, 1])
     assert np.array_equal(got["loaded_bytes"], exp[:, 2])
     assert np.array_equal(got["n_prefetch"], exp[:, 3]) and np.array_equal(got["n_evict"], exp[:, 4])
+
+
+def test_prefetch_overlap_closed_form():
+    """with B's action longer than transfer_time(A), the scalesim preset's stall for A's
+    next request is 0 and the reactive presets' is transfer_time(A) exactly."""
+    from paper_2601_21473_b200 import closed_loop
+    F = 1000 * tg.PAGE_BYTES
+    recs = two_agent_overlap_records(F)
+    blocks = tg.make_blocks([[tg.KIND_KV]] * 2, [[F]] * 2)
+    link, step_s = 55.0, 0.05
+    T_A = F / (link * 1e9)
+    assert T_A < 5 * step_s
+    args = (recs, np.arange(len(recs), dtype=np.int64), blocks.blk_ptr, blocks.blk_size, blocks.blk_host_off,
+            blocks.blk_kind, F, np.full(3, 10.0, np.float32))
+    out = {p: closed_loop.run(*args, policy=p, link_GBs=link, step_s=step_s)
+           for p in ("scalesim", "hicache_like", "sglang_like")}
+    assert out["scalesim"]["stall_s"][7] == 0.0
+    assert abs(out["hicache_like"]["stall_s"][7] - T_A) <= 1e-12 * T_A, out["hicache_like"]["stall_s"]
+    for p in ("hicache_like", "sglang_like"):
+        assert out[p]["misses"][7] == 1
+    # sglang_like: A's KV was dropped when B took the slot: recomputed, not moved (S:479)
+    assert out["sglang_like"]["recompute_bytes"][7] == F and out["sglang_like"]["stall_s"][7] == 0.0
+    assert out["scalesim"]["misses"][7] == 0 and out["scalesim"]["n_prefetch"][2] == 1
+    # the cold starts (steps 0 and 1) stall every preset by one transfer
+    for p in out:
+        assert abs(out[p]["stall_s"][0] - T_A) <= 1e-12 * T_A and abs(out[p]["stall_s"][1] - T_A) <= 1e-12 * T_A
+
+
+def test_sglang_like_drops_and_recomputes_kv():
+    """sglang_like (S:479): evicted KV / history is not written back, its reload is recompute;
+    hicache_like writes dirty KV back and reloads it over the link."""
+    from paper_2601_21473_b200 import closed_loop
+    w = tg.config_c2(seed=5, steps=30, n=2000, lora=4 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
+    b = w.blocks
+    args = (w.rec, w.now, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta)
+    hi = closed_loop.run(*args, policy="hicache_like")
+    sg = closed_loop.run(*args, policy="sglang_like")
+    assert np.array_equal(hi["misses"], sg["misses"])  # the same LRU plans
+    assert sg["writeback_bytes"].sum() == 0 and hi["writeback_bytes"].sum() > 0
+    assert sg["recompute_bytes"].sum() > 0
+    assert np.array_equal(sg["loaded_bytes"] + sg["recompute_bytes"], hi["loaded_bytes"])

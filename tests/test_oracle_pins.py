@@ -479,3 +479,40 @@ def test_bfs_closed_forms():
     assert all(h2[y * W + x] == min(x + y, (W - 1 - x) + (H - 1 - y)) for y in range(H) for x in range(W))
     # unreachable vertices, out-of-range source ignored
     assert oracle.bfs_hops(*_csr([[1], [0], []]), [0, 99]).tolist() == [0, 1, 0xFFFFFFFF]
+
+
+def test_prefetch_overlap_plans_two_agents():
+    """S:538 / P:174-185: in the two-agent, one-slot timeline the distance planner reloads A at
+    step 2 (while B acts, so A's transfer has 5 steps to finish: stall 0), while the reactive
+    LRU baseline keeps B and loads A only when A calls again at step 7 (stall = its transfer)."""
+    from helpers import two_agent_overlap_records
+    F = 1000 * tg.PAGE_BYTES
+    recs = two_agent_overlap_records(F)
+    res_d = np.zeros(2, np.uint8)
+    res_l = np.zeros(2, np.uint8)
+    last = np.full(2, 0xFFFFFFFF, np.uint32)
+    pf_d, pf_l = {}, {}
+    for t in range(len(recs)):
+        d, _ = oracle.score(recs[t], None, t)
+        p = oracle.plan(recs[t], d, res_d, np.full(3, 10.0, np.float32), F)
+        pf_d[t] = list(p["prefetch"])
+        res_d = p["resident"]
+        rl = oracle.lru_records(recs[t], t, last)
+        dl, _ = oracle.explicit_dist(rl)
+        q = oracle.plan(rl, dl, res_l, np.zeros(3, np.float32), F)
+        pf_l[t] = list(q["prefetch"])
+        res_l = q["resident"]
+    assert pf_d == {0: [0], 1: [1], 2: [0], 3: [], 4: [], 5: [], 6: [], 7: [], 8: []}
+    assert pf_l == {0: [0], 1: [1], 2: [], 3: [], 4: [], 5: [], 6: [], 7: [0], 8: []}
+
+
+def test_score_sampled_equals_full_score():
+    """The sampled oracle (full-size grid parity at 10^6 interaction agents) gives exactly the
+    full oracle's distances of the sampled agents (C3 shape, every class)."""
+    w = tg.config_c3(seed=4, steps=2, n=6000, budget=10 ** 9)
+    rng = np.random.default_rng(1)
+    for s in range(2):
+        d, st = oracle.score(w.rec[s], w.kin[s], int(w.now[s]), w.hop_scale)
+        idx = rng.choice(w.n, 500, replace=False)
+        ds, st2 = oracle.score_sampled(w.rec[s], w.kin[s], int(w.now[s]), idx, w.hop_scale)
+        assert np.array_equal(ds.view(np.uint32), d[idx].view(np.uint32))

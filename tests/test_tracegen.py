@@ -74,3 +74,25 @@ def test_records_and_blocks_layout():
     assert set(np.unique(cls).tolist()) == {0, 1, 2}
     ki = w.rec[0, cls == 1, 3]
     assert np.array_equal(ki, np.arange(len(ki)))
+
+
+def test_noise_knob_estimates_only():
+    """the noise knob perturbs only the recorded action ends (the estimates); phases
+    (the true lifecycle) are unchanged, noise 0 reproduces the exact trace, and the estimate
+    error of an action is lognormal with the knob's sigma (up to rounding)."""
+    P0, T0, D0 = tg.gen_independent(20000, 30, seed=3)
+    Pz, Tz, Dz = tg.gen_independent(20000, 30, seed=3, noise=0.0)
+    assert np.array_equal(P0, Pz) and np.array_equal(T0, Tz) and np.array_equal(D0, Dz)
+    P1, T1, D1 = tg.gen_independent(20000, 30, seed=3, noise=0.5)
+    assert np.array_equal(P0, P1) and np.array_equal(D0, D1)
+    acting = P0 == tg.PH_ACTING
+    assert np.array_equal(T0[~acting], T1[~acting])
+    assert (T0[acting] != T1[acting]).mean() > 0.3
+    # per action (first step an agent is ACTING after an LLM phase): log(est / true) duration
+    s = 5
+    start = acting[s] & ~acting[s - 1]
+    true = (T0[s, start] - s).astype(float)
+    est = (T1[s, start] - s).astype(float)
+    big = true >= 20  # (rounding negligible)
+    r = np.log(est[big] / true[big])
+    assert abs(r.mean()) < 0.05 and abs(r.std() - 0.5) < 0.05, (r.mean(), r.std(), big.sum())

@@ -159,14 +159,26 @@ def _calibrate_mu0(rng, active: float, sigma: float, g_mean: float) -> float:
 
 def gen_independent(n: int, steps: int, seed: int, active: float = 0.05, sigma: float = 1.0,
                     g_choices=(1, 2, 3), fixed_dur: Optional[tuple] = None, t0: int = 0,
-                    dirty_window: int = 16):
+                    dirty_window: int = 16, noise: float = 0.0):
     """AgentSociety-shaped independent agents.
 
     Each agent alternates an LLM phase of g ~ U(g_choices) steps (first step WAITING, then
     GENERATING) and an action of integer duration ~ Geometric(1/mu_i), mu_i ~
     LogNormal(ln mu0, sigma) (skewed invocation orders, heavy integer ties).  With
     ``fixed_dur=(lo, hi)`` durations are U{lo..hi} instead.  Initial phases are staggered.
+    ``noise`` > 0: the recorded action end is an estimate ("an optional
+    multiplicative noise knob perturbs D_action to model imperfect estimates"; "these
+    estimates do not need to be exact"): each action's duration is reported as
+    max(1, round(true duration * exp(noise * z))), z ~ N(0, 1) drawn once per action, while the
+    agent's phases follow the true durations (noise = 0: exact, and no extra random draws).
     Returns phase, t_next, dirty arrays of shape (steps, n)."""
+    nz_rng = np.random.Generator(np.random.PCG64(seed + 7919)) if noise > 0 else None
+
+    def estimate(start, dur):
+        if nz_rng is None:
+            return start + dur
+        z = nz_rng.standard_normal(len(dur))
+        return start + np.maximum(1, np.rint(dur * np.exp(noise * z))).astype(np.int64)
     rng = np.random.Generator(np.random.PCG64(seed))
     g_choices = np.asarray(g_choices, dtype=np.int64)
     if fixed_dur is None:
@@ -193,6 +205,7 @@ def gen_independent(n: int, steps: int, seed: int, active: float = 0.05, sigma: 
     else:
         remain = 1 + (rng.random(n) * dur).astype(np.int64)
     t_end = np.where(gen_now, t0 + rng.choice(g_choices, size=n), t0 + remain)
+    est_end = estimate(np.full(n, t0, np.int64), remain)  # (used while ACTING)
     last_gen = np.where(gen_now, t0, -(10 ** 9))
     gen_start = np.where(gen_now, t0 - 1, -(10 ** 9))
 
@@ -206,7 +219,9 @@ def gen_independent(n: int, steps: int, seed: int, active: float = 0.05, sigma: 
         idx = np.nonzero(done_gen)[0]
         if len(idx):
             phase[idx] = PH_ACTING
-            t_end[idx] = t + draw_dur(idx)
+            dd = draw_dur(idx)
+            t_end[idx] = t + dd
+            est_end[idx] = estimate(np.full(len(idx), t, np.int64), dd)
         # action finished -> issue an LLM call (S:146 activations at t_end)
         done_act = (phase == PH_ACTING) & (t_end <= t)
         idx = np.nonzero(done_act)[0]
@@ -219,7 +234,7 @@ def gen_independent(n: int, steps: int, seed: int, active: float = 0.05, sigma: 
         act = phase != PH_ACTING
         last_gen[act] = t
         P[s] = phase
-        T[s] = np.where(phase == PH_ACTING, t_end, 0)
+        T[s] = np.where(phase == PH_ACTING, est_end, 0)
         D[s] = (t - last_gen) < dirty_window
     return P, T, D
 
@@ -457,15 +472,16 @@ def config_c1(seed: int = 1, theta=(3.0, 3.0, 3.0), steps: int = 8, variant: str
 
 def config_c2(seed: int = 1, steps: int = 64, n: int = 10_000, host_bytes: Optional[int] = None,
               budget_frac: float = 0.25, theta_ind: float = 4.0, lora: int = LORA_7B, kv: int = KV_7B,
-              kv_mean: float = 3.0) -> Workload:
+              kv_mean: float = 3.0, noise: float = 0.0) -> Workload:
     """C2: AgentSociety-shaped trace, 10k agents, ~5% activated per step, 1 LoRA (rank 16,
-    Qwen2.5-7B q/k/v/o) + K ~ 1+Poisson(3) KV pages per agent; budget 25% of the total."""
+    Qwen2.5-7B q/k/v/o) + K ~ 1+Poisson(3) KV pages per agent; budget 25% of the total.
+    noise: the S:187 knob (recorded action ends are estimates, gen_independent)."""
     rng = np.random.Generator(np.random.PCG64(seed + 1000))
     n_kv = 1 + rng.poisson(kv_mean, size=n)
     blocks = _blocks_vectorized(n, lora, kv, n_kv, 0, host_bytes)
     fp = blocks.footprint
     budget = int(int(fp.sum()) * budget_frac)
-    P, T, D = gen_independent(n, steps, seed, active=0.05)
+    P, T, D = gen_independent(n, steps, seed, active=0.05, noise=noise)
     return _assemble("c2", P, T, D, np.full(n, CL_IND), fp, blocks, budget, (theta_ind, theta_ind, theta_ind),
                      meta=dict(budget_frac=budget_frac))
 
