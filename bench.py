@@ -383,6 +383,58 @@ def closed_loop_leg(dev, steps=64, seed=1):
                     "on one 55 GB/s channel, counted when its LLM call starts (reading R24)"}
 
 
+def sweep_leg(torch, dev, peak_gbs, ns_m=(1, 2, 4, 8, 16, 32, 64), K=10, reps=5, seed=1):
+    """N-sweep (SURVEY 8(d) "Report an N-sweep (1M..64M)"): the C4 population (1M independent
+    AgentSociety-shaped agents, C3 footprints, budget 25%) replicated m times = m x 1M agents on
+    one GPU, planned with the default kernel for its size (shared-memory tile up to 1.8M agents,
+    the streaming variant above); per N: K eager steps per repeat, 5 repeats (median, p10,
+    p90 of ms/step), each step reading its own record buffer; achieved HBM GB/s of the
+    algorithmic 16.25 B/agent against the measured peak and the 8 TB/s datasheet figure."""
+    from paper_2601_21473_b200.planner import Planner
+    T1 = 6 + K
+    w1 = tg.config_c4(seed=seed, steps=T1, n=1_000_000)
+    fp1 = np.ascontiguousarray(w1.rec[0][:, 1]).astype(np.uint32)
+    base = [torch.from_numpy(np.ascontiguousarray(w1.rec[s]).view(np.uint8).reshape(-1, 16)).to(dev) for s in range(T1)]
+    out = []
+    for m in ns_m:
+        n = m * 1_000_000
+        blk_ptr = np.arange(n + 1, dtype=np.uint64)
+        blk_size = np.tile(fp1, m)
+        pl = Planner(n, blk_ptr, blk_size, np.zeros(n, np.uint64), np.full(n, tg.KIND_KV, np.uint8), m * w1.budget,
+                     w1.theta, transfer=False, device=dev.index, keep_dist=False, exclusive=True)
+        del blk_ptr, blk_size
+        recs = [b.repeat(m, 1).reshape(-1) for b in base]
+        for s in range(6):
+            pl.set_inputs_ptr(recs[s].data_ptr())
+            pl.step(int(w1.now[s]))
+        hdr = pl.sync()
+        ms = []
+        for r in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(pl.stream):
+                torch.cuda._sleep(int(2e9 * 0.02 + K * 2e5 * max(1, m // 4)))
+            e0.record(pl.stream)
+            for k in range(K):  # (the same K record buffers each repeat; > L2 from 8M agents)
+                s = 6 + k
+                pl.set_inputs_ptr(recs[s].data_ptr())
+                pl.step(int(w1.now[s]))
+            e1.record(pl.stream)
+            torch.cuda.synchronize(dev)
+            ms.append(e0.elapsed_time(e1) / K)
+        hdr = pl.sync()
+        med = float(np.median(ms))
+        gbs = n * BYTES_PER_AGENT_STEP / (med / 1e3) / 1e9
+        out.append({"n_agents": n, "kernel": "streaming (fused_big)" if pl.big else ("shared-memory tile" if pl.fused else "multi-kernel"),
+                    "ms_per_step_median": med, "ms_p10": float(np.percentile(ms, 10)), "ms_p90": float(np.percentile(ms, 90)),
+                    "agent_plans_per_s": n / (med / 1e3), "hbm_GBs": gbs, "frac_measured_peak": gbs / peak_gbs,
+                    "frac_8TBs": gbs / 8000.0, "status": hdr["status"], "n_prefetch": hdr["n_prefetch"]})
+        pl.close()
+        del recs
+        torch.cuda.empty_cache()
+    return {"workload": "C4 population replicated: m x (1M independent agents, C3 footprints, budget 25%, theta 4)",
+            "repeats": reps, "steps_per_repeat": K, "launch_mode": "SCALESIM_F_EXCLUSIVE", "points": out}
+
+
 def sched_leg(torch, dev, link=None, seed=3):
     """NEXT #2: the preemptive load scheduler (scalesim_sched_run) moving C2-sized agents
     (7B rank-16 LoRA + KV pages, ~24 MB each) in 16 MB chunks over the host link: 160 prefetch
@@ -577,6 +629,7 @@ def main():
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 planning + transfer overlap leg")
     ap.add_argument("--no-closed-loop", action="store_true", help="skip the closed-loop policy comparison (NEXT #3)")
     ap.add_argument("--no-sched", action="store_true", help="skip the load scheduler leg (NEXT #2)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the 1M..64M agent N-sweep")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -786,6 +839,9 @@ def main():
                           f"instances sharded over {world} GPU(s), scalesim_step_batch",
               "instances_per_gpu": r5["instances"], "steps": r5["steps"], "ms_per_step": r5["ms"] / r5["steps"],
               "gpu_launches": r5["launches"]}
+    sweep = None
+    if not args.no_sweep and rank == 0:
+        sweep = sweep_leg(torch, dev, peaks()["hbm_gbs"])
     objects = None
     if not args.no_objects and rank == 0:
         objects = objects_leg(torch, dev)
@@ -852,6 +908,8 @@ def main():
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": sampler.result()}
     if c5 is not None:
         line["c5"] = c5
+    if sweep is not None:
+        line["n_sweep"] = sweep
     if objects is not None:
         line["objects"] = objects
     if c3 is not None:

@@ -65,6 +65,12 @@ typedef enum {
 #define SCALESIM_ST_NO_PAGES 8u     /* free page pool exhausted (cannot happen for a valid config) */
 #define SCALESIM_ST_SYNC 16u        /* internal: a fused-kernel CTA timed out waiting for another
                                        CTA's published offsets (cannot happen: grid co-resident) */
+#define SCALESIM_ST_LIMIT 32u       /* a large context (more than 12288 agents per SM, integer
+                                       distances: the streaming single-kernel plan) met a step
+                                       outside its scope: D* >= 2048 ticks, or more than 256
+                                       eligible agents at finite distances >= 2048 ticks; the
+                                       step's plan is not produced (create the context with
+                                       SCALESIM_F_MULTI_KERNEL for such workloads) */
 
 /* Config flags. */
 #define SCALESIM_F_NO_TRANSFER 1u   /* plan + byte accounting only: no arena, no pages, no copies
@@ -308,8 +314,10 @@ scalesim_status scalesim_nccl_unique_id(void *out128);
  * CUDA-graph capture that contains scalesim_transfer). */
 scalesim_status scalesim_join(scalesim_ctx *ctx);
 
-/* 1 if this context plans each step with the single persistent kernel, 0 if with the
- * multi-kernel path (world > 1, SCALESIM_F_MULTI_KERNEL, or tiles too large), -1 on NULL. */
+/* 1 if this context plans each step with the single persistent kernel, 2 with its streaming
+ * variant (integer distances, more than 12288 agents per SM: fused_big.cu), 0 with the
+ * multi-kernel path (world > 1 over NCCL, SCALESIM_F_MULTI_KERNEL, or large non-integer
+ * contexts), -1 on NULL. */
 int scalesim_fused(const scalesim_ctx *ctx);
 
 /* Device pointer to 64 uint64 %globaltimer stamps (ns) written by the fused plan kernel:

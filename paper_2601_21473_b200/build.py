@@ -10,8 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libscalesim.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "fused.cu", "objects.cu", "interaction.cu", "baselines.cu", "bfs.cu", "sched.cu", "api.cpp")]
-HEADERS = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "scalesim.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "fused.cu", "fused_big.cu", "objects.cu", "interaction.cu", "baselines.cu", "bfs.cu", "sched.cu", "api.cpp")]
+HEADERS = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "fused_common.cuh"), os.path.join(ROOT, "include", "scalesim.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

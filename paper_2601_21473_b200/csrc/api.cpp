@@ -115,7 +115,8 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_pos = take(8 * 2 * 4096 * (uint64_t)FUSED_MAX_CTAS);
   L.f_rt = take(8 * 2 * (uint64_t)FUSED_MAX_CTAS);
   L.f_crow = take(4 * 2 * 4096 * (uint64_t)FUSED_MAX_CTAS);
-  L.f_ovf = take(16 * 2 * (uint64_t)FUSED_OVF_CAP);
+  L.f_ovf = take(16 * 2 * (uint64_t)BIG_OVF_CAP);
+  L.big_codes = take(2 * n1);
   L.total = off;
   return L;
 }
@@ -198,6 +199,7 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_rt = (unsigned long long *)(b + L.f_rt);
   d.f_crow = (uint32_t *)(b + L.f_crow);
   d.f_ovf = (uint4 *)(b + L.f_ovf);
+  d.big_codes = (uint16_t *)(b + L.big_codes);
   return d;
 }
 
@@ -268,6 +270,7 @@ struct scalesim_ctx {
   bool xfer_pending = false;
   bool xfer_recorded[2] = {false, false};  // ev_xfer[b] has been recorded at least once
   bool exclusive = false;                  // SCALESIM_F_EXCLUSIVE
+  bool big = false;                        // large context: the streaming single-kernel plan
   cudaEvent_t ev_fused = nullptr;          // after this context's last single-kernel plan
   // fused single-kernel plan (world == 1)
   bool fused = false;
@@ -354,7 +357,7 @@ extern "C" scalesim_status scalesim_nccl_unique_id(void *out128) {
 
 extern "C" uint64_t scalesim_launch_count(const scalesim_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
-extern "C" int scalesim_fused(const scalesim_ctx *ctx) { return ctx ? (ctx->fused ? 1 : 0) : -1; }
+extern "C" int scalesim_fused(const scalesim_ctx *ctx) { return ctx ? (ctx->big ? 2 : (ctx->fused ? 1 : 0)) : -1; }
 
 extern "C" const uint64_t *scalesim_profile_stamps(const scalesim_ctx *ctx) {
   return ctx ? reinterpret_cast<const uint64_t *>(ctx->p.d.f_prof) : nullptr;
@@ -542,6 +545,17 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
       c->fused_tile = tile;
       c->fused_grid = g;
       c->sms = sms;
+    } else if (cfg->world == 1 && p.int_mode) {
+      // more agents per CTA than shared memory holds: the streaming kernel (fused_big.cu)
+      uint64_t t = (p.n_local + g - 1) / g;
+      t = (t + 31) / 32 * 32;
+      if (t > FUSED_MAX_TILE && t <= FUSED_BIG_MAX_TILE && g <= FUSED_MAX_CTAS && fused_big_prepare((uint32_t)g)) {
+        c->fused = true;
+        c->big = true;
+        c->fused_tile = (uint32_t)t;
+        c->fused_grid = g;
+        c->sms = sms;
+      }
       if (cudaMemsetAsync(p.d.f_mm1, 0xFF, 4 * 2 * 2 * 4096, c->stream) != cudaSuccess ||
           cudaMemsetAsync(p.d.f_mm2, 0xFF, 4 * 2 * 2 * 1024, c->stream) != cudaSuccess)
         return fail(SCALESIM_E_CUDA);
@@ -625,6 +639,19 @@ static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out);
 // One single-kernel plan launch (n instances on c's stream): cooperative unless c is an
 // exclusive context; exclusive launches of different contexts of a device are chained.
 static int launch_fused(scalesim_ctx *c, const FusedInst *insts, uint32_t n, uint32_t gsize, uint32_t wsize = 1) {
+  if (c->big) {  // (single instance)
+    if (!c->exclusive) return launch_fused_big(insts[0], gsize, c->stream, true);
+    std::lock_guard<std::mutex> g(g_excl_mu);
+    ExclusiveChain &x = g_excl[c->cfg.device];
+    if (x.contexts > 1 && x.stream && x.stream != c->stream) cudaStreamWaitEvent(c->stream, x.event, 0);
+    const int k = launch_fused_big(insts[0], gsize, c->stream, false);
+    if (x.contexts > 1) {
+      cudaEventRecord(c->ev_fused, c->stream);
+      x.stream = c->stream;
+      x.event = c->ev_fused;
+    }
+    return k;
+  }
   if (!c->exclusive) return launch_fused_batch(insts, n, gsize, c->stream, true, wsize);
   std::lock_guard<std::mutex> g(g_excl_mu);
   ExclusiveChain &x = g_excl[c->cfg.device];
@@ -811,7 +838,7 @@ extern "C" scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32
   if (!c0) return SCALESIM_E_INVALID;
   for (uint32_t i = 0; i < n; ++i) {
     scalesim_ctx *c = ctxs[i];
-    if (!c || !c->fused || c->stream != c0->stream || c->cfg.device != c0->cfg.device ||
+    if (!c || !c->fused || c->big || c->stream != c0->stream || c->cfg.device != c0->cfg.device ||
         c->exclusive != c0->exclusive)
       return SCALESIM_E_INVALID;
     for (uint32_t j = 0; j < i; ++j)
@@ -894,7 +921,7 @@ extern "C" scalesim_status scalesim_step_group(scalesim_ctx *const *ctxs, uint32
 
 static scalesim_status status_of_header(uint64_t st) {
   if (st & (SCALESIM_ST_BAD_RECORD | SCALESIM_ST_BAD_KIN)) return SCALESIM_E_BAD_INPUT;
-  if (st & (SCALESIM_ST_NO_PAGES | SCALESIM_ST_SYNC)) return SCALESIM_E_INVARIANT;
+  if (st & (SCALESIM_ST_NO_PAGES | SCALESIM_ST_SYNC | SCALESIM_ST_LIMIT)) return SCALESIM_E_INVARIANT;
   if (st & SCALESIM_ST_INSUFFICIENT) return SCALESIM_E_INSUFFICIENT;
   return SCALESIM_OK;
 }

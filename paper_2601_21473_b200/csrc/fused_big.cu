@@ -1,0 +1,720 @@
+// fused_big.cu — the single-kernel plan of LARGE integer-distance contexts: more agents per SM
+// than fused.cu's shared-memory tile holds (> FUSED_MAX_TILE = 12288 per CTA, i.e. above
+// ~1.8M agents on 148 SMs), up to 2^19 agents per CTA (~77M per GPU).
+//
+// Same method and same bucket-owner list placement as fused.cu, but the
+// per-agent state between the score pass and the emit pass lives in HBM as one 16-bit code per
+// agent (level-1 value bucket, eligibility, residency, dirty bit: 2 B written + 2 B read per
+// agent on top of the 16-byte record) instead of shared memory; footprints are re-read from the
+// record only for the agents that need them (the tie group at D*, prefetched agents).
+//   P1   stream the CTA's records: distance, eligibility, bucket; byte and count histograms in
+//        shared memory; code -> HBM
+//   B1   grid barrier; select D* (warp 0) while the other warps stage this CTA's bucket-owner
+//        columns; owner pass; this CTA's list-bucket positions from the owners
+//   P34  the CTA's words in chunks of 1024, from the highest id down: tie bytes per word, their
+//        scan (the offset of a chunk follows from the CTA's tie total and the chunks above it),
+//        kept / prefetch / evict words, new residency, byte sums; the chunk's list candidates
+//        in descending id order are placed by two warps with per-bucket cursors (evict: next
+//        free position; prefetch: counting down from the bucket's last position, so that the
+//        list stays in ascending id order)
+// Limits (status SCALESIM_ST_LIMIT, the step's plan is not produced): the boundary D* falls in
+// a multi-valued bucket (>= 2048 ticks), or more than BIG_OVF_CAP (4096) eligible agents have
+// finite distances >= 2048 ticks (or more than 128 in one CTA).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fused_common.cuh"
+
+namespace ss {
+
+constexpr uint32_t BIG_CW = 1024;    // words per P34 chunk (one per thread)
+constexpr uint32_t BIG_MCAP = 2048;  // list candidates per placement round (per list)
+
+static uint32_t big_rb(uint32_t gsize) { return ((NB1 + gsize - 1) / gsize + 3u) & ~3u; }
+
+size_t fused_big_smem_bytes(uint32_t gsize) {
+  const uint32_t RB = big_rb(gsize);
+  return (size_t)4 * 4 * NB1             // histograms / counts / need list, later positions
+         + (size_t)4 * RB * (gsize + 4)  // bucket-owner staging
+         + (size_t)4 * 8 * BIG_CW        // per-word masks of a chunk
+         + (size_t)8 * 2 * BIG_CW        // per-word tie bytes and offsets
+         + (size_t)4 * 2 * BIG_MCAP      // the two candidate lists of a round
+         + 64;
+}
+
+__global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ FusedArgs<1> B) {
+  const uint32_t c = blockIdx.x, G = B.gsize;
+  const FusedInst &I = B.inst[0];
+  __shared__ __align__(16) Params sp;
+  {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(I.params);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(&sp);
+    for (uint32_t q = threadIdx.x; q < sizeof(Params) / 4; q += FT) dst[q] = src[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sp.rec = I.rec;
+    sp.kin = I.kin;
+    sp.cur = (int)I.cur;
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const Params &p = sp;
+  const Dev &d = p.d;
+  const int par = (int)I.parity;
+  const uint32_t tile = I.tile, ep = I.epoch & 0xFFFFu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  GridBar wgrid{d.f_bar + 2 + par, 0u, G};
+  if (c == 0 && threadIdx.x == 0) {
+    d.f_bar[2 + (par ^ 1)] = 0u;
+    unsigned long long *H = d.header;
+    H[H_N_PF] = H[H_N_EV] = H[H_H2D] = H[H_D2H] = H[H_KEPT] = H[H_N_ELIG] = H[H_STATUS] = 0ull;
+  }
+  unsigned long long *prof = d.f_prof;
+  PROBE(if (threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    atomicMin(&prof[0], t);
+  })
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint32_t *h = reinterpret_cast<uint32_t *>(smem_raw);  // [4 NB1]
+  const uint32_t RB = ((NB1 + G - 1) / G + 3u) & ~3u;
+  uint32_t *col = h + 4 * NB1;                            // [G][RB] + [4][RB]
+  uint32_t *mE = col + RB * (G + 4);                      // per-word masks of a chunk [8][CW]
+  uint32_t *mR = mE + BIG_CW, *mY = mR + BIG_CW, *mLT = mY + BIG_CW, *mTIE = mLT + BIG_CW;
+  uint32_t *mPFC = mTIE + BIG_CW, *mEVC = mPFC + BIG_CW, *mKEPT = mEVC + BIG_CW;
+  unsigned long long *sTB = reinterpret_cast<unsigned long long *>(mKEPT + BIG_CW);  // [CW]
+  unsigned long long *sLO = sTB + BIG_CW;                                            // [CW]
+  uint32_t *lpf = reinterpret_cast<uint32_t *>(sLO + BIG_CW), *lev = lpf + BIG_MCAP;  // candidates
+  const uint64_t base = (uint64_t)c * tile;
+  const uint32_t n_here =
+      base >= p.n_local ? 0u : (uint32_t)((p.n_local - base) < tile ? (p.n_local - base) : tile);
+  const uint32_t tw_here = (n_here + 31) / 32;
+  unsigned long long *acc = d.f_acc + 8 * par;
+  const uint32_t *bm_old = d.bm[p.cur];
+  uint32_t *bm_new = d.bm[p.cur ^ 1];
+  uint16_t *codes = d.big_codes + base;
+  const uint4 *rec = p.rec + base;
+
+  // ---------------- P1: score, histograms, codes
+  for (int b = threadIdx.x; b < 3 * NB1; b += FT) h[b] = 0u;
+  constexpr uint32_t LOVF = 128;
+  __shared__ uint4 s_ovf[LOVF];
+  __shared__ uint32_t s_novf;
+  __shared__ uint32_t sacc[24];
+  if (threadIdx.x == 0) s_novf = 0;
+  if (threadIdx.x < 24) sacc[threadIdx.x] = 0;
+  __syncthreads();
+  {
+    const float hop_scale = p.hop_scale, th0 = p.theta[0], th1 = p.theta[1], th2 = p.theta[2];
+    const int64_t now = I.now;
+    const bool now32 = now >= 0 && now <= 0xFFFFFFFFll;
+    const uint32_t nowl = (uint32_t)now;
+    uint32_t st = 0;
+    uint32_t *gkeys = p.keep_dist ? d.keys + base : nullptr;
+    const uint32_t last = n_here ? n_here - 1 : 0u;
+    const uint32_t BS = LOAD_BATCH * FT, nk = tw_here * 32;
+    uint4 r[LOAD_BATCH], r2[LOAD_BATCH];
+    uint32_t bw[LOAD_BATCH], bw2[LOAD_BATCH];  // the residency words, loaded with the records
+    const uint32_t tw_all = (uint32_t)((p.n_local + 31) / 32);
+    auto load_into = [&](uint4 (&rr)[LOAD_BATCH], uint32_t (&ww)[LOAD_BATCH], uint32_t k0) {
+#pragma unroll
+      for (int j = 0; j < LOAD_BATCH; ++j) {
+        rr[j] = n_here ? ld_stream(rec + min(k0 + j * FT + threadIdx.x, last)) : make_uint4(0, 0, 0, 0);
+        const uint64_t wi = (base + k0 + j * FT + threadIdx.x) >> 5;
+        ww[j] = wi < tw_all ? bm_old[wi] : 0u;
+      }
+    };
+    load_into(r, bw, 0);
+#pragma unroll 1
+    for (uint32_t k0 = 0; k0 < nk; k0 += BS) {
+      if (k0 + BS < nk) load_into(r2, bw2, k0 + BS);
+#pragma unroll
+      for (int j = 0; j < LOAD_BATCH; ++j) {
+        const uint32_t k = k0 + j * FT + threadIdx.x;  // (k & 31 == lane)
+        if (k0 + j * FT >= nk) break;                  // (CTA-uniform)
+        const uint4 rj = r[j];
+        const bool valid = k < n_here;
+        const uint32_t rw = valid ? bw[j] : 0u;  // (one word per warp)
+        const bool res = (rw >> lane) & 1u;
+        const uint32_t ph = rj.z & 3u, cl = (rj.z >> 2) & 3u;
+        float dist, th;
+        if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {  // interaction / diffusion / malformed
+          dist = valid ? distance_of(rj, now, hop_scale, d.dint, p.n_kin, st) : 0.0f;
+          th = (cl & 2u) ? ((cl & 1u) ? 0.0f : th2) : ((cl & 1u) ? th1 : th0);
+        } else {
+          float d_action;
+          if (now32) d_action = rj.x > nowl ? __uint2float_rn(rj.x - nowl) : 0.0f;
+          else {
+            const int64_t remain = (int64_t)rj.x - now;
+            d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
+          }
+          dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
+          th = th0;
+        }
+        const uint32_t bits = valid ? __float_as_uint(dist) : 0u;
+        const bool elig = valid && (res || dist == 0.0f || dist < th);
+        const uint32_t q = ibucket(bits);
+        if (elig) {
+          atomicAdd(&h[q], rj.y & 0xFFFFu);
+          atomicAdd(&h[NB1 + q], rj.y >> 16);
+          atomicAdd(&h[2 * NB1 + q], res ? 0x10000u : 1u);
+          if (ib_multi(q)) {
+            const uint32_t jo = atomicAdd(&s_novf, 1u);
+            if (jo < LOVF) s_ovf[jo] = make_uint4(bits, (uint32_t)(p.shard_begin + base + k), res ? 1u : 0u, 0u);
+          }
+        }
+        if (valid) {
+          codes[k] = (uint16_t)(q | (elig ? 1u << 12 : 0u) | (res ? 1u << 13 : 0u) | (((rj.z >> 4) & 1u) << 14));
+          if (gkeys) gkeys[k] = bits;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < LOAD_BATCH; ++j) {
+        r[j] = r2[j];
+        bw[j] = bw2[j];
+      }
+    }
+    st = __reduce_or_sync(0xFFFFFFFFu, st);
+    if (lane == 0 && st) atomicOr(reinterpret_cast<unsigned int *>(&acc[5]), st);
+  }
+  __syncthreads();
+  STAMP_MAX(25)  // P1 loop
+  publish_hist(h, NB1, d.f_hist1 + NB1 * par, nullptr, d.f_rows1 + (uint64_t)c * NB1, d.f_hist1 + 2 * NB1 + 64 * par,
+               false);
+  reinterpret_cast<uint4 *>(d.f_crow + ((uint64_t)par * G + c) * NB1)[threadIdx.x] =
+      reinterpret_cast<const uint4 *>(h + 2 * NB1)[threadIdx.x];  // (NB1 / 4 == FT)
+  {
+    const uint32_t nov = s_novf;
+    if (nov) {
+      __shared__ unsigned long long s_ovbase;
+      if (threadIdx.x == 0)
+        s_ovbase = atomicAdd(&acc[6], nov <= LOVF ? (unsigned long long)nov : BIG_OVF_CAP + 1ull);
+      __syncthreads();
+      const unsigned long long ob = s_ovbase;
+      if (threadIdx.x < nov && nov <= LOVF && ob + threadIdx.x < BIG_OVF_CAP)
+        d.f_ovf[(uint64_t)par * BIG_OVF_CAP + ob + threadIdx.x] = s_ovf[threadIdx.x];
+    }
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long zb = ((unsigned long long)h[NB1] << 16) + h[0];  // bucket 0: d == 0
+    if (zb) atomicAdd(&acc[0], zb);
+  }
+  STAMP_MAX(26)  // published
+  wgrid.sync();
+  STAMP_MAX(4)   // B1
+
+  // ---------------- select, bucket owners, list-bucket positions
+  {
+    const int q = par ^ 1;
+    const uint32_t gt = c * FT + threadIdx.x, gs = G * FT;
+    for (uint32_t b = gt; b < NB1; b += gs) {
+      d.f_hist1[NB1 * q + b] = 0;
+      if (b < 64) d.f_hist1[2 * NB1 + 64 * q + b] = 0;
+    }
+    if (gt < 8) d.f_acc[8 * q + gt] = 0;
+  }
+  const uint32_t o_lo = min((uint32_t)NB1, c * RB), o_n = min((uint32_t)NB1, o_lo + RB) - o_lo;
+  const uint32_t QP = (G + 31) / 32;
+  if (warp > 0) {
+    const uint32_t ch = o_n / 4;
+    for (uint32_t x = threadIdx.x - 32; x < G * ch; x += FT - 32) {
+      const uint32_t qq = x / ch, k = x - qq * ch;
+      cp_async16(col + qq * RB + 4 * k, d.f_crow + ((uint64_t)par * G + qq) * NB1 + o_lo + 4 * k);
+    }
+    cp_async_commit();
+  }
+  __shared__ unsigned long long sh_novf;
+  if (threadIdx.x == 32) sh_novf = acc[6];
+  __shared__ WorldPtrs sw;
+  if (threadIdx.x == 0) {
+    sw.nw = 1;
+    sw.rank = 0;
+    sw.h1[0] = d.f_hist1;
+    sw.h2[0] = d.f_hist2;
+    sw.h3[0] = d.f_hist3;
+    sw.m1[0] = d.f_mm1;
+    sw.m2[0] = d.f_mm2;
+    sw.acc[0] = d.f_acc;
+    sw.hdr[0] = d.header;
+  }
+  __syncthreads();
+  Sel sel = {0, 0, 0, 0xFFFFFFFFu, 0, 0, 1, 0};
+  select_level1_warp(sw, par, p.budget, sel, true, prof);
+  const bool all_fit = sel.all_fit;
+  const uint32_t dstar = sel.dstar;
+  const uint32_t bs = all_fit ? (uint32_t)NB1 : sel.b_res;
+  const bool ok = sh_novf <= BIG_OVF_CAP && (all_fit || (sel.done && sel.level_res == 1 && !ib_multi(bs)));
+  cp_async_wait_all();
+  __syncthreads();
+  if (!ok) {  // outside this kernel's scope: the step's plan is not produced (documented limit)
+    if (c == 0 && threadIdx.x == 0) {
+      unsigned long long *H = d.header;
+      H[H_STATUS] = ST_LIMIT;
+      H[H_SEQ] = H[H_SEQ] + 1;
+    }
+    return;
+  }
+  // preceding CTAs' bytes at D* (tie prefix), and this CTA's own
+  __shared__ unsigned long long sh_tpre, sh_town;
+  unsigned long long t_rows = 0;
+  if (!all_fit && threadIdx.x < c) t_rows = d.f_rows1[(uint64_t)threadIdx.x * NB1 + bs];
+  if (!all_fit && threadIdx.x == FT - 1) sh_town = d.f_rows1[(uint64_t)c * NB1 + bs];
+  if (all_fit && threadIdx.x == FT - 1) sh_town = 0;
+  // bucket owner pass (as fused.cu)
+  {
+    uint32_t *tn = col + G * RB, *tr = tn + RB, *wn = tr + RB, *wr = wn + RB;
+    for (uint32_t j = warp; j < o_n; j += FWARPS) {
+      uint32_t a = 0, e = 0;
+      for (uint32_t i = 0; i < QP; ++i) {
+        const uint32_t q = lane * QP + i;
+        if (q < G) {
+          const uint32_t v = col[q * RB + j];
+          a += v & 0xFFFFu;
+          e += v >> 16;
+        }
+      }
+      a = __reduce_add_sync(0xFFFFFFFFu, a);
+      e = __reduce_add_sync(0xFFFFFFFFu, e);
+      if (lane == 0) {
+        tn[j] = a;
+        tr[j] = e;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t JP = (o_n + 31) / 32;
+      uint32_t sa = 0, se = 0;
+      for (uint32_t i = 0; i < JP; ++i) {
+        const uint32_t j = lane * JP + i;
+        if (j < o_n) {
+          sa += tn[j];
+          se += tr[j];
+        }
+      }
+      const uint32_t ia = warp_incl_scan(sa), ie = warp_incl_scan(se);
+      const uint32_t TA = __shfl_sync(0xFFFFFFFFu, ia, 31), TE = __shfl_sync(0xFFFFFFFFu, ie, 31);
+      uint32_t ra = ia - sa, re = ie - se;
+      for (uint32_t i = 0; i < JP; ++i) {
+        const uint32_t j = lane * JP + i;
+        if (j < o_n) {
+          wn[j] = ra;
+          ra += tn[j];
+          re += tr[j];
+          wr[j] = TE - re;
+        }
+      }
+      if (lane == 0) st_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + c], pack_ep(ep, TA, TE));
+    }
+    __syncthreads();
+    for (uint32_t j = warp; j < o_n; j += FWARPS) {
+      const uint32_t w_n = wn[j], w_r = wr[j], t_r = tr[j];
+      unsigned long long *P = d.f_pos + ((uint64_t)par * NB1 + o_lo + j) * FUSED_MAX_CTAS;
+      uint32_t ca = 0, ce = 0;
+      for (uint32_t q0 = 0; q0 < G; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        const uint32_t v = q < G ? col[q * RB + j] : 0u;
+        const uint32_t a = v & 0xFFFFu, e = v >> 16;
+        const uint32_t ia = warp_incl_scan(a), ie = warp_incl_scan(e);
+        if (q < G) st_relaxed_u64(&P[q], pack_ep(ep, w_n + ca + ia - a, w_r + t_r - (ce + ie)));
+        ca += __shfl_sync(0xFFFFFFFFu, ia, 31);
+        ce += __shfl_sync(0xFFFFFFFFu, ie, 31);
+      }
+    }
+  }
+  warp_add_u64(t_rows, sacc + 20);
+  // the buckets where this CTA has list candidates (multi-valued ones: the overflow CTA)
+  uint32_t *lcnt = h + 2 * NB1, *need = h + 3 * NB1;
+  __shared__ uint32_t sh_m;
+  if (threadIdx.x == 0) sh_m = 0;
+  __syncthreads();
+#pragma unroll 1
+  for (uint32_t b = threadIdx.x; b < NB1; b += FT) {
+    const uint32_t v = lcnt[b];
+    const bool nd = !ib_multi(b) && (b < bs ? (v & 0xFFFFu) != 0u : (b > bs ? (v >> 16) != 0u : v != 0u));
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, nd);
+    uint32_t j0 = 0;
+    if (lane == 0 && bal) j0 = atomicAdd(&sh_m, (uint32_t)__popc(bal));
+    j0 = __shfl_sync(0xFFFFFFFFu, j0, 0);
+    if (nd) need[j0 + __popc(bal & lanemask_lt())] = b;
+  }
+  __syncthreads();
+  const uint32_t m_need = sh_m;
+  STAMP_MAX(41)  // select, owner pass, need list
+  const unsigned long long tie_pre = parts_u64(sacc + 20), tie_own = sh_town;
+  // positions: range starts from the owners' totals, then each list bucket's offsets for this
+  // CTA; prefetch cursors count down from the bucket's last position (candidates come in
+  // descending id order), evict cursors up from the first
+  uint32_t *h32 = h;  // [0, NB1): prefetch cursors, [NB1, 2 NB1): evict cursors
+  __shared__ uint32_t sh_spf, sh_sev, sh_mvpf, sh_mvev;
+  {
+    uint32_t *rps = col, *rpe = col + G;
+    const unsigned long long *Pc = d.f_pos + (uint64_t)par * NB1 * FUSED_MAX_CTAS + c;
+    const unsigned long long pv0 =
+        threadIdx.x < m_need ? ld_relaxed_u64(Pc + (uint64_t)need[threadIdx.x] * FUSED_MAX_CTAS) : 0ull;
+    unsigned long long rv = 0;
+    if (threadIdx.x < G) rv = poll_ep(&d.f_rt[par * FUSED_MAX_CTAS + threadIdx.x], ep, d.header);
+    const uint32_t ra = (uint32_t)(rv >> 24) & 0xFFFFFFu, re = (uint32_t)rv & 0xFFFFFFu;
+    unsigned long long pk[1] = {(unsigned long long)ra | ((unsigned long long)re << 32)}, tt[1];
+    cta_scan1(pk, tt);
+    const uint32_t r_tot = (uint32_t)(tt[0] >> 32);
+    if (threadIdx.x < G) {
+      rps[threadIdx.x] = (uint32_t)pk[0];
+      rpe[threadIdx.x] = r_tot - (uint32_t)(pk[0] >> 32) - re;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < m_need; j += FT) {
+      const uint32_t b = need[j];
+      unsigned long long v = j == threadIdx.x ? pv0 : ld_relaxed_u64(Pc + (uint64_t)b * FUSED_MAX_CTAS);
+      if ((uint32_t)(v >> 48) != ep) v = poll_ep(Pc + (uint64_t)b * FUSED_MAX_CTAS, ep, d.header);
+      const uint32_t nr = lcnt[b] & 0xFFFFu;
+      h32[b] = rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu) + nr - 1u;  // (wraps when nr == 0: unused)
+      h32[NB1 + b] = rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
+    }
+    auto pos_pf = [&](uint32_t b) {
+      const unsigned long long v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS], ep, d.header);
+      return rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
+    };
+    auto pos_ev = [&](uint32_t b) {
+      const unsigned long long v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS + G - 1], ep, d.header);
+      return rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
+    };
+    if (c == 0 && threadIdx.x == 0) {
+      sh_spf = bs < (uint32_t)NB1 ? pos_pf(bs) : (uint32_t)tt[0];
+      sh_sev = bs < (uint32_t)NB1 ? pos_ev(bs) : 0u;
+    }
+    if (c == G - 1 && threadIdx.x == 32) {
+      sh_mvpf = pos_pf(IB_EXACT);
+      sh_mvev = pos_ev(IB_INF - 1);
+    }
+    __syncthreads();
+  }
+
+  STAMP_MAX(17)  // positions
+  // ---------------- P34: chunks of words from the highest id down
+  PROBE(unsigned long long dta = 0, dtb = 0, dtc = 0, dtd = 0, tq = gtimer();)
+#define LAP(v) PROBE(if (threadIdx.x == 0) { const unsigned long long t_ = gtimer(); v += t_ - tq; tq = t_; })
+  unsigned long long h2d = 0, tie_kept = 0, d2h = 0;
+  uint32_t n_el = 0, n_pfb = 0, n_evb = 0;
+  unsigned long long above = 0;  // tie bytes of the chunks done (all above this chunk)
+  const unsigned long long rem = sel.rem;
+  const uint32_t n_chunks = (tw_here + BIG_CW - 1) / BIG_CW;
+  __shared__ unsigned long long sh_ctot;
+  __shared__ uint32_t sh_cp, sh_ce;
+  for (int ch = (int)n_chunks - 1; ch >= 0; --ch) {
+    const uint32_t w0 = (uint32_t)ch * BIG_CW, wn = min(BIG_CW, tw_here - w0);
+    // (a) decode the chunk's codes: masks and tie bytes, one word (32 agents, 64 bytes of
+    // codes) per thread
+    if (threadIdx.x < wn) {
+      const uint32_t i = threadIdx.x, w = w0 + i;
+      const uint4 *cw = reinterpret_cast<const uint4 *>(codes + (uint64_t)w * 32);
+      uint4 q4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q4[u] = cw[u];  // (beyond n_here: zero codes, ineligible)
+      uint32_t em = 0, rm = 0, ym = 0, lm = 0, tm = 0, pm = 0, mv = 0;
+#pragma unroll
+      for (int l = 0; l < 32; ++l) {
+        const uint32_t word = (&q4[l >> 3].x)[(l >> 1) & 3];
+        const uint32_t code = (l & 1) ? (word >> 16) : (word & 0xFFFFu);
+        const uint32_t q = code & 0xFFFu, bit = 1u << l;
+        const bool e = (code >> 12) & 1u, r = (code >> 13) & 1u;
+        em |= e ? bit : 0u;
+        rm |= r ? bit : 0u;
+        ym |= ((code >> 14) & 1u) ? bit : 0u;
+        lm |= (e && (all_fit || q < bs)) ? bit : 0u;
+        tm |= (e && !all_fit && q == bs) ? bit : 0u;
+        pm |= (e && !r && (all_fit || q <= bs) && !ib_multi(q)) ? bit : 0u;
+        mv |= (e && ib_multi(q)) ? bit : 0u;
+      }
+      unsigned long long tb = 0;
+      for (uint32_t m = tm; m; m &= m - 1) tb += rec[w * 32 + __ffs(m) - 1].y;  // (ties: few)
+      mE[i] = em;
+      mR[i] = rm;
+      mY[i] = ym;
+      mLT[i] = lm;
+      mTIE[i] = tm;
+      mPFC[i] = pm;
+      mEVC[i] = mv;  // (multi-valued mask for now)
+      sTB[i] = tb;
+    }
+    __syncthreads();
+    LAP(dta)
+    // (b) offsets of the words' tie bytes: the chunk starts after the preceding CTAs' ties and
+    // this CTA's ties below the chunk (= own total - chunks above - this chunk)
+    {
+      unsigned long long v[1] = {threadIdx.x < wn ? sTB[threadIdx.x] : 0ull}, tt[1];
+      cta_scan1(v, tt);
+      const unsigned long long off = tie_pre + (tie_own - above - tt[0]);
+      if (threadIdx.x < wn) sLO[threadIdx.x] = off + v[0];
+      if (threadIdx.x == 0) sh_ctot = tt[0];
+    }
+    __syncthreads();
+    LAP(dtb)
+    above += sh_ctot;
+    // (c) kept / prefetch / evict words, residency, byte sums: one word per thread
+    if (threadIdx.x < wn) {
+      const uint32_t i = threadIdx.x, w = w0 + i;
+      uint32_t kw = mLT[i];
+      const uint32_t tiew = mTIE[i];
+      if (tiew) {
+        const unsigned long long lo = sLO[i], hi = lo + sTB[i];
+        if (hi <= rem) {
+          kw |= tiew;
+          tie_kept += sTB[i];
+        } else if (lo <= rem) {  // the straddling word: its ties in id order
+          unsigned long long incl = lo;
+          for (uint32_t m = tiew; m; m &= m - 1) {
+            const int l = __ffs(m) - 1;
+            const uint32_t fp = rec[w * 32 + l].y;
+            incl += fp;
+            if (incl <= rem) {
+              kw |= 1u << l;
+              tie_kept += fp;
+            }
+          }
+        }
+      }
+      const uint32_t rm = mR[i];
+      const uint32_t pfw = kw & ~rm, evw = rm & ~kw;
+      if (w < tw_here) bm_new[(base >> 5) + w] = kw;
+      n_el += __popc(mE[i]);
+      n_pfb += __popc(pfw & tiew);
+      n_evb += __popc(evw & tiew);
+      mKEPT[i] = kw;
+      mEVC[i] = evw & ~mEVC[i];  // evict members outside multi-valued buckets
+      for (uint32_t m = pfw; m; m &= m - 1) h2d += rec[w * 32 + __ffs(m) - 1].y;
+      for (uint32_t m = evw & mY[i]; m; m &= m - 1) d2h += d.wb_bytes[base + w * 32 + __ffs(m) - 1];
+    }
+    __syncthreads();
+    LAP(dtc)
+    // (d) the chunk's candidates in descending id order, placed by two warps in rounds
+    {
+      // reversed word order: word wn-1-t at thread t
+      const uint32_t t = threadIdx.x;
+      const uint32_t iw = t < wn ? wn - 1 - t : 0u;
+      const uint32_t cp = t < wn ? __popc(mPFC[iw]) : 0u, ce = t < wn ? __popc(mEVC[iw]) : 0u;
+      unsigned long long v[1] = {(unsigned long long)cp | ((unsigned long long)ce << 32)}, tt[1];
+      cta_scan1(v, tt);
+      const uint32_t xp = (uint32_t)v[0], xe = (uint32_t)(v[0] >> 32);
+      if (t == 0) {
+        sh_cp = (uint32_t)tt[0];
+        sh_ce = (uint32_t)(tt[0] >> 32);
+      }
+      __syncthreads();
+      const uint32_t np = sh_cp, ne = sh_ce;
+      for (uint32_t r0 = 0; r0 < max(np, ne); r0 += BIG_MCAP) {
+        if (t < wn) {  // this word's candidates in the round's window, highest lane first
+          const uint32_t wbase = (w0 + iw) * 32;
+          uint32_t m = mPFC[iw], o = xp;
+          const uint32_t km = mKEPT[iw];
+          while (m) {
+            const int bit = 31 - __clz(m);
+            m &= ~(1u << bit);
+            if (o >= r0 && o < r0 + BIG_MCAP) {
+              const uint32_t k = wbase + bit;
+              lpf[o - r0] = ((uint32_t)(codes[k] & 0xFFFu) << 20) | (((km >> bit) & 1u) << 19) | k;
+            }
+            ++o;
+          }
+          m = mEVC[iw];
+          o = xe;
+          while (m) {
+            const int bit = 31 - __clz(m);
+            m &= ~(1u << bit);
+            if (o >= r0 && o < r0 + BIG_MCAP) {
+              const uint32_t k = wbase + bit;
+              lev[o - r0] = ((uint32_t)(codes[k] & 0xFFFu) << 20) | k;
+            }
+            ++o;
+          }
+        }
+        __syncthreads();
+        // each list of the round: a stable sort of (bucket, position in the list) groups the
+        // candidates by bucket in list order; a candidate's rank in its bucket is its sorted
+        // index minus the bucket's first (binary search); the prefetch cursor counts down, the
+        // evict cursor up, and the bucket's first candidate moves the cursor after all are placed
+        uint32_t *ka = h + 2 * NB1, *ia = ka + BIG_MCAP, *kb = ia + BIG_MCAP, *ib = kb + BIG_MCAP;  // (free now)
+        uint32_t *cnt = reinterpret_cast<uint32_t *>(sTB);  // 256 x 16 counters (16 KB: sTB, sLO)
+        for (int lst = 0; lst < 2; ++lst) {
+          const uint32_t tot = lst == 0 ? np : ne;
+          if (r0 >= tot) continue;  // (CTA-uniform)
+          const uint32_t n = min(tot - r0, BIG_MCAP);
+          const uint32_t *src = lst == 0 ? lpf : lev;
+          for (uint32_t e = threadIdx.x; e < n; e += FT) {
+            ka[e] = src[e] >> 20;
+            ia[e] = e;
+          }
+          __syncthreads();
+          cta_sort_pairs(ka, ia, kb, ib, n, cnt);
+          uint32_t *cur = h32 + (lst == 0 ? 0u : (uint32_t)NB1);
+          uint32_t *out = lst == 0 ? d.pf_ids : d.ev_ids;
+          uint32_t my_b[2], my_n[2];
+          uint32_t nm = 0;
+          for (uint32_t i = threadIdx.x; i < n; i += FT) {
+            const uint32_t b = ka[i];
+            uint32_t lo = 0, hi = i;  // first sorted index of bucket b
+            while (lo < hi) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (ka[mid] < b) lo = mid + 1;
+              else hi = mid;
+            }
+            const uint32_t rk = i - lo, x = src[ia[i]], k = x & 0x7FFFFu;
+            if (lst == 0) {
+              if ((x >> 19) & 1u) out[cur[b] - rk] = (uint32_t)(p.shard_begin + base + k);
+            } else {
+              out[cur[b] + rk] = (uint32_t)(p.shard_begin + base + k);
+            }
+            if (rk == 0 && nm < 2) {  // this thread moves bucket b's cursor afterwards
+              uint32_t l2 = i + 1, h2 = n;
+              while (l2 < h2) {
+                const uint32_t mid = (l2 + h2) >> 1;
+                if (ka[mid] <= b) l2 = mid + 1;
+                else h2 = mid;
+              }
+              my_b[nm] = b;
+              my_n[nm] = l2 - i;
+              ++nm;
+            }
+          }
+          __syncthreads();  // (every position read its cursor)
+          for (uint32_t j = 0; j < nm; ++j) {
+            if (lst == 0) cur[my_b[j]] -= my_n[j];
+            else cur[my_b[j]] += my_n[j];
+          }
+          __syncthreads();
+        }
+        __syncthreads();
+      }
+    }
+    LAP(dtd)
+  }
+  PROBE(if (threadIdx.x == 0) {
+    atomicMax(&prof[22], dta);
+    atomicMax(&prof[23], dtb);
+    atomicMax(&prof[24], dtc);
+    atomicMax(&prof[29], dtd);
+  })
+  STAMP_MAX(39)  // P34 done
+  // the agents in multi-valued buckets (all CTAs'): one CTA sorts them -- prefetch members
+  // (non-residents below b*) ascending by (key, id) after the value buckets below 2048, evict
+  // members (residents above b*) descending after the +inf bucket (bitonic sorts of packed
+  // (key, id) in shared memory; the chunk arrays are free now)
+  if (c == G - 1 && sh_novf > 0) {
+    const uint32_t nov = (uint32_t)sh_novf;
+    unsigned long long *la = reinterpret_cast<unsigned long long *>(mE);  // [BIG_OVF_CAP]
+    unsigned long long *lb = reinterpret_cast<unsigned long long *>(lpf);  // [BIG_OVF_CAP] (32 KB)
+    __shared__ uint32_t sh_na, sh_nb;
+    if (threadIdx.x == 0) sh_na = sh_nb = 0;
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < nov; x += FT) {
+      const uint4 q = d.f_ovf[(uint64_t)par * BIG_OVF_CAP + x];
+      const uint32_t b = ibucket(q.x);
+      if (!q.z && b < bs) la[atomicAdd(&sh_na, 1u)] = ((unsigned long long)q.x << 32) | q.y;
+      else if (q.z && b > bs) lb[atomicAdd(&sh_nb, 1u)] = ~(((unsigned long long)q.x << 32) | q.y);
+    }
+    __syncthreads();
+    const uint32_t na = sh_na, nb = sh_nb;
+    for (int lst = 0; lst < 2; ++lst) {
+      unsigned long long *v = lst == 0 ? la : lb;
+      const uint32_t m = lst == 0 ? na : nb;
+      if (m == 0) continue;
+      uint32_t N = 1;
+      while (N < m) N <<= 1;
+      for (uint32_t x = m + threadIdx.x; x < N; x += FT) v[x] = ~0ull;
+      __syncthreads();
+      for (uint32_t k = 2; k <= N; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t i = threadIdx.x; i < N; i += FT) {
+            const uint32_t ij = i ^ j;
+            if (ij > i) {
+              const unsigned long long a = v[i], bb = v[ij];
+              if ((a > bb) == ((i & k) == 0)) {
+                v[i] = bb;
+                v[ij] = a;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      uint32_t *out = lst == 0 ? d.pf_ids + sh_mvpf : d.ev_ids + sh_mvev;
+      for (uint32_t x = threadIdx.x; x < m; x += FT) out[x] = (uint32_t)(lst == 0 ? v[x] : ~v[x]);
+      __syncthreads();
+    }
+  }
+  // sums into the header (zeroed before B1)
+  warp_add_u44(h2d, sacc + 4);
+  warp_add_u44(tie_kept, sacc + 8);
+  warp_add_u44(d2h, sacc + 6);
+  n_el = __reduce_add_sync(0xFFFFFFFFu, n_el);  // (every thread counted its words)
+  n_pfb = __reduce_add_sync(0xFFFFFFFFu, n_pfb);
+  n_evb = __reduce_add_sync(0xFFFFFFFFu, n_evb);
+  if (lane == 0) {
+    if (n_el) atomicAdd(&sacc[10], n_el);
+    if (n_pfb) atomicAdd(&sacc[11], n_pfb);
+    if (n_evb) atomicAdd(&sacc[12], n_evb);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long *H = d.header;
+    const unsigned long long v_h2d = parts_u44(sacc + 4), v_tie = parts_u44(sacc + 8), v_wb = parts_u44(sacc + 6);
+    if (v_h2d) atomicAdd(&H[H_H2D], v_h2d);
+    if (v_tie) atomicAdd(&H[H_KEPT], v_tie);
+    if (v_wb) atomicAdd(&H[H_D2H], v_wb);
+    if (sacc[10]) atomicAdd(&H[H_N_ELIG], (unsigned long long)sacc[10]);
+    if (sacc[11]) atomicAdd(&H[H_N_PF], (unsigned long long)sacc[11]);
+    if (sacc[12]) atomicAdd(&H[H_N_EV], (unsigned long long)sacc[12]);
+    if (c == 0) {
+      if (sh_spf) atomicAdd(&H[H_N_PF], (unsigned long long)sh_spf);
+      if (sh_sev) atomicAdd(&H[H_N_EV], (unsigned long long)sh_sev);
+      atomicAdd(&H[H_KEPT], p.budget - rem);
+      uint32_t status = (uint32_t)acc[5] | d.state->status;
+      if (acc[0] > p.budget) status |= ST_INSUFFICIENT;
+      H[H_CUT_BITS] = all_fit ? 0xFFFFFFFFull : dstar;
+      H[H_CUT_REM] = rem;
+      atomicOr(reinterpret_cast<unsigned int *>(&H[H_STATUS]), status);
+      H[H_SEQ] = H[H_SEQ] + 1;
+    }
+    PROBE(atomicMax(&prof[1], gtimer());)
+  }
+}
+
+bool fused_big_prepare(uint32_t gsize) {
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return false;
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, k_fused_big) != cudaSuccess) return false;
+  const size_t sm = fused_big_smem_bytes(gsize);
+  if (sm + a.sharedSizeBytes > (size_t)optin) return false;
+  if (cudaFuncSetAttribute(k_fused_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+    return false;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_big, FT, sm) != cudaSuccess) return false;
+  return per_sm >= 1;
+}
+
+int launch_fused_big(const FusedInst &inst, uint32_t gsize, cudaStream_t s, bool coop) {
+  FusedArgs<1> B;
+  B.n_inst = 1;
+  B.gsize = gsize;
+  B.fastok = 1;
+  B.wsize = 1;
+  B.inst[0] = inst;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(gsize);
+  cfg.blockDim = dim3(FT);
+  cfg.dynamicSmemBytes = fused_big_smem_bytes(gsize);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = coop ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, k_fused_big, B);
+  return 1;
+}
+
+}  // namespace ss

@@ -22,10 +22,12 @@ constexpr int COPY_CTAS = 8;              // a6: CTAs per page-copy launch (two 
                                           // t+1 runs beside the copies of step t
 constexpr uint32_t FUSED_MAX_TILE = 12288;  // fused path: agents per CTA held in shared memory
 constexpr uint32_t FUSED_OVF_CAP = 256;     // fused fast lists: agents in multi-valued level-1 buckets
+constexpr uint32_t BIG_OVF_CAP = 4096;      // ... in the streaming kernel of large contexts (sorted, not counted)
 constexpr uint32_t FUSED_MAX_WORLD = 8;     // ranks of one world planned in one launch (SCALESIM_F_LOOPBACK)
 
 // status bits (mirror include/scalesim.h)
-constexpr uint32_t ST_INSUFFICIENT = 1u, ST_BAD_RECORD = 2u, ST_BAD_KIN = 4u, ST_NO_PAGES = 8u, ST_SYNC = 16u;
+constexpr uint32_t ST_INSUFFICIENT = 1u, ST_BAD_RECORD = 2u, ST_BAD_KIN = 4u, ST_NO_PAGES = 8u, ST_SYNC = 16u,
+                   ST_LIMIT = 32u;
 
 // header fields (mirror SCALESIM_H_*)
 enum { H_N_PF = 0, H_N_EV, H_H2D, H_D2H, H_CUT_BITS, H_CUT_REM, H_STATUS, H_N_D2H, H_N_H2D,
@@ -74,7 +76,7 @@ struct Layout {
   uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_cpf, f_cta_cev, f_tot, f_acc;
   uint64_t f_rows1, f_rows2, f_rows3, f_cta_lmm;
   uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes, params_dev;
-  uint64_t f_pos, f_rt, f_crow, f_ovf;
+  uint64_t f_pos, f_rt, f_crow, f_ovf, big_codes;
   uint64_t total;
 };
 
@@ -130,7 +132,8 @@ struct Dev {
   uint32_t *f_crow;            // [2][G][4096] per-CTA eligible counts per level-1 bucket (non-resident | resident << 16)
   unsigned long long *f_pos;   // [2][4096][FUSED_MAX_CTAS] bucket owners' list offsets per (bucket, CTA), epoch-tagged
   unsigned long long *f_rt;    // [2][FUSED_MAX_CTAS] bucket owners' range totals, epoch-tagged
-  uint4 *f_ovf;                // [2][FUSED_OVF_CAP] eligible agents in multi-valued buckets: {key, id, resident, 0}
+  uint4 *f_ovf;                // [2][BIG_OVF_CAP] eligible agents in multi-valued buckets: {key, id, resident, 0}
+  uint16_t *big_codes;         // [n_local] large contexts (fused_big.cu): bucket | eligible << 12 | resident << 13 | dirty << 14
 };
 
 Dev make_dev(void *ws, const Layout &L);
@@ -189,6 +192,10 @@ constexpr int FUSED_MAX_BATCH = 160;
 int launch_fused_batch(const FusedInst *insts, uint32_t n, uint32_t gsize, cudaStream_t s, bool coop,
                        uint32_t wsize = 1);
 bool fused_prepare(int grid, uint32_t tile, uint32_t gsize);
+// large integer-distance contexts (fused_big.cu): tiles beyond shared memory, up to 2^19 per CTA
+constexpr uint32_t FUSED_BIG_MAX_TILE = 1u << 19;
+bool fused_big_prepare(uint32_t gsize);
+int launch_fused_big(const FusedInst &inst, uint32_t gsize, cudaStream_t s, bool coop);
 size_t fused_smem_bytes(uint32_t tile);
 
 }  // namespace ss

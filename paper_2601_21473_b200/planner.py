@@ -207,7 +207,12 @@ class Planner:
 
     @property
     def fused(self) -> bool:
-        return int(self.lib.scalesim_fused(self.ctx)) == 1
+        return int(self.lib.scalesim_fused(self.ctx)) >= 1
+
+    @property
+    def big(self) -> bool:
+        """The streaming single-kernel plan of large integer-distance contexts."""
+        return int(self.lib.scalesim_fused(self.ctx)) == 2
 
     def launch_count(self) -> int:
         return int(self.lib.scalesim_launch_count(self.ctx))
