@@ -28,7 +28,11 @@
 namespace ss {
 
 constexpr uint32_t BIG_CW = 1024;    // words per P34 chunk (one per thread)
-constexpr uint32_t BIG_MCAP = 2048;  // list candidates per placement round (per list)
+constexpr uint32_t BIG_MCAP = 2048;  // (shared-memory layout: candidate staging, reused by the overflow sort)
+#ifndef BIG_LB_V
+#define BIG_LB_V 4
+#endif
+constexpr int BIG_LB = BIG_LB_V;     // records in flight per thread in P1 (two batches)
 
 static uint32_t big_rb(uint32_t gsize) { return ((NB1 + gsize - 1) / gsize + 3u) & ~3u; }
 
@@ -113,13 +117,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     uint32_t st = 0;
     uint32_t *gkeys = p.keep_dist ? d.keys + base : nullptr;
     const uint32_t last = n_here ? n_here - 1 : 0u;
-    const uint32_t BS = LOAD_BATCH * FT, nk = tw_here * 32;
-    uint4 r[LOAD_BATCH], r2[LOAD_BATCH];
-    uint32_t bw[LOAD_BATCH], bw2[LOAD_BATCH];  // the residency words, loaded with the records
+    constexpr int LB = BIG_LB;
+    const uint32_t BS = LB * FT, nk = tw_here * 32;
+    uint4 r[LB], r2[LB];
+    uint32_t bw[LB], bw2[LB];  // the residency words, loaded with the records
     const uint32_t tw_all = (uint32_t)((p.n_local + 31) / 32);
-    auto load_into = [&](uint4 (&rr)[LOAD_BATCH], uint32_t (&ww)[LOAD_BATCH], uint32_t k0) {
+    auto load_into = [&](uint4 (&rr)[LB], uint32_t (&ww)[LB], uint32_t k0) {
 #pragma unroll
-      for (int j = 0; j < LOAD_BATCH; ++j) {
+      for (int j = 0; j < LB; ++j) {
         rr[j] = n_here ? ld_stream(rec + min(k0 + j * FT + threadIdx.x, last)) : make_uint4(0, 0, 0, 0);
         const uint64_t wi = (base + k0 + j * FT + threadIdx.x) >> 5;
         ww[j] = wi < tw_all ? bm_old[wi] : 0u;
@@ -130,7 +135,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     for (uint32_t k0 = 0; k0 < nk; k0 += BS) {
       if (k0 + BS < nk) load_into(r2, bw2, k0 + BS);
 #pragma unroll
-      for (int j = 0; j < LOAD_BATCH; ++j) {
+      for (int j = 0; j < LB; ++j) {
         const uint32_t k = k0 + j * FT + threadIdx.x;  // (k & 31 == lane)
         if (k0 + j * FT >= nk) break;                  // (CTA-uniform)
         const uint4 rj = r[j];
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         }
       }
 #pragma unroll
-      for (int j = 0; j < LOAD_BATCH; ++j) {
+      for (int j = 0; j < LB; ++j) {
         r[j] = r2[j];
         bw[j] = bw2[j];
       }
@@ -400,7 +405,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   const unsigned long long rem = sel.rem;
   const uint32_t n_chunks = (tw_here + BIG_CW - 1) / BIG_CW;
   __shared__ unsigned long long sh_ctot;
-  __shared__ uint32_t sh_cp, sh_ce;
+  // this CTA's list candidates (HBM scratch of the tile's range): bucket << 20 | kept << 19 | k
+  uint32_t *g_lpf = d.sort_ka + base, *g_lev = d.sort_va + base;
+  uint32_t n_lpf = 0, n_lev = 0;  // (CTA-uniform)
   for (int ch = (int)n_chunks - 1; ch >= 0; --ch) {
     const uint32_t w0 = (uint32_t)ch * BIG_CW, wn = min(BIG_CW, tw_here - w0);
     // (a) decode the chunk's codes: masks and tie bytes, one word (32 agents, 64 bytes of
@@ -487,104 +494,36 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     }
     __syncthreads();
     LAP(dtc)
-    // (d) the chunk's candidates in descending id order, placed by two warps in rounds
+    // (d) the chunk's candidates, appended in descending id order to this CTA's two candidate
+    // lists (HBM scratch, placed once after the last chunk)
     {
-      // reversed word order: word wn-1-t at thread t
       const uint32_t t = threadIdx.x;
-      const uint32_t iw = t < wn ? wn - 1 - t : 0u;
+      const uint32_t iw = t < wn ? wn - 1 - t : 0u;  // reversed word order: word wn-1-t at thread t
       const uint32_t cp = t < wn ? __popc(mPFC[iw]) : 0u, ce = t < wn ? __popc(mEVC[iw]) : 0u;
       unsigned long long v[1] = {(unsigned long long)cp | ((unsigned long long)ce << 32)}, tt[1];
       cta_scan1(v, tt);
-      const uint32_t xp = (uint32_t)v[0], xe = (uint32_t)(v[0] >> 32);
-      if (t == 0) {
-        sh_cp = (uint32_t)tt[0];
-        sh_ce = (uint32_t)(tt[0] >> 32);
-      }
-      __syncthreads();
-      const uint32_t np = sh_cp, ne = sh_ce;
-      for (uint32_t r0 = 0; r0 < max(np, ne); r0 += BIG_MCAP) {
-        if (t < wn) {  // this word's candidates in the round's window, highest lane first
-          const uint32_t wbase = (w0 + iw) * 32;
-          uint32_t m = mPFC[iw], o = xp;
-          const uint32_t km = mKEPT[iw];
-          while (m) {
-            const int bit = 31 - __clz(m);
-            m &= ~(1u << bit);
-            if (o >= r0 && o < r0 + BIG_MCAP) {
-              const uint32_t k = wbase + bit;
-              lpf[o - r0] = ((uint32_t)(codes[k] & 0xFFFu) << 20) | (((km >> bit) & 1u) << 19) | k;
-            }
-            ++o;
-          }
-          m = mEVC[iw];
-          o = xe;
-          while (m) {
-            const int bit = 31 - __clz(m);
-            m &= ~(1u << bit);
-            if (o >= r0 && o < r0 + BIG_MCAP) {
-              const uint32_t k = wbase + bit;
-              lev[o - r0] = ((uint32_t)(codes[k] & 0xFFFu) << 20) | k;
-            }
-            ++o;
-          }
+      if (t < wn) {
+        const uint32_t wbase = (w0 + iw) * 32;
+        uint32_t m = mPFC[iw], o = n_lpf + (uint32_t)v[0];
+        const uint32_t km = mKEPT[iw];
+        while (m) {
+          const int bit = 31 - __clz(m);
+          m &= ~(1u << bit);
+          const uint32_t k = wbase + bit;
+          g_lpf[o++] = ((uint32_t)(codes[k] & 0xFFFu) << 20) | (((km >> bit) & 1u) << 19) | k;
         }
-        __syncthreads();
-        // each list of the round: a stable sort of (bucket, position in the list) groups the
-        // candidates by bucket in list order; a candidate's rank in its bucket is its sorted
-        // index minus the bucket's first (binary search); the prefetch cursor counts down, the
-        // evict cursor up, and the bucket's first candidate moves the cursor after all are placed
-        uint32_t *ka = h + 2 * NB1, *ia = ka + BIG_MCAP, *kb = ia + BIG_MCAP, *ib = kb + BIG_MCAP;  // (free now)
-        uint32_t *cnt = reinterpret_cast<uint32_t *>(sTB);  // 256 x 16 counters (16 KB: sTB, sLO)
-        for (int lst = 0; lst < 2; ++lst) {
-          const uint32_t tot = lst == 0 ? np : ne;
-          if (r0 >= tot) continue;  // (CTA-uniform)
-          const uint32_t n = min(tot - r0, BIG_MCAP);
-          const uint32_t *src = lst == 0 ? lpf : lev;
-          for (uint32_t e = threadIdx.x; e < n; e += FT) {
-            ka[e] = src[e] >> 20;
-            ia[e] = e;
-          }
-          __syncthreads();
-          cta_sort_pairs(ka, ia, kb, ib, n, cnt);
-          uint32_t *cur = h32 + (lst == 0 ? 0u : (uint32_t)NB1);
-          uint32_t *out = lst == 0 ? d.pf_ids : d.ev_ids;
-          uint32_t my_b[2], my_n[2];
-          uint32_t nm = 0;
-          for (uint32_t i = threadIdx.x; i < n; i += FT) {
-            const uint32_t b = ka[i];
-            uint32_t lo = 0, hi = i;  // first sorted index of bucket b
-            while (lo < hi) {
-              const uint32_t mid = (lo + hi) >> 1;
-              if (ka[mid] < b) lo = mid + 1;
-              else hi = mid;
-            }
-            const uint32_t rk = i - lo, x = src[ia[i]], k = x & 0x7FFFFu;
-            if (lst == 0) {
-              if ((x >> 19) & 1u) out[cur[b] - rk] = (uint32_t)(p.shard_begin + base + k);
-            } else {
-              out[cur[b] + rk] = (uint32_t)(p.shard_begin + base + k);
-            }
-            if (rk == 0 && nm < 2) {  // this thread moves bucket b's cursor afterwards
-              uint32_t l2 = i + 1, h2 = n;
-              while (l2 < h2) {
-                const uint32_t mid = (l2 + h2) >> 1;
-                if (ka[mid] <= b) l2 = mid + 1;
-                else h2 = mid;
-              }
-              my_b[nm] = b;
-              my_n[nm] = l2 - i;
-              ++nm;
-            }
-          }
-          __syncthreads();  // (every position read its cursor)
-          for (uint32_t j = 0; j < nm; ++j) {
-            if (lst == 0) cur[my_b[j]] -= my_n[j];
-            else cur[my_b[j]] += my_n[j];
-          }
-          __syncthreads();
+        m = mEVC[iw];
+        o = n_lev + (uint32_t)(v[0] >> 32);
+        while (m) {
+          const int bit = 31 - __clz(m);
+          m &= ~(1u << bit);
+          const uint32_t k = wbase + bit;
+          g_lev[o++] = ((uint32_t)(codes[k] & 0xFFFu) << 20) | k;
         }
-        __syncthreads();
       }
+      n_lpf += (uint32_t)tt[0];
+      n_lev += (uint32_t)(tt[0] >> 32);
+      __syncthreads();  // (the next chunk rewrites the masks; the placement reads the lists)
     }
     LAP(dtd)
   }
@@ -594,6 +533,41 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     atomicMax(&prof[24], dtc);
     atomicMax(&prof[29], dtd);
   })
+  // (e) placement: per list, a stable sort of the candidates by bucket (list order kept within a
+  // bucket); a candidate's rank in its bucket = sorted index - the bucket's first index; evict
+  // positions count up from the bucket's cursor, prefetch positions down from its last one
+  // (only kept candidates are members)
+  {
+    uint32_t *start = h + 2 * NB1;  // [NB1] first sorted index per bucket (the counts are no longer needed)
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(sTB);  // 256 x 16 sort counters (sTB, sLO)
+    uint32_t *ka = d.sort_kb + base, *ia = d.sort_vb + base, *kb = d.f_sk2 + base, *ib = d.f_sv2 + base;
+    for (int lst = 0; lst < 2; ++lst) {
+      const uint32_t n = lst == 0 ? n_lpf : n_lev;
+      if (n == 0) continue;  // (CTA-uniform)
+      const uint32_t *src = lst == 0 ? g_lpf : g_lev;
+      for (uint32_t e = threadIdx.x; e < n; e += FT) {
+        ka[e] = src[e] >> 20;
+        ia[e] = e;
+      }
+      __syncthreads();
+      cta_sort_pairs(ka, ia, kb, ib, n, cnt);
+      for (uint32_t i = threadIdx.x; i < n; i += FT)
+        if (i == 0 || ka[i - 1] != ka[i]) start[ka[i]] = i;
+      __syncthreads();
+      const uint32_t *cur = h32 + (lst == 0 ? 0u : (uint32_t)NB1);
+      uint32_t *out = lst == 0 ? d.pf_ids : d.ev_ids;
+      for (uint32_t i = threadIdx.x; i < n; i += FT) {
+        const uint32_t b = ka[i], rk = i - start[b], x = src[ia[i]], k = x & 0x7FFFFu;
+        const uint32_t pos = lst == 0 ? cur[b] - rk : cur[b] + rk;
+        if (pos >= p.n_local) {  // (cannot happen: flagged instead of writing out of bounds)
+          atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), ST_SYNC);
+          continue;
+        }
+        if (lst == 1 || ((x >> 19) & 1u)) out[pos] = (uint32_t)(p.shard_begin + base + k);
+      }
+      __syncthreads();
+    }
+  }
   STAMP_MAX(39)  // P34 done
   // the agents in multi-valued buckets (all CTAs'): one CTA sorts them -- prefetch members
   // (non-residents below b*) ascending by (key, id) after the value buckets below 2048, evict
