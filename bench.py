@@ -834,7 +834,13 @@ def main():
             sm = t.clone()
             dist.all_reduce(sm)
             r5["ms"], r5["agents_per_step"] = float(mx[0].item()), int(sm[1].item())
+        c5_gbs = r5["agents_per_step"] * BYTES_PER_AGENT_STEP / (r5["ms"] / r5["steps"] / 1e3) / 1e9
         c5 = {"value": r5["agents_per_step"] * r5["steps"] / (r5["ms"] / 1e3), "unit": "agent-plans/s",
+              "roofline": {"bound": "hbm", "achieved": c5_gbs, "peak": peaks()["hbm_gbs"], "unit": "GB/s",
+                           "frac": c5_gbs / peaks()["hbm_gbs"], "frac_8TBs": c5_gbs / 8000.0,
+                           "algorithmic_bytes_per_step": r5["agents_per_step"] * BYTES_PER_AGENT_STEP,
+                           "timing": "the step's launches (ceil(instances / 148) batched plan kernels) on one stream, "
+                                     "CUDA events around the timed steps"},
               "workload": f"c5: {args.c5_replicas} replicas x 9 budgets (10..90%) of the C2 shape (10k agents), "
                           f"instances sharded over {world} GPU(s), scalesim_step_batch",
               "instances_per_gpu": r5["instances"], "steps": r5["steps"], "ms_per_step": r5["ms"] / r5["steps"],

@@ -18,4 +18,8 @@ for mk in (False, True):
     w = tg.config_c2(seed=2, steps=4, n=1200, lora=4 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
     run_parity(w, multi_kernel=mk)
     run_parity(w, transfer=False, multi_kernel=mk, keep_dist=False)
+# the streaming kernel of large contexts (a small tile forced: 150k agents on 4 CTAs would not
+# exercise it; a 2.1M-agent C4 shard does) and a loopback world
+w = tg.config_c4(seed=3, steps=2, n=2_100_000)
+run_parity(w, transfer=False, keep_dist=False)
 print("SANITIZE_RUN_OK")
