@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       // evict offset  W_r(b) + sum_{q' > q} r_q'(b), relative to the range start (W: the range's
       // buckets before b ascending / after b descending), published tagged with the launch
       // epoch; and the range totals.  Consumers add the range starts.
-      uint32_t *tn = s.col + G * RB, *tr = tn + RB, *wn = tr + RB, *wr = wn + RB;
+      uint32_t *tn = s.col + G * RB, *tr = tn + RB;
       for (uint32_t j = warp; j < o_n; j += FWARPS) {  // totals over the CTAs
         uint32_t a = 0, e = 0;
         for (uint32_t i = 0; i < QP; ++i) {
@@ -438,34 +438,26 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       }
       __syncthreads();
       STAMP_MAX(46)  // owner pass 1
-      if (warp == 0) {  // offsets of the buckets within the range, and the range totals
-        const uint32_t JP = (o_n + 31) / 32;
-        uint32_t sa = 0, se = 0;
-        for (uint32_t i = 0; i < JP; ++i) {
-          const uint32_t j = lane * JP + i;
-          if (j < o_n) {
-            sa += tn[j];
-            se += tr[j];
-          }
+      // the range's totals (owner o's share of both lists), published; each warp of the pass below
+      // sums the offsets of its bucket within the range itself (no serial scan)
+      if (warp == 0) {
+        uint32_t ta = 0, te = 0;
+        for (uint32_t l = lane; l < o_n; l += 32) {
+          ta += tn[l];
+          te += tr[l];
         }
-        const uint32_t ia = warp_incl_scan(sa), ie = warp_incl_scan(se);
-        const uint32_t TA = __shfl_sync(0xFFFFFFFFu, ia, 31), TE = __shfl_sync(0xFFFFFFFFu, ie, 31);
-        uint32_t ra = ia - sa, re = ie - se;
-        for (uint32_t i = 0; i < JP; ++i) {
-          const uint32_t j = lane * JP + i;
-          if (j < o_n) {
-            wn[j] = ra;
-            ra += tn[j];
-            re += tr[j];
-            wr[j] = TE - re;
-          }
-        }
-        if (lane == 0) st_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + c], pack_ep(ep, TA, TE));
+        ta = __reduce_add_sync(0xFFFFFFFFu, ta);
+        te = __reduce_add_sync(0xFFFFFFFFu, te);
+        if (lane == 0) st_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + c], pack_ep(ep, ta, te));
       }
-      __syncthreads();
-      STAMP_MAX(47)  // owner range scan
       for (uint32_t j = warp; j < o_n; j += FWARPS) {  // per-CTA offsets: 32 consecutive CTAs per store
-        const uint32_t w_n = wn[j], w_r = wr[j], t_r = tr[j];
+        uint32_t w_n = 0, w_r = 0;  // the range's buckets before j (prefetch) / after j (evict)
+        for (uint32_t l0 = 0; l0 < o_n; l0 += 32) {
+          const uint32_t l = l0 + lane;
+          w_n += __reduce_add_sync(0xFFFFFFFFu, (l < o_n && l < j) ? tn[l] : 0u);
+          w_r += __reduce_add_sync(0xFFFFFFFFu, (l < o_n && l > j) ? tr[l] : 0u);
+        }
+        const uint32_t t_r = tr[j];
         unsigned long long *P = d.f_pos + ((uint64_t)par * NB1 + o_lo + j) * FUSED_MAX_CTAS;
         uint32_t ca = 0, ce = 0;  // running sums over the previous 32-CTA chunks
         for (uint32_t q0 = 0; q0 < G; q0 += 32) {
@@ -500,116 +492,86 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     m_need = sh_m;
   }
   STAMP_MAX(42)  // need list
+  // the owners' range totals and this CTA's first list-bucket offsets: loads issued now (their
+  // latency hides behind P3 / P4), the epoch tag checked where they are used
+  unsigned long long rv_pre = 0, pv_pre = 0;
+  if (fastp && G > 1) {
+    if (threadIdx.x < m_need)
+      pv_pre = ld_relaxed_u64(d.f_pos + ((uint64_t)par * NB1 + need[threadIdx.x]) * FUSED_MAX_CTAS + c);
+    if (threadIdx.x < G) rv_pre = ld_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + threadIdx.x]);
+  }
 
-  // ---------------- P3: tie group: id-order prefix of the bytes at d == D*
-  unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw]
-#pragma unroll 1
-  for (uint32_t w = warp; w < A.tw; w += FWARPS) {
-    const uint32_t k = w * 32 + lane;
-    const bool tie = !all_fit && ((s.elig_w[w] >> lane) & 1u) && s.keys[k] == dstar;
-    unsigned long long v = 0;
-    if (__ballot_sync(0xFFFFFFFFu, tie)) v = warp_sum_u32_exact(tie ? s.fp[k] : 0u);  // most words: no tie
-    if (lane == 0) word_tie[w] = v;
-  }
-  __syncthreads();
-  // exclusive scan over the tile's words (tw <= FUSED_MAX_TILE / 32 <= FT: one word per
-  // thread) and, in the same pass, the preceding CTAs' total
-  if (warp * 32 < c || (warp == FWARPS - 1 && rank > 0)) warp_add_u64(t_rows, sacc + 20);  // preceding CTAs' and ranks' total
-  {
-    const uint32_t w = threadIdx.x;
-    unsigned long long v[1] = {w < A.tw ? word_tie[w] : 0ull}, tt[1];
-    cta_scan1(v, tt);  // (its barriers complete the sum)
-    if (w < A.tw) word_tie[w] = v[0];
-    if (threadIdx.x == 0) word_tie[A.tw] = tt[0];  // (memb holds tile / 2 >= tw + 1 words of 64 bits)
-  }
-  const unsigned long long sh_tie_excl = parts_u64(sacc + 20);
-  __syncthreads();
-  STAMP0(10)
-  STAMP_MAX(14)
-
-  // ---------------- P4: emit
-  uint32_t *cnt_pf = s.h, *cnt_ev = s.h + NBL;  // per-CTA list members per list bucket
-  uint32_t *lor_l = s.h + 6 * NBL;   // [2][NBL]: OR of the key bits below the list bucket
-  uint32_t *mm_l = s.h + 10 * NBL;  // [4][NBL]: prefetch min, prefetch ~max, evict min, evict ~max
-  if (!fastp) {
-    for (int b = threadIdx.x; b < 2 * NBL; b += FT) {
-      s.h[b] = 0;
-      lor_l[b] = 0;
-    }
-    for (int b = threadIdx.x; b < 4 * NBL; b += FT) mm_l[b] = 0xFFFFFFFFu;
-  }
-  __syncthreads();
-  unsigned long long h2d = 0, tie_kept = 0;
-  uint32_t n_el = 0;
-#pragma unroll 1
-  for (uint32_t w = warp; w < A.tw; w += FWARPS) {
-    const uint32_t k = w * 32 + lane;
-    const uint32_t elw = s.elig_w[w];  // 0 beyond n_here
-    const uint32_t key = s.keys[k];
-    uint32_t kw = elw;  // kept agents of the word
-    if (!all_fit) {
-      kw = __ballot_sync(0xFFFFFFFFu, key < dstar) & elw;
-      const uint32_t tiew = __ballot_sync(0xFFFFFFFFu, key == dstar) & elw;
-      if (tiew) {  // id-order inclusive prefix of the tie bytes
-        const bool tie = (tiew >> lane) & 1u;
-        const uint32_t fp = s.fp[k];
-        // the word's tie bytes lie in (lo, hi]: every tie of the word fits when hi <= rem, none
-        // when lo > rem (one word of the grid straddles rem: only it needs the in-word prefix)
-        const unsigned long long lo = sh_tie_excl + word_tie[w], hi = sh_tie_excl + word_tie[w + 1];
-        if (hi <= sel.rem) {
-          if (tie) tie_kept += fp;
-          kw |= tiew;
-        } else if (lo <= sel.rem) {
-          unsigned long long incl = tie ? fp : 0u;
-          for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += t;
-          }
-          incl += lo;
-          const bool ok = tie && incl <= sel.rem;
-          if (ok) tie_kept += fp;
-          kw |= __ballot_sync(0xFFFFFFFFu, ok);
-        }
-      }
-    }
-    const uint32_t old = s.old_w[w];
-    const uint32_t pfw = kw & ~old, evw = old & ~kw;
-    if (lane == 0) {
-      if (w < tw_here) bm_new[base / 32 + w] = kw;
-      s.pf_w[w] = pfw;
-      s.ev_w[w] = evw;
-      n_el += __popc(elw);
-    }
-    if (fastp) {
-      if ((pfw >> lane) & 1u) h2d += s.fp[k];
-    } else if (pfw | evw) {  // list members in this word (slow path: list-bucket counts)
-      const uint32_t bk = key >> 21;
-      if ((pfw >> lane) & 1u) {
-        h2d += s.fp[k];
-        atomicAdd(&cnt_pf[bk], 1u);
-        atomicMin(&mm_l[bk], key);
-        atomicMin(&mm_l[NBL + bk], ~key);
-        atomicOr(&lor_l[bk], key & 0x1FFFFFu);
-      }
-      if ((evw >> lane) & 1u) {
-        atomicAdd(&cnt_ev[bk], 1u);
-        atomicMin(&mm_l[2 * NBL + bk], key);
-        atomicMin(&mm_l[3 * NBL + bk], ~key);
-        atomicOr(&lor_l[NBL + bk], key & 0x1FFFFFu);
-      }
-    }
-  }
-  __syncthreads();
-  STAMP_MAX(27)  // P4 word loop done
+  // ---------------- fast list placement tail (integer distances, fastp: grid-uniform)
   if (fastp) {
     uint32_t *const h32 = s.h;  // [0, NB1): prefetch positions, [NB1, 2 NB1): evict positions
-    __shared__ uint32_t sh_spf, sh_sev, sh_fpf, sh_fev;
-    // write-back bytes (R13) of this tile's dirty evicted agents: up to two loads per word
-    // issued now into registers, consumed at the end
-    uint32_t wbm = 0, wb0 = 0, wb1 = 0;
+    __shared__ uint32_t sh_spf, sh_sev, sh_mvpf, sh_mvev;
+    unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw + 1]
+    unsigned long long sh_tie_excl = 0;
+    if (!all_fit) {  // (CTA-uniform)
+      // P3: per word (a warp) the kept agents below D* and the tie group at D* (staged in the
+      // prefetch / evict word arrays), the tie bytes; their id-order scan over the tile
+#pragma unroll 1
+      for (uint32_t w = warp; w < A.tw; w += FWARPS) {
+        const uint32_t k = w * 32 + lane;
+        const uint32_t elw = s.elig_w[w], key = s.keys[k];
+        const uint32_t klt = __ballot_sync(0xFFFFFFFFu, key < dstar) & elw;
+        const uint32_t tiew = __ballot_sync(0xFFFFFFFFu, key == dstar) & elw;
+        unsigned long long v = 0;
+        if (tiew) v = warp_sum_u32_exact(((tiew >> lane) & 1u) ? s.fp[k] : 0u);
+        if (lane == 0) {
+          word_tie[w] = v;
+          s.pf_w[w] = klt;
+          s.ev_w[w] = tiew;
+        }
+      }
+      __syncthreads();
+      if (warp * 32 < c || (warp == FWARPS - 1 && rank > 0)) warp_add_u64(t_rows, sacc + 20);  // preceding CTAs' and ranks' total
+      {
+        const uint32_t w = threadIdx.x;
+        unsigned long long v[1] = {w < A.tw ? word_tie[w] : 0ull}, tt[1];
+        cta_scan1(v, tt);  // (its barriers complete the sum)
+        if (w < A.tw) word_tie[w] = v[0];
+        if (threadIdx.x == 0) word_tie[A.tw] = tt[0];  // (memb holds tile / 2 >= tw + 1 words of 64 bits)
+      }
+      sh_tie_excl = parts_u64(sacc + 20);
+      __syncthreads();
+    }
+    STAMP_MAX(14)
+    // P4, one word per thread: kept word (the tie group's id-order prefix within the budget),
+    // prefetch / evict words, new residency, byte sums; the write-back byte loads of the evicted
+    // dirty agents go out now and are consumed at the end
+    unsigned long long h2d = 0, tie_kept = 0;
+    uint32_t pfw = 0, evw = 0, wbm = 0, wb0 = 0, wb1 = 0, n_el = 0;
     if (threadIdx.x < A.tw) {
-      wbm = s.ev_w[threadIdx.x] & s.dirty_w[threadIdx.x];
-      const uint32_t *wbw = d.wb_bytes + base + 32 * threadIdx.x;
+      const uint32_t w = threadIdx.x;
+      const uint32_t elw = s.elig_w[w];
+      uint32_t kw = all_fit ? elw : s.pf_w[w];
+      const uint32_t tiew = all_fit ? 0u : s.ev_w[w];
+      if (tiew) {
+        const unsigned long long lo = sh_tie_excl + word_tie[w], hi = sh_tie_excl + word_tie[w + 1];
+        if (hi <= sel.rem) {
+          kw |= tiew;
+          tie_kept = hi - lo;
+        } else if (lo <= sel.rem) {  // the one word of the grid that straddles the budget
+          unsigned long long incl = lo;
+          for (uint32_t m = tiew; m; m &= m - 1) {
+            const uint32_t l = __ffs(m) - 1, fp = s.fp[w * 32 + l];
+            incl += fp;
+            if (incl <= sel.rem) {
+              kw |= 1u << l;
+              tie_kept += fp;
+            }
+          }
+        }
+      }
+      const uint32_t old = s.old_w[w];
+      pfw = kw & ~old;
+      evw = old & ~kw;
+      if (w < tw_here) bm_new[base / 32 + w] = kw;
+      n_el = __popc(elw);
+      for (uint32_t m = pfw; m; m &= m - 1) h2d += s.fp[w * 32 + __ffs(m) - 1];
+      wbm = evw & s.dirty_w[w];
+      const uint32_t *wbw = d.wb_bytes + base + 32 * w;
       if (wbm) {
         wb0 = wbw[__ffs(wbm) - 1];
         wbm &= wbm - 1;
@@ -619,31 +581,62 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         wbm &= wbm - 1;
       }
     }
+    STAMP_MAX(27)  // P4 done
     warp_add_u44(h2d, sacc + 4);
     warp_add_u44(tie_kept, sacc + 8);
+    n_el = __reduce_add_sync(0xFFFFFFFFu, n_el);
     if (lane == 0 && n_el) atomicAdd(&sacc[10], n_el);
-    __shared__ uint32_t sh_mvpf, sh_mvev;  // list starts of the multi-valued buckets' members
+    // one scan for two things: [0] this tile's list members per word (prefetch | evict << 32),
+    // [1] the range starts from the owners' range totals (G > 1) or, one CTA, its own counts
+    unsigned long long sv[2], s2[2];
+    sv[0] = (unsigned long long)__popc(pfw) | ((unsigned long long)__popc(evw) << 32);
+    uint32_t re = 0, tv[4];
     if (G > 1) {
-      // range starts from the owners' range totals: prefetch ascending, evict descending
-      uint32_t *rps = s.col, *rpe = s.col + G;  // (the owner staging is free)
-      // this thread's first list bucket: its offsets load goes out with the range totals'
-      const unsigned long long *Pc = d.f_pos + (uint64_t)par * NB1 * FUSED_MAX_CTAS + c;
-      const unsigned long long pv0 = threadIdx.x < m_need ? ld_relaxed_u64(Pc + (uint64_t)need[threadIdx.x] * FUSED_MAX_CTAS) : 0ull;
-      unsigned long long rv = 0;
-      if (threadIdx.x < G) rv = poll_ep(&d.f_rt[par * FUSED_MAX_CTAS + threadIdx.x], ep, d.header);
-      const uint32_t ra = (uint32_t)(rv >> 24) & 0xFFFFFFu, re = (uint32_t)rv & 0xFFFFFFu;
-      unsigned long long pk[1] = {(unsigned long long)ra | ((unsigned long long)re << 32)}, tt[1];
-      cta_scan1(pk, tt);
-      const uint32_t r_tot = (uint32_t)(tt[0] >> 32);
+      unsigned long long rv = rv_pre;
+      if (threadIdx.x < G && (uint32_t)(rv >> 48) != ep) rv = poll_ep(&d.f_rt[par * FUSED_MAX_CTAS + threadIdx.x], ep, d.header);
+      re = (uint32_t)rv & 0xFFFFFFu;
+      sv[1] = ((rv >> 24) & 0xFFFFFFull) | ((unsigned long long)re << 32);
+    } else {
+      unsigned long long loc = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        tv[k] = lcnt[4 * threadIdx.x + k];
+        loc += (unsigned long long)(tv[k] & 0xFFFFu) | ((unsigned long long)(tv[k] >> 16) << 32);
+      }
+      sv[1] = loc;
+    }
+    cta_scan2(sv, s2);
+    const uint32_t tp = (uint32_t)s2[0], te = (uint32_t)(s2[0] >> 32);  // this tile's members per list
+    {  // this tile's members in list order (prefetch ascending id, evict descending id)
+      const uint32_t w = threadIdx.x;
+      const uint32_t vp = (uint32_t)sv[0], ve = (uint32_t)(sv[0] >> 32);
+      uint32_t m = pfw, o = vp;
+      while (m) {  // (bucket << 16 | local index: tile < 2^16)
+        const uint32_t k = w * 32 + __ffs(m) - 1;
+        s.memb[o++] = (ibucket(s.keys[k]) << 16) | k;
+        m &= m - 1;
+      }
+      m = evw;
+      o = tp + te - 1 - ve;
+      while (m) {
+        const uint32_t k = w * 32 + __ffs(m) - 1;
+        s.memb[o--] = (ibucket(s.keys[k]) << 16) | k;
+        m &= m - 1;
+      }
+    }
+    if (G > 1) {
+      uint32_t *rps = s.col, *rpe = s.col + G;  // range starts (the owner staging is free)
+      const uint32_t r_tot = (uint32_t)(s2[1] >> 32);
       if (threadIdx.x < G) {
-        rps[threadIdx.x] = (uint32_t)pk[0];
-        rpe[threadIdx.x] = r_tot - (uint32_t)(pk[0] >> 32) - re;
+        rps[threadIdx.x] = (uint32_t)sv[1];
+        rpe[threadIdx.x] = r_tot - (uint32_t)(sv[1] >> 32) - re;
       }
       __syncthreads();
       // positions of this CTA's first member in each of its list buckets
+      const unsigned long long *Pc = d.f_pos + (uint64_t)par * NB1 * FUSED_MAX_CTAS + c;
       for (uint32_t j = threadIdx.x; j < m_need; j += FT) {
         const uint32_t b = need[j];
-        unsigned long long v = j == threadIdx.x ? pv0 : ld_relaxed_u64(Pc + (uint64_t)b * FUSED_MAX_CTAS);
+        unsigned long long v = j == threadIdx.x ? pv_pre : ld_relaxed_u64(Pc + (uint64_t)b * FUSED_MAX_CTAS);
         if ((uint32_t)(v >> 48) != ep) v = poll_ep(Pc + (uint64_t)b * FUSED_MAX_CTAS, ep, d.header);
         h32[b] = rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
         h32[NB1 + b] = rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
@@ -657,7 +650,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         return rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
       };
       if (c == 0 && threadIdx.x == 0) {
-        sh_spf = bs < (uint32_t)NB1 ? pos_pf(bs) : (uint32_t)tt[0];
+        sh_spf = bs < (uint32_t)NB1 ? pos_pf(bs) : (uint32_t)s2[1];
         sh_sev = bs < (uint32_t)NB1 ? pos_ev(bs) : 0u;
       }
       if (c == G - 1 && threadIdx.x == 32) {
@@ -666,17 +659,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       }
     } else {
       // one CTA: its counts are the totals (S_pf(b) = sum_{b' < b} NR, S_ev(b) = sum_{b' > b} R)
-      uint32_t tv[4];
-      unsigned long long loc = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        tv[k] = lcnt[4 * threadIdx.x + k];
-        loc += (unsigned long long)(tv[k] & 0xFFFFu) | ((unsigned long long)(tv[k] >> 16) << 32);
-      }
-      unsigned long long ex[1] = {loc}, tt[1];
-      cta_scan1(ex, tt);
-      const uint32_t r_tot = (uint32_t)(tt[0] >> 32);
-      unsigned long long run = ex[0];
+      const uint32_t r_tot = (uint32_t)(s2[1] >> 32);
+      unsigned long long run = sv[1];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t b = 4 * threadIdx.x + k;
@@ -692,42 +676,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         if (b == IB_INF - 1) sh_mvev = sev;
       }
       if (bs == (uint32_t)NB1 && threadIdx.x == 0) {
-        sh_spf = (uint32_t)tt[0];
+        sh_spf = (uint32_t)s2[1];
         sh_sev = 0;
       }
     }
     __syncthreads();
-    STAMP_MAX(17)  // positions ready
-    // this tile's members in list order (prefetch ascending id, evict descending id)
-    {
-      const uint32_t w = threadIdx.x;
-      const uint32_t pw = w < A.tw ? s.pf_w[w] : 0u, ew = w < A.tw ? s.ev_w[w] : 0u;
-      unsigned long long pv[1] = {(unsigned long long)__popc(pw) | ((unsigned long long)__popc(ew) << 32)}, pt[1];
-      cta_scan1(pv, pt);
-      const uint32_t vp = (uint32_t)pv[0], ve = (uint32_t)(pv[0] >> 32);
-      const uint32_t tp = (uint32_t)pt[0], te = (uint32_t)(pt[0] >> 32);
-      if (threadIdx.x == 0) {
-        sh_fpf = tp;
-        sh_fev = te;
-      }
-      // (bucket << 16 | local index: tile < 2^16)
-      uint32_t m = pw, o = vp;
-      while (m) {
-        const uint32_t k = w * 32 + __ffs(m) - 1;
-        s.memb[o++] = (ibucket(s.keys[k]) << 16) | k;
-        m &= m - 1;
-      }
-      m = ew;
-      o = tp + te - 1 - ve;
-      while (m) {
-        const uint32_t k = w * 32 + __ffs(m) - 1;
-        s.memb[o--] = (ibucket(s.keys[k]) << 16) | k;
-        m &= m - 1;
-      }
-    }
-    __syncthreads();
-    STAMP_MAX(38)  // member lists
-    const uint32_t m_pf = sh_fpf, m_ev = sh_fev;
+    STAMP_MAX(38)  // positions and member lists
+    const uint32_t m_pf = tp, m_ev = te;
     // positions: warp 0 the prefetch members, warp 1 the evict members, 32 at a time in list
     // order; the bucket positions serve as cursors
     if (warp < 2) {
@@ -815,6 +770,102 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       STAMP_MAX(1)
     return;
   }
+  // ---------------- P3 (general path): tie group: id-order prefix of the bytes at d == D*
+  unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw]
+#pragma unroll 1
+  for (uint32_t w = warp; w < A.tw; w += FWARPS) {
+    const uint32_t k = w * 32 + lane;
+    const bool tie = !all_fit && ((s.elig_w[w] >> lane) & 1u) && s.keys[k] == dstar;
+    unsigned long long v = 0;
+    if (__ballot_sync(0xFFFFFFFFu, tie)) v = warp_sum_u32_exact(tie ? s.fp[k] : 0u);  // most words: no tie
+    if (lane == 0) word_tie[w] = v;
+  }
+  __syncthreads();
+  // exclusive scan over the tile's words (tw <= FUSED_MAX_TILE / 32 <= FT: one word per
+  // thread) and, in the same pass, the preceding CTAs' total
+  if (warp * 32 < c || (warp == FWARPS - 1 && rank > 0)) warp_add_u64(t_rows, sacc + 20);  // preceding CTAs' and ranks' total
+  {
+    const uint32_t w = threadIdx.x;
+    unsigned long long v[1] = {w < A.tw ? word_tie[w] : 0ull}, tt[1];
+    cta_scan1(v, tt);  // (its barriers complete the sum)
+    if (w < A.tw) word_tie[w] = v[0];
+    if (threadIdx.x == 0) word_tie[A.tw] = tt[0];  // (memb holds tile / 2 >= tw + 1 words of 64 bits)
+  }
+  const unsigned long long sh_tie_excl = parts_u64(sacc + 20);
+  __syncthreads();
+  STAMP0(10)
+  STAMP_MAX(14)
+
+  // ---------------- P4: emit
+  uint32_t *cnt_pf = s.h, *cnt_ev = s.h + NBL;  // per-CTA list members per list bucket
+  uint32_t *lor_l = s.h + 6 * NBL;   // [2][NBL]: OR of the key bits below the list bucket
+  uint32_t *mm_l = s.h + 10 * NBL;  // [4][NBL]: prefetch min, prefetch ~max, evict min, evict ~max
+  for (int b = threadIdx.x; b < 2 * NBL; b += FT) {
+    s.h[b] = 0;
+    lor_l[b] = 0;
+  }
+  for (int b = threadIdx.x; b < 4 * NBL; b += FT) mm_l[b] = 0xFFFFFFFFu;
+  __syncthreads();
+  unsigned long long h2d = 0, tie_kept = 0;
+  uint32_t n_el = 0;
+#pragma unroll 1
+  for (uint32_t w = warp; w < A.tw; w += FWARPS) {
+    const uint32_t k = w * 32 + lane;
+    const uint32_t elw = s.elig_w[w];  // 0 beyond n_here
+    const uint32_t key = s.keys[k];
+    uint32_t kw = elw;  // kept agents of the word
+    if (!all_fit) {
+      kw = __ballot_sync(0xFFFFFFFFu, key < dstar) & elw;
+      const uint32_t tiew = __ballot_sync(0xFFFFFFFFu, key == dstar) & elw;
+      if (tiew) {  // id-order inclusive prefix of the tie bytes
+        const bool tie = (tiew >> lane) & 1u;
+        const uint32_t fp = s.fp[k];
+        // the word's tie bytes lie in (lo, hi]: every tie of the word fits when hi <= rem, none
+        // when lo > rem (one word of the grid straddles rem: only it needs the in-word prefix)
+        const unsigned long long lo = sh_tie_excl + word_tie[w], hi = sh_tie_excl + word_tie[w + 1];
+        if (hi <= sel.rem) {
+          if (tie) tie_kept += fp;
+          kw |= tiew;
+        } else if (lo <= sel.rem) {
+          unsigned long long incl = tie ? fp : 0u;
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          incl += lo;
+          const bool ok = tie && incl <= sel.rem;
+          if (ok) tie_kept += fp;
+          kw |= __ballot_sync(0xFFFFFFFFu, ok);
+        }
+      }
+    }
+    const uint32_t old = s.old_w[w];
+    const uint32_t pfw = kw & ~old, evw = old & ~kw;
+    if (lane == 0) {
+      if (w < tw_here) bm_new[base / 32 + w] = kw;
+      s.pf_w[w] = pfw;
+      s.ev_w[w] = evw;
+      n_el += __popc(elw);
+    }
+    if (pfw | evw) {  // list members in this word (list-bucket counts)
+      const uint32_t bk = key >> 21;
+      if ((pfw >> lane) & 1u) {
+        h2d += s.fp[k];
+        atomicAdd(&cnt_pf[bk], 1u);
+        atomicMin(&mm_l[bk], key);
+        atomicMin(&mm_l[NBL + bk], ~key);
+        atomicOr(&lor_l[bk], key & 0x1FFFFFu);
+      }
+      if ((evw >> lane) & 1u) {
+        atomicAdd(&cnt_ev[bk], 1u);
+        atomicMin(&mm_l[2 * NBL + bk], key);
+        atomicMin(&mm_l[3 * NBL + bk], ~key);
+        atomicOr(&lor_l[NBL + bk], key & 0x1FFFFFu);
+      }
+    }
+  }
+  __syncthreads();
+  STAMP_MAX(27)  // P4 word loop done
   // list bucket totals (global atomics, issued now: they drain while the members are
   // staged); the CTA's min / max key and OR of the low key bits per bucket go to its rows
   {

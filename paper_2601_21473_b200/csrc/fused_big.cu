@@ -121,57 +121,70 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     const uint32_t BS = LB * FT, nk = tw_here * 32;
     uint4 r[LB], r2[LB];
     uint32_t bw[LB], bw2[LB];  // the residency words, loaded with the records
-    const uint32_t tw_all = (uint32_t)((p.n_local + 31) / 32);
+    // (the tile is a multiple of 32 agents: the CTA's residency words start at base / 32)
+    const uint32_t *bmt = bm_old + (base >> 5);
+    const uint32_t twm1 = tw_here ? tw_here - 1 : 0u;
     auto load_into = [&](uint4 (&rr)[LB], uint32_t (&ww)[LB], uint32_t k0) {
 #pragma unroll
       for (int j = 0; j < LB; ++j) {
-        rr[j] = n_here ? ld_stream(rec + min(k0 + j * FT + threadIdx.x, last)) : make_uint4(0, 0, 0, 0);
-        const uint64_t wi = (base + k0 + j * FT + threadIdx.x) >> 5;
-        ww[j] = wi < tw_all ? bm_old[wi] : 0u;
+        rr[j] = ld_stream(rec + min(k0 + j * FT + threadIdx.x, last));
+        ww[j] = bmt[min((k0 + j * FT) / 32 + warp, twm1)];  // (warp-uniform)
       }
     };
-    load_into(r, bw, 0);
+    // One record; compiled two ways: CHECK (a batch that runs past the tile's end: `valid`
+    // masks) and FAST (32-bit now, no distance copy: the class-0 arithmetic with nothing else
+    // live; warps holding other classes still take the general definition)
+    auto record = [&](const uint4 rj, const uint32_t rw, const uint32_t k, auto check_tag, auto fast_tag) {
+      constexpr bool CHECK = decltype(check_tag)::value, FAST = decltype(fast_tag)::value;
+      const bool valid = CHECK ? k < n_here : true;
+      const bool res = valid && ((rw >> lane) & 1u);
+      const uint32_t ph = rj.z & 3u, cl = (rj.z >> 2) & 3u;
+      float dist, th;
+      if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {  // interaction / diffusion / malformed
+        dist = valid ? distance_of(rj, now, hop_scale, d.dint, p.n_kin, st) : 0.0f;
+        th = (cl & 2u) ? ((cl & 1u) ? 0.0f : th2) : ((cl & 1u) ? th1 : th0);
+      } else {
+        float d_action;
+        if (FAST || now32) d_action = rj.x > nowl ? __uint2float_rn(rj.x - nowl) : 0.0f;
+        else {
+          const int64_t remain = (int64_t)rj.x - now;
+          d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
+        }
+        dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
+        th = th0;
+      }
+      const uint32_t bits = valid ? __float_as_uint(dist) : 0u;
+      const bool elig = valid && (res || dist == 0.0f || dist < th);
+      const uint32_t q = ibucket(bits);
+      if (elig) {
+        atomicAdd(&h[q], rj.y & 0xFFFFu);
+        atomicAdd(&h[NB1 + q], rj.y >> 16);
+        atomicAdd(&h[2 * NB1 + q], res ? 0x10000u : 1u);
+        if (ib_multi(q)) {
+          const uint32_t jo = atomicAdd(&s_novf, 1u);
+          if (jo < LOVF) s_ovf[jo] = make_uint4(bits, (uint32_t)(p.shard_begin + base + k), res ? 1u : 0u, 0u);
+        }
+      }
+      if (valid) {
+        codes[k] = (uint16_t)(q | (elig ? 1u << 12 : 0u) | (res ? 1u << 13 : 0u) | (((rj.z >> 4) & 1u) << 14));
+        if (!FAST && gkeys) gkeys[k] = bits;
+      }
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    const bool fast = now32 && gkeys == nullptr;
+    if (n_here) load_into(r, bw, 0);
 #pragma unroll 1
     for (uint32_t k0 = 0; k0 < nk; k0 += BS) {
       if (k0 + BS < nk) load_into(r2, bw2, k0 + BS);
+      if (fast && k0 + BS <= n_here) {  // (CTA-uniform) a whole batch inside the tile
 #pragma unroll
-      for (int j = 0; j < LB; ++j) {
-        const uint32_t k = k0 + j * FT + threadIdx.x;  // (k & 31 == lane)
-        if (k0 + j * FT >= nk) break;                  // (CTA-uniform)
-        const uint4 rj = r[j];
-        const bool valid = k < n_here;
-        const uint32_t rw = valid ? bw[j] : 0u;  // (one word per warp)
-        const bool res = (rw >> lane) & 1u;
-        const uint32_t ph = rj.z & 3u, cl = (rj.z >> 2) & 3u;
-        float dist, th;
-        if (__ballot_sync(0xFFFFFFFFu, valid && cl != 0u)) {  // interaction / diffusion / malformed
-          dist = valid ? distance_of(rj, now, hop_scale, d.dint, p.n_kin, st) : 0.0f;
-          th = (cl & 2u) ? ((cl & 1u) ? 0.0f : th2) : ((cl & 1u) ? th1 : th0);
-        } else {
-          float d_action;
-          if (now32) d_action = rj.x > nowl ? __uint2float_rn(rj.x - nowl) : 0.0f;
-          else {
-            const int64_t remain = (int64_t)rj.x - now;
-            d_action = remain <= 0 ? 0.0f : __ll2float_rn(remain);
-          }
-          dist = (ph == 1u || ph == 2u) ? 0.0f : (ph == 3u ? __int_as_float(0x7F800000) : d_action);
-          th = th0;
-        }
-        const uint32_t bits = valid ? __float_as_uint(dist) : 0u;
-        const bool elig = valid && (res || dist == 0.0f || dist < th);
-        const uint32_t q = ibucket(bits);
-        if (elig) {
-          atomicAdd(&h[q], rj.y & 0xFFFFu);
-          atomicAdd(&h[NB1 + q], rj.y >> 16);
-          atomicAdd(&h[2 * NB1 + q], res ? 0x10000u : 1u);
-          if (ib_multi(q)) {
-            const uint32_t jo = atomicAdd(&s_novf, 1u);
-            if (jo < LOVF) s_ovf[jo] = make_uint4(bits, (uint32_t)(p.shard_begin + base + k), res ? 1u : 0u, 0u);
-          }
-        }
-        if (valid) {
-          codes[k] = (uint16_t)(q | (elig ? 1u << 12 : 0u) | (res ? 1u << 13 : 0u) | (((rj.z >> 4) & 1u) << 14));
-          if (gkeys) gkeys[k] = bits;
+        for (int j = 0; j < LB; ++j) record(r[j], bw[j], k0 + j * FT + threadIdx.x, F_(), T_());
+      } else {
+#pragma unroll
+        for (int j = 0; j < LB; ++j) {
+          if (k0 + j * FT >= nk) break;  // (CTA-uniform)
+          record(r[j], bw[j], k0 + j * FT + threadIdx.x, T_(), F_());
         }
       }
 #pragma unroll
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   if (all_fit && threadIdx.x == FT - 1) sh_town = 0;
   // bucket owner pass (as fused.cu)
   {
-    uint32_t *tn = col + G * RB, *tr = tn + RB, *wn = tr + RB, *wr = wn + RB;
+    uint32_t *tn = col + G * RB, *tr = tn + RB;
     for (uint32_t j = warp; j < o_n; j += FWARPS) {
       uint32_t a = 0, e = 0;
       for (uint32_t i = 0; i < QP; ++i) {
@@ -287,33 +300,26 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       }
     }
     __syncthreads();
+    // the range's totals (owner o's share of both lists), published; each warp of the pass below
+    // sums the offsets of its bucket within the range itself (no serial scan)
     if (warp == 0) {
-      const uint32_t JP = (o_n + 31) / 32;
-      uint32_t sa = 0, se = 0;
-      for (uint32_t i = 0; i < JP; ++i) {
-        const uint32_t j = lane * JP + i;
-        if (j < o_n) {
-          sa += tn[j];
-          se += tr[j];
-        }
+      uint32_t ta = 0, te = 0;
+      for (uint32_t l = lane; l < o_n; l += 32) {
+        ta += tn[l];
+        te += tr[l];
       }
-      const uint32_t ia = warp_incl_scan(sa), ie = warp_incl_scan(se);
-      const uint32_t TA = __shfl_sync(0xFFFFFFFFu, ia, 31), TE = __shfl_sync(0xFFFFFFFFu, ie, 31);
-      uint32_t ra = ia - sa, re = ie - se;
-      for (uint32_t i = 0; i < JP; ++i) {
-        const uint32_t j = lane * JP + i;
-        if (j < o_n) {
-          wn[j] = ra;
-          ra += tn[j];
-          re += tr[j];
-          wr[j] = TE - re;
-        }
-      }
-      if (lane == 0) st_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + c], pack_ep(ep, TA, TE));
+      ta = __reduce_add_sync(0xFFFFFFFFu, ta);
+      te = __reduce_add_sync(0xFFFFFFFFu, te);
+      if (lane == 0) st_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + c], pack_ep(ep, ta, te));
     }
-    __syncthreads();
     for (uint32_t j = warp; j < o_n; j += FWARPS) {
-      const uint32_t w_n = wn[j], w_r = wr[j], t_r = tr[j];
+      uint32_t w_n = 0, w_r = 0;  // the range's buckets before j (prefetch) / after j (evict)
+      for (uint32_t l0 = 0; l0 < o_n; l0 += 32) {
+        const uint32_t l = l0 + lane;
+        w_n += __reduce_add_sync(0xFFFFFFFFu, (l < o_n && l < j) ? tn[l] : 0u);
+        w_r += __reduce_add_sync(0xFFFFFFFFu, (l < o_n && l > j) ? tr[l] : 0u);
+      }
+      const uint32_t t_r = tr[j];
       unsigned long long *P = d.f_pos + ((uint64_t)par * NB1 + o_lo + j) * FUSED_MAX_CTAS;
       uint32_t ca = 0, ce = 0;
       for (uint32_t q0 = 0; q0 < G; q0 += 32) {

@@ -262,6 +262,9 @@ __device__ __forceinline__ unsigned long long parts_u64(const uint32_t *acc4) {
 static __device__ __noinline__ void cta_scan1(unsigned long long (&v)[1], unsigned long long (&tot)[1]) {
   block_excl_scan_v<unsigned long long, 1, FT>(v, tot);
 }
+static __device__ __noinline__ void cta_scan2(unsigned long long (&v)[2], unsigned long long (&tot)[2]) {
+  block_excl_scan_v<unsigned long long, 2, FT>(v, tot);
+}
 
 // The ranks of one world planned in one launch (scalesim_step_group, SCALESIM_F_LOOPBACK): each
 // rank's published arrays.  The select sums the ranks' histograms after the world barrier, the
