@@ -28,7 +28,6 @@
 namespace ss {
 
 constexpr uint32_t BIG_CW = 1024;    // words per P34 chunk (one per thread)
-constexpr uint32_t BIG_MCAP = 2048;  // (shared-memory layout: candidate staging, reused by the overflow sort)
 #ifndef BIG_LB_V
 #define BIG_LB_V 4
 #endif
@@ -38,11 +37,9 @@ static uint32_t big_rb(uint32_t gsize) { return ((NB1 + gsize - 1) / gsize + 3u)
 
 size_t fused_big_smem_bytes(uint32_t gsize) {
   const uint32_t RB = big_rb(gsize);
-  return (size_t)4 * 4 * NB1             // histograms / counts / need list, later positions
+  return (size_t)4 * 4 * NB1             // histograms / counts / need list, later cursors
          + (size_t)4 * RB * (gsize + 4)  // bucket-owner staging
-         + (size_t)4 * 8 * BIG_CW        // per-word masks of a chunk
-         + (size_t)8 * 2 * BIG_CW        // per-word tie bytes and offsets
-         + (size_t)4 * 2 * BIG_MCAP      // the two candidate lists of a round
+         + (size_t)8 * 2 * BIG_OVF_CAP   // overflow sort (its first half: the (e) sort counters)
          + 64;
 }
 
@@ -84,12 +81,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   uint32_t *h = reinterpret_cast<uint32_t *>(smem_raw);  // [4 NB1]
   const uint32_t RB = ((NB1 + G - 1) / G + 3u) & ~3u;
   uint32_t *col = h + 4 * NB1;                            // [G][RB] + [4][RB]
-  uint32_t *mE = col + RB * (G + 4);                      // per-word masks of a chunk [8][CW]
-  uint32_t *mR = mE + BIG_CW, *mY = mR + BIG_CW, *mLT = mY + BIG_CW, *mTIE = mLT + BIG_CW;
-  uint32_t *mPFC = mTIE + BIG_CW, *mEVC = mPFC + BIG_CW, *mKEPT = mEVC + BIG_CW;
-  unsigned long long *sTB = reinterpret_cast<unsigned long long *>(mKEPT + BIG_CW);  // [CW]
-  unsigned long long *sLO = sTB + BIG_CW;                                            // [CW]
-  uint32_t *lpf = reinterpret_cast<uint32_t *>(sLO + BIG_CW), *lev = lpf + BIG_MCAP;  // candidates
+  // scratch after the owner staging: the (e) sort counters, then the overflow sort's two lists
+  unsigned long long *la = reinterpret_cast<unsigned long long *>(col + RB * (G + 4));  // [BIG_OVF_CAP]
+  unsigned long long *lb = la + BIG_OVF_CAP;                                            // [BIG_OVF_CAP]
   const uint64_t base = (uint64_t)c * tile;
   const uint32_t n_here =
       base >= p.n_local ? 0u : (uint32_t)((p.n_local - base) < tile ? (p.n_local - base) : tile);
@@ -274,7 +268,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     return;
   }
   // preceding CTAs' bytes at D* (tie prefix), and this CTA's own
-  __shared__ unsigned long long sh_tpre, sh_town;
+  __shared__ unsigned long long sh_town;
   unsigned long long t_rows = 0;
   if (!all_fit && threadIdx.x < c) t_rows = d.f_rows1[(uint64_t)threadIdx.x * NB1 + bs];
   if (!all_fit && threadIdx.x == FT - 1) sh_town = d.f_rows1[(uint64_t)c * NB1 + bs];
@@ -327,7 +321,15 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         const uint32_t v = q < G ? col[q * RB + j] : 0u;
         const uint32_t a = v & 0xFFFFu, e = v >> 16;
         const uint32_t ia = warp_incl_scan(a), ie = warp_incl_scan(e);
-        if (q < G) st_relaxed_u64(&P[q], pack_ep(ep, w_n + ca + ia - a, w_r + t_r - (ce + ie)));
+        // (only the entries a consumer reads: its list buckets, and CTA 0's / the last CTA's)
+        const uint32_t b = o_lo + j;
+        const bool used =
+#ifdef NO_OWNER_SKIP
+            true;
+#else
+            (b < bs ? a != 0u : (b > bs ? e != 0u : v != 0u)) || q == 0 || q == G - 1;
+#endif
+        if (q < G && used) st_relaxed_u64(&P[q], pack_ep(ep, w_n + ca + ia - a, w_r + t_r - (ce + ie)));
         ca += __shfl_sync(0xFFFFFFFFu, ia, 31);
         ce += __shfl_sync(0xFFFFFFFFu, ie, 31);
       }
@@ -403,28 +405,31 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
 
   STAMP_MAX(17)  // positions
   // ---------------- P34: chunks of words from the highest id down
-  PROBE(unsigned long long dta = 0, dtb = 0, dtc = 0, dtd = 0, tq = gtimer();)
+  PROBE(unsigned long long dta = 0, dtb = 0, dtc = 0, dtd = 0, tq = gtimer();)  // (dtd: unused)
 #define LAP(v) PROBE(if (threadIdx.x == 0) { const unsigned long long t_ = gtimer(); v += t_ - tq; tq = t_; })
   unsigned long long h2d = 0, tie_kept = 0, d2h = 0;
   uint32_t n_el = 0, n_pfb = 0, n_evb = 0;
   unsigned long long above = 0;  // tie bytes of the chunks done (all above this chunk)
   const unsigned long long rem = sel.rem;
   const uint32_t n_chunks = (tw_here + BIG_CW - 1) / BIG_CW;
-  __shared__ unsigned long long sh_ctot;
   // this CTA's list candidates (HBM scratch of the tile's range): bucket << 20 | kept << 19 | k
   uint32_t *g_lpf = d.sort_ka + base, *g_lev = d.sort_va + base;
   uint32_t n_lpf = 0, n_lev = 0;  // (CTA-uniform)
   for (int ch = (int)n_chunks - 1; ch >= 0; --ch) {
     const uint32_t w0 = (uint32_t)ch * BIG_CW, wn = min(BIG_CW, tw_here - w0);
-    // (a) decode the chunk's codes: masks and tie bytes, one word (32 agents, 64 bytes of
-    // codes) per thread
-    if (threadIdx.x < wn) {
-      const uint32_t i = threadIdx.x, w = w0 + i;
+    // Word w0 + i belongs to thread i in every step of the chunk: its masks stay in registers.
+    const uint32_t i = threadIdx.x, w = w0 + i;
+    const bool mine = i < wn;
+    // (a) decode the word's codes (32 agents, 64 bytes): eligible, resident, dirty, kept below
+    // the boundary, tie group, prefetch candidates, multi-valued; evict candidates (residents
+    // outside the kept buckets: the evicted ones and the resident ties, which the cut may keep)
+    uint32_t em = 0, rm = 0, ym = 0, lm = 0, tm = 0, pm = 0, mv = 0;
+    unsigned long long tb = 0;  // the word's tie bytes
+    if (mine) {
       const uint4 *cw = reinterpret_cast<const uint4 *>(codes + (uint64_t)w * 32);
       uint4 q4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) q4[u] = cw[u];  // (beyond n_here: zero codes, ineligible)
-      uint32_t em = 0, rm = 0, ym = 0, lm = 0, tm = 0, pm = 0, mv = 0;
 #pragma unroll
       for (int l = 0; l < 32; ++l) {
         const uint32_t word = (&q4[l >> 3].x)[(l >> 1) & 3];
@@ -439,44 +444,36 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         pm |= (e && !r && (all_fit || q <= bs) && !ib_multi(q)) ? bit : 0u;
         mv |= (e && ib_multi(q)) ? bit : 0u;
       }
-      unsigned long long tb = 0;
       for (uint32_t m = tm; m; m &= m - 1) tb += rec[w * 32 + __ffs(m) - 1].y;  // (ties: few)
-      mE[i] = em;
-      mR[i] = rm;
-      mY[i] = ym;
-      mLT[i] = lm;
-      mTIE[i] = tm;
-      mPFC[i] = pm;
-      mEVC[i] = mv;  // (multi-valued mask for now)
-      sTB[i] = tb;
     }
-    __syncthreads();
+    const uint32_t ec = rm & ~lm & ~mv;  // evict candidates
     LAP(dta)
-    // (b) offsets of the words' tie bytes: the chunk starts after the preceding CTAs' ties and
-    // this CTA's ties below the chunk (= own total - chunks above - this chunk)
+    // (b) one scan: the words' tie bytes in id order (the chunk's ties start after the preceding
+    // CTAs' and this CTA's below the chunk = own total - chunks above - this chunk) and their
+    // candidate counts (list offsets in descending id order: total - inclusive prefix)
+    unsigned long long lo, cv;
+    uint32_t tcp, tce;
     {
-      unsigned long long v[1] = {threadIdx.x < wn ? sTB[threadIdx.x] : 0ull}, tt[1];
-      cta_scan1(v, tt);
-      const unsigned long long off = tie_pre + (tie_own - above - tt[0]);
-      if (threadIdx.x < wn) sLO[threadIdx.x] = off + v[0];
-      if (threadIdx.x == 0) sh_ctot = tt[0];
+      unsigned long long v[2] = {tb, (unsigned long long)__popc(pm) | ((unsigned long long)__popc(ec) << 32)}, tt[2];
+      cta_scan2(v, tt);
+      lo = tie_pre + (tie_own - above - tt[0]) + v[0];
+      above += tt[0];
+      cv = v[1];
+      tcp = (uint32_t)tt[1];
+      tce = (uint32_t)(tt[1] >> 32);
     }
-    __syncthreads();
     LAP(dtb)
-    above += sh_ctot;
-    // (c) kept / prefetch / evict words, residency, byte sums: one word per thread
-    if (threadIdx.x < wn) {
-      const uint32_t i = threadIdx.x, w = w0 + i;
-      uint32_t kw = mLT[i];
-      const uint32_t tiew = mTIE[i];
-      if (tiew) {
-        const unsigned long long lo = sLO[i], hi = lo + sTB[i];
+    if (mine) {
+      // (c) kept / prefetch / evict words, residency, byte sums
+      uint32_t kw = lm;
+      if (tm) {
+        const unsigned long long hi = lo + tb;
         if (hi <= rem) {
-          kw |= tiew;
-          tie_kept += sTB[i];
+          kw |= tm;
+          tie_kept += tb;
         } else if (lo <= rem) {  // the straddling word: its ties in id order
           unsigned long long incl = lo;
-          for (uint32_t m = tiew; m; m &= m - 1) {
+          for (uint32_t m = tm; m; m &= m - 1) {
             const int l = __ffs(m) - 1;
             const uint32_t fp = rec[w * 32 + l].y;
             incl += fp;
@@ -487,52 +484,68 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
           }
         }
       }
-      const uint32_t rm = mR[i];
       const uint32_t pfw = kw & ~rm, evw = rm & ~kw;
       if (w < tw_here) bm_new[(base >> 5) + w] = kw;
-      n_el += __popc(mE[i]);
-      n_pfb += __popc(pfw & tiew);
-      n_evb += __popc(evw & tiew);
-      mKEPT[i] = kw;
-      mEVC[i] = evw & ~mEVC[i];  // evict members outside multi-valued buckets
-      for (uint32_t m = pfw; m; m &= m - 1) h2d += rec[w * 32 + __ffs(m) - 1].y;
-      for (uint32_t m = evw & mY[i]; m; m &= m - 1) d2h += d.wb_bytes[base + w * 32 + __ffs(m) - 1];
-    }
-    __syncthreads();
-    LAP(dtc)
-    // (d) the chunk's candidates, appended in descending id order to this CTA's two candidate
-    // lists (HBM scratch, placed once after the last chunk)
-    {
-      const uint32_t t = threadIdx.x;
-      const uint32_t iw = t < wn ? wn - 1 - t : 0u;  // reversed word order: word wn-1-t at thread t
-      const uint32_t cp = t < wn ? __popc(mPFC[iw]) : 0u, ce = t < wn ? __popc(mEVC[iw]) : 0u;
-      unsigned long long v[1] = {(unsigned long long)cp | ((unsigned long long)ce << 32)}, tt[1];
-      cta_scan1(v, tt);
-      if (t < wn) {
-        const uint32_t wbase = (w0 + iw) * 32;
-        uint32_t m = mPFC[iw], o = n_lpf + (uint32_t)v[0];
-        const uint32_t km = mKEPT[iw];
-        while (m) {
-          const int bit = 31 - __clz(m);
-          m &= ~(1u << bit);
-          const uint32_t k = wbase + bit;
-          g_lpf[o++] = ((uint32_t)(codes[k] & 0xFFFu) << 20) | (((km >> bit) & 1u) << 19) | k;
+      n_el += __popc(em);
+      n_pfb += __popc(pfw & tm);
+      n_evb += __popc(evw & tm);
+      // footprints of the prefetched agents and write-back bytes of the dirty evicted ones: up
+      // to two of each per round trip (most words have none or one)
+      uint32_t mp = pfw, me = evw & ym;
+      while (mp | me) {
+        uint32_t v0 = 0, v1 = 0, u0 = 0, u1 = 0;
+        if (mp) {
+          v0 = rec[w * 32 + __ffs(mp) - 1].y;
+          mp &= mp - 1;
         }
-        m = mEVC[iw];
-        o = n_lev + (uint32_t)(v[0] >> 32);
-        while (m) {
-          const int bit = 31 - __clz(m);
-          m &= ~(1u << bit);
-          const uint32_t k = wbase + bit;
-          g_lev[o++] = ((uint32_t)(codes[k] & 0xFFFu) << 20) | k;
+        if (mp) {
+          v1 = rec[w * 32 + __ffs(mp) - 1].y;
+          mp &= mp - 1;
+        }
+        if (me) {
+          u0 = d.wb_bytes[base + w * 32 + __ffs(me) - 1];
+          me &= me - 1;
+        }
+        if (me) {
+          u1 = d.wb_bytes[base + w * 32 + __ffs(me) - 1];
+          me &= me - 1;
+        }
+        h2d += (unsigned long long)v0 + v1;
+        d2h += (unsigned long long)u0 + u1;
+      }
+      // (d) the word's candidates appended in descending id order to this CTA's two candidate
+      // lists (HBM scratch, placed once after the last chunk), each with its kept bit; four
+      // code loads per round trip (the lists are disjoint: non-resident / resident)
+      uint32_t op = n_lpf + tcp - (uint32_t)cv - __popc(pm);
+      uint32_t oe = n_lev + tce - (uint32_t)(cv >> 32) - __popc(ec);
+      const uint32_t wbase = w * 32;
+      uint32_t m = pm | ec;
+      while (m) {
+        uint32_t bt[4], cd[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          bt[u] = 32;
+          cd[u] = 0;
+          if (m) {
+            bt[u] = 31 - __clz(m);
+            m &= ~(1u << bt[u]);
+            cd[u] = codes[wbase + bt[u]];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (bt[u] == 32) break;
+          const uint32_t bit = bt[u], x = ((cd[u] & 0xFFFu) << 20) | (((kw >> bit) & 1u) << 19) | (wbase + bit);
+          if ((pm >> bit) & 1u) g_lpf[op++] = x;
+          else g_lev[oe++] = x;
         }
       }
-      n_lpf += (uint32_t)tt[0];
-      n_lev += (uint32_t)(tt[0] >> 32);
-      __syncthreads();  // (the next chunk rewrites the masks; the placement reads the lists)
     }
-    LAP(dtd)
+    n_lpf += tcp;
+    n_lev += tce;
+    LAP(dtc)
   }
+  __syncthreads();  // (the placement reads every thread's candidates)
   PROBE(if (threadIdx.x == 0) {
     atomicMax(&prof[22], dta);
     atomicMax(&prof[23], dtb);
@@ -545,7 +558,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   // (only kept candidates are members)
   {
     uint32_t *start = h + 2 * NB1;  // [NB1] first sorted index per bucket (the counts are no longer needed)
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(sTB);  // 256 x 16 sort counters (sTB, sLO)
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(la);  // 256 x 16 sort counters
     uint32_t *ka = d.sort_kb + base, *ia = d.sort_vb + base, *kb = d.f_sk2 + base, *ib = d.f_sv2 + base;
     for (int lst = 0; lst < 2; ++lst) {
       const uint32_t n = lst == 0 ? n_lpf : n_lev;
@@ -565,11 +578,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       for (uint32_t i = threadIdx.x; i < n; i += FT) {
         const uint32_t b = ka[i], rk = i - start[b], x = src[ia[i]], k = x & 0x7FFFFu;
         const uint32_t pos = lst == 0 ? cur[b] - rk : cur[b] + rk;
+        // members: kept prefetch candidates, evict candidates the cut does not keep
+        if (((x >> 19) & 1u) != (lst == 0 ? 1u : 0u)) continue;
         if (pos >= p.n_local) {  // (cannot happen: flagged instead of writing out of bounds)
+#ifdef DEBUG_SYNC
+          atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), 1u << 20);
+#endif
           atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), ST_SYNC);
           continue;
         }
-        if (lst == 1 || ((x >> 19) & 1u)) out[pos] = (uint32_t)(p.shard_begin + base + k);
+        out[pos] = (uint32_t)(p.shard_begin + base + k);
       }
       __syncthreads();
     }
@@ -581,8 +599,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   // (key, id) in shared memory; the chunk arrays are free now)
   if (c == G - 1 && sh_novf > 0) {
     const uint32_t nov = (uint32_t)sh_novf;
-    unsigned long long *la = reinterpret_cast<unsigned long long *>(mE);  // [BIG_OVF_CAP]
-    unsigned long long *lb = reinterpret_cast<unsigned long long *>(lpf);  // [BIG_OVF_CAP] (32 KB)
     __shared__ uint32_t sh_na, sh_nb;
     if (threadIdx.x == 0) sh_na = sh_nb = 0;
     __syncthreads();

@@ -240,6 +240,30 @@ def test_fused_wide_code_segments():
     run_parity(w, transfer=False, multi_kernel=True)
 
 
+@pytest.mark.parametrize("keep", [True, False])
+def test_remaining_ticks_beyond_2_24(keep):
+    """R8 at the GPU: remaining action times from 2^24 up to the largest 32-bit t_next (cast
+    round-to-nearest-even, halfway cases included) mixed with small ones; the boundary falls
+    among the large values in some steps and among the small ones in others."""
+    from gpu_harness import run_parity
+    n = 40000
+    now = 1000
+    rng = np.random.default_rng(29)
+    fp = rng.choice([1, 2, 3], n) * tg.PAGE_BYTES
+    steps = []
+    for s in range(3):
+        big = rng.random(n) < (0.2 if s != 1 else 0.7)
+        d = np.where(big, rng.integers(1 << 24, 0xFFFFFFFF - now, n), rng.integers(0, 60, n))
+        d[:8] = [(1 << 24) + 1, (1 << 24) + 3, (1 << 25) + 2, (1 << 25) + 6, 0xFFFFFFFF - now, 1 << 24, (1 << 24) - 1, 0]
+        steps.append(rec_of([dict(d=int(x), fp=int(fp[i])) for i, x in enumerate(d)], now))
+    blocks = tg.make_blocks([[tg.KIND_KV]] * n, [[int(f)] for f in fp])
+    w = tg.Workload("wide24", n, np.full(3, now, np.int64), np.stack(steps), None, blocks, int(fp.sum() * 0.3),
+                    np.full(3, 40.0, np.float32))
+    run_parity(w, transfer=False, keep_dist=keep)
+    if keep:
+        run_parity(w, transfer=False, multi_kernel=True)
+
+
 @pytest.mark.parametrize("mk", PATHS)
 def test_interaction_grid_pruning_exact(mk):
     """a1' with the spatial grid (>= 2048 participants): clusters far denser than the grid,

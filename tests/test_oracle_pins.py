@@ -145,6 +145,25 @@ def test_phase_rules():
     assert list(d3[6:8]) == [3.0, 6.0]
 
 
+def test_remaining_ticks_beyond_2_24_round_to_nearest():
+    """R8: D_action = max(0, t_next - now) computed exactly in integers and cast to float32
+    round-to-nearest-even ("remaining action duration"; the survey's 2^24 limit is
+    replaced by the cast).  Expected values: the exact rational rounded by the textbook rule
+    (helpers.round_f32), including the halfway cases 2^24 + 1 (down to even) and 2^24 + 3 (up to
+    even), and the largest representable t_next."""
+    now = 1000
+    rem = [(1 << 24) - 1, 1 << 24, (1 << 24) + 1, (1 << 24) + 2, (1 << 24) + 3, (1 << 25) + 2, (1 << 25) + 6,
+           123456789, 0xFFFFFFFF - now]
+    d, st = oracle.score(rec_of([dict(d=r) for r in rem], now), None, now)
+    assert st == 0
+    want = [round_f32(Fraction(r)) for r in rem]
+    assert [float(x) for x in d] == [float(x) for x in want]
+    assert float(d[2]) == float(1 << 24) and float(d[4]) == float((1 << 24) + 4)
+    # now beyond 2^32 (int64 clock): every 32-bit t_next is in the past -> 0
+    d, _ = oracle.score(rec_of([dict(d=0), dict(d=5)], 0), None, (1 << 32) + 7)
+    assert list(d) == [0.0, 0.0]
+
+
 def test_bad_records_flagged():
     agents = [dict(cls=3, d=4), dict(cls=tg.CL_INT, d=4, kin=7)]
     d, st = oracle.score(rec_of(agents), np.zeros((1, 4), np.float32), 0)
