@@ -502,31 +502,17 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   STAMP_MAX(42)  // need list
   // the owners' range totals and this CTA's first list-bucket offsets: loads issued now (their
   // latency hides behind P3 / P4), the epoch tag checked where they are used
-  // Idle threads of the last warp (past the need list) also fetch what the end of the kernel
-  // waits on: the list positions of the boundary bucket (CTA 0) and the multi-valued buckets'
-  // list starts (the overflow CTA), the plan state's status and the world's zero-distance bytes.
   unsigned long long rv_pre = 0, pv_pre = 0;
-  const bool spare = m_need + 6 <= FT;  // (CTA-uniform) threads FT-6 .. FT-1 free
   if (fastp && G > 1) {
-    const unsigned long long *Pb = d.f_pos + (uint64_t)par * NB1 * FUSED_MAX_CTAS;
-    if (threadIdx.x < m_need) pv_pre = ld_relaxed_u64(Pb + (uint64_t)need[threadIdx.x] * FUSED_MAX_CTAS + c);
+    if (threadIdx.x < m_need)
+      pv_pre = ld_relaxed_u64(d.f_pos + ((uint64_t)par * NB1 + need[threadIdx.x]) * FUSED_MAX_CTAS + c);
     if (threadIdx.x < G) rv_pre = ld_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + threadIdx.x]);
-    if (spare && threadIdx.x >= FT - 4) {
-      const uint32_t x = FT - 1 - threadIdx.x;  // 0, 1: CTA 0; 2, 3: CTA G - 1
-      const uint32_t b = x < 2 ? bs : (x == 2 ? (uint32_t)IB_EXACT : (uint32_t)IB_INF - 1);
-      if ((x < 2 ? c == 0 && bs < (uint32_t)NB1 : c == G - 1))
-        pv_pre = ld_relaxed_u64(Pb + (uint64_t)b * FUSED_MAX_CTAS + ((x & 1) ? G - 1 : 0));
-    }
   }
-  if (fastp && spare && c == 0 && threadIdx.x == FT - 5) pv_pre = d.state->status;
-  if (fastp && spare && c == 0 && threadIdx.x == FT - 6)
-    for (uint32_t r = 0; r < nw; ++r) pv_pre += W.acc[r][8 * par];  // (complete since B1)
 
   // ---------------- fast list placement tail (integer distances, fastp: grid-uniform)
   if (fastp) {
     uint32_t *const h32 = s.h;  // [0, NB1): prefetch positions, [NB1, 2 NB1): evict positions
-    __shared__ uint32_t sh_spf, sh_sev, sh_mvpf, sh_mvev, sh_st0;
-    __shared__ unsigned long long sh_zb;
+    __shared__ uint32_t sh_spf, sh_sev, sh_mvpf, sh_mvev;
     unsigned long long *word_tie = reinterpret_cast<unsigned long long *>(s.memb);  // [tw + 1]
     unsigned long long sh_tie_excl = 0;
     if (!all_fit) {  // (CTA-uniform)
@@ -663,20 +649,22 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         h32[b] = rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
         h32[NB1 + b] = rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
       }
-      // list position of bucket b's first member (prefetch: CTA 0's entry, sum_{b' < b} NR[b'])
-      // or last-CTA position (evict: sum_{b' > b} R[b']), from the prefetched entry when it
-      // carries this launch's epoch
-      auto pos_at = [&](uint32_t b, bool ev, unsigned long long v) {
-        const unsigned long long *e = &d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS + (ev ? G - 1 : 0)];
-        if (!spare || (uint32_t)(v >> 48) != ep) v = poll_ep(e, ep, d.header);
-        return ev ? rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu) : rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
+      auto pos_pf = [&](uint32_t b) {  // sum_{b' < b} NR[b']
+        const unsigned long long v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS], ep, d.header);
+        return rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
       };
-      if (c == 0 && threadIdx.x == FT - 1) sh_spf = bs < (uint32_t)NB1 ? pos_at(bs, false, pv_pre) : (uint32_t)s2[1];
-      if (c == 0 && threadIdx.x == FT - 2) sh_sev = bs < (uint32_t)NB1 ? pos_at(bs, true, pv_pre) : 0u;
-      if (c == G - 1 && threadIdx.x == FT - 3) sh_mvpf = pos_at(IB_EXACT, false, pv_pre);
-      if (c == G - 1 && threadIdx.x == FT - 4) sh_mvev = pos_at(IB_INF - 1, true, pv_pre);
-      if (spare && c == 0 && threadIdx.x == FT - 5) sh_st0 = (uint32_t)pv_pre;
-      if (spare && c == 0 && threadIdx.x == FT - 6) sh_zb = pv_pre;
+      auto pos_ev = [&](uint32_t b) {  // sum_{b' > b} R[b']
+        const unsigned long long v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS + G - 1], ep, d.header);
+        return rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
+      };
+      if (c == 0 && threadIdx.x == 0) {
+        sh_spf = bs < (uint32_t)NB1 ? pos_pf(bs) : (uint32_t)s2[1];
+        sh_sev = bs < (uint32_t)NB1 ? pos_ev(bs) : 0u;
+      }
+      if (c == G - 1 && threadIdx.x == 32) {
+        sh_mvpf = pos_pf(IB_EXACT);
+        sh_mvev = pos_ev(IB_INF - 1);
+      }
     } else {
       // one CTA: its counts are the totals (S_pf(b) = sum_{b' < b} NR, S_ev(b) = sum_{b' > b} R)
       const uint32_t r_tot = (uint32_t)(s2[1] >> 32);
@@ -776,17 +764,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         if (sh_spf) atomicAdd(&H[H_N_PF], (unsigned long long)sh_spf);
         if (sh_sev) atomicAdd(&H[H_N_EV], (unsigned long long)sh_sev);
         atomicAdd(&H[H_KEPT], p.budget - sel.rem);
-        uint32_t st0;
-        unsigned long long zb;  // bytes of the world's distance-0 agents
-        if (spare && G > 1) {
-          st0 = sh_st0;
-          zb = sh_zb;
-        } else {
-          st0 = d.state->status;
-          zb = 0;
-          for (uint32_t r = 0; r < nw; ++r) zb += W.acc[r][8 * par];
-        }
+        const uint32_t st0 = d.state->status;
         uint32_t status = (uint32_t)acc[5] | st0;
+        unsigned long long zb = 0;  // bytes of the world's distance-0 agents
+        for (uint32_t r = 0; r < nw; ++r) zb += W.acc[r][8 * par];
         if (zb > p.budget) status |= ST_INSUFFICIENT;
         H[H_CUT_BITS] = all_fit ? 0xFFFFFFFFull : dstar;
         H[H_CUT_REM] = sel.rem;

@@ -2,20 +2,22 @@
 // than fused.cu's shared-memory tile holds (> FUSED_MAX_TILE = 12288 per CTA, i.e. above
 // ~1.8M agents on 148 SMs), up to 2^19 agents per CTA (~77M per GPU).
 //
-// Same method and same bucket-owner list placement as fused.cu (DESIGN.md §7.1), but the
-// per-agent state between the score pass and the emit pass lives in HBM as one 16-bit code per
-// agent (level-1 value bucket, eligibility, residency, dirty bit: 2 B written + 2 B read per
-// agent on top of the 16-byte record) instead of shared memory; footprints are re-read from the
-// record only for the agents that need them (the tie group at D*, prefetched agents).
-//   P1   stream the CTA's records: distance, eligibility, bucket; byte and count histograms in
-//        shared memory; code -> HBM
+// Same method and same bucket-owner list placement as fused.cu (DESIGN.md §7.1b), but the
+// per-agent state between the score pass and the emit pass lives in HBM: the level-1 bucket of
+// each agent (2 B) and, per 32-agent word, the eligible / resident / dirty / multi-valued masks
+// (16 B), written by P1 and read once by P34, instead of shared memory.
+//   P1   stream the CTA's records: distance, eligibility, bucket; byte and count histograms and
+//        the eligible non-residents' byte histogram in shared memory; codes and word masks -> HBM
 //   B1   grid barrier; select D* (warp 0) while the other warps stage this CTA's bucket-owner
-//        columns; owner pass; this CTA's list-bucket positions from the owners
-//   P34  the CTA's words in chunks of 1024, from the highest id down: tie bytes per word, their
-//        scan (the offset of a chunk follows from the CTA's tie total and the chunks above it),
-//        kept / prefetch / evict words, new residency, byte sums; the chunk's list candidates
-//        in descending id order are placed by two warps with per-bucket cursors (evict: next
-//        free position; prefetch: counting down from the bucket's last position, so that the
+//        columns; the prefetched bytes below the boundary from the non-resident histogram; owner
+//        pass; this CTA's list-bucket positions from the owners; the first chunk of codes is
+//        copied into a shared-memory stash meanwhile
+//   P34  the CTA's words in chunks of 1024 from the highest id down, word i = thread i: below /
+//        at-boundary masks from the stashed codes (SWAR, two per 32-bit pair), tie bytes, one
+//        two-value scan (tie-byte offsets in id order, candidate counts), kept / prefetch / evict
+//        words, residency, write-back bytes; candidates appended in descending id order
+//   (e)  per list one stable sort of the candidates by bucket; positions from per-bucket cursors
+//        (evict: up from the bucket's first position; prefetch: down from its last, so that the
 //        list stays in ascending id order)
 // Limits (status SCALESIM_ST_LIMIT, the step's plan is not produced): the boundary D* falls in
 // a multi-valued bucket (>= 2048 ticks), or more than BIG_OVF_CAP (4096) eligible agents have
@@ -33,14 +35,44 @@ constexpr uint32_t BIG_CW = 1024;    // words per P34 chunk (one per thread)
 #endif
 constexpr int BIG_LB = BIG_LB_V;     // records in flight per thread in P1 (two batches)
 
+// the codes of chunk ch of this tile (words [ch * BIG_CW, ...)) into L2 ahead of its decode
+__device__ __forceinline__ void prefetch_chunk_codes(const uint16_t *codes, uint32_t tw, int ch) {
+#ifdef BIG_NO_PF
+  return;
+#endif
+  if (ch < 0) return;
+  const uint32_t w0 = (uint32_t)ch * BIG_CW, wn = min(BIG_CW, tw - w0);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(codes + (uint64_t)w0 * 32), "r"(wn * 64u) : "memory");
+}
+
+
 static uint32_t big_rb(uint32_t gsize) { return ((NB1 + gsize - 1) / gsize + 3u) & ~3u; }
+
+constexpr uint32_t BIG_STASH = 64 * BIG_CW;  // bytes of codes per chunk
+// One stash (refilled after each chunk from L2, where the next chunk's codes were prefetched
+// meanwhile) or two (the next chunk copied while this one is processed).  Two cost 64 KB more
+// shared memory, i.e. less L1 for the loads in flight of the score pass (measured slower).
+#ifndef BIG_NSTASH
+#define BIG_NSTASH 1
+#endif
 
 size_t fused_big_smem_bytes(uint32_t gsize) {
   const uint32_t RB = big_rb(gsize);
   return (size_t)4 * 4 * NB1             // histograms / counts / need list, later cursors
          + (size_t)4 * RB * (gsize + 4)  // bucket-owner staging
-         + (size_t)8 * 2 * BIG_OVF_CAP   // overflow sort (its first half: the (e) sort counters)
+         + (size_t)BIG_NSTASH * BIG_STASH  // R: the code stashes (also the P1 byte histogram, the sorts)
          + 64;
+}
+
+// Chunk ch of this tile's codes (words [ch * BIG_CW, ...)) into a shared-memory stash, 16 bytes
+// per cp.async (coalesced); 16-byte unit x (word x / 4, codes 8 (x % 4) ..) lands at
+// x ^ ((x >> 3) & 3): a thread reading its word's four units hits eight distinct bank groups
+// per quarter warp.
+__device__ __forceinline__ void stash_chunk(uint8_t *stash, const uint16_t *codes, uint32_t tw, int ch) {
+  const uint32_t w0 = (uint32_t)ch * BIG_CW, nx = 4 * min(BIG_CW, tw - w0);
+  const uint4 *src = reinterpret_cast<const uint4 *>(codes + (uint64_t)w0 * 32);
+  for (uint32_t x = threadIdx.x; x < nx; x += FT) cp_async16(stash + 16 * (x ^ ((x >> 3) & 3u)), src + x);
+  cp_async_commit();
 }
 
 __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ FusedArgs<1> B) {
@@ -81,9 +113,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   uint32_t *h = reinterpret_cast<uint32_t *>(smem_raw);  // [4 NB1]
   const uint32_t RB = ((NB1 + G - 1) / G + 3u) & ~3u;
   uint32_t *col = h + 4 * NB1;                            // [G][RB] + [4][RB]
-  // scratch after the owner staging: the (e) sort counters, then the overflow sort's two lists
-  unsigned long long *la = reinterpret_cast<unsigned long long *>(col + RB * (G + 4));  // [BIG_OVF_CAP]
-  unsigned long long *lb = la + BIG_OVF_CAP;                                            // [BIG_OVF_CAP]
+  // region R after the owner staging, three lives: P1's non-resident byte histogram [2 NB1];
+  // P34's two code stashes (a chunk of codes each, 64 KB); the (e) sort counters and the
+  // overflow sort's two lists
+  uint8_t *R = reinterpret_cast<uint8_t *>(col + RB * (G + 4));
+  uint32_t *nrb = reinterpret_cast<uint32_t *>(R);                       // [2 NB1] (16-bit halves)
+  unsigned long long *la = reinterpret_cast<unsigned long long *>(R);    // [BIG_OVF_CAP]
+  unsigned long long *lb = la + BIG_OVF_CAP;                             // [BIG_OVF_CAP]
   const uint64_t base = (uint64_t)c * tile;
   const uint32_t n_here =
       base >= p.n_local ? 0u : (uint32_t)((p.n_local - base) < tile ? (p.n_local - base) : tile);
@@ -92,10 +128,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   const uint32_t *bm_old = d.bm[p.cur];
   uint32_t *bm_new = d.bm[p.cur ^ 1];
   uint16_t *codes = d.big_codes + base;
+  uint4 *wmask = d.big_wmask + (base >> 5);
   const uint4 *rec = p.rec + base;
 
   // ---------------- P1: score, histograms, codes
   for (int b = threadIdx.x; b < 3 * NB1; b += FT) h[b] = 0u;
+  for (int b = threadIdx.x; b < 2 * NB1; b += FT) nrb[b] = 0u;
   constexpr uint32_t LOVF = 128;
   __shared__ uint4 s_ovf[LOVF];
   __shared__ uint32_t s_novf;
@@ -154,13 +192,24 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         atomicAdd(&h[q], rj.y & 0xFFFFu);
         atomicAdd(&h[NB1 + q], rj.y >> 16);
         atomicAdd(&h[2 * NB1 + q], res ? 0x10000u : 1u);
+        if (!res) {  // eligible non-residents: the prefetched bytes follow from the boundary
+          atomicAdd(&nrb[q], rj.y & 0xFFFFu);
+          atomicAdd(&nrb[NB1 + q], rj.y >> 16);
+        }
         if (ib_multi(q)) {
           const uint32_t jo = atomicAdd(&s_novf, 1u);
           if (jo < LOVF) s_ovf[jo] = make_uint4(bits, (uint32_t)(p.shard_begin + base + k), res ? 1u : 0u, 0u);
         }
       }
+      // the word's masks (one 16-byte store per 32 agents) and the agent's bucket; within a word
+      // lane l's code sits at 2 (l % 16) + l / 16, so that 32-bit pair j of the word holds
+      // agents j and j + 16 (P34 decodes pairs into masks without a bit permutation)
+      const uint32_t emw = __ballot_sync(0xFFFFFFFFu, elig), rmw = __ballot_sync(0xFFFFFFFFu, res);
+      const uint32_t ymw = __ballot_sync(0xFFFFFFFFu, valid && ((rj.z >> 4) & 1u));
+      const uint32_t mvw = __ballot_sync(0xFFFFFFFFu, elig && ib_multi(q));
+      if (lane == 0 && (!CHECK || k < nk)) wmask[k >> 5] = make_uint4(emw, rmw, ymw, mvw);  // (the tile's words only)
       if (valid) {
-        codes[k] = (uint16_t)(q | (elig ? 1u << 12 : 0u) | (res ? 1u << 13 : 0u) | (((rj.z >> 4) & 1u) << 14));
+        codes[(k & ~31u) | ((lane & 15) << 1) | (lane >> 4)] = (uint16_t)q;
         if (!FAST && gkeys) gkeys[k] = bits;
       }
     };
@@ -215,6 +264,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   STAMP_MAX(26)  // published
   wgrid.sync();
   STAMP_MAX(4)   // B1
+  // the first chunk P34 decodes (the highest) into L2 while the select and the owners run
+  if (threadIdx.x == 0 && tw_here) prefetch_chunk_codes(codes, tw_here, (int)((tw_here - 1) / BIG_CW));
 
   // ---------------- select, bucket owners, list-bucket positions
   {
@@ -267,6 +318,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     }
     return;
   }
+  // this CTA's prefetched bytes below the boundary bucket (every eligible non-resident there is
+  // prefetched, R2); the tie group's kept non-residents are added in P34.  Then R turns into
+  // the code stashes: the first chunk P34 decodes (the highest) is copied in meanwhile.
+  unsigned long long h2d = 0;
+  for (uint32_t b = threadIdx.x; b < bs; b += FT) h2d += ((unsigned long long)nrb[NB1 + b] << 16) + nrb[b];
+  const uint32_t n_chunks = (tw_here + BIG_CW - 1) / BIG_CW;
+  __syncthreads();
+  if (n_chunks) stash_chunk(R, codes, tw_here, (int)n_chunks - 1);
   // preceding CTAs' bytes at D* (tie prefix), and this CTA's own
   __shared__ unsigned long long sh_town;
   unsigned long long t_rows = 0;
@@ -407,44 +466,71 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   // ---------------- P34: chunks of words from the highest id down
   PROBE(unsigned long long dta = 0, dtb = 0, dtc = 0, dtd = 0, tq = gtimer();)  // (dtd: unused)
 #define LAP(v) PROBE(if (threadIdx.x == 0) { const unsigned long long t_ = gtimer(); v += t_ - tq; tq = t_; })
-  unsigned long long h2d = 0, tie_kept = 0, d2h = 0;
+  unsigned long long tie_kept = 0, d2h = 0;
   uint32_t n_el = 0, n_pfb = 0, n_evb = 0;
   unsigned long long above = 0;  // tie bytes of the chunks done (all above this chunk)
   const unsigned long long rem = sel.rem;
-  const uint32_t n_chunks = (tw_here + BIG_CW - 1) / BIG_CW;
   // this CTA's list candidates (HBM scratch of the tile's range): bucket << 20 | kept << 19 | k
   uint32_t *g_lpf = d.sort_ka + base, *g_lev = d.sort_va + base;
   uint32_t n_lpf = 0, n_lev = 0;  // (CTA-uniform)
-  for (int ch = (int)n_chunks - 1; ch >= 0; --ch) {
+  uint32_t buf = 0;  // (two stashes: the current one)
+  for (int ch = (int)n_chunks - 1; ch >= 0; --ch, buf ^= 1u) {
     const uint32_t w0 = (uint32_t)ch * BIG_CW, wn = min(BIG_CW, tw_here - w0);
+    const uint4 wm = threadIdx.x < wn ? wmask[w0 + threadIdx.x] : make_uint4(0, 0, 0, 0);
+#if BIG_NSTASH == 2
+    // the next chunk's codes into the other stash while this one is processed
+    if (ch > 0) {
+      stash_chunk(R + (buf ^ 1u) * BIG_STASH, codes, tw_here, ch - 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      cp_async_wait_all();
+    }
+    const uint8_t *stash = R + buf * BIG_STASH;
+#else
+    if (threadIdx.x == 0) prefetch_chunk_codes(codes, tw_here, ch - 1);  // (L2, for the refill below)
+    cp_async_wait_all();
+    const uint8_t *stash = R;
+#endif
+    __syncthreads();
     // Word w0 + i belongs to thread i in every step of the chunk: its masks stay in registers.
     const uint32_t i = threadIdx.x, w = w0 + i;
+    const uint32_t sw = (i >> 1) & 3u;  // the word's unit swizzle in the stash
     const bool mine = i < wn;
-    // (a) decode the word's codes (32 agents, 64 bytes): eligible, resident, dirty, kept below
-    // the boundary, tie group, prefetch candidates, multi-valued; evict candidates (residents
-    // outside the kept buckets: the evicted ones and the resident ties, which the cut may keep)
-    uint32_t em = 0, rm = 0, ym = 0, lm = 0, tm = 0, pm = 0, mv = 0;
-    unsigned long long tb = 0;  // the word's tie bytes
+    // (a) the word's masks: eligible, resident, dirty, multi-valued (written by P1), below /
+    // at the boundary bucket from its 32 codes, two per 32-bit pair by SWAR: with a guard bit
+    // over each 12-bit bucket q, bit 12 of (q + 4096 - t) is q >= t (no borrow crosses the
+    // halves); pair j holds agents j and j + 16, so one shift puts both bits in place
+    uint32_t em = 0, rm = 0, ym = 0, mv = 0, lm = 0, tm = 0, pm = 0;
+    unsigned long long tb = 0, tbn = 0;  // the word's tie bytes (all, non-resident)
     if (mine) {
-      const uint4 *cw = reinterpret_cast<const uint4 *>(codes + (uint64_t)w * 32);
-      uint4 q4[4];
+      em = wm.x;
+      rm = wm.y;
+      ym = wm.z;
+      mv = wm.w;
+      if (all_fit) {
+        lm = em;
+        pm = em & ~rm & ~mv;
+      } else {
+        const uint32_t B0 = bs * 0x10001u, B1 = (bs + 1u) * 0x10001u;  // (bs < 4096)
+        uint32_t ge0 = 0, ge1 = 0;  // q >= bs, q >= bs + 1
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q4[u] = cw[u];  // (beyond n_here: zero codes, ineligible)
-#pragma unroll
-      for (int l = 0; l < 32; ++l) {
-        const uint32_t word = (&q4[l >> 3].x)[(l >> 1) & 3];
-        const uint32_t code = (l & 1) ? (word >> 16) : (word & 0xFFFFu);
-        const uint32_t q = code & 0xFFFu, bit = 1u << l;
-        const bool e = (code >> 12) & 1u, r = (code >> 13) & 1u;
-        em |= e ? bit : 0u;
-        rm |= r ? bit : 0u;
-        ym |= ((code >> 14) & 1u) ? bit : 0u;
-        lm |= (e && (all_fit || q < bs)) ? bit : 0u;
-        tm |= (e && !all_fit && q == bs) ? bit : 0u;
-        pm |= (e && !r && (all_fit || q <= bs) && !ib_multi(q)) ? bit : 0u;
-        mv |= (e && ib_multi(q)) ? bit : 0u;
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t X = *reinterpret_cast<const uint32_t *>(stash + 16 * ((4 * i + (j >> 2)) ^ sw) + 4 * (j & 3)) |
+                             0x10001000u;
+          const uint32_t g0 = (X - B0) & 0x10001000u, g1 = (X - B1) & 0x10001000u;
+          ge0 |= j <= 12 ? g0 >> (12 - j) : g0 << (j - 12);
+          ge1 |= j <= 12 ? g1 >> (12 - j) : g1 << (j - 12);
+        }
+        lm = em & ~ge0;
+        tm = em & ge0 & ~ge1;
+        pm = em & ~rm & ~ge1 & ~mv;
       }
-      for (uint32_t m = tm; m; m &= m - 1) tb += rec[w * 32 + __ffs(m) - 1].y;  // (ties: few)
+      for (uint32_t m = tm; m; m &= m - 1) {  // (ties: few)
+        const int l = __ffs(m) - 1;
+        const uint32_t fp = rec[w * 32 + l].y;
+        tb += fp;
+        if (!((rm >> l) & 1u)) tbn += fp;
+      }
     }
     const uint32_t ec = rm & ~lm & ~mv;  // evict candidates
     LAP(dta)
@@ -471,6 +557,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         if (hi <= rem) {
           kw |= tm;
           tie_kept += tb;
+          h2d += tbn;
         } else if (lo <= rem) {  // the straddling word: its ties in id order
           unsigned long long incl = lo;
           for (uint32_t m = tm; m; m &= m - 1) {
@@ -480,6 +567,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
             if (incl <= rem) {
               kw |= 1u << l;
               tie_kept += fp;
+              if (!((rm >> l) & 1u)) h2d += fp;
             }
           }
         }
@@ -489,29 +577,19 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       n_el += __popc(em);
       n_pfb += __popc(pfw & tm);
       n_evb += __popc(evw & tm);
-      // footprints of the prefetched agents and write-back bytes of the dirty evicted ones: up
-      // to two of each per round trip (most words have none or one)
-      uint32_t mp = pfw, me = evw & ym;
-      while (mp | me) {
-        uint32_t v0 = 0, v1 = 0, u0 = 0, u1 = 0;
-        if (mp) {
-          v0 = rec[w * 32 + __ffs(mp) - 1].y;
-          mp &= mp - 1;
+      // write-back bytes of the dirty evicted agents: up to four per round trip (most words have
+      // none or one)
+      for (uint32_t me = evw & ym; me;) {
+        uint32_t u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          u[k] = 0;
+          if (me) {
+            u[k] = d.wb_bytes[base + w * 32 + __ffs(me) - 1];
+            me &= me - 1;
+          }
         }
-        if (mp) {
-          v1 = rec[w * 32 + __ffs(mp) - 1].y;
-          mp &= mp - 1;
-        }
-        if (me) {
-          u0 = d.wb_bytes[base + w * 32 + __ffs(me) - 1];
-          me &= me - 1;
-        }
-        if (me) {
-          u1 = d.wb_bytes[base + w * 32 + __ffs(me) - 1];
-          me &= me - 1;
-        }
-        h2d += (unsigned long long)v0 + v1;
-        d2h += (unsigned long long)u0 + u1;
+        d2h += (unsigned long long)u[0] + u[1] + u[2] + u[3];
       }
       // (d) the word's candidates appended in descending id order to this CTA's two candidate
       // lists (HBM scratch, placed once after the last chunk), each with its kept bit; four
@@ -529,7 +607,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
           if (m) {
             bt[u] = 31 - __clz(m);
             m &= ~(1u << bt[u]);
-            cd[u] = codes[wbase + bt[u]];
+            const uint32_t pos = ((bt[u] & 15u) << 1) | (bt[u] >> 4);  // (the code's place in the word)
+            cd[u] = *reinterpret_cast<const uint16_t *>(stash + 16 * ((4 * i + (pos >> 3)) ^ sw) + 2 * (pos & 7u));
           }
         }
 #pragma unroll
@@ -544,8 +623,11 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     n_lpf += tcp;
     n_lev += tce;
     LAP(dtc)
+    __syncthreads();  // (the stash is refilled; the placement reads every thread's candidates)
+#if BIG_NSTASH == 1
+    if (ch > 0) stash_chunk(R, codes, tw_here, ch - 1);
+#endif
   }
-  __syncthreads();  // (the placement reads every thread's candidates)
   PROBE(if (threadIdx.x == 0) {
     atomicMax(&prof[22], dta);
     atomicMax(&prof[23], dtb);
@@ -556,7 +638,43 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   // bucket); a candidate's rank in its bucket = sorted index - the bucket's first index; evict
   // positions count up from the bucket's cursor, prefetch positions down from its last one
   // (only kept candidates are members)
-  {
+  // Up to BIG_STASH / 4 candidates of both lists (the usual case): staged in shared memory in
+  // list order, then one warp per list walks them 32 at a time, the members of a bucket among
+  // the 32 ranked by __match_any_sync, the bucket cursor advanced by their count.
+  const uint32_t *cur_pf = h32, *cur_ev = h32 + NB1;
+  auto place = [&](uint32_t x, uint32_t pos, bool pf) {  // x: a member's candidate entry
+    if (pos >= p.n_local) {  // (cannot happen: flagged instead of writing out of bounds)
+#ifdef DEBUG_SYNC
+      atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), 1u << 20);
+#endif
+      atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), ST_SYNC);
+      return;
+    }
+    (pf ? d.pf_ids : d.ev_ids)[pos] = (uint32_t)(p.shard_begin + base + (x & 0x7FFFFu));
+  };
+  if (n_lpf + n_lev <= BIG_NSTASH * BIG_STASH / 4) {
+    uint32_t *sl = reinterpret_cast<uint32_t *>(R);
+    for (uint32_t e = threadIdx.x; e < n_lpf; e += FT) sl[e] = g_lpf[e];
+    for (uint32_t e = threadIdx.x; e < n_lev; e += FT) sl[n_lpf + e] = g_lev[e];
+    __syncthreads();
+    if (warp < 2) {
+      const bool pf = warp == 0;
+      const uint32_t n = pf ? n_lpf : n_lev, *src = sl + (pf ? 0u : n_lpf);
+      uint32_t *cur = h32 + (pf ? 0u : (uint32_t)NB1);
+      for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const uint32_t x = e < n ? src[e] : 0u, b = e < n ? x >> 20 : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b), before = __popc(peers & lanemask_lt());
+        const uint32_t c0 = e < n ? cur[b] : 0u;
+        __syncwarp();
+        if (e < n && before == 0) cur[b] = pf ? c0 - __popc(peers) : c0 + __popc(peers);
+        __syncwarp();
+        // members: kept prefetch candidates, evict candidates the cut does not keep
+        if (e < n && ((x >> 19) & 1u) == (pf ? 1u : 0u)) place(x, pf ? c0 - before : c0 + before, pf);
+      }
+    }
+    __syncthreads();
+  } else {
     uint32_t *start = h + 2 * NB1;  // [NB1] first sorted index per bucket (the counts are no longer needed)
     uint32_t *cnt = reinterpret_cast<uint32_t *>(la);  // 256 x 16 sort counters
     uint32_t *ka = d.sort_kb + base, *ia = d.sort_vb + base, *kb = d.f_sk2 + base, *ib = d.f_sv2 + base;
@@ -573,21 +691,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       for (uint32_t i = threadIdx.x; i < n; i += FT)
         if (i == 0 || ka[i - 1] != ka[i]) start[ka[i]] = i;
       __syncthreads();
-      const uint32_t *cur = h32 + (lst == 0 ? 0u : (uint32_t)NB1);
-      uint32_t *out = lst == 0 ? d.pf_ids : d.ev_ids;
+      const uint32_t *cur = lst == 0 ? cur_pf : cur_ev;
       for (uint32_t i = threadIdx.x; i < n; i += FT) {
-        const uint32_t b = ka[i], rk = i - start[b], x = src[ia[i]], k = x & 0x7FFFFu;
-        const uint32_t pos = lst == 0 ? cur[b] - rk : cur[b] + rk;
-        // members: kept prefetch candidates, evict candidates the cut does not keep
-        if (((x >> 19) & 1u) != (lst == 0 ? 1u : 0u)) continue;
-        if (pos >= p.n_local) {  // (cannot happen: flagged instead of writing out of bounds)
-#ifdef DEBUG_SYNC
-          atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), 1u << 20);
-#endif
-          atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), ST_SYNC);
-          continue;
-        }
-        out[pos] = (uint32_t)(p.shard_begin + base + k);
+        const uint32_t b = ka[i], rk = i - start[b], x = src[ia[i]];
+        if (((x >> 19) & 1u) == (lst == 0 ? 1u : 0u)) place(x, lst == 0 ? cur[b] - rk : cur[b] + rk, lst == 0);
       }
       __syncthreads();
     }
@@ -642,6 +749,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   warp_add_u44(tie_kept, sacc + 8);
   warp_add_u44(d2h, sacc + 6);
   n_el = __reduce_add_sync(0xFFFFFFFFu, n_el);  // (every thread counted its words)
+
   n_pfb = __reduce_add_sync(0xFFFFFFFFu, n_pfb);
   n_evb = __reduce_add_sync(0xFFFFFFFFu, n_evb);
   if (lane == 0) {
