@@ -117,7 +117,6 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_crow = take(4 * 2 * 4096 * (uint64_t)FUSED_MAX_CTAS);
   L.f_ovf = take(16 * 2 * (uint64_t)BIG_OVF_CAP);
   L.big_codes = take(2 * 32 * ((n1 + 31) / 32) + 64);  // (whole words; the stash copies 16-byte units)
-  L.big_wmask = take(16 * ((n1 + 31) / 32));
   L.total = off;
   return L;
 }
@@ -201,7 +200,6 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_crow = (uint32_t *)(b + L.f_crow);
   d.f_ovf = (uint4 *)(b + L.f_ovf);
   d.big_codes = (uint16_t *)(b + L.big_codes);
-  d.big_wmask = (uint4 *)(b + L.big_wmask);
   return d;
 }
 

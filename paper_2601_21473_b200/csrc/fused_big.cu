@@ -128,7 +128,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   const uint32_t *bm_old = d.bm[p.cur];
   uint32_t *bm_new = d.bm[p.cur ^ 1];
   uint16_t *codes = d.big_codes + base;
-  uint4 *wmask = d.big_wmask + (base >> 5);
   const uint4 *rec = p.rec + base;
 
   // ---------------- P1: score, histograms, codes
@@ -201,15 +200,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
           if (jo < LOVF) s_ovf[jo] = make_uint4(bits, (uint32_t)(p.shard_begin + base + k), res ? 1u : 0u, 0u);
         }
       }
-      // the word's masks (one 16-byte store per 32 agents) and the agent's bucket; within a word
-      // lane l's code sits at 2 (l % 16) + l / 16, so that 32-bit pair j of the word holds
-      // agents j and j + 16 (P34 decodes pairs into masks without a bit permutation)
-      const uint32_t emw = __ballot_sync(0xFFFFFFFFu, elig), rmw = __ballot_sync(0xFFFFFFFFu, res);
-      const uint32_t ymw = __ballot_sync(0xFFFFFFFFu, valid && ((rj.z >> 4) & 1u));
-      const uint32_t mvw = __ballot_sync(0xFFFFFFFFu, elig && ib_multi(q));
-      if (lane == 0 && (!CHECK || k < nk)) wmask[k >> 5] = make_uint4(emw, rmw, ymw, mvw);  // (the tile's words only)
+      // the agent's code: bucket | eligible << 12 | dirty << 13; within a word lane l's code sits
+      // at 2 (l % 16) + l / 16, so that 32-bit pair j of the word holds agents j and j + 16
+      // (P34 decodes pairs into masks without a bit permutation)
       if (valid) {
-        codes[(k & ~31u) | ((lane & 15) << 1) | (lane >> 4)] = (uint16_t)q;
+        codes[(k & ~31u) | ((lane & 15) << 1) | (lane >> 4)] =
+            (uint16_t)(q | (elig ? 1u << 12 : 0u) | (((rj.z >> 4) & 1u) << 13));
         if (!FAST && gkeys) gkeys[k] = bits;
       }
     };
@@ -473,10 +469,11 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   // this CTA's list candidates (HBM scratch of the tile's range): bucket << 20 | kept << 19 | k
   uint32_t *g_lpf = d.sort_ka + base, *g_lev = d.sort_va + base;
   uint32_t n_lpf = 0, n_lev = 0;  // (CTA-uniform)
+  const bool cta_mv = s_novf > 0;  // this CTA holds eligible agents in multi-valued buckets
   uint32_t buf = 0;  // (two stashes: the current one)
   for (int ch = (int)n_chunks - 1; ch >= 0; --ch, buf ^= 1u) {
     const uint32_t w0 = (uint32_t)ch * BIG_CW, wn = min(BIG_CW, tw_here - w0);
-    const uint4 wm = threadIdx.x < wn ? wmask[w0 + threadIdx.x] : make_uint4(0, 0, 0, 0);
+    const uint32_t rmw = threadIdx.x < wn ? bm_old[(base >> 5) + w0 + threadIdx.x] : 0u;  // (issued before the wait)
 #if BIG_NSTASH == 2
     // the next chunk's codes into the other stash while this one is processed
     if (ch > 0) {
@@ -496,35 +493,49 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     const uint32_t i = threadIdx.x, w = w0 + i;
     const uint32_t sw = (i >> 1) & 3u;  // the word's unit swizzle in the stash
     const bool mine = i < wn;
-    // (a) the word's masks: eligible, resident, dirty, multi-valued (written by P1), below /
-    // at the boundary bucket from its 32 codes, two per 32-bit pair by SWAR: with a guard bit
-    // over each 12-bit bucket q, bit 12 of (q + 4096 - t) is q >= t (no borrow crosses the
-    // halves); pair j holds agents j and j + 16, so one shift puts both bits in place
-    uint32_t em = 0, rm = 0, ym = 0, mv = 0, lm = 0, tm = 0, pm = 0;
+    // (a) the word's masks from its 32 codes, two per 32-bit pair by SWAR: eligible (bit 12 of
+    // each half); with a guard bit over each 12-bit bucket q, bit 12 of (q + 4096 - t) is
+    // q >= t (no borrow crosses the halves): below / at the boundary bucket, and the multi-valued
+    // range [2048, 3920) where this CTA has such agents; pair j holds agents j and j + 16, so
+    // one shift puts both bits in place.  Resident: the old residency word.
+    uint32_t em = 0, rm = 0, mv = 0, lm = 0, tm = 0, pm = 0;
     unsigned long long tb = 0, tbn = 0;  // the word's tie bytes (all, non-resident)
     if (mine) {
-      em = wm.x;
-      rm = wm.y;
-      ym = wm.z;
-      mv = wm.w;
+      rm = rmw;
+      auto pair = [&](int j) {
+        return *reinterpret_cast<const uint32_t *>(stash + 16 * ((4 * i + (j >> 2)) ^ sw) + 4 * (j & 3));
+      };
+      constexpr uint32_t G12 = 0x10001000u;
+#define SWAR_SH(v, j) ((j) <= 12 ? (v) >> (12 - (j)) : (v) << ((j) - 12))
       if (all_fit) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) em |= SWAR_SH(pair(j) & G12, j);
         lm = em;
-        pm = em & ~rm & ~mv;
       } else {
         const uint32_t B0 = bs * 0x10001u, B1 = (bs + 1u) * 0x10001u;  // (bs < 4096)
         uint32_t ge0 = 0, ge1 = 0;  // q >= bs, q >= bs + 1
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const uint32_t X = *reinterpret_cast<const uint32_t *>(stash + 16 * ((4 * i + (j >> 2)) ^ sw) + 4 * (j & 3)) |
-                             0x10001000u;
-          const uint32_t g0 = (X - B0) & 0x10001000u, g1 = (X - B1) & 0x10001000u;
-          ge0 |= j <= 12 ? g0 >> (12 - j) : g0 << (j - 12);
-          ge1 |= j <= 12 ? g1 >> (12 - j) : g1 << (j - 12);
+          const uint32_t W = pair(j), X = (W & 0x0FFF0FFFu) | G12;
+          em |= SWAR_SH(W & G12, j);
+          ge0 |= SWAR_SH((X - B0) & G12, j);
+          ge1 |= SWAR_SH((X - B1) & G12, j);
         }
         lm = em & ~ge0;
         tm = em & ge0 & ~ge1;
-        pm = em & ~rm & ~ge1 & ~mv;
       }
+      if (cta_mv) {  // (CTA-uniform, rare)
+        uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t X = (pair(j) & 0x0FFF0FFFu) | G12;
+          m0 |= SWAR_SH((X - (uint32_t)IB_EXACT * 0x10001u) & G12, j);
+          m1 |= SWAR_SH((X - (uint32_t)IB_INF * 0x10001u) & G12, j);
+        }
+        mv = em & m0 & ~m1;
+      }
+#undef SWAR_SH
+      pm = em & ~rm & ~mv & (all_fit ? 0xFFFFFFFFu : (lm | tm));
       for (uint32_t m = tm; m; m &= m - 1) {  // (ties: few)
         const int l = __ffs(m) - 1;
         const uint32_t fp = rec[w * 32 + l].y;
@@ -579,7 +590,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       n_evb += __popc(evw & tm);
       // write-back bytes of the dirty evicted agents: up to four per round trip (most words have
       // none or one)
-      for (uint32_t me = evw & ym; me;) {
+      uint32_t me = 0;  // the dirty ones among them (dirty bit of the stashed code)
+      for (uint32_t m = evw; m; m &= m - 1) {
+        const uint32_t l = __ffs(m) - 1, pos = ((l & 15u) << 1) | (l >> 4);
+        if ((*reinterpret_cast<const uint16_t *>(stash + 16 * ((4 * i + (pos >> 3)) ^ sw) + 2 * (pos & 7u)) >> 13) & 1u)
+          me |= 1u << l;
+      }
+      while (me) {
         uint32_t u[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {

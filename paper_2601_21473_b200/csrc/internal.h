@@ -76,7 +76,7 @@ struct Layout {
   uint64_t f_hist1, f_mm1, f_hist2, f_mm2, f_hist3, f_cta_cpf, f_cta_cev, f_tot, f_acc;
   uint64_t f_rows1, f_rows2, f_rows3, f_cta_lmm;
   uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes, params_dev;
-  uint64_t f_pos, f_rt, f_crow, f_ovf, big_codes, big_wmask;
+  uint64_t f_pos, f_rt, f_crow, f_ovf, big_codes;
   uint64_t total;
 };
 
@@ -133,8 +133,7 @@ struct Dev {
   unsigned long long *f_pos;   // [2][4096][FUSED_MAX_CTAS] bucket owners' list offsets per (bucket, CTA), epoch-tagged
   unsigned long long *f_rt;    // [2][FUSED_MAX_CTAS] bucket owners' range totals, epoch-tagged
   uint4 *f_ovf;                // [2][BIG_OVF_CAP] eligible agents in multi-valued buckets: {key, id, resident, 0}
-  uint16_t *big_codes;         // [n_words * 32] large contexts (fused_big.cu): level-1 bucket per agent (lanes of a word permuted, fused_big.cu)
-  uint4 *big_wmask;            // [n_words] large contexts: per 32-agent word {eligible, resident, dirty, multi-valued bucket} masks
+  uint16_t *big_codes;         // [n_words * 32] large contexts (fused_big.cu): bucket | eligible << 12 | dirty << 13 per agent (lanes of a word permuted)
 };
 
 Dev make_dev(void *ws, const Layout &L);
