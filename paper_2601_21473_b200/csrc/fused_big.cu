@@ -655,9 +655,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   // bucket); a candidate's rank in its bucket = sorted index - the bucket's first index; evict
   // positions count up from the bucket's cursor, prefetch positions down from its last one
   // (only kept candidates are members)
-  // Up to BIG_STASH / 4 candidates of both lists (the usual case): staged in shared memory in
-  // list order, then one warp per list walks them 32 at a time, the members of a bucket among
-  // the 32 ranked by __match_any_sync, the bucket cursor advanced by their count.
+  // The sort runs in shared memory (region R: counters + four arrays) when the list fits,
+  // else on HBM scratch.
   const uint32_t *cur_pf = h32, *cur_ev = h32 + NB1;
   auto place = [&](uint32_t x, uint32_t pos, bool pf) {  // x: a member's candidate entry
     if (pos >= p.n_local) {  // (cannot happen: flagged instead of writing out of bounds)
@@ -669,39 +668,30 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     }
     (pf ? d.pf_ids : d.ev_ids)[pos] = (uint32_t)(p.shard_begin + base + (x & 0x7FFFFu));
   };
-  if (n_lpf + n_lev <= BIG_NSTASH * BIG_STASH / 4) {
-    uint32_t *sl = reinterpret_cast<uint32_t *>(R);
-    for (uint32_t e = threadIdx.x; e < n_lpf; e += FT) sl[e] = g_lpf[e];
-    for (uint32_t e = threadIdx.x; e < n_lev; e += FT) sl[n_lpf + e] = g_lev[e];
-    __syncthreads();
-    if (warp < 2) {
-      const bool pf = warp == 0;
-      const uint32_t n = pf ? n_lpf : n_lev, *src = sl + (pf ? 0u : n_lpf);
-      uint32_t *cur = h32 + (pf ? 0u : (uint32_t)NB1);
-      for (uint32_t e0 = 0; e0 < n; e0 += 32) {
-        const uint32_t e = e0 + lane;
-        const uint32_t x = e < n ? src[e] : 0u, b = e < n ? x >> 20 : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b), before = __popc(peers & lanemask_lt());
-        const uint32_t c0 = e < n ? cur[b] : 0u;
-        __syncwarp();
-        if (e < n && before == 0) cur[b] = pf ? c0 - __popc(peers) : c0 + __popc(peers);
-        __syncwarp();
-        // members: kept prefetch candidates, evict candidates the cut does not keep
-        if (e < n && ((x >> 19) & 1u) == (pf ? 1u : 0u)) place(x, pf ? c0 - before : c0 + before, pf);
-      }
-    }
-    __syncthreads();
-  } else {
+  {
+    constexpr uint32_t SMAX = (BIG_NSTASH * BIG_STASH / 4 - 256 * SW) / 4;  // entries sortable in R
     uint32_t *start = h + 2 * NB1;  // [NB1] first sorted index per bucket (the counts are no longer needed)
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(la);  // 256 x 16 sort counters
-    uint32_t *ka = d.sort_kb + base, *ia = d.sort_vb + base, *kb = d.f_sk2 + base, *ib = d.f_sv2 + base;
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(R);  // 256 x SW sort counters
     for (int lst = 0; lst < 2; ++lst) {
       const uint32_t n = lst == 0 ? n_lpf : n_lev;
       if (n == 0) continue;  // (CTA-uniform)
       const uint32_t *src = lst == 0 ? g_lpf : g_lev;
+      uint32_t *ka, *ia, *kb, *ib;  // keys (buckets) and values (the entries)
+      if (n <= SMAX) {
+        ka = cnt + 256 * SW;
+        ia = ka + SMAX;
+        kb = ia + SMAX;
+        ib = kb + SMAX;
+      } else {
+        ka = d.sort_kb + base;
+        ia = d.sort_vb + base;
+        kb = d.f_sk2 + base;
+        ib = d.f_sv2 + base;
+      }
       for (uint32_t e = threadIdx.x; e < n; e += FT) {
-        ka[e] = src[e] >> 20;
-        ia[e] = e;
+        const uint32_t x = src[e];
+        ka[e] = x >> 20;
+        ia[e] = x;
       }
       __syncthreads();
       cta_sort_pairs(ka, ia, kb, ib, n, cnt);
@@ -710,7 +700,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       __syncthreads();
       const uint32_t *cur = lst == 0 ? cur_pf : cur_ev;
       for (uint32_t i = threadIdx.x; i < n; i += FT) {
-        const uint32_t b = ka[i], rk = i - start[b], x = src[ia[i]];
+        const uint32_t b = ka[i], rk = i - start[b], x = ia[i];
+        // members: kept prefetch candidates, evict candidates the cut does not keep
         if (((x >> 19) & 1u) == (lst == 0 ? 1u : 0u)) place(x, lst == 0 ? cur[b] - rk : cur[b] + rk, lst == 0);
       }
       __syncthreads();
