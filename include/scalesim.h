@@ -104,7 +104,30 @@ typedef enum {
                                        single-kernel plan, floor(SMs / world) CTAs per rank, the
                                        exchange of the global cut through the ranks' workspaces
                                        after a world-wide barrier.  Shards must be
-                                       contiguous, in rank order and cover [0, n_agents). */
+                                       contiguous, in rank order and cover [0, n_agents).
+                                       Interaction agents (n_kin > 0) are allowed: each rank's
+                                       pair scan runs over the world's participants, gathered
+                                       from every rank's kinematics through device memory
+                                       (SURVEY §8(e) "all-gather of kin for active INT agents";
+                                       exact all-pairs, Eq. 2).  The ranks of
+                                       one world must agree on n_kin > 0 (the distance class mix
+                                       decides the histogram layout). */
+#define SCALESIM_F_TP_SLICED 64u    /* with SCALESIM_F_LOOPBACK and transfers: tensor-parallel
+                                       agent memory (§4.2: "All multi-GPU setups
+                                       use tensor parallelism"; reading R16).  Every rank holds
+                                       slice `rank` (bytes [rank * page_bytes / world, +
+                                       page_bytes / world)) of every resident page, so the block
+                                       tables of every rank cover ALL n_agents agents (blk_ptr has
+                                       n_agents + 1 entries) and a device page slot is
+                                       page_bytes / world bytes (dev_bytes / slot slots, at least
+                                       ceil(budget / page_bytes)).  Per step the ranks' lists are
+                                       merged into the world's lists in every rank (SURVEY §8(e)
+                                       step 4, the all-gather of per-rank lists), every rank
+                                       assigns the pages of the whole plan (the same FIFO pool
+                                       evolution on every rank) and copies its slice of each
+                                       listed page.  Requires page_bytes % (16 * world) == 0 and
+                                       no resident_init.  The merged lists and their transfer
+                                       header: scalesim_world_view. */
 
 /* Agent record: 4 x uint32 per agent, 16-byte aligned, one 128-bit load.
  *   [0] t_next : action-end tick (ACTING independent / interaction agents), or remaining hop
@@ -142,7 +165,7 @@ typedef struct {
   const uint32_t *agent_rec;    /* 4 * n_local uint32, n_local = shard_end - shard_begin, 16-B aligned */
   const float *agent_kin;       /* 4 * n_kin float, 16-B aligned; may be NULL when n_kin == 0 */
   /* device, read-only after init: CSR agent -> memory blocks (local agents) */
-  const uint64_t *blk_ptr;      /* n_local + 1 */
+  const uint64_t *blk_ptr;      /* n_local + 1 (SCALESIM_F_TP_SLICED: n_agents + 1, every agent) */
   const uint32_t *blk_size;     /* n_blocks, multiples of page_bytes */
   const uint64_t *blk_host_off; /* n_blocks, byte offset of the block in host_arena (page aligned) */
   const uint8_t *blk_kind;      /* n_blocks, 0 LORA / 1 KV / 2 HIST */
@@ -246,6 +269,21 @@ scalesim_status scalesim_step_batch(scalesim_ctx *const *ctxs, uint32_t n, int64
  * world-wide, the other header fields the rank's.  plan(world) == plan(1) restricted to the
  * shard (tests/test_gpu_world.py).  Errors: SCALESIM_E_INVALID for a malformed world. */
 scalesim_status scalesim_step_group(scalesim_ctx *const *ctxs, uint32_t world, int64_t now_tick);
+
+/* The world's merged plan of a SCALESIM_F_TP_SLICED rank after its last step (device views into
+ * the workspace, overwritten by the next step): prefetch_ids (ascending (distance, id)) and
+ * evict_ids (descending), identical in every rank and equal to the world-1 plan's lists
+ * (Table 1 Evict / DispatchLoadTasks); header: SCALESIM_H_N_PREFETCH /
+ * _N_EVICT (the world's counts), SCALESIM_H_N_D2H / _N_H2D (pages of the whole plan; this rank
+ * moves its slice of each), SCALESIM_H_BYTES_D2H (the world's write-back bytes, R13).  The
+ * rank's own header (scalesim_view) keeps its shard's plan and carries the page counts.
+ * Errors: SCALESIM_E_INVALID (NULL, not TP-sliced), SCALESIM_E_ORDER (before the first step). */
+typedef struct {
+  const uint32_t *prefetch_ids;
+  const uint32_t *evict_ids;
+  const uint64_t *header;  /* SCALESIM_H_* fields as above */
+} scalesim_world_view_t;
+scalesim_status scalesim_world_view(scalesim_ctx *ctx, scalesim_world_view_t *out);
 
 /* ---- NEXT #2: the preemptive priority load scheduler (App. A "Load task scheduler"
  * and "Preemption support"; SPEC.md S:291-293, S:324-327, S:348-356, S:366-374;

@@ -17,6 +17,7 @@ F_MULTI_KERNEL = 4
 F_EXPLICIT_DIST = 8
 F_EXCLUSIVE = 16
 F_LOOPBACK = 32
+F_TP_SLICED = 64
 
 ST_INSUFFICIENT = 1
 ST_BAD_RECORD = 2
@@ -33,7 +34,7 @@ HEADER_NAMES = ["n_prefetch", "n_evict", "bytes_h2d", "bytes_d2h", "cut_bits", "
 
 # Every symbol include/scalesim.h declares (checked by tests/test_abi.py).
 EXPORTS = ["scalesim_workspace_bytes", "scalesim_init", "scalesim_score", "scalesim_plan",
-           "scalesim_transfer", "scalesim_view", "scalesim_step", "scalesim_step_batch", "scalesim_step_group", "scalesim_step_host", "scalesim_set_inputs",
+           "scalesim_transfer", "scalesim_view", "scalesim_step", "scalesim_step_batch", "scalesim_step_group", "scalesim_world_view", "scalesim_step_host", "scalesim_set_inputs",
            "scalesim_sync", "scalesim_join", "scalesim_nccl_unique_id", "scalesim_fused", "scalesim_profile_stamps", "scalesim_object_min", "scalesim_lru_records", "scalesim_bfs_scratch_bytes", "scalesim_bfs_hops", "scalesim_sched_scratch_bytes", "scalesim_sched_run", "scalesim_launch_count", "scalesim_destroy",
            "scalesim_strerror"]
 
@@ -60,6 +61,10 @@ class Tables(C.Structure):
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
         ("resident_init", C.c_void_p),
     ]
+
+
+class WorldView(C.Structure):
+    _fields_ = [("prefetch_ids", C.c_void_p), ("evict_ids", C.c_void_p), ("header", C.c_void_p)]
 
 
 class PlanView(C.Structure):
@@ -113,6 +118,8 @@ def lib():
         L.scalesim_step_batch.restype = C.c_int
         L.scalesim_step_group.argtypes = [C.POINTER(vp), C.c_uint32, i64]
         L.scalesim_step_group.restype = C.c_int
+        L.scalesim_world_view.argtypes = [vp, C.POINTER(WorldView)]
+        L.scalesim_world_view.restype = C.c_int
         L.scalesim_step_host.argtypes = [vp, i64, vp, vp, C.POINTER(PlanHost), vp, vp]
         L.scalesim_step_host.restype = C.c_int
         L.scalesim_set_inputs.argtypes = [vp, vp, vp]

@@ -21,7 +21,8 @@ namespace ss {
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t n_block_pages,
-                   uint64_t n_dev_pages, uint64_t world, bool transfer) {
+                   uint64_t n_dev_pages, uint64_t world, bool transfer, uint64_t n_tab, uint64_t n_wkin, bool tp) {
+  if (n_tab < n_local) n_tab = n_local;
   Layout L = {};
   L.n_local = n_local;
   L.n_words = (n_local + 31) / 32;
@@ -33,7 +34,7 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.desc_cap = transfer ? (n_block_pages < n_dev_pages ? n_block_pages : n_dev_pages) : 0;
   L.world = world;
   L.max_sort_chunks = (n_local + SORT_CH - 1) / SORT_CH + 1;
-  L.max_exp_chunks = (n_local + EXP_CH - 1) / EXP_CH + 1;
+  L.max_exp_chunks = ((tp ? n_tab : n_local) + EXP_CH - 1) / EXP_CH + 1;  // (TP: the merged lists)
   uint64_t off = 0;
   auto take = [&](uint64_t bytes) {
     uint64_t o = off;
@@ -117,6 +118,15 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.f_crow = take(4 * 2 * 4096 * (uint64_t)FUSED_MAX_CTAS);
   L.f_ovf = take(16 * 2 * (uint64_t)BIG_OVF_CAP);
   L.big_codes = take(2 * 32 * ((n1 + 31) / 32) + 64);  // (whole words; the stash copies 16-byte units)
+  L.wkin = take(16 * (n_wkin ? n_wkin : 1));
+  L.wcnt = take(4 * (FUSED_MAX_WORLD + 1));
+  const uint64_t tn = tp ? n_tab : 1, tl = tp ? n1 : 1;
+  L.tp_pf = take(4 * tn);
+  L.tp_ev = take(4 * tn);
+  L.tp_dirty = take(tn);
+  L.tp_hdr = take(8 * H_FIELDS);
+  L.tp_kpf = take(4 * tl);
+  L.tp_kev = take(4 * tl);
   L.total = off;
   return L;
 }
@@ -200,6 +210,14 @@ Dev make_dev(void *ws, const Layout &L) {
   d.f_crow = (uint32_t *)(b + L.f_crow);
   d.f_ovf = (uint4 *)(b + L.f_ovf);
   d.big_codes = (uint16_t *)(b + L.big_codes);
+  d.wkin = (float4 *)(b + L.wkin);
+  d.wcnt = (uint32_t *)(b + L.wcnt);
+  d.tp_pf = (uint32_t *)(b + L.tp_pf);
+  d.tp_ev = (uint32_t *)(b + L.tp_ev);
+  d.tp_dirty = (uint8_t *)(b + L.tp_dirty);
+  d.tp_hdr = (unsigned long long *)(b + L.tp_hdr);
+  d.tp_kpf = (uint32_t *)(b + L.tp_kpf);
+  d.tp_kev = (uint32_t *)(b + L.tp_kev);
   return d;
 }
 
@@ -307,11 +325,16 @@ static scalesim_status validate_config(const scalesim_config *c) {
   if (c->n_agents > 0xFFFFFFFFull) return SCALESIM_E_INVALID;  // ids are uint32
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return SCALESIM_E_INVALID;
   if (c->world == 1 && (c->shard_begin != 0 || c->shard_end != c->n_agents)) return SCALESIM_E_INVALID;
-  if (c->world > 1 && c->n_kin > 0) return SCALESIM_E_INVALID;  // interaction agents: single rank
+  // interaction agents at world > 1: the kinematics all-gather of a loopback world
+  if (c->world > 1 && c->n_kin > 0 && !(c->flags & SCALESIM_F_LOOPBACK)) return SCALESIM_E_INVALID;
   if ((c->flags & SCALESIM_F_LOOPBACK) && (c->world < 2 || c->world > (int)FUSED_MAX_WORLD)) return SCALESIM_E_INVALID;
+  if ((c->flags & SCALESIM_F_TP_SLICED) &&
+      (!(c->flags & SCALESIM_F_LOOPBACK) || (c->flags & SCALESIM_F_NO_TRANSFER) || c->page_bytes % (16ull * c->world) != 0))
+    return SCALESIM_E_INVALID;
   if ((c->flags & SCALESIM_F_EXPLICIT_DIST) && c->n_kin > 0) return SCALESIM_E_INVALID;
   if (c->flags & ~(uint32_t)(SCALESIM_F_NO_TRANSFER | SCALESIM_F_KEEP_DIST | SCALESIM_F_MULTI_KERNEL |
-                             SCALESIM_F_EXPLICIT_DIST | SCALESIM_F_EXCLUSIVE | SCALESIM_F_LOOPBACK))
+                             SCALESIM_F_EXPLICIT_DIST | SCALESIM_F_EXCLUSIVE | SCALESIM_F_LOOPBACK |
+                             SCALESIM_F_TP_SLICED))
     return SCALESIM_E_INVALID;
   for (int k = 0; k < 3; ++k)
     if (std::isnan(c->theta[k]) || c->theta[k] < 0.0f) return SCALESIM_E_INVALID;
@@ -322,13 +345,21 @@ static scalesim_status validate_config(const scalesim_config *c) {
   return SCALESIM_OK;
 }
 
+// the context's layout: block tables over the shard (or, TP-sliced, over every agent), device
+// page slots of page_bytes (TP-sliced: page_bytes / world, every rank holding one slice)
+static Layout layout_of(const scalesim_config *cfg, const scalesim_tables *t) {
+  const bool transfer = !(cfg->flags & SCALESIM_F_NO_TRANSFER), tp = (cfg->flags & SCALESIM_F_TP_SLICED) != 0;
+  const uint64_t n_local = cfg->shard_end - cfg->shard_begin;
+  const uint64_t slot = tp ? cfg->page_bytes / cfg->world : cfg->page_bytes;
+  const uint64_t n_dev_pages = transfer ? t->dev_bytes / slot : 0;
+  const uint64_t n_wkin = (cfg->world > 1 && cfg->n_kin > 0) ? cfg->n_agents : 0;
+  return make_layout(n_local, cfg->n_kin, t->n_blocks, t->n_block_pages, n_dev_pages, cfg->world, transfer,
+                     tp ? cfg->n_agents : n_local, n_wkin, tp);
+}
+
 extern "C" uint64_t scalesim_workspace_bytes(const scalesim_config *cfg, const scalesim_tables *t) {
   if (validate_config(cfg) != SCALESIM_OK || !t) return 0;
-  const bool transfer = !(cfg->flags & SCALESIM_F_NO_TRANSFER);
-  const uint64_t n_local = cfg->shard_end - cfg->shard_begin;
-  const uint64_t n_dev_pages = transfer ? t->dev_bytes / cfg->page_bytes : 0;
-  Layout L = make_layout(n_local, cfg->n_kin, t->n_blocks, t->n_block_pages, n_dev_pages, cfg->world, transfer);
-  return L.total;
+  return layout_of(cfg, t).total;
 }
 
 extern "C" const char *scalesim_strerror(scalesim_status s) {
@@ -374,15 +405,19 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
   if (cfg->n_kin > 0 && (!t->agent_kin || !aligned(t->agent_kin, 16))) return SCALESIM_E_INVALID;
   if (!t->blk_ptr || (t->n_blocks > 0 && (!t->blk_size || !t->blk_kind || !t->blk_host_off))) return SCALESIM_E_INVALID;
   if (!t->workspace || !aligned(t->workspace, 256)) return SCALESIM_E_INVALID;
+  const bool tp = (cfg->flags & SCALESIM_F_TP_SLICED) != 0;
+  const uint64_t slot = tp ? cfg->page_bytes / cfg->world : cfg->page_bytes;
+  const uint64_t n_tab = tp ? cfg->n_agents : n_local;  // agents the block tables cover
+  if (tp && t->resident_init) return SCALESIM_E_INVALID;  // (TP-sliced worlds start empty)
   uint64_t n_dev_pages = 0;
   if (transfer) {
     if (!t->dev_arena || !t->host_arena) return SCALESIM_E_INVALID;
     if (!aligned(t->dev_arena, 16) || !aligned(t->host_arena, 16)) return SCALESIM_E_INVALID;
-    n_dev_pages = t->dev_bytes / cfg->page_bytes;
+    n_dev_pages = t->dev_bytes / slot;
     const uint64_t need = (cfg->budget_bytes + cfg->page_bytes - 1) / cfg->page_bytes;
     if (n_dev_pages < need || n_dev_pages > 0xFFFFFFFFull) return SCALESIM_E_INVALID;
   }
-  Layout L = make_layout(n_local, cfg->n_kin, t->n_blocks, t->n_block_pages, n_dev_pages, cfg->world, transfer);
+  Layout L = layout_of(cfg, t);
   if (t->workspace_bytes < L.total) return SCALESIM_E_INVALID;
 
   CK(cudaSetDevice(cfg->device));
@@ -412,6 +447,11 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
 
   Params &p = c->p;
   p.n_local = n_local;
+  p.n_agents = cfg->n_agents;
+  p.slot_bytes = slot;
+  p.slice_off = tp ? (uint64_t)cfg->rank * slot : 0;
+  p.tp = tp ? 1 : 0;
+  p.ev_dirty = nullptr;
   p.n_words = L.n_words;
   p.n_kin = cfg->n_kin;
   p.n_tiles = L.n_tiles;
@@ -442,11 +482,11 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
 
   // Host-side validation of the block table: sizes are page multiples, CSR is monotone,
   // n_block_pages matches; page_first (prefix of pages per block) goes to the workspace.
-  std::vector<uint64_t> bp(n_local + 1);
-  if (cudaMemcpy(bp.data(), t->blk_ptr, 8 * (n_local + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+  std::vector<uint64_t> bp(n_tab + 1);
+  if (cudaMemcpy(bp.data(), t->blk_ptr, 8 * (n_tab + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(SCALESIM_E_CUDA);
-  if (bp[0] != 0 || bp[n_local] != t->n_blocks) return fail(SCALESIM_E_INVALID);
-  for (uint64_t a = 0; a < n_local; ++a)
+  if (bp[0] != 0 || bp[n_tab] != t->n_blocks) return fail(SCALESIM_E_INVALID);
+  for (uint64_t a = 0; a < n_tab; ++a)
     if (bp[a + 1] < bp[a]) return fail(SCALESIM_E_INVALID);
   std::vector<uint64_t> pf(t->n_blocks + 1, 0);
   if (t->n_blocks > 0) {
@@ -475,9 +515,10 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
     if (cudaMemcpy(bs.data(), t->blk_size, 4 * t->n_blocks, cudaMemcpyDeviceToHost) != cudaSuccess ||
         cudaMemcpy(bk.data(), t->blk_kind, t->n_blocks, cudaMemcpyDeviceToHost) != cudaSuccess)
       return fail(SCALESIM_E_CUDA);
+    const uint64_t a0 = tp ? cfg->shard_begin : 0;  // (TP-sliced: global tables)
     for (uint64_t a = 0; a < n_local; ++a) {
       uint64_t s = 0;
-      for (uint64_t b = bp[a]; b < bp[a + 1]; ++b)
+      for (uint64_t b = bp[a0 + a]; b < bp[a0 + a + 1]; ++b)
         if (bk[b] != 0) s += bs[b];
       if (s > 0xFFFFFFFFull) return fail(SCALESIM_E_INVALID);
       wb[a] = (uint32_t)s;
@@ -740,7 +781,8 @@ static scalesim_status finish_plan(scalesim_ctx *c, scalesim_plan_view *out) {
   }
   // byte accounting (multi-kernel path) and page assignment (transfers); the fused kernel
   // accounts the write-back bytes itself
-  if (c->transfer || !c->last_fused) c->launches += launch_expand(p, c->stream);
+  // (TP-sliced ranks: the expansion of the world's merged lists ran in scalesim_step_group)
+  if ((c->transfer && !p.tp) || !c->last_fused) c->launches += launch_expand(p, c->stream);
   // the transfer's copy streams wait on this event (plan-only contexts record nothing: in a
   // captured graph consecutive plan kernels then stay directly linked, so their programmatic
   // launch overlap is kept)
@@ -890,7 +932,8 @@ extern "C" scalesim_status scalesim_step_group(scalesim_ctx *const *ctxs, uint32
     if (c->stream != c0->stream || c->cfg.device != c0->cfg.device || c->exclusive != c0->exclusive ||
         c->cfg.n_agents != c0->cfg.n_agents || c->cfg.budget_bytes != c0->cfg.budget_bytes ||
         c->cfg.hop_scale != c0->cfg.hop_scale || c->fused_steps != c0->fused_steps ||
-        c->fused_grid != c0->fused_grid || c->p.int_mode != c0->p.int_mode)
+        c->fused_grid != c0->fused_grid || c->p.int_mode != c0->p.int_mode || c->p.tp != c0->p.tp ||
+        c->transfer != c0->transfer || c->p.explicit_dist != c0->p.explicit_dist)
       return SCALESIM_E_INVALID;
     for (int k = 0; k < 3; ++k)
       if (c->cfg.theta[k] != c0->cfg.theta[k]) return SCALESIM_E_INVALID;
@@ -899,14 +942,48 @@ extern "C" scalesim_status scalesim_step_group(scalesim_ctx *const *ctxs, uint32
   }
   if (next != c0->cfg.n_agents) return SCALESIM_E_INVALID;
   CK(cudaGetLastError());
+  const Params *ps[FUSED_MAX_WORLD];
+  bool kin = false;
   for (uint32_t r = 0; r < world; ++r) {
-    scalesim_status s = scalesim_score(ctxs[r], now, nullptr);
-    if (s != SCALESIM_OK) return s;
+    ps[r] = &ctxs[r]->p;
+    kin = kin || ctxs[r]->p.n_kin > 0;
   }
+  // score: every agent is scored inside the plan kernel; the interaction pair scan first needs
+  // the world's participants (§8(e): the all-gather of their kinematics, through device memory)
+  for (uint32_t r = 0; r < world; ++r) {
+    scalesim_ctx *c = ctxs[r];
+    if (c->scored) c->launches += launch_plan_init(c->p, c->stream);
+    c->deferred = true;
+    c->deferred_now = now;
+    c->scored = true;
+  }
+  if (kin) c0->launches += launch_world_interaction(ps, world, now, c0->stream);
   FusedInst insts[FUSED_MAX_WORLD];
   for (uint32_t r = 0; r < world; ++r) insts[r] = fused_inst(ctxs[r], ctxs[r]->fused_tile);
   c0->launches += launch_fused(c0, insts, world, (uint32_t)c0->fused_grid, world);
   CK(cudaGetLastError());
+  if (c0->p.tp && c0->transfer) {
+    // §8(e) step 4: the ranks' lists merged into the world's lists in every rank (all-gather
+    // over device memory), then every rank assigns the pages of the whole plan (the same FIFO
+    // on every rank) and moves its slice of each page
+    c0->launches += launch_tp_merge(ps, world, now, c0->stream);
+    for (uint32_t r = 0; r < world; ++r) {
+      scalesim_ctx *c = ctxs[r];
+      const int buf = (int)(c->step & 1);
+      CK(cudaStreamWaitEvent(c->stream, c->ev_xfer[buf], 0));  // (its descriptor buffer's last reader)
+      Params q = c->p;
+      q.desc_buf = buf;
+      q.shard_begin = 0;
+      q.n_local = c->p.n_agents;
+      q.d.pf_ids = c->p.d.tp_pf;
+      q.d.ev_ids = c->p.d.tp_ev;
+      q.d.header = c->p.d.tp_hdr;
+      q.ev_dirty = c->p.d.tp_dirty;
+      c->launches += launch_expand(q, c->stream);
+      c->launches += launch_tp_finish(c->p, c->stream);
+    }
+    CK(cudaGetLastError());
+  }
   for (uint32_t r = 0; r < world; ++r) {
     scalesim_ctx *c = ctxs[r];
     c->fused_steps++;
@@ -916,6 +993,16 @@ extern "C" scalesim_status scalesim_step_group(scalesim_ctx *const *ctxs, uint32
     if (s != SCALESIM_OK) return s;
     if ((s = scalesim_transfer(c, nullptr)) != SCALESIM_OK) return s;
   }
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_world_view(scalesim_ctx *c, scalesim_world_view_t *out) {
+  if (!c || !out) return SCALESIM_E_INVALID;
+  if (!c->p.tp) return SCALESIM_E_INVALID;
+  if (!c->planned) return SCALESIM_E_ORDER;
+  out->prefetch_ids = c->p.d.tp_pf;
+  out->evict_ids = c->p.d.tp_ev;
+  out->header = reinterpret_cast<const uint64_t *>(c->p.d.tp_hdr);
   return SCALESIM_OK;
 }
 

@@ -77,11 +77,17 @@ struct Layout {
   uint64_t f_rows1, f_rows2, f_rows3, f_cta_lmm;
   uint64_t f_sk2, f_sv2, f_sk3, f_sv3, f_bar, f_prof, wb_bytes, params_dev;
   uint64_t f_pos, f_rt, f_crow, f_ovf, big_codes;
+  // world > 1 on one device (SCALESIM_F_LOOPBACK): the gathered interaction participants of the
+  // world, and (SCALESIM_F_TP_SLICED) the world's merged lists and their transfer header
+  uint64_t wkin, wcnt, tp_pf, tp_ev, tp_dirty, tp_hdr, tp_kpf, tp_kev;
   uint64_t total;
 };
 
+// n_tab: agents the block tables cover (n_local, or n_agents when TP-sliced); n_wkin: capacity of
+// the world's gathered interaction list (0 unless a loopback world has interaction agents)
 Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t n_block_pages,
-                   uint64_t n_dev_pages, uint64_t world, bool transfer);
+                   uint64_t n_dev_pages, uint64_t world, bool transfer, uint64_t n_tab = 0, uint64_t n_wkin = 0,
+                   bool tp = false);
 
 // Pointers derived from the layout.
 struct Dev {
@@ -134,6 +140,13 @@ struct Dev {
   unsigned long long *f_rt;    // [2][FUSED_MAX_CTAS] bucket owners' range totals, epoch-tagged
   uint4 *f_ovf;                // [2][BIG_OVF_CAP] eligible agents in multi-valued buckets: {key, id, resident, 0}
   uint16_t *big_codes;         // [n_words * 32] large contexts (fused_big.cu): bucket | eligible << 12 | dirty << 13 per agent (lanes of a word permuted)
+  // loopback worlds
+  float4 *wkin;                // [n_agents] the world's interaction participants, rank-major (kin all-gather)
+  uint32_t *wcnt;              // [FUSED_MAX_WORLD + 1] rank offsets into wkin, then the world's count
+  uint32_t *tp_pf, *tp_ev;     // [n_agents] the world's merged lists (TP-sliced transfers)
+  uint8_t *tp_dirty;           // [n_agents] dirty bit of each merged evict entry
+  unsigned long long *tp_hdr;  // [H_FIELDS] list counts and transfer fields of the merged plan
+  uint32_t *tp_kpf, *tp_kev;   // [n_local] distance bits of this rank's list entries (merge keys)
 };
 
 Dev make_dev(void *ws, const Layout &L);
@@ -141,6 +154,11 @@ Dev make_dev(void *ws, const Layout &L);
 struct Params {
   // sizes
   uint64_t n_local, n_words, n_kin, n_tiles, shard_begin, budget, page_bytes, n_dev_pages, desc_cap;
+  uint64_t n_agents;
+  // a6 page slots: slot_bytes per device page slot, slice_off = this rank's byte offset within a
+  // page (TP-sliced: page_bytes / world and rank * slot_bytes; otherwise page_bytes and 0)
+  uint64_t slot_bytes, slice_off;
+  const uint8_t *ev_dirty;  // expansion of merged lists: dirty bit per evict entry (else from rec)
   float theta[3];
   float hop_scale;
   int rank, world;
@@ -157,6 +175,7 @@ struct Params {
   int int_mode;   // every distance is an integer or +inf (no interaction class, integral hop_scale)
   int explicit_dist;  // SCALESIM_F_EXPLICIT_DIST: record word 0 holds the distance bits (R19)
   int loopback;       // SCALESIM_F_LOOPBACK: a rank of a world planned in one launch (step_group)
+  int tp;             // SCALESIM_F_TP_SLICED: every rank holds slice `rank` of every resident page
   int cur;  // index of the residency bitmap holding the residency before this plan
   int desc_buf;
   Dev d;
@@ -177,6 +196,11 @@ int launch_transfer(const Params &p, cudaStream_t s, int ctas);
 int launch_transfer_split(const Params &p, cudaStream_t s, cudaStream_t s2, int ctas);
 int launch_init_pages(const Params &p, const uint32_t *resident_init, cudaStream_t s);
 int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s);
+// loopback worlds (kernels.cu): ps[r] = rank r's (host) parameters; the world kernels read the
+// ranks' static fields from their device copies (d.params_dev) and the per-step inputs from ps
+int launch_world_interaction(const Params *const *ps, uint32_t G, int64_t now, cudaStream_t s);
+int launch_tp_merge(const Params *const *ps, uint32_t G, int64_t now, cudaStream_t s);
+int launch_tp_finish(const Params &rank_p, cudaStream_t s);
 bool fused_supported(const Params &p, int grid, uint32_t *tile_out);
 // one instance of a fused launch (see fused.cu)
 struct FusedInst {

@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(NT) k_exp_count(Params p, uint64_t max_chunks)
   unsigned long long wb_bytes = 0;
   if (e < n_ev) {
     const uint32_t a = p.d.ev_ids[e] - (uint32_t)p.shard_begin;
-    const bool dirty = (p.rec[a].z >> 4) & 1u;
+    const bool dirty = p.ev_dirty ? p.ev_dirty[e] != 0 : ((p.rec[a].z >> 4) & 1u);
     agent_pages(p, a, dirty, evp, evw);
     if (dirty)  // R13: KV + HIST blocks of a dirty evicted agent are written back
       for (uint64_t b = p.blk_ptr[a]; b < p.blk_ptr[a + 1]; ++b)
@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(NT) k_pages(Params p, uint64_t max_chunks) {
   bool dirty = false;
   if (e < count) {
     a = (RELEASE ? p.d.ev_ids[e] : p.d.pf_ids[e]) - (uint32_t)p.shard_begin;
-    dirty = RELEASE && ((p.rec[a].z >> 4) & 1u);
+    dirty = RELEASE && (p.ev_dirty ? p.ev_dirty[e] != 0 : ((p.rec[a].z >> 4) & 1u));
     agent_pages(p, a, dirty, pages, wb);
   }
   const unsigned long long ex = block_excl_scan((unsigned long long)pages, &sh_t);
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(NT) k_pages(Params p, uint64_t max_chunks) {
   const uint32_t n_here = min(count - c0, EXP_CH);
   for (uint32_t k = warp; k < n_here; k += NT / 32) {
     const uint32_t ag = (RELEASE ? p.d.ev_ids[c0 + k] : p.d.pf_ids[c0 + k]) - (uint32_t)p.shard_begin;
-    const bool dty = RELEASE && ((p.rec[ag].z >> 4) & 1u);
+    const bool dty = RELEASE && (p.ev_dirty ? p.ev_dirty[c0 + k] != 0 : ((p.rec[ag].z >> 4) & 1u));
     unsigned long long off = sh_off[k];
     unsigned long long woff = sh_wb[k];
     for (uint64_t b = p.blk_ptr[ag]; b < p.blk_ptr[ag + 1]; ++b) {
@@ -829,20 +829,22 @@ __global__ void k_init_page_table(Params p, uint64_t n_block_pages) {
 // in flight across PCIe; the grid is small (the copy overlaps the next plan).
 
 // MODE 0: write-backs (device page -> host), all; MODE 1: loads (host -> device page)
-// [0, n_indep); MODE 2: loads [n_indep, n_h2d) (after the write-backs).
+// [0, n_indep); MODE 2: loads [n_indep, n_h2d) (after the write-backs).  Each descriptor moves
+// `slot` bytes: host page bytes [off, off + slot) <-> device slot pg (slot = page_bytes, off = 0;
+// TP-sliced: this rank's slice of the page).
 template <int MODE>
 __global__ void __launch_bounds__(NT) k_copy_pages(const unsigned long long *desc_base, uint8_t *host, uint8_t *dev,
-                                                  uint64_t page_bytes, uint64_t desc_cap) {
+                                                  uint64_t slot, uint64_t off, uint64_t desc_cap) {
   constexpr bool D2H = MODE == 0;
   const unsigned long long lo = MODE == 2 ? desc_base[2] : 0ull;
   const unsigned long long hi = MODE == 0 ? desc_base[0] : (MODE == 1 ? desc_base[2] : desc_base[1]);
   const unsigned long long *desc = desc_base + DESC_HDR + (D2H ? 0 : 2 * desc_cap);
-  const uint32_t vec_per_page = (uint32_t)(page_bytes / 16);
+  const uint32_t vec_per_page = (uint32_t)(slot / 16);
   for (unsigned long long k = lo + blockIdx.x; k < hi; k += gridDim.x) {
-    const unsigned long long hoff = desc[2 * k];
+    const unsigned long long hoff = desc[2 * k] + off;
     const unsigned long long pg = desc[2 * k + 1];
-    const uint4 *src = reinterpret_cast<const uint4 *>(D2H ? dev + pg * page_bytes : host + hoff);
-    uint4 *dst = reinterpret_cast<uint4 *>(D2H ? host + hoff : dev + pg * page_bytes);
+    const uint4 *src = reinterpret_cast<const uint4 *>(D2H ? dev + pg * slot : host + hoff);
+    uint4 *dst = reinterpret_cast<uint4 *>(D2H ? host + hoff : dev + pg * slot);
     for (uint32_t v0 = 0; v0 < vec_per_page; v0 += NT * 16) {
       uint4 buf[16];
 #pragma unroll
@@ -867,7 +869,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)_
 
 template <int MODE>
 __global__ void __launch_bounds__(32) k_copy_pages_tma(const unsigned long long *desc_base, uint8_t *host, uint8_t *dev,
-                                                      uint64_t page_bytes, uint64_t desc_cap) {
+                                                      uint64_t slot, uint64_t off, uint64_t desc_cap) {
   constexpr bool D2H = MODE == 0;
   extern __shared__ __align__(128) uint8_t tbuf[];
   __shared__ __align__(8) unsigned long long bar[TMA_NB];
@@ -875,7 +877,10 @@ __global__ void __launch_bounds__(32) k_copy_pages_tma(const unsigned long long 
   const unsigned long long lo = MODE == 2 ? desc_base[2] : 0ull;
   const unsigned long long hi = MODE == 0 ? desc_base[0] : (MODE == 1 ? desc_base[2] : desc_base[1]);
   const unsigned long long *desc = desc_base + DESC_HDR + (D2H ? 0 : 2 * desc_cap);
-  const uint32_t cpp = (uint32_t)(page_bytes / TMA_CH);  // chunks per page (page_bytes % 16 KB == 0 here)
+  // chunk size: 16 KB, or the whole slot when it is smaller (slot % 16 == 0, and slot % 16 KB == 0
+  // when larger: checked by the launcher)
+  const uint32_t CH = slot < TMA_CH ? (uint32_t)slot : TMA_CH;
+  const uint32_t cpp = (uint32_t)(slot / CH);  // chunks per slot
   const unsigned long long mine = hi > lo + blockIdx.x ? (hi - lo - blockIdx.x + gridDim.x - 1) / gridDim.x : 0ull;
   const unsigned long long n = mine * cpp;  // this CTA's chunks: its pages in order, chunks in order
   if (n == 0) return;
@@ -883,19 +888,19 @@ __global__ void __launch_bounds__(32) k_copy_pages_tma(const unsigned long long 
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   auto src_dst = [&](unsigned long long j, const uint8_t *&src, uint8_t *&dst) {
-    const unsigned long long k = lo + blockIdx.x + (j / cpp) * gridDim.x, off = (j % cpp) * TMA_CH;
-    const unsigned long long hoff = desc[2 * k], pg = desc[2 * k + 1];
-    src = (D2H ? dev + pg * page_bytes : host + hoff) + off;
-    dst = (D2H ? host + hoff : dev + pg * page_bytes) + off;
+    const unsigned long long k = lo + blockIdx.x + (j / cpp) * gridDim.x, co = (j % cpp) * CH;
+    const unsigned long long hoff = desc[2 * k] + off, pg = desc[2 * k + 1];
+    src = (D2H ? dev + pg * slot : host + hoff) + co;
+    dst = (D2H ? host + hoff : dev + pg * slot) + co;
   };
   auto load = [&](unsigned long long j) {
     const uint8_t *src;
     uint8_t *dst;
     src_dst(j, src, dst);
     const uint32_t b = smem_u32(&bar[j % TMA_NB]), sm = smem_u32(tbuf + (j % TMA_NB) * TMA_CH);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(TMA_CH) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(CH) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sm),
-                 "l"(src), "r"(TMA_CH), "r"(b)
+                 "l"(src), "r"(CH), "r"(b)
                  : "memory");
   };
   for (unsigned long long j = 0; j < n && j < TMA_NB; ++j) load(j);
@@ -911,7 +916,7 @@ __global__ void __launch_bounds__(32) k_copy_pages_tma(const unsigned long long 
     uint8_t *dst;
     src_dst(j, src, dst);
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                 "r"(smem_u32(tbuf + (j % TMA_NB) * TMA_CH)), "r"(TMA_CH)
+                 "r"(smem_u32(tbuf + (j % TMA_NB) * TMA_CH)), "r"(CH)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     // the previous chunk's store has read its buffer: refill that buffer
@@ -1013,9 +1018,9 @@ int launch_expand(const Params &p, cudaStream_t s) {
 
 int launch_transfer(const Params &p, cudaStream_t s, int ctas) {
   const unsigned long long *desc = p.d.desc[p.desc_buf];
-  k_copy_pages<0><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
-  k_copy_pages<1><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
-  k_copy_pages<2><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  k_copy_pages<0><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
+  k_copy_pages<1><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
+  k_copy_pages<2><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
   return 3;
 }
 
@@ -1026,7 +1031,7 @@ int launch_transfer_split(const Params &p, cudaStream_t s, cudaStream_t s2, int 
   // bulk copies when pages are whole 16 KB chunks (A/B: the same link fraction as the
   // register-staged copy, profiles/r02_copy_tma_ab.log, with one thread and no registers per CTA)
 #ifndef COPY_REGS
-  if (p.page_bytes % TMA_CH == 0) {
+  if (p.slot_bytes % 16 == 0 && (p.slot_bytes <= TMA_CH || p.slot_bytes % TMA_CH == 0)) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_copy_pages_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_CH * TMA_NB);
@@ -1034,15 +1039,15 @@ int launch_transfer_split(const Params &p, cudaStream_t s, cudaStream_t s2, int 
       cudaFuncSetAttribute(k_copy_pages_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_CH * TMA_NB);
       attr = true;
     }
-    k_copy_pages_tma<0><<<ctas, 32, TMA_CH * TMA_NB, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
-    k_copy_pages_tma<1><<<ctas, 32, TMA_CH * TMA_NB, s2>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
-    k_copy_pages_tma<2><<<ctas, 32, TMA_CH * TMA_NB, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+    k_copy_pages_tma<0><<<ctas, 32, TMA_CH * TMA_NB, s>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
+    k_copy_pages_tma<1><<<ctas, 32, TMA_CH * TMA_NB, s2>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
+    k_copy_pages_tma<2><<<ctas, 32, TMA_CH * TMA_NB, s>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
     return 3;
   }
 #endif
-  k_copy_pages<0><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
-  k_copy_pages<1><<<ctas, NT, 0, s2>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
-  k_copy_pages<2><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.page_bytes, p.desc_cap);
+  k_copy_pages<0><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
+  k_copy_pages<1><<<ctas, NT, 0, s2>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
+  k_copy_pages<2><<<ctas, NT, 0, s>>>(desc, p.host_arena, p.dev_arena, p.slot_bytes, p.slice_off, p.desc_cap);
   return 3;
 }
 
@@ -1084,5 +1089,226 @@ void launch_init_page_table(const Params &p, uint64_t n_block_pages, const uint3
 }
 
 void launch_init_transfer(const Params &p, cudaStream_t s, int ctas) { launch_transfer(p, s, ctas); }
+
+// ------------------------------------------------------------------------------------
+// Loopback worlds (SCALESIM_F_LOOPBACK): the exchanges of §8(e) through device
+// memory, one launch for the world.  Per-step inputs (records, kinematics) by value; every
+// other field of rank r from its device parameter copy.
+struct WRank {
+  const Params *pd;
+  const uint4 *rec;
+};
+struct WArgs {
+  uint32_t G;
+  int64_t now;
+  WRank r[FUSED_MAX_WORLD];
+};
+
+static WArgs world_args(const Params *const *ps, uint32_t G, int64_t now) {
+  WArgs w = {};
+  w.G = G;
+  w.now = now;
+  for (uint32_t r = 0; r < G; ++r) {
+    w.r[r].pd = reinterpret_cast<const Params *>(ps[r]->d.params_dev);
+    w.r[r].rec = ps[r]->rec;
+  }
+  return w;
+}
+
+// §8(e) "an all-gather of kin for active INT agents": rank s's participants (k_int_compact's
+// list) copied into every rank's world list at s's offset (participants of lower ranks first);
+// block (d, s) of chunk x.  wcnt[d][r] = offset of rank r, wcnt[d][G] = the world's count.
+__global__ void __launch_bounds__(NT) k_kin_allgather(WArgs w) {
+  const uint32_t dr = blockIdx.y, sr = blockIdx.z;
+  const Dev &dd = w.r[dr].pd->d;
+  uint32_t off = 0, tot = 0;
+  for (uint32_t r = 0; r < w.G; ++r) {
+    const uint32_t n = w.r[r].pd->n_kin ? w.r[r].pd->d.state->int_count : 0u;
+    if (r < sr) off += n;
+    tot += n;
+  }
+  if (blockIdx.x == 0 && sr == 0 && threadIdx.x == 0) {
+    uint32_t o = 0;
+    for (uint32_t r = 0; r < w.G; ++r) {
+      dd.wcnt[r] = o;
+      o += w.r[r].pd->n_kin ? w.r[r].pd->d.state->int_count : 0u;
+    }
+    dd.wcnt[w.G] = tot;
+  }
+  const Params &ps = *w.r[sr].pd;
+  if (ps.n_kin == 0 || w.r[dr].pd->n_kin == 0) return;  // (a rank without interaction agents scans nothing)
+  const uint32_t n = ps.d.state->int_count;
+  for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) dd.wkin[off + i] = ps.d.ilist_kin[i];
+}
+
+// Eq. 2 over the world's participants: rank r's participant i against every
+// participant j of the world but itself (j == wcnt[r] + i); the same rounding and division
+// filter as k_pairmin, so D_int is the exact min of the rounded quotients at any world size.
+__global__ void __launch_bounds__(NT) k_pairmin_world(Params p) {
+  __shared__ float4 tile[NT];
+  const uint32_t count = p.d.state->int_count, total = p.d.wcnt[p.world], self = p.d.wcnt[p.rank];
+  const uint32_t i = blockIdx.x * NT + threadIdx.x;
+  if (blockIdx.x * NT >= count) return;
+  const bool mine = i < count;
+  const float4 ki = mine ? p.d.ilist_kin[i] : make_float4(0, 0, 0, 0);
+  float best = __int_as_float(0x7F800000);
+  for (uint32_t j0 = 0; j0 < total; j0 += NT) {
+    __syncthreads();
+    if (j0 + threadIdx.x < total) tile[threadIdx.x] = p.d.wkin[j0 + threadIdx.x];
+    __syncthreads();
+    const uint32_t jn = min((uint32_t)NT, total - j0);
+    if (mine) {
+      for (uint32_t jj = 0; jj < jn; ++jj) {
+        const float4 kj = tile[jj];
+        const float dx = __fsub_rn(kj.x, ki.x);
+        const float dy = __fsub_rn(kj.y, ki.y);
+        const float dvx = __fsub_rn(kj.z, ki.z);
+        const float dvy = __fsub_rn(kj.w, ki.w);
+        const float rw = __fadd_rn(__fmul_rn(dx, dvx), __fmul_rn(dy, dvy));
+        if (rw < 0.0f && (j0 + jj) != self + i) {
+          const float g2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+          const float den = -rw;
+          if (!(g2 > __fmul_ru(best, den))) {
+            const float t = __fdiv_rn(g2, den);
+            if (t < best) best = t;
+          }
+        }
+      }
+    }
+  }
+  if (mine) p.d.dint[p.d.ilist_idx[i]] = best;
+}
+
+int launch_world_interaction(const Params *const *ps, uint32_t G, int64_t now, cudaStream_t s) {
+  int n = 0;
+  uint64_t most = 0;
+  for (uint32_t r = 0; r < G; ++r) {
+    if (ps[r]->n_kin == 0) continue;
+    const int g = max(1, min(1184, ceil_div(max(ps[r]->n_local, ps[r]->n_kin), NT)));
+    k_int_compact<<<g, NT, 0, s>>>(*ps[r], now);
+    ++n;
+    most = ps[r]->n_kin > most ? ps[r]->n_kin : most;
+  }
+  if (n == 0) return 0;
+  const WArgs w = world_args(ps, G, now);
+  k_kin_allgather<<<dim3(max(1, min(64, ceil_div(most, NT))), G, G), NT, 0, s>>>(w);
+  ++n;
+  for (uint32_t r = 0; r < G; ++r) {
+    if (ps[r]->n_kin == 0) continue;
+    k_pairmin_world<<<max(1, ceil_div(ps[r]->n_kin, NT)), NT, 0, s>>>(*ps[r]);
+    ++n;
+  }
+  return n;
+}
+
+// §8(e) step 4, "all-gather of per-rank prefetch/evict id lists" merged into the global lists:
+// rank r's entry i of a list (its shard's members in list order) sits in the global list at
+//   i + sum over the other ranks r' of the entries of r' that precede it in list order,
+// i.e. (prefetch, ascending (d, id)) r' < r: keys <= k, r' > r: keys < k; (evict, descending
+// (d, id)) r' > r: keys >= k, r' < r: keys > k -- ranks own contiguous ascending id ranges.
+// The keys are the distance bits, recomputed from the records by the definition (a1).
+__device__ __forceinline__ uint32_t world_key(const Params &P, const uint4 *rec, uint32_t id, int64_t now) {
+  const uint4 r = rec[id - (uint32_t)P.shard_begin];
+  uint32_t st = 0;
+  const float d = P.explicit_dist ? explicit_distance_of(r, st) : distance_of(r, now, P.hop_scale, P.d.dint, P.n_kin, st);
+  return __float_as_uint(d);
+}
+
+__global__ void __launch_bounds__(NT) k_tp_keys(WArgs w) {
+  const uint32_t r = blockIdx.y, lst = blockIdx.z;
+  const Params &P = *w.r[r].pd;
+  const uint32_t n = (uint32_t)P.d.header[lst == 0 ? H_N_PF : H_N_EV];
+  const uint32_t *ids = lst == 0 ? P.d.pf_ids : P.d.ev_ids;
+  uint32_t *key = lst == 0 ? P.d.tp_kpf : P.d.tp_kev;
+  for (uint32_t i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) key[i] = world_key(P, w.r[r].rec, ids[i], w.now);
+}
+
+// one entry per 8 lanes (lane g searches rank g's list), 128 entries per block
+__global__ void __launch_bounds__(1024) k_tp_merge(WArgs w) {
+  const uint32_t r = blockIdx.y, lst = blockIdx.z;
+  const Params &P = *w.r[r].pd;
+  const uint32_t n = (uint32_t)P.d.header[lst == 0 ? H_N_PF : H_N_EV];
+  const uint32_t g = threadIdx.x & 7u;
+  const uint32_t i = blockIdx.x * 128 + (threadIdx.x >> 3);
+  if (blockIdx.x == 0 && r == 0 && lst == 0 && threadIdx.x < w.G) {  // merged counts into every rank
+    unsigned long long npf = 0, nev = 0;
+    for (uint32_t q = 0; q < w.G; ++q) {
+      npf += w.r[q].pd->d.header[H_N_PF];
+      nev += w.r[q].pd->d.header[H_N_EV];
+    }
+    unsigned long long *H = w.r[threadIdx.x].pd->d.tp_hdr;
+    H[H_N_PF] = npf;
+    H[H_N_EV] = nev;
+    H[H_STATUS] = 0;
+  }
+  if (blockIdx.x * 128 >= n) return;  // (block-uniform)
+  const bool on = i < n;
+  uint32_t k = 0, id = 0;
+  if (on) {
+    k = (lst == 0 ? P.d.tp_kpf : P.d.tp_kev)[i];
+    id = (lst == 0 ? P.d.pf_ids : P.d.ev_ids)[i];
+  }
+  uint32_t cnt = 0;
+  if (on && g < w.G) {
+    if (g == r) {
+      cnt = i;
+    } else {
+      const Params &Q = *w.r[g].pd;
+      const uint32_t m = (uint32_t)Q.d.header[lst == 0 ? H_N_PF : H_N_EV];
+      const uint32_t *kq = lst == 0 ? Q.d.tp_kpf : Q.d.tp_kev;
+      // count of the leading entries of rank g's list that precede (k, id): a prefix of its list
+      const bool lower = g < r;
+      uint32_t lo = 0, hi = m;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1, kk = kq[mid];
+        const bool before = lst == 0 ? (lower ? kk <= k : kk < k) : (lower ? kk > k : kk >= k);
+        if (before) lo = mid + 1;
+        else hi = mid;
+      }
+      cnt = lo;
+    }
+  }
+  cnt += __shfl_xor_sync(FULL, cnt, 1);
+  cnt += __shfl_xor_sync(FULL, cnt, 2);
+  cnt += __shfl_xor_sync(FULL, cnt, 4);
+  if (!on || g >= w.G) return;
+  // lane g writes rank g's copy (the all-gather's destination)
+  const Dev &dd = w.r[g].pd->d;
+  if (lst == 0) {
+    dd.tp_pf[cnt] = id;
+  } else {
+    dd.tp_ev[cnt] = id;
+    dd.tp_dirty[cnt] = (uint8_t)((w.r[r].rec[id - (uint32_t)P.shard_begin].z >> 4) & 1u);
+  }
+}
+
+int launch_tp_merge(const Params *const *ps, uint32_t G, int64_t now, cudaStream_t s) {
+  uint64_t most = 1;
+  for (uint32_t r = 0; r < G; ++r) most = ps[r]->n_local > most ? ps[r]->n_local : most;
+  const WArgs w = world_args(ps, G, now);
+  k_tp_keys<<<dim3(max(1, min(148, ceil_div(most, NT))), G, 2), NT, 0, s>>>(w);
+  k_tp_merge<<<dim3(ceil_div(most, 128), G, 2), 1024, 0, s>>>(w);
+  return 2;
+}
+
+// after the expansion of the merged lists: this rank's header carries the world's page counts
+// (its transfer moves slice `rank` of each listed page) and a pool shortage
+__global__ void k_tp_finish(Params p) {
+  const unsigned long long *T = p.d.tp_hdr;
+  unsigned long long *H = p.d.header;
+  H[H_N_D2H] = T[H_N_D2H];
+  H[H_N_H2D] = T[H_N_H2D];
+  H[H_POOL_HEAD] = T[H_POOL_HEAD];
+  H[H_POOL_TAIL] = T[H_POOL_TAIL];
+  if (T[H_STATUS] & ST_NO_PAGES) {
+    H[H_STATUS] |= ST_NO_PAGES;
+    p.d.state->status |= ST_NO_PAGES;
+  }
+}
+
+int launch_tp_finish(const Params &p, cudaStream_t s) {
+  k_tp_finish<<<1, 1, 0, s>>>(p);
+  return 1;
+}
 
 }  // namespace ss

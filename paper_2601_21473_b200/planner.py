@@ -37,7 +37,7 @@ class Planner:
                  shard: Optional[tuple] = None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None,
                  multi_kernel: bool = False, keep_dist: bool = True, explicit_dist: bool = False,
-                 exclusive: bool = False, loopback: bool = False):
+                 exclusive: bool = False, loopback: bool = False, tp_sliced: bool = False):
         self.lib = L.lib()
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
@@ -72,8 +72,8 @@ class Planner:
                     initial=0) + page_bytes + (int(blk_size.max()) if len(blk_size) else 0))
                 host_arena = torch.zeros(hb, dtype=torch.uint8, pin_memory=True)
             self.host_arena = host_arena
-            if dev_bytes is None:
-                dev_bytes = (self.budget + page_bytes - 1) // page_bytes * page_bytes
+            if dev_bytes is None:  # (TP-sliced: a slot holds this rank's 1/world of a page)
+                dev_bytes = (self.budget + page_bytes - 1) // page_bytes * (page_bytes // (world if tp_sliced else 1))
             self.dev_arena = torch.empty(max(int(dev_bytes), page_bytes), dtype=torch.uint8, device=dev)
         self.res_init = None
         if resident_init is not None:
@@ -89,7 +89,10 @@ class Planner:
         cfg.abi_version = L.ABI_VERSION
         cfg.flags = (0 if transfer else L.F_NO_TRANSFER) | (L.F_MULTI_KERNEL if multi_kernel else 0) | \
             (L.F_KEEP_DIST if keep_dist else 0) | (L.F_EXPLICIT_DIST if explicit_dist else 0) | \
-            (L.F_EXCLUSIVE if exclusive else 0) | (L.F_LOOPBACK if loopback else 0)
+            (L.F_EXCLUSIVE if exclusive else 0) | (L.F_LOOPBACK if loopback else 0) | \
+            (L.F_TP_SLICED if tp_sliced else 0)
+        self.tp_sliced = bool(tp_sliced)
+        self.slot_bytes = self.page_bytes // (world if tp_sliced else 1)
         cfg.n_agents = self.n_agents
         cfg.shard_begin = self.lo
         cfg.shard_end = self.hi
@@ -246,6 +249,18 @@ class Planner:
 
     def page_table(self) -> np.ndarray:
         return self._read(self.view.page_table, 4 * self.n_block_pages).view(np.uint32)
+
+    def world_lists(self):
+        """TP-sliced rank: the world's merged prefetch / evict lists and header fields after the
+        last step (scalesim_world_view)."""
+        wv = L.WorldView()
+        L.check(self.lib.scalesim_world_view(self.ctx, C.byref(wv)), "scalesim_world_view")
+        h = self._read(wv.header, 8 * 16).view(np.uint64)
+        hdr = dict(n_prefetch=int(h[0]), n_evict=int(h[1]), bytes_d2h=int(h[3]), n_d2h=int(h[7]), n_h2d=int(h[8]),
+                   status=int(h[6]))
+        pf = self._read(wv.prefetch_ids, 4 * hdr["n_prefetch"]).view(np.uint32)
+        ev = self._read(wv.evict_ids, 4 * hdr["n_evict"]).view(np.uint32)
+        return pf, ev, hdr
 
     def descriptors(self, hdr=None):
         hdr = hdr or self.sync()

@@ -142,3 +142,133 @@ def test_world_physical_transfers():
     """C2-mini with physical page copies: each rank assigns and moves the pages of its shard."""
     w = tg.config_c2(seed=2, steps=12, n=3001, lora=4 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
     run_world(w, [0, 1400, 3001], transfer=True)
+
+
+def run_world_tp(w, cuts, content_pages=48):
+    """TP-sliced world (SCALESIM_F_TP_SLICED, R16): every rank plans its shard (lists ==
+    oracle restricted to the shard), holds the world's merged lists (== the world-1 oracle
+    lists), assigns the pages of the whole plan exactly as the world-1 oracle page pool does
+    (descriptors and page table), and its arena slot of a loaded page holds its slice of the
+    page's host bytes."""
+    import torch
+    from gpu_harness import fill_pattern
+    from paper_2601_21473_b200.planner import Planner, step_group
+    G = len(cuts) - 1
+    stream = torch.cuda.Stream()
+    b = w.blocks
+    host = torch.empty(int(b.host_bytes), dtype=torch.uint8, pin_memory=True)
+    fill_pattern(host)
+    pages = max((w.budget + w.page_bytes - 1) // w.page_bytes, 1)
+    su = w.page_bytes // G
+    ranks = [Planner(w.n, b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.budget, w.theta,
+                     hop_scale=w.hop_scale, transfer=True, page_bytes=w.page_bytes, host_arena=host,
+                     dev_bytes=pages * su, shard=(cuts[r], cuts[r + 1]), rank=r, world=G, loopback=True,
+                     tp_sliced=True, stream=stream, keep_dist=False) for r in range(G)]
+    assert all(pl.fused for pl in ranks)
+    om = oracle.OracleMem(b.blk_ptr, b.blk_size, b.blk_host_off, b.blk_kind, w.page_bytes, pages)
+    page_first = np.concatenate([[0], np.cumsum(b.blk_size.astype(np.int64) // w.page_bytes)])
+    page_host = np.zeros(int(page_first[-1]), np.int64)  # host offset of every block page
+    for blk in range(len(b.blk_size)):
+        q0, q1 = int(page_first[blk]), int(page_first[blk + 1])
+        page_host[q0:q1] = int(b.blk_host_off[blk]) + np.arange(q1 - q0) * w.page_bytes
+    res = np.zeros(w.n, np.uint8)
+    rng = np.random.default_rng(0)
+    fp = None
+    for s in range(w.steps):
+        rec = w.rec[s]
+        for r, pl in enumerate(ranks):
+            pl.set_records(rec[cuts[r]:cuts[r + 1]])
+        step_group(ranks, int(w.now[s]))
+        d, _ = oracle.score(rec, None, int(w.now[s]), w.hop_scale)
+        p = oracle.plan(rec, d, res, w.theta, w.budget)
+        mo = om.apply(rec, p["prefetch"], p["evict"])
+        pt = om.page_table()
+        fp = rec[:, 1].astype(np.int64)
+        for r, pl in enumerate(ranks):
+            lo, hi = cuts[r], cuts[r + 1]
+            hdr = pl.sync()
+            pf, ev = pl.lists(hdr)
+            assert np.array_equal(pf, p["prefetch"][(p["prefetch"] >= lo) & (p["prefetch"] < hi)]), (s, r)
+            assert np.array_equal(ev, p["evict"][(p["evict"] >= lo) & (p["evict"] < hi)]), (s, r)
+            assert hdr["bytes_h2d"] == int(fp[pf].sum()), (s, r)
+            gpf, gev, gh = pl.world_lists()
+            assert np.array_equal(gpf, p["prefetch"]) and np.array_equal(gev, p["evict"]), (s, r)
+            assert gh["bytes_d2h"] == mo["bytes_d2h"] and gh["status"] == 0, (s, r, gh)
+            assert hdr["n_d2h"] == len(mo["d2h_page"]) and hdr["n_h2d"] == len(mo["h2d_page"]), (s, r)
+            d2h, h2d = pl.descriptors(hdr)
+            assert np.array_equal(h2d[:, 0], mo["h2d_host"]) and np.array_equal(h2d[:, 1], mo["h2d_page"]), (s, r)
+            assert np.array_equal(d2h[:, 0], mo["d2h_host"]) and np.array_equal(d2h[:, 1], mo["d2h_page"]), (s, r)
+            assert np.array_equal(pl.page_table(), pt), (s, r)
+            # content: the rank's slot of a resident page holds slice r of the page's host bytes
+            held = np.nonzero(pt != 0xFFFFFFFF)[0]
+            for q in rng.permutation(held)[:content_pages]:
+                slot, ho = int(pt[q]), int(page_host[q]) + r * su
+                got = pl.dev_arena[slot * su:(slot + 1) * su].cpu()
+                assert torch.equal(got, host[ho:ho + su]), (s, r, int(q), slot)
+        res = p["resident"]
+    for pl in ranks:
+        pl.close()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_world_tp_sliced_transfers(G):
+    """§8(e) step 4 / R16: TP-sliced page transfers of a loopback world (C2-mini, 64 KiB pages:
+    32 / 16 / 8 KiB slices, the last below the 16 KB bulk-copy chunk)."""
+    w = tg.config_c2(seed=4, steps=10, n=3001, lora=4 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
+    assert w.page_bytes == 65536
+    cuts = [round(w.n * r / G) for r in range(G + 1)]
+    run_world_tp(w, cuts)
+
+
+def shard_kin(w, s, lo, hi):
+    """Rank [lo, hi)'s records of step s with its own kinematics array (the interaction agents of
+    its shard, kinematics index rebased) -- the per-rank input of a loopback world."""
+    rec = w.rec[s, lo:hi].copy()
+    cls = (rec[:, 2] >> 2) & 3
+    idx = rec[cls == 1, 3].astype(np.int64)
+    if len(idx) == 0:
+        return rec, np.zeros((1, 4), np.float32)
+    base = int(idx.min())
+    assert np.array_equal(np.sort(idx), np.arange(base, base + len(idx)))  # (contiguous in C3)
+    rec[cls == 1, 3] = (idx - base).astype(np.uint32)
+    return rec, np.ascontiguousarray(w.kin[s, base:base + len(idx)])
+
+
+@pytest.mark.parametrize("cuts", [[0, 50_000, 100_000], [0, 40_000, 52_000, 100_000]])
+def test_world_interaction_kin_allgather(cuts):
+    """§8(e) kin all-gather: C3 (three classes) sharded so that every rank holds interaction
+    agents; each rank's pair scan sees the world's participants, plan(world) == oracle."""
+    import torch
+    from paper_2601_21473_b200.planner import Planner, step_group
+    w = tg.config_c3(seed=2, steps=3, n=100_000)
+    G = len(cuts) - 1
+    stream = torch.cuda.Stream()
+    ranks = []
+    for r in range(G):
+        lo, hi = cuts[r], cuts[r + 1]
+        bp, bs, bo, bk = shard_blocks(w.blocks, lo, hi)
+        _, kin0 = shard_kin(w, 0, lo, hi)
+        ranks.append(Planner(w.n, bp, bs, bo, bk, w.budget, w.theta, hop_scale=w.hop_scale, n_kin=len(kin0),
+                             transfer=False, shard=(lo, hi), rank=r, world=G, loopback=True, stream=stream,
+                             keep_dist=False))
+        assert ranks[-1].fused
+    res = np.zeros(w.n, np.uint8)
+    for s in range(w.steps):
+        for r, pl in enumerate(ranks):
+            rr, kk = shard_kin(w, s, cuts[r], cuts[r + 1])
+            pl.set_records(rr, kk)
+        step_group(ranks, int(w.now[s]))
+        d, _ = oracle.score(w.rec[s], w.kin[s], int(w.now[s]), w.hop_scale)
+        p = oracle.plan(w.rec[s], d, res, w.theta, w.budget)
+        for r, pl in enumerate(ranks):
+            lo, hi = cuts[r], cuts[r + 1]
+            hdr = pl.sync()
+            pf, ev = pl.lists(hdr)
+            assert np.array_equal(pf, p["prefetch"][(p["prefetch"] >= lo) & (p["prefetch"] < hi)]), (s, r)
+            assert np.array_equal(ev, p["evict"][(p["evict"] >= lo) & (p["evict"] < hi)]), (s, r)
+            assert np.array_equal(pl.resident(), p["resident"][lo:hi]), (s, r)
+            assert hdr["cut_bits"] == p["cut_bits"] and hdr["cut_rem"] == p["cut_rem"], (s, r)
+            assert hdr["kept_bytes"] == p["kept_bytes"] and hdr["n_eligible"] == p["n_eligible"], (s, r)
+        res = p["resident"]
+    for pl in ranks:
+        pl.close()
