@@ -112,6 +112,16 @@ typedef enum {
                                        exact all-pairs, Eq. 2).  The ranks of
                                        one world must agree on n_kin > 0 (the distance class mix
                                        decides the histogram layout). */
+#define SCALESIM_F_THREADS 128u     /* world > 1 on one device without NCCL, multi-kernel path: rank
+                                       `rank` of a world whose ranks are contexts of this process on
+                                       one device, each driven by its own host thread calling the
+                                       same sequence of score / plan / step (a host barrier per
+                                       collective).  The collectives the NCCL path calls (DESIGN §8:
+                                       sums of the byte histograms, min of the bucket min keys,
+                                       the all-gather of the ranks' bytes at D*, the kept tie bytes)
+                                       run as reductions over the ranks' device buffers.  The
+                                       group is the contexts created with the same 128-byte
+                                       nccl_unique_id (any bytes).  Not with SCALESIM_F_LOOPBACK. */
 #define SCALESIM_F_TP_SLICED 64u    /* with SCALESIM_F_LOOPBACK and transfers: tensor-parallel
                                        agent memory (§4.2: "All multi-GPU setups
                                        use tensor parallelism"; reading R16).  Every rank holds

@@ -18,6 +18,7 @@ F_EXPLICIT_DIST = 8
 F_EXCLUSIVE = 16
 F_LOOPBACK = 32
 F_TP_SLICED = 64
+F_THREADS = 128
 
 ST_INSUFFICIENT = 1
 ST_BAD_RECORD = 2

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -127,6 +128,7 @@ Layout make_layout(uint64_t n_local, uint64_t n_kin, uint64_t n_blocks, uint64_t
   L.tp_hdr = take(8 * H_FIELDS);
   L.tp_kpf = take(4 * tl);
   L.tp_kev = take(4 * tl);
+  L.xscratch = take(world > 1 ? 32768 : 1);
   L.total = off;
   return L;
 }
@@ -218,6 +220,7 @@ Dev make_dev(void *ws, const Layout &L) {
   d.tp_hdr = (unsigned long long *)(b + L.tp_hdr);
   d.tp_kpf = (uint32_t *)(b + L.tp_kpf);
   d.tp_kev = (uint32_t *)(b + L.tp_kev);
+  d.xscratch = (uint8_t *)(b + L.xscratch);
   return d;
 }
 
@@ -253,6 +256,63 @@ struct Nccl {
 };
 static Nccl g_nccl;
 
+// ---- SCALESIM_F_THREADS: the world > 1 collectives between ranks on one device, each rank
+// driven by its own host thread (the exchange the NCCL calls perform, through device memory;
+// DESIGN §8).  A group = the contexts created with the same 128-byte id.  Each collective:
+// every rank records its input's readiness and publishes the pointer (host barrier); every rank
+// waits for all inputs on its stream and reduces them into its scratch (host barrier: every
+// wait is enqueued before any input is reused); the result lands in the rank's buffer.
+struct ThreadGroup {
+  int world = 0, joined = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  const void *in[FUSED_MAX_WORLD] = {};
+  cudaEvent_t ev_in[FUSED_MAX_WORLD] = {}, ev_red[FUSED_MAX_WORLD] = {};
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+static std::mutex g_groups_mu;
+static std::vector<std::pair<std::vector<uint8_t>, ThreadGroup *>> g_groups;
+
+static ThreadGroup *join_group(const void *id, int world) {
+  std::vector<uint8_t> key(static_cast<const uint8_t *>(id), static_cast<const uint8_t *>(id) + 128);
+  std::lock_guard<std::mutex> lk(g_groups_mu);
+  for (auto &e : g_groups)
+    if (e.first == key) {
+      if (e.second->world != world) return nullptr;
+      e.second->joined++;
+      return e.second;
+    }
+  ThreadGroup *g = new (std::nothrow) ThreadGroup();
+  if (!g) return nullptr;
+  g->world = world;
+  g->joined = 1;
+  g_groups.emplace_back(key, g);
+  return g;
+}
+
+static void leave_group(ThreadGroup *g) {
+  std::lock_guard<std::mutex> lk(g_groups_mu);
+  if (--g->joined > 0) return;
+  for (size_t i = 0; i < g_groups.size(); ++i)
+    if (g_groups[i].second == g) {
+      g_groups.erase(g_groups.begin() + (long)i);
+      break;
+    }
+  delete g;
+}
+
 // SCALESIM_F_EXCLUSIVE: the single-kernel plans of the exclusive contexts of a device run one
 // after another (their grid barriers need every SM): the last launch's stream and event per
 // device, and the number of such contexts (with one, nothing is recorded: consecutive launches
@@ -284,6 +344,8 @@ struct scalesim_ctx {
   bool scored = false, planned = false, transferred = true;
   uint64_t launches = 0;
   ncclComm_t comm = nullptr;
+  ThreadGroup *tgroup = nullptr;  // SCALESIM_F_THREADS
+  cudaEvent_t ev_xin = nullptr, ev_xred = nullptr;
   int last_buf = 0;
   bool xfer_pending = false;
   bool xfer_recorded[2] = {false, false};  // ev_xfer[b] has been recorded at least once
@@ -328,13 +390,16 @@ static scalesim_status validate_config(const scalesim_config *c) {
   // interaction agents at world > 1: the kinematics all-gather of a loopback world
   if (c->world > 1 && c->n_kin > 0 && !(c->flags & SCALESIM_F_LOOPBACK)) return SCALESIM_E_INVALID;
   if ((c->flags & SCALESIM_F_LOOPBACK) && (c->world < 2 || c->world > (int)FUSED_MAX_WORLD)) return SCALESIM_E_INVALID;
+  if ((c->flags & SCALESIM_F_THREADS) &&
+      (c->world < 2 || c->world > (int)FUSED_MAX_WORLD || (c->flags & SCALESIM_F_LOOPBACK) || !c->nccl_unique_id))
+    return SCALESIM_E_INVALID;
   if ((c->flags & SCALESIM_F_TP_SLICED) &&
       (!(c->flags & SCALESIM_F_LOOPBACK) || (c->flags & SCALESIM_F_NO_TRANSFER) || c->page_bytes % (16ull * c->world) != 0))
     return SCALESIM_E_INVALID;
   if ((c->flags & SCALESIM_F_EXPLICIT_DIST) && c->n_kin > 0) return SCALESIM_E_INVALID;
   if (c->flags & ~(uint32_t)(SCALESIM_F_NO_TRANSFER | SCALESIM_F_KEEP_DIST | SCALESIM_F_MULTI_KERNEL |
                              SCALESIM_F_EXPLICIT_DIST | SCALESIM_F_EXCLUSIVE | SCALESIM_F_LOOPBACK |
-                             SCALESIM_F_TP_SLICED))
+                             SCALESIM_F_TP_SLICED | SCALESIM_F_THREADS))
     return SCALESIM_E_INVALID;
   for (int k = 0; k < 3; ++k)
     if (std::isnan(c->theta[k]) || c->theta[k] < 0.0f) return SCALESIM_E_INVALID;
@@ -614,7 +679,12 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
     return fail(SCALESIM_E_CUDA);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail(SCALESIM_E_CUDA);
   if (p.loopback && !c->fused) return fail(SCALESIM_E_INVALID);  // (shard too large for its CTAs)
-  if (cfg->world > 1 && !p.loopback) {
+  if (cfg->flags & SCALESIM_F_THREADS) {
+    if (cudaEventCreateWithFlags(&c->ev_xin, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_xred, cudaEventDisableTiming) != cudaSuccess)
+      return fail(SCALESIM_E_CUDA);
+    if (!(c->tgroup = join_group(cfg->nccl_unique_id, cfg->world))) return fail(SCALESIM_E_INVALID);
+  } else if (cfg->world > 1 && !p.loopback) {
     if (!cfg->nccl_unique_id || !g_nccl.load()) return fail(SCALESIM_E_NCCL);
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_unique_id, sizeof(id));
@@ -656,8 +726,56 @@ extern "C" scalesim_status scalesim_score(scalesim_ctx *c, int64_t now, float *d
   return SCALESIM_OK;
 }
 
+// in-place all-reduce (sum of u64 or min of u32) over the world's ranks: NCCL, or the thread
+// group's device-memory exchange
 static scalesim_status allreduce(scalesim_ctx *c, void *buf, size_t n, ncclDataType_t t, ncclRedOp_t op) {
-  NK(g_nccl.AllReduce(buf, buf, n, t, op, c->comm, c->stream));
+  if (!c->tgroup) {
+    NK(g_nccl.AllReduce(buf, buf, n, t, op, c->comm, c->stream));
+    return SCALESIM_OK;
+  }
+  ThreadGroup &g = *c->tgroup;
+  const int r = c->cfg.rank, G = c->cfg.world;
+  const size_t bytes = n * (t == ncclUint64 ? 8 : 4);
+  if (bytes > 32768) return SCALESIM_E_INVALID;
+  CK(cudaEventRecord(c->ev_xin, c->stream));
+  g.in[r] = buf;
+  g.ev_in[r] = c->ev_xin;
+  g.barrier();
+  for (int q = 0; q < G; ++q)
+    if (q != r) CK(cudaStreamWaitEvent(c->stream, g.ev_in[q], 0));
+  c->launches += launch_xreduce(c->p.d.xscratch, g.in, (uint32_t)G, n, t == ncclUint64 ? 0 : 1, c->stream);
+  CK(cudaEventRecord(c->ev_xred, c->stream));
+  g.ev_red[r] = c->ev_xred;
+  g.barrier();  // (every rank's waits on the inputs are enqueued)
+  for (int q = 0; q < G; ++q)
+    if (q != r) CK(cudaStreamWaitEvent(c->stream, g.ev_red[q], 0));  // (nobody still reads this input)
+  CK(cudaMemcpyAsync(buf, c->p.d.xscratch, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  g.barrier();  // (every wait on this collective's events is enqueued before they are re-recorded)
+  (void)op;
+  return SCALESIM_OK;
+}
+
+// all-gather of one u64 per rank into recv[0, world)
+static scalesim_status allgather_u64(scalesim_ctx *c, const unsigned long long *send, unsigned long long *recv) {
+  if (!c->tgroup) {
+    NK(g_nccl.AllGather(send, recv, 1, ncclUint64, c->comm, c->stream));
+    return SCALESIM_OK;
+  }
+  ThreadGroup &g = *c->tgroup;
+  const int r = c->cfg.rank, G = c->cfg.world;
+  CK(cudaEventRecord(c->ev_xin, c->stream));
+  g.in[r] = send;
+  g.ev_in[r] = c->ev_xin;
+  g.barrier();
+  for (int q = 0; q < G; ++q)
+    if (q != r) CK(cudaStreamWaitEvent(c->stream, g.ev_in[q], 0));
+  c->launches += launch_xgather(recv, g.in, (uint32_t)G, c->stream);
+  CK(cudaEventRecord(c->ev_xred, c->stream));
+  g.ev_red[r] = c->ev_xred;
+  g.barrier();
+  for (int q = 0; q < G; ++q)
+    if (q != r) CK(cudaStreamWaitEvent(c->stream, g.ev_red[q], 0));
+  g.barrier();
   return SCALESIM_OK;
 }
 
@@ -757,7 +875,8 @@ extern "C" scalesim_status scalesim_plan(scalesim_ctx *c, scalesim_plan_view *ou
   c->launches += launch_select(p, 3, c->stream);
   c->launches += launch_tie(p, c->stream);
   if (multi) {
-    NK(g_nccl.AllGather(&p.d.state->tie_local, p.d.gather, 1, ncclUint64, c->comm, c->stream));
+    scalesim_status s;
+    if ((s = allgather_u64(c, &p.d.state->tie_local, p.d.gather)) != SCALESIM_OK) return s;
   }
   c->launches += launch_emit(p, c->stream);
   if (multi) {
@@ -1051,6 +1170,9 @@ extern "C" void scalesim_destroy(scalesim_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->tgroup) leave_group(c->tgroup);
+  if (c->ev_xin) cudaEventDestroy(c->ev_xin);
+  if (c->ev_xred) cudaEventDestroy(c->ev_xred);
   if (c->exclusive) {
     std::lock_guard<std::mutex> g(g_excl_mu);
     ExclusiveChain &x = g_excl[c->cfg.device];

@@ -79,7 +79,7 @@ struct Layout {
   uint64_t f_pos, f_rt, f_crow, f_ovf, big_codes;
   // world > 1 on one device (SCALESIM_F_LOOPBACK): the gathered interaction participants of the
   // world, and (SCALESIM_F_TP_SLICED) the world's merged lists and their transfer header
-  uint64_t wkin, wcnt, tp_pf, tp_ev, tp_dirty, tp_hdr, tp_kpf, tp_kev;
+  uint64_t wkin, wcnt, tp_pf, tp_ev, tp_dirty, tp_hdr, tp_kpf, tp_kev, xscratch;
   uint64_t total;
 };
 
@@ -147,6 +147,7 @@ struct Dev {
   uint8_t *tp_dirty;           // [n_agents] dirty bit of each merged evict entry
   unsigned long long *tp_hdr;  // [H_FIELDS] list counts and transfer fields of the merged plan
   uint32_t *tp_kpf, *tp_kev;   // [n_local] distance bits of this rank's list entries (merge keys)
+  uint8_t *xscratch;           // [32 KB] result of a thread-exchange collective before it lands
 };
 
 Dev make_dev(void *ws, const Layout &L);
@@ -201,6 +202,9 @@ int launch_copy_dist(const Params &p, float *dist_out, cudaStream_t s);
 int launch_world_interaction(const Params *const *ps, uint32_t G, int64_t now, cudaStream_t s);
 int launch_tp_merge(const Params *const *ps, uint32_t G, int64_t now, cudaStream_t s);
 int launch_tp_finish(const Params &rank_p, cudaStream_t s);
+// collectives between same-device ranks driven by host threads (SCALESIM_F_THREADS)
+int launch_xreduce(void *out, const void *const *ins, uint32_t G, uint64_t n, int kind, cudaStream_t s);
+int launch_xgather(unsigned long long *out, const void *const *ins, uint32_t G, cudaStream_t s);
 bool fused_supported(const Params &p, int grid, uint32_t *tile_out);
 // one instance of a fused launch (see fused.cu)
 struct FusedInst {

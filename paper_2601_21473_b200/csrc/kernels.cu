@@ -1311,4 +1311,40 @@ int launch_tp_finish(const Params &p, cudaStream_t s) {
   return 1;
 }
 
+// The collectives of the multi-kernel world > 1 path between ranks that share one
+// device, each rank driven by its own host thread (SCALESIM_F_THREADS): out = reduction over the
+// G ranks' buffers (kind 0: sum of u64, 1: min of u32), or the all-gather of one u64 per rank.
+struct XIn {
+  const void *in[FUSED_MAX_WORLD];
+};
+__global__ void __launch_bounds__(NT) k_xreduce(void *out, XIn x, uint32_t G, uint64_t n, int kind) {
+  for (uint64_t i = blockIdx.x * (uint64_t)NT + threadIdx.x; i < n; i += (uint64_t)gridDim.x * NT) {
+    if (kind == 0) {
+      unsigned long long v = 0;
+      for (uint32_t r = 0; r < G; ++r) v += static_cast<const unsigned long long *>(x.in[r])[i];
+      static_cast<unsigned long long *>(out)[i] = v;
+    } else {
+      uint32_t v = 0xFFFFFFFFu;
+      for (uint32_t r = 0; r < G; ++r) v = min(v, static_cast<const uint32_t *>(x.in[r])[i]);
+      static_cast<uint32_t *>(out)[i] = v;
+    }
+  }
+}
+__global__ void k_xgather(unsigned long long *out, XIn x, uint32_t G) {
+  if (threadIdx.x < G) out[threadIdx.x] = *static_cast<const unsigned long long *>(x.in[threadIdx.x]);
+}
+
+int launch_xreduce(void *out, const void *const *ins, uint32_t G, uint64_t n, int kind, cudaStream_t s) {
+  XIn x = {};
+  for (uint32_t r = 0; r < G; ++r) x.in[r] = ins[r];
+  k_xreduce<<<max(1, min(64, ceil_div(n, NT))), NT, 0, s>>>(out, x, G, n, kind);
+  return 1;
+}
+int launch_xgather(unsigned long long *out, const void *const *ins, uint32_t G, cudaStream_t s) {
+  XIn x = {};
+  for (uint32_t r = 0; r < G; ++r) x.in[r] = ins[r];
+  k_xgather<<<1, 32, 0, s>>>(out, x, G);
+  return 1;
+}
+
 }  // namespace ss

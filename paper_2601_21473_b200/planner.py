@@ -37,7 +37,7 @@ class Planner:
                  shard: Optional[tuple] = None, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  stream: Optional[torch.cuda.Stream] = None, copy_stream: Optional[torch.cuda.Stream] = None,
                  multi_kernel: bool = False, keep_dist: bool = True, explicit_dist: bool = False,
-                 exclusive: bool = False, loopback: bool = False, tp_sliced: bool = False):
+                 exclusive: bool = False, loopback: bool = False, tp_sliced: bool = False, threads: bool = False):
         self.lib = L.lib()
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
@@ -90,7 +90,7 @@ class Planner:
         cfg.flags = (0 if transfer else L.F_NO_TRANSFER) | (L.F_MULTI_KERNEL if multi_kernel else 0) | \
             (L.F_KEEP_DIST if keep_dist else 0) | (L.F_EXPLICIT_DIST if explicit_dist else 0) | \
             (L.F_EXCLUSIVE if exclusive else 0) | (L.F_LOOPBACK if loopback else 0) | \
-            (L.F_TP_SLICED if tp_sliced else 0)
+            (L.F_TP_SLICED if tp_sliced else 0) | (L.F_THREADS if threads else 0)
         self.tp_sliced = bool(tp_sliced)
         self.slot_bytes = self.page_bytes // (world if tp_sliced else 1)
         cfg.n_agents = self.n_agents

@@ -272,3 +272,92 @@ def test_world_interaction_kin_allgather(cuts):
         res = p["resident"]
     for pl in ranks:
         pl.close()
+
+
+def run_world_threads(w, cuts, transfer=False):
+    """The multi-kernel world > 1 path (the NCCL path's launches and collectives) with the
+    SCALESIM_F_THREADS exchange: one context per rank on this device, each stepped by its own
+    host thread; plan(world) == oracle restricted to each shard, bit for bit."""
+    import threading
+    import torch
+    from gpu_harness import fill_pattern
+    from paper_2601_21473_b200.planner import Planner
+    G = len(cuts) - 1
+    gid = bytes([7, G]) + bytes(126)
+    host = None
+    if transfer:
+        host = torch.empty(int(w.blocks.host_bytes), dtype=torch.uint8, pin_memory=True)
+        fill_pattern(host)
+    ranks, oms = [], []
+    pages = max((w.budget + w.page_bytes - 1) // w.page_bytes, 1)
+    for r in range(G):
+        lo, hi = cuts[r], cuts[r + 1]
+        bp, bs, bo, bk = shard_blocks(w.blocks, lo, hi)
+        ranks.append(Planner(w.n, bp, bs, bo, bk, w.budget, w.theta, hop_scale=w.hop_scale, transfer=transfer,
+                             page_bytes=w.page_bytes, host_arena=host, dev_bytes=pages * w.page_bytes,
+                             shard=(lo, hi), rank=r, world=G, nccl_id=gid, threads=True, keep_dist=False))
+        assert not ranks[-1].fused  # (the multi-kernel path)
+        if transfer:
+            oms.append(oracle.OracleMem(bp, bs, bo, bk, w.page_bytes, pages))
+    res = np.zeros(w.n, np.uint8)
+    for s in range(w.steps):
+        rec = w.rec[s]
+        errs = []
+
+        def run(r):
+            try:
+                ranks[r].set_records(rec[cuts[r]:cuts[r + 1]])
+                ranks[r].step(int(w.now[s]))
+            except Exception as e:  # noqa: BLE001
+                errs.append((r, e))
+        th = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=120)
+        assert not errs and not any(t.is_alive() for t in th), errs
+        d, _ = oracle.score(rec, None, int(w.now[s]), w.hop_scale)
+        p = oracle.plan(rec, d, res, w.theta, w.budget)
+        fp = rec[:, 1].astype(np.int64)
+        for r, pl in enumerate(ranks):
+            lo, hi = cuts[r], cuts[r + 1]
+            hdr = pl.sync()
+            pf, ev = pl.lists(hdr)
+            assert np.array_equal(pf, p["prefetch"][(p["prefetch"] >= lo) & (p["prefetch"] < hi)]), (s, r)
+            assert np.array_equal(ev, p["evict"][(p["evict"] >= lo) & (p["evict"] < hi)]), (s, r)
+            assert np.array_equal(pl.resident(), p["resident"][lo:hi]), (s, r)
+            assert hdr["cut_bits"] == p["cut_bits"] and hdr["cut_rem"] == p["cut_rem"], (s, r)
+            assert hdr["kept_bytes"] == p["kept_bytes"], (s, r, hdr["kept_bytes"], p["kept_bytes"])
+            assert hdr["bytes_h2d"] == int(fp[pf].sum()), (s, r)
+            if transfer:
+                mo = oms[r].apply(rec[lo:hi], pf - lo, ev - lo)
+                assert hdr["bytes_d2h"] == mo["bytes_d2h"], (s, r)
+                d2h, h2d = pl.descriptors(hdr)
+                assert np.array_equal(h2d[:, 1], mo["h2d_page"]) and np.array_equal(h2d[:, 0], mo["h2d_host"]), (s, r)
+        res = p["resident"]
+    for pl in ranks:
+        pl.close()
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_world_threads_multikernel(G):
+    """The NCCL path's plan sequence (7 collectives per step) over the thread exchange, C4-shaped."""
+    n = 120_000
+    w = tg.config_c4(seed=11, steps=6, n=n)
+    cuts = [round(n * r / G) + (0 if r in (0, G) else 137 * r) for r in range(G + 1)]
+    run_world_threads(w, cuts)
+
+
+def test_world_threads_tie_cut_and_transfers():
+    """Tie cut inside rank 1 (id-order prefix across ranks through the gathered tie bytes) and
+    per-rank physical transfers on the multi-kernel world path."""
+    n = 30_000
+    rng = np.random.default_rng(5)
+    fp = rng.choice([1, 2, 3], n) * tg.PAGE_BYTES
+    blocks = tg.make_blocks([[tg.KIND_KV]] * n, [[int(f)] for f in fp])
+    rec = rec_of([dict(d=5, fp=int(fp[i])) for i in range(n)])[None]
+    budget = int(fp[:12_345].sum())
+    w = tg.Workload("ties", n, np.array([0]), rec, None, blocks, budget, np.full(3, 9.0, np.float32))
+    run_world_threads(w, [0, 10_000, 20_000, n])
+    w2 = tg.config_c2(seed=3, steps=8, n=3001, lora=4 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
+    run_world_threads(w2, [0, 1500, 3001], transfer=True)
