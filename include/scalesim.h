@@ -67,10 +67,15 @@ typedef enum {
                                        CTA's published offsets (cannot happen: grid co-resident) */
 #define SCALESIM_ST_LIMIT 32u       /* a large context (more than 12288 agents per SM, integer
                                        distances: the streaming single-kernel plan) met a step
-                                       outside its scope: D* >= 2048 ticks, or more than 256
-                                       eligible agents at finite distances >= 2048 ticks; the
-                                       step's plan is not produced (create the context with
-                                       SCALESIM_F_MULTI_KERNEL for such workloads) */
+                                       outside its scope: D* >= 2048 ticks, or more than 4096
+                                       eligible agents at finite distances >= 2048 ticks (128
+                                       per SM); the step's plan is not produced (create the
+                                       context with SCALESIM_F_MULTI_KERNEL for such workloads).
+                                       Not detected, also outside that kernel's scope: more than
+                                       65535 eligible agents of one SM's id range (one CTA tile:
+                                       contexts above ~9.7M agents) at the same distance value
+                                       (its per-CTA bucket counters are 32-bit sums of 16-bit
+                                       parts) */
 
 /* Config flags. */
 #define SCALESIM_F_NO_TRANSFER 1u   /* plan + byte accounting only: no arena, no pages, no copies
