@@ -459,14 +459,25 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         }
         const uint32_t t_r = tr[j];
         unsigned long long *P = d.f_pos + ((uint64_t)par * NB1 + o_lo + j) * FUSED_MAX_CTAS;
-        uint32_t ca = 0, ce = 0;  // running sums over the previous 32-CTA chunks
-        for (uint32_t q0 = 0; q0 < G; q0 += 32) {
-          const uint32_t q = q0 + lane;
-          const uint32_t v = q < G ? s.col[q * RB + j] : 0u;
-          const uint32_t a = v & 0xFFFFu, e = v >> 16;
-          const uint32_t ia = warp_incl_scan(a), ie = warp_incl_scan(e);
+        // lane l owns CTAs [l QP, (l + 1) QP) (QP <= 5): their counts summed in registers, one
+        // scan pair over the lanes, then the lane's own running sums (no chain of 32-CTA rounds)
+        constexpr int QMAX = (FUSED_MAX_CTAS + 31) / 32;
+        uint32_t vv[QMAX], a_l = 0, e_l = 0;
+#pragma unroll
+        for (int i = 0; i < QMAX; ++i) {
+          const uint32_t q = lane * QP + i;
+          vv[i] = ((uint32_t)i < QP && q < G) ? s.col[q * RB + j] : 0u;
+          a_l += vv[i] & 0xFFFFu;
+          e_l += vv[i] >> 16;
+        }
+        const uint32_t ia = warp_incl_scan(a_l), ie = warp_incl_scan(e_l);
+        uint32_t ca = ia - a_l, ce = ie - e_l;  // the CTAs before the lane's first
+        const uint32_t b = o_lo + j;
+#pragma unroll
+        for (int i = 0; i < QMAX; ++i) {
+          const uint32_t q = lane * QP + i;
+          const uint32_t v = vv[i], a = v & 0xFFFFu, e = v >> 16;
           // (only the entries a consumer reads: its list buckets, and CTA 0's / the last CTA's)
-          const uint32_t b = o_lo + j;
           const bool used =
 #ifdef NO_OWNER_SKIP
             true;
@@ -474,9 +485,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
             (b < bs ? a != 0u : (b > bs ? e != 0u : v != 0u)) || q == 0 || q == G - 1;
 #endif
           // prefetch: CTAs before q; evict: CTAs after q (total minus inclusive prefix)
-          if (q < G && used) st_relaxed_u64(&P[q], pack_ep(ep, w_n + ca + ia - a, w_r + t_r - (ce + ie)));
-          ca += __shfl_sync(0xFFFFFFFFu, ia, 31);
-          ce += __shfl_sync(0xFFFFFFFFu, ie, 31);
+          if ((uint32_t)i < QP && q < G && used) st_relaxed_u64(&P[q], pack_ep(ep, w_n + ca, w_r + t_r - (ce + e)));
+          ca += a;
+          ce += e;
         }
       }
     }
