@@ -268,6 +268,7 @@ struct ThreadGroup {
   std::condition_variable cv;
   int arrived = 0;
   uint64_t gen = 0;
+  uint64_t shard[FUSED_MAX_WORLD][2] = {};  // the ranks' id ranges (checked at the first collective)
   const void *in[FUSED_MAX_WORLD] = {};
   cudaEvent_t ev_in[FUSED_MAX_WORLD] = {}, ev_red[FUSED_MAX_WORLD] = {};
   void barrier() {
@@ -689,6 +690,19 @@ extern "C" scalesim_status scalesim_init(const scalesim_config *cfg, const scale
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_unique_id, sizeof(id));
     if (g_nccl.CommInitRank(&c->comm, cfg->world, id, cfg->rank) != ncclSuccess) return fail(SCALESIM_E_NCCL);
+    // the ranks' shards must be contiguous, in rank order and cover [0, n_agents) (the tie prefix
+    // over lower ranks assumes it): all-gather (shard_begin, shard_end) once
+    uint64_t *g = reinterpret_cast<uint64_t *>(p.d.xscratch);
+    const uint64_t mine[2] = {cfg->shard_begin, cfg->shard_end};
+    std::vector<uint64_t> all(2 * cfg->world);
+    if (cudaMemcpyAsync(g, mine, 16, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        g_nccl.AllGather(g, g + 2, 2, ncclUint64, c->comm, c->stream) != ncclSuccess ||
+        cudaMemcpyAsync(all.data(), g + 2, 16 * cfg->world, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+      return fail(SCALESIM_E_NCCL);
+    for (int r = 0; r < cfg->world; ++r)
+      if (all[2 * r] != (r == 0 ? 0 : all[2 * r - 1]) || (r == cfg->world - 1 && all[2 * r + 1] != cfg->n_agents))
+        return fail(SCALESIM_E_INVALID);
   }
   *out = c;
   return SCALESIM_OK;
@@ -740,7 +754,13 @@ static scalesim_status allreduce(scalesim_ctx *c, void *buf, size_t n, ncclDataT
   CK(cudaEventRecord(c->ev_xin, c->stream));
   g.in[r] = buf;
   g.ev_in[r] = c->ev_xin;
+  g.shard[r][0] = c->cfg.shard_begin;
+  g.shard[r][1] = c->cfg.shard_end;
   g.barrier();
+  // (every rank sees the same shards: all fail together, before the next barrier)
+  for (int q = 0; q < G; ++q)
+    if (g.shard[q][0] != (q == 0 ? 0 : g.shard[q - 1][1]) || (q == G - 1 && g.shard[q][1] != c->cfg.n_agents))
+      return SCALESIM_E_INVALID;
   for (int q = 0; q < G; ++q)
     if (q != r) CK(cudaStreamWaitEvent(c->stream, g.ev_in[q], 0));
   c->launches += launch_xreduce(c->p.d.xscratch, g.in, (uint32_t)G, n, t == ncclUint64 ? 0 : 1, c->stream);

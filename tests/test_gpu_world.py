@@ -361,3 +361,38 @@ def test_world_threads_tie_cut_and_transfers():
     run_world_threads(w, [0, 10_000, 20_000, n])
     w2 = tg.config_c2(seed=3, steps=8, n=3001, lora=4 * tg.PAGE_BYTES, kv=tg.PAGE_BYTES)
     run_world_threads(w2, [0, 1500, 3001], transfer=True)
+
+
+def test_world_threads_rejects_non_contiguous_shards():
+    """the tie prefix over lower ranks assumes contiguous shards in rank order; a world
+    whose shards leave a gap fails its first collective with SCALESIM_E_INVALID on every rank."""
+    import threading
+    from paper_2601_21473_b200 import _lib as L
+    from paper_2601_21473_b200.planner import Planner
+    n = 4000
+    w = tg.config_c4(seed=2, steps=1, n=n)
+    cuts = [(0, 1500), (1700, n)]
+    gid = bytes([9, 2]) + bytes(126)
+    ranks = []
+    for r, (lo, hi) in enumerate(cuts):
+        bp, bs, bo, bk = shard_blocks(w.blocks, lo, hi)
+        ranks.append(Planner(n, bp, bs, bo, bk, w.budget, w.theta, transfer=False, shard=(lo, hi), rank=r, world=2,
+                             nccl_id=gid, threads=True, keep_dist=False))
+    codes = {}
+
+    def run(r):
+        lo, hi = cuts[r]
+        ranks[r].set_records(w.rec[0][lo:hi])
+        try:
+            ranks[r].step(int(w.now[0]))
+            codes[r] = 0
+        except L.ScaleSimError as e:
+            codes[r] = e.status
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=60)
+    assert codes == {0: L.E_INVALID, 1: L.E_INVALID}, codes
+    for pl in ranks:
+        pl.close()
