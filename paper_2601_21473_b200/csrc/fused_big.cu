@@ -260,8 +260,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   STAMP_MAX(26)  // published
   wgrid.sync();
   STAMP_MAX(4)   // B1
-  // the first chunk P34 decodes (the highest) into L2 while the select and the owners run
-  if (threadIdx.x == 0 && tw_here) prefetch_chunk_codes(codes, tw_here, (int)((tw_here - 1) / BIG_CW));
+  // P34's word range of each warp (its codes into L2 while the select and the owners run)
+  const uint32_t WPW = (tw_here + FWARPS - 1) / FWARPS;
+  const uint32_t wlo = min(tw_here, (uint32_t)warp * WPW), whi = min(tw_here, wlo + WPW);
+  if (lane == 0 && whi > wlo)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(codes + (uint64_t)wlo * 32), "r"((whi - wlo) * 64u)
+                 : "memory");
 
   // ---------------- select, bucket owners, list-bucket positions
   {
@@ -319,9 +323,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   // the code stashes: the first chunk P34 decodes (the highest) is copied in meanwhile.
   unsigned long long h2d = 0;
   for (uint32_t b = threadIdx.x; b < bs; b += FT) h2d += ((unsigned long long)nrb[NB1 + b] << 16) + nrb[b];
-  const uint32_t n_chunks = (tw_here + BIG_CW - 1) / BIG_CW;
   __syncthreads();
-  if (n_chunks) stash_chunk(R, codes, tw_here, (int)n_chunks - 1);
   // preceding CTAs' bytes at D* (tie prefix), and this CTA's own
   __shared__ unsigned long long sh_town;
   unsigned long long t_rows = 0;
@@ -459,67 +461,79 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   }
 
   STAMP_MAX(17)  // positions
-  // ---------------- P34: chunks of words from the highest id down
-  PROBE(unsigned long long dta = 0, dtb = 0, dtc = 0, dtd = 0, tq = gtimer();)  // (dtd: unused)
+  // ---------------- P34: one pass, each warp over its own word range from the highest id down
+  // (no CTA barrier inside: the warps' code loads overlap).  Two words per step: half-warp h
+  // holds word hw - 1 + h, lane j of a half the 32-bit pair j of its word (agents j and j + 16,
+  // P1's lane permutation); ballots assemble the word masks.  Decisions that need the other
+  // warps (the tie group's id-order prefix) are deferred: tie agents, and the evicted dirty
+  // agents whose write-back bytes are summed, go to per-warp lists and are resolved after the
+  // pass.  List candidates (bucket << 20 | kept << 19 | k) go to per-warp slabs of the tile's
+  // scratch range, each in descending id order; the placement reads them warp 31 first.
+  PROBE(unsigned long long dta = 0, dtb = 0, dtc = 0, dtd = 0, tq = gtimer();)
 #define LAP(v) PROBE(if (threadIdx.x == 0) { const unsigned long long t_ = gtimer(); v += t_ - tq; tq = t_; })
   unsigned long long tie_kept = 0, d2h = 0;
   uint32_t n_el = 0, n_pfb = 0, n_evb = 0;
-  unsigned long long above = 0;  // tie bytes of the chunks done (all above this chunk)
   const unsigned long long rem = sel.rem;
-  // this CTA's list candidates (HBM scratch of the tile's range): bucket << 20 | kept << 19 | k
-  uint32_t *g_lpf = d.sort_ka + base, *g_lev = d.sort_va + base;
-  uint32_t n_lpf = 0, n_lev = 0;  // (CTA-uniform)
   const bool cta_mv = s_novf > 0;  // this CTA holds eligible agents in multi-valued buckets
-  uint32_t buf = 0;  // (two stashes: the current one)
-  for (int ch = (int)n_chunks - 1; ch >= 0; --ch, buf ^= 1u) {
-    const uint32_t w0 = (uint32_t)ch * BIG_CW, wn = min(BIG_CW, tw_here - w0);
-    const uint32_t rmw = threadIdx.x < wn ? bm_old[(base >> 5) + w0 + threadIdx.x] : 0u;  // (issued before the wait)
-#if BIG_NSTASH == 2
-    // the next chunk's codes into the other stash while this one is processed
-    if (ch > 0) {
-      stash_chunk(R + (buf ^ 1u) * BIG_STASH, codes, tw_here, ch - 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      cp_async_wait_all();
-    }
-    const uint8_t *stash = R + buf * BIG_STASH;
-#else
-    if (threadIdx.x == 0) prefetch_chunk_codes(codes, tw_here, ch - 1);  // (L2, for the refill below)
-    cp_async_wait_all();
-    const uint8_t *stash = R;
-#endif
-    __syncthreads();
-    // Word w0 + i belongs to thread i in every step of the chunk: its masks stay in registers.
-    const uint32_t i = threadIdx.x, w = w0 + i;
-    const uint32_t sw = (i >> 1) & 3u;  // the word's unit swizzle in the stash
-    const bool mine = i < wn;
-    // (a) the word's masks from its 32 codes, two per 32-bit pair by SWAR: eligible (bit 12 of
-    // each half); with a guard bit over each 12-bit bucket q, bit 12 of (q + 4096 - t) is
-    // q >= t (no borrow crosses the halves): below / at the boundary bucket, and the multi-valued
-    // range [2048, 3920) where this CTA has such agents; pair j holds agents j and j + 16, so
-    // one shift puts both bits in place.  Resident: the old residency word.
-    uint32_t em = 0, rm = 0, mv = 0, lm = 0, tm = 0, pm = 0;
-    unsigned long long tb = 0, tbn = 0;  // the word's tie bytes (all, non-resident)
-    if (mine) {
-      rm = rmw;
-      auto pair = [&](int j) {
-        return *reinterpret_cast<const uint32_t *>(stash + 16 * ((4 * i + (j >> 2)) ^ sw) + 4 * (j & 3));
+  const uint32_t slab = wlo * 32;  // this warp's slab in the tile-range scratch arrays
+  uint32_t *w_pf = d.sort_ka + base + slab, *w_ev = d.sort_va + base + slab;  // candidates
+  uint32_t *w_tk = d.pfa_key + base + slab, *w_tp = d.pfa_val + base + slab;  // ties: k | res, dirty; slab pos
+  uint32_t *w_wb = d.f_sk3 + base + slab;                                     // evicted dirty (not ties)
+  uint32_t o_pf = 0, o_ev = 0, o_t = 0, o_w = 0;  // (warp-uniform)
+  {
+    // thread-per-word: step s of warp w covers the 32 words [whi - 32 (s + 1), whi - 32 s), lane
+    // l the word whi - 32 s - 32 + l (coalesced 64-byte rows); the lane's four 16-byte loads of
+    // the next step go out before this step is decoded
+    const uint4 *codes4 = reinterpret_cast<const uint4 *>(codes);
+    const uint32_t *bmt = bm_old + (base >> 5);
+    const uint32_t nst = (whi - wlo + 31) / 32;
+    uint4 c4[4];
+    uint32_t crm = 0;
+    auto load_step = [&](uint32_t t) {
+      const int wd = (int)whi - 32 * ((int)t + 1) + lane;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c4[u] = make_uint4(0, 0, 0, 0);
+      crm = 0;
+      if (t < nst && wd >= (int)wlo) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c4[u] = codes4[(uint32_t)wd * 4 + u];
+        crm = bmt[wd];
+      }
+    };
+    load_step(0);
+    constexpr uint32_t G12 = 0x10001000u;
+    const uint32_t B0 = bs * 0x10001u, B1 = (bs + 1u) * 0x10001u;  // (bs < 4096 unless all fit)
+#pragma unroll 1
+    for (uint32_t t = 0; t < nst; ++t) {
+      const uint4 q0 = c4[0], q1 = c4[1], q2 = c4[2], q3 = c4[3];
+      const uint32_t rmw = crm;
+      load_step(t + 1);
+      const int wd = (int)whi - 32 * ((int)t + 1) + lane;
+      const bool on = wd >= (int)wlo;
+      auto pair = [&](int jj) -> uint32_t {
+        const uint4 &qq = jj < 4 ? q0 : (jj < 8 ? q1 : (jj < 12 ? q2 : q3));
+        const int r = jj & 3;
+        return r == 0 ? qq.x : (r == 1 ? qq.y : (r == 2 ? qq.z : qq.w));
       };
-      constexpr uint32_t G12 = 0x10001000u;
 #define SWAR_SH(v, j) ((j) <= 12 ? (v) >> (12 - (j)) : (v) << ((j) - 12))
+      uint32_t em = 0, lm = 0, tm = 0, mv = 0, dm = 0;
       if (all_fit) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) em |= SWAR_SH(pair(j) & G12, j);
+        for (int jj = 0; jj < 16; ++jj) {
+          const uint32_t W = pair(jj);
+          em |= SWAR_SH(W & G12, jj);
+          dm |= SWAR_SH((W >> 1) & G12, jj);
+        }
         lm = em;
       } else {
-        const uint32_t B0 = bs * 0x10001u, B1 = (bs + 1u) * 0x10001u;  // (bs < 4096)
-        uint32_t ge0 = 0, ge1 = 0;  // q >= bs, q >= bs + 1
+        uint32_t ge0 = 0, ge1 = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t W = pair(j), X = (W & 0x0FFF0FFFu) | G12;
-          em |= SWAR_SH(W & G12, j);
-          ge0 |= SWAR_SH((X - B0) & G12, j);
-          ge1 |= SWAR_SH((X - B1) & G12, j);
+        for (int jj = 0; jj < 16; ++jj) {
+          const uint32_t W = pair(jj), X = (W & 0x0FFF0FFFu) | G12;
+          em |= SWAR_SH(W & G12, jj);
+          dm |= SWAR_SH((W >> 1) & G12, jj);
+          ge0 |= SWAR_SH((X - B0) & G12, jj);
+          ge1 |= SWAR_SH((X - B1) & G12, jj);
         }
         lm = em & ~ge0;
         tm = em & ge0 & ~ge1;
@@ -527,142 +541,143 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       if (cta_mv) {  // (CTA-uniform, rare)
         uint32_t m0 = 0, m1 = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t X = (pair(j) & 0x0FFF0FFFu) | G12;
-          m0 |= SWAR_SH((X - (uint32_t)IB_EXACT * 0x10001u) & G12, j);
-          m1 |= SWAR_SH((X - (uint32_t)IB_INF * 0x10001u) & G12, j);
+        for (int jj = 0; jj < 16; ++jj) {
+          const uint32_t X = (pair(jj) & 0x0FFF0FFFu) | G12;
+          m0 |= SWAR_SH((X - (uint32_t)IB_EXACT * 0x10001u) & G12, jj);
+          m1 |= SWAR_SH((X - (uint32_t)IB_INF * 0x10001u) & G12, jj);
         }
         mv = em & m0 & ~m1;
       }
 #undef SWAR_SH
-      pm = em & ~rm & ~mv & (all_fit ? 0xFFFFFFFFu : (lm | tm));
-      for (uint32_t m = tm; m; m &= m - 1) {  // (ties: few)
-        const int l = __ffs(m) - 1;
-        const uint32_t fp = rec[w * 32 + l].y;
-        tb += fp;
-        if (!((rm >> l) & 1u)) tbn += fp;
+      if (!on) em = lm = tm = mv = dm = 0;
+      const uint32_t rm = on ? rmw : 0u;
+      const uint32_t pm = em & ~rm & ~mv & (lm | tm), ec = rm & ~lm & ~mv;
+      const uint32_t wbm = rm & ~lm & ~tm & dm;  // evicted whatever the cut, dirty
+      if (on) {
+        bm_new[(base >> 5) + wd] = lm;  // (kept ties OR'ed in after the pass)
+        n_el += __popc(em);
+      }
+      // list offsets of this step in descending id order: the higher lanes first
+      const uint32_t npm = __popc(pm), nec = __popc(ec), ntm = __popc(tm), nwb = __popc(wbm);
+      const unsigned long long c01 = (unsigned long long)npm | ((unsigned long long)nec << 32);
+      const unsigned long long c23 = (unsigned long long)ntm | ((unsigned long long)nwb << 32);
+      unsigned long long i01 = c01, i23 = c23;  // inclusive suffix sums (lanes >= l)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long x01 = __shfl_down_sync(0xFFFFFFFFu, i01, o);
+        const unsigned long long x23 = __shfl_down_sync(0xFFFFFFFFu, i23, o);
+        if (lane + o < 32) {
+          i01 += x01;
+          i23 += x23;
+        }
+      }
+      const unsigned long long t01 = __shfl_sync(0xFFFFFFFFu, i01, 0), t23 = __shfl_sync(0xFFFFFFFFu, i23, 0);
+      uint32_t bpf = o_pf + (uint32_t)(i01 - c01), bev = o_ev + (uint32_t)((i01 - c01) >> 32);
+      uint32_t bt = o_t + (uint32_t)(i23 - c23), bw = o_w + (uint32_t)((i23 - c23) >> 32);
+      o_pf += (uint32_t)t01;
+      o_ev += (uint32_t)(t01 >> 32);
+      o_t += (uint32_t)t23;
+      o_w += (uint32_t)(t23 >> 32);
+      const uint32_t kb = (uint32_t)wd * 32 - slab;  // (slab-relative id of the word's agent 0)
+      // the word's candidates, ties and write-backs, from its highest agent down; a code's place
+      // in the word: agent a sits in pair a % 16, half a / 16
+      for (uint32_t m = pm | ec | tm | wbm; m; ) {
+        const uint32_t a = 31 - __clz(m);
+        m &= ~(1u << a);
+        const uint32_t q = codes[(uint32_t)wd * 32 + (((a & 15u) << 1) | (a >> 4))] & 0xFFFu, bit = 1u << a;
+        uint32_t cpos = 0xFFFFFFFFu;
+        if (pm & bit) {
+          w_pf[bpf] = (q << 20) | (((lm >> a) & 1u) << 19) | (kb + a);
+          cpos = bpf++;
+        } else if (ec & bit) {
+          w_ev[bev] = (q << 20) | (kb + a);
+          cpos = (bev++) | 0x80000000u;
+        }
+        if (tm & bit) {
+          w_tk[bt] = (kb + a + slab) | (((rm >> a) & 1u) << 31) | (((dm >> a) & 1u) << 30);
+          w_tp[bt++] = cpos;
+        }
+        if (wbm & bit) w_wb[bw++] = kb + a + slab;
       }
     }
-    const uint32_t ec = rm & ~lm & ~mv;  // evict candidates
-    LAP(dta)
-    // (b) one scan: the words' tie bytes in id order (the chunk's ties start after the preceding
-    // CTAs' and this CTA's below the chunk = own total - chunks above - this chunk) and their
-    // candidate counts (list offsets in descending id order: total - inclusive prefix)
-    unsigned long long lo, cv;
-    uint32_t tcp, tce;
-    {
-      unsigned long long v[2] = {tb, (unsigned long long)__popc(pm) | ((unsigned long long)__popc(ec) << 32)}, tt[2];
-      cta_scan2(v, tt);
-      lo = tie_pre + (tie_own - above - tt[0]) + v[0];
-      above += tt[0];
-      cv = v[1];
-      tcp = (uint32_t)tt[1];
-      tce = (uint32_t)(tt[1] >> 32);
-    }
-    LAP(dtb)
-    if (mine) {
-      // (c) kept / prefetch / evict words, residency, byte sums
-      uint32_t kw = lm;
-      if (tm) {
-        const unsigned long long hi = lo + tb;
-        if (hi <= rem) {
-          kw |= tm;
-          tie_kept += tb;
-          h2d += tbn;
-        } else if (lo <= rem) {  // the straddling word: its ties in id order
-          unsigned long long incl = lo;
-          for (uint32_t m = tm; m; m &= m - 1) {
-            const int l = __ffs(m) - 1;
-            const uint32_t fp = rec[w * 32 + l].y;
-            incl += fp;
-            if (incl <= rem) {
-              kw |= 1u << l;
-              tie_kept += fp;
-              if (!((rm >> l) & 1u)) h2d += fp;
-            }
-          }
-        }
-      }
-      const uint32_t pfw = kw & ~rm, evw = rm & ~kw;
-      if (w < tw_here) bm_new[(base >> 5) + w] = kw;
-      n_el += __popc(em);
-      n_pfb += __popc(pfw & tm);
-      n_evb += __popc(evw & tm);
-      // write-back bytes of the dirty evicted agents: up to four per round trip (most words have
-      // none or one)
-      uint32_t me = 0;  // the dirty ones among them (dirty bit of the stashed code)
-      for (uint32_t m = evw; m; m &= m - 1) {
-        const uint32_t l = __ffs(m) - 1, pos = ((l & 15u) << 1) | (l >> 4);
-        if ((*reinterpret_cast<const uint16_t *>(stash + 16 * ((4 * i + (pos >> 3)) ^ sw) + 2 * (pos & 7u)) >> 13) & 1u)
-          me |= 1u << l;
-      }
-      while (me) {
-        uint32_t u[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          u[k] = 0;
-          if (me) {
-            u[k] = d.wb_bytes[base + w * 32 + __ffs(me) - 1];
-            me &= me - 1;
-          }
-        }
-        d2h += (unsigned long long)u[0] + u[1] + u[2] + u[3];
-      }
-      // (d) the word's candidates appended in descending id order to this CTA's two candidate
-      // lists (HBM scratch, placed once after the last chunk), each with its kept bit; four
-      // code loads per round trip (the lists are disjoint: non-resident / resident)
-      uint32_t op = n_lpf + tcp - (uint32_t)cv - __popc(pm);
-      uint32_t oe = n_lev + tce - (uint32_t)(cv >> 32) - __popc(ec);
-      const uint32_t wbase = w * 32;
-      uint32_t m = pm | ec;
-      while (m) {
-        uint32_t bt[4], cd[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          bt[u] = 32;
-          cd[u] = 0;
-          if (m) {
-            bt[u] = 31 - __clz(m);
-            m &= ~(1u << bt[u]);
-            const uint32_t pos = ((bt[u] & 15u) << 1) | (bt[u] >> 4);  // (the code's place in the word)
-            cd[u] = *reinterpret_cast<const uint16_t *>(stash + 16 * ((4 * i + (pos >> 3)) ^ sw) + 2 * (pos & 7u));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (bt[u] == 32) break;
-          const uint32_t bit = bt[u], x = ((cd[u] & 0xFFFu) << 20) | (((kw >> bit) & 1u) << 19) | (wbase + bit);
-          if ((pm >> bit) & 1u) g_lpf[op++] = x;
-          else g_lev[oe++] = x;
-        }
-      }
-    }
-    n_lpf += tcp;
-    n_lev += tce;
-    LAP(dtc)
-    __syncthreads();  // (the stash is refilled; the placement reads every thread's candidates)
-#if BIG_NSTASH == 1
-    if (ch > 0) stash_chunk(R, codes, tw_here, ch - 1);
-#endif
   }
-  PROBE(if (threadIdx.x == 0) {
-    atomicMax(&prof[22], dta);
-    atomicMax(&prof[23], dtb);
-    atomicMax(&prof[24], dtc);
-    atomicMax(&prof[29], dtd);
-  })
+  // write-back bytes of the warp's other evicted dirty agents (R13): its list, 32 loads at a time
+  for (uint32_t i = lane; i < o_w; i += 32) d2h += d.wb_bytes[base + w_wb[i]];
+  LAP(dta)
+  // the warps' list lengths: candidates / ties / write-backs
+  __shared__ uint32_t s_cnt[4][FWARPS], s_pre[4][FWARPS + 1];
+  if (lane == 0) {
+    s_cnt[0][warp] = o_pf;
+    s_cnt[1][warp] = o_ev;
+    s_cnt[2][warp] = o_t;
+    s_cnt[3][warp] = o_w;
+  }
+  __syncthreads();
+  if (warp < 4) {  // [0], [1]: warp 31 first (list order); [2], [3]: warp 0 first (ascending id)
+    const uint32_t src = warp < 2 ? (uint32_t)(FWARPS - 1 - lane) : (uint32_t)lane;
+    const uint32_t c = s_cnt[warp][src], inc = warp_incl_scan(c);
+    s_pre[warp][lane] = inc - c;
+    if (lane == 31) s_pre[warp][FWARPS] = inc;
+  }
+  __syncthreads();
+  // ties in ascending id order (warp w's list reversed, after the lower warps'); their bytes'
+  // inclusive prefix decides each one (kept iff tie_pre + prefix <= rem, P:241 R3).  Each warp
+  // stages its ties (entry, candidate place, bytes) at their ascending positions in shared
+  // memory (region R, free now), TCAP at a time
+  {
+    const uint32_t nt = s_pre[2][FWARPS];
+    constexpr uint32_t TCAP = 4096;  // ties per round (3 x 16 KB of R)
+    uint32_t *t_e = reinterpret_cast<uint32_t *>(R), *t_c = t_e + TCAP, *t_f = t_c + TCAP;
+    __shared__ unsigned long long s_tot;
+    unsigned long long carry = 0;
+    const uint32_t my_n = s_cnt[2][warp], my_pre = s_pre[2][warp];
+    for (uint32_t g0 = 0; g0 < nt; g0 += TCAP) {  // (CTA-uniform)
+      for (uint32_t i = lane; i < my_n; i += 32) {
+        const uint32_t g = my_pre + (my_n - 1 - i);
+        if (g < g0 || g >= g0 + TCAP) continue;
+        const uint32_t e = w_tk[i], cp = w_tp[i];
+        t_e[g - g0] = e;
+        t_c[g - g0] = cp == 0xFFFFFFFFu ? cp : (cp & 0x80000000u) | (slab + (cp & 0x7FFFFFFFu));  // (tile-relative)
+        t_f[g - g0] = rec[e & 0x7FFFFu].y;
+      }
+      __syncthreads();
+      const uint32_t nr = min(TCAP, nt - g0);
+      for (uint32_t x0 = 0; x0 < nr; x0 += FT) {  // (CTA-uniform)
+        const uint32_t x = x0 + threadIdx.x;
+        const uint32_t fp = x < nr ? t_f[x] : 0u;
+        const unsigned long long ex = block_excl_scan<unsigned long long, FT>((unsigned long long)fp, &s_tot);
+        if (x < nr) {
+          const bool kept = tie_pre + carry + ex + fp <= rem;
+          const uint32_t e = t_e[x], cp = t_c[x], k = e & 0x7FFFFu;
+          const bool res = (e >> 31) & 1u, dirty = (e >> 30) & 1u;
+          if (kept) {
+            atomicOr(&bm_new[(base >> 5) + (k >> 5)], 1u << (k & 31));
+            if (cp != 0xFFFFFFFFu) atomicOr((cp >> 31) ? &d.sort_va[base + (cp & 0x7FFFFFFFu)] : &d.sort_ka[base + cp], 1u << 19);
+            tie_kept += fp;
+            if (!res) {
+              h2d += fp;
+              ++n_pfb;
+            }
+          } else if (res) {
+            ++n_evb;
+            if (dirty) d2h += d.wb_bytes[base + k];
+          }
+        }
+        carry += s_tot;
+      }
+      __syncthreads();
+    }
+  }
+  LAP(dtb)
+  __syncthreads();  // (the tie patches of the candidate entries are visible to the placement)
   // (e) placement: per list, a stable sort of the candidates by bucket (list order kept within a
   // bucket); a candidate's rank in its bucket = sorted index - the bucket's first index; evict
   // positions count up from the bucket's cursor, prefetch positions down from its last one
-  // (only kept candidates are members)
-  // The sort runs in shared memory (region R: counters + four arrays) when the list fits,
-  // else on HBM scratch.
+  // (only kept candidates are members).  The sort runs in shared memory (region R: counters +
+  // four arrays) when the list fits, else on HBM scratch.
   const uint32_t *cur_pf = h32, *cur_ev = h32 + NB1;
   auto place = [&](uint32_t x, uint32_t pos, bool pf) {  // x: a member's candidate entry
     if (pos >= p.n_local) {  // (cannot happen: flagged instead of writing out of bounds)
-#ifdef DEBUG_SYNC
-      atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), 1u << 20);
-#endif
       atomicOr(reinterpret_cast<unsigned int *>(&d.header[H_STATUS]), ST_SYNC);
       return;
     }
@@ -673,9 +688,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     uint32_t *start = h + 2 * NB1;  // [NB1] first sorted index per bucket (the counts are no longer needed)
     uint32_t *cnt = reinterpret_cast<uint32_t *>(R);  // 256 x SW sort counters
     for (int lst = 0; lst < 2; ++lst) {
-      const uint32_t n = lst == 0 ? n_lpf : n_lev;
+      const uint32_t n = s_pre[lst][FWARPS];
       if (n == 0) continue;  // (CTA-uniform)
-      const uint32_t *src = lst == 0 ? g_lpf : g_lev;
+      const uint32_t *src = lst == 0 ? d.sort_ka + base : d.sort_va + base;
       uint32_t *ka, *ia, *kb, *ib;  // keys (buckets) and values (the entries)
       if (n <= SMAX) {
         ka = cnt + 256 * SW;
@@ -688,10 +703,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         kb = d.f_sk2 + base;
         ib = d.f_sv2 + base;
       }
-      for (uint32_t e = threadIdx.x; e < n; e += FT) {
-        const uint32_t x = src[e];
-        ka[e] = x >> 20;
-        ia[e] = x;
+      {  // the slabs, warp 31's first: each warp copies its own
+        const uint32_t mine = s_cnt[lst][warp], at = s_pre[lst][FWARPS - 1 - warp];
+        for (uint32_t i = lane; i < mine; i += 32) {
+          const uint32_t x0 = src[slab + i];
+          const uint32_t x = (x0 & 0xFFF80000u) | (slab + (x0 & 0x7FFFFu));  // (tile-relative k)
+          ka[at + i] = x >> 20;
+          ia[at + i] = x;
+        }
       }
       __syncthreads();
       cta_sort_pairs(ka, ia, kb, ib, n, cnt);
@@ -707,6 +726,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       __syncthreads();
     }
   }
+  LAP(dtc)
+  PROBE(if (threadIdx.x == 0) {
+    atomicMax(&prof[22], dta);
+    atomicMax(&prof[23], dtb);
+    atomicMax(&prof[24], dtc);
+    atomicMax(&prof[29], dtd);
+  })
   STAMP_MAX(39)  // P34 done
   // the agents in multi-valued buckets (all CTAs'): one CTA sorts them -- prefetch members
   // (non-residents below b*) ascending by (key, id) after the value buckets below 2048, evict
