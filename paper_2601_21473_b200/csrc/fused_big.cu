@@ -263,9 +263,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   // P34's word range of each warp (its codes into L2 while the select and the owners run)
   const uint32_t WPW = (tw_here + FWARPS - 1) / FWARPS;
   const uint32_t wlo = min(tw_here, (uint32_t)warp * WPW), whi = min(tw_here, wlo + WPW);
-  if (lane == 0 && whi > wlo)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(codes + (uint64_t)wlo * 32), "r"((whi - wlo) * 64u)
+  // (the first P34_PF steps of 32 words, 2 KB each, from the top of the range down)
+  constexpr uint32_t P34_PF = 4;
+  if (lane == 0 && whi > wlo) {
+    const uint32_t n0 = min(whi - wlo, 32 * P34_PF);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(codes + (uint64_t)(whi - n0) * 32), "r"(n0 * 64u)
                  : "memory");
+  }
 
   // ---------------- select, bucket owners, list-bucket positions
   {
@@ -475,6 +479,21 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   uint32_t n_el = 0, n_pfb = 0, n_evb = 0;
   const unsigned long long rem = sel.rem;
   const bool cta_mv = s_novf > 0;  // this CTA holds eligible agents in multi-valued buckets
+  // the words holding them (from P1's list of this CTA's such agents: at most LOVF): only those
+  // words decode the multi-valued mask
+  __shared__ uint32_t s_mvw[FUSED_BIG_MAX_TILE / 1024];
+  if (cta_mv) {  // (CTA-uniform)
+    for (uint32_t x = threadIdx.x; x < FUSED_BIG_MAX_TILE / 1024; x += FT) s_mvw[x] = 0;
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < min(s_novf, LOVF); x += FT) {
+      const uint32_t k = s_ovf[x].y - (uint32_t)(p.shard_begin + base);
+      atomicOr(&s_mvw[k >> 10], 1u << ((k >> 5) & 31u));
+    }
+    __syncthreads();
+  }
+  __shared__ uint32_t s_wbn[FWARPS];  // the warps' write-back list lengths
+  if (lane == 0) s_wbn[warp] = 0;
+  __syncwarp();
   const uint32_t slab = wlo * 32;  // this warp's slab in the tile-range scratch arrays
   uint32_t *w_pf = d.sort_ka + base + slab, *w_ev = d.sort_va + base + slab;  // candidates
   uint32_t *w_tk = d.pfa_key + base + slab, *w_tp = d.pfa_val + base + slab;  // ties: k | res, dirty; slab pos
@@ -485,6 +504,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     // l the word whi - 32 s - 32 + l (coalesced 64-byte rows); the lane's four 16-byte loads of
     // the next step go out before this step is decoded
     const uint4 *codes4 = reinterpret_cast<const uint4 *>(codes);
+    uint8_t *const myrow = R + 64u * threadIdx.x;  // (region R is free during the pass: 1024 x 64 B)
     const uint32_t *bmt = bm_old + (base >> 5);
     const uint32_t nst = (whi - wlo + 31) / 32;
     uint4 c4[4];
@@ -507,7 +527,21 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     for (uint32_t t = 0; t < nst; ++t) {
       const uint4 q0 = c4[0], q1 = c4[1], q2 = c4[2], q3 = c4[3];
       const uint32_t rmw = crm;
+      {  // the word's codes also into the thread's 64-byte row of region R (16-byte units swizzled:
+         // a quarter warp's stores hit eight distinct bank groups), read back by the candidates
+        const uint32_t sz = (threadIdx.x >> 1) & 3u;
+        uint4 *row4 = reinterpret_cast<uint4 *>(myrow);
+        row4[0 ^ sz] = q0;
+        row4[1 ^ sz] = q1;
+        row4[2 ^ sz] = q2;
+        row4[3 ^ sz] = q3;
+      }
       load_step(t + 1);
+      if (lane == 0 && t + P34_PF < nst) {  // step t + P34_PF into L2 (the range's codes do not all fit L2 at once)
+        const int w1 = (int)whi - 32 * (int)(t + P34_PF), w0 = max((int)wlo, w1 - 32);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(codes + (uint64_t)w0 * 32), "r"((uint32_t)(w1 - w0) * 64u)
+                     : "memory");
+      }
       const int wd = (int)whi - 32 * ((int)t + 1) + lane;
       const bool on = wd >= (int)wlo;
       auto pair = [&](int jj) -> uint32_t {
@@ -516,14 +550,10 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         return r == 0 ? qq.x : (r == 1 ? qq.y : (r == 2 ? qq.z : qq.w));
       };
 #define SWAR_SH(v, j) ((j) <= 12 ? (v) >> (12 - (j)) : (v) << ((j) - 12))
-      uint32_t em = 0, lm = 0, tm = 0, mv = 0, dm = 0;
+      uint32_t em = 0, lm = 0, tm = 0, mv = 0;
       if (all_fit) {
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const uint32_t W = pair(jj);
-          em |= SWAR_SH(W & G12, jj);
-          dm |= SWAR_SH((W >> 1) & G12, jj);
-        }
+        for (int jj = 0; jj < 16; ++jj) em |= SWAR_SH(pair(jj) & G12, jj);
         lm = em;
       } else {
         uint32_t ge0 = 0, ge1 = 0;
@@ -531,14 +561,13 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         for (int jj = 0; jj < 16; ++jj) {
           const uint32_t W = pair(jj), X = (W & 0x0FFF0FFFu) | G12;
           em |= SWAR_SH(W & G12, jj);
-          dm |= SWAR_SH((W >> 1) & G12, jj);
           ge0 |= SWAR_SH((X - B0) & G12, jj);
           ge1 |= SWAR_SH((X - B1) & G12, jj);
         }
         lm = em & ~ge0;
         tm = em & ge0 & ~ge1;
       }
-      if (cta_mv) {  // (CTA-uniform, rare)
+      if (cta_mv && on && ((s_mvw[(uint32_t)wd >> 5] >> (wd & 31)) & 1u)) {  // (rare: a word with such agents)
         uint32_t m0 = 0, m1 = 0;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
@@ -549,16 +578,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         mv = em & m0 & ~m1;
       }
 #undef SWAR_SH
-      if (!on) em = lm = tm = mv = dm = 0;
+      if (!on) em = lm = tm = mv = 0;
       const uint32_t rm = on ? rmw : 0u;
       const uint32_t pm = em & ~rm & ~mv & (lm | tm), ec = rm & ~lm & ~mv;
-      const uint32_t wbm = rm & ~lm & ~tm & dm;  // evicted whatever the cut, dirty
+      const uint32_t evk = rm & ~lm & ~tm;  // evicted whatever the cut (write-back bytes if dirty)
       if (on) {
         bm_new[(base >> 5) + wd] = lm;  // (kept ties OR'ed in after the pass)
         n_el += __popc(em);
       }
       // list offsets of this step in descending id order: the higher lanes first
-      const uint32_t npm = __popc(pm), nec = __popc(ec), ntm = __popc(tm), nwb = __popc(wbm);
+      const uint32_t npm = __popc(pm), nec = __popc(ec), ntm = __popc(tm), nwb = 0;
       const unsigned long long c01 = (unsigned long long)npm | ((unsigned long long)nec << 32);
       const unsigned long long c23 = (unsigned long long)ntm | ((unsigned long long)nwb << 32);
       unsigned long long i01 = c01, i23 = c23;  // inclusive suffix sums (lanes >= l)
@@ -573,18 +602,24 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       }
       const unsigned long long t01 = __shfl_sync(0xFFFFFFFFu, i01, 0), t23 = __shfl_sync(0xFFFFFFFFu, i23, 0);
       uint32_t bpf = o_pf + (uint32_t)(i01 - c01), bev = o_ev + (uint32_t)((i01 - c01) >> 32);
-      uint32_t bt = o_t + (uint32_t)(i23 - c23), bw = o_w + (uint32_t)((i23 - c23) >> 32);
+      uint32_t bt = o_t + (uint32_t)(i23 - c23);
       o_pf += (uint32_t)t01;
       o_ev += (uint32_t)(t01 >> 32);
       o_t += (uint32_t)t23;
-      o_w += (uint32_t)(t23 >> 32);
       const uint32_t kb = (uint32_t)wd * 32 - slab;  // (slab-relative id of the word's agent 0)
       // the word's candidates, ties and write-backs, from its highest agent down; a code's place
       // in the word: agent a sits in pair a % 16, half a / 16
-      for (uint32_t m = pm | ec | tm | wbm; m; ) {
+#ifdef AB_NO_CAND
+      for (uint32_t m = 0; m; ) {
+#else
+      for (uint32_t m = pm | ec | tm | evk; m; ) {
+#endif
         const uint32_t a = 31 - __clz(m);
         m &= ~(1u << a);
-        const uint32_t q = codes[(uint32_t)wd * 32 + (((a & 15u) << 1) | (a >> 4))] & 0xFFFu, bit = 1u << a;
+        // (the code from the thread's shared-memory row: pair a % 16 in unit (a % 16) / 4, swizzled)
+        const uint32_t jj = a & 15u, un = (jj >> 2) ^ ((threadIdx.x >> 1) & 3u);
+        const uint32_t code = *reinterpret_cast<const uint16_t *>(myrow + un * 16 + (jj & 3u) * 4 + (a >> 4) * 2);
+        const uint32_t q = code & 0xFFFu, dirty = (code >> 13) & 1u, bit = 1u << a;
         uint32_t cpos = 0xFFFFFFFFu;
         if (pm & bit) {
           w_pf[bpf] = (q << 20) | (((lm >> a) & 1u) << 19) | (kb + a);
@@ -594,13 +629,18 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
           cpos = (bev++) | 0x80000000u;
         }
         if (tm & bit) {
-          w_tk[bt] = (kb + a + slab) | (((rm >> a) & 1u) << 31) | (((dm >> a) & 1u) << 30);
+          w_tk[bt] = (kb + a + slab) | (((rm >> a) & 1u) << 31) | (dirty << 30);
           w_tp[bt++] = cpos;
         }
-        if (wbm & bit) w_wb[bw++] = kb + a + slab;
+        if ((evk & bit) && dirty) w_wb[atomicAdd(&s_wbn[warp], 1u)] = kb + a + slab;  // (order irrelevant: a sum)
       }
     }
   }
+  __syncwarp();
+  o_w = s_wbn[warp];
+#ifdef AB_NO_CAND
+  o_pf = o_ev = o_t = o_w = 0;
+#endif
   // write-back bytes of the warp's other evicted dirty agents (R13): its list, 32 loads at a time
   for (uint32_t i = lane; i < o_w; i += 32) d2h += d.wb_bytes[base + w_wb[i]];
   LAP(dta)
