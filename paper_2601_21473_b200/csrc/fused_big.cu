@@ -724,42 +724,36 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     (pf ? d.pf_ids : d.ev_ids)[pos] = (uint32_t)(p.shard_begin + base + (x & 0x7FFFFu));
   };
   {
-    constexpr uint32_t SMAX = (BIG_NSTASH * BIG_STASH / 4 - 256 * SW) / 4;  // entries sortable in R
+    constexpr uint32_t SMAX = (BIG_NSTASH * BIG_STASH / 4 - 64 * FWARPS) / 2;  // entries sortable in R
     uint32_t *start = h + 2 * NB1;  // [NB1] first sorted index per bucket (the counts are no longer needed)
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(R);  // 256 x SW sort counters
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(R);  // 64 x FWARPS sort counters
     for (int lst = 0; lst < 2; ++lst) {
       const uint32_t n = s_pre[lst][FWARPS];
       if (n == 0) continue;  // (CTA-uniform)
       const uint32_t *src = lst == 0 ? d.sort_ka + base : d.sort_va + base;
-      uint32_t *ka, *ia, *kb, *ib;  // keys (buckets) and values (the entries)
+      uint32_t *xa, *xb;  // the entries (bucket << 20 | kept << 19 | k), sorted by bucket
       if (n <= SMAX) {
-        ka = cnt + 256 * SW;
-        ia = ka + SMAX;
-        kb = ia + SMAX;
-        ib = kb + SMAX;
+        xa = cnt + 64 * FWARPS;
+        xb = xa + SMAX;
       } else {
-        ka = d.sort_kb + base;
-        ia = d.sort_vb + base;
-        kb = d.f_sk2 + base;
-        ib = d.f_sv2 + base;
+        xa = d.sort_kb + base;
+        xb = d.sort_vb + base;
       }
       {  // the slabs, warp 31's first: each warp copies its own
         const uint32_t mine = s_cnt[lst][warp], at = s_pre[lst][FWARPS - 1 - warp];
         for (uint32_t i = lane; i < mine; i += 32) {
           const uint32_t x0 = src[slab + i];
-          const uint32_t x = (x0 & 0xFFF80000u) | (slab + (x0 & 0x7FFFFu));  // (tile-relative k)
-          ka[at + i] = x >> 20;
-          ia[at + i] = x;
+          xa[at + i] = (x0 & 0xFFF80000u) | (slab + (x0 & 0x7FFFFu));  // (tile-relative k)
         }
       }
       __syncthreads();
-      cta_sort_pairs(ka, ia, kb, ib, n, cnt);
+      cta_sort_buckets(xa, xb, n, cnt);
       for (uint32_t i = threadIdx.x; i < n; i += FT)
-        if (i == 0 || ka[i - 1] != ka[i]) start[ka[i]] = i;
+        if (i == 0 || (xa[i - 1] >> 20) != (xa[i] >> 20)) start[xa[i] >> 20] = i;
       __syncthreads();
       const uint32_t *cur = lst == 0 ? cur_pf : cur_ev;
       for (uint32_t i = threadIdx.x; i < n; i += FT) {
-        const uint32_t b = ka[i], rk = i - start[b], x = ia[i];
+        const uint32_t x = xa[i], b = x >> 20, rk = i - start[b];
         // members: kept prefetch candidates, evict candidates the cut does not keep
         if (((x >> 19) & 1u) == (lst == 0 ? 1u : 0u)) place(x, lst == 0 ? cur[b] - rk : cur[b] + rk, lst == 0);
       }

@@ -513,4 +513,79 @@ static __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, 
 }
 
 
+// Stable sort of n 32-bit entries by their bits [20, 32) (the list bucket of a streaming-kernel
+// candidate), ascending, for one CTA: LSD radix sort with 6-bit digits over the varying digits
+// only.  Warp w owns the contiguous range [w*L, (w+1)*L), so (digit, warp, position) order is
+// stable; a lane's rank among the lower lanes of its digit comes from six ballots.  cnt: 64 *
+// FWARPS words of shared memory.  Buffers may be shared or global memory.  Result in a.
+static __device__ void cta_sort_buckets(uint32_t *a, uint32_t *b, uint32_t n, uint32_t *cnt) {
+  if (n <= 1) return;
+  __shared__ uint32_t sh_or2, sh_and2, sh_tot2;
+  if (threadIdx.x == 0) {
+    sh_or2 = 0;
+    sh_and2 = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  uint32_t o = 0, an = 0xFFFFFFFFu;
+  for (uint32_t e = threadIdx.x; e < n; e += FT) {
+    o |= a[e];
+    an &= a[e];
+  }
+  o = __reduce_or_sync(0xFFFFFFFFu, o);
+  an = __reduce_and_sync(0xFFFFFFFFu, an);
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&sh_or2, o);
+    atomicAnd(&sh_and2, an);
+  }
+  __syncthreads();
+  const uint32_t varying = sh_or2 ^ sh_and2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t L = (n + FWARPS - 1) / FWARPS;
+  const uint32_t lo = min(n, warp * L), hi = min(n, lo + L);
+  uint32_t *src = a, *dst = b;
+  for (int shift = 20; shift < 32; shift += 6) {
+    if (((varying >> shift) & 0x3Fu) == 0) continue;
+    // cnt[d * FWARPS + w]: entries of digit d in warp w's range
+    for (int x = threadIdx.x; x < 64 * FWARPS; x += FT) cnt[x] = 0;
+    __syncthreads();
+    for (uint32_t e = lo + lane; e < hi; e += 32) atomicAdd(&cnt[((src[e] >> shift) & 0x3Fu) * FWARPS + warp], 1u);
+    __syncthreads();
+    {  // exclusive scan in (digit, warp) order: 2 consecutive entries per thread
+      const uint32_t v0 = cnt[threadIdx.x * 2], v1 = cnt[threadIdx.x * 2 + 1];
+      const uint32_t ex = block_excl_scan<uint32_t, FT>(v0 + v1, &sh_tot2);
+      cnt[threadIdx.x * 2] = ex;
+      cnt[threadIdx.x * 2 + 1] = ex + v0;
+    }
+    __syncthreads();
+    for (uint32_t e0 = lo; e0 < hi; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      const bool valid = e < hi;
+      const uint32_t x = valid ? src[e] : 0u, dg = (x >> shift) & 0x3Fu;
+      uint32_t peers = __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+      for (int bb = 0; bb < 6; ++bb) {
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (dg >> bb) & 1u);
+        peers &= ((dg >> bb) & 1u) ? bal : ~bal;
+      }
+      const uint32_t below = __popc(peers & lanemask_lt());
+      const uint32_t c0 = valid ? cnt[dg * FWARPS + warp] : 0u;
+      __syncwarp();
+      if (valid) {
+        dst[c0 + below] = x;
+        if (below == 0) cnt[dg * FWARPS + warp] = c0 + __popc(peers);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    uint32_t *t = src;
+    src = dst;
+    dst = t;
+  }
+  if (src != a) {
+    for (uint32_t e = threadIdx.x; e < n; e += FT) a[e] = src[e];
+    __syncthreads();
+  }
+}
+
+
 }  // namespace ss
