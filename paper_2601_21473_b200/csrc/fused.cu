@@ -702,9 +702,32 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     __syncthreads();
     STAMP_MAX(38)  // positions and member lists
     const uint32_t m_pf = tp, m_ev = te;
-    // positions: warp 0 the prefetch members, warp 1 the evict members, 32 at a time in list
-    // order; the bucket positions serve as cursors
-    if (warp < 2) {
+    // positions: a member's place = its bucket's first position for this CTA + its rank among
+    // the bucket's members before it in list order.  One thread per member (rank by a scan of the
+    // members before it in shared memory) when both lists fit the CTA; else warp 0 the prefetch
+    // members, warp 1 the evict members, 32 at a time in list order with the bucket positions as
+    // cursors
+    const bool par_place = m_pf + m_ev <= (uint32_t)FT;  // (CTA-uniform)
+    if (par_place) {
+      const uint32_t t = threadIdx.x;
+      const bool pf = t < m_pf, mine = t < m_pf + m_ev;
+      bool at_bs = false;
+      if (mine) {
+        const uint32_t i = pf ? t : t - m_pf;
+        const uint32_t *mem = s.memb + (pf ? 0u : m_pf);
+        const uint32_t bk = mem[i], b = bk >> 16;
+        if (!ib_multi(b)) {
+          uint32_t rank = 0;
+          for (uint32_t j = 0; j < i; ++j) rank += (mem[j] >> 16) == b;
+          (pf ? d.pf_ids : d.ev_ids)[h32[(pf ? 0u : (uint32_t)NB1) + b] + rank] = (uint32_t)(p.shard_begin + base + (bk & 0xFFFFu));
+          at_bs = b == bs;
+        }
+      }
+      const uint32_t npb = __popc(__ballot_sync(0xFFFFFFFFu, at_bs && pf)), neb = __popc(__ballot_sync(0xFFFFFFFFu, at_bs && !pf));
+      if (lane == 0 && npb) atomicAdd(&d.header[H_N_PF], (unsigned long long)npb);
+      if (lane == 0 && neb) atomicAdd(&d.header[H_N_EV], (unsigned long long)neb);
+      PROBE(if (threadIdx.x == 0) atomicMax(&prof[43], gtimer());)
+    } else if (warp < 2) {
       const uint32_t m = warp == 0 ? m_pf : m_ev;
       const uint32_t *mem = s.memb + (warp == 0 ? 0u : m_pf);
       uint32_t *cur = h32 + (warp == 0 ? 0u : (uint32_t)NB1);
@@ -726,7 +749,8 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       }
       if (lane == 0 && nb) atomicAdd(&d.header[warp == 0 ? H_N_PF : H_N_EV], (unsigned long long)nb);
       PROBE(if (lane == 0) atomicMax(&prof[43 + warp], gtimer());)
-    } else if (c == G - 1 && sh_novf > 0) {
+    }
+    if (c == G - 1 && sh_novf > 0 && warp >= 2) {
       // the agents in multi-valued buckets (all CTAs'): prefetch members (non-residents below
       // b*) after the value buckets below 2048, evict members (residents above b*) after the
       // +inf bucket; ranked by (key, id) among themselves
