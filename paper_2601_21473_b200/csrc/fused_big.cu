@@ -3,22 +3,21 @@
 // ~1.8M agents on 148 SMs), up to 2^19 agents per CTA (~77M per GPU).
 //
 // Same method and same bucket-owner list placement as fused.cu, but the
-// per-agent state between the score pass and the emit pass lives in HBM: the level-1 bucket of
-// each agent (2 B) and, per 32-agent word, the eligible / resident / dirty / multi-valued masks
-// (16 B), written by P1 and read once by P34, instead of shared memory.
+// per-agent state between the score pass and the emit pass lives in HBM: one 16-bit code per
+// agent (level-1 bucket | eligible << 12 | dirty << 13), written by P1 and read once by P34.
 //   P1   stream the CTA's records: distance, eligibility, bucket; byte and count histograms and
-//        the eligible non-residents' byte histogram in shared memory; codes and word masks -> HBM
+//        the eligible non-residents' byte histogram in shared memory; codes -> HBM
 //   B1   grid barrier; select D* (warp 0) while the other warps stage this CTA's bucket-owner
 //        columns; the prefetched bytes below the boundary from the non-resident histogram; owner
-//        pass; this CTA's list-bucket positions from the owners; the first chunk of codes is
-//        copied into a shared-memory stash meanwhile
-//   P34  the CTA's words in chunks of 1024 from the highest id down, word i = thread i: below /
-//        at-boundary masks from the stashed codes (SWAR, two per 32-bit pair), tie bytes, one
-//        two-value scan (tie-byte offsets in id order, candidate counts), kept / prefetch / evict
-//        words, residency, write-back bytes; candidates appended in descending id order
-//   (e)  per list one stable sort of the candidates by bucket; positions from per-bucket cursors
-//        (evict: up from the bucket's first position; prefetch: down from its last, so that the
-//        list stays in ascending id order)
+//        pass; this CTA's list-bucket positions from the owners
+//   P34  one pass without CTA barriers: each warp streams its own word range from the highest
+//        id down, a thread per word (coalesced 64-byte code rows, the next step's loads in
+//        flight): masks by SWAR compares on 32-bit code pairs, kept / residency words, list
+//        candidates, tie agents and evicted dirty agents appended to per-warp slabs; then the
+//        tie group's id-order prefix (one CTA scan over the ties) and the write-back bytes
+//   (e)  per list one stable sort of the candidates by bucket (list order kept within a
+//        bucket); positions from per-bucket cursors (evict: up from the bucket's first
+//        position; prefetch: down from its last, so that the list stays in ascending id order)
 // Limits (status SCALESIM_ST_LIMIT, the step's plan is not produced): the boundary D* falls in
 // a multi-valued bucket (>= 2048 ticks), or more than BIG_OVF_CAP (4096) eligible agents have
 // finite distances >= 2048 ticks (or more than 128 in one CTA).
@@ -29,50 +28,23 @@
 
 namespace ss {
 
-constexpr uint32_t BIG_CW = 1024;    // words per P34 chunk (one per thread)
 #ifndef BIG_LB_V
 #define BIG_LB_V 4
 #endif
 constexpr int BIG_LB = BIG_LB_V;     // records in flight per thread in P1 (two batches)
 
-// the codes of chunk ch of this tile (words [ch * BIG_CW, ...)) into L2 ahead of its decode
-__device__ __forceinline__ void prefetch_chunk_codes(const uint16_t *codes, uint32_t tw, int ch) {
-#ifdef BIG_NO_PF
-  return;
-#endif
-  if (ch < 0) return;
-  const uint32_t w0 = (uint32_t)ch * BIG_CW, wn = min(BIG_CW, tw - w0);
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(codes + (uint64_t)w0 * 32), "r"(wn * 64u) : "memory");
-}
-
-
 static uint32_t big_rb(uint32_t gsize) { return ((NB1 + gsize - 1) / gsize + 3u) & ~3u; }
 
-constexpr uint32_t BIG_STASH = 64 * BIG_CW;  // bytes of codes per chunk
-// One stash (refilled after each chunk from L2, where the next chunk's codes were prefetched
-// meanwhile) or two (the next chunk copied while this one is processed).  Two cost 64 KB more
-// shared memory, i.e. less L1 for the loads in flight of the score pass (measured slower).
-#ifndef BIG_NSTASH
-#define BIG_NSTASH 1
-#endif
+// Region R of shared memory: P1's non-resident byte histogram, then P34's per-thread code rows
+// (1024 x 64 B), the tie staging, the placement sort's counters and arrays, the overflow sort.
+constexpr uint32_t BIG_R = 64 * FT;
 
 size_t fused_big_smem_bytes(uint32_t gsize) {
   const uint32_t RB = big_rb(gsize);
   return (size_t)4 * 4 * NB1             // histograms / counts / need list, later cursors
          + (size_t)4 * RB * (gsize + 4)  // bucket-owner staging
-         + (size_t)BIG_NSTASH * BIG_STASH  // R: the code stashes (also the P1 byte histogram, the sorts)
+         + (size_t)BIG_R                 // region R
          + 64;
-}
-
-// Chunk ch of this tile's codes (words [ch * BIG_CW, ...)) into a shared-memory stash, 16 bytes
-// per cp.async (coalesced); 16-byte unit x (word x / 4, codes 8 (x % 4) ..) lands at
-// x ^ ((x >> 3) & 3): a thread reading its word's four units hits eight distinct bank groups
-// per quarter warp.
-__device__ __forceinline__ void stash_chunk(uint8_t *stash, const uint16_t *codes, uint32_t tw, int ch) {
-  const uint32_t w0 = (uint32_t)ch * BIG_CW, nx = 4 * min(BIG_CW, tw - w0);
-  const uint4 *src = reinterpret_cast<const uint4 *>(codes + (uint64_t)w0 * 32);
-  for (uint32_t x = threadIdx.x; x < nx; x += FT) cp_async16(stash + 16 * (x ^ ((x >> 3) & 3u)), src + x);
-  cp_async_commit();
 }
 
 __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ FusedArgs<1> B) {
@@ -113,9 +85,9 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   uint32_t *h = reinterpret_cast<uint32_t *>(smem_raw);  // [4 NB1]
   const uint32_t RB = ((NB1 + G - 1) / G + 3u) & ~3u;
   uint32_t *col = h + 4 * NB1;                            // [G][RB] + [4][RB]
-  // region R after the owner staging, three lives: P1's non-resident byte histogram [2 NB1];
-  // P34's two code stashes (a chunk of codes each, 64 KB); the (e) sort counters and the
-  // overflow sort's two lists
+  // region R after the owner staging (BIG_R bytes), several lives: P1's non-resident byte
+  // histogram [2 NB1]; P34's per-thread code rows; the tie staging; the (e) sort counters and
+  // arrays; the overflow sort's two lists
   uint8_t *R = reinterpret_cast<uint8_t *>(col + RB * (G + 4));
   uint32_t *nrb = reinterpret_cast<uint32_t *>(R);                       // [2 NB1] (16-bit halves)
   unsigned long long *la = reinterpret_cast<unsigned long long *>(R);    // [BIG_OVF_CAP]
@@ -323,8 +295,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     return;
   }
   // this CTA's prefetched bytes below the boundary bucket (every eligible non-resident there is
-  // prefetched, R2); the tie group's kept non-residents are added in P34.  Then R turns into
-  // the code stashes: the first chunk P34 decodes (the highest) is copied in meanwhile.
+  // prefetched, R2); the tie group's kept non-residents are added in P34.
   unsigned long long h2d = 0;
   for (uint32_t b = threadIdx.x; b < bs; b += FT) h2d += ((unsigned long long)nrb[NB1 + b] << 16) + nrb[b];
   __syncthreads();
@@ -609,11 +580,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
       const uint32_t kb = (uint32_t)wd * 32 - slab;  // (slab-relative id of the word's agent 0)
       // the word's candidates, ties and write-backs, from its highest agent down; a code's place
       // in the word: agent a sits in pair a % 16, half a / 16
-#ifdef AB_NO_CAND
-      for (uint32_t m = 0; m; ) {
-#else
       for (uint32_t m = pm | ec | tm | evk; m; ) {
-#endif
         const uint32_t a = 31 - __clz(m);
         m &= ~(1u << a);
         // (the code from the thread's shared-memory row: pair a % 16 in unit (a % 16) / 4, swizzled)
@@ -638,9 +605,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   }
   __syncwarp();
   o_w = s_wbn[warp];
-#ifdef AB_NO_CAND
-  o_pf = o_ev = o_t = o_w = 0;
-#endif
   // write-back bytes of the warp's other evicted dirty agents (R13): its list, 32 loads at a time
   for (uint32_t i = lane; i < o_w; i += 32) d2h += d.wb_bytes[base + w_wb[i]];
   LAP(dta)
@@ -724,7 +688,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     (pf ? d.pf_ids : d.ev_ids)[pos] = (uint32_t)(p.shard_begin + base + (x & 0x7FFFFu));
   };
   {
-    constexpr uint32_t SMAX = (BIG_NSTASH * BIG_STASH / 4 - 64 * FWARPS) / 2;  // entries sortable in R
+    constexpr uint32_t SMAX = (BIG_R / 4 - 64 * FWARPS) / 2;  // entries sortable in R
     uint32_t *start = h + 2 * NB1;  // [NB1] first sorted index per bucket (the counts are no longer needed)
     uint32_t *cnt = reinterpret_cast<uint32_t *>(R);  // 64 x FWARPS sort counters
     for (int lst = 0; lst < 2; ++lst) {
