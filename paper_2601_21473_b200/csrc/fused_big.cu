@@ -606,7 +606,15 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
   __syncwarp();
   o_w = s_wbn[warp];
   // write-back bytes of the warp's other evicted dirty agents (R13): its list, 32 loads at a time
-  for (uint32_t i = lane; i < o_w; i += 32) d2h += d.wb_bytes[base + w_wb[i]];
+  for (uint32_t i0 = 0; i0 < o_w; i0 += 128) {  // (four independent loads in flight per lane)
+    uint32_t ix[4], v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ix[u] = i0 + 32u * u + lane < o_w ? w_wb[i0 + 32u * u + lane] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ix[u] != 0xFFFFFFFFu ? d.wb_bytes[base + ix[u]] : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d2h += v[u];
+  }
   LAP(dta)
   // the warps' list lengths: candidates / ties / write-backs
   __shared__ uint32_t s_cnt[4][FWARPS], s_pre[4][FWARPS + 1];
