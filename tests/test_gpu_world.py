@@ -174,8 +174,27 @@ def run_world_tp(w, cuts, content_pages=48):
     res = np.zeros(w.n, np.uint8)
     rng = np.random.default_rng(0)
     fp = None
+    newer = set()  # (slot, rank) written on the device since its last load: newer than the host
+    n_wb_checked = 0
     for s in range(w.steps):
         rec = w.rec[s]
+        # simulated KV / history writes of dirty resident agents: every rank stamps its slice of
+        # their non-LoRA pages; a written-back page must carry each rank's stamp in its slice
+        stamped = {}
+        pt0 = om.page_table()
+        dirty = np.nonzero(((rec[:, 2] >> 4) & 1).astype(bool) & res.astype(bool))[0]
+        for a in rng.permutation(dirty)[:6]:
+            for blk in range(int(b.blk_ptr[a]), int(b.blk_ptr[a + 1])):
+                if b.blk_kind[blk] == tg.KIND_LORA:
+                    continue
+                for q in range(int(page_first[blk]), int(page_first[blk + 1])):
+                    slot = int(pt0[q])
+                    for r, pl in enumerate(ranks):
+                        mark = np.array([0x7A000000 + s, slot, r, q], np.uint32)
+                        pl.dev_arena[slot * su: slot * su + 16].copy_(torch.from_numpy(mark.view(np.uint8)))
+                        stamped[(slot, r)] = mark
+                        newer.add((slot, r))
+        torch.cuda.synchronize()
         for r, pl in enumerate(ranks):
             pl.set_records(rec[cuts[r]:cuts[r + 1]])
         step_group(ranks, int(w.now[s]))
@@ -199,13 +218,23 @@ def run_world_tp(w, cuts, content_pages=48):
             assert np.array_equal(h2d[:, 0], mo["h2d_host"]) and np.array_equal(h2d[:, 1], mo["h2d_page"]), (s, r)
             assert np.array_equal(d2h[:, 0], mo["d2h_host"]) and np.array_equal(d2h[:, 1], mo["d2h_page"]), (s, r)
             assert np.array_equal(pl.page_table(), pt), (s, r)
+            for k in range(len(d2h)):  # written-back pages: this rank's slice carries its stamp
+                ho, slot = int(d2h[k, 0]), int(d2h[k, 1])
+                if (slot, r) in stamped:
+                    got = host[ho + r * su: ho + r * su + 16].numpy().view(np.uint32)
+                    assert np.array_equal(got, stamped[(slot, r)]), (s, r, k, got, stamped[(slot, r)])
+                    n_wb_checked += 1
             # content: the rank's slot of a resident page holds slice r of the page's host bytes
             held = np.nonzero(pt != 0xFFFFFFFF)[0]
             for q in rng.permutation(held)[:content_pages]:
                 slot, ho = int(pt[q]), int(page_host[q]) + r * su
+                if (slot, r) in newer:  # (written on the device since its load: newer than the host)
+                    continue
                 got = pl.dev_arena[slot * su:(slot + 1) * su].cpu()
                 assert torch.equal(got, host[ho:ho + su]), (s, r, int(q), slot)
         res = p["resident"]
+        newer -= {(int(x), r) for x in mo["h2d_page"] for r in range(G)}  # (reloaded from the host)
+    assert n_wb_checked > 0  # (some stamped slices were written back and checked)
     for pl in ranks:
         pl.close()
 
