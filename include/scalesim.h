@@ -126,7 +126,11 @@ typedef enum {
                                        the all-gather of the ranks' bytes at D*, the kept tie bytes)
                                        run as reductions over the ranks' device buffers.  The
                                        group is the contexts created with the same 128-byte
-                                       nccl_unique_id (any bytes).  Not with SCALESIM_F_LOOPBACK. */
+                                       nccl_unique_id (any bytes).  Not with SCALESIM_F_LOOPBACK.
+                                       Like NCCL ranks, a rank that stops calling (an error
+                                       before a collective) leaves the others waiting in theirs;
+                                       shards that are not contiguous in rank order fail the
+                                       first collective with SCALESIM_E_INVALID on every rank. */
 #define SCALESIM_F_TP_SLICED 64u    /* with SCALESIM_F_LOOPBACK and transfers: tensor-parallel
                                        agent memory (§4.2: "All multi-GPU setups
                                        use tensor parallelism"; reading R16).  Every rank holds
