@@ -696,16 +696,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
     (pf ? d.pf_ids : d.ev_ids)[pos] = (uint32_t)(p.shard_begin + base + (x & 0x7FFFFu));
   };
   {
-    constexpr uint32_t SMAX = (BIG_R / 4 - 64 * FWARPS) / 2;  // entries sortable in R
+    constexpr uint32_t SMAX = (BIG_R / 4 - SB_CNT) / 2;  // entries sortable in R
     uint32_t *start = h + 2 * NB1;  // [NB1] first sorted index per bucket (the counts are no longer needed)
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(R);  // 64 x FWARPS sort counters
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(R);  // SB_CNT sort counters
     for (int lst = 0; lst < 2; ++lst) {
       const uint32_t n = s_pre[lst][FWARPS];
       if (n == 0) continue;  // (CTA-uniform)
       const uint32_t *src = lst == 0 ? d.sort_ka + base : d.sort_va + base;
       uint32_t *xa, *xb;  // the entries (bucket << 20 | kept << 19 | k), sorted by bucket
       if (n <= SMAX) {
-        xa = cnt + 64 * FWARPS;
+        xa = cnt + SB_CNT;
         xb = xa + SMAX;
       } else {
         xa = d.sort_kb + base;
@@ -719,7 +719,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_big(const __grid_constant__ Fus
         }
       }
       __syncthreads();
+      PROBE(const unsigned long long ts0 = gtimer();)
       cta_sort_buckets(xa, xb, n, cnt);
+      PROBE(if (threadIdx.x == 0) {
+        atomicMax(&prof[50 + lst], gtimer() - ts0);
+        atomicMax(&prof[52 + lst], (unsigned long long)n);
+      })
       for (uint32_t i = threadIdx.x; i < n; i += FT)
         if (i == 0 || (xa[i - 1] >> 20) != (xa[i] >> 20)) start[xa[i] >> 20] = i;
       __syncthreads();

@@ -516,8 +516,10 @@ static __device__ void cta_sort_pairs(uint32_t *ka, uint32_t *ia, uint32_t *kb, 
 // Stable sort of n 32-bit entries by their bits [20, 32) (the list bucket of a streaming-kernel
 // candidate), ascending, for one CTA: LSD radix sort with 6-bit digits over the varying digits
 // only.  Warp w owns the contiguous range [w*L, (w+1)*L), so (digit, warp, position) order is
-// stable; a lane's rank among the lower lanes of its digit comes from six ballots.  cnt: 64 *
-// FWARPS words of shared memory.  Buffers may be shared or global memory.  Result in a.
+// stable; a lane's rank among the lower lanes of its digit comes from six ballots.  cnt:
+// SB_CNT words of shared memory, warp-major with a 65-word stride (a warp's lanes with different
+// digits hit different banks).  Buffers may be shared or global memory.  Result in a.
+constexpr uint32_t SB_STRIDE = 65, SB_CNT = FWARPS * SB_STRIDE;
 static __device__ void cta_sort_buckets(uint32_t *a, uint32_t *b, uint32_t n, uint32_t *cnt) {
   if (n <= 1) return;
   __shared__ uint32_t sh_or2, sh_and2, sh_tot2;
@@ -545,16 +547,18 @@ static __device__ void cta_sort_buckets(uint32_t *a, uint32_t *b, uint32_t n, ui
   uint32_t *src = a, *dst = b;
   for (int shift = 20; shift < 32; shift += 6) {
     if (((varying >> shift) & 0x3Fu) == 0) continue;
-    // cnt[d * FWARPS + w]: entries of digit d in warp w's range
-    for (int x = threadIdx.x; x < 64 * FWARPS; x += FT) cnt[x] = 0;
+    // cnt[w * SB_STRIDE + d]: entries of digit d in warp w's range
+    for (int x = threadIdx.x; x < (int)SB_CNT; x += FT) cnt[x] = 0;
     __syncthreads();
-    for (uint32_t e = lo + lane; e < hi; e += 32) atomicAdd(&cnt[((src[e] >> shift) & 0x3Fu) * FWARPS + warp], 1u);
+    for (uint32_t e = lo + lane; e < hi; e += 32) atomicAdd(&cnt[warp * SB_STRIDE + ((src[e] >> shift) & 0x3Fu)], 1u);
     __syncthreads();
-    {  // exclusive scan in (digit, warp) order: 2 consecutive entries per thread
-      const uint32_t v0 = cnt[threadIdx.x * 2], v1 = cnt[threadIdx.x * 2 + 1];
+    {  // exclusive scan in (digit, warp) order: entries 2t and 2t + 1 of that order per thread
+      const uint32_t e0 = threadIdx.x * 2, e1 = e0 + 1;
+      const uint32_t a0 = (e0 % FWARPS) * SB_STRIDE + e0 / FWARPS, a1 = (e1 % FWARPS) * SB_STRIDE + e1 / FWARPS;
+      const uint32_t v0 = cnt[a0], v1 = cnt[a1];
       const uint32_t ex = block_excl_scan<uint32_t, FT>(v0 + v1, &sh_tot2);
-      cnt[threadIdx.x * 2] = ex;
-      cnt[threadIdx.x * 2 + 1] = ex + v0;
+      cnt[a0] = ex;
+      cnt[a1] = ex + v0;
     }
     __syncthreads();
     for (uint32_t e0 = lo; e0 < hi; e0 += 32) {
@@ -568,11 +572,11 @@ static __device__ void cta_sort_buckets(uint32_t *a, uint32_t *b, uint32_t n, ui
         peers &= ((dg >> bb) & 1u) ? bal : ~bal;
       }
       const uint32_t below = __popc(peers & lanemask_lt());
-      const uint32_t c0 = valid ? cnt[dg * FWARPS + warp] : 0u;
+      const uint32_t c0 = valid ? cnt[warp * SB_STRIDE + dg] : 0u;
       __syncwarp();
       if (valid) {
         dst[c0 + below] = x;
-        if (below == 0) cnt[dg * FWARPS + warp] = c0 + __popc(peers);
+        if (below == 0) cnt[warp * SB_STRIDE + dg] = c0 + __popc(peers);
       }
       __syncwarp();
     }

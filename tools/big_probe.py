@@ -30,5 +30,5 @@ for s in range(12):
         r = lambda q: round((int(st[q]) - int(st[0])) / 1e3, 1) if st[q] else None  # noqa: E731
         print(f"step {s}: us P1 {r(25)} pub {r(26)} B1 {r(4)} sel+own {r(41)} pos {r(17)} P34 {r(39)} end {r(1)} | "
               f"P34 parts (max over CTAs, us): a {st[22]/1e3:.1f} b {st[23]/1e3:.1f} c {st[24]/1e3:.1f} d {st[29]/1e3:.1f} "
-              f"| npf {h['n_prefetch']} nev {h['n_evict']}")
+              f"| npf {h['n_prefetch']} nev {h['n_evict']} | sort ns max (pf, ev) {st[50]} {st[51]} n max {st[52]} {st[53]}")
 pl.close()
