@@ -356,6 +356,20 @@ scalesim_status scalesim_step_host(scalesim_ctx *ctx, int64_t now_tick, const ui
                                    const float *host_kin, scalesim_plan_host *out,
                                    uint32_t *prefetch_out, uint32_t *evict_out);
 
+/* Pipelined end-to-end steps (the host side of P:242's overlap: a later step's inputs cross
+ * the host link while this step plans).  Starts the host->device copy of a LATER step's
+ * inputs — host_rec (4*n_local uint32) and host_kin (4*n_kin float; may be NULL when
+ * n_kin == 0), ideally pinned — into one of two library-owned device buffers on a
+ * library-owned stream, and returns at once.  The host buffers must stay unchanged until the
+ * scalesim_step_host call that consumes them returns.  A later scalesim_step_host(ctx, now,
+ * host_rec, host_kin, ...) with the SAME pointers plans from the staged copy (its plan waits
+ * for that copy on the device, not on the host) instead of copying synchronously; the
+ * context's own input buffers (init / scalesim_set_inputs) are left untouched.  Usage:
+ * stage(in[0]); for t: { stage(in[t+1]); step_host(in[t]); }.  At most two staged steps may
+ * be outstanding.  Errors: SCALESIM_E_INVALID (NULL ctx / host_rec, or host_kin NULL with
+ * n_kin > 0), SCALESIM_E_ORDER (two staged steps not yet consumed), SCALESIM_E_CUDA. */
+scalesim_status scalesim_stage_host(scalesim_ctx *ctx, const uint32_t *host_rec, const float *host_kin);
+
 /* Point the context at another record / kinematics buffer (same sizes; device). */
 scalesim_status scalesim_set_inputs(scalesim_ctx *ctx, const uint32_t *agent_rec, const float *agent_kin);
 

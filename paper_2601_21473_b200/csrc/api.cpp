@@ -362,6 +362,14 @@ struct scalesim_ctx {
   bool last_fused = false;
   int sms = 148;
   int64_t deferred_now = 0;
+  // pipelined host inputs (scalesim_stage_host): two library-owned device buffers, each the
+  // records (16 n_local B) followed by the kinematics (16 n_kin B), filled on in_stream
+  cudaStream_t in_stream = nullptr;
+  uint8_t *sbuf[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  const void *staged_rec[2] = {nullptr, nullptr}, *staged_kin[2] = {nullptr, nullptr};
+  bool staged[2] = {false, false}, sbuf_used[2] = {false, false};
+  int stage_next = 0;
 };
 
 static scalesim_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SCALESIM_OK : SCALESIM_E_CUDA; }
@@ -1167,10 +1175,28 @@ extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, cons
                                               uint32_t *ev_out) {
   if (!c || !host_rec) return SCALESIM_E_INVALID;
   if (c->p.n_kin > 0 && !host_kin) return SCALESIM_E_INVALID;
-  CK(cudaMemcpyAsync(const_cast<uint4 *>(c->p.rec), host_rec, 16 * c->p.n_local, cudaMemcpyHostToDevice, c->stream));
-  if (c->p.n_kin > 0)
-    CK(cudaMemcpyAsync(const_cast<float4 *>(c->p.kin), host_kin, 16 * c->p.n_kin, cudaMemcpyHostToDevice, c->stream));
-  scalesim_status s = scalesim_step(c, now, nullptr);
+  int si = -1;  // inputs staged by scalesim_stage_host (their copy may still be in flight)
+  for (int i = 0; i < 2; ++i)
+    if (c->staged[i] && c->staged_rec[i] == host_rec && (c->p.n_kin == 0 || c->staged_kin[i] == host_kin)) si = i;
+  scalesim_status s;
+  if (si >= 0) {
+    const uint4 *rec0 = c->p.rec;
+    const float4 *kin0 = c->p.kin;
+    CK(cudaStreamWaitEvent(c->stream, c->ev_in[si], 0));
+    c->p.rec = reinterpret_cast<const uint4 *>(c->sbuf[si]);
+    c->p.kin = reinterpret_cast<const float4 *>(c->sbuf[si] + 16 * c->p.n_local);
+    s = scalesim_step(c, now, nullptr);  // (the launches capture the input pointers)
+    c->p.rec = rec0;
+    c->p.kin = kin0;
+    c->staged[si] = false;
+    c->sbuf_used[si] = true;
+    CK(cudaEventRecord(c->ev_used[si], c->stream));  // the next copy into sbuf[si] waits for it
+  } else {
+    CK(cudaMemcpyAsync(const_cast<uint4 *>(c->p.rec), host_rec, 16 * c->p.n_local, cudaMemcpyHostToDevice, c->stream));
+    if (c->p.n_kin > 0)
+      CK(cudaMemcpyAsync(const_cast<float4 *>(c->p.kin), host_kin, 16 * c->p.n_kin, cudaMemcpyHostToDevice, c->stream));
+    s = scalesim_step(c, now, nullptr);
+  }
   if (s != SCALESIM_OK) return s;
   scalesim_plan_host h;
   CK(cudaMemcpyAsync(h.f, c->p.d.header, sizeof(h.f), cudaMemcpyDeviceToHost, c->stream));
@@ -1185,9 +1211,45 @@ extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, cons
   return status_of_header(h.f[SCALESIM_H_STATUS]);
 }
 
+extern "C" scalesim_status scalesim_stage_host(scalesim_ctx *c, const uint32_t *host_rec, const float *host_kin) {
+  if (!c || !host_rec) return SCALESIM_E_INVALID;
+  if (c->p.n_kin > 0 && !host_kin) return SCALESIM_E_INVALID;
+  int i = c->stage_next;
+  if (c->staged[i]) i ^= 1;
+  if (c->staged[i]) return SCALESIM_E_ORDER;  // two staged steps not yet run
+  if (!c->in_stream) {
+    CK(cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_used[k], cudaEventDisableTiming));
+    }
+  }
+  const size_t rb = 16 * (size_t)c->p.n_local, kb = 16 * (size_t)c->p.n_kin;
+  if (!c->sbuf[i]) CK(cudaMalloc(&c->sbuf[i], rb + kb > 0 ? rb + kb : 16));
+  if (c->sbuf_used[i]) CK(cudaStreamWaitEvent(c->in_stream, c->ev_used[i], 0));  // its last step read it
+  if (rb) CK(cudaMemcpyAsync(c->sbuf[i], host_rec, rb, cudaMemcpyHostToDevice, c->in_stream));
+  if (kb) CK(cudaMemcpyAsync(c->sbuf[i] + rb, host_kin, kb, cudaMemcpyHostToDevice, c->in_stream));
+  CK(cudaEventRecord(c->ev_in[i], c->in_stream));
+  c->staged[i] = true;
+  c->staged_rec[i] = host_rec;
+  c->staged_kin[i] = host_kin;
+  c->stage_next = i ^ 1;
+  return SCALESIM_OK;
+}
+
 extern "C" void scalesim_destroy(scalesim_ctx *c) {
   if (!c) return;
+  if (c->in_stream) {
+    cudaStreamSynchronize(c->in_stream);
+    cudaStreamDestroy(c->in_stream);
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
+    if (c->ev_used[k]) cudaEventDestroy(c->ev_used[k]);
+  }
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int k = 0; k < 2; ++k)
+    if (c->sbuf[k]) cudaFree(c->sbuf[k]);
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->tgroup) leave_group(c->tgroup);

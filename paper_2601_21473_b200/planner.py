@@ -39,6 +39,7 @@ class Planner:
                  multi_kernel: bool = False, keep_dist: bool = True, explicit_dist: bool = False,
                  exclusive: bool = False, loopback: bool = False, tp_sliced: bool = False, threads: bool = False):
         self.lib = L.lib()
+        self._staged_refs = {}  # host arrays of staged steps (scalesim_stage_host)
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         lo, hi = shard if shard is not None else (0, n_agents)
@@ -176,8 +177,17 @@ class Planner:
         st = self.lib.scalesim_step_host(self.ctx, int(now), rp, kp, C.byref(h),
                                          None if pf_out is None else pf_out.ctypes.data,
                                          None if ev_out is None else ev_out.ctypes.data)
+        self._staged_refs.pop(rp, None)
         L.check(st, "scalesim_step_host", allow=(L.OK, L.E_INSUFFICIENT))
         return h.as_dict()
+
+    def stage_host(self, rec_host: np.ndarray, kin_host: Optional[np.ndarray] = None):
+        """Start the host->device copy of a later step's inputs (scalesim_stage_host); the
+        step_host call with the same arrays plans from the staged copy.  The arrays are kept
+        alive here until that call."""
+        kp = kin_host.ctypes.data if kin_host is not None else None
+        L.check(self.lib.scalesim_stage_host(self.ctx, rec_host.ctypes.data, kp), "scalesim_stage_host")
+        self._staged_refs[rec_host.ctypes.data] = (rec_host, kin_host)
 
     def join(self):
         L.check(self.lib.scalesim_join(self.ctx), "scalesim_join")

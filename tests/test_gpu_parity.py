@@ -162,6 +162,40 @@ def test_call_order_and_host_step():
     pl2.close()
 
 
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_pipelined_host_steps_c4_shape(exclusive):
+    """scalesim_stage_host + scalesim_step_host back to back (the bench's e2e loop: step t+1's
+    records cross the link while step t plans, keep_dist=False as benched): every step's header
+    and lists equal the oracle's; the staged buffers alternate, a third stage is refused."""
+    import torch
+    from paper_2601_21473_b200 import _lib as L
+    from gpu_harness import make_planner
+    w = tg.config_c4(seed=5, steps=7, n=300_000)
+    pl = make_planner(w, transfer=False, keep_dist=False, exclusive=exclusive)
+    recs = [torch.from_numpy(np.ascontiguousarray(w.rec[s])).pin_memory().numpy() for s in range(w.steps)]
+    pf = np.zeros(w.n, np.uint32)
+    ev = np.zeros(w.n, np.uint32)
+    res = np.zeros(w.n, np.uint8)
+    pl.stage_host(recs[0])
+    for s in range(w.steps):
+        if s + 1 < w.steps:
+            pl.stage_host(recs[s + 1])
+            if s == 0:
+                with pytest.raises(L.ScaleSimError) as e:
+                    pl.stage_host(recs[2])
+                assert e.value.status == L.E_ORDER
+        h = pl.step_host(int(w.now[s]), recs[s], None, pf, ev)
+        d_or, _ = oracle.score(w.rec[s], None, int(w.now[s]), w.hop_scale)
+        p = oracle.plan(w.rec[s], d_or, res, w.theta, w.budget)
+        assert h["cut_bits"] == p["cut_bits"] and h["cut_rem"] == p["cut_rem"], s
+        assert h["kept_bytes"] == p["kept_bytes"] and h["bytes_h2d"] == p["bytes_h2d"], s
+        assert h["n_prefetch"] == len(p["prefetch"]) and h["n_evict"] == len(p["evict"]), s
+        assert np.array_equal(pf[:h["n_prefetch"]], p["prefetch"]), s
+        assert np.array_equal(ev[:h["n_evict"]], p["evict"]), s
+        res = p["resident"].astype(np.uint8)
+    pl.close()
+
+
 def test_fused_multi_level_select_and_segments():
     """Distances spread over many values (boundary bucket with several distances: select
     levels 2 and 3; evict segments that need the re-sort by full key), fused vs oracle."""
