@@ -805,23 +805,42 @@ def main():
     ev = np.zeros(n, np.uint32)
     if world > 1:
         dist.barrier()
-    def e2e_loop(pipelined):
+    # the changed records of each step (the simulation emits them as its agents act; computed
+    # before the region), pinned
+    upd = [None]
+    for k in range(1, e2e_k):
+        ch = np.nonzero(np.any(w.rec[t_base + k] != w.rec[t_base + k - 1], axis=1))[0].astype(np.uint32)
+        upd.append((torch.from_numpy(ch + np.uint32(rank * n)).pin_memory().numpy(),  # global ids
+                    torch.from_numpy(np.ascontiguousarray(w.rec[t_base + k][ch])).pin_memory().numpy()))
+
+    def e2e_loop(mode):
         """e2e_k steps through the host entry points; returns (seconds, h2d bytes, d2h bytes).
-        pipelined: scalesim_stage_host starts step k+1's record copy (copy engine, its own
-        stream) before step k's scalesim_step_host, whose plan waits for its own staged copy
-        on the device; every step's H2D and its header + lists D2H stay inside the region."""
+        sync: scalesim_step_host alone (copy, plan, read back, one step at a time).
+        full: scalesim_stage_host starts step k+1's record copy (copy engine, its own stream)
+        before step k's scalesim_step_host, whose plan waits for its staged copy on the device.
+        updates: after step 0's whole records, each step sends only its changed records
+        (scalesim_stage_updates one step ahead + scalesim_step_updates).  Every step's H2D and
+        its header + lists D2H are inside the region."""
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         hb = db = 0
-        if pipelined:
+        if mode == "full":
             pl.stage_host(rec_host[0])
         for k in range(e2e_k):
-            if pipelined and k + 1 < e2e_k:
-                pl.stage_host(rec_host[k + 1])
-            h = pl.step_host(int(w.now[t_base + k]), rec_host[k], None, pf, ev)
-            hb += rec_host[k].nbytes
+            if mode == "updates" and k > 0:
+                if k + 1 < e2e_k:
+                    pl.stage_updates(*upd[k + 1])
+                h = pl.step_updates(int(w.now[t_base + k]), upd[k][0], upd[k][1], pf, ev)
+                hb += upd[k][0].nbytes + upd[k][1].nbytes
+            else:
+                if mode == "full" and k + 1 < e2e_k:
+                    pl.stage_host(rec_host[k + 1])
+                h = pl.step_host(int(w.now[t_base + k]), rec_host[k], None, pf, ev)
+                hb += rec_host[k].nbytes
+                if mode == "updates" and e2e_k > 1:
+                    pl.stage_updates(*upd[1])
             db += 128 + 4 * (h["n_prefetch"] + h["n_evict"])
         el = time.perf_counter() - t0
         if world > 1:
@@ -830,13 +849,20 @@ def main():
             el = float(t.item())
         return el, hb, db
 
-    el_s, _, _ = e2e_loop(False)
-    el_e, h2d_b, d2h_b = e2e_loop(True)
+    el_s, _, _ = e2e_loop("sync")
+    el_f, h2d_f, _ = e2e_loop("full")
+    el_e, h2d_b, d2h_b = e2e_loop("updates")
     e2e = {"value": n * world * e2e_k / el_e, "unit": "agent-plans/s", "h2d_bytes_per_step": h2d_b // e2e_k,
            "d2h_bytes_per_step": d2h_b // e2e_k, "steps": e2e_k,
-           "h2d_GBs": h2d_b / el_e / 1e9,
+           "api": "scalesim_step_updates: step 0 whole records (scalesim_step_host), then each step's "
+                  "changed records (ids + 16-byte records, pinned) staged one step ahead by "
+                  "scalesim_stage_updates; header + lists back every step; host-timed",
+           "changed_per_step": float(np.mean([len(u[0]) for u in upd[1:]])) if e2e_k > 1 else None,
+           "whole_records_value": n * world * e2e_k / el_f, "whole_records_h2d_bytes_per_step": h2d_f // e2e_k,
+           "whole_records_h2d_GBs": h2d_f / el_f / 1e9,
+           "whole_records_api": "scalesim_stage_host(records of step t+1) + scalesim_step_host(step t)",
            "synchronous_value": n * world * e2e_k / el_s,
-           "api": "scalesim_stage_host(records of step t+1) + scalesim_step_host(step t): pinned host records in, header + lists out, host-timed; synchronous_value: scalesim_step_host alone (copy, plan, read back, one step at a time)"}
+           "synchronous_api": "scalesim_step_host alone (16 MB records in, plan, header + lists out, one step at a time)"}
 
     pl.close()
     c5 = None

@@ -370,6 +370,30 @@ scalesim_status scalesim_step_host(scalesim_ctx *ctx, int64_t now_tick, const ui
  * n_kin > 0), SCALESIM_E_ORDER (two staged steps not yet consumed), SCALESIM_E_CUDA. */
 scalesim_status scalesim_stage_host(scalesim_ctx *ctx, const uint32_t *host_rec, const float *host_kin);
 
+/* Incremental end-to-end steps.  Agent state changes only where the simulation acted (P:197-205:
+ * an invocation starts or ends an action; ~5% of AgentSociety's agents per step), so the
+ * step's inputs are the CHANGED records: host_ids (n_upd global agent ids of this shard,
+ * distinct — with a repeated id, which of its records lands is unspecified) and host_rec
+ * (4*n_upd uint32, the new 16-byte records in the layout of scalesim_init's agent_rec).  The
+ * records are written into the context's current record buffer (scalesim_init /
+ * scalesim_set_inputs, device, caller-owned: it must hold the previous step's records, e.g.
+ * after one scalesim_step_host), then the step runs and its header and lists come back as in
+ * scalesim_step_host.  scalesim_stage_updates starts the host->device copy of a LATER step's
+ * updates (library-owned staging shared with scalesim_stage_host: at most two staged steps)
+ * and returns at once; scalesim_step_updates with the same (host_ids, host_rec, n_upd) uses
+ * that copy (the scatter waits for it on the device), otherwise it copies synchronously.  The
+ * scatter runs on the plan stream after the previous step's plan, so staging never races a
+ * plan still reading the records.  Contexts with kinematics (n_kin > 0) use
+ * scalesim_step_host.  Errors: SCALESIM_E_INVALID (NULL ctx, NULL arrays with n_upd > 0,
+ * n_upd > n_local, n_kin > 0), SCALESIM_E_ORDER (two staged steps not yet consumed),
+ * SCALESIM_E_BAD_INPUT (ids outside the shard: skipped, the step still runs on the others),
+ * else as scalesim_step_host. */
+scalesim_status scalesim_stage_updates(scalesim_ctx *ctx, const uint32_t *host_ids, const uint32_t *host_rec,
+                                       uint32_t n_upd);
+scalesim_status scalesim_step_updates(scalesim_ctx *ctx, int64_t now_tick, const uint32_t *host_ids,
+                                      const uint32_t *host_rec, uint32_t n_upd, scalesim_plan_host *out,
+                                      uint32_t *prefetch_out, uint32_t *evict_out);
+
 /* Point the context at another record / kinematics buffer (same sizes; device). */
 scalesim_status scalesim_set_inputs(scalesim_ctx *ctx, const uint32_t *agent_rec, const float *agent_kin);
 

@@ -369,7 +369,10 @@ struct scalesim_ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   const void *staged_rec[2] = {nullptr, nullptr}, *staged_kin[2] = {nullptr, nullptr};
   bool staged[2] = {false, false}, sbuf_used[2] = {false, false};
+  bool staged_upd[2] = {false, false};  // the slot holds (ids, records) updates, not whole inputs
+  uint32_t staged_n[2] = {0, 0};
   int stage_next = 0;
+  uint32_t *upd_err_h = nullptr, *upd_err_d = nullptr;  // host-mapped count of out-of-shard ids
 };
 
 static scalesim_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SCALESIM_OK : SCALESIM_E_CUDA; }
@@ -1170,6 +1173,21 @@ extern "C" scalesim_status scalesim_sync(scalesim_ctx *c, scalesim_plan_host *ou
   return c->planned ? status_of_header(h.f[SCALESIM_H_STATUS]) : SCALESIM_OK;
 }
 
+// The step's header, then its lists, to the host (waits for the plan and its transfer).
+static scalesim_status read_back(scalesim_ctx *c, scalesim_plan_host *out, uint32_t *pf_out, uint32_t *ev_out) {
+  scalesim_plan_host h;
+  CK(cudaMemcpyAsync(h.f, c->p.d.header, sizeof(h.f), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (pf_out && h.f[SCALESIM_H_N_PREFETCH])
+    CK(cudaMemcpyAsync(pf_out, c->p.d.pf_ids, 4 * h.f[SCALESIM_H_N_PREFETCH], cudaMemcpyDeviceToHost, c->stream));
+  if (ev_out && h.f[SCALESIM_H_N_EVICT])
+    CK(cudaMemcpyAsync(ev_out, c->p.d.ev_ids, 4 * h.f[SCALESIM_H_N_EVICT], cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->copy_stream));
+  if (out) *out = h;
+  return status_of_header(h.f[SCALESIM_H_STATUS]);
+}
+
 extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, const uint32_t *host_rec,
                                               const float *host_kin, scalesim_plan_host *out, uint32_t *pf_out,
                                               uint32_t *ev_out) {
@@ -1177,7 +1195,9 @@ extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, cons
   if (c->p.n_kin > 0 && !host_kin) return SCALESIM_E_INVALID;
   int si = -1;  // inputs staged by scalesim_stage_host (their copy may still be in flight)
   for (int i = 0; i < 2; ++i)
-    if (c->staged[i] && c->staged_rec[i] == host_rec && (c->p.n_kin == 0 || c->staged_kin[i] == host_kin)) si = i;
+    if (c->staged[i] && !c->staged_upd[i] && c->staged_rec[i] == host_rec &&
+        (c->p.n_kin == 0 || c->staged_kin[i] == host_kin))
+      si = i;
   scalesim_status s;
   if (si >= 0) {
     const uint4 *rec0 = c->p.rec;
@@ -1198,43 +1218,111 @@ extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, cons
     s = scalesim_step(c, now, nullptr);
   }
   if (s != SCALESIM_OK) return s;
-  scalesim_plan_host h;
-  CK(cudaMemcpyAsync(h.f, c->p.d.header, sizeof(h.f), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  if (pf_out && h.f[SCALESIM_H_N_PREFETCH])
-    CK(cudaMemcpyAsync(pf_out, c->p.d.pf_ids, 4 * h.f[SCALESIM_H_N_PREFETCH], cudaMemcpyDeviceToHost, c->stream));
-  if (ev_out && h.f[SCALESIM_H_N_EVICT])
-    CK(cudaMemcpyAsync(ev_out, c->p.d.ev_ids, 4 * h.f[SCALESIM_H_N_EVICT], cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  CK(cudaStreamSynchronize(c->copy_stream));
-  if (out) *out = h;
-  return status_of_header(h.f[SCALESIM_H_STATUS]);
+  return read_back(c, out, pf_out, ev_out);
+}
+
+// A free staging slot (two per context), its buffer allocated and its last reader waited for
+// on in_stream; -1 when both slots hold staged steps.
+static int stage_slot(scalesim_ctx *c, scalesim_status *err) {
+  *err = SCALESIM_OK;
+  int i = c->stage_next;
+  if (c->staged[i]) i ^= 1;
+  if (c->staged[i]) {
+    *err = SCALESIM_E_ORDER;  // two staged steps not yet run
+    return -1;
+  }
+  auto fail = [&](cudaError_t e) { return e != cudaSuccess ? (*err = SCALESIM_E_CUDA, true) : false; };
+  if (!c->in_stream) {
+    if (fail(cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking))) return -1;
+    for (int k = 0; k < 2; ++k)
+      if (fail(cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming)) ||
+          fail(cudaEventCreateWithFlags(&c->ev_used[k], cudaEventDisableTiming)))
+        return -1;
+  }
+  // whole inputs (records + kinematics) or up to n_local (id, record) updates
+  const size_t full = 16 * (size_t)c->p.n_local + 16 * (size_t)c->p.n_kin, upd = 20 * (size_t)c->p.n_local + 16;
+  if (!c->sbuf[i] && fail(cudaMalloc(&c->sbuf[i], (full > upd ? full : upd) + 16))) return -1;
+  if (c->sbuf_used[i] && fail(cudaStreamWaitEvent(c->in_stream, c->ev_used[i], 0))) return -1;  // its last step read it
+  return i;
+}
+
+static void stage_commit(scalesim_ctx *c, int i, const void *key0, const void *key1, bool upd, uint32_t n) {
+  c->staged[i] = true;
+  c->staged_upd[i] = upd;
+  c->staged_rec[i] = key0;
+  c->staged_kin[i] = key1;
+  c->staged_n[i] = n;
+  c->stage_next = i ^ 1;
 }
 
 extern "C" scalesim_status scalesim_stage_host(scalesim_ctx *c, const uint32_t *host_rec, const float *host_kin) {
   if (!c || !host_rec) return SCALESIM_E_INVALID;
   if (c->p.n_kin > 0 && !host_kin) return SCALESIM_E_INVALID;
-  int i = c->stage_next;
-  if (c->staged[i]) i ^= 1;
-  if (c->staged[i]) return SCALESIM_E_ORDER;  // two staged steps not yet run
-  if (!c->in_stream) {
-    CK(cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking));
-    for (int k = 0; k < 2; ++k) {
-      CK(cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&c->ev_used[k], cudaEventDisableTiming));
-    }
-  }
+  scalesim_status err;
+  const int i = stage_slot(c, &err);
+  if (i < 0) return err;
   const size_t rb = 16 * (size_t)c->p.n_local, kb = 16 * (size_t)c->p.n_kin;
-  if (!c->sbuf[i]) CK(cudaMalloc(&c->sbuf[i], rb + kb > 0 ? rb + kb : 16));
-  if (c->sbuf_used[i]) CK(cudaStreamWaitEvent(c->in_stream, c->ev_used[i], 0));  // its last step read it
   if (rb) CK(cudaMemcpyAsync(c->sbuf[i], host_rec, rb, cudaMemcpyHostToDevice, c->in_stream));
   if (kb) CK(cudaMemcpyAsync(c->sbuf[i] + rb, host_kin, kb, cudaMemcpyHostToDevice, c->in_stream));
   CK(cudaEventRecord(c->ev_in[i], c->in_stream));
-  c->staged[i] = true;
-  c->staged_rec[i] = host_rec;
-  c->staged_kin[i] = host_kin;
-  c->stage_next = i ^ 1;
+  stage_commit(c, i, host_rec, host_kin, false, 0);
   return SCALESIM_OK;
+}
+
+// staged (ids, records) of n updates in slot i: ids at offset 0, records at the next 16-byte
+// boundary
+static size_t upd_rec_off(uint32_t n) { return ((size_t)4 * n + 15) / 16 * 16; }
+
+extern "C" scalesim_status scalesim_stage_updates(scalesim_ctx *c, const uint32_t *host_ids,
+                                                  const uint32_t *host_rec, uint32_t n_upd) {
+  if (!c || (n_upd > 0 && (!host_ids || !host_rec)) || n_upd > c->p.n_local || c->p.n_kin > 0)
+    return SCALESIM_E_INVALID;
+  scalesim_status err;
+  const int i = stage_slot(c, &err);
+  if (i < 0) return err;
+  if (n_upd) {
+    CK(cudaMemcpyAsync(c->sbuf[i], host_ids, 4 * (size_t)n_upd, cudaMemcpyHostToDevice, c->in_stream));
+    CK(cudaMemcpyAsync(c->sbuf[i] + upd_rec_off(n_upd), host_rec, 16 * (size_t)n_upd, cudaMemcpyHostToDevice,
+                       c->in_stream));
+  }
+  CK(cudaEventRecord(c->ev_in[i], c->in_stream));
+  stage_commit(c, i, host_ids, host_rec, true, n_upd);
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_step_updates(scalesim_ctx *c, int64_t now, const uint32_t *host_ids,
+                                                 const uint32_t *host_rec, uint32_t n_upd, scalesim_plan_host *out,
+                                                 uint32_t *pf_out, uint32_t *ev_out) {
+  if (!c || (n_upd > 0 && (!host_ids || !host_rec)) || n_upd > c->p.n_local || c->p.n_kin > 0)
+    return SCALESIM_E_INVALID;
+  int si = -1;
+  for (int i = 0; i < 2; ++i)
+    if (c->staged[i] && c->staged_upd[i] && c->staged_rec[i] == host_ids && c->staged_kin[i] == host_rec &&
+        c->staged_n[i] == n_upd)
+      si = i;
+  scalesim_status s;
+  if (si < 0) {  // not staged: stage now (the copy is then waited for right away)
+    if ((s = scalesim_stage_updates(c, host_ids, host_rec, n_upd)) != SCALESIM_OK) return s;
+    si = c->stage_next ^ 1;
+  }
+  if (!c->upd_err_h) {
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->upd_err_h), 16, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->upd_err_d), c->upd_err_h, 0));
+  }
+  *reinterpret_cast<volatile uint32_t *>(c->upd_err_h) = 0u;  // (the previous step has completed)
+  CK(cudaStreamWaitEvent(c->stream, c->ev_in[si], 0));
+  const uint8_t *b = c->sbuf[si];
+  c->launches += launch_apply_updates(const_cast<uint4 *>(c->p.rec), reinterpret_cast<const uint32_t *>(b),
+                                      reinterpret_cast<const uint4 *>(b + upd_rec_off(n_upd)), n_upd,
+                                      c->p.shard_begin, c->p.n_local, c->upd_err_d, c->stream);
+  CK(cudaGetLastError());
+  c->staged[si] = false;
+  c->sbuf_used[si] = true;
+  CK(cudaEventRecord(c->ev_used[si], c->stream));  // the next copy into sbuf[si] waits for the scatter
+  if ((s = scalesim_step(c, now, nullptr)) != SCALESIM_OK) return s;
+  s = read_back(c, out, pf_out, ev_out);
+  if (s == SCALESIM_OK && *reinterpret_cast<volatile uint32_t *>(c->upd_err_h)) return SCALESIM_E_BAD_INPUT;
+  return s;
 }
 
 extern "C" void scalesim_destroy(scalesim_ctx *c) {
@@ -1250,6 +1338,7 @@ extern "C" void scalesim_destroy(scalesim_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (int k = 0; k < 2; ++k)
     if (c->sbuf[k]) cudaFree(c->sbuf[k]);
+  if (c->upd_err_h) cudaFreeHost(c->upd_err_h);
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->tgroup) leave_group(c->tgroup);

@@ -1348,3 +1348,23 @@ int launch_xgather(unsigned long long *out, const void *const *ins, uint32_t G, 
 }
 
 }  // namespace ss
+
+namespace ss {
+// Incremental inputs (scalesim_stage_updates / scalesim_step_updates): the step's changed
+// agent records scattered into the context's resident record array.  One thread per update;
+// ids outside this shard are skipped and counted into *err (host-mapped, rare path).
+__global__ void k_apply_updates(uint4 *rec, const uint32_t *ids, const uint4 *upd, uint32_t n, uint64_t shard_begin,
+                                uint64_t n_local, uint32_t *err) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t a = (uint64_t)ids[i] - shard_begin;  // (ids below the shard wrap past n_local)
+    if (a < n_local) rec[a] = upd[i];
+    else atomicAdd(err, 1u);
+  }
+}
+int launch_apply_updates(uint4 *rec, const uint32_t *ids, const uint4 *upd, uint32_t n, uint64_t shard_begin,
+                         uint64_t n_local, uint32_t *err, cudaStream_t s) {
+  if (n == 0) return 0;
+  k_apply_updates<<<max(1, min(4 * 148, ceil_div(n, NT))), NT, 0, s>>>(rec, ids, upd, n, shard_begin, n_local, err);
+  return 1;
+}
+}  // namespace ss

@@ -189,6 +189,28 @@ class Planner:
         L.check(self.lib.scalesim_stage_host(self.ctx, rec_host.ctypes.data, kp), "scalesim_stage_host")
         self._staged_refs[rec_host.ctypes.data] = (rec_host, kin_host)
 
+    def stage_updates(self, ids: np.ndarray, recs: np.ndarray):
+        """Start the host->device copy of a later step's changed records (scalesim_stage_updates):
+        ids (n,) uint32 global agent ids, recs (n, 4) uint32, both C-contiguous (pinned for an
+        asynchronous copy).  Kept alive here until the matching step_updates."""
+        assert ids.dtype == np.uint32 and recs.dtype == np.uint32 and recs.shape == (len(ids), 4)
+        L.check(self.lib.scalesim_stage_updates(self.ctx, ids.ctypes.data, recs.ctypes.data, len(ids)),
+                "scalesim_stage_updates")
+        self._staged_refs[ids.ctypes.data] = (ids, recs)
+
+    def step_updates(self, now: int, ids: np.ndarray, recs: np.ndarray, pf_out: Optional[np.ndarray] = None,
+                     ev_out: Optional[np.ndarray] = None):
+        """Incremental end-to-end step (scalesim_step_updates): the changed records scattered into
+        the context's record buffer, the step, header + lists back."""
+        assert ids.dtype == np.uint32 and recs.dtype == np.uint32 and recs.shape == (len(ids), 4)
+        h = L.PlanHost()
+        st = self.lib.scalesim_step_updates(self.ctx, int(now), ids.ctypes.data, recs.ctypes.data, len(ids),
+                                            C.byref(h), None if pf_out is None else pf_out.ctypes.data,
+                                            None if ev_out is None else ev_out.ctypes.data)
+        self._staged_refs.pop(ids.ctypes.data, None)
+        L.check(st, "scalesim_step_updates", allow=(L.OK, L.E_INSUFFICIENT))
+        return h.as_dict()
+
     def join(self):
         L.check(self.lib.scalesim_join(self.ctx), "scalesim_join")
 

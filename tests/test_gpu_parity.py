@@ -196,6 +196,60 @@ def test_pipelined_host_steps_c4_shape(exclusive):
     pl.close()
 
 
+def _oracle_step(w, s, res):
+    d_or, _ = oracle.score(w.rec[s], None, int(w.now[s]), w.hop_scale)
+    return oracle.plan(w.rec[s], d_or, res, w.theta, w.budget)
+
+
+def _assert_host_plan(h, pf, ev, p, s):
+    assert h["cut_bits"] == p["cut_bits"] and h["cut_rem"] == p["cut_rem"], s
+    assert h["kept_bytes"] == p["kept_bytes"] and h["bytes_h2d"] == p["bytes_h2d"], s
+    assert h["n_prefetch"] == len(p["prefetch"]) and h["n_evict"] == len(p["evict"]), s
+    assert np.array_equal(pf[:h["n_prefetch"]], p["prefetch"]), s
+    assert np.array_equal(ev[:h["n_evict"]], p["evict"]), s
+
+
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_incremental_host_steps_c4_shape(exclusive):
+    """scalesim_stage_updates + scalesim_step_updates (the bench's e2e loop): after one whole
+    upload, each step sends only the records that changed; staged one step ahead, plus one
+    unstaged step and one step without changes; every plan equals the oracle's on the full
+    records.  An id outside the shard is reported (E_BAD_INPUT) and skipped."""
+    import torch
+    from paper_2601_21473_b200 import _lib as L
+    from gpu_harness import make_planner
+    w = tg.config_c4(seed=6, steps=8, n=300_000)
+    w.rec[5] = w.rec[4]  # a step without changes
+    pl = make_planner(w, transfer=False, keep_dist=False, exclusive=exclusive)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    ids, recs = [None], [None]
+    for s in range(1, w.steps):
+        ch = np.nonzero(np.any(w.rec[s] != w.rec[s - 1], axis=1))[0].astype(np.uint32)
+        ids.append(pin(ch))
+        recs.append(pin(w.rec[s][ch]))
+    assert len(ids[5]) == 0 and 0 < len(ids[1]) < w.n // 5
+    pf = np.zeros(w.n, np.uint32)
+    ev = np.zeros(w.n, np.uint32)
+    res = np.zeros(w.n, np.uint8)
+    h = pl.step_host(int(w.now[0]), pin(w.rec[0]), None, pf, ev)
+    p = _oracle_step(w, 0, res)
+    _assert_host_plan(h, pf, ev, p, 0)
+    res = p["resident"].astype(np.uint8)
+    pl.stage_updates(ids[1], recs[1])
+    for s in range(1, w.steps):
+        if s + 1 < w.steps and s != 2:  # step 3 is not staged: its copy is synchronous
+            pl.stage_updates(ids[s + 1], recs[s + 1])
+        h = pl.step_updates(int(w.now[s]), ids[s], recs[s], pf, ev)
+        p = _oracle_step(w, s, res)
+        _assert_host_plan(h, pf, ev, p, s)
+        res = p["resident"].astype(np.uint8)
+    bad = pin(np.array([w.n + 7], np.uint32))
+    with pytest.raises(L.ScaleSimError) as e:
+        pl.step_updates(int(w.now[w.steps - 1]), bad, pin(w.rec[0][:1]), pf, ev)
+    assert e.value.status == L.E_BAD_INPUT
+    pl.close()
+
+
 def test_fused_multi_level_select_and_segments():
     """Distances spread over many values (boundary bucket with several distances: select
     levels 2 and 3; evict segments that need the re-sort by full key), fused vs oracle."""
