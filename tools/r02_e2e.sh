@@ -1,0 +1,13 @@
+#!/bin/bash
+# The host entry points: parity tests of the pipelined / incremental host steps, then the bench's
+# e2e legs (headline leg only)
+TAG=${TAG:-r02_vX}
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests -m gpu -x -q -k "pipelined or incremental or host_step" > gpurun_out/${TAG}_pytest_e2e.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_e2e.log
+tail -3 gpurun_out/${TAG}_pytest_e2e.log
+ARGS="--no-transfer-leg --no-cpu-baseline --no-c5 --no-objects --no-c3 --no-closed-loop --no-sweep --no-sched"
+timeout 600 python bench.py $ARGS > gpurun_out/${TAG}_bench_e2e.jsonl 2> gpurun_out/${TAG}_bench_e2e.err; echo "bench rc=$?" >> gpurun_out/${TAG}_bench_e2e.err
+tail -3 gpurun_out/${TAG}_bench_e2e.err
+python -c "
+import json; l=json.loads(open('gpurun_out/${TAG}_bench_e2e.jsonl').read().strip().splitlines()[-1]); print('BENCH', l['value'], l['ms_per_step']); print(json.dumps(l['e2e']))"
