@@ -37,6 +37,25 @@ size_t fused_smem_bytes(uint32_t tile) {
   return (size_t)4 * (3 * tile + 5 * tw + 4 * NB1) + 16;
 }
 
+// A/B only (-DAB_P1_TMA): P1 staging by bulk copies (fast variant): the tile's records land in
+// shared memory in chunks of P1_CH records, each with its own mbarrier, all issued at once by
+// one thread.  The chunks live in memory P1 does not use: the scratch array s.memb, then from
+// s.h + 3 NB1 on (the need list, the owner staging s.col and any dynamic shared memory beyond
+// them).  Parity-green, but measured slower at C4 (profiles/r02_v65_ab_p1_tma.log,
+// r02_v66_probe.log: P1 loop 8.1 vs 6.8 us, step 26.9 vs 24.5 us): the register-load P1 is
+// issue-bound, not load-bound, so taking the loads off the warps gains nothing while the
+// copies arrive later than the warps' own batches.
+constexpr uint32_t P1_CH = 256, P1_MAXCH = 32;
+static size_t p1_region2_off(uint32_t tile) {  // byte offset of s.h + 3 NB1 (carve)
+  return ((size_t)4 * (3 * tile + 5 * (tile / 32)) + 15) / 16 * 16 + (size_t)4 * 3 * NB1;
+}
+// dynamic shared memory the staging needs for a full tile (0: staging impossible)
+static size_t p1_staging_bytes(uint32_t tile) {
+  const uint32_t ch_m = tile * 4 / (P1_CH * 16), nch = (tile + P1_CH - 1) / P1_CH;
+  if (nch > P1_MAXCH) return 0;
+  return p1_region2_off(tile) + (size_t)(nch > ch_m ? nch - ch_m : 0) * P1_CH * 16;
+}
+
 template <int MAXB>
 __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ FusedArgs<MAXB> B) {
   // (single context: instance 0 at constant offsets, so its fields stay in uniform registers)
@@ -126,6 +145,39 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       base >= p.n_local ? 0u : (uint32_t)((p.n_local - base) < A.tile ? (p.n_local - base) : A.tile);
   const uint32_t tw_here = (n_here + 31) / 32;
   const int par = A.parity;
+  // P1 record staging (see P1_CH): CTA-uniform decision; the copies go out right away
+  const bool fast = p.int_mode != 0 && p.explicit_dist == 0 && A.now >= 0 && A.now <= 0xFFFFFFFFll && !p.keep_dist;
+  __shared__ __align__(8) unsigned long long s_p1bar[P1_MAXCH];
+  const uint32_t p1_chm = A.tile * 4 / (P1_CH * 16), p1_nch = (n_here + P1_CH - 1) / P1_CH;
+  uint4 *const p1_r1 = reinterpret_cast<uint4 *>(s.memb), *const p1_r2 = reinterpret_cast<uint4 *>(s.h + 3 * NB1);
+  bool p1_tma;
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const uint32_t off2 = (uint32_t)(reinterpret_cast<uint8_t *>(p1_r2) - smem_raw);
+    const uint32_t ch2 = dyn > off2 ? (dyn - off2) / (P1_CH * 16) : 0u;
+#ifdef AB_P1_TMA
+    p1_tma = fast && n_here > 0 && p1_nch <= P1_MAXCH && p1_nch <= p1_chm + ch2;
+#else
+    p1_tma = false;
+#endif
+  }
+  if (p1_tma && threadIdx.x == 0) {
+    for (uint32_t j = 0; j < p1_nch; ++j)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_p1bar[j])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (uint32_t j = 0; j < p1_nch; ++j) {
+      const uint32_t nb = 16 * min(P1_CH, n_here - j * P1_CH);
+      const uint32_t b = (uint32_t)__cvta_generic_to_shared(&s_p1bar[j]);
+      uint4 *dst = j < p1_chm ? p1_r1 + j * P1_CH : p1_r2 + (j - p1_chm) * P1_CH;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(nb) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(dst)),
+                   "l"(p.rec + base + j * P1_CH), "r"(nb), "r"(b)
+                   : "memory");
+    }
+  }
   // accumulators of this launch: [0] zero-distance bytes [1] h2d [2] d2h [3] tie kept
   // [4] eligible agents [5] status
   unsigned long long *acc = d.f_acc + 8 * par;
@@ -158,7 +210,14 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   };
   const uint32_t *bm_tile = bm_old + base / 32;
   for (uint32_t w = threadIdx.x; w < A.tw; w += FT) s.old_w[w] = w < tw_here ? bm_tile[w] : 0u;
-  clear_hist(s.h, NB1);
+  if (p1_tma) {  // (integer mode: no min / max rows; [3 NB1, 4 NB1) holds staged records)
+    for (int b = threadIdx.x; b < NB1; b += FT) {
+      s.h[b] = 0;
+      s.h[NB1 + b] = 0;
+    }
+  } else {
+    clear_hist(s.h, NB1);
+  }
   if (imode)  // [2 * NB1, 3 * NB1): eligible counts per bucket (non-resident | resident << 16)
     for (int b = threadIdx.x; b < NB1; b += FT) s.h[2 * NB1 + b] = 0u;  // (4 per thread)
   // this CTA's eligible agents in multi-valued integer buckets (placed by one CTA, fast path)
@@ -233,7 +292,6 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   };
   using T_ = std::true_type;
   using F_ = std::false_type;
-  const bool fast = imode && !xdist && now32 && gkeys == nullptr;
   // one record body per variant (always masked; a rolled loop): the kernel's executed code has
   // to stay small (instruction-fetch stalls, see PROBE)
   auto batch = [&](uint4 (&rr)[LOAD_BATCH], uint32_t k0) {
@@ -249,6 +307,26 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   // (measured: P1 loop 6.0 vs 6.3 us with single batches, profiles/r01_v9_ab_dbuf.log)
   uint4 r2[LOAD_BATCH];
   const uint32_t BS = LOAD_BATCH * FT, nk = A.tw * 32;
+  if (p1_tma) {  // records from the staged chunks, each consumed as soon as its copy lands
+#pragma unroll 1
+    for (uint32_t k0 = 0; k0 < nk; k0 += FT) {
+      const uint32_t wd = k0 / 32 + warp;
+      if (wd >= A.tw) break;  // (warp-uniform; later rounds are further out)
+      const uint32_t k = k0 + threadIdx.x, j = k / P1_CH;
+      uint4 rj = make_uint4(0, 0, 0, 0);
+      if (k < n_here) {
+        const uint32_t b = (uint32_t)__cvta_generic_to_shared(&s_p1bar[j]);
+        uint32_t ok = 0;
+        while (!ok)
+          asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0; selp.u32 %0, 1, 0, q; }"
+                       : "=r"(ok)
+                       : "r"(b)
+                       : "memory");
+        rj = (j < p1_chm ? p1_r1 + j * P1_CH : p1_r2 + (j - p1_chm) * P1_CH)[k % P1_CH];
+      }
+      record(rj, wd, T_(), T_());
+    }
+  } else {
   load_into(r, 0);
 #ifdef AB_P1_UNROLL2  // A/B: the two batches of a loop iteration as separate code copies
   for (uint32_t k0 = 0; k0 < nk; k0 += 2 * BS) {
@@ -267,6 +345,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     for (int j = 0; j < LOAD_BATCH; ++j) r[j] = r2[j];
   }
 #endif
+  }
   if (!imode) warp_add_u64(zero_b, sacc);
   __syncthreads();
   STAMP_MAX(25)  // P1 loop done
@@ -1458,15 +1537,23 @@ static size_t smem_limit() {
 template <int MAXB>
 static size_t launch_smem(uint32_t tile, uint32_t gsize, uint32_t *fastok) {
   const size_t base = fused_smem_bytes(tile), lim = smem_limit<MAXB>();
+  size_t sm;
   if (gsize <= 1) {  // one CTA per instance: no bucket owners
     *fastok = 1;
-    return base;
+    sm = base;
+  } else {
+    // bucket-owner staging: [G][RB] counts + [4][RB] totals / offsets
+    const uint32_t RB = ((4096 + gsize - 1) / gsize + 3u) & ~3u;
+    const size_t need = (size_t)4 * RB * (gsize + 4);
+    *fastok = base + need <= lim ? 1u : 0u;  // else the two-barrier list path
+    sm = base + (*fastok ? need : 0);
   }
-  // bucket-owner staging: [G][RB] counts + [4][RB] totals / offsets
-  const uint32_t RB = ((4096 + gsize - 1) / gsize + 3u) & ~3u;
-  const size_t need = (size_t)4 * RB * (gsize + 4);
-  *fastok = base + need <= lim ? 1u : 0u;  // else the two-barrier list path
-  return base + (*fastok ? need : 0);
+#ifdef AB_P1_TMA
+  // P1 record staging when the whole tile fits (the kernel checks %dynamic_smem_size)
+  const size_t st = p1_staging_bytes(tile);
+  if (st > sm && st <= lim) sm = st;
+#endif
+  return sm;
 }
 
 // 1 CTA of FT threads per SM must be resident for the whole grid (grid barrier).

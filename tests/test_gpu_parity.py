@@ -267,6 +267,7 @@ def test_fused_multi_level_select_and_segments():
     budget = int(fp.sum() * 0.3)
     w = tg.Workload("spread", n, np.array([0, 0]), rec, None, blocks, budget, np.full(3, np.inf, np.float32))
     run_parity(w, transfer=False)
+    run_parity(w, transfer=False, keep_dist=False)  # (staged P1 records, two-barrier list path)
     run_parity(w, transfer=False, multi_kernel=True)
     run_parity(w)
 
@@ -325,6 +326,7 @@ def test_fused_wide_code_segments():
     w = tg.Workload("wide", n, np.zeros(3, np.int64), np.stack(recs), None, blocks, int(fp.sum() * 0.3),
                     np.full(3, np.inf, np.float32))
     run_parity(w, transfer=False)
+    run_parity(w, transfer=False, keep_dist=False)
     run_parity(w, transfer=False, multi_kernel=True)
 
 
