@@ -622,7 +622,7 @@ def main():
     ap.add_argument("--eager", action="store_true", help="no CUDA graph")
     ap.add_argument("--no-transfer-leg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=32)
+    ap.add_argument("--e2e-steps", type=int, default=64)
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 replicas x budgets leg")
     ap.add_argument("--c5-replicas", type=int, default=64)
     ap.add_argument("--no-objects", action="store_true", help="skip the shared-object leg (NEXT #1)")
@@ -828,7 +828,19 @@ def main():
         hb = db = 0
         if mode == "full":
             pl.stage_host(rec_host[0])
-        for k in range(e2e_k):
+        if mode == "submit":  # two steps in flight: step k+1 plans while step k is collected
+            h = pl.step_host(int(w.now[t_base]), rec_host[0], None, pf, ev)
+            hb += rec_host[0].nbytes
+            db += 128 + 4 * (h["n_prefetch"] + h["n_evict"])
+            if e2e_k > 1:
+                pl.submit_updates(int(w.now[t_base + 1]), *upd[1])
+            for k in range(1, e2e_k):
+                if k + 1 < e2e_k:
+                    pl.submit_updates(int(w.now[t_base + k + 1]), *upd[k + 1])
+                h = pl.collect(pf, ev)
+                hb += upd[k][0].nbytes + upd[k][1].nbytes
+                db += 128 + 4 * (h["n_prefetch"] + h["n_evict"])
+        for k in range(e2e_k if mode != "submit" else 0):
             if mode == "updates" and k > 0:
                 if k + 1 < e2e_k:
                     pl.stage_updates(*upd[k + 1])
@@ -853,12 +865,15 @@ def main():
     # are allocated on first use), then timed
     el_s, _, _ = [e2e_loop("sync") for _ in range(2)][-1]
     el_f, h2d_f, _ = [e2e_loop("full") for _ in range(2)][-1]
-    el_e, h2d_b, d2h_b = [e2e_loop("updates") for _ in range(2)][-1]
+    el_u, _, _ = [e2e_loop("updates") for _ in range(2)][-1]
+    el_e, h2d_b, d2h_b = [e2e_loop("submit") for _ in range(2)][-1]
     e2e = {"value": n * world * e2e_k / el_e, "unit": "agent-plans/s", "h2d_bytes_per_step": h2d_b // e2e_k,
            "d2h_bytes_per_step": d2h_b // e2e_k, "steps": e2e_k,
-           "api": "scalesim_step_updates: step 0 whole records (scalesim_step_host), then each step's "
-                  "changed records (ids + 16-byte records, pinned) staged one step ahead by "
-                  "scalesim_stage_updates; header + lists back every step; host-timed",
+           "api": "step 0 whole records (scalesim_step_host), then each step's changed records (ids + "
+                  "16-byte records, pinned) by scalesim_submit_updates, two steps in flight, header + "
+                  "lists of every step back through scalesim_collect; host-timed, all copies inside",
+           "sync_updates_value": n * world * e2e_k / el_u,
+           "sync_updates_api": "scalesim_stage_updates one step ahead + scalesim_step_updates (synchronous)",
            "changed_per_step": float(np.mean([len(u[0]) for u in upd[1:]])) if e2e_k > 1 else None,
            "whole_records_value": n * world * e2e_k / el_f, "whole_records_h2d_bytes_per_step": h2d_f // e2e_k,
            "whole_records_h2d_GBs": h2d_f / el_f / 1e9,

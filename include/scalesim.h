@@ -20,8 +20,12 @@
  * Conventions (all calls):
  *   - Every entry point returns scalesim_status and never throws or aborts.
  *   - Ownership: the caller owns every buffer (typically torch tensors) and keeps them alive
- *     until scalesim_destroy.  The library never allocates device memory after init; all
- *     scratch lives in the caller's workspace (size from scalesim_workspace_bytes).
+ *     until scalesim_destroy.  The device entry points never allocate memory after init; all
+ *     scratch lives in the caller's workspace (size from scalesim_workspace_bytes).  The host
+ *     entry points (scalesim_step_host, _stage_host, _stage_updates, _step_updates,
+ *     _submit_updates, _collect) allocate, on first use, library-owned staging: two device
+ *     input buffers of max(16 (n_local + n_kin), 20 n_local) bytes, two host-mapped pinned
+ *     read-back slots of 256 + 8 n_local bytes, and one input stream; freed by scalesim_destroy.
  *   - Asynchrony: score/plan/transfer/step enqueue work on the caller's CUDA streams and
  *     return without a host synchronisation (graph-capturable).  Device-detected conditions
  *     (budget too small for the active agents, malformed records) are reported in the
@@ -393,6 +397,23 @@ scalesim_status scalesim_stage_updates(scalesim_ctx *ctx, const uint32_t *host_i
 scalesim_status scalesim_step_updates(scalesim_ctx *ctx, int64_t now_tick, const uint32_t *host_ids,
                                       const uint32_t *host_rec, uint32_t n_upd, scalesim_plan_host *out,
                                       uint32_t *prefetch_out, uint32_t *evict_out);
+
+/* Asynchronous form of scalesim_step_updates: submit enqueues the step (its updates' copy on
+ * the library's input stream, the scatter, the plan, and the read-back of header and lists
+ * into library-owned host-mapped memory) and returns at once; collect waits for the OLDEST
+ * submitted step and copies its header and lists out (prefetch_out / evict_out: host,
+ * n_local capacity each, may be NULL).  Steps run in submission order on the device; while
+ * the host collects step t, step t+1 already plans.  Usage: submit(0); for t: { submit(t+1);
+ * collect(t); }.  At most two submitted steps may be uncollected (SCALESIM_E_ORDER), and
+ * scalesim_step_host / scalesim_step_updates refuse to run (SCALESIM_E_ORDER) until all are
+ * collected.  The host arrays must stay unchanged until their step is collected.  Errors of
+ * submit: as scalesim_stage_updates; of collect: SCALESIM_E_ORDER (nothing submitted),
+ * SCALESIM_E_BAD_INPUT (that step had ids outside the shard), SCALESIM_E_INSUFFICIENT /
+ * SCALESIM_E_INVARIANT per its status word, SCALESIM_E_CUDA. */
+scalesim_status scalesim_submit_updates(scalesim_ctx *ctx, int64_t now_tick, const uint32_t *host_ids,
+                                        const uint32_t *host_rec, uint32_t n_upd);
+scalesim_status scalesim_collect(scalesim_ctx *ctx, scalesim_plan_host *out, uint32_t *prefetch_out,
+                                 uint32_t *evict_out);
 
 /* Point the context at another record / kinematics buffer (same sizes; device). */
 scalesim_status scalesim_set_inputs(scalesim_ctx *ctx, const uint32_t *agent_rec, const float *agent_kin);

@@ -35,7 +35,7 @@ HEADER_NAMES = ["n_prefetch", "n_evict", "bytes_h2d", "bytes_d2h", "cut_bits", "
 
 # Every symbol include/scalesim.h declares (checked by tests/test_abi.py).
 EXPORTS = ["scalesim_workspace_bytes", "scalesim_init", "scalesim_score", "scalesim_plan",
-           "scalesim_transfer", "scalesim_view", "scalesim_step", "scalesim_step_batch", "scalesim_step_group", "scalesim_world_view", "scalesim_step_host", "scalesim_stage_host", "scalesim_stage_updates", "scalesim_step_updates", "scalesim_set_inputs",
+           "scalesim_transfer", "scalesim_view", "scalesim_step", "scalesim_step_batch", "scalesim_step_group", "scalesim_world_view", "scalesim_step_host", "scalesim_stage_host", "scalesim_stage_updates", "scalesim_step_updates", "scalesim_submit_updates", "scalesim_collect", "scalesim_set_inputs",
            "scalesim_sync", "scalesim_join", "scalesim_nccl_unique_id", "scalesim_fused", "scalesim_profile_stamps", "scalesim_object_min", "scalesim_lru_records", "scalesim_bfs_scratch_bytes", "scalesim_bfs_hops", "scalesim_sched_scratch_bytes", "scalesim_sched_run", "scalesim_launch_count", "scalesim_destroy",
            "scalesim_strerror"]
 
@@ -129,6 +129,10 @@ def lib():
         L.scalesim_stage_updates.restype = C.c_int
         L.scalesim_step_updates.argtypes = [vp, i64, vp, vp, C.c_uint32, C.POINTER(PlanHost), vp, vp]
         L.scalesim_step_updates.restype = C.c_int
+        L.scalesim_submit_updates.argtypes = [vp, i64, vp, vp, C.c_uint32]
+        L.scalesim_submit_updates.restype = C.c_int
+        L.scalesim_collect.argtypes = [vp, C.POINTER(PlanHost), vp, vp]
+        L.scalesim_collect.restype = C.c_int
         L.scalesim_set_inputs.argtypes = [vp, vp, vp]
         L.scalesim_set_inputs.restype = C.c_int
         L.scalesim_sync.argtypes = [vp, C.POINTER(PlanHost)]

@@ -373,6 +373,12 @@ struct scalesim_ctx {
   uint32_t staged_n[2] = {0, 0};
   int stage_next = 0;
   uint32_t *upd_err_h = nullptr, *upd_err_d = nullptr;  // host-mapped count of out-of-shard ids
+  // host read-back (read_back): host-mapped pinned [done word | header | prefetch | evict]
+  uint8_t *rb_h = nullptr, *rb_d = nullptr;
+  unsigned int *rb_tickets = nullptr;
+  unsigned long long rb_seq = 0;          // read-backs enqueued (slot = seq % 2)
+  unsigned long long rb_pending[2] = {0, 0};  // submitted steps not yet collected, oldest first
+  int n_pending = 0;
 };
 
 static scalesim_status cuda_status(cudaError_t e) { return e == cudaSuccess ? SCALESIM_OK : SCALESIM_E_CUDA; }
@@ -1173,19 +1179,59 @@ extern "C" scalesim_status scalesim_sync(scalesim_ctx *c, scalesim_plan_host *ou
   return c->planned ? status_of_header(h.f[SCALESIM_H_STATUS]) : SCALESIM_OK;
 }
 
-// The step's header, then its lists, to the host (waits for the plan and its transfer).
-static scalesim_status read_back(scalesim_ctx *c, scalesim_plan_host *out, uint32_t *pf_out, uint32_t *ev_out) {
+// The step's header and lists to the host: k_readback writes them into host-mapped pinned
+// memory (two slots, seq % 2: [done word | header @128 | prefetch @256 | evict]) and then the
+// slot's completion word, which the host polls (one kernel instead of three copies and two
+// stream synchronisations); the stream is queried now and then so that a failed launch returns
+// instead of spinning.
+static size_t rb_slot_bytes(const scalesim_ctx *c) { return 256 + 8 * (size_t)c->p.n_local; }
+
+static scalesim_status enqueue_readback(scalesim_ctx *c, unsigned long long *seq_out) {
+  if (!c->rb_h) {
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->rb_h), 2 * rb_slot_bytes(c), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->rb_d), c->rb_h, 0));
+    CK(cudaMalloc(&c->rb_tickets, 16));
+    CK(cudaMemset(c->rb_tickets, 0, 16));
+    for (int k = 0; k < 2; ++k) *reinterpret_cast<volatile unsigned long long *>(c->rb_h + k * rb_slot_bytes(c)) = 0ull;
+  }
+  const unsigned long long seq = ++c->rb_seq;
+  uint8_t *d = c->rb_d + (seq & 1) * rb_slot_bytes(c);
+  auto *wd = reinterpret_cast<unsigned long long *>(d);
+  c->launches += launch_readback(reinterpret_cast<const unsigned long long *>(c->p.d.header), c->p.d.pf_ids,
+                                 c->p.d.ev_ids, wd + 16, reinterpret_cast<uint32_t *>(d + 256),
+                                 reinterpret_cast<uint32_t *>(d + 256 + 4 * c->p.n_local), wd, seq,
+                                 c->rb_tickets + (seq & 1), c->stream);
+  CK(cudaGetLastError());
+  *seq_out = seq;
+  return SCALESIM_OK;
+}
+
+static scalesim_status wait_readback(scalesim_ctx *c, unsigned long long seq, scalesim_plan_host *out,
+                                     uint32_t *pf_out, uint32_t *ev_out) {
+  const uint8_t *hb = c->rb_h + (seq & 1) * rb_slot_bytes(c);
+  volatile const unsigned long long *word = reinterpret_cast<volatile const unsigned long long *>(hb);
+  for (uint64_t spin = 1; *word != seq; ++spin) {
+    if ((spin & 1023) == 0) {
+      const cudaError_t e = cudaStreamQuery(c->stream);
+      if (e == cudaSuccess && *word != seq) return SCALESIM_E_CUDA;  // (done without the word: cannot happen)
+      if (e != cudaSuccess && e != cudaErrorNotReady) return cuda_status(e);
+    }
+  }
   scalesim_plan_host h;
-  CK(cudaMemcpyAsync(h.f, c->p.d.header, sizeof(h.f), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  if (pf_out && h.f[SCALESIM_H_N_PREFETCH])
-    CK(cudaMemcpyAsync(pf_out, c->p.d.pf_ids, 4 * h.f[SCALESIM_H_N_PREFETCH], cudaMemcpyDeviceToHost, c->stream));
-  if (ev_out && h.f[SCALESIM_H_N_EVICT])
-    CK(cudaMemcpyAsync(ev_out, c->p.d.ev_ids, 4 * h.f[SCALESIM_H_N_EVICT], cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  CK(cudaStreamSynchronize(c->copy_stream));
+  memcpy(h.f, hb + 128, sizeof(h.f));
+  if (pf_out && h.f[SCALESIM_H_N_PREFETCH]) memcpy(pf_out, hb + 256, 4 * h.f[SCALESIM_H_N_PREFETCH]);
+  if (ev_out && h.f[SCALESIM_H_N_EVICT]) memcpy(ev_out, hb + 256 + 4 * c->p.n_local, 4 * h.f[SCALESIM_H_N_EVICT]);
+  if (c->transfer) CK(cudaStreamSynchronize(c->copy_stream));
   if (out) *out = h;
   return status_of_header(h.f[SCALESIM_H_STATUS]);
+}
+
+// (waits for the plan and its transfer)
+static scalesim_status read_back(scalesim_ctx *c, scalesim_plan_host *out, uint32_t *pf_out, uint32_t *ev_out) {
+  if (c->n_pending) return SCALESIM_E_ORDER;  // submitted steps not collected (their slots)
+  unsigned long long seq;
+  scalesim_status s = enqueue_readback(c, &seq);
+  return s != SCALESIM_OK ? s : wait_readback(c, seq, out, pf_out, ev_out);
 }
 
 extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, const uint32_t *host_rec,
@@ -1193,6 +1239,7 @@ extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, cons
                                               uint32_t *ev_out) {
   if (!c || !host_rec) return SCALESIM_E_INVALID;
   if (c->p.n_kin > 0 && !host_kin) return SCALESIM_E_INVALID;
+  if (c->n_pending) return SCALESIM_E_ORDER;  // submitted steps not collected
   int si = -1;  // inputs staged by scalesim_stage_host (their copy may still be in flight)
   for (int i = 0; i < 2; ++i)
     if (c->staged[i] && !c->staged_upd[i] && c->staged_rec[i] == host_rec &&
@@ -1290,9 +1337,10 @@ extern "C" scalesim_status scalesim_stage_updates(scalesim_ctx *c, const uint32_
   return SCALESIM_OK;
 }
 
-extern "C" scalesim_status scalesim_step_updates(scalesim_ctx *c, int64_t now, const uint32_t *host_ids,
-                                                 const uint32_t *host_rec, uint32_t n_upd, scalesim_plan_host *out,
-                                                 uint32_t *pf_out, uint32_t *ev_out) {
+// Scatter of one step's updates (staged or copied now on in_stream) and the step, enqueued;
+// the step's out-of-shard count goes to the host-mapped word of read-back slot `slot`.
+static scalesim_status enqueue_updates_step(scalesim_ctx *c, int64_t now, const uint32_t *host_ids,
+                                            const uint32_t *host_rec, uint32_t n_upd, int slot) {
   if (!c || (n_upd > 0 && (!host_ids || !host_rec)) || n_upd > c->p.n_local || c->p.n_kin > 0)
     return SCALESIM_E_INVALID;
   int si = -1;
@@ -1301,7 +1349,7 @@ extern "C" scalesim_status scalesim_step_updates(scalesim_ctx *c, int64_t now, c
         c->staged_n[i] == n_upd)
       si = i;
   scalesim_status s;
-  if (si < 0) {  // not staged: stage now (the copy is then waited for right away)
+  if (si < 0) {  // not staged: the copy goes out now
     if ((s = scalesim_stage_updates(c, host_ids, host_rec, n_upd)) != SCALESIM_OK) return s;
     si = c->stage_next ^ 1;
   }
@@ -1309,19 +1357,55 @@ extern "C" scalesim_status scalesim_step_updates(scalesim_ctx *c, int64_t now, c
     CK(cudaHostAlloc(reinterpret_cast<void **>(&c->upd_err_h), 16, cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->upd_err_d), c->upd_err_h, 0));
   }
-  *reinterpret_cast<volatile uint32_t *>(c->upd_err_h) = 0u;  // (the previous step has completed)
+  // (the slot's previous step has been collected: its kernels are done)
+  reinterpret_cast<volatile uint32_t *>(c->upd_err_h)[slot] = 0u;
   CK(cudaStreamWaitEvent(c->stream, c->ev_in[si], 0));
   const uint8_t *b = c->sbuf[si];
   c->launches += launch_apply_updates(const_cast<uint4 *>(c->p.rec), reinterpret_cast<const uint32_t *>(b),
                                       reinterpret_cast<const uint4 *>(b + upd_rec_off(n_upd)), n_upd,
-                                      c->p.shard_begin, c->p.n_local, c->upd_err_d, c->stream);
+                                      c->p.shard_begin, c->p.n_local, c->upd_err_d + slot, c->stream);
   CK(cudaGetLastError());
   c->staged[si] = false;
   c->sbuf_used[si] = true;
   CK(cudaEventRecord(c->ev_used[si], c->stream));  // the next copy into sbuf[si] waits for the scatter
-  if ((s = scalesim_step(c, now, nullptr)) != SCALESIM_OK) return s;
+  return scalesim_step(c, now, nullptr);
+}
+
+extern "C" scalesim_status scalesim_step_updates(scalesim_ctx *c, int64_t now, const uint32_t *host_ids,
+                                                 const uint32_t *host_rec, uint32_t n_upd, scalesim_plan_host *out,
+                                                 uint32_t *pf_out, uint32_t *ev_out) {
+  if (!c) return SCALESIM_E_INVALID;
+  if (c->n_pending) return SCALESIM_E_ORDER;
+  const int slot = (int)((c->rb_seq + 1) & 1);
+  scalesim_status s = enqueue_updates_step(c, now, host_ids, host_rec, n_upd, slot);
+  if (s != SCALESIM_OK) return s;
   s = read_back(c, out, pf_out, ev_out);
-  if (s == SCALESIM_OK && *reinterpret_cast<volatile uint32_t *>(c->upd_err_h)) return SCALESIM_E_BAD_INPUT;
+  if (s == SCALESIM_OK && reinterpret_cast<volatile uint32_t *>(c->upd_err_h)[slot]) return SCALESIM_E_BAD_INPUT;
+  return s;
+}
+
+extern "C" scalesim_status scalesim_submit_updates(scalesim_ctx *c, int64_t now, const uint32_t *host_ids,
+                                                   const uint32_t *host_rec, uint32_t n_upd) {
+  if (!c) return SCALESIM_E_INVALID;
+  if (c->n_pending >= 2) return SCALESIM_E_ORDER;  // both read-back slots hold uncollected steps
+  const int slot = (int)((c->rb_seq + 1) & 1);
+  scalesim_status s = enqueue_updates_step(c, now, host_ids, host_rec, n_upd, slot);
+  if (s != SCALESIM_OK) return s;
+  unsigned long long seq;
+  if ((s = enqueue_readback(c, &seq)) != SCALESIM_OK) return s;
+  c->rb_pending[c->n_pending++] = seq;
+  return SCALESIM_OK;
+}
+
+extern "C" scalesim_status scalesim_collect(scalesim_ctx *c, scalesim_plan_host *out, uint32_t *pf_out,
+                                            uint32_t *ev_out) {
+  if (!c) return SCALESIM_E_INVALID;
+  if (c->n_pending == 0) return SCALESIM_E_ORDER;
+  const unsigned long long seq = c->rb_pending[0];
+  c->rb_pending[0] = c->rb_pending[1];
+  c->n_pending--;
+  scalesim_status s = wait_readback(c, seq, out, pf_out, ev_out);
+  if (s == SCALESIM_OK && reinterpret_cast<volatile uint32_t *>(c->upd_err_h)[seq & 1]) return SCALESIM_E_BAD_INPUT;
   return s;
 }
 
@@ -1339,6 +1423,8 @@ extern "C" void scalesim_destroy(scalesim_ctx *c) {
   for (int k = 0; k < 2; ++k)
     if (c->sbuf[k]) cudaFree(c->sbuf[k]);
   if (c->upd_err_h) cudaFreeHost(c->upd_err_h);
+  if (c->rb_h) cudaFreeHost(c->rb_h);
+  if (c->rb_tickets) cudaFree(c->rb_tickets);
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->tgroup) leave_group(c->tgroup);

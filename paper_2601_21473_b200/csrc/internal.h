@@ -225,6 +225,9 @@ constexpr uint32_t FUSED_BIG_MAX_TILE = 1u << 19;
 bool fused_big_prepare(uint32_t gsize);
 int launch_fused_big(const FusedInst &inst, uint32_t gsize, cudaStream_t s, bool coop);
 size_t fused_smem_bytes(uint32_t tile);
+int launch_readback(const unsigned long long *hdr, const uint32_t *pf, const uint32_t *ev, unsigned long long *out_hdr,
+                    uint32_t *out_pf, uint32_t *out_ev, unsigned long long *done_word, unsigned long long seq,
+                    unsigned int *tickets, cudaStream_t s);
 int launch_apply_updates(uint4 *rec, const uint32_t *ids, const uint4 *upd, uint32_t n, uint64_t shard_begin,
                          uint64_t n_local, uint32_t *err, cudaStream_t s);
 

@@ -1368,3 +1368,32 @@ int launch_apply_updates(uint4 *rec, const uint32_t *ids, const uint4 *upd, uint
   return 1;
 }
 }  // namespace ss
+
+namespace ss {
+// Host read-back of a step (scalesim_step_host / scalesim_step_updates): the header and both
+// lists written straight into host-mapped pinned memory, then a completion word (the step's
+// sequence number) the host polls instead of synchronising the stream.  Each CTA fences its
+// writes at system scope before taking a ticket; the last CTA writes the word.
+__global__ void k_readback(const unsigned long long *hdr, const uint32_t *pf, const uint32_t *ev,
+                           unsigned long long *out_hdr, uint32_t *out_pf, uint32_t *out_ev,
+                           volatile unsigned long long *done_word, unsigned long long seq, unsigned int *tickets) {
+  const unsigned long long n_pf = hdr[H_N_PF], n_ev = hdr[H_N_EV];
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, ts = (uint64_t)gridDim.x * blockDim.x;
+  if (t0 < 16) out_hdr[t0] = hdr[t0];
+  for (uint64_t i = t0; i < n_pf; i += ts) out_pf[i] = pf[i];
+  for (uint64_t i = t0; i < n_ev; i += ts) out_ev[i] = ev[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(tickets, 1u) == gridDim.x - 1) {
+    *tickets = 0u;  // (the next launch on this stream starts after this one)
+    __threadfence_system();
+    *done_word = seq;
+  }
+}
+int launch_readback(const unsigned long long *hdr, const uint32_t *pf, const uint32_t *ev, unsigned long long *out_hdr,
+                    uint32_t *out_pf, uint32_t *out_ev, unsigned long long *done_word, unsigned long long seq,
+                    unsigned int *tickets, cudaStream_t s) {
+  k_readback<<<16, 256, 0, s>>>(hdr, pf, ev, out_hdr, out_pf, out_ev, done_word, seq, tickets);
+  return 1;
+}
+}  // namespace ss

@@ -40,6 +40,7 @@ class Planner:
                  exclusive: bool = False, loopback: bool = False, tp_sliced: bool = False, threads: bool = False):
         self.lib = L.lib()
         self._staged_refs = {}  # host arrays of staged steps (scalesim_stage_host)
+        self._pending = []  # host arrays of submitted, uncollected steps (scalesim_submit_updates)
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         lo, hi = shard if shard is not None else (0, n_agents)
@@ -209,6 +210,24 @@ class Planner:
                                             None if ev_out is None else ev_out.ctypes.data)
         self._staged_refs.pop(ids.ctypes.data, None)
         L.check(st, "scalesim_step_updates", allow=(L.OK, L.E_INSUFFICIENT))
+        return h.as_dict()
+
+    def submit_updates(self, now: int, ids: np.ndarray, recs: np.ndarray):
+        """Enqueue an incremental step and return at once (scalesim_submit_updates); its
+        header and lists come back from collect(), oldest first."""
+        assert ids.dtype == np.uint32 and recs.dtype == np.uint32 and recs.shape == (len(ids), 4)
+        L.check(self.lib.scalesim_submit_updates(self.ctx, int(now), ids.ctypes.data, recs.ctypes.data, len(ids)),
+                "scalesim_submit_updates")
+        self._pending.append((ids, recs))
+
+    def collect(self, pf_out: Optional[np.ndarray] = None, ev_out: Optional[np.ndarray] = None):
+        """Header (dict) and lists of the oldest submitted step (scalesim_collect)."""
+        h = L.PlanHost()
+        st = self.lib.scalesim_collect(self.ctx, C.byref(h), None if pf_out is None else pf_out.ctypes.data,
+                                       None if ev_out is None else ev_out.ctypes.data)
+        if self._pending:
+            self._pending.pop(0)
+        L.check(st, "scalesim_collect", allow=(L.OK, L.E_INSUFFICIENT))
         return h.as_dict()
 
     def join(self):

@@ -250,6 +250,63 @@ def test_incremental_host_steps_c4_shape(exclusive):
     pl.close()
 
 
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_submitted_incremental_steps_c4_shape(exclusive):
+    """scalesim_submit_updates / scalesim_collect (two steps in flight: step t+1 plans while the
+    host collects t): every collected plan equals the oracle's on the full records; a third
+    submission and step_host with steps pending are refused; an out-of-shard id is reported by
+    the collect of its own step only."""
+    import torch
+    from paper_2601_21473_b200 import _lib as L
+    from gpu_harness import make_planner
+    w = tg.config_c4(seed=7, steps=7, n=300_000)
+    pl = make_planner(w, transfer=False, keep_dist=False, exclusive=exclusive)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    ids, recs = [None], [None]
+    for s in range(1, w.steps):
+        ch = np.nonzero(np.any(w.rec[s] != w.rec[s - 1], axis=1))[0].astype(np.uint32)
+        ids.append(pin(ch))
+        recs.append(pin(w.rec[s][ch]))
+    pf = np.zeros(w.n, np.uint32)
+    ev = np.zeros(w.n, np.uint32)
+    res = np.zeros(w.n, np.uint8)
+    rec0 = pin(w.rec[0])
+    h = pl.step_host(int(w.now[0]), rec0, None, pf, ev)
+    p = _oracle_step(w, 0, res)
+    _assert_host_plan(h, pf, ev, p, 0)
+    res = p["resident"].astype(np.uint8)
+    pl.submit_updates(int(w.now[1]), ids[1], recs[1])
+    for s in range(1, w.steps):
+        if s + 1 < w.steps:
+            pl.submit_updates(int(w.now[s + 1]), ids[s + 1], recs[s + 1])
+            if s == 1:
+                with pytest.raises(L.ScaleSimError) as e:
+                    pl.submit_updates(int(w.now[s + 1]), ids[s + 1], recs[s + 1])
+                assert e.value.status == L.E_ORDER
+                with pytest.raises(L.ScaleSimError) as e:
+                    pl.step_host(int(w.now[0]), rec0, None, pf, ev)
+                assert e.value.status == L.E_ORDER
+        h = pl.collect(pf, ev)
+        p = _oracle_step(w, s, res)
+        _assert_host_plan(h, pf, ev, p, s)
+        res = p["resident"].astype(np.uint8)
+    with pytest.raises(L.ScaleSimError) as e:
+        pl.collect(pf, ev)
+    assert e.value.status == L.E_ORDER
+    last = w.steps - 1
+    bad = pin(np.array([w.n + 3], np.uint32))
+    pl.submit_updates(int(w.now[last]), bad, pin(w.rec[last][:1]))
+    pl.submit_updates(int(w.now[last]), pin(np.zeros(0, np.uint32)), pin(np.zeros((0, 4), np.uint32)))
+    with pytest.raises(L.ScaleSimError) as e:
+        pl.collect(pf, ev)
+    assert e.value.status == L.E_BAD_INPUT
+    h = pl.collect(pf, ev)  # the next step has no bad id (both plan the last records again)
+    res = _oracle_step(w, last, res)["resident"].astype(np.uint8)
+    p = _oracle_step(w, last, res)
+    _assert_host_plan(h, pf, ev, p, last)
+    pl.close()
+
+
 def test_fused_multi_level_select_and_segments():
     """Distances spread over many values (boundary bucket with several distances: select
     levels 2 and 3; evict segments that need the re-sort by full key), fused vs oracle."""

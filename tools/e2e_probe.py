@@ -32,6 +32,13 @@ def loop(kind):
     pl.step_host(int(w.now[0]), rec0, None, pf, ev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    if kind == "submit":
+        pl.submit_updates(int(w.now[1]), *upd[1])
+        for s in range(1, S):
+            if s + 1 < S:
+                pl.submit_updates(int(w.now[s + 1]), *upd[s + 1])
+            pl.collect(pf, ev)
+        return (time.perf_counter() - t0) / (S - 1) * 1e6
     if kind in ("staged", "staged_nolists"):
         pl.stage_updates(*upd[1])
     for s in range(1, S):
@@ -53,5 +60,5 @@ def loop(kind):
 
 
 for rep in range(2):
-    for kind in ("staged", "staged_nolists", "unstaged", "device_step_sync", "sync_only"):
+    for kind in ("submit", "staged", "staged_nolists", "unstaged", "device_step_sync", "sync_only"):
         print(rep, kind, round(loop(kind), 1), "us/step", flush=True)
