@@ -250,16 +250,18 @@ def test_incremental_host_steps_c4_shape(exclusive):
     pl.close()
 
 
-@pytest.mark.parametrize("exclusive", [False, True])
-def test_submitted_incremental_steps_c4_shape(exclusive):
+@pytest.mark.parametrize("n,exclusive", [(300_000, False), (300_000, True), (1_000_000, True)],
+                         ids=["300k-coop", "300k-excl", "bench-e2e-c4-1M-excl"])
+def test_submitted_incremental_steps_c4_shape(n, exclusive):
     """scalesim_submit_updates / scalesim_collect (two steps in flight: step t+1 plans while the
-    host collects t): every collected plan equals the oracle's on the full records; a third
-    submission and step_host with steps pending are refused; an out-of-shard id is reported by
-    the collect of its own step only."""
+    host collects t; at 1M agents, exclusive, keep_dist off: the bench's e2e configuration):
+    every collected plan equals the oracle's on the full records; a third submission and
+    step_host with steps pending are refused; an out-of-shard id is reported by the collect of
+    its own step only."""
     import torch
     from paper_2601_21473_b200 import _lib as L
     from gpu_harness import make_planner
-    w = tg.config_c4(seed=7, steps=7, n=300_000)
+    w = tg.config_c4(seed=7, steps=7, n=n)
     pl = make_planner(w, transfer=False, keep_dist=False, exclusive=exclusive)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     ids, recs = [None], [None]
