@@ -828,15 +828,15 @@ def main():
         hb = db = 0
         if mode == "full":
             pl.stage_host(rec_host[0])
-        if mode == "submit":  # two steps in flight: step k+1 plans while step k is collected
+        if mode == "submit":  # three steps in flight: steps k+1, k+2 copy and plan while k is collected
             h = pl.step_host(int(w.now[t_base]), rec_host[0], None, pf, ev)
             hb += rec_host[0].nbytes
             db += 128 + 4 * (h["n_prefetch"] + h["n_evict"])
-            if e2e_k > 1:
-                pl.submit_updates(int(w.now[t_base + 1]), *upd[1])
+            for k in range(1, min(3, e2e_k)):
+                pl.submit_updates(int(w.now[t_base + k]), *upd[k])
             for k in range(1, e2e_k):
-                if k + 1 < e2e_k:
-                    pl.submit_updates(int(w.now[t_base + k + 1]), *upd[k + 1])
+                if k + 2 < e2e_k:
+                    pl.submit_updates(int(w.now[t_base + k + 2]), *upd[k + 2])
                 h = pl.collect(pf, ev)
                 hb += upd[k][0].nbytes + upd[k][1].nbytes
                 db += 128 + 4 * (h["n_prefetch"] + h["n_evict"])
@@ -870,7 +870,7 @@ def main():
     e2e = {"value": n * world * e2e_k / el_e, "unit": "agent-plans/s", "h2d_bytes_per_step": h2d_b // e2e_k,
            "d2h_bytes_per_step": d2h_b // e2e_k, "steps": e2e_k,
            "api": "step 0 whole records (scalesim_step_host), then each step's changed records (ids + "
-                  "16-byte records, pinned) by scalesim_submit_updates, two steps in flight, header + "
+                  "16-byte records, pinned) by scalesim_submit_updates, three steps in flight, header + "
                   "lists of every step back through scalesim_collect; host-timed, all copies inside",
            "sync_updates_value": n * world * e2e_k / el_u,
            "sync_updates_api": "scalesim_stage_updates one step ahead + scalesim_step_updates (synchronous)",

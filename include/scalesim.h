@@ -23,8 +23,8 @@
  *     until scalesim_destroy.  The device entry points never allocate memory after init; all
  *     scratch lives in the caller's workspace (size from scalesim_workspace_bytes).  The host
  *     entry points (scalesim_step_host, _stage_host, _stage_updates, _step_updates,
- *     _submit_updates, _collect) allocate, on first use, library-owned staging: two device
- *     input buffers of max(16 (n_local + n_kin), 20 n_local) bytes, two host-mapped pinned
+ *     _submit_updates, _collect) allocate, on first use, library-owned staging: three device
+ *     input buffers of max(16 (n_local + n_kin), 20 n_local) bytes, three host-mapped pinned
  *     read-back slots of 256 + 8 n_local bytes, and one input stream; freed by scalesim_destroy.
  *   - Asynchrony: score/plan/transfer/step enqueue work on the caller's CUDA streams and
  *     return without a host synchronisation (graph-capturable).  Device-detected conditions
@@ -369,9 +369,9 @@ scalesim_status scalesim_step_host(scalesim_ctx *ctx, int64_t now_tick, const ui
  * host_rec, host_kin, ...) with the SAME pointers plans from the staged copy (its plan waits
  * for that copy on the device, not on the host) instead of copying synchronously; the
  * context's own input buffers (init / scalesim_set_inputs) are left untouched.  Usage:
- * stage(in[0]); for t: { stage(in[t+1]); step_host(in[t]); }.  At most two staged steps may
- * be outstanding.  Errors: SCALESIM_E_INVALID (NULL ctx / host_rec, or host_kin NULL with
- * n_kin > 0), SCALESIM_E_ORDER (two staged steps not yet consumed), SCALESIM_E_CUDA. */
+ * stage(in[0]); for t: { stage(in[t+1]); step_host(in[t]); }.  At most three staged steps
+ * may be outstanding.  Errors: SCALESIM_E_INVALID (NULL ctx / host_rec, or host_kin NULL with
+ * n_kin > 0), SCALESIM_E_ORDER (three staged steps not yet consumed), SCALESIM_E_CUDA. */
 scalesim_status scalesim_stage_host(scalesim_ctx *ctx, const uint32_t *host_rec, const float *host_kin);
 
 /* Incremental end-to-end steps.  Agent state changes only where the simulation acted (P:197-205:
@@ -383,13 +383,13 @@ scalesim_status scalesim_stage_host(scalesim_ctx *ctx, const uint32_t *host_rec,
  * scalesim_set_inputs, device, caller-owned: it must hold the previous step's records, e.g.
  * after one scalesim_step_host), then the step runs and its header and lists come back as in
  * scalesim_step_host.  scalesim_stage_updates starts the host->device copy of a LATER step's
- * updates (library-owned staging shared with scalesim_stage_host: at most two staged steps)
+ * updates (library-owned staging shared with scalesim_stage_host: at most three staged steps)
  * and returns at once; scalesim_step_updates with the same (host_ids, host_rec, n_upd) uses
  * that copy (the scatter waits for it on the device), otherwise it copies synchronously.  The
  * scatter runs on the plan stream after the previous step's plan, so staging never races a
  * plan still reading the records.  Contexts with kinematics (n_kin > 0) use
  * scalesim_step_host.  Errors: SCALESIM_E_INVALID (NULL ctx, NULL arrays with n_upd > 0,
- * n_upd > n_local, n_kin > 0), SCALESIM_E_ORDER (two staged steps not yet consumed),
+ * n_upd > n_local, n_kin > 0), SCALESIM_E_ORDER (three staged steps not yet consumed),
  * SCALESIM_E_BAD_INPUT (ids outside the shard: skipped, the step still runs on the others),
  * else as scalesim_step_host. */
 scalesim_status scalesim_stage_updates(scalesim_ctx *ctx, const uint32_t *host_ids, const uint32_t *host_rec,
@@ -403,8 +403,9 @@ scalesim_status scalesim_step_updates(scalesim_ctx *ctx, int64_t now_tick, const
  * into library-owned host-mapped memory) and returns at once; collect waits for the OLDEST
  * submitted step and copies its header and lists out (prefetch_out / evict_out: host,
  * n_local capacity each, may be NULL).  Steps run in submission order on the device; while
- * the host collects step t, step t+1 already plans.  Usage: submit(0); for t: { submit(t+1);
- * collect(t); }.  At most two submitted steps may be uncollected (SCALESIM_E_ORDER), and
+ * the host collects step t, steps t+1 and t+2 already copy and plan.  Usage: submit(0);
+ * submit(1); for t: { submit(t+2); collect(t); }.  At most three submitted steps may be
+ * uncollected (SCALESIM_E_ORDER), and
  * scalesim_step_host / scalesim_step_updates refuse to run (SCALESIM_E_ORDER) until all are
  * collected.  The host arrays must stay unchanged until their step is collected.  Errors of
  * submit: as scalesim_stage_updates; of collect: SCALESIM_E_ORDER (nothing submitted),

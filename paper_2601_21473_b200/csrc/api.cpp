@@ -330,6 +330,9 @@ static ExclusiveChain g_excl[64];
 
 using namespace ss;
 
+// staging / read-back slots of the host entry points: host steps in flight
+constexpr int NSLOT = 3;
+
 struct scalesim_ctx {
   scalesim_config cfg;
   scalesim_tables tab;
@@ -365,19 +368,19 @@ struct scalesim_ctx {
   // pipelined host inputs (scalesim_stage_host): two library-owned device buffers, each the
   // records (16 n_local B) followed by the kinematics (16 n_kin B), filled on in_stream
   cudaStream_t in_stream = nullptr;
-  uint8_t *sbuf[2] = {nullptr, nullptr};
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
-  const void *staged_rec[2] = {nullptr, nullptr}, *staged_kin[2] = {nullptr, nullptr};
-  bool staged[2] = {false, false}, sbuf_used[2] = {false, false};
-  bool staged_upd[2] = {false, false};  // the slot holds (ids, records) updates, not whole inputs
-  uint32_t staged_n[2] = {0, 0};
+  uint8_t *sbuf[NSLOT] = {};
+  cudaEvent_t ev_in[NSLOT] = {}, ev_used[NSLOT] = {};
+  const void *staged_rec[NSLOT] = {}, *staged_kin[NSLOT] = {};
+  bool staged[NSLOT] = {}, sbuf_used[NSLOT] = {};
+  bool staged_upd[NSLOT] = {};  // the slot holds (ids, records) updates, not whole inputs
+  uint32_t staged_n[NSLOT] = {};
   int stage_next = 0;
   uint32_t *upd_err_h = nullptr, *upd_err_d = nullptr;  // host-mapped count of out-of-shard ids
   // host read-back (read_back): host-mapped pinned [done word | header | prefetch | evict]
   uint8_t *rb_h = nullptr, *rb_d = nullptr;
   unsigned int *rb_tickets = nullptr;
   unsigned long long rb_seq = 0;          // read-backs enqueued (slot = seq % 2)
-  unsigned long long rb_pending[2] = {0, 0};  // submitted steps not yet collected, oldest first
+  unsigned long long rb_pending[NSLOT] = {};  // submitted steps not yet collected, oldest first
   int n_pending = 0;
 };
 
@@ -1184,23 +1187,24 @@ extern "C" scalesim_status scalesim_sync(scalesim_ctx *c, scalesim_plan_host *ou
 // slot's completion word, which the host polls (one kernel instead of three copies and two
 // stream synchronisations); the stream is queried now and then so that a failed launch returns
 // instead of spinning.
-static size_t rb_slot_bytes(const scalesim_ctx *c) { return 256 + 8 * (size_t)c->p.n_local; }
+static size_t rb_list_bytes(const scalesim_ctx *c) { return ((size_t)4 * c->p.n_local + 15) / 16 * 16; }
+static size_t rb_slot_bytes(const scalesim_ctx *c) { return 256 + 2 * rb_list_bytes(c); }
 
 static scalesim_status enqueue_readback(scalesim_ctx *c, unsigned long long *seq_out) {
   if (!c->rb_h) {
-    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->rb_h), 2 * rb_slot_bytes(c), cudaHostAllocMapped));
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->rb_h), NSLOT * rb_slot_bytes(c), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->rb_d), c->rb_h, 0));
     CK(cudaMalloc(&c->rb_tickets, 16));
     CK(cudaMemset(c->rb_tickets, 0, 16));
-    for (int k = 0; k < 2; ++k) *reinterpret_cast<volatile unsigned long long *>(c->rb_h + k * rb_slot_bytes(c)) = 0ull;
+    for (int k = 0; k < NSLOT; ++k) *reinterpret_cast<volatile unsigned long long *>(c->rb_h + k * rb_slot_bytes(c)) = 0ull;
   }
   const unsigned long long seq = ++c->rb_seq;
-  uint8_t *d = c->rb_d + (seq & 1) * rb_slot_bytes(c);
+  uint8_t *d = c->rb_d + (seq % NSLOT) * rb_slot_bytes(c);
   auto *wd = reinterpret_cast<unsigned long long *>(d);
   c->launches += launch_readback(reinterpret_cast<const unsigned long long *>(c->p.d.header), c->p.d.pf_ids,
                                  c->p.d.ev_ids, wd + 16, reinterpret_cast<uint32_t *>(d + 256),
-                                 reinterpret_cast<uint32_t *>(d + 256 + 4 * c->p.n_local), wd, seq,
-                                 c->rb_tickets + (seq & 1), c->stream);
+                                 reinterpret_cast<uint32_t *>(d + 256 + rb_list_bytes(c)), wd, seq,
+                                 c->rb_tickets + (seq % NSLOT), c->stream);
   CK(cudaGetLastError());
   *seq_out = seq;
   return SCALESIM_OK;
@@ -1208,7 +1212,7 @@ static scalesim_status enqueue_readback(scalesim_ctx *c, unsigned long long *seq
 
 static scalesim_status wait_readback(scalesim_ctx *c, unsigned long long seq, scalesim_plan_host *out,
                                      uint32_t *pf_out, uint32_t *ev_out) {
-  const uint8_t *hb = c->rb_h + (seq & 1) * rb_slot_bytes(c);
+  const uint8_t *hb = c->rb_h + (seq % NSLOT) * rb_slot_bytes(c);
   volatile const unsigned long long *word = reinterpret_cast<volatile const unsigned long long *>(hb);
   for (uint64_t spin = 1; *word != seq; ++spin) {
     if ((spin & 1023) == 0) {
@@ -1220,7 +1224,7 @@ static scalesim_status wait_readback(scalesim_ctx *c, unsigned long long seq, sc
   scalesim_plan_host h;
   memcpy(h.f, hb + 128, sizeof(h.f));
   if (pf_out && h.f[SCALESIM_H_N_PREFETCH]) memcpy(pf_out, hb + 256, 4 * h.f[SCALESIM_H_N_PREFETCH]);
-  if (ev_out && h.f[SCALESIM_H_N_EVICT]) memcpy(ev_out, hb + 256 + 4 * c->p.n_local, 4 * h.f[SCALESIM_H_N_EVICT]);
+  if (ev_out && h.f[SCALESIM_H_N_EVICT]) memcpy(ev_out, hb + 256 + rb_list_bytes(c), 4 * h.f[SCALESIM_H_N_EVICT]);
   if (c->transfer) CK(cudaStreamSynchronize(c->copy_stream));
   if (out) *out = h;
   return status_of_header(h.f[SCALESIM_H_STATUS]);
@@ -1241,7 +1245,7 @@ extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, cons
   if (c->p.n_kin > 0 && !host_kin) return SCALESIM_E_INVALID;
   if (c->n_pending) return SCALESIM_E_ORDER;  // submitted steps not collected
   int si = -1;  // inputs staged by scalesim_stage_host (their copy may still be in flight)
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < NSLOT; ++i)
     if (c->staged[i] && !c->staged_upd[i] && c->staged_rec[i] == host_rec &&
         (c->p.n_kin == 0 || c->staged_kin[i] == host_kin))
       si = i;
@@ -1273,7 +1277,7 @@ extern "C" scalesim_status scalesim_step_host(scalesim_ctx *c, int64_t now, cons
 static int stage_slot(scalesim_ctx *c, scalesim_status *err) {
   *err = SCALESIM_OK;
   int i = c->stage_next;
-  if (c->staged[i]) i ^= 1;
+  for (int k = 0; k < NSLOT && c->staged[i]; ++k) i = (i + 1) % NSLOT;
   if (c->staged[i]) {
     *err = SCALESIM_E_ORDER;  // two staged steps not yet run
     return -1;
@@ -1281,7 +1285,7 @@ static int stage_slot(scalesim_ctx *c, scalesim_status *err) {
   auto fail = [&](cudaError_t e) { return e != cudaSuccess ? (*err = SCALESIM_E_CUDA, true) : false; };
   if (!c->in_stream) {
     if (fail(cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking))) return -1;
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < NSLOT; ++k)
       if (fail(cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming)) ||
           fail(cudaEventCreateWithFlags(&c->ev_used[k], cudaEventDisableTiming)))
         return -1;
@@ -1299,7 +1303,7 @@ static void stage_commit(scalesim_ctx *c, int i, const void *key0, const void *k
   c->staged_rec[i] = key0;
   c->staged_kin[i] = key1;
   c->staged_n[i] = n;
-  c->stage_next = i ^ 1;
+  c->stage_next = (i + 1) % NSLOT;
 }
 
 extern "C" scalesim_status scalesim_stage_host(scalesim_ctx *c, const uint32_t *host_rec, const float *host_kin) {
@@ -1344,14 +1348,14 @@ static scalesim_status enqueue_updates_step(scalesim_ctx *c, int64_t now, const 
   if (!c || (n_upd > 0 && (!host_ids || !host_rec)) || n_upd > c->p.n_local || c->p.n_kin > 0)
     return SCALESIM_E_INVALID;
   int si = -1;
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < NSLOT; ++i)
     if (c->staged[i] && c->staged_upd[i] && c->staged_rec[i] == host_ids && c->staged_kin[i] == host_rec &&
         c->staged_n[i] == n_upd)
       si = i;
   scalesim_status s;
   if (si < 0) {  // not staged: the copy goes out now
     if ((s = scalesim_stage_updates(c, host_ids, host_rec, n_upd)) != SCALESIM_OK) return s;
-    si = c->stage_next ^ 1;
+    si = (c->stage_next + NSLOT - 1) % NSLOT;
   }
   if (!c->upd_err_h) {
     CK(cudaHostAlloc(reinterpret_cast<void **>(&c->upd_err_h), 16, cudaHostAllocMapped));
@@ -1376,7 +1380,7 @@ extern "C" scalesim_status scalesim_step_updates(scalesim_ctx *c, int64_t now, c
                                                  uint32_t *pf_out, uint32_t *ev_out) {
   if (!c) return SCALESIM_E_INVALID;
   if (c->n_pending) return SCALESIM_E_ORDER;
-  const int slot = (int)((c->rb_seq + 1) & 1);
+  const int slot = (int)((c->rb_seq + 1) % NSLOT);
   scalesim_status s = enqueue_updates_step(c, now, host_ids, host_rec, n_upd, slot);
   if (s != SCALESIM_OK) return s;
   s = read_back(c, out, pf_out, ev_out);
@@ -1387,8 +1391,8 @@ extern "C" scalesim_status scalesim_step_updates(scalesim_ctx *c, int64_t now, c
 extern "C" scalesim_status scalesim_submit_updates(scalesim_ctx *c, int64_t now, const uint32_t *host_ids,
                                                    const uint32_t *host_rec, uint32_t n_upd) {
   if (!c) return SCALESIM_E_INVALID;
-  if (c->n_pending >= 2) return SCALESIM_E_ORDER;  // both read-back slots hold uncollected steps
-  const int slot = (int)((c->rb_seq + 1) & 1);
+  if (c->n_pending >= NSLOT) return SCALESIM_E_ORDER;  // every read-back slot holds an uncollected step
+  const int slot = (int)((c->rb_seq + 1) % NSLOT);
   scalesim_status s = enqueue_updates_step(c, now, host_ids, host_rec, n_upd, slot);
   if (s != SCALESIM_OK) return s;
   unsigned long long seq;
@@ -1402,10 +1406,10 @@ extern "C" scalesim_status scalesim_collect(scalesim_ctx *c, scalesim_plan_host 
   if (!c) return SCALESIM_E_INVALID;
   if (c->n_pending == 0) return SCALESIM_E_ORDER;
   const unsigned long long seq = c->rb_pending[0];
-  c->rb_pending[0] = c->rb_pending[1];
+  for (int k = 1; k < NSLOT; ++k) c->rb_pending[k - 1] = c->rb_pending[k];
   c->n_pending--;
   scalesim_status s = wait_readback(c, seq, out, pf_out, ev_out);
-  if (s == SCALESIM_OK && reinterpret_cast<volatile uint32_t *>(c->upd_err_h)[seq & 1]) return SCALESIM_E_BAD_INPUT;
+  if (s == SCALESIM_OK && reinterpret_cast<volatile uint32_t *>(c->upd_err_h)[seq % NSLOT]) return SCALESIM_E_BAD_INPUT;
   return s;
 }
 
@@ -1415,12 +1419,12 @@ extern "C" void scalesim_destroy(scalesim_ctx *c) {
     cudaStreamSynchronize(c->in_stream);
     cudaStreamDestroy(c->in_stream);
   }
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < NSLOT; ++k) {
     if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
     if (c->ev_used[k]) cudaEventDestroy(c->ev_used[k]);
   }
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < NSLOT; ++k)
     if (c->sbuf[k]) cudaFree(c->sbuf[k]);
   if (c->upd_err_h) cudaFreeHost(c->upd_err_h);
   if (c->rb_h) cudaFreeHost(c->rb_h);

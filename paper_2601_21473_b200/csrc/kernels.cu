@@ -1380,8 +1380,15 @@ __global__ void k_readback(const unsigned long long *hdr, const uint32_t *pf, co
   const unsigned long long n_pf = hdr[H_N_PF], n_ev = hdr[H_N_EV];
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, ts = (uint64_t)gridDim.x * blockDim.x;
   if (t0 < 16) out_hdr[t0] = hdr[t0];
-  for (uint64_t i = t0; i < n_pf; i += ts) out_pf[i] = pf[i];
-  for (uint64_t i = t0; i < n_ev; i += ts) out_ev[i] = ev[i];
+  // 16-byte stores (a warp writes 512 contiguous bytes of host memory): 4-byte stores over the
+  // host link cost ~4x (measured: 15.8 us for C4's ~60 KB of lists, r02_v77)
+  auto copy = [&](const uint32_t *src, uint32_t *dst, unsigned long long n) {
+    const uint64_t n4 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) ? 0 : n / 4;
+    for (uint64_t i = t0; i < n4; i += ts) reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+    for (uint64_t i = 4 * n4 + t0; i < n; i += ts) dst[i] = src[i];
+  };
+  copy(pf, out_pf, n_pf);
+  copy(ev, out_ev, n_ev);
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(tickets, 1u) == gridDim.x - 1) {
@@ -1393,7 +1400,7 @@ __global__ void k_readback(const unsigned long long *hdr, const uint32_t *pf, co
 int launch_readback(const unsigned long long *hdr, const uint32_t *pf, const uint32_t *ev, unsigned long long *out_hdr,
                     uint32_t *out_pf, uint32_t *out_ev, unsigned long long *done_word, unsigned long long seq,
                     unsigned int *tickets, cudaStream_t s) {
-  k_readback<<<16, 256, 0, s>>>(hdr, pf, ev, out_hdr, out_pf, out_ev, done_word, seq, tickets);
+  k_readback<<<32, 256, 0, s>>>(hdr, pf, ev, out_hdr, out_pf, out_ev, done_word, seq, tickets);
   return 1;
 }
 }  // namespace ss

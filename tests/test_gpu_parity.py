@@ -164,9 +164,9 @@ def test_call_order_and_host_step():
 
 @pytest.mark.parametrize("exclusive", [False, True])
 def test_pipelined_host_steps_c4_shape(exclusive):
-    """scalesim_stage_host + scalesim_step_host back to back (the bench's e2e loop: step t+1's
-    records cross the link while step t plans, keep_dist=False as benched): every step's header
-    and lists equal the oracle's; the staged buffers alternate, a third stage is refused."""
+    """scalesim_stage_host + scalesim_step_host back to back (step t+1's records cross the link
+    while step t plans, keep_dist=False as benched): every step's header and lists equal the
+    oracle's; the staged buffers rotate, a fourth outstanding stage is refused."""
     import torch
     from paper_2601_21473_b200 import _lib as L
     from gpu_harness import make_planner
@@ -178,11 +178,12 @@ def test_pipelined_host_steps_c4_shape(exclusive):
     res = np.zeros(w.n, np.uint8)
     pl.stage_host(recs[0])
     for s in range(w.steps):
-        if s + 1 < w.steps:
+        if s + 1 < w.steps and s != 1:  # (recs[2] was staged at s == 0)
             pl.stage_host(recs[s + 1])
-            if s == 0:
+            if s == 0:  # three staged steps at most
+                pl.stage_host(recs[2])
                 with pytest.raises(L.ScaleSimError) as e:
-                    pl.stage_host(recs[2])
+                    pl.stage_host(recs[3])
                 assert e.value.status == L.E_ORDER
         h = pl.step_host(int(w.now[s]), recs[s], None, pf, ev)
         d_or, _ = oracle.score(w.rec[s], None, int(w.now[s]), w.hop_scale)
@@ -253,8 +254,8 @@ def test_incremental_host_steps_c4_shape(exclusive):
 @pytest.mark.parametrize("n,exclusive", [(300_000, False), (300_000, True), (1_000_000, True)],
                          ids=["300k-coop", "300k-excl", "bench-e2e-c4-1M-excl"])
 def test_submitted_incremental_steps_c4_shape(n, exclusive):
-    """scalesim_submit_updates / scalesim_collect (two steps in flight: step t+1 plans while the
-    host collects t; at 1M agents, exclusive, keep_dist off: the bench's e2e configuration):
+    """scalesim_submit_updates / scalesim_collect (three steps in flight: steps t+1, t+2 copy and
+    plan while the host collects t; at 1M agents, exclusive, keep_dist off: the bench's e2e configuration):
     every collected plan equals the oracle's on the full records; a third submission and
     step_host with steps pending are refused; an out-of-shard id is reported by the collect of
     its own step only."""
@@ -278,12 +279,13 @@ def test_submitted_incremental_steps_c4_shape(n, exclusive):
     _assert_host_plan(h, pf, ev, p, 0)
     res = p["resident"].astype(np.uint8)
     pl.submit_updates(int(w.now[1]), ids[1], recs[1])
+    pl.submit_updates(int(w.now[2]), ids[2], recs[2])
     for s in range(1, w.steps):
-        if s + 1 < w.steps:
-            pl.submit_updates(int(w.now[s + 1]), ids[s + 1], recs[s + 1])
-            if s == 1:
+        if s + 2 < w.steps:
+            pl.submit_updates(int(w.now[s + 2]), ids[s + 2], recs[s + 2])
+            if s == 1:  # three steps in flight at most
                 with pytest.raises(L.ScaleSimError) as e:
-                    pl.submit_updates(int(w.now[s + 1]), ids[s + 1], recs[s + 1])
+                    pl.submit_updates(int(w.now[s + 3]), ids[s + 3], recs[s + 3])
                 assert e.value.status == L.E_ORDER
                 with pytest.raises(L.ScaleSimError) as e:
                     pl.step_host(int(w.now[0]), rec0, None, pf, ev)
