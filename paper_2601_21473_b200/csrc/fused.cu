@@ -593,10 +593,24 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   // the owners' range totals and this CTA's first list-bucket offsets: loads issued now (their
   // latency hides behind P3 / P4), the epoch tag checked where they are used
   unsigned long long rv_pre = 0, pv_pre = 0;
+  // ... and the list starts CTA 0 (bucket b*) and the last CTA (the multi-valued buckets) need:
+  // threads 0 / 1 of CTA 0 and 32 / 33 of the last CTA, one entry each (sp_b / sp_q: its bucket
+  // and CTA column)
+  unsigned long long sp_pre = 0;
+  uint32_t sp_b = NB1, sp_q = 0;
   if (fastp && G > 1) {
     if (threadIdx.x < m_need)
       pv_pre = ld_relaxed_u64(d.f_pos + ((uint64_t)par * NB1 + need[threadIdx.x]) * FUSED_MAX_CTAS + c);
     if (threadIdx.x < G) rv_pre = ld_relaxed_u64(&d.f_rt[par * FUSED_MAX_CTAS + threadIdx.x]);
+    if (c == 0 && threadIdx.x < 2 && bs < (uint32_t)NB1) {
+      sp_b = bs;
+      sp_q = threadIdx.x == 0 ? 0u : G - 1;
+    }
+    if (c == G - 1 && (threadIdx.x == 32 || threadIdx.x == 33)) {
+      sp_b = threadIdx.x == 32 ? IB_EXACT : IB_INF - 1;
+      sp_q = threadIdx.x == 32 ? 0u : G - 1;
+    }
+    if (sp_b < (uint32_t)NB1) sp_pre = ld_relaxed_u64(&d.f_pos[((uint64_t)par * NB1 + sp_b) * FUSED_MAX_CTAS + sp_q]);
   }
 
   // ---------------- fast list placement tail (integer distances, fastp: grid-uniform)
@@ -684,17 +698,54 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     warp_add_u44(tie_kept, sacc + 8);
     n_el = __reduce_add_sync(0xFFFFFFFFu, n_el);
     if (lane == 0 && n_el) atomicAdd(&sacc[10], n_el);
-    // one scan for two things: [0] this tile's list members per word (prefetch | evict << 32),
-    // [1] the range starts from the owners' range totals (G > 1) or, one CTA, its own counts
-    unsigned long long sv[2], s2[2];
-    sv[0] = (unsigned long long)__popc(pfw) | ((unsigned long long)__popc(evw) << 32);
-    uint32_t re = 0, tv[4];
+    STAMP_MAX(50)
+    // one scan for two things: [0] this tile's list members per word (prefetch | evict << 16 /
+    // << 32), [1] the range starts from the owners' range totals (G > 1) or, one CTA, its own
+    // counts.  G > 1: every nonzero value sits in the first max(tw, G) threads, and every sum fits
+    // 32 bits (members of a tile < 2^16 per list, list lengths < 2^24), so only those warps scan,
+    // in 32-bit parts, behind one barrier (measured: the generic two-level u64 scan took ~1 us)
+    uint32_t vp, ve, tp, te, rs_pf = 0, rs_ev = 0, r_tot = 0, rp_tot = 0, re = 0, tv[4];
+    unsigned long long s2_1 = 0, sv_1 = 0;  // (G == 1)
     if (G > 1) {
       unsigned long long rv = rv_pre;
       if (threadIdx.x < G && (uint32_t)(rv >> 48) != ep) rv = poll_ep(&d.f_rt[par * FUSED_MAX_CTAS + threadIdx.x], ep, d.header);
-      re = (uint32_t)rv & 0xFFFFFFu;
-      sv[1] = ((rv >> 24) & 0xFFFFFFull) | ((unsigned long long)re << 32);
+      re = threadIdx.x < G ? (uint32_t)rv & 0xFFFFFFu : 0u;
+      const uint32_t a0 = (uint32_t)__popc(pfw) | ((uint32_t)__popc(evw) << 16);
+      const uint32_t b0 = threadIdx.x < G ? (uint32_t)(rv >> 24) & 0xFFFFFFu : 0u;
+      __shared__ uint32_t sh3[3][FWARPS];
+      const uint32_t nsw = ((A.tw > G ? A.tw : G) + 31) / 32;  // (CTA-uniform)
+      uint32_t ia = 0, ib = 0, ic = 0;
+      if (warp < nsw) {
+        ia = warp_incl_scan(a0);
+        ib = warp_incl_scan(b0);
+        ic = warp_incl_scan(re);
+        if (lane == 31) {
+          sh3[0][warp] = ia;
+          sh3[1][warp] = ib;
+          sh3[2][warp] = ic;
+        }
+      }
+      __syncthreads();
+      const uint32_t x0 = lane < nsw ? sh3[0][lane] : 0u, x2 = lane < nsw ? sh3[2][lane] : 0u;
+      const uint32_t x1 = lane < nsw ? sh3[1][lane] : 0u;
+      const uint32_t t0 = __reduce_add_sync(0xFFFFFFFFu, x0);
+      r_tot = __reduce_add_sync(0xFFFFFFFFu, x2);
+      rp_tot = __reduce_add_sync(0xFFFFFFFFu, x1);
+      tp = t0 & 0xFFFFu;
+      te = t0 >> 16;
+      if (warp < nsw) {
+        const uint32_t lt = (uint32_t)lane < (uint32_t)warp;
+        const uint32_t e0 = __reduce_add_sync(0xFFFFFFFFu, lt ? x0 : 0u) + ia - a0;
+        vp = e0 & 0xFFFFu;
+        ve = e0 >> 16;
+        rs_pf = __reduce_add_sync(0xFFFFFFFFu, lt ? x1 : 0u) + ib - b0;
+        rs_ev = __reduce_add_sync(0xFFFFFFFFu, lt ? x2 : 0u) + ic - re;
+      } else {
+        vp = ve = 0;
+      }
     } else {
+      unsigned long long sv[2], s2[2];
+      sv[0] = (unsigned long long)__popc(pfw) | ((unsigned long long)__popc(evw) << 32);
       unsigned long long loc = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -702,12 +753,17 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         loc += (unsigned long long)(tv[k] & 0xFFFFu) | ((unsigned long long)(tv[k] >> 16) << 32);
       }
       sv[1] = loc;
+      cta_scan2(sv, s2);
+      vp = (uint32_t)sv[0];
+      ve = (uint32_t)(sv[0] >> 32);
+      tp = (uint32_t)s2[0];
+      te = (uint32_t)(s2[0] >> 32);
+      sv_1 = sv[1];
+      s2_1 = s2[1];
+      r_tot = (uint32_t)(s2_1 >> 32);
     }
-    cta_scan2(sv, s2);
-    const uint32_t tp = (uint32_t)s2[0], te = (uint32_t)(s2[0] >> 32);  // this tile's members per list
     {  // this tile's members in list order (prefetch ascending id, evict descending id)
       const uint32_t w = threadIdx.x;
-      const uint32_t vp = (uint32_t)sv[0], ve = (uint32_t)(sv[0] >> 32);
       uint32_t m = pfw, o = vp;
       while (m) {  // (bucket << 16 | local index: tile < 2^16)
         const uint32_t k = w * 32 + __ffs(m) - 1;
@@ -724,12 +780,12 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
     }
     if (G > 1) {
       uint32_t *rps = s.col, *rpe = s.col + G;  // range starts (the owner staging is free)
-      const uint32_t r_tot = (uint32_t)(s2[1] >> 32);
       if (threadIdx.x < G) {
-        rps[threadIdx.x] = (uint32_t)sv[1];
-        rpe[threadIdx.x] = r_tot - (uint32_t)(sv[1] >> 32) - re;
+        rps[threadIdx.x] = rs_pf;
+        rpe[threadIdx.x] = r_tot - rs_ev - re;
       }
       __syncthreads();
+      STAMP_MAX(53)
       // positions of this CTA's first member in each of its list buckets
       const unsigned long long *Pc = d.f_pos + (uint64_t)par * NB1 * FUSED_MAX_CTAS + c;
       for (uint32_t j = threadIdx.x; j < m_need; j += FT) {
@@ -739,26 +795,25 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         h32[b] = rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
         h32[NB1 + b] = rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
       }
-      auto pos_pf = [&](uint32_t b) {  // sum_{b' < b} NR[b']
-        const unsigned long long v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS], ep, d.header);
-        return rps[b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu);
+      // the prefetched entry (sp_pre) of bucket sp_b, CTA column sp_q (0: the prefetch start,
+      // sum_{b' < b} NR[b']; G - 1: the evict start, sum_{b' > b} R[b']), polled if not yet current
+      auto sp_pos = [&]() {
+        unsigned long long v = sp_pre;
+        if ((uint32_t)(v >> 48) != ep) v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + sp_b) * FUSED_MAX_CTAS + sp_q], ep, d.header);
+        return sp_q == 0 ? rps[sp_b / RB] + ((uint32_t)(v >> 24) & 0xFFFFFFu) : rpe[sp_b / RB] + ((uint32_t)v & 0xFFFFFFu);
       };
-      auto pos_ev = [&](uint32_t b) {  // sum_{b' > b} R[b']
-        const unsigned long long v = poll_ep(&d.f_pos[((uint64_t)par * NB1 + b) * FUSED_MAX_CTAS + G - 1], ep, d.header);
-        return rpe[b / RB] + ((uint32_t)v & 0xFFFFFFu);
-      };
-      if (c == 0 && threadIdx.x == 0) {
-        sh_spf = bs < (uint32_t)NB1 ? pos_pf(bs) : (uint32_t)s2[1];
-        sh_sev = bs < (uint32_t)NB1 ? pos_ev(bs) : 0u;
+      if (c == 0 && threadIdx.x < 2) {
+        if (threadIdx.x == 0) sh_spf = bs < (uint32_t)NB1 ? sp_pos() : rp_tot;
+        else sh_sev = bs < (uint32_t)NB1 ? sp_pos() : 0u;
       }
-      if (c == G - 1 && threadIdx.x == 32) {
-        sh_mvpf = pos_pf(IB_EXACT);
-        sh_mvev = pos_ev(IB_INF - 1);
+      if (c == G - 1 && (threadIdx.x == 32 || threadIdx.x == 33)) {
+        if (threadIdx.x == 32) sh_mvpf = sp_pos();
+        else sh_mvev = sp_pos();
       }
+      STAMP_MAX(54)
     } else {
       // one CTA: its counts are the totals (S_pf(b) = sum_{b' < b} NR, S_ev(b) = sum_{b' > b} R)
-      const uint32_t r_tot = (uint32_t)(s2[1] >> 32);
-      unsigned long long run = sv[1];
+      unsigned long long run = sv_1;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t b = 4 * threadIdx.x + k;
@@ -774,7 +829,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         if (b == IB_INF - 1) sh_mvev = sev;
       }
       if (bs == (uint32_t)NB1 && threadIdx.x == 0) {
-        sh_spf = (uint32_t)s2[1];
+        sh_spf = (uint32_t)s2_1;
         sh_sev = 0;
       }
     }

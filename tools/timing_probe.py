@@ -59,7 +59,7 @@ for mode in ("eager", "graph", "eager_sync"):
                       "P5tab", r(7), "| max over CTAs: P1end", r(11), "P3end", r(14), "P4loop", r(27), "P4lists", r(17), "P4ranks", r(19), "P4rows", r(28),
                       "P4end", r(12), "B4max", r(30), "P5tot", r(31), "P5tables", r(13), "end", r(1), "| slots", int(st[16]), "max_sorted_seg", int(st[18]),
                       "slot_loop_ns_max", int(st[21]), "sections(seg+col, gather, scan, place) ns max", [int(st[q]) for q in (22, 23, 24, 29)],
-                      "| fast: owner landed", r(40), "o.pass1", r(46), "o.scan", r(47), "owner done", r(41), "need", r(42), "positions", r(17), "members", r(38), "pf placed", r(43), "ev placed", r(44), "placed", r(39), "paths", (int(st[48]), int(st[49])), "| P1loop", r(25), "P1pub", r(26), "| last CTA start", r(15), "| cta0 select: cleared", r(32), "coarse", r(33), "fine", r(34), "barrier", r(35))
+                      "| fast: owner landed", r(40), "o.pass1", r(46), "o.scan", r(47), "owner done", r(41), "need", r(42), "positions", r(17), "members", r(38), "pf placed", r(43), "ev placed", r(44), "placed", r(39), "paths", (int(st[48]), int(st[49])), "| P1loop", r(25), "P1pub", r(26), "| last CTA start", r(15), "| cta0 select: cleared", r(32), "coarse", r(33), "fine", r(34), "barrier", r(35), "| members sub: sums", r(50), "pre-scan", r(51), "scan", r(52), "lists+sync", r(53), "positions", r(54))
         print("eager_sync per-step ms", np.round(ts, 4))
         t0.record(pl.stream); t1.record(pl.stream)
     torch.cuda.synchronize()
