@@ -386,6 +386,22 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
   STAMP0(3)
   wgrid.sync();  // (the world's CTAs: every instance's own when nw == 1)
   STAMP0(4)
+  // CTA 0's header inputs of the fast tail (the status bits, the plan sequence number, the
+  // world's zero-distance bytes), all final now: copied into shared memory asynchronously, so
+  // that the kernel does not end on a chain of dependent global loads
+  // (16-byte pairs through L2 (cp.async.cg): acc[4..5], header[12..13], each rank's acc[0..1])
+  __shared__ __align__(16) unsigned long long s_tail[4 + 2 * FUSED_MAX_WORLD];
+  __shared__ uint32_t s_st0;
+  if (c == 0 && threadIdx.x == 0) {
+    cp_async16(&s_tail[0], &acc[4]);
+    cp_async16(&s_tail[2], &d.header[H_SEQ - 1]);
+    for (uint32_t r = 0; r < nw; ++r) cp_async16(&s_tail[4 + 2 * r], &W.acc[r][8 * par]);
+    // (written by an earlier kernel: no stale L1 copy)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_st0)),
+                 "l"(&d.state->status)
+                 : "memory");
+    cp_async_commit();
+  }
 
   // ---------------- P2: select
   {  // clear the other parity's accumulators for the next launch, spread over the CTAs
@@ -638,12 +654,23 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
       }
       __syncthreads();
       if (warp * 32 < c || (warp == FWARPS - 1 && rank > 0)) warp_add_u64(t_rows, sacc + 20);  // preceding CTAs' and ranks' total
-      {
-        const uint32_t w = threadIdx.x;
-        unsigned long long v[1] = {w < A.tw ? word_tie[w] : 0ull}, tt[1];
-        cta_scan1(v, tt);  // (its barriers complete the sum)
-        if (w < A.tw) word_tie[w] = v[0];
-        if (threadIdx.x == 0) word_tie[A.tw] = tt[0];  // (memb holds tile / 2 >= tw + 1 words of 64 bits)
+      {  // exclusive scan of the words' tie bytes on the first ceil(tw / 32) warps, one barrier
+         // (which also completes the sum above)
+        const uint32_t w = threadIdx.x, nsw = (A.tw + 31) / 32;
+        __shared__ unsigned long long sh_wt[FWARPS];
+        const unsigned long long v = w < A.tw ? word_tie[w] : 0ull;
+        unsigned long long incl = 0;
+        if ((uint32_t)warp < nsw) {
+          incl = warp_incl_scan(v);
+          if (lane == 31) sh_wt[warp] = incl;
+        }
+        __syncthreads();
+        if ((uint32_t)warp < nsw) {
+          unsigned long long pre = 0;
+          for (int k = 0; k < warp; ++k) pre += sh_wt[k];
+          if (w < A.tw) word_tie[w] = pre + incl - v;
+          if ((uint32_t)warp == nsw - 1 && lane == 31) word_tie[A.tw] = pre + incl;  // (memb: tile / 2 >= tw + 1 u64)
+        }
       }
       sh_tie_excl = parts_u64(sacc + 20);
       __syncthreads();
@@ -933,15 +960,15 @@ __global__ void __launch_bounds__(FT, 1) k_fused_plan(const __grid_constant__ Fu
         if (sh_spf) atomicAdd(&H[H_N_PF], (unsigned long long)sh_spf);
         if (sh_sev) atomicAdd(&H[H_N_EV], (unsigned long long)sh_sev);
         atomicAdd(&H[H_KEPT], p.budget - sel.rem);
-        const uint32_t st0 = d.state->status;
-        uint32_t status = (uint32_t)acc[5] | st0;
+        cp_async_wait_all();  // (s_tail, s_st0: this thread's copies)
+        uint32_t status = (uint32_t)s_tail[1] | s_st0;
         unsigned long long zb = 0;  // bytes of the world's distance-0 agents
-        for (uint32_t r = 0; r < nw; ++r) zb += W.acc[r][8 * par];
+        for (uint32_t r = 0; r < nw; ++r) zb += s_tail[4 + 2 * r];
         if (zb > p.budget) status |= ST_INSUFFICIENT;
         H[H_CUT_BITS] = all_fit ? 0xFFFFFFFFull : dstar;
         H[H_CUT_REM] = sel.rem;
         atomicOr(reinterpret_cast<unsigned int *>(&H[H_STATUS]), status);
-        H[H_SEQ] = H[H_SEQ] + 1;
+        H[H_SEQ] = s_tail[3] + 1;
       }
     }
       STAMP_MAX(1)
