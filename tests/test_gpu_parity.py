@@ -197,6 +197,33 @@ def test_pipelined_host_steps_c4_shape(exclusive):
     pl.close()
 
 
+def test_pipelined_host_steps_with_kinematics():
+    """scalesim_stage_host with kinematics (C3-mini: interaction agents, n_kin > 0): the staged
+    records AND kinematics reach the plan of their own step (the pair scan reads the staged
+    kinematics), every step's header and lists equal the oracle's."""
+    import torch
+    from gpu_harness import make_planner
+    w = tg.config_c3(seed=2, steps=5, n=9001, budget=int(9001 * 3.41e6 * 0.235), host_bytes=4 << 30)
+    assert w.n_kin > 0
+    pl = make_planner(w, transfer=False)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    recs = [pin(w.rec[s]) for s in range(w.steps)]
+    kins = [pin(w.kin[s]) for s in range(w.steps)]
+    pf = np.zeros(w.n, np.uint32)
+    ev = np.zeros(w.n, np.uint32)
+    res = np.zeros(w.n, np.uint8)
+    pl.stage_host(recs[0], kins[0])
+    for s in range(w.steps):
+        if s + 1 < w.steps:
+            pl.stage_host(recs[s + 1], kins[s + 1])
+        h = pl.step_host(int(w.now[s]), recs[s], kins[s], pf, ev)
+        d_or, _ = oracle.score(w.rec[s], w.kin[s], int(w.now[s]), w.hop_scale)
+        p = oracle.plan(w.rec[s], d_or, res, w.theta, w.budget)
+        _assert_host_plan(h, pf, ev, p, s)
+        res = p["resident"].astype(np.uint8)
+    pl.close()
+
+
 def _oracle_step(w, s, res):
     d_or, _ = oracle.score(w.rec[s], None, int(w.now[s]), w.hop_scale)
     return oracle.plan(w.rec[s], d_or, res, w.theta, w.budget)
